@@ -1,0 +1,156 @@
+/*
+ * lpqt_b200.h — C ABI of liblpqt_b200.so, the sm_100a FP6 (e3m2) W6A16 path.
+ *
+ * The reference (`lpqt` 0.1.0, /root/reference/pkg/src/lpqt) is a pure-Python
+ * package with no FFI; each entry point below replaces one reference function
+ * on the hot path (cited as file:line) and is what a ctypes / cffi binding
+ * of that function binds to.  The Python package
+ * `paper_2312_08583_b200` is the in-repo binding.
+ *
+ * Conventions
+ *  - Plain pointers + sizes; every pointer is DEVICE memory unless noted.
+ *  - Every call is asynchronous on the caller's `stream` (a cudaStream_t
+ *    passed as void*; NULL = legacy default stream) and allocates nothing:
+ *    callers pass workspaces sized by the *_bytes() queries.
+ *  - Return value: LPQT_OK or a negative LPQT_E_* code for argument errors
+ *    detected on the host.  Data-dependent errors (non-finite weights, a scale
+ *    that overflows binary16, a folded scale above 65504) are OR-ed as
+ *    LPQT_F_* bits into the caller's device word `dev_flags`, which the
+ *    caller zeroes before and reads after the call (the Python binding maps
+ *    them to the reference's InvalidInput / ScaleOverflow exceptions,
+ *    errors.py:8, :32).
+ *  - dtype codes: LPQT_F64, LPQT_F32, LPQT_F16, LPQT_BF16.
+ */
+#ifndef LPQT_B200_H_
+#define LPQT_B200_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes (host-detected) — errors.py:4-53 ------------------- */
+#define LPQT_OK                 0
+#define LPQT_E_INVALID_INPUT   -1   /* InvalidInput      errors.py:8   */
+#define LPQT_E_SHAPE           -2   /* ShapeError        errors.py:28  */
+#define LPQT_E_SCALE_OVERFLOW  -3   /* ScaleOverflow     errors.py:32  */
+#define LPQT_E_PAYLOAD         -4   /* PayloadMismatch   errors.py:24  */
+#define LPQT_E_INVALID_CODE    -5   /* InvalidCode       errors.py:20  */
+#define LPQT_E_UNSUPPORTED     -6   /* dtype/layout not offered         */
+#define LPQT_E_WORKSPACE       -7   /* workspace too small              */
+#define LPQT_E_CUDA           -100  /* CUDA launch/driver failure       */
+
+/* ---- device flag bits (data-dependent errors) --------------------------- */
+#define LPQT_F_NONFINITE      1u    /* quantizer.py:200-201, codec.py:119-120 -> InvalidInput */
+#define LPQT_F_SCALE_INF      2u    /* quantizer.py:150-151                  -> InvalidInput */
+#define LPQT_F_FOLD_OVERFLOW  4u    /* dequant.py:66-68                       -> ScaleOverflow */
+#define LPQT_F_BAD_SCALE      8u    /* dequant.py:63-64 (scale <= 0 / inf)    -> InvalidInput */
+#define LPQT_F_BAD_CODE      16u    /* packing.py:56-60 code >= 64            -> InvalidCode  */
+
+/* ---- dtype / layout codes ------------------------------------------------ */
+#define LPQT_F64   0
+#define LPQT_F32   1
+#define LPQT_F16   2
+#define LPQT_BF16  3
+
+#define LPQT_Y_NM  0   /* Y[n, m] (reference layout, gemm.py:65 returns N x M) */
+#define LPQT_Y_MN  1   /* Y[m, n] (torch.nn.Linear layout)                     */
+
+const char* lpqt_strerror(int status);
+int lpqt_abi_version(void);               /* bumps on any signature change */
+
+/* codec.py:116-132 encode_rtn_array: x[n] (dtype) -> codes[n] (u8). */
+int lpqt_fp6_encode_rtn(const void* x, int dtype, int64_t n, uint8_t* codes,
+                        uint32_t* dev_flags, void* stream);
+
+/* packing.py:63-90 pack: codes[n] -> canonical seg4[seg4_length(n)],
+ * seg2[tail_length(n)] (pad bytes written as zero). */
+int lpqt_fp6_pack(const uint8_t* codes, int64_t n, uint8_t* seg4, uint8_t* seg2,
+                  uint32_t* dev_flags, void* stream);
+/* packing.py:93-118 unpack: canonical planes -> codes[n]. */
+int lpqt_fp6_unpack(const uint8_t* seg4, const uint8_t* seg2, int64_t n,
+                    uint8_t* codes, void* stream);
+int64_t lpqt_fp6_seg4_length(int64_t n);  /* packing.py:28-30 */
+int64_t lpqt_fp6_tail_length(int64_t n);  /* packing.py:33-36 */
+
+/* dequant.py:61-69 fold_scale_array: f16 scales[n] -> folded[n] = S * 2^12. */
+int lpqt_fp6_fold_scales(const uint16_t* scales, int64_t n, uint16_t* folded,
+                         uint32_t* dev_flags, void* stream);
+
+/* dequant.py:82-86 dequant_bias_shift_array (elementwise, f16 out) and
+ * dequant.py:72-79 dequant_naive_array.  `scale` is per element. */
+int lpqt_fp6_dequant_bias_shift(const uint8_t* codes, const uint16_t* folded,
+                                int64_t n, uint16_t* out, void* stream);
+int lpqt_fp6_dequant_naive(const uint8_t* codes, const uint16_t* scales,
+                           int64_t n, uint16_t* out, void* stream);
+
+/* quantizer.py:189-248 quantize_tensor, CGQ x FP6_E3M2 (one scale per row).
+ * W[N, K] row-major with row stride ldw (elements), any LPQT_* dtype.
+ * Writes scales[N] (f16 bits), folded[N] when bias_shift, and the canonical
+ * planes seg4/seg2 of the row-major code stream (flat index r*K + k).
+ * `codes_ws` (N*K bytes) is needed only when K % 8 != 0, else may be NULL. */
+int lpqt_fp6_quantize_pack(const void* W, int dtype, int64_t N, int64_t K,
+                           int64_t ldw, int bias_shift, uint16_t* scales,
+                           uint16_t* folded, uint8_t* seg4, uint8_t* seg2,
+                           uint8_t* codes_ws, uint32_t* dev_flags, void* stream);
+
+/* quantizer.py:269-299 dequantize_tensor for CGQ FP6 from canonical planes:
+ * out[N, K] = compose[c] * folded[row] (path 1, "bias_shift") or
+ * value[c] * scales[row] (path 0, "naive"); out dtype F64 (exact, the
+ * reference's return type) or F16 (the bias-shift binary16 rounding). */
+int lpqt_fp6_dequantize_tensor(const uint8_t* seg4, const uint8_t* seg2,
+                               const uint16_t* row_scale, int path,
+                               int64_t N, int64_t K, void* out, int out_dtype,
+                               void* stream);
+
+/* ---- B200 weight tile layout (new; no reference counterpart) -------------
+ * The GEMM consumes weights in a tile-contiguous layout: 128-row x 128-k
+ * tiles of 12288 bytes (6 bits/weight) stored [row_tile][k_tile], N and K
+ * zero-padded to multiples of 128.  The canonical planes stay the parity
+ * artifact; prepack/unprepack are exact inverses. */
+int64_t lpqt_fp6_tiles_bytes(int64_t N, int64_t K);
+int lpqt_fp6_prepack(const uint8_t* seg4, const uint8_t* seg2, int64_t N,
+                     int64_t K, uint8_t* tiles, void* stream);
+int lpqt_fp6_unprepack(const uint8_t* tiles, int64_t N, int64_t K,
+                       uint8_t* codes, void* stream);
+/* Standalone transform (the GEMM's register dequant): tiles -> out[N, K]
+ * f16 = compose[c] * folded[row] rounded to binary16 (dequant.py:82-86). */
+int lpqt_fp6_tiles_dequant(const uint8_t* tiles, const uint16_t* folded,
+                           int64_t N, int64_t K, uint16_t* out, void* stream);
+
+/* Activation staging: X in the reference layout [K, M] (gemm.py:65, any
+ * dtype, row stride ldx) -> Xt[M, Kp] f16 row-major (K-major operand),
+ * Kp = round_up(K, 8), pad columns zero.  Values round to binary16 (A16). */
+int lpqt_stage_activations(const void* X, int dtype, int64_t K, int64_t M,
+                           int64_t ldx, uint16_t* Xt, int64_t Kp, void* stream);
+
+/* gemm.py:65-94 gemm_quantized (CGQ FP6): Y = diag(S * 2^12) * (C . X) where
+ * C holds the bias-shifted code values (== diag(S) * (V . X), exactly); the
+ * fold S * 2^12 (dequant.py:46-69) is formed in an fp32 register, so it is
+ * exact and has no binary16 overflow limit.
+ * tiles: prepacked weights; scales[N] f16 bits (S); Xt[M, ldx] f16 K-major
+ * (ldx >= K, ldx % 8 == 0, 16-B aligned); Y per y_dtype (F32/F16/BF16)
+ * and y_layout (LPQT_Y_NM: Y[n*ldy + m]; LPQT_Y_MN: Y[m*ldy + n]).
+ * split_k: 0 = auto (plan below), else forced.  The kernel is tcgen05 (A =
+ * dequantized weights in TMEM, B = X via TMA, fp32 accumulate in TMEM).
+ * Workspace: lpqt_w6a16_workspace_bytes(); it must be zeroed once at
+ * allocation (split-K tile counters are self-resetting). */
+int64_t lpqt_w6a16_workspace_bytes(int64_t M, int64_t N, int64_t K, int split_k);
+int lpqt_w6a16_plan(int64_t M, int64_t N, int64_t K, int split_k,
+                    int* block_n, int* splits, int* grid, int* stages);
+int lpqt_w6a16_linear(const uint8_t* tiles, const uint16_t* scales,
+                      const uint16_t* Xt, int64_t ldx, int64_t M, int64_t N,
+                      int64_t K, void* Y, int y_dtype, int y_layout,
+                      int64_t ldy, int split_k, void* workspace,
+                      int64_t workspace_bytes, void* stream);
+
+/* Number of kernel launches performed by this library since load (for the
+ * bench's gpu_launches claim). */
+int64_t lpqt_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LPQT_B200_H_ */

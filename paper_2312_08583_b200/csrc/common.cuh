@@ -1,0 +1,287 @@
+// common.cuh — shared device helpers for liblpqt_b200 (sm_100a only).
+//
+// FP6 e3m2 constants and the bias-shift bit algebra follow the reference
+// (codec.py:48-49, dequant.py:33-43); the PTX wrappers (mbarrier, bulk/TMA
+// copies, tcgen05 alloc/mma/ld/st/commit) are the Blackwell primitives the
+// W6A16 GEMM is built from.
+#pragma once
+
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/lpqt_b200.h"
+
+#if defined(__CUDA_ARCH__) && (__CUDA_ARCH__ < 1000)
+#error "liblpqt_b200 targets sm_100a only"
+#endif
+
+namespace lpqt {
+
+// ---------------------------------------------------------------------------
+// Host-side bookkeeping
+// ---------------------------------------------------------------------------
+void note_launch();           // increments the launch counter (capi.cu)
+int check_launch();           // cudaGetLastError -> LPQT_OK / LPQT_E_CUDA
+
+inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+inline int grid_for(int64_t n, int threads, int64_t cap = 148 * 32) {
+  int64_t g = (n + threads - 1) / threads;
+  if (g < 1) g = 1;
+  if (g > cap) g = cap;
+  return static_cast<int>(g);
+}
+
+// ---------------------------------------------------------------------------
+// FP6 e3m2 scalar algebra (codec.py:63-96, dequant.py:33-43)
+// ---------------------------------------------------------------------------
+// magnitude grid g[i], i in 0..31 (codec.py:85-89): subnormal (E=0) i/16,
+// normal (1 + M/4) * 2^(E-3).  Every value and every midpoint is a short
+// binary fraction, so double comparisons against midpoints are exact.
+__host__ __device__ inline double fp6_magnitude(int i) {
+  const int e = i >> 2, m = i & 3;
+  if (e == 0) return m * 0.0625;                   // (m/4) * 2^-2
+  double v = 1.0 + m * 0.25;
+  int sh = e - 3;
+  return sh >= 0 ? v * (double)(1 << sh) : v / (double)(1 << (-sh));
+}
+
+// composed binary16 pattern of a code: sign<<15 | E<<10 | M<<8 (dequant.py:40)
+__host__ __device__ __forceinline__ uint16_t fp6_compose_bits(uint32_t c) {
+  return static_cast<uint16_t>(((c & 0x20u) << 10) | ((c & 0x1Fu) << 8));
+}
+
+// byte form used by the tile layout: s00eeemm (fp16 high byte of compose)
+__host__ __device__ __forceinline__ uint32_t fp6_byteform(uint32_t c) {
+  return ((c & 0x20u) << 2) | (c & 0x1Fu);
+}
+__host__ __device__ __forceinline__ uint32_t fp6_from_byteform(uint32_t b) {
+  return ((b & 0x80u) >> 2) | (b & 0x1Fu);
+}
+
+// ---------------------------------------------------------------------------
+// The register transform: 6 words of the tile layout (32 weights) -> 16 half2
+// of composed binary16 bit patterns in ascending k.  ~1.2 ALU ops / weight:
+// one LOP3 mask + two PRMT per 4 "direct" weights; the 8 "spare" weights are
+// gathered from bits 5-6 of every byte.  Layout contract (see prepack.cu):
+//   word i (0..5), byte t: weight k = 4i+t in s00eeemm form, bits 5,6 spare
+//   E0 (k 24..27) byte t = W0[5:6]->[0:1] | W1[5:6]->[2:3] | W2[5]->[4] | W5[6]->[7]
+//   E1 (k 28..31) byte t = W3[5:6]->[0:1] | W4[5:6]->[2:3] | W2[6]->[4] | W5[5]->[7]
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void fp6x32_to_f16x32(const uint32_t w[6], uint32_t out[16]) {
+#pragma unroll
+  for (int i = 0; i < 6; ++i) {
+    const uint32_t q = w[i] & 0x9F9F9F9Fu;
+    out[2 * i] = __byte_perm(q, 0u, 0x1404);
+    out[2 * i + 1] = __byte_perm(q, 0u, 0x3424);
+  }
+  const uint32_t e0 = ((w[0] >> 5) & 0x03030303u) | ((w[1] >> 3) & 0x0C0C0C0Cu) |
+                      ((w[2] >> 1) & 0x10101010u) | ((w[5] << 1) & 0x80808080u);
+  const uint32_t e1 = ((w[3] >> 5) & 0x03030303u) | ((w[4] >> 3) & 0x0C0C0C0Cu) |
+                      ((w[2] >> 2) & 0x10101010u) | ((w[5] << 2) & 0x80808080u);
+  out[12] = __byte_perm(e0, 0u, 0x1404);
+  out[13] = __byte_perm(e0, 0u, 0x3424);
+  out[14] = __byte_perm(e1, 0u, 0x1404);
+  out[15] = __byte_perm(e1, 0u, 0x3424);
+}
+
+// Inverse direction used by prepack: 32 codes (k ascending) -> 6 words.
+__host__ __device__ inline void fp6x32_pack_words(const uint8_t c[32], uint32_t w[6]) {
+  uint32_t b[32];
+  for (int j = 0; j < 32; ++j) b[j] = fp6_byteform(c[j]);
+  for (int i = 0; i < 6; ++i) {
+    w[i] = b[4 * i] | (b[4 * i + 1] << 8) | (b[4 * i + 2] << 16) | (b[4 * i + 3] << 24);
+  }
+  for (int t = 0; t < 4; ++t) {
+    const uint32_t e0 = b[24 + t], e1 = b[28 + t];
+    const int s = 8 * t;
+    w[0] |= ((e0 >> 0) & 3u) << (s + 5);
+    w[1] |= ((e0 >> 2) & 3u) << (s + 5);
+    w[2] |= ((e0 >> 4) & 1u) << (s + 5);
+    w[2] |= ((e1 >> 4) & 1u) << (s + 6);
+    w[3] |= ((e1 >> 0) & 3u) << (s + 5);
+    w[4] |= ((e1 >> 2) & 3u) << (s + 5);
+    w[5] |= ((e0 >> 7) & 1u) << (s + 6);
+    w[5] |= ((e1 >> 7) & 1u) << (s + 5);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Tile layout geometry (shared by prepack, tiles_dequant and the GEMM)
+//   tile = 128 rows x 128 k = 12288 B, stored [row_tile][k_tile]
+//   inside a tile: [khalf 2][quad 3][row 128][16 B]; thread (row, khalf) owns
+//   3 quads = 12 words = 64 weights = two 32-weight groups (words 0-5, 6-11).
+// ---------------------------------------------------------------------------
+constexpr int kTileN = 128;
+constexpr int kTileK = 128;
+constexpr int kTileBytes = kTileN * kTileK * 6 / 8;  // 12288
+
+// byte offset of word wi (0..5) of the 32-weight group starting at (n, k32*32)
+__host__ __device__ __forceinline__ int64_t tile_word_addr(int64_t n, int64_t g32, int wi,
+                                                           int64_t k_tiles) {
+  const int64_t rt = n / kTileN, rr = n % kTileN;
+  const int64_t kt = g32 / 4;               // 4 groups of 32 per 128-k tile
+  const int gin = static_cast<int>(g32 % 4);
+  const int khalf = gin >> 1, grp = gin & 1;
+  const int word = grp * 6 + wi;            // 0..11 within the (row,khalf) slot
+  const int quad = word >> 2, wq = word & 3;
+  return (rt * k_tiles + kt) * kTileBytes + ((int64_t)(khalf * 3 + quad) * kTileN + rr) * 16 + wq * 4;
+}
+
+// ---------------------------------------------------------------------------
+// PTX wrappers
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ bool mbar_try_wait(uint32_t addr, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(addr), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+// Spin with a watchdog: a pipeline deadlock traps (the launch fails with an
+// error) instead of hanging the device.  ~2^28 polls is tens of seconds.
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  const uint32_t a = smem_u32(bar);
+  uint32_t spins = 0;
+  while (!mbar_try_wait(a, parity)) {
+    if (++spins == (1u << 28)) __trap();
+  }
+}
+
+// 1-D bulk copy global -> shared, completes tx bytes on `bar`; evict-first
+// L2 policy for the streamed weight tiles.
+__device__ __forceinline__ uint64_t l2_evict_first_policy() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar,
+                                         uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
+          smem_u32(dst)),
+      "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
+      : "memory");
+}
+__device__ __forceinline__ void prefetch_tmap(const CUtensorMap* map) {
+  asm volatile("prefetch.tensormap [%0];" ::"l"(map) : "memory");
+}
+
+// tcgen05 -------------------------------------------------------------------
+__device__ __forceinline__ void tmem_alloc(uint32_t* dst_smem, uint32_t ncols) {
+  asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(dst_smem)),
+               "r"(ncols)
+               : "memory");
+}
+__device__ __forceinline__ void tmem_relinquish() {
+  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tmem_dealloc(uint32_t taddr, uint32_t ncols) {
+  asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(ncols) : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+               : "memory");
+}
+// D[tmem] (+)= A[tmem] * B[smem desc]; kind::f16 (fp16 in, fp32 accumulate)
+__device__ __forceinline__ void mma_f16_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc,
+                                           uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+
+// Shared-memory matrix descriptor: K-major, 128-byte swizzle, 8-row atoms
+// of 1024 B (SBO), version 1 (sm_100).
+__device__ __forceinline__ uint64_t sdesc_kmajor_sw128(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= static_cast<uint64_t>((saddr & 0x3FFFFu) >> 4);
+  d |= static_cast<uint64_t>(1) << 16;            // LBO (unused for swizzled K-major)
+  d |= static_cast<uint64_t>(1024 >> 4) << 32;    // SBO
+  d |= static_cast<uint64_t>(1) << 46;            // descriptor version (sm_100)
+  d |= static_cast<uint64_t>(2) << 61;            // SWIZZLE_128B
+  return d;
+}
+
+// instruction descriptor for kind::f16: A,B fp16 K-major, D fp32, M=128
+__host__ __device__ constexpr uint32_t idesc_f16_m128(int n) {
+  return (1u << 4) | (0u << 7) | (0u << 10) | (static_cast<uint32_t>(n >> 3) << 17) |
+         (static_cast<uint32_t>(128 >> 4) << 24);
+}
+
+#define LPQT_R8(o) "r"(o[0]), "r"(o[1]), "r"(o[2]), "r"(o[3]), "r"(o[4]), "r"(o[5]), "r"(o[6]), "r"(o[7])
+#define LPQT_W8(o) "=r"(o[0]), "=r"(o[1]), "=r"(o[2]), "=r"(o[3]), "=r"(o[4]), "=r"(o[5]), "=r"(o[6]), "=r"(o[7])
+
+// 32 lanes x 32 consecutive 32-bit columns store (one TMEM lane per thread)
+__device__ __forceinline__ void tmem_st_x32(uint32_t taddr, const uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, "
+      "%14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31, %32};" ::"r"(taddr),
+      LPQT_R8((r + 0)), LPQT_R8((r + 8)), LPQT_R8((r + 16)), LPQT_R8((r + 24))
+      : "memory");
+}
+__device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+
+__device__ __forceinline__ void tmem_ld_x16(uint32_t taddr, uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+      "%15}, [%16];"
+      : LPQT_W8((r + 0)), LPQT_W8((r + 8))
+      : "r"(taddr)
+      : "memory");
+}
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+
+__device__ __forceinline__ void named_bar_sync(int id, int nthreads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+
+__device__ __forceinline__ uint4 lds128(const void* p) {
+  uint4 v;
+  asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "r"(smem_u32(p)));
+  return v;
+}
+
+}  // namespace lpqt

@@ -1,0 +1,129 @@
+// prepack.cu — K2 (canonical 4+2 planes -> B200 tile layout), its inverse,
+// and K3 (the standalone register transform, tiles -> binary16).
+//
+// The canonical planes (packing.py:63-90) are the reference's storage format
+// and stay the parity artifact.  The GEMM instead streams 128x128 weight
+// tiles of 12288 contiguous bytes (one 1-D bulk copy each) whose bit order is
+// chosen so the in-register FP6 -> FP16 rebuild costs ~1.2 ALU ops per
+// weight (see fp6x32_to_f16x32 in common.cuh).  K3 runs exactly that
+// transform and multiplies by the folded scale in binary16, reproducing
+// dequant_bias_shift_array (dequant.py:82-86) bit for bit.
+#include "common.cuh"
+
+namespace lpqt {
+
+__device__ __forceinline__ uint32_t canon_code_at(const uint8_t* __restrict__ seg4, const uint8_t* __restrict__ seg2,
+                                                  int64_t i) {
+  const uint32_t hi = (seg4[i >> 1] >> (4 * (i & 1))) & 15u;
+  const uint32_t lo = (seg2[i >> 2] >> (2 * (i & 3))) & 3u;
+  return (hi << 2) | lo;
+}
+
+// one thread per (row n < Np, 32-weight group g < Kp/32)
+__global__ void prepack_kernel(const uint8_t* __restrict__ seg4, const uint8_t* __restrict__ seg2, int64_t N,
+                               int64_t K, int64_t Np, int64_t Kp, uint8_t* __restrict__ tiles) {
+  const int64_t groups = Kp / 32, total = Np * groups, k_tiles = Kp / kTileK;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t n = t / groups, g = t % groups;
+    uint8_t c[32];
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+      const int64_t k = g * 32 + j;
+      c[j] = (n < N && k < K) ? static_cast<uint8_t>(canon_code_at(seg4, seg2, n * K + k)) : 0;
+    }
+    uint32_t w[6];
+    fp6x32_pack_words(c, w);
+#pragma unroll
+    for (int i = 0; i < 6; ++i) *reinterpret_cast<uint32_t*>(tiles + tile_word_addr(n, g, i, k_tiles)) = w[i];
+  }
+}
+
+__device__ __forceinline__ void load_group(const uint8_t* __restrict__ tiles, int64_t n, int64_t g, int64_t k_tiles,
+                                           uint32_t w[6]) {
+#pragma unroll
+  for (int i = 0; i < 6; ++i) w[i] = *reinterpret_cast<const uint32_t*>(tiles + tile_word_addr(n, g, i, k_tiles));
+}
+
+// exact inverse of prepack over the valid region -> row-major codes[N, K]
+__global__ void unprepack_kernel(const uint8_t* __restrict__ tiles, int64_t N, int64_t K, int64_t Kp,
+                                 uint8_t* __restrict__ codes) {
+  const int64_t groups = Kp / 32, total = N * groups, k_tiles = Kp / kTileK;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t n = t / groups, g = t % groups;
+    uint32_t w[6], h[16];
+    load_group(tiles, n, g, k_tiles, w);
+    fp6x32_to_f16x32(w, h);  // the GEMM's transform; codes come back out of the fp16 high bytes
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+      const int64_t k = g * 32 + j;
+      if (k < K) {
+        const uint32_t b = (h[j >> 1] >> (16 * (j & 1) + 8)) & 0xFFu;
+        codes[n * K + k] = static_cast<uint8_t>(fp6_from_byteform(b));
+      }
+    }
+  }
+}
+
+// K3: tiles -> out[N, K] binary16 = compose[c] * folded[n]
+__global__ void tiles_dequant_kernel(const uint8_t* __restrict__ tiles, const uint16_t* __restrict__ folded,
+                                     int64_t N, int64_t K, int64_t Kp, uint16_t* __restrict__ out) {
+  const int64_t groups = Kp / 32, total = N * groups, k_tiles = Kp / kTileK;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t n = t / groups, g = t % groups;
+    uint32_t w[6], h[16];
+    load_group(tiles, n, g, k_tiles, w);
+    fp6x32_to_f16x32(w, h);
+    const __half2 f2 = __half2half2(__ushort_as_half(folded[n]));
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      __half2 v = *reinterpret_cast<const __half2*>(&h[j]);
+      v = __hmul2(v, f2);
+      const int64_t k = g * 32 + 2 * j;
+      if (k < K) out[n * K + k] = __half_as_ushort(__low2half(v));
+      if (k + 1 < K) out[n * K + k + 1] = __half_as_ushort(__high2half(v));
+    }
+  }
+}
+
+}  // namespace lpqt
+
+using namespace lpqt;
+
+static inline int64_t round_up(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
+
+extern "C" {
+
+int64_t lpqt_fp6_tiles_bytes(int64_t N, int64_t K) {
+  if (N <= 0 || K <= 0) return 0;
+  return round_up(N, kTileN) / kTileN * (round_up(K, kTileK) / kTileK) * kTileBytes;
+}
+
+int lpqt_fp6_prepack(const uint8_t* seg4, const uint8_t* seg2, int64_t N, int64_t K, uint8_t* tiles, void* stream) {
+  if (N < 0 || K < 0) return LPQT_E_SHAPE;
+  if (N == 0 || K == 0) return LPQT_OK;
+  const int64_t Np = round_up(N, kTileN), Kp = round_up(K, kTileK);
+  prepack_kernel<<<grid_for(Np * (Kp / 32), 256), 256, 0, as_stream(stream)>>>(seg4, seg2, N, K, Np, Kp, tiles);
+  note_launch();
+  return check_launch();
+}
+
+int lpqt_fp6_unprepack(const uint8_t* tiles, int64_t N, int64_t K, uint8_t* codes, void* stream) {
+  if (N < 0 || K < 0) return LPQT_E_SHAPE;
+  if (N == 0 || K == 0) return LPQT_OK;
+  const int64_t Kp = round_up(K, kTileK);
+  unprepack_kernel<<<grid_for(N * (Kp / 32), 256), 256, 0, as_stream(stream)>>>(tiles, N, K, Kp, codes);
+  note_launch();
+  return check_launch();
+}
+
+int lpqt_fp6_tiles_dequant(const uint8_t* tiles, const uint16_t* folded, int64_t N, int64_t K, uint16_t* out,
+                           void* stream) {
+  if (N < 0 || K < 0) return LPQT_E_SHAPE;
+  if (N == 0 || K == 0) return LPQT_OK;
+  const int64_t Kp = round_up(K, kTileK);
+  tiles_dequant_kernel<<<grid_for(N * (Kp / 32), 256), 256, 0, as_stream(stream)>>>(tiles, folded, N, K, Kp, out);
+  note_launch();
+  return check_launch();
+}
+
+}  // extern "C"

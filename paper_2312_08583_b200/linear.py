@@ -1,0 +1,195 @@
+"""Device-resident FP6 weights and the W6A16 linear (the B200 hot path).
+
+`Fp6Weight` holds a weight matrix the way the GEMM streams it: the B200 tile
+layout (128 x 128 tiles of 12288 B, `lpqt_fp6_prepack`) plus the f16 row
+scales.  `w6a16_linear` is the torch-facing call (x[M, K] fp16 -> y[M, N]);
+`gemm_nm` is the reference-layout call used by `gemm.gemm_quantized`
+(X[K, M] -> Y[N, M] f32, gemm.py:65-94).  Both launch the tcgen05 kernel
+`lpqt_w6a16_linear`; nothing here computes on the CPU.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+from . import _lib
+from .errors import ShapeError
+from .packing import seg4_length
+
+TILE = 128
+
+
+def _round_up(x: int, m: int) -> int:
+    return (x + m - 1) // m * m
+
+
+def prepack(seg4, seg2, n: int, k: int):
+    """Canonical planes (CUDA uint8) -> tile layout (CUDA uint8)."""
+    t = _lib.torch()
+    nbytes = int(_lib.load().lpqt_fp6_tiles_bytes(n, k))
+    tiles = t.empty(nbytes, dtype=t.uint8, device=seg4.device)
+    _lib.check(_lib.load().lpqt_fp6_prepack(seg4.data_ptr(), seg2.data_ptr(), n, k, tiles.data_ptr(),
+                                            _lib.stream_ptr()), "prepack")
+    return tiles
+
+
+class Fp6Weight:
+    """An N x K FP6 (e3m2) weight resident in HBM in the GEMM's tile layout."""
+
+    def __init__(self, tiles, scales, n: int, k: int, folded=None):
+        self.tiles = tiles
+        self.scales = scales          # f16 [N]  (S; the GEMM folds S * 2^12 in-register)
+        self.folded = folded          # f16 [N] or None (bias-shift artifact, API parity)
+        self.n = int(n)
+        self.k = int(k)
+
+    # -- construction -------------------------------------------------------
+    @classmethod
+    def from_planes(cls, seg4, seg2, scales, n: int, k: int, folded=None) -> "Fp6Weight":
+        return cls(prepack(seg4, seg2, n, k), scales, n, k, folded)
+
+    @classmethod
+    def quantize(cls, W, bias_shift: bool = True) -> "Fp6Weight":
+        """RTN per-row FP6 quantize on the GPU (quantizer.py:189-248), then prepack."""
+        from .quantizer import _weights_to_device, quantize_device
+        w, _ = _weights_to_device(W)
+        n, k = (int(v) for v in w.shape)
+        d = quantize_device(w, bias_shift)
+        return cls.from_planes(d["seg4"], d["seg2"], d["scales"], n, k, d["folded"])
+
+    @classmethod
+    def from_quantized(cls, q) -> "Fp6Weight":
+        from .quantizer import _require_path, device_planes
+        _require_path(q.scheme)
+        cache = q.device_cache
+        if cache is not None and "weight" in cache:
+            return cache["weight"]
+        s4, s2, sc = device_planes(q)
+        w = cls.from_planes(s4, s2, sc, q.rows, q.cols)
+        if cache is not None:
+            cache["weight"] = w
+        return w
+
+    # -- inspection -----------------------------------------------------------
+    @property
+    def nbytes(self) -> int:
+        return int(self.tiles.numel() + 2 * self.scales.numel())
+
+    def stream_bytes(self) -> int:
+        """Algorithmic weight bytes per GEMM: 0.75 B/weight + 2 B/row (cli.py:75-80)."""
+        nk = self.n * self.k
+        return seg4_length(nk) + _round_up((2 * nk + 7) // 8, 4) + 2 * self.n
+
+    def codes(self):
+        """Row-major codes [N, K] recovered from the tile layout (test hook)."""
+        t = _lib.torch()
+        out = t.empty((self.n, self.k), dtype=t.uint8, device=self.tiles.device)
+        _lib.check(_lib.load().lpqt_fp6_unprepack(self.tiles.data_ptr(), self.n, self.k, out.data_ptr(),
+                                                  _lib.stream_ptr()), "unprepack")
+        return out
+
+    def dequantize_f16(self, folded=None):
+        """[N, K] binary16 via the GEMM's register transform: compose[c] *
+        folded (dequant.py:82-86)."""
+        t = _lib.torch()
+        f = folded if folded is not None else self.folded
+        if f is None:
+            raise ValueError("folded scales required")
+        out = t.empty((self.n, self.k), dtype=t.float16, device=self.tiles.device)
+        _lib.check(_lib.load().lpqt_fp6_tiles_dequant(self.tiles.data_ptr(), f.data_ptr(), self.n, self.k,
+                                                      out.data_ptr(), _lib.stream_ptr()), "tiles_dequant")
+        return out
+
+
+def plan(m: int, n: int, k: int, split_k: int = 0) -> dict:
+    """The launch plan the library picks: block_n (MMA N), splits, grid, stages."""
+    import ctypes
+    vals = [ctypes.c_int(0) for _ in range(4)]
+    _lib.check(_lib.load().lpqt_w6a16_plan(m, n, k, split_k, *[ctypes.addressof(v) for v in vals]), "plan")
+    return dict(zip(("block_n", "splits", "grid", "stages"), (v.value for v in vals)))
+
+
+def _launch(weight: Fp6Weight, xt, ldx: int, m: int, y, y_dtype: int, y_layout: int, ldy: int, split_k: int):
+    lib = _lib.load()
+    ws_bytes = int(lib.lpqt_w6a16_workspace_bytes(m, weight.n, weight.k, split_k))
+    ws = _lib.Workspace.get(ws_bytes) if ws_bytes else None
+    _lib.check(lib.lpqt_w6a16_linear(
+        weight.tiles.data_ptr(), weight.scales.data_ptr(), xt.data_ptr(), ldx, m, weight.n, weight.k,
+        y.data_ptr(), y_dtype, y_layout, ldy, split_k, _lib.ptr(ws), ws.numel() if ws is not None else 0,
+        _lib.stream_ptr()), "w6a16_linear")
+
+
+def stage_activations(X, k: int):
+    """Reference-layout activations X[K, M] (any float dtype, numpy or CUDA)
+    -> Xt[M, round_up(K, 8)] fp16 on the GPU (lpqt_stage_activations)."""
+    t = _lib.torch()
+    xd = X if _lib.is_torch(X) else np.asarray(X)
+    if not _lib.is_torch(xd) and xd.dtype not in (np.float64, np.float32, np.float16):
+        xd = xd.astype(np.float64)
+    xd = _lib.to_device(xd)
+    if xd.dtype not in (t.float64, t.float32, t.float16, t.bfloat16):
+        xd = xd.to(t.float64)
+    m = int(xd.shape[1])
+    kp = _round_up(max(k, 1), 8)
+    xt = t.empty((m, kp), dtype=t.float16, device=xd.device)
+    _lib.check(_lib.load().lpqt_stage_activations(xd.data_ptr(), _lib.dtype_code(xd.dtype), k, m, m,
+                                                  xt.data_ptr(), kp, _lib.stream_ptr()), "stage_activations")
+    return xt, kp
+
+
+def gemm_nm(weight: Fp6Weight, xt, ldx: int, m: int, out=None, split_k: int = 0):
+    """Y[N, M] f32 = W_hat @ X in the reference layout (gemm.py:65-94)."""
+    t = _lib.torch()
+    y = out if out is not None else t.empty((weight.n, m), dtype=t.float32, device=xt.device)
+    if m and weight.n:
+        _launch(weight, xt, ldx, m, y, _lib.F32, _lib.Y_NM, m, split_k)
+    return y
+
+
+def w6a16_linear(x, weight: Fp6Weight, out=None, out_dtype=None, split_k: int = 0):
+    """y = x @ W_hat^T for x[..., K] (CUDA, fp16 preferred) -> y[..., N].
+
+    x is the K-major B operand as is when it is contiguous fp16 with K % 8 ==
+    0; otherwise it is cast / padded once.  out_dtype: fp16 (default for
+    fp16 x), bf16 or fp32.
+    """
+    t = _lib.torch()
+    if x.shape[-1] != weight.k:
+        raise ShapeError(f"inner dimensions differ: weights K={weight.k}, activations K={x.shape[-1]}")
+    lead = tuple(x.shape[:-1])
+    x2 = x.reshape(-1, weight.k)
+    m = int(x2.shape[0])
+    if x2.dtype != t.float16:
+        x2 = x2.to(t.float16)
+    if weight.k % 8 or not x2.is_contiguous() or x2.data_ptr() % 16:
+        kp = _round_up(weight.k, 8)
+        xp = t.zeros((m, kp), dtype=t.float16, device=x2.device)
+        xp[:, : weight.k] = x2
+        x2, ldx = xp, kp
+    else:
+        ldx = weight.k
+    odt = out_dtype or (x.dtype if x.dtype in (t.float16, t.bfloat16, t.float32) else t.float16)
+    code = {t.float32: _lib.F32, t.float16: _lib.F16, t.bfloat16: _lib.BF16}[odt]
+    y = out if out is not None else t.empty((m, weight.n), dtype=odt, device=x2.device)
+    if m and weight.n:
+        if weight.k == 0:
+            y.zero_()
+        else:
+            _launch(weight, x2, ldx, m, y, code, _lib.Y_MN, weight.n, split_k)
+    return y.reshape(*lead, weight.n)
+
+
+class Fp6Linear:
+    """torch.nn.Linear-style callable over an Fp6Weight (no bias)."""
+
+    def __init__(self, weight: Fp6Weight):
+        self.weight = weight
+        self.in_features = weight.k
+        self.out_features = weight.n
+
+    @classmethod
+    def from_dense(cls, W, bias_shift: bool = True) -> "Fp6Linear":
+        return cls(Fp6Weight.quantize(W, bias_shift))
+
+    def __call__(self, x, out=None):
+        return w6a16_linear(x, self.weight, out=out)

@@ -1,0 +1,128 @@
+"""Canonical 4+2 bit-split planes — reference packing.py:24-141.
+
+`pack`/`unpack` run on the GPU (`lpqt_fp6_pack` / `lpqt_fp6_unpack`) and are
+byte-identical to the reference: code i puts c>>2 in nibble i of `seg4`
+(even index low) and c&3 in 2-bit lane i of `seg_tail`, both zero-padded to a
+4-byte multiple.  The GEMM's own tile layout is derived from these planes by
+`linear.prepack`.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+from .codec import MiniFloatFormat, require_fp6
+from .errors import InvalidCode, InvalidScheme, PayloadMismatch
+
+
+def _align4(n: int) -> int:
+    return (n + 3) // 4 * 4
+
+
+def seg4_length(code_count: int) -> int:
+    """Bytes of the 4-bit plane (packing.py:28-30)."""
+    return _align4((code_count + 1) // 2)
+
+
+def tail_length(fmt: MiniFloatFormat, code_count: int) -> int:
+    """Bytes of the tail plane (packing.py:33-36)."""
+    return _align4((code_count * fmt.mantissa_bits + 7) // 8)
+
+
+@dataclass(frozen=True)
+class PackedSegments:
+    """The two planes holding one code stream (packing.py:39-45).  Arrays
+    are numpy on the numpy API and CUDA tensors on the torch API."""
+
+    seg4: object
+    seg_tail: object
+    code_count: int
+
+
+def split_code(fmt: MiniFloatFormat, code: int) -> tuple[int, int]:
+    """(sign+exponent nibble, mantissa bits) of one code (packing.py:48-53)."""
+    code = int(code)
+    if not 0 <= code < fmt.code_count:
+        raise InvalidCode(f"code {code:#x} does not fit {fmt.total_bits} bits")
+    return code >> fmt.mantissa_bits, code & fmt.mantissa_mask
+
+
+def _codes_to_device(fmt: MiniFloatFormat, codes):
+    t = _lib.torch()
+    if _lib.is_torch(codes):
+        c = codes.reshape(-1)
+        if c.dtype != t.uint8:
+            if c.numel() and (int(c.min()) < 0 or int(c.max()) >= fmt.code_count):
+                raise InvalidCode(f"codes must fit {fmt.total_bits} bits")
+            c = c.to(t.uint8)
+        return c.to(_lib.device()).contiguous(), True
+    a = np.asarray(codes).reshape(-1)
+    if a.dtype != np.uint8:
+        if a.size and (a.min() < 0 or a.max() >= fmt.code_count):
+            raise InvalidCode(f"codes must fit {fmt.total_bits} bits")
+        a = a.astype(np.uint8)
+    return _lib.to_device(a), False
+
+
+def pack_device(codes_dev, n: int):
+    """codes (uint8 CUDA tensor, n) -> (seg4, seg2) CUDA tensors."""
+    t = _lib.torch()
+    seg4 = t.empty(seg4_length(n), dtype=t.uint8, device=codes_dev.device)
+    seg2 = t.empty(_align4((2 * n + 7) // 8), dtype=t.uint8, device=codes_dev.device)
+    if seg2.numel():
+        flags = _lib.Flags()
+        _lib.check(_lib.load().lpqt_fp6_pack(codes_dev.data_ptr(), n, seg4.data_ptr(), seg2.data_ptr(),
+                                             flags.ptr, _lib.stream_ptr()), "pack")
+        if flags.value():
+            raise InvalidCode("codes must fit 6 bits")
+    return seg4, seg2
+
+
+def unpack_device(seg4, seg2, n: int):
+    t = _lib.torch()
+    codes = t.empty(n, dtype=t.uint8, device=seg4.device)
+    if n:
+        _lib.check(_lib.load().lpqt_fp6_unpack(seg4.data_ptr(), seg2.data_ptr(), n, codes.data_ptr(),
+                                               _lib.stream_ptr()), "unpack")
+    return codes
+
+
+def pack(fmt: MiniFloatFormat, codes) -> PackedSegments:
+    """Pack a code stream into the canonical planes (packing.py:63-90)."""
+    require_fp6(fmt)
+    c, torch_in = _codes_to_device(fmt, codes)
+    n = c.numel()
+    seg4, seg2 = pack_device(c, n)
+    if torch_in:
+        return PackedSegments(seg4, seg2, n)
+    return PackedSegments(seg4.cpu().numpy(), seg2.cpu().numpy(), n)
+
+
+def unpack(fmt: MiniFloatFormat, segments: PackedSegments):
+    """Recover the first `code_count` codes; pad bits ignored (packing.py:93-118)."""
+    require_fp6(fmt)
+    n = int(segments.code_count)
+    torch_in = _lib.is_torch(segments.seg4)
+    s4 = segments.seg4 if torch_in else np.asarray(segments.seg4, dtype=np.uint8)
+    s2 = segments.seg_tail if torch_in else np.asarray(segments.seg_tail, dtype=np.uint8)
+    n4 = s4.numel() if torch_in else s4.size
+    n2 = s2.numel() if torch_in else s2.size
+    if n4 != seg4_length(n) or n2 != tail_length(fmt, n):
+        raise PayloadMismatch(f"segment lengths ({n4}, {n2}) inconsistent with code count {n}")
+    d4 = _lib.to_device(s4).reshape(-1)
+    d2 = _lib.to_device(s2).reshape(-1)
+    codes = unpack_device(d4, d2, n)
+    return codes if torch_in else codes.cpu().numpy()
+
+
+def pack_int4(levels):
+    """INT4 nibbles (packing.py:121-129): outside the B200 FP6 path."""
+    raise InvalidScheme("INT4 packing is outside the B200 FP6 path")
+
+
+def unpack_int4(data, count: int):
+    """INT4 nibbles (packing.py:132-141): outside the B200 FP6 path."""
+    raise InvalidScheme("INT4 packing is outside the B200 FP6 path")

@@ -1,0 +1,297 @@
+"""Per-output-channel FP6 quantization — reference quantizer.py:1-320.
+
+`quantize_tensor` for CGQ x FP6_E3M2 (the north-star path: RTN, one scale per
+weight row) runs as one fused GPU kernel (`lpqt_fp6_quantize_pack`): row
+max|w|, S = RN_f16(peak/28), fold S*2^12, RTN codes of W/S and the canonical
+4+2 planes, bit-exact with the reference for f64/f32/f16/bf16 input.
+`dequantize_tensor` is the GPU `lpqt_fp6_dequantize_tensor` (f64 exact).
+FGQ, FP5 and INT4 schemes are outside this path and raise InvalidScheme.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+from enum import Enum
+
+import numpy as np
+
+from . import _lib
+from .codec import FP5_E3M1, FP6_E3M2, MiniFloatFormat
+from .errors import (InvalidInput, InvalidScheme, PathUnavailable, PayloadMismatch,
+                     ShapeError)
+from .packing import PackedSegments, seg4_length, tail_length
+
+
+class Granularity(Enum):
+    CGQ = "cgq"
+    FGQ = "fgq"
+
+
+class TensorFormat(Enum):
+    FP6_E3M2 = "fp6"
+    FP5_E3M1 = "fp5"
+    INT4_ASYM = "int4"
+
+    @property
+    def minifloat(self) -> MiniFloatFormat | None:
+        if self is TensorFormat.FP6_E3M2:
+            return FP6_E3M2
+        if self is TensorFormat.FP5_E3M1:
+            return FP5_E3M1
+        return None
+
+
+@dataclass(frozen=True)
+class QuantScheme:
+    """Granularity + format; `block_size` is FGQ-only (quantizer.py:46-52)."""
+
+    granularity: Granularity
+    fmt: TensorFormat
+    block_size: int = 0
+
+
+@dataclass(frozen=True)
+class BlockParams:
+    scale: np.float16
+    zero_point: np.float16 | None = None
+
+
+@dataclass(frozen=True)
+class ErrorReport:
+    mse: float
+    max_abs_error: float
+    sqnr_db: float
+
+
+@dataclass(frozen=True)
+class QuantizedTensor:
+    """Reference fields (quantizer.py:70-83) plus a private device cache."""
+
+    rows: int
+    cols: int
+    scheme: QuantScheme
+    scales: object
+    zero_points: object
+    payload: object
+    bias_shift: bool = False
+    folded_scales: object = None
+    device_cache: dict | None = field(default=None, compare=False, repr=False)
+
+    @property
+    def num_blocks(self) -> int:
+        s = self.scales
+        return int(s.numel() if _lib.is_torch(s) else np.asarray(s).size)
+
+
+CGQ_FP6 = QuantScheme(Granularity.CGQ, TensorFormat.FP6_E3M2)
+
+
+def _validate_scheme(scheme: QuantScheme) -> None:
+    if scheme.granularity is Granularity.FGQ and scheme.block_size < 1:
+        raise InvalidScheme(f"FGQ requires block_size >= 1, got {scheme.block_size}")
+
+
+def _require_path(scheme: QuantScheme) -> None:
+    _validate_scheme(scheme)
+    if scheme.fmt is not TensorFormat.FP6_E3M2 or scheme.granularity is not Granularity.CGQ:
+        raise InvalidScheme(
+            f"{scheme.granularity.name} x {scheme.fmt.name} is outside the B200 path "
+            "(per-output-channel CGQ x FP6_E3M2 only)")
+
+
+def blocks_per_row(cols: int, scheme: QuantScheme) -> int:
+    _validate_scheme(scheme)
+    if cols == 0:
+        return 0
+    if scheme.granularity is Granularity.CGQ:
+        return 1
+    return -(-cols // scheme.block_size)
+
+
+def block_widths(cols: int, scheme: QuantScheme) -> np.ndarray:
+    """Widths of the blocks inside one row (quantizer.py:100-109)."""
+    bpr = blocks_per_row(cols, scheme)
+    if scheme.granularity is Granularity.CGQ:
+        return np.array([cols] * bpr, dtype=np.int64)
+    d = scheme.block_size
+    w = np.full(bpr, d, dtype=np.int64)
+    if bpr and cols % d:
+        w[-1] = cols % d
+    return w
+
+
+def num_blocks(rows: int, cols: int, scheme: QuantScheme) -> int:
+    if rows == 0 or cols == 0:
+        return 0
+    return rows * blocks_per_row(cols, scheme)
+
+
+def partition_blocks(rows: int, cols: int, scheme: QuantScheme) -> list[tuple[int, int, int]]:
+    """(row, col_start, col_end) per block, row-major (quantizer.py:118-130)."""
+    if rows < 0 or cols < 0:
+        raise InvalidScheme("dimensions must be non-negative")
+    _validate_scheme(scheme)
+    widths = block_widths(cols, scheme)
+    bounds = np.concatenate([[0], np.cumsum(widths)])
+    return [(r, int(bounds[j]), int(bounds[j + 1]))
+            for r in range(rows if cols else 0) for j in range(len(widths))]
+
+
+# ---------------------------------------------------------------------------
+def _weights_to_device(W):
+    """-> (2-D CUDA tensor in a kernel dtype, torch_in)."""
+    t = _lib.torch()
+    if _lib.is_torch(W):
+        if W.dim() != 2:
+            raise ShapeError(f"expected a 2-D matrix, got shape {tuple(W.shape)}")
+        w = W
+        if w.dtype not in (t.float64, t.float32, t.float16, t.bfloat16):
+            w = w.to(t.float64)
+        return w.to(_lib.device()).contiguous(), True
+    a = np.asarray(W)
+    if a.ndim != 2:
+        raise ShapeError(f"expected a 2-D matrix, got shape {a.shape}")
+    if a.dtype not in (np.float64, np.float32, np.float16):
+        a = a.astype(np.float64)
+    return _lib.to_device(a), False
+
+
+def quantize_device(w, bias_shift: bool = True):
+    """GPU quantize of a 2-D CUDA tensor -> dict of CUDA tensors
+    {scales, folded, seg4, seg2} (canonical planes, flat index r*K + k)."""
+    t = _lib.torch()
+    n, k = (int(v) for v in w.shape)
+    dev = w.device
+    scales = t.empty(n, dtype=t.float16, device=dev)
+    folded = t.empty(n, dtype=t.float16, device=dev) if bias_shift else None
+    nk = n * k
+    seg4 = t.empty(seg4_length(nk), dtype=t.uint8, device=dev)
+    seg2 = t.empty(tail_length(FP6_E3M2, nk), dtype=t.uint8, device=dev)
+    if seg4.numel():
+        seg4[-4:].zero_()
+        seg2[-4:].zero_()
+    ws = t.empty(nk, dtype=t.uint8, device=dev) if k % 8 else None
+    flags = _lib.Flags()
+    _lib.check(_lib.load().lpqt_fp6_quantize_pack(
+        w.data_ptr(), _lib.dtype_code(w.dtype), n, k, k, int(bool(bias_shift)), scales.data_ptr(),
+        _lib.ptr(folded), seg4.data_ptr(), seg2.data_ptr(), _lib.ptr(ws), flags.ptr, _lib.stream_ptr()),
+        "quantize_tensor")
+    flags.raise_if_set()
+    return {"scales": scales, "folded": folded, "seg4": seg4, "seg2": seg2}
+
+
+def quantize_tensor(W, scheme: QuantScheme, bias_shift: bool = False) -> QuantizedTensor:
+    """Quantize a dense N x K matrix (quantizer.py:189-248) on the GPU.
+
+    numpy / array-like in -> numpy fields (the reference's types); a torch
+    tensor in -> CUDA tensor fields.  Errors: ShapeError (not 2-D),
+    InvalidInput (non-finite, scale overflows binary16), ScaleOverflow
+    (bias_shift and S * 2^12 > 65504), InvalidScheme (outside CGQ x FP6).
+    """
+    _validate_scheme(scheme)
+    if bias_shift and scheme.fmt.minifloat is None:
+        raise InvalidScheme("bias shift applies to minifloat formats only")
+    _require_path(scheme)
+    w, torch_in = _weights_to_device(W)
+    n, k = (int(v) for v in w.shape)
+    t = _lib.torch()
+    if n == 0 or k == 0:
+        if torch_in:
+            e16 = t.zeros(0, dtype=t.float16, device=w.device)
+            e8 = t.zeros(0, dtype=t.uint8, device=w.device)
+            return QuantizedTensor(n, k, scheme, e16, None, PackedSegments(e8, e8.clone(), 0), bias_shift,
+                                   e16.clone() if bias_shift else None)
+        e16 = np.zeros(0, dtype=np.float16)
+        e8 = np.zeros(0, dtype=np.uint8)
+        return QuantizedTensor(n, k, scheme, e16, None, PackedSegments(e8, e8.copy(), 0), bias_shift,
+                               e16.copy() if bias_shift else None)
+    d = quantize_device(w, bias_shift)
+    cache = {"scales": d["scales"], "seg4": d["seg4"], "seg2": d["seg2"]}
+    if torch_in:
+        return QuantizedTensor(n, k, scheme, d["scales"], None, PackedSegments(d["seg4"], d["seg2"], n * k),
+                               bias_shift, d["folded"], cache)
+    return QuantizedTensor(n, k, scheme, d["scales"].cpu().numpy(), None,
+                           PackedSegments(d["seg4"].cpu().numpy(), d["seg2"].cpu().numpy(), n * k),
+                           bias_shift, None if d["folded"] is None else d["folded"].cpu().numpy(), cache)
+
+
+def compute_scale_fp(values, fmt: MiniFloatFormat) -> BlockParams:
+    """Max-abs scale of one block (quantizer.py:156-163), via the GPU quantizer."""
+    if fmt != FP6_E3M2:
+        raise InvalidScheme(f"{fmt.name} is outside the B200 FP6 path")
+    v = np.asarray(values, dtype=np.float64).ravel()
+    if v.size == 0:
+        raise InvalidInput("block must be non-empty")
+    q = quantize_tensor(v.reshape(1, -1), CGQ_FP6, bias_shift=False)
+    return BlockParams(scale=np.float16(q.scales[0]))
+
+
+def compute_affine_params_int4(values) -> BlockParams:
+    raise InvalidScheme("INT4 is outside the B200 FP6 path")
+
+
+def device_planes(q: QuantizedTensor):
+    """(seg4, seg2, scales) of `q` as CUDA tensors (cached when built here)."""
+    if q.device_cache is not None and "seg4" in q.device_cache:
+        c = q.device_cache
+        return c["seg4"], c["seg2"], c["scales"]
+    n = q.rows * q.cols
+    if not isinstance(q.payload, PackedSegments) or q.payload.code_count != n:
+        raise PayloadMismatch("payload does not hold rows*cols codes")
+    s4 = _lib.to_device(q.payload.seg4).reshape(-1)
+    s2 = _lib.to_device(q.payload.seg_tail).reshape(-1)
+    if s4.numel() != seg4_length(n) or s2.numel() != tail_length(FP6_E3M2, n):
+        raise PayloadMismatch("segment lengths inconsistent with rows*cols")
+    t = _lib.torch()
+    sc = q.scales if _lib.is_torch(q.scales) else np.asarray(q.scales, dtype=np.float16)
+    sc = _lib.to_device(sc).reshape(-1).to(t.float16)
+    return s4, s2, sc
+
+
+def dequantize_tensor(q: QuantizedTensor, path: str = "naive"):
+    """f64-exact reconstruction (quantizer.py:269-299) on the GPU."""
+    torch_in = _lib.is_torch(q.scales)
+    t = _lib.torch()
+    if q.rows == 0 or q.cols == 0:
+        return t.zeros((q.rows, q.cols), dtype=t.float64, device=_lib.device()) if torch_in \
+            else np.zeros((q.rows, q.cols), dtype=np.float64)
+    if q.num_blocks != num_blocks(q.rows, q.cols, q.scheme):
+        raise PayloadMismatch("block parameter count does not match the scheme")
+    _require_path(q.scheme)
+    if path == "naive":
+        s4, s2, row_scale = device_planes(q)
+        p = 0
+    elif path == "bias_shift":
+        if q.folded_scales is None:
+            raise PathUnavailable("tensor carries no folded scales")
+        s4, s2, _ = device_planes(q)
+        f = q.folded_scales if _lib.is_torch(q.folded_scales) else np.asarray(q.folded_scales, np.float16)
+        row_scale = _lib.to_device(f).reshape(-1).to(t.float16)
+        p = 1
+    else:
+        raise ValueError(f"unknown dequantization path {path!r}")
+    out = t.empty((q.rows, q.cols), dtype=t.float64, device=s4.device)
+    _lib.check(_lib.load().lpqt_fp6_dequantize_tensor(
+        s4.data_ptr(), s2.data_ptr(), row_scale.data_ptr(), p, q.rows, q.cols, out.data_ptr(), _lib.F64,
+        _lib.stream_ptr()), "dequantize_tensor")
+    return out if torch_in else out.cpu().numpy()
+
+
+def error_report(W, W_hat) -> ErrorReport:
+    """MSE / max-abs / SQNR between a tensor and its proxy (quantizer.py:302-320).
+    A metrics utility, not on the compute path."""
+    if _lib.is_torch(W):
+        W = W.detach().cpu().numpy()
+    if _lib.is_torch(W_hat):
+        W_hat = W_hat.detach().cpu().numpy()
+    W = np.asarray(W, dtype=np.float64)
+    W_hat = np.asarray(W_hat, dtype=np.float64)
+    if W.shape != W_hat.shape:
+        raise ShapeError(f"shape mismatch: {W.shape} vs {W_hat.shape}")
+    if W.size == 0:
+        return ErrorReport(0.0, 0.0, float("inf"))
+    err = W - W_hat
+    mse = float(np.mean(err * err))
+    sig = float(np.mean(W * W))
+    sqnr = float("inf") if mse == 0.0 else (float("-inf") if sig == 0.0 else 10.0 * float(np.log10(sig / mse)))
+    return ErrorReport(mse, float(np.max(np.abs(err))), sqnr)

@@ -1,0 +1,239 @@
+"""GPU parity: the CUDA path (through the C ABI) against the reference's golden
+vectors and the CPU oracle.
+
+Bars (BASELINE.json north_star): codes / packed bytes / scales / folded are
+BIT-EXACT; GEMM outputs have normwise relative error
+max|Y - Y_ref| / max|Y_ref| <= 1e-3 against the fp32 dequantize-then-matmul
+(and, where the reference's own test uses it, the elementwise bound
+gemm_tolerance = 4 eps32 K max|W_hat| max|X|, gemm.py:118-122).
+"""
+
+import hashlib
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = [pytest.mark.gpu,
+              pytest.mark.skipif(not torch.cuda.is_available(), reason="needs a CUDA device")]
+
+import paper_2312_08583_b200 as L  # noqa: E402
+from oracle import lpqt_oracle as O  # noqa: E402  (checker only)
+from tests.conftest import names  # noqa: E402
+
+CGQ = L.QuantScheme(L.Granularity.CGQ, L.TensorFormat.FP6_E3M2)
+REL_TOL = 1e-3
+
+
+def normwise_rel(Y, Yref):
+    Y = np.asarray(Y, np.float64)
+    Yref = np.asarray(Yref, np.float64)
+    den = np.max(np.abs(Yref))
+    return float(np.max(np.abs(Y - Yref)) / den) if den else float(np.max(np.abs(Y)))
+
+
+# ---------------------------------------------------------------- quantize
+def test_quantize_bit_exact_vs_reference(golden):
+    for name in names(golden, "q_names"):
+        W = golden[f"q/{name}/W"]
+        if name.startswith("bf16"):
+            Win = torch.from_numpy(W).to(torch.bfloat16).cuda()
+            q = L.quantize_tensor(Win, CGQ, bias_shift=True)
+            scales, folded = q.scales.cpu().numpy(), q.folded_scales.cpu().numpy()
+            seg4, seg2 = q.payload.seg4.cpu().numpy(), q.payload.seg_tail.cpu().numpy()
+        else:
+            q = L.quantize_tensor(W, CGQ, bias_shift=True)
+            scales, folded, seg4, seg2 = q.scales, q.folded_scales, q.payload.seg4, q.payload.seg_tail
+        assert np.array_equal(scales.view(np.uint16), golden[f"q/{name}/scales"]), name
+        assert np.array_equal(folded.view(np.uint16), golden[f"q/{name}/folded"]), name
+        assert np.array_equal(seg4, golden[f"q/{name}/seg4"]), name
+        assert np.array_equal(seg2, golden[f"q/{name}/seg2"]), name
+        deq = L.dequantize_tensor(q, "bias_shift")
+        deq = deq.cpu().numpy() if torch.is_tensor(deq) else deq
+        assert np.array_equal(deq, golden[f"q/{name}/deq"]), name
+        naive = L.dequantize_tensor(q, "naive")
+        naive = naive.cpu().numpy() if torch.is_tensor(naive) else naive
+        assert np.array_equal(naive, golden[f"q/{name}/deq"]), name
+
+
+def test_quantize_error_cases_vs_reference(golden):
+    for name in names(golden, "e_names"):
+        W = golden[f"e/{name}/W"]
+        bs = bool(golden[f"e/{name}/bias_shift"])
+        want = str(golden[f"e/{name}/result"])
+        try:
+            q = L.quantize_tensor(W, CGQ, bias_shift=bs)
+            got = "ok"
+            assert np.array_equal(q.scales.view(np.uint16), golden[f"e/{name}/scales"])
+        except L.LpqtError as exc:
+            got = type(exc).__name__
+        assert got == want, name
+
+
+@pytest.mark.parametrize("dtype", [np.float64, np.float32, np.float16])
+@pytest.mark.parametrize("shape", [(1, 1), (3, 5), (17, 40), (128, 264), (257, 1000)])
+def test_quantize_random_vs_oracle(dtype, shape):
+    rng = np.random.default_rng(hash((shape, np.dtype(dtype).name)) % 2**32)
+    W = (rng.standard_normal(shape) * rng.choice([1e-3, 0.02, 1.0, 30.0])).astype(dtype)
+    W[rng.random(shape) < 0.05] = 0
+    q = L.quantize_tensor(W, CGQ, bias_shift=True)
+    o = O.quantize_tensor(W, bias_shift=True)
+    assert np.array_equal(q.scales.view(np.uint16), o["scales"].view(np.uint16))
+    assert np.array_equal(q.folded_scales.view(np.uint16), o["folded"].view(np.uint16))
+    assert np.array_equal(q.payload.seg4, o["seg4"])
+    assert np.array_equal(q.payload.seg_tail, o["seg2"])
+
+
+def test_quantize_llama_shape_codes_match_oracle():
+    # full-row property at a realistic size: codes of every row equal the oracle's
+    rng = np.random.default_rng(7)
+    W = (rng.standard_normal((512, 4096)) * 0.02).astype(np.float16)
+    q = L.quantize_tensor(torch.from_numpy(W).cuda(), CGQ, bias_shift=True)
+    o = O.quantize_tensor(W, bias_shift=True)
+    assert np.array_equal(q.payload.seg4.cpu().numpy(), o["seg4"])
+    assert np.array_equal(q.payload.seg_tail.cpu().numpy(), o["seg2"])
+
+
+def test_empty_inputs():
+    q = L.quantize_tensor(np.zeros((0, 5)), CGQ, bias_shift=True)
+    assert q.scales.size == 0 and q.payload.code_count == 0
+    q = L.quantize_tensor(np.zeros((3, 0)), CGQ)
+    Y = L.gemm_quantized(q, np.zeros((0, 2), np.float32))
+    assert Y.shape == (3, 2) and not Y.any()
+
+
+# ---------------------------------------------------------------- codec / packing / fold
+def test_encode_vs_reference(golden):
+    assert np.array_equal(L.encode_rtn_array(L.FP6_E3M2, golden["enc/x"]), golden["enc/codes"])
+    with pytest.raises(L.InvalidInput):
+        L.encode_rtn_array(L.FP6_E3M2, np.array([1.0, np.inf]))
+    assert L.encode_rtn(L.FP6_E3M2, 26.0) == 0b011110
+
+
+def test_pack_unpack_vs_reference(golden):
+    for n in golden["p_lens"]:
+        c = golden[f"p/{n}/codes"]
+        seg = L.pack(L.FP6_E3M2, c)
+        assert np.array_equal(seg.seg4, golden[f"p/{n}/seg4"]), n
+        assert np.array_equal(seg.seg_tail, golden[f"p/{n}/seg2"]), n
+        assert np.array_equal(L.unpack(L.FP6_E3M2, seg), c)
+    seg = L.pack(L.FP6_E3M2, [0b011111, 0b001100, 0, 0b100001])
+    assert list(seg.seg4) == [0x37, 0x80, 0, 0] and list(seg.seg_tail) == [0x43, 0, 0, 0]
+    with pytest.raises(L.InvalidCode):
+        L.pack(L.FP6_E3M2, [64])
+    with pytest.raises(L.PayloadMismatch):
+        L.unpack(L.FP6_E3M2, L.PackedSegments(seg.seg4[:-1], seg.seg_tail, 4))
+
+
+def test_fold_and_exhaustive_bias_shift_sweep(golden):
+    s = golden["fold/scales"].view(np.float16)
+    f = L.fold_scale_array(L.FP6_E3M2, s)
+    assert np.array_equal(f.view(np.uint16), golden["fold/folded"])
+    codes = np.arange(64, dtype=np.uint8)
+    sweep = L.dequant_bias_shift_array(L.FP6_E3M2, codes[:, None], f[None, :])
+    naive = L.dequant_naive_array(L.FP6_E3M2, codes[:, None], s[None, :])
+    assert np.array_equal(sweep.view(np.uint16), naive.view(np.uint16))
+    assert hashlib.sha256(sweep.view(np.uint16).tobytes()).hexdigest() == str(golden["fold/sweep_sha256"])
+    with pytest.raises(L.ScaleOverflow):
+        L.fold_scale(L.FP6_E3M2, np.float16(16.0))
+    with pytest.raises(L.InvalidInput):
+        L.fold_scale_array(L.FP6_E3M2, np.array([0.0], np.float16))
+
+
+# ---------------------------------------------------------------- tile layout + transform
+@pytest.mark.parametrize("shape", [(1, 1), (5, 33), (128, 128), (130, 300), (384, 1024)])
+def test_prepack_roundtrip_and_register_transform(shape):
+    rng = np.random.default_rng(11)
+    n, k = shape
+    codes = rng.integers(0, 64, size=n * k, dtype=np.uint8)
+    seg4, seg2 = O.pack(codes)
+    scales = (rng.uniform(1e-4, 15.9, size=n)).astype(np.float16)
+    folded = O.fold_scale_array(scales)
+    w = L.Fp6Weight.from_planes(torch.from_numpy(seg4).cuda(), torch.from_numpy(seg2).cuda(),
+                                torch.from_numpy(scales).cuda(), n, k, torch.from_numpy(folded).cuda())
+    assert np.array_equal(w.codes().cpu().numpy().ravel(), codes)
+    deq = w.dequantize_f16().cpu().numpy()
+    ref = O.dequant_bias_shift_array(codes.reshape(n, k), folded[:, None])
+    assert np.array_equal(deq.view(np.uint16), ref.view(np.uint16))
+
+
+# ---------------------------------------------------------------- GEMM
+def test_gemm_vs_reference_golden(golden):
+    for name in names(golden, "g_names"):
+        W, X = golden[f"g/{name}/W"], golden[f"g/{name}/X"]
+        q = L.quantize_tensor(W, CGQ, bias_shift=True)
+        Y = L.gemm_quantized(q, X)
+        assert Y.dtype == np.float32 and Y.shape == golden[f"g/{name}/Y"].shape
+        assert normwise_rel(Y, golden[f"g/{name}/Y"]) <= REL_TOL, name
+        # the reference's own elementwise f32-vs-f64 bound (tests/test_gemm.py:100-107)
+        assert np.max(np.abs(Y - golden[f"g/{name}/Yf64"])) <= float(golden[f"g/{name}/tol"]) + 1e-30, name
+        if name.startswith("grid_exact"):
+            assert np.array_equal(Y.astype(np.float64), golden[f"g/{name}/Yf64"])
+
+
+def test_gemm_identity_weights_exact():
+    # pkg/tests/test_gemm.py:59-64: identity stored with unit scale
+    n = 130
+    codes = np.zeros((n, n), np.uint8)
+    codes[np.arange(n), np.arange(n)] = 0b001100
+    s4, s2 = O.pack(codes.ravel())
+    q = L.QuantizedTensor(n, n, CGQ, np.ones(n, np.float16), None, L.PackedSegments(s4, s2, n * n))
+    X = np.random.default_rng(31).standard_normal((n, 5)).astype(np.float16)
+    assert np.array_equal(L.gemm_quantized(q, X), X.astype(np.float32))
+
+
+def test_gemm_subnormal_codes_one_hot():
+    # composed values of codes 1-3 are binary16 subnormals (dequant.py:40):
+    # one-hot activation columns must reproduce every weight exactly
+    rng = np.random.default_rng(5)
+    n, k = 256, 128
+    codes = rng.choice(np.array([1, 2, 3, 33, 34, 35, 0, 31, 63], np.uint8), size=(n, k))
+    scales = rng.uniform(1e-3, 15.0, size=n).astype(np.float16)
+    s4, s2 = O.pack(codes.ravel())
+    q = L.QuantizedTensor(n, k, CGQ, scales, None, L.PackedSegments(s4, s2, n * k))
+    X = np.eye(k, dtype=np.float16)
+    Y = L.gemm_quantized(q, X)
+    ref = O.dequantize_tensor(codes.ravel(), n, k, scales=scales, path="naive").astype(np.float32)
+    assert np.array_equal(Y, ref)
+
+
+SHAPES = [(4096, 4096, 1), (4096, 4096, 16), (1024, 2048, 7), (512, 640, 33), (256, 1024, 129),
+          (384, 512, 300), (256, 384, 600)]
+
+
+@pytest.mark.parametrize("n,k,m", SHAPES)
+def test_gemm_llama_like_vs_dequant_matmul(n, k, m):
+    g = torch.Generator(device="cuda").manual_seed(n * 7 + k * 3 + m)
+    W = (torch.randn(n, k, generator=g, device="cuda") * 0.02).half()
+    X = torch.randn(k, m, generator=g, device="cuda").half()
+    q = L.quantize_tensor(W, CGQ, bias_shift=True)
+    W_hat = L.dequantize_tensor(q, "bias_shift")       # f64, exact
+    Y = L.gemm_quantized(q, X)
+    Y_ref = (W_hat @ X.double()).float()                  # dequantize-then-matmul (f64)
+    assert normwise_rel(Y.cpu().numpy(), Y_ref.cpu().numpy()) <= REL_TOL
+
+
+@pytest.mark.parametrize("split_k", [1, 2, 3, 7])
+def test_gemm_split_k_variants_agree(split_k):
+    g = torch.Generator(device="cuda").manual_seed(3)
+    W = (torch.randn(512, 3072, generator=g, device="cuda") * 0.02).half()
+    X = torch.randn(3072, 16, generator=g, device="cuda").half()
+    q = L.quantize_tensor(W, CGQ, bias_shift=True)
+    Y = L.gemm_quantized(q, X, split_k=split_k)
+    Y_ref = (L.dequantize_tensor(q, "bias_shift") @ X.double()).float()
+    assert normwise_rel(Y.cpu().numpy(), Y_ref.cpu().numpy()) <= REL_TOL
+    Y2 = L.gemm_quantized(q, X, split_k=split_k)
+    assert torch.equal(Y.view(torch.int32), Y2.view(torch.int32))   # deterministic
+
+
+def test_w6a16_linear_torch_layout():
+    g = torch.Generator(device="cuda").manual_seed(9)
+    W = (torch.randn(1000, 520, generator=g, device="cuda") * 0.05).half()
+    lin = L.Fp6Linear.from_dense(W)
+    for m in (1, 5, 16, 40):
+        x = torch.randn(m, 520, generator=g, device="cuda").half()
+        y = lin(x)
+        assert y.shape == (m, 1000) and y.dtype == torch.float16
+        q = L.quantize_tensor(W, CGQ, bias_shift=True)
+        ref = (L.dequantize_tensor(q, "bias_shift") @ x.double().T).T
+        assert normwise_rel(y.float().cpu().numpy(), ref.cpu().numpy()) <= REL_TOL
