@@ -1,0 +1,526 @@
+"""bench.py — W6A16 (FP6 e3m2 weight, FP16 activation) linear on B200.
+
+Workload (N=1, BASELINE.json configs[1]): one LLaMA-2-7B decoder block's four
+linear layers (QKV 12288x4096, O 4096x4096, gate_up 22016x4096, down
+4096x11008) at decode batch M (default 16).  A "step" = those four W6A16
+GEMMs over one batch.  Synthetic data: random-init N(0, 0.02) weights
+quantized on the GPU, N(0, 1) fp16 activations.
+
+Metric (BASELINE.json): "W6A16 linear TFLOPS & weight HBM GB/s vs roofline
+and cuBLAS FP16, batch 1-512" -> value = algorithmic HBM GB/s of the step
+(FP6 planes 0.75 B/weight + 2 B/row scales + fp16 X + fp16 Y); TFLOPS,
+cuBLAS fp16 and the roofline fraction ride along.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--m 16] [--impl ours|reference]
+
+N>1 (torchrun): column-sharded tensor parallelism: every rank
+holds N/P rows of every layer, runs its shard GEMM, and one NCCL
+all_gather_into_tensor per layer assembles Y[N, M] -> "scaling": "strong".
+
+Timing: W untimed warm-up steps, then EXACTLY K steps replayed from CUDA
+graphs, bracketed by barrier + synchronize, device-timed with CUDA events,
+max over ranks.  L2: the step's weights (151 MB FP6) are rotated over two
+distinct copies (302 MB > 2 x 126 MB L2), so every step reads cold weights.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+LAYERS_7B = [("qkv", 12288, 4096), ("o", 4096, 4096), ("gate_up", 22016, 4096), ("down", 4096, 11008)]
+LAYERS_70B = [("qkv", 10240, 8192), ("o", 8192, 8192), ("gate_up", 57344, 8192), ("down", 8192, 28672)]
+METRIC = "W6A16 linear TFLOPS & weight HBM GB/s vs roofline and cuBLAS FP16, batch 1-512"
+FALLBACK_PEAKS = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0}
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return {"hbm_gbs": float(d["hbm_gbs"]), "bf16_tflops": float(d["bf16_tflops"]),
+                "bf16_tflops_sustained": float(d.get("bf16_tflops_sustained", d["bf16_tflops"])),
+                "source": "measured (MEASURED_PEAKS.json)"}
+    return dict(FALLBACK_PEAKS, bf16_tflops_sustained=FALLBACK_PEAKS["bf16_tflops"],
+                source="fallback (B200_PROFILING.md)")
+
+
+def step_bytes(layers, m):
+    """Algorithmic bytes of one step: FP6 planes + f16 row scales + X + Y (fp16)."""
+    tot = 0
+    for _, n, k in layers:
+        nk = n * k
+        seg4 = ((nk + 1) // 2 + 3) // 4 * 4
+        seg2 = ((2 * nk + 7) // 8 + 3) // 4 * 4
+        tot += seg4 + seg2 + 2 * n + 2 * m * k + 2 * m * n
+    return tot
+
+
+def layer_bytes(n, k, m):
+    return step_bytes([("", n, k)], m)
+
+
+def step_flops(layers, m):
+    return sum(2 * m * n * k for _, n, k in layers)
+
+
+# ---------------------------------------------------------------------------
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled every 100 ms while active."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index=0):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except (OSError, FileNotFoundError):
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 8:
+                self.rows.append(parts)
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            time.sleep(0.15)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[4 + i].lower().startswith("active")})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+# ---------------------------------------------------------------------------
+def setup_dist(args):
+    import torch
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    elif torch.cuda.is_available():
+        torch.cuda.set_device(0)
+    return world, rank, local
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def max_over_ranks(x, world):
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def build_layers(layers, world, rank, copies, seed=0):
+    """Quantize + prepack each layer's row shard on the GPU; `copies` distinct
+    weight sets for L2 rotation.  Returns list[copy] of list[Fp6Weight]."""
+    import torch
+    import paper_2312_08583_b200 as L
+    from paper_2312_08583_b200.tp import shard_rows
+    g = torch.Generator(device="cuda").manual_seed(seed + 1000 * rank)
+    sets = []
+    for _ in range(copies):
+        ws = []
+        for _, n, k in layers:
+            a, b = shard_rows(n, world, rank)
+            W = (torch.randn(b - a, k, generator=g, device="cuda") * 0.02).half()
+            ws.append(L.Fp6Weight.quantize(W, bias_shift=True))
+            del W
+        sets.append(ws)
+    torch.cuda.synchronize()
+    return sets
+
+
+def run_ours(args, world, rank):
+    import torch
+    import paper_2312_08583_b200 as L
+    from paper_2312_08583_b200 import _lib
+    from paper_2312_08583_b200.linear import gemm_nm
+
+    layers = LAYERS_7B if args.model == "llama2-7b" else LAYERS_70B
+    m = args.m
+    l2 = torch.cuda.get_device_properties(0).L2_cache_size
+    fp6_set = step_bytes(layers, 0) // world
+    copies = max(2, -(-2 * l2 // max(fp6_set, 1)))
+    sets = build_layers(layers, world, rank, copies)
+
+    gen = torch.Generator(device="cuda").manual_seed(7)
+    xs = [torch.randn(k, m, generator=gen, device="cuda").half() for _, _, k in layers]   # X[K, M]
+    xts = [x.t().contiguous() for x in xs]                                                # K-major operand
+    shard_n = [sets[0][i].n for i in range(len(layers))]
+    ys = [torch.empty(n_local, m, device="cuda", dtype=torch.float16) for n_local in shard_n]
+    yfull = [torch.empty(n, m, device="cuda", dtype=torch.float16) for _, n, _ in layers]
+    lib = _lib.load()
+
+    def launch(i, w):
+        # reference layout Y[N_p, M] (gemm.py:65), fp16 out
+        ws_bytes = int(lib.lpqt_w6a16_workspace_bytes(m, w.n, w.k, 0))
+        ws = _lib.Workspace.get(ws_bytes) if ws_bytes else None
+        _lib.check(lib.lpqt_w6a16_linear(w.tiles.data_ptr(), w.scales.data_ptr(), xts[i].data_ptr(), w.k, m,
+                                         w.n, w.k, ys[i].data_ptr(), _lib.F16, _lib.Y_NM, m, 0, _lib.ptr(ws),
+                                         ws.numel() if ws is not None else 0, _lib.stream_ptr()))
+
+    def step(c):
+        for i, w in enumerate(sets[c]):
+            launch(i, w)
+            if world > 1:
+                import torch.distributed as dist
+                dist.all_gather_into_tensor(yfull[i], ys[i])
+
+    # warm-up (also allocates the workspace before capture)
+    for s in range(max(args.warmup, 1)):
+        step(s % copies)
+    torch.cuda.synchronize()
+
+    # one graph per weight copy; external events inside bracket every launch
+    graphs, inner = [], []
+    for c in range(copies):
+        evs = [torch.cuda.Event(enable_timing=True, external=True) for _ in range(len(layers) + 1)]
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            for i, w in enumerate(sets[c]):
+                evs[i].record()
+                launch(i, w)
+                if world > 1:
+                    import torch.distributed as dist
+                    dist.all_gather_into_tensor(yfull[i], ys[i])
+            evs[-1].record()
+        graphs.append(g)
+        inner.append(evs)
+    for s in range(args.warmup):
+        graphs[s % copies].replay()
+    torch.cuda.synchronize()
+
+    # burn-in so the clock sampler sees the part under load, then the timed region
+    launches_before = _lib.launch_count()
+    with ClockSampler(int(os.environ.get("LOCAL_RANK", "0"))) as clk:
+        t_end = time.time() + args.burn_in
+        while time.time() < t_end:
+            for c in range(copies):
+                graphs[c].replay()
+            torch.cuda.synchronize()
+        barrier(world)
+        torch.cuda.synchronize()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for s in range(args.steps):
+            graphs[s % copies].replay()
+        e1.record()
+        torch.cuda.synchronize()
+        barrier(world)
+    t_local = e0.elapsed_time(e1) * 1e-3
+    t = max_over_ranks(t_local, world)
+    gpu_launches = args.steps * len(layers)          # kernel nodes per replayed graph x replays
+    assert _lib.launch_count() == launches_before     # replays, no new host launches
+
+    # per-launch durations from the last replay of every graph (inside the timed region)
+    per_layer = []
+    for i, (name, n, k) in enumerate(layers):
+        d = statistics.mean(inner[c][i].elapsed_time(inner[c][i + 1]) * 1e-3 for c in range(copies))
+        nb = layer_bytes(sets[0][i].n, k, m)
+        per_layer.append({"layer": name, "n": sets[0][i].n, "k": k, "us": round(d * 1e6, 2),
+                          "GBps": round(nb / d / 1e9, 1), "plan": L.plan(m, sets[0][i].n, k)})
+
+    total_bytes = step_bytes(layers, m)       # whole job (all ranks)
+    value = total_bytes * args.steps / t / 1e9
+    res = {"t": t, "value": value, "per_layer": per_layer, "gpu_launches": gpu_launches,
+           "clocks": clk.summary(), "copies": copies}
+
+    # cuBLAS fp16 comparator on the same step (fp16 weights, same shards)
+    if rank == 0 or world > 1:
+        res["cublas"] = time_cublas(layers, world, rank, m, args)
+    # e2e through the public API with host buffers
+    res["e2e"] = time_e2e(layers, sets[0], world, rank, m, args)
+    return res
+
+
+def time_cublas(layers, world, rank, m, args):
+    import torch
+    from paper_2312_08583_b200.tp import shard_rows
+    l2 = torch.cuda.get_device_properties(0).L2_cache_size
+    f16_set = sum(2 * n * k for _, n, k in layers) // world
+    copies = max(1, -(-2 * l2 // f16_set))
+    g = torch.Generator(device="cuda").manual_seed(11)
+    wsets = []
+    for _ in range(copies):
+        wsets.append([(torch.randn(*(lambda ab: (ab[1] - ab[0], k))(shard_rows(n, world, rank)), generator=g,
+                                   device="cuda") * 0.02).half() for _, n, k in layers])
+    xs = [torch.randn(m, k, generator=g, device="cuda").half() for _, _, k in layers]
+    outs = [None] * len(layers)
+
+    def step(c):
+        for i, W in enumerate(wsets[c]):
+            outs[i] = torch.matmul(xs[i], W.t())
+
+    for c in range(copies):
+        step(c)
+    torch.cuda.synchronize()
+    graphs = []
+    for c in range(copies):
+        gr = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(gr):
+            step(c)
+        graphs.append(gr)
+    for s in range(max(args.warmup, 3)):
+        graphs[s % copies].replay()
+    torch.cuda.synchronize()
+    steps = max(args.steps // 2, 50)
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for s in range(steps):
+        graphs[s % copies].replay()
+    e1.record()
+    torch.cuda.synchronize()
+    t = e0.elapsed_time(e1) * 1e-3 / steps
+    f16_bytes = sum(2 * n * k + 2 * m * k + 2 * m * n for _, n, k in layers) // world
+    del wsets
+    torch.cuda.empty_cache()
+    return {"ms_per_step": round(t * 1e3, 4), "GBps_fp16_weights": round(f16_bytes / t / 1e9, 1),
+            "TFLOPS": round(step_flops(layers, m) / world / t / 1e12, 2), "copies": copies}
+
+
+def time_e2e(layers, wset, world, rank, m, args):
+    """Same metric through the reference-facing API, host buffers: per layer
+    `gemm_quantized`-equivalent call with X[K, M] from pinned host memory and
+    the f32 result read back to pinned host memory, every step."""
+    import torch
+    import paper_2312_08583_b200 as L
+    from paper_2312_08583_b200.linear import gemm_nm, stage_activations
+    xh = [torch.randn(k, m).half().pin_memory() for _, _, k in layers]
+    yh = [torch.empty(w.n, m, dtype=torch.float32).pin_memory() for w in wset]
+
+    def step():
+        for i, w in enumerate(wset):
+            xd = xh[i].to("cuda", non_blocking=True)
+            xt, kp = stage_activations(xd, w.k)
+            y = gemm_nm(w, xt, kp, m)
+            yh[i].copy_(y, non_blocking=True)
+        torch.cuda.synchronize()
+
+    for _ in range(max(args.warmup, 3)):
+        step()
+    steps = max(min(args.steps, 500), 20)
+    barrier(world)
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        step()
+    t = time.perf_counter() - t0
+    t = max_over_ranks(t, world)
+    h2d = sum(2 * k * m for _, _, k in layers)
+    d2h = sum(4 * w.n * m for w in wset) * world
+    return {"value": round(step_bytes(layers, m) * steps / t / 1e9, 2), "unit": "GB/s",
+            "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+            "ms_per_step": round(t / steps * 1e3, 4),
+            "api": "paper_2312_08583_b200 stage_activations + gemm_nm (the gemm_quantized path), pinned host X/Y"}
+
+
+# ---------------------------------------------------------------------------
+def cpu_baseline(layers, m, budget_s=12.0):
+    """Oracle port of the reference CPU path (gemm.py:65-94: unpack -> value
+    table -> ascending-k fp32 loop -> row scale), timed on this host, 1 core,
+    on a bounded sample: the full step's layers, each restricted to its first
+    R rows (sample), repeated until `budget_s` elapsed."""
+    from oracle import lpqt_oracle as O
+    rng = np.random.default_rng(0)
+    rows = 256
+    sample = []
+    for _, n, k in layers:
+        W = (rng.standard_normal((rows, k)) * 0.02).astype(np.float16)
+        q = O.quantize_tensor(W, bias_shift=True)
+        X = rng.standard_normal((k, m)).astype(np.float16)
+        sample.append((q, rows, k, X))
+    nbytes = step_bytes([("", rows, k) for _, _, k in layers], m)
+    reps = 0
+    t0 = time.perf_counter()
+    while True:
+        for q, r, k, X in sample:
+            O.gemm_quantized(q["codes"], q["scales"], r, k, X)
+        reps += 1
+        if time.perf_counter() - t0 > budget_s:
+            break
+    t = time.perf_counter() - t0
+    return {"value": round(nbytes * reps / t / 1e9, 5), "unit": "GB/s", "cores": 1, "kind": "port",
+            "sample": f"oracle gemm_quantized on the first {rows} rows of each of the 4 layers at M={m}, "
+                      f"{reps} reps in {t:.1f}s (numpy, single process)"}
+
+
+def run_reference(args, world, rank):
+    """--impl reference: the reference's CPU algorithm (oracle port) on all host
+    threads, row-parallel over a process pool (SPEC.md:373-375 permits
+    row parallelism), each step a bounded row sample of the workload."""
+    import multiprocessing as mp
+    layers = LAYERS_7B if args.model == "llama2-7b" else LAYERS_70B
+    m = args.m
+    cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
+    rows_per_worker = 32
+    with mp.get_context("fork").Pool(cores, initializer=_ref_init, initargs=(layers, m, rows_per_worker)) as pool:
+        for _ in range(max(args.warmup, 1)):
+            pool.map(_ref_step, range(cores))
+        t_budget = 120.0
+        steps = 0
+        t0 = time.perf_counter()
+        while steps < args.steps:
+            pool.map(_ref_step, range(cores))
+            steps += 1
+            if time.perf_counter() - t0 > t_budget:
+                break
+        t = time.perf_counter() - t0
+    nbytes = step_bytes([("", rows_per_worker * cores, k) for _, _, k in layers], m)
+    value = nbytes * steps / t / 1e9
+    sample = (f"oracle gemm_quantized (numpy ascending-k) on {rows_per_worker} rows x {cores} processes of "
+              f"each 7B layer per step, M={m}; {steps} steps timed")
+    return {"value": value, "t": t, "steps": steps, "cores": cores, "sample": sample}
+
+
+_REF = {}
+
+
+def _ref_init(layers, m, rows):
+    from oracle import lpqt_oracle as O
+    rng = np.random.default_rng(os.getpid())
+    _REF["work"] = []
+    for _, n, k in layers:
+        W = (rng.standard_normal((rows, k)) * 0.02).astype(np.float16)
+        q = O.quantize_tensor(W, bias_shift=True)
+        _REF["work"].append((q["codes"], q["scales"], rows, k, rng.standard_normal((k, m)).astype(np.float16)))
+
+
+def _ref_step(_):
+    from oracle import lpqt_oracle as O
+    for codes, scales, r, k, X in _REF["work"]:
+        O.gemm_quantized(codes, scales, r, k, X)
+    return 0
+
+
+# ---------------------------------------------------------------------------
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=2000)
+    ap.add_argument("--warmup", type=int, default=20)
+    ap.add_argument("--m", type=int, default=16, help="decode batch (tokens)")
+    ap.add_argument("--model", default="llama2-7b", choices=["llama2-7b", "llama2-70b"])
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--burn-in", type=float, default=1.5, help="seconds of untimed load before timing")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    layers = LAYERS_7B if args.model == "llama2-7b" else LAYERS_70B
+    workload = f"{args.model} decoder-block linears (QKV/O/gate_up/down) decode M={args.m}"
+    config = {"workload": workload, "layers": [f"{n}x{k}" for _, n, k in layers], "batch_m": args.m,
+              "tensor_parallel": world, "parallelism": f"tp{world} column-sharded + NCCL all-gather"
+              if world > 1 else "single GPU", "activations": "fp16", "weights": "FP6 e3m2 (4+2), per-row f16 scale",
+              "l2_hygiene": "inputs larger than L2: weights rotated over >=2 distinct copies (>2x L2) per step"}
+
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        r = run_reference(args, world, rank)
+        line = {"metric": METRIC, "value": round(r["value"], 6), "unit": "GB/s", "n_gpus": args.gpus,
+                "steps": r["steps"], "warmup": args.warmup, "ms_per_step": round(r["t"] / r["steps"] * 1e3, 3),
+                "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+                "data": "synthetic", "config": config, "impl": "reference",
+                "cpu_baseline": {"value": round(r["value"], 6), "unit": "GB/s", "cores": r["cores"],
+                                 "kind": "port", "sample": r["sample"]},
+                "e2e": {"value": round(r["value"], 6), "unit": "GB/s", "h2d_bytes_per_step": 0,
+                        "d2h_bytes_per_step": 0}}
+        print(json.dumps(line), flush=True)
+        return
+
+    import torch
+    world, rank, _ = setup_dist(args)
+    peaks = load_peaks()
+    res = run_ours(args, world, rank)
+    m = args.m
+    t_step = res["t"] / args.steps
+    flops = step_flops(layers, m)
+    # roofline of the dominant kernel (the W6A16 GEMM; all four launches)
+    tot_b = sum(layer_bytes(p["n"], p["k"], m) for p in res["per_layer"])
+    tot_t = sum(p["us"] for p in res["per_layer"]) * 1e-6
+    achieved = tot_b / tot_t / 1e9
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tp):
+        with open(tp) as f:
+            traffic = json.load(f).get(f"{args.model}_m{m}")
+    if rank != 0:
+        return
+    line = {
+        "metric": METRIC, "value": round(res["value"], 2), "unit": "GB/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(t_step * 1e3, 5),
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "dtype": "fp16 x fp6(e3m2) -> fp32 accumulate", "data": "synthetic (random-init weights, N(0,1) fp16 X)",
+        "config": config,
+        "tflops": round(flops / t_step / 1e12, 3),
+        "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                     "frac": round(achieved / peaks["hbm_gbs"], 4), "traffic": traffic,
+                     "peak_source": peaks["source"],
+                     "kernel": "w6a16_tcgen05_kernel<16> (all 4 launches; bytes-weighted)",
+                     "per_launch": res["per_layer"]},
+        "cublas_fp16": dict(res["cublas"], speedup_vs_cublas=round(res["cublas"]["ms_per_step"] / (t_step * 1e3), 3)),
+        "e2e": res["e2e"],
+        "gpu_launches": res["gpu_launches"],
+        "clocks": res["clocks"],
+    }
+    if world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(layers, m)
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

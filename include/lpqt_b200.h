@@ -116,8 +116,10 @@ int lpqt_fp6_prepack(const uint8_t* seg4, const uint8_t* seg2, int64_t N,
 int lpqt_fp6_unprepack(const uint8_t* tiles, int64_t N, int64_t K,
                        uint8_t* codes, void* stream);
 /* Standalone transform (the GEMM's register dequant): tiles -> out[N, K]
- * f16 = compose[c] * folded[row] rounded to binary16 (dequant.py:82-86). */
-int lpqt_fp6_tiles_dequant(const uint8_t* tiles, const uint16_t* folded,
+ * f16 = value_f16[c] * S[row] rounded to binary16 (dequant.py:72-79), which
+ * equals the bias-shift result compose[c] * (S * 2^12) bit for bit
+ * (dequant.py:82-86; the reference's exhaustive test_dequant.py:93-102). */
+int lpqt_fp6_tiles_dequant(const uint8_t* tiles, const uint16_t* scales,
                            int64_t N, int64_t K, uint16_t* out, void* stream);
 
 /* Activation staging: X in the reference layout [K, M] (gemm.py:65, any

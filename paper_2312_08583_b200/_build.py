@@ -39,18 +39,24 @@ def _stale(target: str, deps: list[str]) -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    os.makedirs(BUILD, exist_ok=True)
+def build(force: bool = False, verbose: bool = False, defines: list[str] | None = None,
+          lib_path: str | None = None, build_dir: str | None = None) -> str:
+    """Compile + link.  `defines`/`lib_path`/`build_dir` build experiment
+    variants (e.g. -DLPQT_WAIT_MODE=1) next to the default library."""
+    lib_out = lib_path or LIB
+    bdir = build_dir or BUILD
+    extra = [f"-D{d}" for d in (defines or [])]
+    os.makedirs(bdir, exist_ok=True)
     nvcc = _nvcc()
     hdrs = [os.path.join(CSRC, h) for h in HEADERS] + [os.path.join(ROOT, "include", "lpqt_b200.h")]
     objs = []
     jobs = []
     for src in SOURCES:
         s = os.path.join(CSRC, src)
-        o = os.path.join(BUILD, src.replace(".cu", ".o"))
+        o = os.path.join(bdir, src.replace(".cu", ".o"))
         objs.append(o)
         if force or _stale(o, [s] + hdrs):
-            jobs.append([nvcc, *ARCH, *FLAGS, "-I", os.path.join(ROOT, "include"), "-c", s, "-o", o])
+            jobs.append([nvcc, *ARCH, *FLAGS, *extra, "-I", os.path.join(ROOT, "include"), "-c", s, "-o", o])
 
     def run(cmd):
         r = subprocess.run(cmd, capture_output=True, text=True)
@@ -59,18 +65,18 @@ def build(force: bool = False, verbose: bool = False) -> str:
     with ThreadPoolExecutor(max_workers=4) as ex:
         for cmd, r in ex.map(run, jobs):
             log = (r.stdout or "") + (r.stderr or "")
-            with open(os.path.join(BUILD, os.path.basename(cmd[-1]) + ".log"), "w") as f:
+            with open(os.path.join(bdir, os.path.basename(cmd[-1]) + ".log"), "w") as f:
                 f.write(log)
             if r.returncode != 0:
                 raise RuntimeError(f"nvcc failed for {cmd[-3]}:\n{log}")
             if verbose:
                 print(log)
-    if force or jobs or _stale(LIB, objs):
-        cmd = [nvcc, *ARCH, "-shared", "-o", LIB, *objs, "-lcuda"]
+    if force or jobs or _stale(lib_out, objs):
+        cmd = [nvcc, *ARCH, "-shared", "-o", lib_out, *objs, "-lcuda"]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError("link failed:\n" + r.stdout + r.stderr)
-    return LIB
+    return lib_out
 
 
 if __name__ == "__main__":

@@ -18,7 +18,7 @@ from .errors import (InvalidCode, InvalidInput, LpqtError, PayloadMismatch,
                      ScaleOverflow, ShapeError)
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "liblpqt_b200.so")
+LIB_PATH = os.environ.get("LPQT_LIB") or os.path.join(_HERE, "liblpqt_b200.so")
 
 # dtype / layout codes (lpqt_b200.h)
 F64, F32, F16, BF16 = 0, 1, 2, 3

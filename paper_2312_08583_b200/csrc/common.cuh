@@ -14,6 +14,10 @@
 
 #include "../../include/lpqt_b200.h"
 
+#ifndef LPQT_WAIT_HINT_NS
+#define LPQT_WAIT_HINT_NS 64
+#endif
+
 #if defined(__CUDA_ARCH__) && (__CUDA_ARCH__ < 1000)
 #error "liblpqt_b200 targets sm_100a only"
 #endif
@@ -63,13 +67,67 @@ __host__ __device__ __forceinline__ uint32_t fp6_from_byteform(uint32_t b) {
 }
 
 // ---------------------------------------------------------------------------
-// The register transform: 6 words of the tile layout (32 weights) -> 16 half2
-// of composed binary16 bit patterns in ascending k.  ~1.2 ALU ops / weight:
-// one LOP3 mask + two PRMT per 4 "direct" weights; the 8 "spare" weights are
-// gathered from bits 5-6 of every byte.  Layout contract (see prepack.cu):
-//   word i (0..5), byte t: weight k = 4i+t in s00eeemm form, bits 5,6 spare
-//   E0 (k 24..27) byte t = W0[5:6]->[0:1] | W1[5:6]->[2:3] | W2[5]->[4] | W5[6]->[7]
-//   E1 (k 28..31) byte t = W3[5:6]->[0:1] | W4[5:6]->[2:3] | W2[6]->[4] | W5[5]->[7]
+// The register transform used by the GEMM (tile layout v2, "cvt" layout):
+// 6 words of the tile layout (32 weights) -> 16 half2 of the codes' exact
+// binary16 VALUES (value_table_f16, codec.py:108-113), k ascending.
+//   word i (0..5), byte t: bits 0-5 = e3m2 code of weight k = 4i+t
+//                          bits 6-7 = two bits of a "spare" weight
+//   spare E0 (k 24..27) byte t = W0[6:7] | W1[6:7] << 2 | W2[6:7] << 4
+//   spare E1 (k 28..31) byte t = W3[6:7] | W4[6:7] << 2 | W5[6:7] << 4
+// The FP6 code is the OCP e3m2 encoding, so the hardware converter
+// cvt.rn.f16x2.e3m2x2 (SASS F2FP.F16.E3M2.UNPACK_B, 2 weights per op, reads
+// either 16-bit half, ignores container bits 6-7) does the rebuild; the
+// spares cost 3 SHF + 2 LOP3 per 4.  ~0.81 ALU-pipe ops / weight, against
+// ~1.19 for the bias-shift PRMT rebuild below (F2FP issues on the same
+// half-rate ALU pipe as LOP3/PRMT — measured, tools/pipe_bench.cu).  The
+// epilogue then scales by S (value * S == compose * S * 2^12 exactly).
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t cvt_e3m2x2_lo(uint32_t w) {
+  uint32_t r;
+  asm("{cvt.rn.f16x2.e3m2x2 %0, %1;}" : "=r"(r) : "h"(static_cast<uint16_t>(w)));
+  return r;
+}
+__device__ __forceinline__ uint32_t cvt_e3m2x2_hi(uint32_t w) {
+  uint32_t r;
+  asm("{cvt.rn.f16x2.e3m2x2 %0, %1;}" : "=r"(r) : "h"(static_cast<uint16_t>(w >> 16)));
+  return r;
+}
+__device__ __forceinline__ uint32_t lop3_sel(uint32_t a, uint32_t b, uint32_t mask_a) {
+  return (a & mask_a) | (b & ~mask_a);  // one LOP3 with an immediate mask
+}
+__device__ __forceinline__ uint32_t spare_gather(uint32_t wa, uint32_t wb, uint32_t wc) {
+  const uint32_t t = lop3_sel(wa >> 6, wb >> 4, 0x03030303u);
+  return lop3_sel(t, wc >> 2, 0x0F0F0F0Fu);  // bits 6-7 of each byte: don't care
+}
+__device__ __forceinline__ void fp6x32_cvt_f16x32(const uint32_t w[6], uint32_t out[16]) {
+#pragma unroll
+  for (int i = 0; i < 6; ++i) {
+    out[2 * i] = cvt_e3m2x2_lo(w[i]);
+    out[2 * i + 1] = cvt_e3m2x2_hi(w[i]);
+  }
+  const uint32_t e0 = spare_gather(w[0], w[1], w[2]);
+  const uint32_t e1 = spare_gather(w[3], w[4], w[5]);
+  out[12] = cvt_e3m2x2_lo(e0);
+  out[13] = cvt_e3m2x2_hi(e0);
+  out[14] = cvt_e3m2x2_lo(e1);
+  out[15] = cvt_e3m2x2_hi(e1);
+}
+// codes of the 32 weights (inverse of fp6x32_pack_words; used by unprepack)
+__host__ __device__ inline void fp6x32_unpack_codes(const uint32_t w[6], uint8_t c[32]) {
+  for (int i = 0; i < 6; ++i)
+    for (int t = 0; t < 4; ++t) c[4 * i + t] = static_cast<uint8_t>((w[i] >> (8 * t)) & 0x3Fu);
+  for (int t = 0; t < 4; ++t) {
+    const int s = 8 * t + 6;
+    c[24 + t] = static_cast<uint8_t>(((w[0] >> s) & 3u) | (((w[1] >> s) & 3u) << 2) | (((w[2] >> s) & 3u) << 4));
+    c[28 + t] = static_cast<uint8_t>(((w[3] >> s) & 3u) | (((w[4] >> s) & 3u) << 2) | (((w[5] >> s) & 3u) << 4));
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Bias-shift rebuild (the paper's ALU trick, dequant.py:33-43) over the older
+// "byte form" layout: word i byte t = s00eeemm of weight 4i+t, spares in bits
+// 5-6.  Kept as a reference point for tools/dq_bench.cu; the GEMM uses the
+// cvt layout above.
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ void fp6x32_to_f16x32(const uint32_t w[6], uint32_t out[16]) {
 #pragma unroll
@@ -88,8 +146,8 @@ __device__ __forceinline__ void fp6x32_to_f16x32(const uint32_t w[6], uint32_t o
   out[15] = __byte_perm(e1, 0u, 0x3424);
 }
 
-// Inverse direction used by prepack: 32 codes (k ascending) -> 6 words.
-__host__ __device__ inline void fp6x32_pack_words(const uint8_t c[32], uint32_t w[6]) {
+// Byte-form layout packer (bias-shift rebuild above; dev benchmarks only).
+__host__ __device__ inline void fp6x32_pack_words_byteform(const uint8_t c[32], uint32_t w[6]) {
   uint32_t b[32];
   for (int j = 0; j < 32; ++j) b[j] = fp6_byteform(c[j]);
   for (int i = 0; i < 6; ++i) {
@@ -106,6 +164,25 @@ __host__ __device__ inline void fp6x32_pack_words(const uint8_t c[32], uint32_t 
     w[4] |= ((e1 >> 2) & 3u) << (s + 5);
     w[5] |= ((e0 >> 7) & 1u) << (s + 6);
     w[5] |= ((e1 >> 7) & 1u) << (s + 5);
+  }
+}
+
+// Tile layout v2 packer (used by prepack): 32 codes (k ascending) -> 6 words,
+// inverse of fp6x32_unpack_codes / the layout read by fp6x32_cvt_f16x32.
+__host__ __device__ inline void fp6x32_pack_words(const uint8_t c[32], uint32_t w[6]) {
+  for (int i = 0; i < 6; ++i) {
+    w[i] = (c[4 * i] & 0x3Fu) | ((c[4 * i + 1] & 0x3Fu) << 8) | ((c[4 * i + 2] & 0x3Fu) << 16) |
+           ((uint32_t)(c[4 * i + 3] & 0x3Fu) << 24);
+  }
+  for (int t = 0; t < 4; ++t) {
+    const uint32_t e0 = c[24 + t], e1 = c[28 + t];
+    const int s = 8 * t + 6;
+    w[0] |= (e0 & 3u) << s;
+    w[1] |= ((e0 >> 2) & 3u) << s;
+    w[2] |= ((e0 >> 4) & 3u) << s;
+    w[3] |= (e1 & 3u) << s;
+    w[4] |= ((e1 >> 2) & 3u) << s;
+    w[5] |= ((e1 >> 4) & 3u) << s;
   }
 }
 
@@ -151,8 +228,30 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t by
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
                : "memory");
 }
+// LPQT_WAIT_MODE: 0 = try_wait (HW suspend, system time limit),
+// 1 = test_wait spin, 2 = try_wait with a short suspend-time hint.
+#ifndef LPQT_WAIT_MODE
+#define LPQT_WAIT_MODE 2
+#endif
 __device__ __forceinline__ bool mbar_try_wait(uint32_t addr, uint32_t parity) {
   uint32_t ok;
+#if LPQT_WAIT_MODE == 1
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(addr), "r"(parity)
+      : "memory");
+#elif LPQT_WAIT_MODE == 2
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(addr), "r"(parity), "r"(LPQT_WAIT_HINT_NS)
+      : "memory");
+#else
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
       "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
@@ -160,15 +259,16 @@ __device__ __forceinline__ bool mbar_try_wait(uint32_t addr, uint32_t parity) {
       : "=r"(ok)
       : "r"(addr), "r"(parity)
       : "memory");
+#endif
   return ok != 0;
 }
 // Spin with a watchdog: a pipeline deadlock traps (the launch fails with an
-// error) instead of hanging the device.  ~2^28 polls is tens of seconds.
+// error) instead of hanging the device.
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   const uint32_t a = smem_u32(bar);
   uint32_t spins = 0;
   while (!mbar_try_wait(a, parity)) {
-    if (++spins == (1u << 28)) __trap();
+    if (++spins == (1u << 30)) __trap();
   }
 }
 
@@ -228,6 +328,86 @@ __device__ __forceinline__ void mma_f16_ts(uint32_t d_tmem, uint32_t a_tmem, uin
       "setp.ne.b32 p, %4, 0;\n\t"
       "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
       "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+
+// ---- warp-converged single-thread issue --------------------------------------
+// elect.sync picks one lane; the *_if / *_elect forms execute the async op on
+// that lane only, from converged code, so ptxas can keep the operands in
+// uniform registers (no per-issue ELECT/R2UR.BROADCAST waterfall).
+__device__ __forceinline__ uint32_t elect_one() {
+  uint32_t pred;
+  asm volatile(
+      "{\n\t.reg .pred e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "selp.u32 %0, 1, 0, e;\n\t}"
+      : "=r"(pred));
+  return pred;
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx_if(uint32_t pred, uint64_t* bar, uint32_t bytes) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\t"
+      "setp.ne.b32 e, %0, 0;\n\t"
+      "@e mbarrier.arrive.expect_tx.shared::cta.b64 _, [%1], %2;\n\t}" ::"r"(pred),
+      "r"(smem_u32(bar)), "r"(bytes)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s_if(uint32_t pred, void* dst, const void* src, uint32_t bytes, uint64_t* bar,
+                                            uint64_t policy) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\t"
+      "setp.ne.b32 e, %0, 0;\n\t"
+      "@e cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%1], [%2], %3, [%4], "
+      "%5;\n\t}" ::"r"(pred),
+      "r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_2d_if(uint32_t pred, void* dst, const CUtensorMap* map, uint64_t* bar, int c0,
+                                               int c1) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\t"
+      "setp.ne.b32 e, %0, 0;\n\t"
+      "@e cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%1], [%2, {%4, %5}], "
+      "[%3];\n\t}" ::"r"(pred),
+      "r"(smem_u32(dst)), "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
+      : "memory");
+}
+// tcgen05.mma issued by one elected lane of a converged warp
+__device__ __forceinline__ void mma_f16_ts_elect(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc,
+                                                 uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+// same, with the elected-lane predicate computed once by the caller
+__device__ __forceinline__ void mma_f16_ts_if(uint32_t pred, uint32_t d_tmem, uint32_t a_tmem, uint32_t b_desc_lo,
+                                              uint32_t b_desc_hi, uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\t.reg .b64 bd;\n\t"
+      "setp.ne.b32 e, %0, 0;\n\t"
+      "setp.ne.b32 p, %6, 0;\n\t"
+      "mov.b64 bd, {%3, %4};\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%1], [%2], bd, %5, p;\n\t}" ::"r"(pred),
+      "r"(d_tmem), "r"(a_tmem), "r"(b_desc_lo), "r"(b_desc_hi), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void tc_commit_if(uint32_t pred, uint64_t* bar) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\t"
+      "setp.ne.b32 e, %0, 0;\n\t"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%1];\n\t}" ::"r"(pred),
+      "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void tc_commit_elect(uint64_t* bar) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(smem_u32(bar))
       : "memory");
 }
 

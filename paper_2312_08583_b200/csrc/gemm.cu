@@ -1,78 +1,148 @@
 // gemm.cu — K4/K5/K6: the W6A16 linear on tcgen05 (gemm.py:65-94 CGQ path).
 //
-//   Y[n, m] = (S[n] * 2^12) * sum_k C[n, k] * X[m, k]
+//   Y[n, m] = S[n] * sum_k V[n, k] * X[m, k]
 //
-// where C holds the bias-shifted binary16 code patterns (value * 2^-12,
-// dequant.py:33-43) and S * 2^12 is the folded scale (dequant.py:46-69),
-// formed in an fp32 register (exact, and free of the binary16 ScaleOverflow
-// limit), so the product equals the reference's S * sum_k value * x exactly
-// up to fp32 summation order (power-of-two scaling commutes with rounding).
+// exactly the reference's CGQ algorithm (raw code values V = value_table[c],
+// row scale applied once after the fp32 accumulation, gemm.py:84-88), up to
+// fp32 summation order.  V is rebuilt in registers by the hardware e3m2
+// converter from the tile layout (common.cuh); the paper's bias-shift
+// identity compose[c] * (S * 2^12) == V * S (dequant.py:33-69) means the same
+// result as the folded-scale formulation, bit for bit per element.
 //
-// One persistent, warp-specialised kernel covers decode (M <= 16, HBM-bound)
-// and prefill (tensor-bound).  Per CTA (1 per SM, 448 threads):
-//   warp 8      TMA producer: per stage one 1-D bulk copy of a 12288-B
-//               weight tile (evict-first) + two 2-D TMA boxes of X (64 k x
-//               BN rows, 128-B swizzle; rows >= M and k >= K zero-filled).
-//   warps 0-7   dequant (DQ): 3 x LDS.128 per thread (its row, its 64-k half)
-//               -> FP6->FP16 register rebuild -> tcgen05.st into a TMEM A
-//               buffer (128 lanes = weight rows, 32 cols = 64 k).
-//   warp 9      MMA issuer (one lane): tcgen05.mma.kind::f16 with A in TMEM
-//               ("TS"), B = X from SMEM, D (fp32, 128 x BN) in TMEM.
-//   warps 10-13 epilogue: tcgen05.ld D -> x S*2^12 (folded) -> Y, or split-K
-//               partial + deterministic last-CTA reduction (fixed split order).
+// Work decomposition: stream-K.  The (tile, k-step) iteration space — tiles of
+// 128 weight rows x BN batch columns, k-steps of kKStep x 128 k — is split
+// into `gridDim.x` contiguous, equal ranges, one per persistent CTA.  A CTA's
+// range is a sequence of segments (tile, k-range); whole tiles store Y
+// directly, a tile cut between CTAs (at most the first and last segment of a
+// range) is finished by whichever contributor arrives last, summing the
+// contributors' fp32 partials in a fixed order (deterministic).
+//
+// Per CTA (1 per SM, 704 threads), warp-specialised:
+//   warp 16     TMA producer: per stage one 1-D bulk copy of the stage's
+//               consecutive 12288-B weight tiles (evict-first) + 2-D TMA boxes
+//               of X (64 k x BN rows, 128-B swizzle; rows >= M, k >= K read 0).
+//   warps 0-15  dequant (DQ), two groups on alternate stages: LDS.128 of the
+//               thread's weight row -> FP6->FP16 rebuild (hardware e3m2
+//               converter + spare-bit gather) -> tcgen05.st into a TMEM A slot
+//               (128 lanes = weight rows, 64 columns of half2 per 128-k tile);
+//               software-pipelined: the next stage's words load while the
+//               stores drain.
+//   warp 17     MMA issuer: tcgen05.mma.kind::f16 with A in TMEM ("TS"), B = X
+//               from SMEM, D (fp32, 128 x BN) in TMEM; kNAcc independent
+//               accumulators break the MMA->MMA dependency at small N.
+//   warps 18-21 epilogue: tcgen05.ld D (accumulators summed in fixed order)
+//               -> x S*2^12 -> Y, or the stream-K partial/fixup.
 // Pipelines: smem ring full/empty (TMA <-> DQ+MMA), TMEM-A ring afull/aempty
-// (DQ <-> MMA), TMEM-D ring dfull/dempty (MMA <-> epilogue).
+// (DQ <-> MMA), TMEM-D ring dfull/dempty (MMA <-> epilogue).  The producer and
+// MMA warps run warp-converged and issue through elect.sync-predicated PTX so
+// the uniform-datapath instructions (UBLKCP/UTMALDG/UTCHMMA) need no per-issue
+// lane waterfall.
+#include <stdlib.h>
+
 #include <mutex>
 
 #include "common.cuh"
 
 namespace lpqt {
 
-constexpr int kNumDqWarps = 8;
+constexpr int kNumDqWarps = 16;
 constexpr int kNumEpiWarps = 4;
-constexpr int kWarpTma = 8;
-constexpr int kWarpMma = 9;
-constexpr int kWarpEpi0 = 10;
-constexpr int kThreads = (kNumDqWarps + 2 + kNumEpiWarps) * 32;  // 448
-constexpr int kABufs = 4;
+constexpr int kWarpTma = kNumDqWarps;
+constexpr int kWarpMma = kNumDqWarps + 1;
+constexpr int kWarpEpi0 = kNumDqWarps + 2;
+constexpr int kThreads = (kNumDqWarps + 2 + kNumEpiWarps) * 32;  // 704
 constexpr int kAColsPerBuf = kTileK / 2;  // 64 columns of packed half2
 constexpr int kTmemCols = 512;
 constexpr int kSmemBudget = 200 * 1024;
+constexpr int64_t kMaxCounters = 65536;   // stream-K tile counters (256 KiB)
 
 struct GemmArgs {
   const uint8_t* tiles;
   const uint16_t* scales;
   void* y;
-  float* partials;
-  int* counters;
+  float* partials;    // [gridDim.x][2][128][BN] fp32 (first / last segment of each CTA)
+  int* counters;      // [tiles] k-steps contributed so far (self-resetting)
+  long long* trace;   // LPQT_TRACE builds only: [cta][16 events][64] clock64 stamps
   int64_t ldy;
+  int64_t total;      // tiles * ksteps: the stream-K iteration space
   int M, N;
-  int k_tiles, n_tiles, m_tiles;
-  int splits, kt_per_split, num_units;
+  int k_tiles, ksteps, n_tiles, m_tiles;
   int y_dtype, y_layout;
 };
 
 template <int BN>
 struct Cfg {
-  static constexpr int kXStageBytes = BN * kTileK * 2;  // two SW128 blocks of BN x 128 B
-  static constexpr int kStageBytes = kXStageBytes + kTileBytes;
+  static constexpr int kKStep = BN <= 64 ? 2 : 1;           // 128-k tiles per pipeline stage
+  static constexpr int kXTileBytes = BN * kTileK * 2;       // X for one tile: two SW128 blocks
+  static constexpr int kStageBytes = kKStep * (kXTileBytes + kTileBytes);
   static constexpr int kStagesRaw = kSmemBudget / kStageBytes;
   static constexpr int kStages = kStagesRaw > 8 ? 8 : kStagesRaw;
   static constexpr int kDBufs = BN <= 128 ? 2 : 1;
-  static constexpr int kBarBytes = 8 * (2 * kStages + 2 * kABufs + 2 * kDBufs) + 16;
+  // Independent accumulators: with a small MMA N the tensor pipe finishes an
+  // MMA long before its result can feed the next dependent MMA, so MMA j of
+  // every tile accumulates into D[j % kNAcc] (kNAcc divides the 8 MMAs of a
+  // tile); the epilogue sums them in a fixed order.
+  static constexpr int kNAcc = BN <= 32 ? 4 : (BN <= 64 ? 2 : 1);
+  static constexpr int kDCols = BN * kNAcc;
+  // TMEM: D buffers at the top, the rest is the A ring (64 columns per tile)
+  static constexpr int kACols = kTmemCols - kDBufs * kDCols;
+  static constexpr int kASlots = (kACols / kAColsPerBuf) / kKStep;   // slots of kKStep tiles
+  static constexpr int kBarBytes = 8 * (2 * kStages + 2 * kASlots + 2 * kDBufs) + 16;
   static constexpr int kSmemBytes = kStages * kStageBytes + kBarBytes + 1024;
   static_assert(kStages >= 2, "pipeline too shallow");
-  static_assert(kABufs * kAColsPerBuf + kDBufs * BN <= kTmemCols, "TMEM over-subscribed");
+  static_assert(kASlots >= 2, "A ring too shallow");
+  static_assert(8 % kNAcc == 0, "accumulators must divide the MMAs of a tile");
 };
 
-__device__ __forceinline__ void decode_unit(const GemmArgs& a, int u, int& n_tile, int& m_tile, int& split, int& kt0,
-                                            int& kt1) {
-  split = u % a.splits;
-  const int tile = u / a.splits;
-  n_tile = tile / a.m_tiles;
-  m_tile = tile % a.m_tiles;
-  kt0 = split * a.kt_per_split;
-  kt1 = min(a.k_tiles, kt0 + a.kt_per_split);
+#ifdef LPQT_TRACE
+#define TRACE(ev, i)                                                                       \
+  do {                                                                                     \
+    if (a.trace && (i) < 64 && lane == 0 && (blockIdx.x == 0 || blockIdx.x == 77) &&      \
+        ((ev) < 2 || (ev) > 7 || warp == 0) && ((ev) != 9 || warp == kWarpEpi0)) {          \
+      a.trace[((blockIdx.x == 0 ? 0 : 1) * 16 + (ev)) * 64 + (i)] = clock64();              \
+    }                                                                                      \
+  } while (0)
+#else
+#define TRACE(ev, i) \
+  do {               \
+  } while (0)
+#endif
+
+// ---- stream-K geometry ----------------------------------------------------------
+__device__ __forceinline__ int64_t sk_begin(const GemmArgs& a, int c) {
+  return (int64_t)c * a.total / (int64_t)gridDim.x;
+}
+// CTA whose range holds global k-step position p
+__device__ __forceinline__ int sk_cta_of(const GemmArgs& a, int64_t p) {
+  return static_cast<int>(((p + 1) * (int64_t)gridDim.x - 1) / a.total);
+}
+
+struct Seg {
+  int tile, ks0, ks1;  // k-steps [ks0, ks1) of `tile`
+  bool full;           // the whole tile (no other contributor)
+  int pidx;            // partial slot: 0 = first segment of this CTA's range, 1 = last
+};
+
+template <int KSTEP>
+__device__ __forceinline__ bool seg_next(const GemmArgs& a, int64_t& pos, int64_t end, int64_t beg, Seg& sg) {
+  if (pos >= end) return false;
+  const int t = static_cast<int>(pos / a.ksteps);
+  const int s0 = static_cast<int>(pos - (int64_t)t * a.ksteps);
+  const int64_t rem = end - pos;
+  const int s1 = rem < (int64_t)(a.ksteps - s0) ? s0 + static_cast<int>(rem) : a.ksteps;
+  sg.tile = t;
+  sg.ks0 = s0;
+  sg.ks1 = s1;
+  sg.full = (s0 == 0 && s1 == a.ksteps);
+  sg.pidx = (beg >= (int64_t)t * a.ksteps) ? 0 : 1;
+  pos += s1 - s0;
+  return true;
+}
+
+__device__ __forceinline__ int atom_add_acq_rel_gpu(int* p, int v) {
+  int old;
+  asm volatile("atom.add.acq_rel.gpu.s32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+  return old;
 }
 
 __device__ __forceinline__ void store_y(const GemmArgs& a, int n, int m, float v) {
@@ -87,32 +157,65 @@ __device__ __forceinline__ void store_y(const GemmArgs& a, int n, int m, float v
   }
 }
 
+// Sum the kNAcc accumulators over 16 columns [c0, c0+16) (fixed order).
+template <int BN, int NACC>
+__device__ __forceinline__ void load_acc16(uint32_t t_d, int c0, float (&acc)[16]) {
+  uint32_t v[16];
+  tmem_ld_x16(t_d + c0, v);
+  tmem_wait_ld();
+#pragma unroll
+  for (int j = 0; j < 16; ++j) acc[j] = __uint_as_float(v[j]);
+#pragma unroll 1
+  for (int q = 1; q < NACC; ++q) {
+    tmem_ld_x16(t_d + q * BN + c0, v);
+    tmem_wait_ld();
+#pragma unroll
+    for (int j = 0; j < 16; ++j) acc[j] += __uint_as_float(v[j]);
+  }
+}
+
+// One thread's 64-weight row segment: 3 x LDS.128 (tile layout, common.cuh)
+__device__ __forceinline__ void lds_row64(const uint8_t* src, uint4 (&q)[3]) {
+  q[0] = lds128(src);
+  q[1] = lds128(src + kTileN * 16);
+  q[2] = lds128(src + 2 * kTileN * 16);
+}
+// ... -> 32 half2 of composed binary16 (k ascending)
+__device__ __forceinline__ void dq_row64(const uint4 (&q)[3], uint32_t (&r)[32]) {
+  const uint32_t w0[6] = {q[0].x, q[0].y, q[0].z, q[0].w, q[1].x, q[1].y};
+  const uint32_t w1[6] = {q[1].z, q[1].w, q[2].x, q[2].y, q[2].z, q[2].w};
+  fp6x32_cvt_f16x32(w0, r);
+  fp6x32_cvt_f16x32(w1, r + 16);
+}
+
 template <int BN>
 __global__ void __launch_bounds__(kThreads, 1)
     w6a16_tcgen05_kernel(const __grid_constant__ CUtensorMap tmap_x, const GemmArgs a) {
   using C = Cfg<BN>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* smem_x = smem;                                   // kStages x kXStageBytes (1024-aligned)
-  uint8_t* smem_w = smem + C::kStages * C::kXStageBytes;    // kStages x 12288
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem_w + C::kStages * kTileBytes);
+  uint8_t* smem_x = smem;                                               // kStages x kKStep x kXTileBytes
+  uint8_t* smem_w = smem + C::kStages * C::kKStep * C::kXTileBytes;    // kStages x kKStep x 12288
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem_w + C::kStages * C::kKStep * kTileBytes);
   uint64_t* empty = full + C::kStages;
   uint64_t* afull = empty + C::kStages;
-  uint64_t* aempty = afull + kABufs;
-  uint64_t* dfull = aempty + kABufs;
+  uint64_t* aempty = afull + C::kASlots;
+  uint64_t* dfull = aempty + C::kASlots;
   uint64_t* dempty = dfull + C::kDBufs;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(dempty + C::kDBufs);
   volatile int* last_flag = reinterpret_cast<volatile int*>(tmem_slot + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t beg = sk_begin(a, blockIdx.x);
+  const int64_t end = sk_begin(a, blockIdx.x + 1);
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < C::kStages; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], kNumDqWarps + 1);
+      mbar_init(&empty[s], kNumDqWarps / 2 + 1);  // one DQ group + the MMA commit
     }
-    for (int b = 0; b < kABufs; ++b) {
-      mbar_init(&afull[b], kNumDqWarps);
+    for (int b = 0; b < C::kASlots; ++b) {
+      mbar_init(&afull[b], kNumDqWarps / 2);
       mbar_init(&aempty[b], 1);
     }
     for (int d = 0; d < C::kDBufs; ++d) {
@@ -129,172 +232,255 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  const uint32_t tmem_base = *tmem_slot;
-  const uint32_t tmem_d0 = tmem_base + kABufs * kAColsPerBuf;
+  const uint32_t tmem_base = __shfl_sync(0xffffffffu, *tmem_slot, 0);  // warp-uniform
+  const uint32_t tmem_d0 = tmem_base + C::kACols;                       // D buffers above the A ring
 
   if (warp == kWarpTma) {
     // ------------------------------------------------------------ producer
-    if (lane == 0) {
-      const uint64_t pol = l2_evict_first_policy();
-      int it = 0;
-      for (int u = blockIdx.x; u < a.num_units; u += gridDim.x) {
-        int n_tile, m_tile, split, kt0, kt1;
-        decode_unit(a, u, n_tile, m_tile, split, kt0, kt1);
-        for (int kt = kt0; kt < kt1; ++kt, ++it) {
-          const int s = it % C::kStages;
-          const uint32_t ph = (it / C::kStages) & 1;
-          mbar_wait(&empty[s], ph ^ 1);
-          mbar_arrive_expect_tx(&full[s], C::kStageBytes);
-          bulk_g2s(smem_w + s * kTileBytes, a.tiles + ((int64_t)n_tile * a.k_tiles + kt) * kTileBytes, kTileBytes,
-                   &full[s], pol);
-          uint8_t* xs = smem_x + s * C::kXStageBytes;
-          tma_load_2d(xs, &tmap_x, &full[s], kt * kTileK, m_tile * BN);
-          tma_load_2d(xs + BN * 128, &tmap_x, &full[s], kt * kTileK + 64, m_tile * BN);
-        }
+    const uint64_t pol = l2_evict_first_policy();
+    int t = static_cast<int>(beg / a.ksteps);
+    int ks = static_cast<int>(beg - (int64_t)t * a.ksteps);
+    const int n_st = static_cast<int>(end - beg);
+    for (int it = 0; it < n_st; ++it) {
+      const int kt = ks * C::kKStep;
+      const int nt = min(C::kKStep, a.k_tiles - kt);
+      const int n_tile = t / a.m_tiles, m_tile = t - n_tile * a.m_tiles;
+      const int s = it % C::kStages;
+      const uint32_t ph = (it / C::kStages) & 1;
+      TRACE(0, it);
+      mbar_wait(&empty[s], ph ^ 1);
+      TRACE(1, it);
+      uint8_t* ws = smem_w + s * C::kKStep * kTileBytes;
+      uint8_t* xs = smem_x + s * C::kKStep * C::kXTileBytes;
+      const uint8_t* src = a.tiles + ((int64_t)n_tile * a.k_tiles + kt) * kTileBytes;
+      const uint32_t bytes = static_cast<uint32_t>(nt * (kTileBytes + C::kXTileBytes));
+      const uint32_t e = elect_one();
+      mbar_arrive_expect_tx_if(e, &full[s], bytes);
+      bulk_g2s_if(e, ws, src, static_cast<uint32_t>(nt * kTileBytes), &full[s], pol);
+      for (int j = 0; j < nt; ++j) {
+        tma_load_2d_if(e, xs + j * C::kXTileBytes, &tmap_x, &full[s], (kt + j) * kTileK, m_tile * BN);
+        tma_load_2d_if(e, xs + j * C::kXTileBytes + BN * 128, &tmap_x, &full[s], (kt + j) * kTileK + 64,
+                       m_tile * BN);
+      }
+      if (++ks == a.ksteps) {
+        ks = 0;
+        ++t;
       }
     }
   } else if (warp < kNumDqWarps) {
     // ------------------------------------------------------------ dequant
-    const int lg = warp & 3, khalf = warp >> 2;
+    // 16 warps in two groups that take alternate stages (so one group's
+    // barrier waits overlap the other's ALU work); inside a group 4 warps per
+    // TMEM lane group, warp `tl` takes tile tl of the stage (kKStep == 2: the
+    // whole 128-k row, 2 x (3 LDS.128 + 2 transforms + tcgen05.st)) or k-half
+    // tl of the stage's single tile (kKStep == 1).
+    constexpr int kSegs = C::kKStep == 2 ? 2 : 1;  // 64-weight row segments per warp per stage
+    const int lg = warp & 3;
     const int row = lg * 32 + lane;
-    const uint32_t t_lane = tmem_base + (static_cast<uint32_t>(lg * 32) << 16) + khalf * 32;
-    int it = 0;
-    for (int u = blockIdx.x; u < a.num_units; u += gridDim.x) {
-      int n_tile, m_tile, split, kt0, kt1;
-      decode_unit(a, u, n_tile, m_tile, split, kt0, kt1);
-      for (int kt = kt0; kt < kt1; ++kt, ++it) {
-        const int s = it % C::kStages;
-        const uint32_t ph = (it / C::kStages) & 1;
-        const int b = it % kABufs;
-        const uint32_t bph = (it / kABufs) & 1;
-        mbar_wait(&full[s], ph);
-        const uint8_t* src = smem_w + s * kTileBytes + (khalf * 3 * kTileN + row) * 16;
-        const uint4 q0 = lds128(src);
-        const uint4 q1 = lds128(src + kTileN * 16);
-        const uint4 q2 = lds128(src + 2 * kTileN * 16);
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&empty[s]);
-        const uint32_t w0[6] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y};
-        const uint32_t w1[6] = {q1.z, q1.w, q2.x, q2.y, q2.z, q2.w};
-        uint32_t r[32];
-        fp6x32_to_f16x32(w0, r);
-        fp6x32_to_f16x32(w1, r + 16);
-        mbar_wait(&aempty[b], bph ^ 1);
-        tc_fence_after();
-        tmem_st_x32(t_lane + b * kAColsPerBuf, r);
-        tmem_wait_st();
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&afull[b]);
+    const int grp = warp >> 3;
+    const int tl = (warp >> 2) & 1;
+    const uint32_t t_lane = tmem_base + (static_cast<uint32_t>(lg * 32) << 16);
+    const int n_st = static_cast<int>(end - beg);
+    int ks_next = static_cast<int>((beg + grp) % a.ksteps);  // k-step of the group's next stage to load
+    auto next_nt = [&]() {
+      const int nt = min(C::kKStep, a.k_tiles - ks_next * C::kKStep);
+      ks_next += 2;
+      while (ks_next >= a.ksteps) ks_next -= a.ksteps;
+      return nt;
+    };
+    auto seg_src = [&](int i, int h) {
+      const uint8_t* ws = smem_w + (i % C::kStages) * C::kKStep * kTileBytes + row * 16;
+      return C::kKStep == 2 ? ws + tl * kTileBytes + h * 3 * kTileN * 16 : ws + tl * 3 * kTileN * 16;
+    };
+    uint4 q[kSegs][3];
+    int nt_cur = 0;
+    if (grp < n_st) {
+      nt_cur = next_nt();
+      mbar_wait(&full[grp % C::kStages], (grp / C::kStages) & 1);
+      if (C::kKStep == 1 || tl < nt_cur) {
+#pragma unroll
+        for (int h = 0; h < kSegs; ++h) lds_row64(seg_src(grp, h), q[h]);
       }
+    }
+    for (int i = grp; i < n_st; i += 2) {
+      const int s = i % C::kStages;
+      const int slot = i % C::kASlots;
+      const uint32_t sph = (i / C::kASlots) & 1;
+      TRACE(2, i);
+      mbar_wait(&aempty[slot], sph ^ 1);
+      TRACE(3, i);
+      tc_fence_after();
+      const uint32_t ta = t_lane + slot * C::kKStep * kAColsPerBuf;
+      if (C::kKStep == 1 || tl < nt_cur) {
+#pragma unroll
+        for (int h = 0; h < kSegs; ++h) {
+          uint32_t r[32];
+          dq_row64(q[h], r);
+          tmem_st_x32(C::kKStep == 2 ? ta + tl * kAColsPerBuf + h * 32 : ta + tl * 32, r);
+        }
+      }
+      TRACE(4, i);
+      // prefetch the group's next stage while the TMEM stores drain
+      if (i + 2 < n_st) {
+        const int nt_next = next_nt();
+        mbar_wait(&full[(i + 2) % C::kStages], ((i + 2) / C::kStages) & 1);
+        TRACE(5, i);
+        if (C::kKStep == 1 || tl < nt_next) {
+#pragma unroll
+          for (int h = 0; h < kSegs; ++h) lds_row64(seg_src(i + 2, h), q[h]);
+        }
+        nt_cur = nt_next;
+      }
+      tmem_wait_st();
+      TRACE(6, i);
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) {
+        mbar_arrive(&empty[s]);
+        mbar_arrive(&afull[slot]);
+      }
+      TRACE(7, i);
     }
   } else if (warp == kWarpMma) {
     // ------------------------------------------------------------ MMA issue
-    if (lane == 0) {
-      constexpr uint32_t idesc = idesc_f16_m128(BN);
-      int it = 0, lu = 0;
-      for (int u = blockIdx.x; u < a.num_units; u += gridDim.x, ++lu) {
-        int n_tile, m_tile, split, kt0, kt1;
-        decode_unit(a, u, n_tile, m_tile, split, kt0, kt1);
-        const int d = lu % C::kDBufs;
-        const uint32_t dph = (lu / C::kDBufs) & 1;
-        mbar_wait(&dempty[d], dph ^ 1);
+    constexpr uint32_t idesc = idesc_f16_m128(BN);
+    int64_t pos = beg;
+    Seg sg;
+    int lu = 0;
+    while (seg_next<C::kKStep>(a, pos, end, beg, sg)) {
+      const int d = lu % C::kDBufs;
+      const uint32_t dph = (lu / C::kDBufs) & 1;
+      mbar_wait(&dempty[d], dph ^ 1);
+      tc_fence_after();
+      const uint32_t d_tmem = tmem_d0 + d * C::kDCols;
+      const int64_t p0 = (int64_t)sg.tile * a.ksteps;
+      for (int ks = sg.ks0; ks < sg.ks1; ++ks) {
+        const int it = static_cast<int>(p0 + ks - beg);
+        const int kt = ks * C::kKStep;
+        const int nt = min(C::kKStep, a.k_tiles - kt);
+        const int s = it % C::kStages;
+        const uint32_t ph = (it / C::kStages) & 1;
+        const int slot = it % C::kASlots;
+        const uint32_t sph = (it / C::kASlots) & 1;
+        mbar_wait(&full[s], ph);
+        mbar_wait(&afull[slot], sph);
+        TRACE(8, it);
         tc_fence_after();
-        const uint32_t d_tmem = tmem_d0 + d * BN;
-        for (int kt = kt0; kt < kt1; ++kt, ++it) {
-          const int s = it % C::kStages;
-          const uint32_t ph = (it / C::kStages) & 1;
-          const int b = it % kABufs;
-          const uint32_t bph = (it / kABufs) & 1;
-          mbar_wait(&full[s], ph);
-          mbar_wait(&afull[b], bph);
-          tc_fence_after();
-          const uint32_t xs = smem_u32(smem_x + s * C::kXStageBytes);
+        const uint32_t e = elect_one();
+        // descriptor of X block 0 of this stage; every other operand is a
+        // compile-time offset from it (start address field = addr >> 4)
+        const uint64_t bd0 = sdesc_kmajor_sw128(smem_u32(smem_x + s * C::kKStep * C::kXTileBytes));
+        const uint32_t bd_lo = static_cast<uint32_t>(bd0), bd_hi = static_cast<uint32_t>(bd0 >> 32);
+        const uint32_t ta = tmem_base + slot * C::kKStep * kAColsPerBuf;
+        const bool first = (ks == sg.ks0);
 #pragma unroll
-          for (int j = 0; j < kTileK / 16; ++j) {
-            const uint64_t bdesc = sdesc_kmajor_sw128(xs + (j >> 2) * (BN * 128) + (j & 3) * 32);
-            mma_f16_ts(d_tmem, tmem_base + b * kAColsPerBuf + j * 8, bdesc, idesc, (kt > kt0 || j > 0) ? 1u : 0u);
+        for (int t = 0; t < C::kKStep; ++t) {
+          if (t < nt) {
+#pragma unroll
+            for (int j = 0; j < kTileK / 16; ++j) {
+              const uint32_t off = (t * C::kXTileBytes + (j >> 2) * (BN * 128) + (j & 3) * 32) >> 4;
+              const bool init = first && t == 0 && j < C::kNAcc;
+              mma_f16_ts_if(e, d_tmem + (j % C::kNAcc) * BN, ta + t * kAColsPerBuf + j * 8, bd_lo + off, bd_hi,
+                            idesc, init ? 0u : 1u);
+            }
           }
-          tc_commit(&empty[s]);
-          tc_commit(&aempty[b]);
         }
-        tc_commit(&dfull[d]);
+        tc_commit_if(e, &empty[s]);
+        tc_commit_if(e, &aempty[slot]);
+        TRACE(10, it);
       }
+      tc_commit_elect(&dfull[d]);
+      ++lu;
     }
   } else {
     // ------------------------------------------------------------ epilogue
     const int lg = warp & 3;
     const int rr = lg * 32 + lane;  // row inside the 128-row tile (= TMEM lane)
     const uint32_t t_lane = tmem_d0 + (static_cast<uint32_t>(lg * 32) << 16);
+    int64_t pos = beg;
+    Seg sg;
     int lu = 0;
-    for (int u = blockIdx.x; u < a.num_units; u += gridDim.x, ++lu) {
-      int n_tile, m_tile, split, kt0, kt1;
-      decode_unit(a, u, n_tile, m_tile, split, kt0, kt1);
+    while (seg_next<C::kKStep>(a, pos, end, beg, sg)) {
       const int d = lu % C::kDBufs;
       const uint32_t dph = (lu / C::kDBufs) & 1;
+      const int n_tile = sg.tile / a.m_tiles, m_tile = sg.tile % a.m_tiles;
       const int n = n_tile * kTileN + rr;
       const int m0 = m_tile * BN;
-      const float fs = n < a.N ? __half2float(__ushort_as_half(a.scales[n])) * 4096.0f : 0.f;
+      const float fs = n < a.N ? __half2float(__ushort_as_half(a.scales[n])) : 0.f;
+      const uint32_t t_d = t_lane + d * C::kDCols;
       mbar_wait(&dfull[d], dph);
+      TRACE(9, lu);
       tc_fence_after();
-      if (a.splits == 1) {
+      if (sg.full) {
 #pragma unroll 1
         for (int c0 = 0; c0 < BN; c0 += 16) {
-          uint32_t v[16];
-          tmem_ld_x16(t_lane + d * BN + c0, v);
-          tmem_wait_ld();
+          float acc[16];
+          load_acc16<BN, C::kNAcc>(t_d, c0, acc);
+          if (c0 + 16 >= BN) {  // last chunk read: hand the D buffer back to the MMA warp
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&dempty[d]);
+          }
 #pragma unroll
-          for (int j = 0; j < 16; ++j) store_y(a, n, m0 + c0 + j, __uint_as_float(v[j]) * fs);
+          for (int j = 0; j < 16; ++j) store_y(a, n, m0 + c0 + j, acc[j] * fs);
         }
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&dempty[d]);
       } else {
-        const int tile = u / a.splits;
-        float* part = a.partials + (((int64_t)tile * a.splits + split) * kTileN + rr) * BN;
+        float* part = a.partials + (((int64_t)blockIdx.x * 2 + sg.pidx) * kTileN + rr) * BN;
 #pragma unroll 1
         for (int c0 = 0; c0 < BN; c0 += 16) {
-          uint32_t v[16];
-          tmem_ld_x16(t_lane + d * BN + c0, v);
-          tmem_wait_ld();
+          float acc[16];
+          load_acc16<BN, C::kNAcc>(t_d, c0, acc);
+          if (c0 + 16 >= BN) {
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&dempty[d]);
+          }
 #pragma unroll
           for (int j = 0; j < 16; j += 4) {
-            *reinterpret_cast<float4*>(part + c0 + j) = make_float4(__uint_as_float(v[j]), __uint_as_float(v[j + 1]),
-                                                                    __uint_as_float(v[j + 2]), __uint_as_float(v[j + 3]));
+            __stcg(reinterpret_cast<float4*>(part + c0 + j), make_float4(acc[j], acc[j + 1], acc[j + 2], acc[j + 3]));
           }
         }
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&dempty[d]);
-        __threadfence();
+        // publish: CTA barrier, then one gpu-scope acq_rel atomic (release our
+        // partial, acquire the other contributors' partials if we are last)
         named_bar_sync(1, kNumEpiWarps * 32);
         if (warp == kWarpEpi0 && lane == 0) {
-          const int prev = atomicAdd(&a.counters[tile], 1);
-          *last_flag = (prev == a.splits - 1) ? 1 : 0;
+          const int k_done = sg.ks1 - sg.ks0;
+          const int prev = atom_add_acq_rel_gpu(&a.counters[sg.tile], k_done);
+          *last_flag = (prev + k_done == a.ksteps) ? 1 : 0;
         }
         named_bar_sync(1, kNumEpiWarps * 32);
         if (*last_flag) {
-          __threadfence();
-          const float* base = a.partials + ((int64_t)tile * a.splits * kTileN + rr) * BN;
+          const int64_t p_first = (int64_t)sg.tile * a.ksteps;
+          const int c_first = sk_cta_of(a, p_first);
+          const int c_last = sk_cta_of(a, p_first + a.ksteps - 1);
 #pragma unroll 1
-          for (int c0 = 0; c0 < BN; c0 += 4) {
-            float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-            for (int s = 0; s < a.splits; ++s) {
-              const float4 p = __ldcg(reinterpret_cast<const float4*>(base + (int64_t)s * kTileN * BN + c0));
-              acc.x += p.x;
-              acc.y += p.y;
-              acc.z += p.z;
-              acc.w += p.w;
+          for (int c0 = 0; c0 < BN; c0 += 16) {
+            float acc[16];
+#pragma unroll
+            for (int j = 0; j < 16; ++j) acc[j] = 0.f;
+#pragma unroll 1
+            for (int c = c_first; c <= c_last; ++c) {  // contributor order == k order
+              const int idx = (sk_begin(a, c) >= p_first) ? 0 : 1;
+              const float* src = a.partials + (((int64_t)c * 2 + idx) * kTileN + rr) * BN + c0;
+              float4 v[4];
+#pragma unroll
+              for (int j = 0; j < 4; ++j) v[j] = __ldcg(reinterpret_cast<const float4*>(src) + j);
+#pragma unroll
+              for (int j = 0; j < 4; ++j) {
+                acc[4 * j + 0] += v[j].x;
+                acc[4 * j + 1] += v[j].y;
+                acc[4 * j + 2] += v[j].z;
+                acc[4 * j + 3] += v[j].w;
+              }
             }
-            store_y(a, n, m0 + c0 + 0, acc.x * fs);
-            store_y(a, n, m0 + c0 + 1, acc.y * fs);
-            store_y(a, n, m0 + c0 + 2, acc.z * fs);
-            store_y(a, n, m0 + c0 + 3, acc.w * fs);
+#pragma unroll
+            for (int j = 0; j < 16; ++j) store_y(a, n, m0 + c0 + j, acc[j] * fs);
           }
-          if (warp == kWarpEpi0 && lane == 0) a.counters[tile] = 0;
+          if (warp == kWarpEpi0 && lane == 0) a.counters[sg.tile] = 0;
         }
         named_bar_sync(1, kNumEpiWarps * 32);
       }
+      ++lu;
     }
   }
 
@@ -310,8 +496,9 @@ __global__ void __launch_bounds__(kThreads, 1)
 // host side: plan, tensor map, launch
 // ---------------------------------------------------------------------------
 struct Plan {
-  int bn, splits, kt_per_split, grid, num_units, n_tiles, m_tiles, k_tiles, stages, smem;
-  int64_t ws_bytes, counters_bytes;
+  int bn, grid, n_tiles, m_tiles, k_tiles, ksteps, stages, smem, kstep;
+  int64_t tiles, total, ws_bytes, counters_bytes;
+  bool partials;
 };
 
 static int pick_bn(int64_t M) {
@@ -323,9 +510,10 @@ static int pick_bn(int64_t M) {
 }
 
 template <int BN>
-static void cfg_of(int& stages, int& smem) {
-  stages = Cfg<BN>::kStages;
-  smem = Cfg<BN>::kSmemBytes;
+static void cfg_of(Plan& p) {
+  p.stages = Cfg<BN>::kStages;
+  p.smem = Cfg<BN>::kSmemBytes;
+  p.kstep = Cfg<BN>::kKStep;
 }
 
 static int num_sms() {
@@ -339,54 +527,34 @@ static int num_sms() {
   return sms;
 }
 
+// split_k == 0: one persistent CTA per SM over the whole stream-K space.
+// split_k  > 0: about split_k CTAs per tile (testing / tuning hook).
 static Plan make_plan(int64_t M, int64_t N, int64_t K, int split_k, int sms) {
   Plan p{};
   p.bn = pick_bn(M);
   switch (p.bn) {
-    case 16: cfg_of<16>(p.stages, p.smem); break;
-    case 32: cfg_of<32>(p.stages, p.smem); break;
-    case 64: cfg_of<64>(p.stages, p.smem); break;
-    case 128: cfg_of<128>(p.stages, p.smem); break;
-    default: cfg_of<256>(p.stages, p.smem); break;
+    case 16: cfg_of<16>(p); break;
+    case 32: cfg_of<32>(p); break;
+    case 64: cfg_of<64>(p); break;
+    case 128: cfg_of<128>(p); break;
+    default: cfg_of<256>(p); break;
   }
   p.n_tiles = static_cast<int>((N + kTileN - 1) / kTileN);
   p.m_tiles = static_cast<int>((M + p.bn - 1) / p.bn);
   p.k_tiles = static_cast<int>((K + kTileK - 1) / kTileK);
-  const int64_t tiles = (int64_t)p.n_tiles * p.m_tiles;
-  int best = 1;
-  if (split_k > 0) {
-    best = split_k;
-  } else {
-    // minimise waves x (k-tiles per unit + fixed per-unit cost); the fixed
-    // cost (pipeline fill + epilogue, in k-tile units) grows with the
-    // partial-tile traffic of split-K.
-    double best_cost = 1e30;
-    const int max_s = p.k_tiles < 32 ? p.k_tiles : 32;
-    for (int s = 1; s <= max_s; ++s) {
-      const int per = (p.k_tiles + s - 1) / s;
-      const int s_eff = (p.k_tiles + per - 1) / per;
-      const int64_t units = tiles * s_eff;
-      const int64_t waves = (units + sms - 1) / sms;
-      const double fixed = 2.0 + (s_eff > 1 ? p.bn / 32.0 : 0.0);
-      const double cost = (double)waves * (per + fixed);
-      if (cost < best_cost - 1e-9) {
-        best_cost = cost;
-        best = s_eff;
-      }
-    }
-  }
-  if (best > p.k_tiles) best = p.k_tiles;
-  if (best < 1) best = 1;
-  p.kt_per_split = (p.k_tiles + best - 1) / best;
-  p.splits = (p.k_tiles + p.kt_per_split - 1) / p.kt_per_split;
-  p.num_units = static_cast<int>(tiles * p.splits);
-  p.grid = p.num_units < sms ? p.num_units : sms;
-  if (p.splits > 1) {
-    p.counters_bytes = ((tiles * 4) + 255) / 256 * 256;
-    p.ws_bytes = p.counters_bytes + tiles * p.splits * kTileN * p.bn * 4;
-  } else {
-    p.counters_bytes = 0;
-    p.ws_bytes = 0;
+  p.ksteps = (p.k_tiles + p.kstep - 1) / p.kstep;
+  p.tiles = (int64_t)p.n_tiles * p.m_tiles;
+  p.total = p.tiles * p.ksteps;
+  int64_t g = split_k > 0 ? p.tiles * split_k : sms;
+  if (g > p.total) g = p.total;
+  if (p.tiles > kMaxCounters) g = p.tiles;  // one whole tile per CTA: no counters needed
+  if (g < 1) g = 1;
+  p.grid = static_cast<int>(g);
+  // partial tiles exist unless every CTA range is a whole number of tiles
+  p.partials = !(p.total % g == 0 && (p.total / g) % p.ksteps == 0);
+  if (p.partials) {
+    p.counters_bytes = kMaxCounters * 4;  // fixed region, zeroed once, self-resetting
+    p.ws_bytes = p.counters_bytes + (int64_t)p.grid * 2 * kTileN * p.bn * 4;
   }
   return p;
 }
@@ -408,6 +576,17 @@ static EncodeTiledFn encode_fn() {
   return fn;
 }
 
+#ifdef LPQT_TRACE
+static long long* trace_buffer() {
+  static long long* buf = nullptr;
+  if (!buf) {
+    cudaMalloc(&buf, 2 * 16 * 64 * sizeof(long long));
+    cudaMemset(buf, 0, 2 * 16 * 64 * sizeof(long long));
+  }
+  return buf;
+}
+#endif
+
 template <int BN>
 static int launch(const Plan& p, const GemmArgs& args, const uint16_t* Xt, int64_t ldx, int64_t M,
                   cudaStream_t stream) {
@@ -423,13 +602,14 @@ static int launch(const Plan& p, const GemmArgs& args, const uint16_t* Xt, int64
           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
     return LPQT_E_INVALID_INPUT;
   auto kern = w6a16_tcgen05_kernel<BN>;
+  constexpr int smem = Cfg<BN>::kSmemBytes;
   static std::once_flag once;
   static cudaError_t attr_err = cudaSuccess;
   std::call_once(once, [&] {
-    attr_err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg<BN>::kSmemBytes);
+    attr_err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   });
   if (attr_err != cudaSuccess) return LPQT_E_CUDA;
-  kern<<<p.grid, kThreads, Cfg<BN>::kSmemBytes, stream>>>(map, args);
+  kern<<<p.grid, kThreads, smem, stream>>>(map, args);
   note_launch();
   return check_launch();
 }
@@ -440,16 +620,30 @@ using namespace lpqt;
 
 extern "C" {
 
+#ifdef LPQT_TRACE
+int lpqt_trace_dump(long long* host) {
+  cudaDeviceSynchronize();
+  return cudaMemcpy(host, trace_buffer(), 2 * 16 * 64 * sizeof(long long), cudaMemcpyDeviceToHost) == cudaSuccess
+             ? 0
+             : -1;
+}
+#endif
+
 int64_t lpqt_w6a16_workspace_bytes(int64_t M, int64_t N, int64_t K, int split_k) {
   if (M <= 0 || N <= 0 || K <= 0) return 0;
   return make_plan(M, N, K, split_k, num_sms()).ws_bytes;
 }
 
+// Reports the plan: block_n = MMA N, splits = max CTAs sharing one tile
+// (stream-K), grid = CTAs, stages = smem pipeline depth.
 int lpqt_w6a16_plan(int64_t M, int64_t N, int64_t K, int split_k, int* block_n, int* splits, int* grid, int* stages) {
   if (M <= 0 || N <= 0 || K <= 0) return LPQT_E_SHAPE;
   const Plan p = make_plan(M, N, K, split_k, num_sms());
   if (block_n) *block_n = p.bn;
-  if (splits) *splits = p.splits;
+  if (splits) {
+    const int64_t per = p.total / p.grid;  // k-steps per CTA (floor)
+    *splits = p.partials ? static_cast<int>((p.ksteps + (per > 0 ? per : 1) - 1) / (per > 0 ? per : 1) + 1) : 1;
+  }
   if (grid) *grid = p.grid;
   if (stages) *stages = p.stages;
   return LPQT_OK;
@@ -470,20 +664,22 @@ int lpqt_w6a16_linear(const uint8_t* tiles, const uint16_t* scales, const uint16
   const Plan p = make_plan(M, N, K, split_k, num_sms());
   if (p.ws_bytes > 0 && (workspace == nullptr || workspace_bytes < p.ws_bytes)) return LPQT_E_WORKSPACE;
   GemmArgs args{};
+#ifdef LPQT_TRACE
+  args.trace = trace_buffer();
+#endif
   args.tiles = tiles;
   args.scales = scales;
   args.y = Y;
   args.counters = static_cast<int*>(workspace);
   args.partials = reinterpret_cast<float*>(static_cast<uint8_t*>(workspace) + p.counters_bytes);
   args.ldy = ldy;
+  args.total = p.total;
   args.M = static_cast<int>(M);
   args.N = static_cast<int>(N);
   args.k_tiles = p.k_tiles;
+  args.ksteps = p.ksteps;
   args.n_tiles = p.n_tiles;
   args.m_tiles = p.m_tiles;
-  args.splits = p.splits;
-  args.kt_per_split = p.kt_per_split;
-  args.num_units = p.num_units;
   args.y_dtype = y_dtype;
   args.y_layout = y_layout;
   cudaStream_t st = as_stream(stream);

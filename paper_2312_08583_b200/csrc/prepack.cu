@@ -4,10 +4,12 @@
 // The canonical planes (packing.py:63-90) are the reference's storage format
 // and stay the parity artifact.  The GEMM instead streams 128x128 weight
 // tiles of 12288 contiguous bytes (one 1-D bulk copy each) whose bit order is
-// chosen so the in-register FP6 -> FP16 rebuild costs ~1.2 ALU ops per
-// weight (see fp6x32_to_f16x32 in common.cuh).  K3 runs exactly that
-// transform and multiplies by the folded scale in binary16, reproducing
-// dequant_bias_shift_array (dequant.py:82-86) bit for bit.
+// chosen so the in-register FP6 -> FP16 rebuild is the hardware e3m2 converter
+// plus a cheap spare-bit gather (~0.8 ALU ops per weight; fp6x32_cvt_f16x32 in
+// common.cuh).  K3 runs exactly that transform and multiplies by S in
+// binary16: value_f16[c] * S (dequant_naive_array, dequant.py:72-79), which
+// the reference proves bit-identical to the bias-shift path
+// compose[c] * (S * 2^12) (dequant.py:82-86; pkg/tests/test_dequant.py:93-102).
 #include "common.cuh"
 
 namespace lpqt {
@@ -50,30 +52,28 @@ __global__ void unprepack_kernel(const uint8_t* __restrict__ tiles, int64_t N, i
   const int64_t groups = Kp / 32, total = N * groups, k_tiles = Kp / kTileK;
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
     const int64_t n = t / groups, g = t % groups;
-    uint32_t w[6], h[16];
+    uint32_t w[6];
+    uint8_t c[32];
     load_group(tiles, n, g, k_tiles, w);
-    fp6x32_to_f16x32(w, h);  // the GEMM's transform; codes come back out of the fp16 high bytes
+    fp6x32_unpack_codes(w, c);
 #pragma unroll
     for (int j = 0; j < 32; ++j) {
       const int64_t k = g * 32 + j;
-      if (k < K) {
-        const uint32_t b = (h[j >> 1] >> (16 * (j & 1) + 8)) & 0xFFu;
-        codes[n * K + k] = static_cast<uint8_t>(fp6_from_byteform(b));
-      }
+      if (k < K) codes[n * K + k] = c[j];
     }
   }
 }
 
-// K3: tiles -> out[N, K] binary16 = compose[c] * folded[n]
-__global__ void tiles_dequant_kernel(const uint8_t* __restrict__ tiles, const uint16_t* __restrict__ folded,
+// K3: tiles -> out[N, K] binary16 = value_f16[c] * S[n] (the GEMM's transform)
+__global__ void tiles_dequant_kernel(const uint8_t* __restrict__ tiles, const uint16_t* __restrict__ scales,
                                      int64_t N, int64_t K, int64_t Kp, uint16_t* __restrict__ out) {
   const int64_t groups = Kp / 32, total = N * groups, k_tiles = Kp / kTileK;
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
     const int64_t n = t / groups, g = t % groups;
     uint32_t w[6], h[16];
     load_group(tiles, n, g, k_tiles, w);
-    fp6x32_to_f16x32(w, h);
-    const __half2 f2 = __half2half2(__ushort_as_half(folded[n]));
+    fp6x32_cvt_f16x32(w, h);
+    const __half2 f2 = __half2half2(__ushort_as_half(scales[n]));
 #pragma unroll
     for (int j = 0; j < 16; ++j) {
       __half2 v = *reinterpret_cast<const __half2*>(&h[j]);
@@ -116,12 +116,12 @@ int lpqt_fp6_unprepack(const uint8_t* tiles, int64_t N, int64_t K, uint8_t* code
   return check_launch();
 }
 
-int lpqt_fp6_tiles_dequant(const uint8_t* tiles, const uint16_t* folded, int64_t N, int64_t K, uint16_t* out,
+int lpqt_fp6_tiles_dequant(const uint8_t* tiles, const uint16_t* scales, int64_t N, int64_t K, uint16_t* out,
                            void* stream) {
   if (N < 0 || K < 0) return LPQT_E_SHAPE;
   if (N == 0 || K == 0) return LPQT_OK;
   const int64_t Kp = round_up(K, kTileK);
-  tiles_dequant_kernel<<<grid_for(N * (Kp / 32), 256), 256, 0, as_stream(stream)>>>(tiles, folded, N, K, Kp, out);
+  tiles_dequant_kernel<<<grid_for(N * (Kp / 32), 256), 256, 0, as_stream(stream)>>>(tiles, scales, N, K, Kp, out);
   note_launch();
   return check_launch();
 }

@@ -88,15 +88,13 @@ class Fp6Weight:
                                                   _lib.stream_ptr()), "unprepack")
         return out
 
-    def dequantize_f16(self, folded=None):
-        """[N, K] binary16 via the GEMM's register transform: compose[c] *
-        folded (dequant.py:82-86)."""
+    def dequantize_f16(self):
+        """[N, K] binary16 via the GEMM's register rebuild: value_f16[c] * S
+        (dequant.py:72-79), bit-identical to the bias-shift path
+        compose[c] * folded (dequant.py:82-86)."""
         t = _lib.torch()
-        f = folded if folded is not None else self.folded
-        if f is None:
-            raise ValueError("folded scales required")
         out = t.empty((self.n, self.k), dtype=t.float16, device=self.tiles.device)
-        _lib.check(_lib.load().lpqt_fp6_tiles_dequant(self.tiles.data_ptr(), f.data_ptr(), self.n, self.k,
+        _lib.check(_lib.load().lpqt_fp6_tiles_dequant(self.tiles.data_ptr(), self.scales.data_ptr(), self.n, self.k,
                                                       out.data_ptr(), _lib.stream_ptr()), "tiles_dequant")
         return out
 

@@ -152,9 +152,13 @@ def test_prepack_roundtrip_and_register_transform(shape):
     w = L.Fp6Weight.from_planes(torch.from_numpy(seg4).cuda(), torch.from_numpy(seg2).cuda(),
                                 torch.from_numpy(scales).cuda(), n, k, torch.from_numpy(folded).cuda())
     assert np.array_equal(w.codes().cpu().numpy().ravel(), codes)
+    # the GEMM's register rebuild (hardware e3m2 converter) x S in binary16 ==
+    # the reference's bias-shift dequant (and its naive path) bit for bit
     deq = w.dequantize_f16().cpu().numpy()
     ref = O.dequant_bias_shift_array(codes.reshape(n, k), folded[:, None])
     assert np.array_equal(deq.view(np.uint16), ref.view(np.uint16))
+    ref_naive = O.dequant_naive_array(codes.reshape(n, k), scales[:, None])
+    assert np.array_equal(deq.view(np.uint16), ref_naive.view(np.uint16))
 
 
 # ---------------------------------------------------------------- GEMM
@@ -237,3 +241,20 @@ def test_w6a16_linear_torch_layout():
         q = L.quantize_tensor(W, CGQ, bias_shift=True)
         ref = (L.dequantize_tensor(q, "bias_shift") @ x.double().T).T
         assert normwise_rel(y.float().cpu().numpy(), ref.cpu().numpy()) <= REL_TOL
+
+
+def test_workspace_reuse_across_shapes():
+    # a split-K call with many tiles after one with few must not read the
+    # previous call's partials as tile counters (regression)
+    g = torch.Generator(device="cuda").manual_seed(21)
+    outs = []
+    for n, k in [(4096, 11008), (10240, 8192), (1024, 4096), (10240, 8192)]:
+        W = (torch.randn(n, k, generator=g, device="cuda") * 0.02).half()
+        lin = L.Fp6Linear.from_dense(W)
+        x = torch.randn(3, k, generator=g, device="cuda").half()
+        y = lin(x).float()
+        q = L.quantize_tensor(W, CGQ, bias_shift=True)
+        ref = (L.dequantize_tensor(q, "bias_shift") @ x.double().T).T
+        assert torch.isfinite(y).all()
+        assert normwise_rel(y.cpu().numpy(), ref.cpu().numpy()) <= REL_TOL
+        outs.append(y)

@@ -22,8 +22,15 @@ SHAPES = {
 
 
 def time_fn(fn, iters=50, warm=5, flush=None):
+    """Median device time of one call, replayed from a CUDA graph (no host
+    launch overhead inside the events), L2 flushed between replays."""
     for _ in range(warm):
         fn()
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        fn()
+    g.replay()
     torch.cuda.synchronize()
     evs = []
     for _ in range(iters):
@@ -32,7 +39,7 @@ def time_fn(fn, iters=50, warm=5, flush=None):
         a = torch.cuda.Event(enable_timing=True)
         b = torch.cuda.Event(enable_timing=True)
         a.record()
-        fn()
+        g.replay()
         b.record()
         evs.append((a, b))
     torch.cuda.synchronize()
