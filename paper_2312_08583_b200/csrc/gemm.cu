@@ -17,7 +17,7 @@
 // range) is finished by whichever contributor arrives last, summing the
 // contributors' fp32 partials in a fixed order (deterministic).
 //
-// Per CTA (1 per SM, 704 threads), warp-specialised:
+// Per CTA (1 per SM, 736 threads), warp-specialised:
 //   warp 16     TMA producer: per stage one 1-D bulk copy of the stage's
 //               consecutive 12288-B weight tiles (evict-first) + 2-D TMA boxes
 //               of X (64 k x BN rows, 128-B swizzle; rows >= M, k >= K read 0).
@@ -27,10 +27,10 @@
 //               (128 lanes = weight rows, 64 columns of half2 per 128-k tile);
 //               software-pipelined: the next stage's words load while the
 //               stores drain.
-//   warp 17     MMA issuer: tcgen05.mma.kind::f16 with A in TMEM ("TS"), B = X
-//               from SMEM, D (fp32, 128 x BN) in TMEM; kNAcc independent
-//               accumulators break the MMA->MMA dependency at small N.
-//   warps 18-21 epilogue: tcgen05.ld D (accumulators summed in fixed order)
+//   warps 17-18 MMA issuers (2 for N <= 64, alternate stages, one
+//               accumulator each): tcgen05.mma.kind::f16, A in TMEM ("TS"),
+//               B = X from SMEM, D (fp32, 128 x BN) in TMEM.
+//   warps 19-22 epilogue: tcgen05.ld D (accumulators summed in fixed order)
 //               -> x S*2^12 -> Y, or the stream-K partial/fixup.
 // Pipelines: smem ring full/empty (TMA <-> DQ+MMA), TMEM-A ring afull/aempty
 // (DQ <-> MMA), TMEM-D ring dfull/dempty (MMA <-> epilogue).  The producer and
@@ -47,10 +47,12 @@ namespace lpqt {
 
 constexpr int kNumDqWarps = 16;
 constexpr int kNumEpiWarps = 4;
-constexpr int kWarpTma = kNumDqWarps;
-constexpr int kWarpMma = kNumDqWarps + 1;
-constexpr int kWarpEpi0 = kNumDqWarps + 2;
-constexpr int kThreads = (kNumDqWarps + 2 + kNumEpiWarps) * 32;  // 704
+constexpr int kMaxMmaWarps = 2;
+constexpr int kWarpTmaW = kNumDqWarps;       // weight-tile producer
+constexpr int kWarpTmaX = kNumDqWarps + 1;   // activation producer
+constexpr int kWarpMma0 = kNumDqWarps + 2;
+constexpr int kWarpEpi0 = kWarpMma0 + kMaxMmaWarps;
+constexpr int kThreads = (kWarpEpi0 + kNumEpiWarps) * 32;  // 768
 constexpr int kAColsPerBuf = kTileK / 2;  // 64 columns of packed half2
 constexpr int kTmemCols = 512;
 constexpr int kSmemBudget = 200 * 1024;
@@ -72,26 +74,41 @@ struct GemmArgs {
 
 template <int BN>
 struct Cfg {
-  static constexpr int kKStep = BN <= 64 ? 2 : 1;           // 128-k tiles per pipeline stage
+  static constexpr int kKStep = BN <= 32 ? 2 : 1;           // 128-k tiles per pipeline stage
   static constexpr int kXTileBytes = BN * kTileK * 2;       // X for one tile: two SW128 blocks
-  static constexpr int kStageBytes = kKStep * (kXTileBytes + kTileBytes);
-  static constexpr int kStagesRaw = kSmemBudget / kStageBytes;
-  static constexpr int kStages = kStagesRaw > 8 ? 8 : kStagesRaw;
+  // Two smem rings per stage index: W (weight tiles, released by the DQ warps
+  // as soon as their LDS are done) and X (activations, released by the MMA
+  // commit), each fed by its own producer warp, so weight prefetch depth does
+  // not wait on MMA completion.  Ring sizes are even: DQ groups (and the two
+  // MMA issuers) own alternate stages, so every slot of every ring is always
+  // consumed by the same party and each parity wait observes every phase of
+  // its barrier (an odd ring would let a consumer skip a phase and pass on a
+  // stale parity).
+  static constexpr int kWStageBytes = kKStep * kTileBytes;
+  static constexpr int kXStageBytes = kKStep * kXTileBytes;
+  static constexpr int kXStages = BN <= 64 ? 6 : (BN <= 128 ? 4 : 2);
+  static constexpr int kWStagesRaw = (kSmemBudget - kXStages * kXStageBytes) / kWStageBytes;
+  static constexpr int kWStages = (kWStagesRaw > 8 ? 8 : kWStagesRaw) & ~1;
+  static constexpr int kStages = kWStages;                  // reported by the plan
   static constexpr int kDBufs = BN <= 128 ? 2 : 1;
-  // Independent accumulators: with a small MMA N the tensor pipe finishes an
-  // MMA long before its result can feed the next dependent MMA, so MMA j of
-  // every tile accumulates into D[j % kNAcc] (kNAcc divides the 8 MMAs of a
-  // tile); the epilogue sums them in a fixed order.
-  static constexpr int kNAcc = BN <= 32 ? 4 : (BN <= 64 ? 2 : 1);
+  // MMA issue: at small N a tcgen05.mma executes in ~9 cycles (measured,
+  // tools/mma_bench.cu) while its single-lane issue sequence (R2UR/VOTEU/
+  // UTCHMMA) takes several times that, so two warps issue alternate stages of
+  // a segment, each into its own accumulator; the epilogue sums the
+  // accumulators in a fixed order.  Prefill MMAs (N >= 128) are long enough
+  // for one issuer.
+  static constexpr int kMmaWarps = BN <= 64 ? 2 : 1;
+  static constexpr int kNAcc = kMmaWarps;
   static constexpr int kDCols = BN * kNAcc;
   // TMEM: D buffers at the top, the rest is the A ring (64 columns per tile)
   static constexpr int kACols = kTmemCols - kDBufs * kDCols;
-  static constexpr int kASlots = (kACols / kAColsPerBuf) / kKStep;   // slots of kKStep tiles
-  static constexpr int kBarBytes = 8 * (2 * kStages + 2 * kASlots + 2 * kDBufs) + 16;
-  static constexpr int kSmemBytes = kStages * kStageBytes + kBarBytes + 1024;
-  static_assert(kStages >= 2, "pipeline too shallow");
+  static constexpr int kASlots = ((kACols / kAColsPerBuf) / kKStep) & ~1;   // slots of kKStep tiles
+  static constexpr int kBarBytes = 8 * (2 * kWStages + 2 * kXStages + 2 * kASlots + 2 * kDBufs) + 16;
+  static constexpr int kSmemBytes = kXStages * kXStageBytes + kWStages * kWStageBytes + kBarBytes + 1024;
+  static_assert(kWStages >= 2 && kXStages >= 2, "pipeline too shallow");
+  static_assert(kSmemBytes <= 227 * 1024, "shared memory");
   static_assert(kASlots >= 2, "A ring too shallow");
-  static_assert(8 % kNAcc == 0, "accumulators must divide the MMAs of a tile");
+  static_assert(kMmaWarps <= kMaxMmaWarps, "MMA issuers");
 };
 
 #ifdef LPQT_TRACE
@@ -157,16 +174,16 @@ __device__ __forceinline__ void store_y(const GemmArgs& a, int n, int m, float v
   }
 }
 
-// Sum the kNAcc accumulators over 16 columns [c0, c0+16) (fixed order).
-template <int BN, int NACC>
-__device__ __forceinline__ void load_acc16(uint32_t t_d, int c0, float (&acc)[16]) {
+// Sum the first `nacc` accumulators over 16 columns [c0, c0+16) (fixed order).
+template <int BN>
+__device__ __forceinline__ void load_acc16(uint32_t t_d, int c0, int q0, int nacc, float (&acc)[16]) {
   uint32_t v[16];
-  tmem_ld_x16(t_d + c0, v);
+  tmem_ld_x16(t_d + q0 * BN + c0, v);
   tmem_wait_ld();
 #pragma unroll
   for (int j = 0; j < 16; ++j) acc[j] = __uint_as_float(v[j]);
 #pragma unroll 1
-  for (int q = 1; q < NACC; ++q) {
+  for (int q = q0 + 1; q < q0 + nacc; ++q) {
     tmem_ld_x16(t_d + q * BN + c0, v);
     tmem_wait_ld();
 #pragma unroll
@@ -194,11 +211,13 @@ __global__ void __launch_bounds__(kThreads, 1)
   using C = Cfg<BN>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* smem_x = smem;                                               // kStages x kKStep x kXTileBytes
-  uint8_t* smem_w = smem + C::kStages * C::kKStep * C::kXTileBytes;    // kStages x kKStep x 12288
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem_w + C::kStages * C::kKStep * kTileBytes);
-  uint64_t* empty = full + C::kStages;
-  uint64_t* afull = empty + C::kStages;
+  uint8_t* smem_x = smem;                                     // kXStages x kXStageBytes (1024-aligned)
+  uint8_t* smem_w = smem + C::kXStages * C::kXStageBytes;     // kWStages x kWStageBytes
+  uint64_t* full_w = reinterpret_cast<uint64_t*>(smem_w + C::kWStages * C::kWStageBytes);
+  uint64_t* empty_w = full_w + C::kWStages;
+  uint64_t* full_x = empty_w + C::kWStages;
+  uint64_t* empty_x = full_x + C::kXStages;
+  uint64_t* afull = empty_x + C::kXStages;
   uint64_t* aempty = afull + C::kASlots;
   uint64_t* dfull = aempty + C::kASlots;
   uint64_t* dempty = dfull + C::kDBufs;
@@ -210,33 +229,40 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int64_t end = sk_begin(a, blockIdx.x + 1);
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < C::kStages; ++s) {
-      mbar_init(&full[s], 1);
-      mbar_init(&empty[s], kNumDqWarps / 2 + 1);  // one DQ group + the MMA commit
+    for (int s = 0; s < C::kWStages; ++s) {
+      mbar_init(&full_w[s], 1);
+      mbar_init(&empty_w[s], kNumDqWarps / 2);  // the DQ group owning the slot
+    }
+    for (int s = 0; s < C::kXStages; ++s) {
+      mbar_init(&full_x[s], 1);
+      mbar_init(&empty_x[s], 1);  // MMA commit
     }
     for (int b = 0; b < C::kASlots; ++b) {
       mbar_init(&afull[b], kNumDqWarps / 2);
       mbar_init(&aempty[b], 1);
     }
     for (int d = 0; d < C::kDBufs; ++d) {
-      mbar_init(&dfull[d], 1);
+      mbar_init(&dfull[d], C::kMmaWarps);
       mbar_init(&dempty[d], kNumEpiWarps);
     }
     fence_mbar_init();
   }
-  if (warp == kWarpMma) {
+  if (warp == kWarpMma0) {
     tmem_alloc(tmem_slot, kTmemCols);
     tmem_relinquish();
   }
-  if (warp == kWarpTma && lane == 0) prefetch_tmap(&tmap_x);
+  if (warp == kWarpTmaX && lane == 0) prefetch_tmap(&tmap_x);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = __shfl_sync(0xffffffffu, *tmem_slot, 0);  // warp-uniform
   const uint32_t tmem_d0 = tmem_base + C::kACols;                       // D buffers above the A ring
 
-  if (warp == kWarpTma) {
-    // ------------------------------------------------------------ producer
+  if (warp == kWarpTmaW || warp == kWarpTmaX) {
+    // ------------------------------------------------------------ producers
+    // warp kWarpTmaW: one 1-D bulk copy of the stage's weight tiles (W ring);
+    // warp kWarpTmaX: the stage's X boxes (X ring).
+    const bool is_w = (warp == kWarpTmaW);
     const uint64_t pol = l2_evict_first_policy();
     int t = static_cast<int>(beg / a.ksteps);
     int ks = static_cast<int>(beg - (int64_t)t * a.ksteps);
@@ -245,22 +271,27 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int kt = ks * C::kKStep;
       const int nt = min(C::kKStep, a.k_tiles - kt);
       const int n_tile = t / a.m_tiles, m_tile = t - n_tile * a.m_tiles;
-      const int s = it % C::kStages;
-      const uint32_t ph = (it / C::kStages) & 1;
-      TRACE(0, it);
-      mbar_wait(&empty[s], ph ^ 1);
-      TRACE(1, it);
-      uint8_t* ws = smem_w + s * C::kKStep * kTileBytes;
-      uint8_t* xs = smem_x + s * C::kKStep * C::kXTileBytes;
-      const uint8_t* src = a.tiles + ((int64_t)n_tile * a.k_tiles + kt) * kTileBytes;
-      const uint32_t bytes = static_cast<uint32_t>(nt * (kTileBytes + C::kXTileBytes));
-      const uint32_t e = elect_one();
-      mbar_arrive_expect_tx_if(e, &full[s], bytes);
-      bulk_g2s_if(e, ws, src, static_cast<uint32_t>(nt * kTileBytes), &full[s], pol);
-      for (int j = 0; j < nt; ++j) {
-        tma_load_2d_if(e, xs + j * C::kXTileBytes, &tmap_x, &full[s], (kt + j) * kTileK, m_tile * BN);
-        tma_load_2d_if(e, xs + j * C::kXTileBytes + BN * 128, &tmap_x, &full[s], (kt + j) * kTileK + 64,
-                       m_tile * BN);
+      if (is_w) {
+        const int s = it % C::kWStages;
+        TRACE(0, it);
+        mbar_wait(&empty_w[s], ((it / C::kWStages) & 1) ^ 1);
+        TRACE(1, it);
+        const uint8_t* src = a.tiles + ((int64_t)n_tile * a.k_tiles + kt) * kTileBytes;
+        const uint32_t bytes = static_cast<uint32_t>(nt * kTileBytes);
+        const uint32_t e = elect_one();
+        mbar_arrive_expect_tx_if(e, &full_w[s], bytes);
+        bulk_g2s_if(e, smem_w + s * C::kWStageBytes, src, bytes, &full_w[s], pol);
+      } else {
+        const int s = it % C::kXStages;
+        mbar_wait(&empty_x[s], ((it / C::kXStages) & 1) ^ 1);
+        uint8_t* xs = smem_x + s * C::kXStageBytes;
+        const uint32_t e = elect_one();
+        mbar_arrive_expect_tx_if(e, &full_x[s], static_cast<uint32_t>(nt * C::kXTileBytes));
+        for (int j = 0; j < nt; ++j) {
+          tma_load_2d_if(e, xs + j * C::kXTileBytes, &tmap_x, &full_x[s], (kt + j) * kTileK, m_tile * BN);
+          tma_load_2d_if(e, xs + j * C::kXTileBytes + BN * 128, &tmap_x, &full_x[s], (kt + j) * kTileK + 64,
+                         m_tile * BN);
+        }
       }
       if (++ks == a.ksteps) {
         ks = 0;
@@ -289,21 +320,26 @@ __global__ void __launch_bounds__(kThreads, 1)
       return nt;
     };
     auto seg_src = [&](int i, int h) {
-      const uint8_t* ws = smem_w + (i % C::kStages) * C::kKStep * kTileBytes + row * 16;
+      const uint8_t* ws = smem_w + (i % C::kWStages) * C::kWStageBytes + row * 16;
       return C::kKStep == 2 ? ws + tl * kTileBytes + h * 3 * kTileN * 16 : ws + tl * 3 * kTileN * 16;
+    };
+    // wait for stage i's weight tiles and load this thread's words; the slot
+    // is released (empty_w) only after the words have been consumed by the
+    // transform, so no refill can race the loads
+    auto load_words = [&](int i, int nt, uint4 (&q)[kSegs][3]) {
+      mbar_wait(&full_w[i % C::kWStages], (i / C::kWStages) & 1);
+      if (C::kKStep == 1 || tl < nt) {
+#pragma unroll
+        for (int h = 0; h < kSegs; ++h) lds_row64(seg_src(i, h), q[h]);
+      }
     };
     uint4 q[kSegs][3];
     int nt_cur = 0;
     if (grp < n_st) {
       nt_cur = next_nt();
-      mbar_wait(&full[grp % C::kStages], (grp / C::kStages) & 1);
-      if (C::kKStep == 1 || tl < nt_cur) {
-#pragma unroll
-        for (int h = 0; h < kSegs; ++h) lds_row64(seg_src(grp, h), q[h]);
-      }
+      load_words(grp, nt_cur, q);
     }
     for (int i = grp; i < n_st; i += 2) {
-      const int s = i % C::kStages;
       const int slot = i % C::kASlots;
       const uint32_t sph = (i / C::kASlots) & 1;
       TRACE(2, i);
@@ -319,30 +355,33 @@ __global__ void __launch_bounds__(kThreads, 1)
           tmem_st_x32(C::kKStep == 2 ? ta + tl * kAColsPerBuf + h * 32 : ta + tl * 32, r);
         }
       }
+      // the words of stage i are consumed (the stores read the transform's
+      // registers): hand the W slot back to the producer
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty_w[i % C::kWStages]);
       TRACE(4, i);
       // prefetch the group's next stage while the TMEM stores drain
       if (i + 2 < n_st) {
         const int nt_next = next_nt();
-        mbar_wait(&full[(i + 2) % C::kStages], ((i + 2) / C::kStages) & 1);
+        load_words(i + 2, nt_next, q);
         TRACE(5, i);
-        if (C::kKStep == 1 || tl < nt_next) {
-#pragma unroll
-          for (int h = 0; h < kSegs; ++h) lds_row64(seg_src(i + 2, h), q[h]);
-        }
         nt_cur = nt_next;
       }
       tmem_wait_st();
       TRACE(6, i);
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) {
-        mbar_arrive(&empty[s]);
-        mbar_arrive(&afull[slot]);
-      }
+      if (lane == 0) mbar_arrive(&afull[slot]);
       TRACE(7, i);
     }
-  } else if (warp == kWarpMma) {
+  } else if (warp < kWarpEpi0) {
     // ------------------------------------------------------------ MMA issue
+    // issuer mw takes the stages of global parity mw (the same stages as DQ
+    // group mw) into accumulator mw; a one-stage segment leaves one issuer
+    // without work: it then arrives on dfull without a commit, and the
+    // epilogue sums only the accumulators that were written.
+    const int mw = warp - kWarpMma0;
+    if (mw < C::kMmaWarps) {
     constexpr uint32_t idesc = idesc_f16_m128(BN);
     int64_t pos = beg;
     Seg sg;
@@ -352,45 +391,51 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t dph = (lu / C::kDBufs) & 1;
       mbar_wait(&dempty[d], dph ^ 1);
       tc_fence_after();
-      const uint32_t d_tmem = tmem_d0 + d * C::kDCols;
+      const uint32_t d_tmem = tmem_d0 + d * C::kDCols + mw * BN;
       const int64_t p0 = (int64_t)sg.tile * a.ksteps;
-      for (int ks = sg.ks0; ks < sg.ks1; ++ks) {
+      const int it0 = static_cast<int>(p0 + sg.ks0 - beg);
+      const int ks_first = sg.ks0 + (C::kMmaWarps == 2 ? ((mw - it0) & 1) : 0);
+      for (int ks = ks_first; ks < sg.ks1; ks += C::kMmaWarps) {
         const int it = static_cast<int>(p0 + ks - beg);
         const int kt = ks * C::kKStep;
         const int nt = min(C::kKStep, a.k_tiles - kt);
-        const int s = it % C::kStages;
-        const uint32_t ph = (it / C::kStages) & 1;
+        const int s = it % C::kXStages;
+        const uint32_t ph = (it / C::kXStages) & 1;
         const int slot = it % C::kASlots;
         const uint32_t sph = (it / C::kASlots) & 1;
-        mbar_wait(&full[s], ph);
+        mbar_wait(&full_x[s], ph);
         mbar_wait(&afull[slot], sph);
         TRACE(8, it);
         tc_fence_after();
         const uint32_t e = elect_one();
         // descriptor of X block 0 of this stage; every other operand is a
         // compile-time offset from it (start address field = addr >> 4)
-        const uint64_t bd0 = sdesc_kmajor_sw128(smem_u32(smem_x + s * C::kKStep * C::kXTileBytes));
+        const uint64_t bd0 = sdesc_kmajor_sw128(smem_u32(smem_x + s * C::kXStageBytes));
         const uint32_t bd_lo = static_cast<uint32_t>(bd0), bd_hi = static_cast<uint32_t>(bd0 >> 32);
         const uint32_t ta = tmem_base + slot * C::kKStep * kAColsPerBuf;
-        const bool first = (ks == sg.ks0);
+        const bool first = (ks == ks_first);
 #pragma unroll
         for (int t = 0; t < C::kKStep; ++t) {
           if (t < nt) {
 #pragma unroll
             for (int j = 0; j < kTileK / 16; ++j) {
               const uint32_t off = (t * C::kXTileBytes + (j >> 2) * (BN * 128) + (j & 3) * 32) >> 4;
-              const bool init = first && t == 0 && j < C::kNAcc;
-              mma_f16_ts_if(e, d_tmem + (j % C::kNAcc) * BN, ta + t * kAColsPerBuf + j * 8, bd_lo + off, bd_hi,
-                            idesc, init ? 0u : 1u);
+              const bool init = first && t == 0 && j == 0;
+              mma_f16_ts_if(e, d_tmem, ta + t * kAColsPerBuf + j * 8, bd_lo + off, bd_hi, idesc, init ? 0u : 1u);
             }
           }
         }
-        tc_commit_if(e, &empty[s]);
+        tc_commit_if(e, &empty_x[s]);
         tc_commit_if(e, &aempty[slot]);
         TRACE(10, it);
       }
-      tc_commit_elect(&dfull[d]);
+      if (ks_first < sg.ks1) {
+        tc_commit_elect(&dfull[d]);
+      } else if (lane == 0) {
+        mbar_arrive(&dfull[d]);  // no MMA of this issuer in the segment
+      }
       ++lu;
+    }
     }
   } else {
     // ------------------------------------------------------------ epilogue
@@ -408,6 +453,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int m0 = m_tile * BN;
       const float fs = n < a.N ? __half2float(__ushort_as_half(a.scales[n])) : 0.f;
       const uint32_t t_d = t_lane + d * C::kDCols;
+      // accumulators written for this segment: both issuers when it spans >= 2
+      // stages, else only the issuer of the single stage's parity
+      const int nacc = min(C::kNAcc, sg.ks1 - sg.ks0);
+      const int q0 = (nacc < C::kNAcc) ? static_cast<int>(((int64_t)sg.tile * a.ksteps + sg.ks0 - beg) & 1) : 0;
       mbar_wait(&dfull[d], dph);
       TRACE(9, lu);
       tc_fence_after();
@@ -415,7 +464,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll 1
         for (int c0 = 0; c0 < BN; c0 += 16) {
           float acc[16];
-          load_acc16<BN, C::kNAcc>(t_d, c0, acc);
+          load_acc16<BN>(t_d, c0, q0, nacc, acc);
           if (c0 + 16 >= BN) {  // last chunk read: hand the D buffer back to the MMA warp
             tc_fence_before();
             __syncwarp();
@@ -429,7 +478,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll 1
         for (int c0 = 0; c0 < BN; c0 += 16) {
           float acc[16];
-          load_acc16<BN, C::kNAcc>(t_d, c0, acc);
+          load_acc16<BN>(t_d, c0, q0, nacc, acc);
           if (c0 + 16 >= BN) {
             tc_fence_before();
             __syncwarp();
@@ -486,7 +535,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   tc_fence_before();
   __syncthreads();
-  if (warp == kWarpMma) {
+  if (warp == kWarpMma0) {
     tc_fence_after();
     tmem_dealloc(tmem_base, kTmemCols);
   }

@@ -202,7 +202,9 @@ def test_gemm_subnormal_codes_one_hot():
 
 
 SHAPES = [(4096, 4096, 1), (4096, 4096, 16), (1024, 2048, 7), (512, 640, 33), (256, 1024, 129),
-          (384, 512, 300), (256, 384, 600)]
+          (384, 512, 300), (256, 384, 600),
+          # long K (many ring wraps per CTA) at every MMA width
+          (1024, 8192, 3), (2048, 8192, 24), (1024, 8192, 48), (2048, 8192, 100), (1024, 8192, 600)]
 
 
 @pytest.mark.parametrize("n,k,m", SHAPES)

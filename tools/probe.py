@@ -69,7 +69,7 @@ def main():
             print(json.dumps({"n": n, "k": k, "m": m, "plan": L.plan(m, n, k, args.split),
                               "us_fp6": round(t6 * 1e6, 2), "us_cublas": round(t16 * 1e6, 2),
                               "speedup": round(t16 / t6, 3), "GBps": round(wbytes / t6 / 1e9, 1),
-                              "TFLOPS": round(2 * m * n * k / t6 / 1e12, 2), "err_vs_fp16W": err}))
+                              "TFLOPS": round(2 * m * n * k / t6 / 1e12, 2), "err_vs_fp16W": err}), flush=True)
 
 
 if __name__ == "__main__":
