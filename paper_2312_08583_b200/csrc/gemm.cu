@@ -119,11 +119,25 @@ struct Cfg {
       a.trace[((blockIdx.x == 0 ? 0 : 1) * 16 + (ev)) * 64 + (i)] = clock64();              \
     }                                                                                      \
   } while (0)
+// per-CTA %globaltimer stamps: trace[kTraceCtaBase + cta * 8 + ev]
+#define CTA_STAMP(ev)                                                   \
+  do {                                                                  \
+    if (a.trace && blockIdx.x < 256) {                                  \
+      uint64_t gt;                                                      \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));            \
+      a.trace[kTraceCtaBase + blockIdx.x * 8 + (ev)] = (long long)gt;   \
+    }                                                                   \
+  } while (0)
 #else
 #define TRACE(ev, i) \
   do {               \
   } while (0)
+#define CTA_STAMP(ev) \
+  do {                \
+  } while (0)
 #endif
+constexpr int kTraceCtaBase = 2 * 16 * 64;
+constexpr int kTraceLen = kTraceCtaBase + 256 * 8;
 
 // ---- stream-K geometry ----------------------------------------------------------
 __device__ __forceinline__ int64_t sk_begin(const GemmArgs& a, int c) {
@@ -225,6 +239,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   volatile int* last_flag = reinterpret_cast<volatile int*>(tmem_slot + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) CTA_STAMP(0);
   const int64_t beg = sk_begin(a, blockIdx.x);
   const int64_t end = sk_begin(a, blockIdx.x + 1);
 
@@ -257,6 +272,14 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc_fence_after();
   const uint32_t tmem_base = __shfl_sync(0xffffffffu, *tmem_slot, 0);  // warp-uniform
   const uint32_t tmem_d0 = tmem_base + C::kACols;                       // D buffers above the A ring
+  if (threadIdx.x == 0) {
+    CTA_STAMP(1);
+#ifdef LPQT_TRACE
+    uint32_t smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    if (a.trace && blockIdx.x < 256) a.trace[kTraceCtaBase + blockIdx.x * 8 + 7] = smid;
+#endif
+  }
 
   if (warp == kWarpTmaW || warp == kWarpTmaX) {
     // ------------------------------------------------------------ producers
@@ -298,6 +321,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         ++t;
       }
     }
+    if (is_w && lane == 0) CTA_STAMP(2);
   } else if (warp < kNumDqWarps) {
     // ------------------------------------------------------------ dequant
     // 16 warps in two groups that take alternate stages (so one group's
@@ -374,6 +398,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (lane == 0) mbar_arrive(&afull[slot]);
       TRACE(7, i);
     }
+    if (warp == 0 && lane == 0) CTA_STAMP(3);
   } else if (warp < kWarpEpi0) {
     // ------------------------------------------------------------ MMA issue
     // issuer mw takes the stages of global parity mw (the same stages as DQ
@@ -436,6 +461,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       ++lu;
     }
+    if (mw == 0 && lane == 0) CTA_STAMP(4);
     }
   } else {
     // ------------------------------------------------------------ epilogue
@@ -531,10 +557,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       ++lu;
     }
+    if (warp == kWarpEpi0 && lane == 0) CTA_STAMP(5);
   }
 
   tc_fence_before();
   __syncthreads();
+  if (threadIdx.x == 0) CTA_STAMP(6);
   if (warp == kWarpMma0) {
     tc_fence_after();
     tmem_dealloc(tmem_base, kTmemCols);
@@ -629,8 +657,8 @@ static EncodeTiledFn encode_fn() {
 static long long* trace_buffer() {
   static long long* buf = nullptr;
   if (!buf) {
-    cudaMalloc(&buf, 2 * 16 * 64 * sizeof(long long));
-    cudaMemset(buf, 0, 2 * 16 * 64 * sizeof(long long));
+    cudaMalloc(&buf, kTraceLen * sizeof(long long));
+    cudaMemset(buf, 0, kTraceLen * sizeof(long long));
   }
   return buf;
 }
@@ -672,7 +700,7 @@ extern "C" {
 #ifdef LPQT_TRACE
 int lpqt_trace_dump(long long* host) {
   cudaDeviceSynchronize();
-  return cudaMemcpy(host, trace_buffer(), 2 * 16 * 64 * sizeof(long long), cudaMemcpyDeviceToHost) == cudaSuccess
+  return cudaMemcpy(host, trace_buffer(), kTraceLen * sizeof(long long), cudaMemcpyDeviceToHost) == cudaSuccess
              ? 0
              : -1;
 }
