@@ -59,7 +59,7 @@ extern "C" {
 #define LPQT_Y_MN  1   /* Y[m, n] (torch.nn.Linear layout)                     */
 
 const char* lpqt_strerror(int status);
-int lpqt_abi_version(void);               /* bumps on any signature change */
+int lpqt_abi_version(void);               /* bumps on any signature change (2: _ex) */
 
 /* codec.py:116-132 encode_rtn_array: x[n] (dtype) -> codes[n] (u8). */
 int lpqt_fp6_encode_rtn(const void* x, int dtype, int64_t n, uint8_t* codes,
@@ -147,6 +147,21 @@ int lpqt_w6a16_linear(const uint8_t* tiles, const uint16_t* scales,
                       int64_t K, void* Y, int y_dtype, int y_layout,
                       int64_t ldy, int split_k, void* workspace,
                       int64_t workspace_bytes, void* stream);
+
+/* Same, with launch flags.  LPQT_LAUNCH_PDL launches the kernel with
+ * programmatic dependent launch: it may start while the preceding kernel on
+ * the stream is still running; it streams and dequantizes weight tiles at
+ * once and waits for the preceding grid only before reading Xt and writing
+ * Y / the workspace.  The caller guarantees the tiles and scales are not
+ * written by any kernel still in flight on the stream (true for weights
+ * quantized ahead of time).  Back-to-back layers then overlap one kernel's
+ * tail with the next one's weight prefetch. */
+#define LPQT_LAUNCH_PDL 1
+int lpqt_w6a16_linear_ex(const uint8_t* tiles, const uint16_t* scales,
+                         const uint16_t* Xt, int64_t ldx, int64_t M, int64_t N,
+                         int64_t K, void* Y, int y_dtype, int y_layout,
+                         int64_t ldy, int split_k, void* workspace,
+                         int64_t workspace_bytes, int flags, void* stream);
 
 /* Number of kernel launches performed by this library since load (for the
  * bench's gpu_launches claim). */

@@ -40,7 +40,8 @@ def _stale(target: str, deps: list[str]) -> bool:
 
 
 def build(force: bool = False, verbose: bool = False, defines: list[str] | None = None,
-          lib_path: str | None = None, build_dir: str | None = None) -> str:
+          lib_path: str | None = None, build_dir: str | None = None,
+          source_override: dict[str, str] | None = None) -> str:
     """Compile + link.  `defines`/`lib_path`/`build_dir` build experiment
     variants (e.g. -DLPQT_WAIT_MODE=1) next to the default library."""
     lib_out = lib_path or LIB
@@ -52,7 +53,7 @@ def build(force: bool = False, verbose: bool = False, defines: list[str] | None 
     objs = []
     jobs = []
     for src in SOURCES:
-        s = os.path.join(CSRC, src)
+        s = (source_override or {}).get(src) or os.path.join(CSRC, src)
         o = os.path.join(bdir, src.replace(".cu", ".o"))
         objs.append(o)
         if force or _stale(o, [s] + hdrs):

@@ -112,6 +112,30 @@ __device__ __forceinline__ void fp6x32_cvt_f16x32(const uint32_t w[6], uint32_t 
   out[14] = cvt_e3m2x2_lo(e1);
   out[15] = cvt_e3m2x2_hi(e1);
 }
+// Same rebuild with the spare-bit gather's right shifts done as IMAD.HI
+// (w * 2^(32-s) >> 32) on the FMA pipe, leaving the half-rate ALU pipe the
+// 16 F2FP + 4 LOP3 per 32 weights.  The multipliers come from kernel
+// arguments so ptxas cannot strength-reduce them back into SHF.
+struct ShiftMuls {
+  uint32_t m26, m28, m30;  // 2^26, 2^28, 2^30  ->  >> 6, >> 4, >> 2
+};
+__device__ __forceinline__ uint32_t spare_gather_fma(uint32_t wa, uint32_t wb, uint32_t wc, const ShiftMuls& sm) {
+  const uint32_t t = lop3_sel(__umulhi(wa, sm.m26), __umulhi(wb, sm.m28), 0x03030303u);
+  return lop3_sel(t, __umulhi(wc, sm.m30), 0x0F0F0F0Fu);
+}
+__device__ __forceinline__ void fp6x32_cvt_f16x32_fma(const uint32_t w[6], uint32_t out[16], const ShiftMuls& sm) {
+#pragma unroll
+  for (int i = 0; i < 6; ++i) {
+    out[2 * i] = cvt_e3m2x2_lo(w[i]);
+    out[2 * i + 1] = cvt_e3m2x2_hi(w[i]);
+  }
+  const uint32_t e0 = spare_gather_fma(w[0], w[1], w[2], sm);
+  const uint32_t e1 = spare_gather_fma(w[3], w[4], w[5], sm);
+  out[12] = cvt_e3m2x2_lo(e0);
+  out[13] = cvt_e3m2x2_hi(e0);
+  out[14] = cvt_e3m2x2_lo(e1);
+  out[15] = cvt_e3m2x2_hi(e1);
+}
 // codes of the 32 weights (inverse of fp6x32_pack_words; used by unprepack)
 __host__ __device__ inline void fp6x32_unpack_codes(const uint32_t w[6], uint8_t c[32]) {
   for (int i = 0; i < 6; ++i)
@@ -262,15 +286,41 @@ __device__ __forceinline__ bool mbar_try_wait(uint32_t addr, uint32_t parity) {
 #endif
   return ok != 0;
 }
+// non-blocking probe: has the phase with `parity` completed?
+__device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
 // Spin with a watchdog: a pipeline deadlock traps (the launch fails with an
 // error) instead of hanging the device.
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-  const uint32_t a = smem_u32(bar);
+__device__ __forceinline__ void mbar_wait_u32(uint32_t a, uint32_t parity) {
   uint32_t spins = 0;
   while (!mbar_try_wait(a, parity)) {
     if (++spins == (1u << 30)) __trap();
   }
 }
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) { mbar_wait_u32(smem_u32(bar), parity); }
+__device__ __forceinline__ void mbar_arrive_u32(uint32_t a) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(a) : "memory");
+}
+// ring cursor: slot index + phase parity, advanced once per use
+template <int N>
+struct RingPos {
+  uint32_t idx = 0, ph = 0;
+  __device__ __forceinline__ void adv() {
+    if (++idx == N) {
+      idx = 0;
+      ph ^= 1u;
+    }
+  }
+};
 
 // 1-D bulk copy global -> shared, completes tx bytes on `bar`; evict-first
 // L2 policy for the streamed weight tiles.
@@ -440,6 +490,13 @@ __device__ __forceinline__ void tmem_st_x32(uint32_t taddr, const uint32_t (&r)[
       LPQT_R8((r + 0)), LPQT_R8((r + 8)), LPQT_R8((r + 16)), LPQT_R8((r + 24))
       : "memory");
 }
+__device__ __forceinline__ void tmem_st_x16(uint32_t taddr, const uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, "
+      "%14, %15, %16};" ::"r"(taddr),
+      LPQT_R8((r + 0)), LPQT_R8((r + 8))
+      : "memory");
+}
 __device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 
 __device__ __forceinline__ void tmem_ld_x16(uint32_t taddr, uint32_t (&r)[16]) {
@@ -455,7 +512,43 @@ __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.
 __device__ __forceinline__ void named_bar_sync(int id, int nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
+__device__ __forceinline__ void named_bar_arrive(int id, int nthreads) {
+  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
 
+// Per-warpgroup register reallocation (all 4 warps of the group execute it).
+template <uint32_t N>
+__device__ __forceinline__ void setmaxnreg_inc() {
+  asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(N));
+}
+template <uint32_t N>
+__device__ __forceinline__ void setmaxnreg_dec() {
+  asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(N));
+}
+
+// Programmatic dependent launch: wait until the preceding grid on the stream
+// has completed and its memory is visible (no-op without the launch
+// attribute); allow the next PDL-launched grid to be scheduled.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_launch_dependents() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
+__device__ __forceinline__ uint4 lds128_u32(uint32_t a) {
+  uint4 v;
+  asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ uint2 lds64_u32(uint32_t a) {
+  uint2 v;
+  asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ uint2 lds64(const void* p) {
+  uint2 v;
+  asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(smem_u32(p)));
+  return v;
+}
 __device__ __forceinline__ uint4 lds128(const void* p) {
   uint4 v;
   asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"

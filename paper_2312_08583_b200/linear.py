@@ -36,17 +36,24 @@ def prepack(seg4, seg2, n: int, k: int):
 class Fp6Weight:
     """An N x K FP6 (e3m2) weight resident in HBM in the GEMM's tile layout."""
 
-    def __init__(self, tiles, scales, n: int, k: int, folded=None):
+    def __init__(self, tiles, scales, n: int, k: int, folded=None, static: bool = False):
         self.tiles = tiles
         self.scales = scales          # f16 [N]  (S; the GEMM folds S * 2^12 in-register)
         self.folded = folded          # f16 [N] or None (bias-shift artifact, API parity)
         self.n = int(n)
         self.k = int(k)
+        # static: tiles/scales are complete and never rewritten, so the GEMM
+        # may be launched with programmatic dependent launch (it prefetches
+        # weights before the preceding kernel on the stream has finished).
+        self.static = bool(static)
 
     # -- construction -------------------------------------------------------
     @classmethod
     def from_planes(cls, seg4, seg2, scales, n: int, k: int, folded=None) -> "Fp6Weight":
-        return cls(prepack(seg4, seg2, n, k), scales, n, k, folded)
+        tiles = prepack(seg4, seg2, n, k)
+        # one-time: the weights are complete before any GEMM can overlap them
+        _lib.torch().cuda.current_stream().synchronize()
+        return cls(tiles, scales, n, k, folded, static=True)
 
     @classmethod
     def quantize(cls, W, bias_shift: bool = True) -> "Fp6Weight":
@@ -111,10 +118,11 @@ def _launch(weight: Fp6Weight, xt, ldx: int, m: int, y, y_dtype: int, y_layout: 
     lib = _lib.load()
     ws_bytes = int(lib.lpqt_w6a16_workspace_bytes(m, weight.n, weight.k, split_k))
     ws = _lib.Workspace.get(ws_bytes) if ws_bytes else None
-    _lib.check(lib.lpqt_w6a16_linear(
+    flags = _lib.LAUNCH_PDL if weight.static else 0
+    _lib.check(lib.lpqt_w6a16_linear_ex(
         weight.tiles.data_ptr(), weight.scales.data_ptr(), xt.data_ptr(), ldx, m, weight.n, weight.k,
         y.data_ptr(), y_dtype, y_layout, ldy, split_k, _lib.ptr(ws), ws.numel() if ws is not None else 0,
-        _lib.stream_ptr()), "w6a16_linear")
+        flags, _lib.stream_ptr()), "w6a16_linear")
 
 
 def stage_activations(X, k: int):
