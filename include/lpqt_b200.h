@@ -59,7 +59,7 @@ extern "C" {
 #define LPQT_Y_MN  1   /* Y[m, n] (torch.nn.Linear layout)                     */
 
 const char* lpqt_strerror(int status);
-int lpqt_abi_version(void);               /* bumps on any signature change (2: _ex) */
+int lpqt_abi_version(void);               /* bumps on any signature change (3: _ex, plan_ex) */
 
 /* codec.py:116-132 encode_rtn_array: x[n] (dtype) -> codes[n] (u8). */
 int lpqt_fp6_encode_rtn(const void* x, int dtype, int64_t n, uint8_t* codes,
@@ -142,6 +142,10 @@ int lpqt_stage_activations(const void* X, int dtype, int64_t K, int64_t M,
 int64_t lpqt_w6a16_workspace_bytes(int64_t M, int64_t N, int64_t K, int split_k);
 int lpqt_w6a16_plan(int64_t M, int64_t N, int64_t K, int split_k,
                     int* block_n, int* splits, int* grid, int* stages);
+/* Plan with schedule flags: out[0..5] = block_n, splits, grid, stages,
+ * schedule (0 stream-K, 1 cluster split-K), cluster size (n_out <= 6). */
+int lpqt_w6a16_plan_ex(int64_t M, int64_t N, int64_t K, int split_k, int flags,
+                       int* out, int n_out);
 int lpqt_w6a16_linear(const uint8_t* tiles, const uint16_t* scales,
                       const uint16_t* Xt, int64_t ldx, int64_t M, int64_t N,
                       int64_t K, void* Y, int y_dtype, int y_layout,
@@ -157,6 +161,12 @@ int lpqt_w6a16_linear(const uint8_t* tiles, const uint16_t* scales,
  * quantized ahead of time).  Back-to-back layers then overlap one kernel's
  * tail with the next one's weight prefetch. */
 #define LPQT_LAUNCH_PDL 1
+/* Schedule overrides (default: automatic).  LPQT_SCHED_STREAMK forces the
+ * stream-K schedule (split_k > 0: about split_k CTAs per tile);
+ * LPQT_SCHED_CLUSTER forces cluster split-K with a cluster of split_k CTAs
+ * (k-split factor, 1..8) for decode batches (M <= 32). */
+#define LPQT_SCHED_STREAMK 2
+#define LPQT_SCHED_CLUSTER 4
 int lpqt_w6a16_linear_ex(const uint8_t* tiles, const uint16_t* scales,
                          const uint16_t* Xt, int64_t ldx, int64_t M, int64_t N,
                          int64_t K, void* Y, int y_dtype, int y_layout,

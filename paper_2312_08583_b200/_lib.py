@@ -29,6 +29,7 @@ OK = 0
 E_INVALID_INPUT, E_SHAPE, E_SCALE_OVERFLOW, E_PAYLOAD = -1, -2, -3, -4
 E_INVALID_CODE, E_UNSUPPORTED, E_WORKSPACE, E_CUDA = -5, -6, -7, -100
 LAUNCH_PDL = 1
+SCHED_STREAMK, SCHED_CLUSTER = 2, 4
 
 # device flag bits
 F_NONFINITE, F_SCALE_INF, F_FOLD_OVERFLOW, F_BAD_SCALE, F_BAD_CODE = 1, 2, 4, 8, 16
@@ -58,6 +59,7 @@ SIGNATURES = {
     "lpqt_stage_activations": (_I32, [_P, _I32, _I64, _I64, _I64, _P, _I64, _P]),
     "lpqt_w6a16_workspace_bytes": (_I64, [_I64, _I64, _I64, _I32]),
     "lpqt_w6a16_plan": (_I32, [_I64, _I64, _I64, _I32, _P, _P, _P, _P]),
+    "lpqt_w6a16_plan_ex": (_I32, [_I64, _I64, _I64, _I32, _I32, _P, _I32]),
     "lpqt_w6a16_linear": (_I32, [_P, _P, _P, _I64, _I64, _I64, _I64, _P, _I32, _I32, _I64, _I32, _P, _I64, _P]),
     "lpqt_w6a16_linear_ex": (_I32, [_P, _P, _P, _I64, _I64, _I64, _I64, _P, _I32, _I32, _I64, _I32, _P, _I64, _I32,
                                     _P]),

@@ -9,44 +9,52 @@
 // identity compose[c] * (S * 2^12) == V * S (dequant.py:33-69) means the same
 // result as the folded-scale formulation, bit for bit per element.
 //
-// Work decomposition: stream-K.  The (tile, k-step) iteration space — tiles of
-// 128 weight rows x BN batch columns, k-steps of kKStep x 128 k — is split
-// into `gridDim.x` contiguous, equal ranges, one per persistent CTA.  A range
-// is a sequence of segments (tile, k-range): at most a partial tail of its
-// first tile ("B"), whole tiles, and a partial head of its last tile ("A").
-// A tile cut between CTAs is finished by whichever contributor arrives last,
-// summing the contributors' fp32 partials in a fixed order (deterministic).
-// Each CTA runs its partial segments FIRST (A, then B, then the whole tiles):
-// every contributor of a cut tile reaches it early, so the cross-CTA fixups
-// overlap the whole-tile work instead of forming the kernel's tail.
+// Output tiles are 128 weight rows x BN batch columns; the contraction runs
+// over "stages" of kKStep 128-k weight tiles.  Two work schedules:
 //
-// Per CTA (1 per SM, 768 threads), warp-specialised:
+//  * stream-K (SK): the (tile, k-step) space is cut into gridDim.x equal
+//    contiguous ranges, one per persistent CTA (1 per SM).  A tile cut
+//    between CTAs is finished by whichever contributor arrives last (global
+//    fp32 partials + an acq_rel tile counter), summing the partials in a fixed
+//    order.  Perfect balance; the cross-CTA fixups cost global round trips.
+//    Used when there are many tiles (prefill, big N).
+//  * cluster split-K (CSK): CTAs form clusters of C (C <= 8); cluster j
+//    takes tiles j, j + #clusters, ... ("rounds"), and rank r of the cluster
+//    contracts k-tiles [r KT / C, (r + 1) KT / C) of each.  The C partial
+//    accumulators of a tile meet in shared memory over DSMEM: every
+//    non-reducer stages its fp32 partial in its own smem and signals the
+//    round's reducer (rank round % C) through a cluster-scope mbarrier; the
+//    reducer reads the partials with ld.shared::cluster, sums them in rank
+//    order (deterministic), scales and stores Y, and hands the staging
+//    buffers back.  No global atomics, no L2 round trips on the tail.  Used
+//    for decode when the tile count is small.
+//
+// Per CTA (768 threads), warp-specialised:
 //   warp 16     W producer: per stage one 1-D bulk copy of the stage's
 //               consecutive 12288-B weight tiles (evict-first); starts at
 //               once, before the preceding kernel finishes (PDL).
 //   warp 17     X producer: 2-D TMA boxes of X (64 k x BN rows, 128-B
 //               swizzle; rows >= M, k >= K read 0) after griddepcontrol.wait.
-//   warps 0-15  dequant (DQ): all 16 warps on every stage; warp w owns TMEM
-//               lane group w % 4 (tcgen05.st restriction) and a 64-weight
-//               (kKStep 2) or 32-weight (kKStep 1) piece of each row: LDS of
-//               the tile layout -> FP6->FP16 rebuild (hardware e3m2
+//   warps 0-15  dequant (DQ): two groups of 8 warps on alternate stages;
+//               LDS of the tile layout -> FP6->FP16 rebuild (hardware e3m2
 //               converter + spare-bit gather) -> tcgen05.st into the stage's
-//               TMEM A slot (128 lanes = weight rows, 64 columns of half2
-//               per 128-k tile).  The A ring is kASlots (>= 3) deep, so the
-//               dequant of stage i overlaps the MMAs of stages i-1, i-2.
+//               TMEM A slot (128 lanes = weight rows, 64 half2 columns per
+//               128-k tile).
 //   warps 18-19 MMA issuers (2 for N <= 64, alternate stages, one
 //               accumulator each): tcgen05.mma.kind::f16, A in TMEM ("TS"),
 //               B = X from SMEM, D (fp32, 128 x BN) in TMEM.
 //   warps 20-23 epilogue: tcgen05.ld D (accumulators summed in fixed order)
-//               -> x S -> Y, or the stream-K partial/fixup.
-// Pipelines: W ring full/empty (W producer <-> DQ), X ring (X producer <->
-// MMA commit), TMEM-A ring afull/aempty (DQ <-> MMA commit), TMEM-D ring
-// dfull/dempty (MMA <-> epilogue).  Every ring slot is always consumed by
-// the same party in stage order, so no parity wait can skip a phase (the X
-// ring is even-sized: issuer i & 1 owns the stages of its parity).
+//               -> x S -> Y, or the split-K reduction.
+// Pipelines: W ring (W producer <-> DQ), X ring (X producer <-> MMA commit),
+// TMEM-A ring (DQ <-> MMA commit), TMEM-D ring (MMA <-> epilogue).  Rings
+// are even-sized where two parties alternate stages, so every slot is always
+// consumed by the same party in stage order and no parity wait can skip a
+// phase.
 #include <stdlib.h>
 
+#include <algorithm>
 #include <mutex>
+#include <type_traits>
 
 #include "common.cuh"
 
@@ -64,58 +72,54 @@ constexpr int kAColsPerBuf = kTileK / 2;  // 64 columns of packed half2
 constexpr int kTmemCols = 512;
 constexpr int kSmemBudget = 200 * 1024;
 constexpr int64_t kMaxCounters = 65536;   // stream-K tile counters (256 KiB)
+constexpr int kMaxCluster = 8;
 
 struct GemmArgs {
   const uint8_t* tiles;
   const uint16_t* scales;
   void* y;
-  float* partials;    // [gridDim.x][2][128][BN] fp32 (first / last segment of each CTA)
-  int* counters;      // [tiles] k-steps contributed so far (self-resetting)
+  float* partials;    // SK: [gridDim.x][2][128][BN] fp32 (first / last segment of each CTA)
+  int* counters;      // SK: [tiles] k-steps contributed so far (self-resetting)
   long long* trace;   // LPQT_TRACE builds only: per-CTA %globaltimer stamps
   int64_t ldy;
-  int64_t total;      // tiles * ksteps: the stream-K iteration space
+  int64_t total;      // SK: tiles * ksteps, the stream-K iteration space
   int M, N;
-  int k_tiles, ksteps, n_tiles, m_tiles;
+  int k_tiles, ksteps, n_tiles, m_tiles, tile_count;
   int y_dtype, y_layout;
+  int csk_c;          // CSK: cluster size C (k-split factor)
   ShiftMuls sm;       // 2^26, 2^28, 2^30: right shifts on the FMA pipe (common.cuh)
 };
 
-template <int BN>
+template <int BN, bool CSK>
 struct Cfg {
   static constexpr int kKStep = BN <= 32 ? 2 : 1;           // 128-k tiles per pipeline stage
   static constexpr int kXTileBytes = BN * kTileK * 2;       // X for one tile: two SW128 blocks
-  // Two smem rings per stage index: W (weight tiles, released by the DQ warps
-  // as soon as their words are consumed) and X (activations, released by the
-  // MMA commit), each fed by its own producer warp.
   static constexpr int kWStageBytes = kKStep * kTileBytes;
   static constexpr int kXStageBytes = kKStep * kXTileBytes;
-  static constexpr int kXStages = BN <= 64 ? 6 : (BN <= 128 ? 4 : 2);
-  static constexpr int kWStagesRaw = (kSmemBudget - kXStages * kXStageBytes) / kWStageBytes;
-  static constexpr int kWStages = (kWStagesRaw > 12 ? 12 : kWStagesRaw) & ~1;  // even: see kASlots
+  static constexpr int kXStages = BN <= 16 ? (CSK ? 4 : 6) : (BN <= 128 ? 4 : 2);
+  // CSK: two partial staging buffers of 128 x BN fp32 (rounds alternate)
+  static constexpr int kStageBufBytes = CSK ? kTileN * BN * 4 : 0;
+  static constexpr int kWStagesRaw = (kSmemBudget - kXStages * kXStageBytes - 2 * kStageBufBytes) / kWStageBytes;
+  static constexpr int kWStages = (kWStagesRaw > 12 ? 12 : kWStagesRaw) & ~1;  // even: see header
   static constexpr int kStages = kWStages;                  // reported by the plan
   static constexpr int kDBufs = BN <= 128 ? 2 : 1;
-  // MMA issue: at small N a tcgen05.mma executes in ~9 cycles (measured,
-  // tools/mma_bench.cu) while its single-lane issue sequence (R2UR/VOTEU/
-  // UTCHMMA) takes several times that, so two warps issue alternate stages,
-  // each into its own accumulator; the epilogue sums the accumulators in a
-  // fixed order.  Prefill MMAs (N >= 128) are long enough for one issuer.
+  // MMA issue: at small N a tcgen05.mma executes in ~9 cycles while its
+  // single-lane issue sequence takes several times that, so two warps issue
+  // alternate stages, each into its own accumulator; the epilogue sums them
+  // in a fixed order.  Prefill MMAs (N >= 128) are long enough for one.
   static constexpr int kMmaWarps = BN <= 64 ? 2 : 1;
   static constexpr int kNAcc = kMmaWarps;
   static constexpr int kDCols = BN * kNAcc;
-  // TMEM: D buffers at the top, the rest is the A ring (64 columns per tile)
   static constexpr int kACols = kTmemCols - kDBufs * kDCols;
-  // slots of kKStep tiles; even, so every slot is always filled by the same
-  // dequant group (groups take alternate stages)
-  static constexpr int kASlots = ((kACols / kAColsPerBuf) / kKStep) & ~1;
-  // dequant work split: 16 warps = 4 TMEM lane groups x 4 pieces per row
-  static constexpr int kDqWeights = kKStep * 32;            // weights per thread per stage
-  static constexpr int kBarBytes = 8 * (2 * kWStages + 2 * kXStages + 2 * kASlots + 2 * kDBufs) + 16;
-  static constexpr int kSmemBytes = kXStages * kXStageBytes + kWStages * kWStageBytes + kBarBytes + 1024;
+  static constexpr int kASlots = ((kACols / kAColsPerBuf) / kKStep) & ~1;  // even
+  static constexpr int kBarCount = 2 * kWStages + 2 * kXStages + 2 * kASlots + 2 * kDBufs + 4;
+  static constexpr int kSmemBytes =
+      kXStages * kXStageBytes + kWStages * kWStageBytes + 2 * kStageBufBytes + 8 * kBarCount + 16;
   static_assert(kWStages >= 2 && kXStages >= 2, "pipeline too shallow");
   static_assert(kMmaWarps == 1 || kXStages % 2 == 0, "X ring slots must keep their issuer");
   static_assert(kSmemBytes <= 227 * 1024, "shared memory");
   static_assert(kASlots >= 2, "A ring too shallow");
-  static_assert(kMmaWarps <= kMaxMmaWarps, "MMA issuers");
+  static_assert(!CSK || BN <= 32, "cluster split-K is the decode schedule");
 };
 
 #ifdef LPQT_TRACE
@@ -128,33 +132,26 @@ struct Cfg {
       a.trace[blockIdx.x * 24 + (ev)] = (long long)gt;                  \
     }                                                                   \
   } while (0)
-// per-stage clock64 events of CTA 0: trace[kTraceEv + ev * 64 + stage]
-#define TRACE(ev, i)                                                          \
-  do {                                                                        \
-    if (a.trace && blockIdx.x == 0 && (i) < 64 && lane == 0)                  \
-      a.trace[kTraceEv + (ev) * 64 + (i)] = clock64();                       \
-  } while (0)
-#define WTRACE(ev, i)                                                                     \
-  do {                                                                                    \
-    if (a.trace && blockIdx.x == 0 && (i) < 64 && lane == 0)                              \
-      a.trace[kTraceWarp + (warp * 3 + (ev)) * 64 + (i)] = clock64();                    \
-  } while (0)
 #else
-#define WTRACE(ev, i) \
-  do {                \
-  } while (0)
 #define CTA_STAMP(ev) \
   do {                \
   } while (0)
-#define TRACE(ev, i) \
-  do {               \
-  } while (0)
 #endif
-constexpr int kTraceEv = 256 * 24;
-constexpr int kTraceWarp = kTraceEv + 12 * 64;   // [dq warp 16][3 events][64 stages] of CTA 0
-constexpr int kTraceLen = kTraceWarp + 16 * 3 * 64;
+constexpr int kTraceLen = 256 * 24;
 
-// ---- stream-K geometry ----------------------------------------------------------
+// ---------------------------------------------------------------------------
+// Work schedules.  Both present the CTA's work as a sequence of segments
+// (one tile, a contiguous k-tile range [kt0, kt1), `len` stages whose local
+// indices start at i0); every role walks the same sequence.
+// ---------------------------------------------------------------------------
+struct Seg {
+  int tile, i0, len, kt0, kt1;
+  bool full;  // SK: the whole tile, no other contributor
+  int pidx;   // SK: partial slot (0 = tile holding the range start, 1 = last tile)
+  int red;    // CSK: reducer rank of this round
+};
+
+// ---- stream-K ------------------------------------------------------------------
 __device__ __forceinline__ int64_t sk_begin(const GemmArgs& a, int c) {
   return (int64_t)c * a.total / (int64_t)gridDim.x;
 }
@@ -163,85 +160,93 @@ __device__ __forceinline__ int sk_cta_of(const GemmArgs& a, int64_t p) {
   return static_cast<int>(((p + 1) * (int64_t)gridDim.x - 1) / a.total);
 }
 
-// This CTA's local work order over its range [beg, end): piece A (the
-// partial head of the last tile, nA k-steps from pA), piece B (the partial
-// tail of the first tile, nB k-steps from beg), then the rest from c0 in
-// global order (whole tiles, or the single partial segment of a range inside
-// one tile).
-struct Order {
-  int64_t beg, pA, c0;
-  int nA, nB, n;
+// A CTA's stream-K range [beg, end) in natural order; segments never
+// straddle a tile.
+struct SkSched {
+  int64_t beg, end;
+  int n;
+  __device__ __forceinline__ void init(const GemmArgs& a) {
+    beg = sk_begin(a, blockIdx.x);
+    end = sk_begin(a, blockIdx.x + 1);
+    n = static_cast<int>(end - beg);
+  }
+  template <int KS>
+  __device__ __forceinline__ bool seg_at(const GemmArgs& a, int i, Seg& sg) const {
+    if (i >= n) return false;
+    const int64_t p = beg + i;
+    const int t = static_cast<int>(p / a.ksteps);
+    const int s0 = static_cast<int>(p - (int64_t)t * a.ksteps);
+    const int64_t rem = end - p;
+    const int len = rem < (int64_t)(a.ksteps - s0) ? static_cast<int>(rem) : a.ksteps - s0;
+    sg.tile = t;
+    sg.i0 = i;
+    sg.len = len;
+    sg.kt0 = s0 * KS;
+    sg.kt1 = min((s0 + len) * KS, a.k_tiles);
+    sg.full = (s0 == 0 && len == a.ksteps);
+    sg.pidx = (beg >= (int64_t)t * a.ksteps) ? 0 : 1;
+    sg.red = 0;
+    return true;
+  }
 };
 
-__device__ __forceinline__ Order make_order(const GemmArgs& a, int64_t beg, int64_t end) {
-  Order o{beg, 0, beg, 0, 0, static_cast<int>(end - beg)};
-#ifdef LPQT_EXP_NATURAL_ORDER
-  return o;
-#endif
-  if (end <= beg) return o;
-  const int64_t ks = a.ksteps;
-  const int64_t t_first = beg / ks, t_last = (end - 1) / ks;
-  if (t_first == t_last) return o;
-  if (end % ks != 0) {
-    o.pA = t_last * ks;
-    o.nA = static_cast<int>(end - o.pA);
-  }
-  if (beg % ks != 0) {
-    o.nB = static_cast<int>((t_first + 1) * ks - beg);
-    o.c0 = (t_first + 1) * ks;
-  }
-  return o;
-}
-__device__ __forceinline__ int64_t order_pos(const Order& o, int i) {
-  if (i < o.nA) return o.pA + i;
-  if (i < o.nA + o.nB) return o.beg + (i - o.nA);
-  return o.c0 + (i - o.nA - o.nB);
+// ---- cluster split-K ------------------------------------------------------------
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
 }
 
-// Walks the local order one stage at a time; divides only at piece starts.
-struct OrderIter {
-  int i, t, kk;  // local stage index, tile, k-step inside the tile
-  __device__ __forceinline__ void seek(const GemmArgs& a, const Order& o, int i_) {
-    i = i_;
-    const int64_t p = order_pos(o, i);
-    t = static_cast<int>(p / a.ksteps);
-    kk = static_cast<int>(p - (int64_t)t * a.ksteps);
+struct CskSched {
+  int C, rank, cid, ncl, kt0, kt1, len, rounds, n;
+  __device__ __forceinline__ void init(const GemmArgs& a, int ks) {
+    C = a.csk_c;
+    rank = static_cast<int>(cluster_rank());
+    cid = static_cast<int>(blockIdx.x) / C;
+    ncl = static_cast<int>(gridDim.x) / C;
+    kt0 = rank * a.k_tiles / C;
+    kt1 = (rank + 1) * a.k_tiles / C;
+    len = (kt1 - kt0 + ks - 1) / ks;
+    rounds = cid < a.tile_count ? (a.tile_count - 1 - cid) / ncl + 1 : 0;
+    n = rounds * len;
   }
-  __device__ __forceinline__ void next(const GemmArgs& a, const Order& o) {
-    ++i;
-    if (i == o.nA || i == o.nA + o.nB) {
-      if (i < o.n) seek(a, o, i);
-    } else if (++kk == a.ksteps) {
-      kk = 0;
-      ++t;
+  template <int KS>
+  __device__ __forceinline__ bool seg_at(const GemmArgs& a, int i, Seg& sg) const {
+    if (i >= n) return false;
+    const int q = i / len;
+    sg.tile = cid + q * ncl;
+    sg.i0 = i;
+    sg.len = len;
+    sg.kt0 = kt0;
+    sg.kt1 = kt1;
+    sg.full = (C == 1);
+    sg.pidx = 0;
+    sg.red = q % C;
+    return true;
+  }
+};
+
+// Stage walker over the segment sequence (divisions only at segment starts)
+template <class S, int KS>
+struct StageIter {
+  Seg sg;
+  int s;  // stage inside the segment
+  bool ok;
+  __device__ __forceinline__ void start(const GemmArgs& a, const S& sc, int i) {
+    ok = sc.template seg_at<KS>(a, 0, sg);
+    s = 0;
+    while (ok && i >= sg.i0 + sg.len) ok = sc.template seg_at<KS>(a, sg.i0 + sg.len, sg);
+    if (ok) s = i - sg.i0;
+  }
+  __device__ __forceinline__ void next(const GemmArgs& a, const S& sc) {
+    if (++s == sg.len) {
+      ok = sc.template seg_at<KS>(a, sg.i0 + sg.len, sg);
+      s = 0;
     }
   }
+  __device__ __forceinline__ int kt() const { return sg.kt0 + s * KS; }
+  __device__ __forceinline__ int nt() const { return min(KS, sg.kt1 - kt()); }
 };
-
-struct Seg {
-  int tile, ks0, ks1;  // k-steps [ks0, ks1) of `tile`
-  int i0;              // local stage index of k-step ks0
-  bool full;           // the whole tile (no other contributor)
-  int pidx;            // partial slot: 0 = tile holding the range's start, 1 = the last tile
-};
-
-// next segment of the local order (segments never straddle a piece or tile)
-__device__ __forceinline__ bool seg_next(const GemmArgs& a, const Order& o, int& i, Seg& sg) {
-  if (i >= o.n) return false;
-  const int64_t p = order_pos(o, i);
-  const int t = static_cast<int>(p / a.ksteps);
-  const int s0 = static_cast<int>(p - (int64_t)t * a.ksteps);
-  const int piece_end = i < o.nA ? o.nA : (i < o.nA + o.nB ? o.nA + o.nB : o.n);
-  const int len = min(piece_end - i, a.ksteps - s0);
-  sg.tile = t;
-  sg.ks0 = s0;
-  sg.ks1 = s0 + len;
-  sg.i0 = i;
-  sg.full = (s0 == 0 && len == a.ksteps);
-  sg.pidx = (o.beg >= (int64_t)t * a.ksteps) ? 0 : 1;
-  i += len;
-  return true;
-}
 
 __device__ __forceinline__ int atom_add_acq_rel_gpu(int* p, int v) {
   int old;
@@ -278,59 +283,62 @@ __device__ __forceinline__ void load_acc16(uint32_t t_d, int c0, int q0, int nac
   }
 }
 
-// Dequant piece of one thread: kKStep 2 -> 64 weights (3 x LDS.128 of the
-// tile layout), kKStep 1 -> 32 weights (LDS.128 + LDS.64).  `src` points at
-// the thread's (row, k-half) slot of the tile (common.cuh tile geometry).
-template <int KSTEP>
-struct DqPiece {
-  uint32_t w[KSTEP * 6];
-  __device__ __forceinline__ void load(uint32_t src, int grp) {
-    if constexpr (KSTEP == 2) {
-      const uint4 q0 = lds128_u32(src), q1 = lds128_u32(src + kTileN * 16), q2 = lds128_u32(src + 2 * kTileN * 16);
-      w[0] = q0.x; w[1] = q0.y; w[2] = q0.z; w[3] = q0.w; w[4] = q1.x; w[5] = q1.y;
-      w[6] = q1.z; w[7] = q1.w; w[8] = q2.x; w[9] = q2.y; w[10] = q2.z; w[11] = q2.w;
-    } else {
-      if (grp == 0) {
-        const uint4 q0 = lds128_u32(src);
-        const uint2 q1 = lds64_u32(src + kTileN * 16);
-        w[0] = q0.x; w[1] = q0.y; w[2] = q0.z; w[3] = q0.w; w[4] = q1.x; w[5] = q1.y;
-      } else {
-        const uint2 q1 = lds64_u32(src + kTileN * 16 + 8);
-        const uint4 q2 = lds128_u32(src + 2 * kTileN * 16);
-        w[0] = q1.x; w[1] = q1.y; w[2] = q2.x; w[3] = q2.y; w[4] = q2.z; w[5] = q2.w;
-      }
-    }
-  }
-  // FP6 -> FP16 rebuild of the piece into KSTEP * 16 half2 registers
-  __device__ __forceinline__ void rebuild(uint32_t (&r)[KSTEP * 16], const ShiftMuls& sm) const {
-    fp6x32_cvt_f16x32_fma(w, r, sm);
-    if constexpr (KSTEP == 2) fp6x32_cvt_f16x32_fma(w + 6, r + 16, sm);
-  }
-};
-
-template <int KSTEP>
-__device__ __forceinline__ void tmem_st_piece(uint32_t taddr, const uint32_t (&r)[KSTEP * 16]) {
-  if constexpr (KSTEP == 2) {
-    tmem_st_x32(taddr, r);
-  } else {
-    tmem_st_x16(taddr, r);
-  }
+// ---- DSMEM / cluster primitives ----------------------------------------------------
+__device__ __forceinline__ uint32_t mapa_shared(uint32_t addr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ float4 ld_dsmem_f4(uint32_t addr) {
+  float4 v;
+  asm volatile("ld.shared::cluster.v4.f32 {%0, %1, %2, %3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "r"(addr)
+               : "memory");
+  return v;
+}
+// arrive (release, cluster scope) on an mbarrier of another CTA of the cluster
+__device__ __forceinline__ void mbar_arrive_remote(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+__device__ __forceinline__ void mbar_wait_cluster(uint32_t addr, uint32_t parity) {
+  uint32_t ok = 0, spins = 0;
+  do {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(addr), "r"(parity)
+        : "memory");
+    if (++spins == (1u << 30)) __trap();
+  } while (!ok);
+}
+__device__ __forceinline__ void cluster_arrive() {
+  asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void cluster_wait() { asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory"); }
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 
-// RAGGED: k_tiles % kKStep != 0, so the last k-step of every tile holds one
-// tile (only possible for kKStep 2; LLaMA/StarCoder K are multiples of 256).
-template <int BN, bool RAGGED>
+// RAGGED: some stage holds fewer than kKStep tiles (the last k-step of a
+// tile when k_tiles % kKStep != 0, or an odd cluster split-K k-range); only
+// then do the dequant warps walk the stage sequence to learn tile counts.
+template <int BN, bool CSK, bool RAGGED>
 __global__ void __launch_bounds__(kThreads, 1)
     w6a16_tcgen05_kernel(const __grid_constant__ CUtensorMap tmap_x, const GemmArgs a) {
-  using C = Cfg<BN>;
+  using C = Cfg<BN, CSK>;
+  constexpr int KS = C::kKStep;
+  using Sched = typename std::conditional<CSK, CskSched, SkSched>::type;
   // The dynamic shared window starts 1024-aligned (as CUTLASS also assumes
   // for SW128 operands; checked below), so every address is a constant offset
-  // from the symbol and needs no runtime re-derivation.
+  // from the symbol.
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* smem = smem_raw;
-  uint8_t* smem_x = smem;                                     // kXStages x kXStageBytes (1024-aligned)
-  uint8_t* smem_w = smem + C::kXStages * C::kXStageBytes;     // kWStages x kWStageBytes
-  uint64_t* full_w = reinterpret_cast<uint64_t*>(smem_w + C::kWStages * C::kWStageBytes);
+  uint8_t* smem_x = smem_raw;                                           // kXStages x kXStageBytes
+  uint8_t* smem_w = smem_x + C::kXStages * C::kXStageBytes;             // kWStages x kWStageBytes
+  uint8_t* smem_stg = smem_w + C::kWStages * C::kWStageBytes;           // CSK: 2 x [BN/4][128] float4
+  uint64_t* full_w = reinterpret_cast<uint64_t*>(smem_stg + 2 * C::kStageBufBytes);
   uint64_t* empty_w = full_w + C::kWStages;
   uint64_t* full_x = empty_w + C::kWStages;
   uint64_t* empty_x = full_x + C::kXStages;
@@ -338,7 +346,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* aempty = afull + C::kASlots;
   uint64_t* dfull = aempty + C::kASlots;
   uint64_t* dempty = dfull + C::kDBufs;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(dempty + C::kDBufs);
+  uint64_t* part_full = dempty + C::kDBufs;  // CSK [2]: this CTA's round partials from the senders
+  uint64_t* stg_free = part_full + 2;        // CSK [2]: this CTA's staging buffer read by the reducer
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(stg_free + 2);
   volatile int* last_flag = reinterpret_cast<volatile int*>(tmem_slot + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -346,8 +356,13 @@ __global__ void __launch_bounds__(kThreads, 1)
     CTA_STAMP(0);
     if (smem_u32(smem_raw) & 1023u) __trap();  // SW128 descriptors need 1024-B alignment
   }
-  const Order ord = make_order(a, sk_begin(a, blockIdx.x), sk_begin(a, blockIdx.x + 1));
-  const int n_st = ord.n;
+  Sched sc;
+  if constexpr (CSK) {
+    sc.init(a, KS);
+  } else {
+    sc.init(a);
+  }
+  const int n_st = sc.n;
 
   // Setup.  The W producer initialises every mbarrier and starts streaming
   // weight tiles at once (weights never depend on the preceding kernel, see
@@ -371,6 +386,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_init(&dfull[d], C::kMmaWarps);
         mbar_init(&dempty[d], kNumEpiWarps);
       }
+      if constexpr (CSK) {
+        for (int b = 0; b < 2; ++b) {
+          mbar_init(&part_full[b], sc.C > 1 ? sc.C - 1 : 1);  // one remote arrive per sender
+          mbar_init(&stg_free[b], 1);                         // one remote arrive by the reducer
+        }
+      }
       fence_mbar_init();
       pdl_launch_dependents();  // the next kernel may queue for this SM as soon as it frees
     }
@@ -386,6 +407,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     named_bar_sync(2, kThreads);
     tc_fence_after();
   }
+  // CSK: every thread arrives on the cluster barrier once its CTA's barriers
+  // are initialised; the epilogue (the only remote user) waits before its
+  // first DSMEM access, every other warp just before the exit sync
+  if constexpr (CSK) cluster_arrive();
   // warp-uniform (not read by the W producer, which may pass before the alloc)
   const uint32_t tmem_base = warp == kWarpTmaW ? 0u : __shfl_sync(0xffffffffu, *tmem_slot, 0);
   const uint32_t tmem_d0 = tmem_base + C::kACols;                       // D buffers above the A ring
@@ -399,8 +424,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 
   // Register split (launch: 768 x 80): each role's warpgroup re-sizes its
-  // registers on entry — dequant 88, producer/MMA 48, epilogue 64
-  // (4 x 128 x 88 + 128 x 48 + 128 x 64 <= 768 x 80).
+  // registers on entry — dequant 88, producer/MMA 48, epilogue 72
+  // (4 x 128 x 88 + 128 x 48 + 128 x 72 <= 768 x 80).
   if (warp == kWarpTmaW || warp == kWarpTmaX) {
     // ------------------------------------------------------------ producers
     setmaxnreg_dec<48>();
@@ -408,24 +433,22 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (!is_w) pdl_wait();  // X is the preceding kernel's output
     if (!is_w && lane == 0) CTA_STAMP(13);
     const uint64_t pol = l2_evict_first_policy();
-    OrderIter oi;
-    if (n_st > 0) oi.seek(a, ord, 0);
-    for (int it = 0; it < n_st; ++it, oi.next(a, ord)) {
-      const int kt = oi.kk * C::kKStep;
-      const int nt = min(C::kKStep, a.k_tiles - kt);
-      const int n_tile = oi.t / a.m_tiles, m_tile = oi.t - n_tile * a.m_tiles;
+    StageIter<Sched, KS> it;
+    it.start(a, sc, 0);
+    for (int i = 0; i < n_st; ++i, it.next(a, sc)) {
+      const int kt = it.kt(), nt = it.nt();
+      const int n_tile = it.sg.tile / a.m_tiles, m_tile = it.sg.tile - n_tile * a.m_tiles;
       if (is_w) {
-        const int s = it % C::kWStages;
-        mbar_wait(&empty_w[s], ((it / C::kWStages) & 1) ^ 1);
-        TRACE(0, it);
+        const int s = i % C::kWStages;
+        mbar_wait(&empty_w[s], ((i / C::kWStages) & 1) ^ 1);
         const uint8_t* src = a.tiles + ((int64_t)n_tile * a.k_tiles + kt) * kTileBytes;
         const uint32_t bytes = static_cast<uint32_t>(nt * kTileBytes);
         const uint32_t e = elect_one();
         mbar_arrive_expect_tx_if(e, &full_w[s], bytes);
         bulk_g2s_if(e, smem_w + s * C::kWStageBytes, src, bytes, &full_w[s], pol);
       } else {
-        const int s = it % C::kXStages;
-        mbar_wait(&empty_x[s], ((it / C::kXStages) & 1) ^ 1);
+        const int s = i % C::kXStages;
+        mbar_wait(&empty_x[s], ((i / C::kXStages) & 1) ^ 1);
         uint8_t* xs = smem_x + s * C::kXStageBytes;
         const uint32_t e = elect_one();
         mbar_arrive_expect_tx_if(e, &full_x[s], static_cast<uint32_t>(nt * C::kXTileBytes));
@@ -445,7 +468,6 @@ __global__ void __launch_bounds__(kThreads, 1)
     // the stage (its whole 128-k row: two 64-weight segments), for kKStep 1
     // k-half tl of the stage's tile.
     setmaxnreg_inc<88>();
-    constexpr int KS = C::kKStep;
     constexpr int kSegs = KS == 2 ? 2 : 1;
     const int lg = warp & 3, grp = warp >> 3, tl = (warp >> 2) & 1;
     const int row = lg * 32 + lane;
@@ -469,16 +491,13 @@ __global__ void __launch_bounds__(kThreads, 1)
     };
     Cur wc{static_cast<uint32_t>(grp), 0u};   // W ring
     Cur ac{static_cast<uint32_t>(grp), 0u};   // A ring
-    OrderIter oi;
-    if (RAGGED && grp < n_st) oi.seek(a, ord, grp);
-    auto nt_next = [&]() -> int {  // tiles of the group's next stage, then advance two stages
-      if constexpr (!RAGGED) {
-        return KS;
+    StageIter<Sched, KS> it;
+    if constexpr (RAGGED) it.start(a, sc, grp);
+    auto stage_nt = [&]() -> int {
+      if constexpr (RAGGED) {
+        return it.nt();
       } else {
-        const int nt = min(KS, a.k_tiles - oi.kk * KS);
-        oi.next(a, ord);
-        oi.next(a, ord);
-        return nt;
+        return KS;
       }
     };
     uint32_t q[kSegs][6 * 2];
@@ -497,15 +516,12 @@ __global__ void __launch_bounds__(kThreads, 1)
     };
     int nt_cur = 0;
     if (grp < n_st) {
-      nt_cur = nt_next();
+      nt_cur = stage_nt();
       load_words(nt_cur);
     }
     if (warp == 0 && lane == 0) CTA_STAMP(12);
     for (int i = grp; i < n_st; i += 2) {
-      if (warp == 0) TRACE(1, i);
       mbar_wait_u32(ae0 + 8 * ac.idx, ac.ph ^ 1u);
-      if (warp == 0) TRACE(2, i);
-      WTRACE(0, i);
       tc_fence_after();
       if (KS == 1 || tl < nt_cur) {
         const uint32_t ta = t_lane + ac.idx * (KS * kAColsPerBuf);
@@ -517,69 +533,64 @@ __global__ void __launch_bounds__(kThreads, 1)
           tmem_st_x32(ta + h * 32, r);
         }
       }
-      if (warp == 0) TRACE(3, i);
-      WTRACE(1, i);
       // the stage's words are consumed: hand the W slot back to the producer
       __syncwarp();
       if (lane == 0) mbar_arrive_u32(ew0 + 8 * wc.idx);
       wc.adv2(C::kWStages);
       // prefetch the group's next stage while the TMEM stores drain
       if (i + 2 < n_st) {
-        const int ntn = nt_next();
-        load_words(ntn);
-        nt_cur = ntn;
+        if constexpr (RAGGED) {
+          it.next(a, sc);
+          it.next(a, sc);
+        }
+        nt_cur = stage_nt();
+        load_words(nt_cur);
       }
-      if (warp == 0) TRACE(4, i);
       tmem_wait_st();
-      if (warp == 0) TRACE(5, i);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive_u32(af0 + 8 * ac.idx);
       ac.adv2(C::kASlots);
-      WTRACE(2, i);
     }
     if (warp == 0 && lane == 0) CTA_STAMP(3);
   } else if (warp < kWarpEpi0) {
     // ------------------------------------------------------------ MMA issue
-    setmaxnreg_dec<48>();
     // issuer mw takes the local stages of parity mw into accumulator mw; a
     // one-stage segment leaves one issuer without work: it then arrives on
     // dfull without a commit, and the epilogue sums only the accumulators
     // that were written.
+    setmaxnreg_dec<48>();
     const int mw = warp - kWarpMma0;
     if (mw < C::kMmaWarps) {
       constexpr uint32_t idesc = idesc_f16_m128(BN);
-      int i = 0;
       Seg sg;
       int lu = 0;
-      while (seg_next(a, ord, i, sg)) {
+      for (int i0 = 0; sc.template seg_at<KS>(a, i0, sg); i0 += sg.len) {
         const int d = lu % C::kDBufs;
         const uint32_t dph = (lu / C::kDBufs) & 1;
         mbar_wait(&dempty[d], dph ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_d0 + d * C::kDCols + mw * BN;
-        const int ks_first = sg.ks0 + (C::kMmaWarps == 2 ? ((mw - sg.i0) & 1) : 0);
-        for (int ks = ks_first; ks < sg.ks1; ks += C::kMmaWarps) {
-          const int it = sg.i0 + (ks - sg.ks0);
-          const int kt = ks * C::kKStep;
-          const int nt = min(C::kKStep, a.k_tiles - kt);
-          const int s = it % C::kXStages;
+        const int s_first = C::kMmaWarps == 2 ? ((mw - sg.i0) & 1) : 0;
+        for (int s = s_first; s < sg.len; s += C::kMmaWarps) {
+          const int it = sg.i0 + s;
+          const int kt = sg.kt0 + s * KS;
+          const int nt = min(KS, sg.kt1 - kt);
+          const int xs = it % C::kXStages;
           const int slot = it % C::kASlots;
-          mbar_wait(&full_x[s], (it / C::kXStages) & 1);
+          mbar_wait(&full_x[xs], (it / C::kXStages) & 1);
           if (it == mw && lane == 0) CTA_STAMP(14);
-          TRACE(7, it);
           mbar_wait(&afull[slot], (it / C::kASlots) & 1);
-          TRACE(8, it);
           tc_fence_after();
           const uint32_t e = elect_one();
           // descriptor of X block 0 of this stage; every other operand is a
           // compile-time offset from it (start address field = addr >> 4)
-          const uint64_t bd0 = sdesc_kmajor_sw128(smem_u32(smem_x + s * C::kXStageBytes));
+          const uint64_t bd0 = sdesc_kmajor_sw128(smem_u32(smem_x + xs * C::kXStageBytes));
           const uint32_t bd_lo = static_cast<uint32_t>(bd0), bd_hi = static_cast<uint32_t>(bd0 >> 32);
-          const uint32_t ta = tmem_base + slot * (C::kKStep * kAColsPerBuf);
-          const bool first = (ks == ks_first);
+          const uint32_t ta = tmem_base + slot * (KS * kAColsPerBuf);
+          const bool first = (s == s_first);
 #pragma unroll
-          for (int t = 0; t < C::kKStep; ++t) {
+          for (int t = 0; t < KS; ++t) {
             if (t < nt) {
 #pragma unroll
               for (int j = 0; j < kTileK / 16; ++j) {
@@ -590,11 +601,10 @@ __global__ void __launch_bounds__(kThreads, 1)
               }
             }
           }
-          tc_commit_if(e, &empty_x[s]);
+          tc_commit_if(e, &empty_x[xs]);
           tc_commit_if(e, &aempty[slot]);
-          TRACE(9, it);
         }
-        if (ks_first < sg.ks1) {
+        if (s_first < sg.len) {
           tc_commit_elect(&dfull[d]);
         } else if (lane == 0) {
           mbar_arrive(&dfull[d]);  // no MMA of this issuer in the segment
@@ -605,15 +615,18 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else {
     // ------------------------------------------------------------ epilogue
-    setmaxnreg_dec<64>();
+    setmaxnreg_dec<72>();
+    if constexpr (CSK) cluster_wait();
     pdl_wait();  // Y / workspace writes: the preceding grid must be complete
     const int lg = warp & 3;
     const int rr = lg * 32 + lane;  // row inside the 128-row tile (= TMEM lane)
     const uint32_t t_lane = tmem_d0 + (static_cast<uint32_t>(lg * 32) << 16);
-    int i = 0;
     Seg sg;
     int lu = 0;
-    while (seg_next(a, ord, i, sg)) {
+    // CSK, one bit per staging buffer: barrier phases to wait for, and
+    // whether the buffer has been sent from before
+    uint32_t pf_bits = 0u, sf_bits = 0u, sent_bits = 0u;
+    for (int i0 = 0; sc.template seg_at<KS>(a, i0, sg); i0 += sg.len, ++lu) {
       const int d = lu % C::kDBufs;
       const uint32_t dph = (lu / C::kDBufs) & 1;
       const int n_tile = sg.tile / a.m_tiles, m_tile = sg.tile % a.m_tiles;
@@ -623,13 +636,95 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t t_d = t_lane + d * C::kDCols;
       // accumulators written for this segment: both issuers when it spans >= 2
       // stages, else only the issuer of the single stage's parity
-      const int nacc = min(C::kNAcc, sg.ks1 - sg.ks0);
+      const int nacc = min(C::kNAcc, sg.len);
       const int q0 = (nacc < C::kNAcc) ? (sg.i0 & 1) : 0;
-      const bool last_seg = i >= n_st;
+      const bool last_seg = sg.i0 + sg.len >= n_st;
       mbar_wait(&dfull[d], dph);
       if (last_seg && warp == kWarpEpi0 && lane == 0) CTA_STAMP(8);
       tc_fence_after();
-      if (sg.full) {
+      if constexpr (CSK) {
+        // ---- cluster split-K: reduce the C partials of this tile over DSMEM
+        const int b = lu & 1;  // staging buffer / barrier of this round
+        // staging layout [BN / 4][128] float4: thread rr writes column chunk
+        // j at (j * 128 + rr) * 16 (conflict-free)
+        const uint32_t stg = smem_u32(smem_stg) + b * C::kStageBufBytes + rr * 16;
+        if (sc.C > 1 && sc.rank != sg.red) {
+          // sender: wait until the reducer that read this buffer last is
+          // done with it, stage the partial, signal this round's reducer
+          if ((sent_bits >> b) & 1u) {
+            mbar_wait_cluster(smem_u32(&stg_free[b]), (sf_bits >> b) & 1u);
+            sf_bits ^= 1u << b;
+          }
+          sent_bits |= 1u << b;
+#pragma unroll 1
+          for (int c0 = 0; c0 < BN; c0 += 16) {
+            float acc[16];
+            load_acc16<BN>(t_d, c0, q0, nacc, acc);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(stg + (c0 / 4 + j) * 128 * 16),
+                           "f"(acc[4 * j]), "f"(acc[4 * j + 1]), "f"(acc[4 * j + 2]), "f"(acc[4 * j + 3])
+                           : "memory");
+            }
+          }
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&dempty[d]);
+          named_bar_sync(1, kNumEpiWarps * 32);
+          if (warp == kWarpEpi0 && lane == 0)
+            mbar_arrive_remote(mapa_shared(smem_u32(&part_full[b]), static_cast<uint32_t>(sg.red)));
+        } else {
+          // reducer: own partial into registers and the D buffer straight
+          // back to the MMA (the reduction below must not stall the
+          // pipeline), then wait for the C - 1 partials and sum in rank order
+          float own[BN];
+#pragma unroll
+          for (int c0 = 0; c0 < BN; c0 += 16) {
+            float t16[16];
+            load_acc16<BN>(t_d, c0, q0, nacc, t16);
+#pragma unroll
+            for (int j = 0; j < 16; ++j) own[c0 + j] = t16[j];
+          }
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&dempty[d]);
+          if (sc.C > 1) {
+            mbar_wait_cluster(smem_u32(&part_full[b]), (pf_bits >> b) & 1u);
+            pf_bits ^= 1u << b;
+          }
+#pragma unroll
+          for (int c0 = 0; c0 < BN; c0 += 16) {
+            float sum[16];
+#pragma unroll
+            for (int j = 0; j < 16; ++j) sum[j] = 0.f;
+#pragma unroll 1
+            for (int r = 0; r < sc.C; ++r) {
+              if (r == sc.rank) {
+#pragma unroll
+                for (int j = 0; j < 16; ++j) sum[j] += own[c0 + j];
+              } else {
+                const uint32_t src = mapa_shared(stg + (c0 / 4) * 128 * 16, static_cast<uint32_t>(r));
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                  const float4 v = ld_dsmem_f4(src + j * 128 * 16);
+                  sum[4 * j] += v.x;
+                  sum[4 * j + 1] += v.y;
+                  sum[4 * j + 2] += v.z;
+                  sum[4 * j + 3] += v.w;
+                }
+              }
+            }
+#pragma unroll
+            for (int j = 0; j < 16; ++j) store_y(a, n, m0 + c0 + j, sum[j] * fs);
+          }
+          if (sc.C > 1) {
+            // the senders' staging buffers are read: hand them back
+            named_bar_sync(1, kNumEpiWarps * 32);
+            if (warp == kWarpEpi0 && lane < sc.C && lane != sc.rank)
+              mbar_arrive_remote(mapa_shared(smem_u32(&stg_free[b]), static_cast<uint32_t>(lane)));
+          }
+        }
+      } else if (sg.full) {
 #pragma unroll 1
         for (int c0 = 0; c0 < BN; c0 += 16) {
           float acc[16];
@@ -643,6 +738,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int j = 0; j < 16; ++j) store_y(a, n, m0 + c0 + j, acc[j] * fs);
         }
       } else {
+        // ---- stream-K partial tile
         float* part = a.partials + (((int64_t)blockIdx.x * 2 + sg.pidx) * kTileN + rr) * BN;
 #pragma unroll 1
         for (int c0 = 0; c0 < BN; c0 += 16) {
@@ -661,25 +757,29 @@ __global__ void __launch_bounds__(kThreads, 1)
         // publish: CTA barrier, then one gpu-scope acq_rel atomic (release our
         // partial, acquire the other contributors' partials if we are last)
         named_bar_sync(1, kNumEpiWarps * 32);
-        if (last_seg && warp == kWarpEpi0 && lane == 0) CTA_STAMP(9);
         if (warp == kWarpEpi0 && lane == 0) {
-          const int k_done = sg.ks1 - sg.ks0;
+          const int k_done = sg.len;
           const int prev = atom_add_acq_rel_gpu(&a.counters[sg.tile], k_done);
           *last_flag = (prev + k_done == a.ksteps) ? 1 : 0;
         }
         named_bar_sync(1, kNumEpiWarps * 32);
-        if (last_seg && warp == kWarpEpi0 && lane == 0) CTA_STAMP(10);
         if (*last_flag) {
           const int64_t p_first = (int64_t)sg.tile * a.ksteps;
           const int c_first = sk_cta_of(a, p_first);
           const int c_last = sk_cta_of(a, p_first + a.ksteps - 1);
+          // partial slot of contributor c: only c_first can have started its
+          // range before the tile (slot 1 = its last segment); every later
+          // contributor starts inside the tile (slot 0 = its first segment)
+          const int idx_first = (sk_begin(a, c_first) >= p_first) ? 0 : 1;
 #pragma unroll 1
           for (int c0 = 0; c0 < BN; c0 += 16) {
             float acc[16];
 #pragma unroll
             for (int j = 0; j < 16; ++j) acc[j] = 0.f;
             // contributors in k order (fixed summation order: deterministic);
-            // kFix of them are loaded at once so their L2 round trips overlap
+            // kFix of them are loaded at once so their L2 round trips
+            // overlap.  Plain (weak) loads: the acquire above ordered them
+            // after every contributor's release.
             constexpr int kFix = 2;
 #pragma unroll 1
             for (int cb = c_first; cb <= c_last; cb += kFix) {
@@ -688,11 +788,11 @@ __global__ void __launch_bounds__(kThreads, 1)
               for (int u = 0; u < kFix; ++u) {
                 const int c = cb + u;
                 if (c <= c_last) {
-                  const int idx = (sk_begin(a, c) >= p_first) ? 0 : 1;
+                  const int idx = c == c_first ? idx_first : 0;
                   const float4* src =
                       reinterpret_cast<const float4*>(a.partials + (((int64_t)c * 2 + idx) * kTileN + rr) * BN + c0);
 #pragma unroll
-                  for (int j = 0; j < 4; ++j) v[u][j] = __ldcg(src + j);
+                  for (int j = 0; j < 4; ++j) v[u][j] = src[j];
                 } else {
 #pragma unroll
                   for (int j = 0; j < 4; ++j) v[u][j] = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -717,13 +817,18 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         named_bar_sync(1, kNumEpiWarps * 32);
       }
-      ++lu;
     }
     if (warp == kWarpEpi0 && lane == 0) CTA_STAMP(5);
   }
 
+  if constexpr (CSK) {
+    if (warp < kWarpEpi0) cluster_wait();  // the setup phase (epilogue waited already)
+  }
   tc_fence_before();
   __syncthreads();
+  // CSK: no CTA may leave while a peer can still read its staging buffer or
+  // arrive on its barriers
+  if constexpr (CSK) cluster_sync_all();
   if (threadIdx.x == 0) CTA_STAMP(6);
   if (warp == kWarpMma0) {
     tc_fence_after();
@@ -738,6 +843,9 @@ struct Plan {
   int bn, grid, n_tiles, m_tiles, k_tiles, ksteps, stages, smem, kstep;
   int64_t tiles, total, ws_bytes, counters_bytes;
   bool partials;
+  bool csk;
+  int cluster;  // CSK cluster size
+  int splits;   // max CTAs contributing to one tile
 };
 
 static int pick_bn(int64_t M) {
@@ -748,11 +856,11 @@ static int pick_bn(int64_t M) {
   return 256;
 }
 
-template <int BN>
+template <int BN, bool CSK>
 static void cfg_of(Plan& p) {
-  p.stages = Cfg<BN>::kStages;
-  p.smem = Cfg<BN>::kSmemBytes;
-  p.kstep = Cfg<BN>::kKStep;
+  p.stages = Cfg<BN, CSK>::kStages;
+  p.smem = Cfg<BN, CSK>::kSmemBytes;
+  p.kstep = Cfg<BN, CSK>::kKStep;
 }
 
 static int num_sms() {
@@ -766,23 +874,101 @@ static int num_sms() {
   return sms;
 }
 
-// split_k == 0: one persistent CTA per SM over the whole stream-K space.
-// split_k  > 0: about split_k CTAs per tile (testing / tuning hook).
-static Plan make_plan(int64_t M, int64_t N, int64_t K, int split_k, int sms) {
+// Co-resident clusters of c CTAs for the decode kernel (GPC packing; 1 CTA
+// per SM).  Queried once per c from the driver; the fallback is a 148-SM
+// B200 as measured (tools/cluster_occ.cu).
+template <int BN>
+static int max_clusters(int c) {
+  static int cache[kMaxCluster + 1] = {0};
+  static std::mutex mu;
+  std::lock_guard<std::mutex> lock(mu);
+  if (cache[c] > 0) return cache[c];
+  static const int fallback[kMaxCluster + 1] = {0, 148, 74, 45, 33, 26, 22, 15, 15};
+  int n = 0;
+  auto kern = w6a16_tcgen05_kernel<BN, true, true>;
+  constexpr int smem = Cfg<BN, true>::kSmemBytes;
+  int dev = 0;
+  if (cudaGetDevice(&dev) == cudaSuccess &&
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) == cudaSuccess) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(c * 64);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = smem;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = c;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    if (cudaOccupancyMaxActiveClusters(&n, kern, &cfg) != cudaSuccess) n = 0;
+  }
+  cudaGetLastError();  // a failed query must not poison later launches
+  if (n <= 0) n = fallback[c];
+  cache[c] = n;
+  return n;
+}
+
+static int max_clusters_bn(int bn, int c) { return bn <= 16 ? max_clusters<16>(c) : max_clusters<32>(c); }
+
+// split_k == 0: automatic schedule.  With LPQT_SCHED_CLUSTER: cluster
+// split-K with C = split_k (>= 1).  Otherwise split_k > 0 is stream-K with
+// about split_k CTAs per tile (testing / tuning hooks).
+static Plan make_plan(int64_t M, int64_t N, int64_t K, int split_k, int flags, int sms) {
   Plan p{};
   p.bn = pick_bn(M);
-  switch (p.bn) {
-    case 16: cfg_of<16>(p); break;
-    case 32: cfg_of<32>(p); break;
-    case 64: cfg_of<64>(p); break;
-    case 128: cfg_of<128>(p); break;
-    default: cfg_of<256>(p); break;
-  }
   p.n_tiles = static_cast<int>((N + kTileN - 1) / kTileN);
   p.m_tiles = static_cast<int>((M + p.bn - 1) / p.bn);
   p.k_tiles = static_cast<int>((K + kTileK - 1) / kTileK);
-  p.ksteps = (p.k_tiles + p.kstep - 1) / p.kstep;
   p.tiles = (int64_t)p.n_tiles * p.m_tiles;
+  // ---- schedule choice (decode, BN <= 32, may use cluster split-K)
+  const bool csk_ok = p.bn <= 32 && p.tiles < ((int64_t)1 << 30);
+  int best_c = 0;
+  if (csk_ok && !(flags & LPQT_SCHED_STREAMK)) {
+    if (flags & LPQT_SCHED_CLUSTER) {
+      best_c = split_k > 0 ? split_k : 1;
+      best_c = std::min(best_c, std::min(kMaxCluster, p.k_tiles));
+    } else if (split_k == 0) {
+      // Time model of one launch (us, measured on B200, tools/abx.py): a CTA
+      // streams its weights at ~40 GB/s; stream-K pays ~6 us of cross-CTA
+      // fixups on its tail when tiles are split, cluster split-K ~1.5 us of
+      // DSMEM reduction per round.  Only C = 2 is chosen automatically:
+      // larger clusters measured slower than this model predicts.
+      const double tile_us = (double)kTileBytes / 40e3;   // one 128x128 weight tile
+      const double sk_splits = (double)p.tiles * p.k_tiles / sms;  // k-tiles per CTA
+      const bool sk_partial = (p.tiles % sms) != 0;
+      const double sk_us = sk_splits * tile_us + (sk_partial ? 6.0 : 0.0);
+      const int c = 2;
+      if (p.k_tiles >= c) {
+        const int64_t ncl = std::min<int64_t>(max_clusters_bn(p.bn, c), p.tiles);
+        const int64_t rounds = (p.tiles + ncl - 1) / ncl;
+        const double csk_us = rounds * (((p.k_tiles + c - 1) / c) * tile_us + 1.5);
+        if (csk_us < sk_us) best_c = c;
+      }
+    }
+  }
+  if (best_c > 0) {
+    p.csk = true;
+    p.cluster = best_c;
+    if (p.bn <= 16) {
+      cfg_of<16, true>(p);
+    } else {
+      cfg_of<32, true>(p);
+    }
+    const int64_t ncl = std::min<int64_t>(max_clusters_bn(p.bn, best_c), p.tiles);
+    p.grid = static_cast<int>(ncl * best_c);
+    p.ksteps = (p.k_tiles + p.kstep - 1) / p.kstep;
+    p.splits = best_c;
+    return p;
+  }
+  switch (p.bn) {
+    case 16: cfg_of<16, false>(p); break;
+    case 32: cfg_of<32, false>(p); break;
+    case 64: cfg_of<64, false>(p); break;
+    case 128: cfg_of<128, false>(p); break;
+    default: cfg_of<256, false>(p); break;
+  }
+  p.ksteps = (p.k_tiles + p.kstep - 1) / p.kstep;
   p.total = p.tiles * p.ksteps;
   int64_t g = split_k > 0 ? p.tiles * split_k : sms;
   if (g > p.total) g = p.total;
@@ -795,6 +981,8 @@ static Plan make_plan(int64_t M, int64_t N, int64_t K, int split_k, int sms) {
     p.counters_bytes = kMaxCounters * 4;  // fixed region, zeroed once, self-resetting
     p.ws_bytes = p.counters_bytes + (int64_t)p.grid * 2 * kTileN * p.bn * 4;
   }
+  const int64_t per = p.total / p.grid;  // k-steps per CTA (floor)
+  p.splits = p.partials ? static_cast<int>((p.ksteps + (per > 0 ? per : 1) - 1) / (per > 0 ? per : 1) + 1) : 1;
   return p;
 }
 
@@ -816,17 +1004,22 @@ static EncodeTiledFn encode_fn() {
 }
 
 #ifdef LPQT_TRACE
+// kTraceSlots trace records; launch n writes record n % kTraceSlots (graph
+// captures bake the record index in at capture time)
+constexpr int kTraceSlots = 16;
 static long long* trace_buffer() {
   static long long* buf = nullptr;
   if (!buf) {
-    cudaMalloc(&buf, kTraceLen * sizeof(long long));
-    cudaMemset(buf, 0, kTraceLen * sizeof(long long));
+    cudaMalloc(&buf, (size_t)kTraceSlots * kTraceLen * sizeof(long long));
+    cudaMemset(buf, 0, (size_t)kTraceSlots * kTraceLen * sizeof(long long));
   }
   return buf;
 }
+static int g_trace_n = 0;  // launches traced so far
+static int trace_next_slot() { return g_trace_n++ % kTraceSlots; }
 #endif
 
-template <int BN, bool RAGGED>
+template <int BN, bool CSK, bool RAGGED>
 static int launch_impl(const Plan& p, const GemmArgs& args, const uint16_t* Xt, int64_t ldx, int64_t M,
                        cudaStream_t stream, int flags) {
   EncodeTiledFn enc = encode_fn();
@@ -840,8 +1033,8 @@ static int launch_impl(const Plan& p, const GemmArgs& args, const uint16_t* Xt, 
           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
     return LPQT_E_INVALID_INPUT;
-  auto kern = w6a16_tcgen05_kernel<BN, RAGGED>;
-  constexpr int smem = Cfg<BN>::kSmemBytes;
+  auto kern = w6a16_tcgen05_kernel<BN, CSK, RAGGED>;
+  constexpr int smem = Cfg<BN, CSK>::kSmemBytes;
   static std::once_flag once;
   static cudaError_t attr_err = cudaSuccess;
   std::call_once(once, [&] {
@@ -853,23 +1046,27 @@ static int launch_impl(const Plan& p, const GemmArgs& args, const uint16_t* Xt, 
   cfg.blockDim = dim3(kThreads);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = stream;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cudaLaunchAttribute attr[2];
+  int na = 0;
+  if (flags & LPQT_LAUNCH_PDL) {
+    attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[na].val.programmaticStreamSerializationAllowed = 1;
+    ++na;
+  }
+  if (CSK) {
+    attr[na].id = cudaLaunchAttributeClusterDimension;
+    attr[na].val.clusterDim.x = p.cluster;
+    attr[na].val.clusterDim.y = 1;
+    attr[na].val.clusterDim.z = 1;
+    ++na;
+  }
   cfg.attrs = attr;
-  cfg.numAttrs = (flags & LPQT_LAUNCH_PDL) ? 1 : 0;
-  if (cudaLaunchKernelEx(&cfg, kern, map, args) != cudaSuccess) return LPQT_E_CUDA;
+  cfg.numAttrs = na;
+  GemmArgs a2 = args;
+  a2.csk_c = CSK ? p.cluster : 0;
+  if (cudaLaunchKernelEx(&cfg, kern, map, a2) != cudaSuccess) return LPQT_E_CUDA;
   note_launch();
   return check_launch();
-}
-
-template <int BN>
-static int launch(const Plan& p, const GemmArgs& args, const uint16_t* Xt, int64_t ldx, int64_t M,
-                  cudaStream_t stream, int flags) {
-  if constexpr (Cfg<BN>::kKStep > 1) {
-    if (p.k_tiles % Cfg<BN>::kKStep != 0) return launch_impl<BN, true>(p, args, Xt, ldx, M, stream, flags);
-  }
-  return launch_impl<BN, false>(p, args, Xt, ldx, M, stream, flags);
 }
 
 }  // namespace lpqt
@@ -879,9 +1076,21 @@ using namespace lpqt;
 extern "C" {
 
 #ifdef LPQT_TRACE
-int lpqt_trace_dump(long long* host) {
+int lpqt_trace_dump(long long* host) {  // the last launch's record
   cudaDeviceSynchronize();
-  return cudaMemcpy(host, trace_buffer(), kTraceLen * sizeof(long long), cudaMemcpyDeviceToHost) == cudaSuccess
+  const int slot = (g_trace_n + kTraceSlots - 1) % kTraceSlots;
+  return cudaMemcpy(host, trace_buffer() + (size_t)slot * kTraceLen, kTraceLen * sizeof(long long),
+                    cudaMemcpyDeviceToHost) == cudaSuccess
+             ? 0
+             : -1;
+}
+// all kTraceSlots records (launch n -> record n % kTraceSlots); returns the
+// number of launches traced so far
+int lpqt_trace_dump_all(long long* host, int* n_launches) {
+  cudaDeviceSynchronize();
+  if (n_launches) *n_launches = g_trace_n;
+  return cudaMemcpy(host, trace_buffer(), (size_t)kTraceSlots * kTraceLen * sizeof(long long),
+                    cudaMemcpyDeviceToHost) == cudaSuccess
              ? 0
              : -1;
 }
@@ -889,21 +1098,31 @@ int lpqt_trace_dump(long long* host) {
 
 int64_t lpqt_w6a16_workspace_bytes(int64_t M, int64_t N, int64_t K, int split_k) {
   if (M <= 0 || N <= 0 || K <= 0) return 0;
-  return make_plan(M, N, K, split_k, num_sms()).ws_bytes;
+  // the largest any schedule of this shape may need (auto or forced stream-K)
+  const Plan p0 = make_plan(M, N, K, split_k, 0, num_sms());
+  const Plan p1 = make_plan(M, N, K, split_k, LPQT_SCHED_STREAMK, num_sms());
+  return p0.ws_bytes > p1.ws_bytes ? p0.ws_bytes : p1.ws_bytes;
 }
 
-// Reports the plan: block_n = MMA N, splits = max CTAs sharing one tile
-// (stream-K), grid = CTAs, stages = smem pipeline depth.
-int lpqt_w6a16_plan(int64_t M, int64_t N, int64_t K, int split_k, int* block_n, int* splits, int* grid, int* stages) {
+int lpqt_w6a16_plan_ex(int64_t M, int64_t N, int64_t K, int split_k, int flags, int* out, int n_out) {
   if (M <= 0 || N <= 0 || K <= 0) return LPQT_E_SHAPE;
-  const Plan p = make_plan(M, N, K, split_k, num_sms());
-  if (block_n) *block_n = p.bn;
-  if (splits) {
-    const int64_t per = p.total / p.grid;  // k-steps per CTA (floor)
-    *splits = p.partials ? static_cast<int>((p.ksteps + (per > 0 ? per : 1) - 1) / (per > 0 ? per : 1) + 1) : 1;
-  }
-  if (grid) *grid = p.grid;
-  if (stages) *stages = p.stages;
+  if ((flags & LPQT_SCHED_STREAMK) && (flags & LPQT_SCHED_CLUSTER)) return LPQT_E_INVALID_INPUT;
+  const Plan p = make_plan(M, N, K, split_k, flags, num_sms());
+  const int v[6] = {p.bn, p.splits, p.grid, p.stages, p.csk ? 1 : 0, p.csk ? p.cluster : 0};
+  for (int i = 0; i < n_out && i < 6; ++i) out[i] = v[i];
+  return LPQT_OK;
+}
+
+// Reports the plan: block_n = MMA N, splits = max CTAs sharing one tile,
+// grid = CTAs, stages = smem pipeline depth.
+int lpqt_w6a16_plan(int64_t M, int64_t N, int64_t K, int split_k, int* block_n, int* splits, int* grid, int* stages) {
+  int v[4];
+  const int st = lpqt_w6a16_plan_ex(M, N, K, split_k, 0, v, 4);
+  if (st != LPQT_OK) return st;
+  if (block_n) *block_n = v[0];
+  if (splits) *splits = v[1];
+  if (grid) *grid = v[2];
+  if (stages) *stages = v[3];
   return LPQT_OK;
 }
 
@@ -917,7 +1136,8 @@ int lpqt_w6a16_linear(const uint8_t* tiles, const uint16_t* scales, const uint16
 int lpqt_w6a16_linear_ex(const uint8_t* tiles, const uint16_t* scales, const uint16_t* Xt, int64_t ldx, int64_t M,
                          int64_t N, int64_t K, void* Y, int y_dtype, int y_layout, int64_t ldy, int split_k,
                          void* workspace, int64_t workspace_bytes, int flags, void* stream) {
-  if (flags & ~LPQT_LAUNCH_PDL) return LPQT_E_INVALID_INPUT;
+  if (flags & ~(LPQT_LAUNCH_PDL | LPQT_SCHED_STREAMK | LPQT_SCHED_CLUSTER)) return LPQT_E_INVALID_INPUT;
+  if ((flags & LPQT_SCHED_STREAMK) && (flags & LPQT_SCHED_CLUSTER)) return LPQT_E_INVALID_INPUT;
   if (M < 0 || N < 0 || K < 0) return LPQT_E_SHAPE;
   if (M == 0 || N == 0) return LPQT_OK;
   if (K == 0) return LPQT_E_SHAPE;  // callers zero-fill (gemm.py:74-75)
@@ -927,11 +1147,11 @@ int lpqt_w6a16_linear_ex(const uint8_t* tiles, const uint16_t* scales, const uin
   if (y_layout == LPQT_Y_NM ? ldy < M : ldy < N) return LPQT_E_SHAPE;
   if (split_k < 0) return LPQT_E_INVALID_INPUT;
   if (N > (int64_t)1 << 30 || M > (int64_t)1 << 30 || K > (int64_t)1 << 30) return LPQT_E_SHAPE;
-  const Plan p = make_plan(M, N, K, split_k, num_sms());
+  const Plan p = make_plan(M, N, K, split_k, flags, num_sms());
   if (p.ws_bytes > 0 && (workspace == nullptr || workspace_bytes < p.ws_bytes)) return LPQT_E_WORKSPACE;
   GemmArgs args{};
 #ifdef LPQT_TRACE
-  args.trace = trace_buffer();
+  args.trace = trace_buffer() + (size_t)trace_next_slot() * kTraceLen;
 #endif
   args.tiles = tiles;
   args.scales = scales;
@@ -946,16 +1166,31 @@ int lpqt_w6a16_linear_ex(const uint8_t* tiles, const uint16_t* scales, const uin
   args.ksteps = p.ksteps;
   args.n_tiles = p.n_tiles;
   args.m_tiles = p.m_tiles;
+  args.tile_count = static_cast<int>(p.tiles);
   args.y_dtype = y_dtype;
   args.y_layout = y_layout;
   args.sm = ShiftMuls{1u << 26, 1u << 28, 1u << 30};
   cudaStream_t st = as_stream(stream);
+  bool ragged = p.k_tiles % p.kstep != 0;
+  if (p.csk) {
+    for (int r = 0; r < p.cluster; ++r)  // k-range of rank r must be a whole number of stages
+      ragged |= ((r + 1) * p.k_tiles / p.cluster - r * p.k_tiles / p.cluster) % p.kstep != 0;
+    if (p.bn <= 16)
+      return ragged ? launch_impl<16, true, true>(p, args, Xt, ldx, M, st, flags)
+                    : launch_impl<16, true, false>(p, args, Xt, ldx, M, st, flags);
+    return ragged ? launch_impl<32, true, true>(p, args, Xt, ldx, M, st, flags)
+                  : launch_impl<32, true, false>(p, args, Xt, ldx, M, st, flags);
+  }
   switch (p.bn) {
-    case 16: return launch<16>(p, args, Xt, ldx, M, st, flags);
-    case 32: return launch<32>(p, args, Xt, ldx, M, st, flags);
-    case 64: return launch<64>(p, args, Xt, ldx, M, st, flags);
-    case 128: return launch<128>(p, args, Xt, ldx, M, st, flags);
-    default: return launch<256>(p, args, Xt, ldx, M, st, flags);
+    case 16:
+      return ragged ? launch_impl<16, false, true>(p, args, Xt, ldx, M, st, flags)
+                    : launch_impl<16, false, false>(p, args, Xt, ldx, M, st, flags);
+    case 32:
+      return ragged ? launch_impl<32, false, true>(p, args, Xt, ldx, M, st, flags)
+                    : launch_impl<32, false, false>(p, args, Xt, ldx, M, st, flags);
+    case 64: return launch_impl<64, false, false>(p, args, Xt, ldx, M, st, flags);
+    case 128: return launch_impl<128, false, false>(p, args, Xt, ldx, M, st, flags);
+    default: return launch_impl<256, false, false>(p, args, Xt, ldx, M, st, flags);
   }
 }
 

@@ -28,8 +28,11 @@ def _check_activation(X, k: int) -> None:
         raise ShapeError(f"inner dimensions differ: weights K={k}, activations K={X.shape[0]}")
 
 
-def gemm_quantized(wq: QuantizedTensor, X, split_k: int = 0):
-    """Y = W_hat @ X for a CGQ FP6 tensor (N x K) and X (K x M) -> f32 (N x M)."""
+def gemm_quantized(wq: QuantizedTensor, X, split_k: int = 0, sched: str = "auto"):
+    """Y = W_hat @ X for a CGQ FP6 tensor (N x K) and X (K x M) -> f32 (N x M).
+
+    `split_k` / `sched` are B200 tuning hooks (default: automatic schedule);
+    the result is the same up to fp32 summation order."""
     if wq.num_blocks != num_blocks(wq.rows, wq.cols, wq.scheme):
         raise PayloadMismatch("block parameter count does not match the scheme")
     torch_in = _lib.is_torch(X)
@@ -43,7 +46,7 @@ def gemm_quantized(wq: QuantizedTensor, X, split_k: int = 0):
         return np.zeros((n, m), dtype=np.float32)
     weight = Fp6Weight.from_quantized(wq)
     xt, kp = stage_activations(Xa, k)
-    y = gemm_nm(weight, xt, kp, m, split_k=split_k)
+    y = gemm_nm(weight, xt, kp, m, split_k=split_k, sched=sched)
     return y if torch_in else y.cpu().numpy()
 
 

@@ -106,19 +106,31 @@ class Fp6Weight:
         return out
 
 
-def plan(m: int, n: int, k: int, split_k: int = 0) -> dict:
-    """The launch plan the library picks: block_n (MMA N), splits, grid, stages."""
+_SCHED_FLAGS = {"auto": 0, "streamk": 2, "cluster": 4}
+
+
+def _sched_flags(sched: str) -> int:
+    if sched not in _SCHED_FLAGS:
+        raise ValueError(f"sched must be one of {sorted(_SCHED_FLAGS)}")
+    return _SCHED_FLAGS[sched]
+
+
+def plan(m: int, n: int, k: int, split_k: int = 0, sched: str = "auto") -> dict:
+    """The launch plan the library picks: block_n (MMA N), splits (CTAs per
+    tile), grid, stages, schedule ("streamk" / "cluster") and cluster size."""
     import ctypes
-    vals = [ctypes.c_int(0) for _ in range(4)]
-    _lib.check(_lib.load().lpqt_w6a16_plan(m, n, k, split_k, *[ctypes.addressof(v) for v in vals]), "plan")
-    return dict(zip(("block_n", "splits", "grid", "stages"), (v.value for v in vals)))
+    out = (ctypes.c_int * 6)()
+    _lib.check(_lib.load().lpqt_w6a16_plan_ex(m, n, k, split_k, _sched_flags(sched), out, 6), "plan")
+    return {"block_n": out[0], "splits": out[1], "grid": out[2], "stages": out[3],
+            "schedule": "cluster" if out[4] else "streamk", "cluster": out[5]}
 
 
-def _launch(weight: Fp6Weight, xt, ldx: int, m: int, y, y_dtype: int, y_layout: int, ldy: int, split_k: int):
+def _launch(weight: Fp6Weight, xt, ldx: int, m: int, y, y_dtype: int, y_layout: int, ldy: int, split_k: int,
+            sched: str = "auto"):
     lib = _lib.load()
     ws_bytes = int(lib.lpqt_w6a16_workspace_bytes(m, weight.n, weight.k, split_k))
     ws = _lib.Workspace.get(ws_bytes) if ws_bytes else None
-    flags = _lib.LAUNCH_PDL if weight.static else 0
+    flags = (_lib.LAUNCH_PDL if weight.static else 0) | _sched_flags(sched)
     _lib.check(lib.lpqt_w6a16_linear_ex(
         weight.tiles.data_ptr(), weight.scales.data_ptr(), xt.data_ptr(), ldx, m, weight.n, weight.k,
         y.data_ptr(), y_dtype, y_layout, ldy, split_k, _lib.ptr(ws), ws.numel() if ws is not None else 0,
@@ -143,16 +155,16 @@ def stage_activations(X, k: int):
     return xt, kp
 
 
-def gemm_nm(weight: Fp6Weight, xt, ldx: int, m: int, out=None, split_k: int = 0):
+def gemm_nm(weight: Fp6Weight, xt, ldx: int, m: int, out=None, split_k: int = 0, sched: str = "auto"):
     """Y[N, M] f32 = W_hat @ X in the reference layout (gemm.py:65-94)."""
     t = _lib.torch()
     y = out if out is not None else t.empty((weight.n, m), dtype=t.float32, device=xt.device)
     if m and weight.n:
-        _launch(weight, xt, ldx, m, y, _lib.F32, _lib.Y_NM, m, split_k)
+        _launch(weight, xt, ldx, m, y, _lib.F32, _lib.Y_NM, m, split_k, sched)
     return y
 
 
-def w6a16_linear(x, weight: Fp6Weight, out=None, out_dtype=None, split_k: int = 0):
+def w6a16_linear(x, weight: Fp6Weight, out=None, out_dtype=None, split_k: int = 0, sched: str = "auto"):
     """y = x @ W_hat^T for x[..., K] (CUDA, fp16 preferred) -> y[..., N].
 
     x is the K-major B operand as is when it is contiguous fp16 with K % 8 ==
@@ -181,7 +193,7 @@ def w6a16_linear(x, weight: Fp6Weight, out=None, out_dtype=None, split_k: int = 
         if weight.k == 0:
             y.zero_()
         else:
-            _launch(weight, x2, ldx, m, y, code, _lib.Y_MN, weight.n, split_k)
+            _launch(weight, x2, ldx, m, y, code, _lib.Y_MN, weight.n, split_k, sched)
     return y.reshape(*lead, weight.n)
 
 

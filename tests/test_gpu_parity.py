@@ -225,11 +225,31 @@ def test_gemm_split_k_variants_agree(split_k):
     W = (torch.randn(512, 3072, generator=g, device="cuda") * 0.02).half()
     X = torch.randn(3072, 16, generator=g, device="cuda").half()
     q = L.quantize_tensor(W, CGQ, bias_shift=True)
-    Y = L.gemm_quantized(q, X, split_k=split_k)
+    Y = L.gemm_quantized(q, X, split_k=split_k, sched="streamk")
     Y_ref = (L.dequantize_tensor(q, "bias_shift") @ X.double()).float()
     assert normwise_rel(Y.cpu().numpy(), Y_ref.cpu().numpy()) <= REL_TOL
-    Y2 = L.gemm_quantized(q, X, split_k=split_k)
+    Y2 = L.gemm_quantized(q, X, split_k=split_k, sched="streamk")
     assert torch.equal(Y.view(torch.int32), Y2.view(torch.int32))   # deterministic
+
+
+@pytest.mark.parametrize("cluster", [1, 2, 3, 4, 5, 8])
+@pytest.mark.parametrize("n,k,m", [(512, 3072, 16), (1280, 1000, 5), (4096, 4096, 1), (640, 11008, 32)])
+def test_gemm_cluster_split_k(n, k, m, cluster):
+    """Cluster split-K (DSMEM reduction) against the dequantize-then-matmul
+    oracle, bit-identical on repeat, and consistent with stream-K."""
+    g = torch.Generator(device="cuda").manual_seed(n + k + m + cluster)
+    W = (torch.randn(n, k, generator=g, device="cuda") * 0.02).half()
+    X = torch.randn(k, m, generator=g, device="cuda").half()
+    q = L.quantize_tensor(W, CGQ, bias_shift=True)
+    p = L.plan(m, n, k, cluster, sched="cluster")
+    assert p["schedule"] == "cluster" and p["cluster"] == min(cluster, (k + 127) // 128)
+    Y = L.gemm_quantized(q, X, split_k=cluster, sched="cluster")
+    Y_ref = (L.dequantize_tensor(q, "bias_shift") @ X.double()).float()
+    assert normwise_rel(Y.cpu().numpy(), Y_ref.cpu().numpy()) <= REL_TOL
+    Y2 = L.gemm_quantized(q, X, split_k=cluster, sched="cluster")
+    assert torch.equal(Y.view(torch.int32), Y2.view(torch.int32))   # deterministic
+    Y3 = L.gemm_quantized(q, X, sched="streamk")
+    assert normwise_rel(Y.cpu().numpy(), Y3.cpu().numpy()) <= REL_TOL
 
 
 def test_w6a16_linear_torch_layout():

@@ -20,6 +20,7 @@ ap.add_argument("--shapes", default="8192x28672,22016x4096,4096x4096,57344x8192"
 ap.add_argument("--m", default="16")
 ap.add_argument("--launches", type=int, default=40)
 ap.add_argument("--split", type=int, default=0)
+ap.add_argument("--sched", default="auto")
 a = ap.parse_args()
 l2 = torch.cuda.get_device_properties(0).L2_cache_size
 for shape in a.shapes.split(","):
@@ -36,12 +37,12 @@ for shape in a.shapes.split(","):
         x = torch.randn(m, k, device="cuda").half()
         y = torch.empty(m, n, device="cuda", dtype=torch.float16)
         for w in ws:
-            L.w6a16_linear(x, w, out=y, split_k=a.split)
+            L.w6a16_linear(x, w, out=y, split_k=a.split, sched=a.sched)
         torch.cuda.synchronize()
         graph = torch.cuda.CUDAGraph()
         with torch.cuda.graph(graph):
             for i in range(a.launches):
-                L.w6a16_linear(x, ws[i % copies], out=y, split_k=a.split)
+                L.w6a16_linear(x, ws[i % copies], out=y, split_k=a.split, sched=a.sched)
         graph.replay()
         torch.cuda.synchronize()
         ts = []
@@ -55,8 +56,9 @@ for shape in a.shapes.split(","):
             ts.append(e0.elapsed_time(e1) * 1e3 / a.launches)
         t = sorted(ts)[len(ts) // 2]
         byt = w0.stream_bytes() + 2 * m * k + 2 * m * n
-        print(json.dumps({"lib": os.path.basename(os.environ.get("LPQT_LIB", "default")), "n": n, "k": k, "m": m,
+        print(json.dumps({"lib": os.path.basename(os.environ.get("LPQT_LIB", "default")) + ":" + a.sched,
+                          "n": n, "k": k, "m": m,
                           "copies": copies, "us": round(t, 2), "GBps": round(byt / t / 1e3, 1),
-                          "plan": L.plan(m, n, k, a.split)}), flush=True)
+                          "plan": L.plan(m, n, k, a.split, sched=a.sched)}), flush=True)
     del ws, w0
     torch.cuda.empty_cache()
