@@ -280,3 +280,43 @@ def test_workspace_reuse_across_shapes():
         assert torch.isfinite(y).all()
         assert normwise_rel(y.cpu().numpy(), ref.cpu().numpy()) <= REL_TOL
         outs.append(y)
+
+
+@pytest.mark.parametrize("y_dtype", [torch.float16, torch.bfloat16, torch.float32])
+@pytest.mark.parametrize("n,k,m", [(4096, 4096, 16), (1000, 2048, 3), (22016, 1024, 16), (512, 1024, 32)])
+def test_linear_output_dtypes_and_layouts(n, k, m, y_dtype):
+    """Both output layouts and all output dtypes, with and without the TMA
+    tensor-store epilogue (unaligned row strides fall back to direct stores)."""
+    g = torch.Generator(device="cuda").manual_seed(n + k + m)
+    W = (torch.randn(n, k, generator=g, device="cuda") * 0.02).half()
+    lin = L.Fp6Linear.from_dense(W)
+    q = L.quantize_tensor(W, CGQ, bias_shift=True)
+    W_hat = L.dequantize_tensor(q, "bias_shift")
+    x = torch.randn(m, k, generator=g, device="cuda").half()
+    ref = (W_hat @ x.double().T).T                       # [M, N]
+    y = L.w6a16_linear(x, lin.weight, out_dtype=y_dtype)    # torch layout [M, N]
+    assert y.dtype == y_dtype and y.shape == (m, n)
+    assert normwise_rel(y.double().cpu().numpy(), ref.cpu().numpy()) <= 1e-3 + (8e-3 if y_dtype == torch.bfloat16 else 0)
+    from paper_2312_08583_b200.linear import gemm_nm, stage_activations
+    xt, kp = stage_activations(x.T.contiguous(), k)
+    ynm = gemm_nm(lin.weight, xt, kp, m)                  # reference layout [N, M] f32
+    assert normwise_rel(ynm.T.double().cpu().numpy(), ref.cpu().numpy()) <= 1e-3
+
+
+def test_chained_layers_read_previous_output():
+    """A GEMM whose activations are the previous GEMM's output, launched back
+    to back (programmatic dependent launch): the consumer must see the
+    producer's complete output (TMA-stored tiles included)."""
+    g = torch.Generator(device="cuda").manual_seed(5)
+    W1 = (torch.randn(4096, 4096, generator=g, device="cuda") * 0.02).half()
+    W2 = (torch.randn(2048, 4096, generator=g, device="cuda") * 0.02).half()
+    l1, l2 = L.Fp6Linear.from_dense(W1), L.Fp6Linear.from_dense(W2)
+    x = torch.randn(16, 4096, generator=g, device="cuda").half()
+    for _ in range(3):
+        y1 = l1(x)
+        y2 = l2(y1)
+        torch.cuda.synchronize()
+        r1 = (L.dequantize_tensor(L.quantize_tensor(W1, CGQ, bias_shift=True), "bias_shift") @ x.double().T).T
+        assert normwise_rel(y1.double().cpu().numpy(), r1.cpu().numpy()) <= 1e-3
+        r2 = (L.dequantize_tensor(L.quantize_tensor(W2, CGQ, bias_shift=True), "bias_shift") @ y1.double().T).T
+        assert normwise_rel(y2.double().cpu().numpy(), r2.cpu().numpy()) <= 1e-3

@@ -17,6 +17,7 @@ ap.add_argument("--shapes", default="12288x4096,4096x4096,22016x4096,4096x11008"
 ap.add_argument("--m", type=int, default=16)
 ap.add_argument("--reps", type=int, default=3)
 ap.add_argument("--sched", default="auto")
+ap.add_argument("--graph", action="store_true", help="replay the chain from a CUDA graph (PDL edges back to back)")
 a = ap.parse_args()
 shapes = [tuple(int(v) for v in s.split("x")) for s in a.shapes.split(",")]
 ws, xs, ys = [], [], []
@@ -29,11 +30,22 @@ lib = _lib.load()
 lib.lpqt_trace_dump_all.argtypes = [ctypes.c_void_p, ctypes.c_void_p]
 SLOTS, LEN = 16, 256 * 24
 flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
+if a.graph:
+    for i in range(len(shapes)):  # warm-up (workspace, attributes) before capture
+        L.w6a16_linear(xs[i], ws[i], out=ys[i], sched=a.sched)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        for i in range(len(shapes)):
+            L.w6a16_linear(xs[i], ws[i], out=ys[i], sched=a.sched)
 for rep in range(a.reps):
     flush.sum()  # read-only L2 flush (clean lines)
     torch.cuda.synchronize()
-    for i in range(len(shapes)):
-        L.w6a16_linear(xs[i], ws[i], out=ys[i], sched=a.sched)
+    if a.graph:
+        g.replay()
+    else:
+        for i in range(len(shapes)):
+            L.w6a16_linear(xs[i], ws[i], out=ys[i], sched=a.sched)
     torch.cuda.synchronize()
 buf = (ctypes.c_longlong * (SLOTS * LEN))()
 n = ctypes.c_int(0)

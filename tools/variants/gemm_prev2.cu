@@ -51,13 +51,12 @@
 // consumed by the same party in stage order and no parity wait can skip a
 // phase.
 #include <stdlib.h>
-#include <string.h>
 
 #include <algorithm>
 #include <mutex>
 #include <type_traits>
 
-#include "common.cuh"
+#include "../../paper_2312_08583_b200/csrc/common.cuh"
 
 namespace lpqt {
 
@@ -71,7 +70,7 @@ constexpr int kWarpEpi0 = kWarpMma0 + kMaxMmaWarps;
 constexpr int kThreads = (kWarpEpi0 + kNumEpiWarps) * 32;  // 768
 constexpr int kAColsPerBuf = kTileK / 2;  // 64 columns of packed half2
 constexpr int kTmemCols = 512;
-constexpr int kSmemBudget = 216 * 1024;
+constexpr int kSmemBudget = 200 * 1024;
 constexpr int64_t kMaxCounters = 65536;   // stream-K tile counters (256 KiB)
 constexpr int kMaxCluster = 8;
 
@@ -88,7 +87,6 @@ struct GemmArgs {
   int k_tiles, ksteps, n_tiles, m_tiles, tile_count;
   int y_dtype, y_layout;
   int csk_c;          // CSK: cluster size C (k-split factor)
-  int y_tma;          // Y tiles leave through the TMA tensor store (tmap_y valid)
   ShiftMuls sm;       // 2^26, 2^28, 2^30: right shifts on the FMA pipe (common.cuh)
 };
 
@@ -101,11 +99,7 @@ struct Cfg {
   static constexpr int kXStages = BN <= 16 ? (CSK ? 4 : 6) : (BN <= 128 ? 4 : 2);
   // CSK: two partial staging buffers of 128 x BN fp32 (rounds alternate)
   static constexpr int kStageBufBytes = CSK ? kTileN * BN * 4 : 0;
-  // decode: output tiles staged in smem (two 128 x BN buffers, fp32-sized) and
-  // written by the TMA tensor store, off the epilogue's critical path
-  static constexpr int kYBufBytes = BN <= 32 ? kTileN * BN * 4 : 0;
-  static constexpr int kWStagesRaw =
-      (kSmemBudget - kXStages * kXStageBytes - 2 * kStageBufBytes - 2 * kYBufBytes) / kWStageBytes;
+  static constexpr int kWStagesRaw = (kSmemBudget - kXStages * kXStageBytes - 2 * kStageBufBytes) / kWStageBytes;
   static constexpr int kWStages = (kWStagesRaw > 12 ? 12 : kWStagesRaw) & ~1;  // even: see header
   static constexpr int kStages = kWStages;                  // reported by the plan
   static constexpr int kDBufs = BN <= 128 ? 2 : 1;
@@ -119,8 +113,8 @@ struct Cfg {
   static constexpr int kACols = kTmemCols - kDBufs * kDCols;
   static constexpr int kASlots = ((kACols / kAColsPerBuf) / kKStep) & ~1;  // even
   static constexpr int kBarCount = 2 * kWStages + 2 * kXStages + 2 * kASlots + 2 * kDBufs + 4;
-  static constexpr int kSmemBytes = kXStages * kXStageBytes + kWStages * kWStageBytes + 2 * kStageBufBytes +
-                                    2 * kYBufBytes + 8 * kBarCount + 16;
+  static constexpr int kSmemBytes =
+      kXStages * kXStageBytes + kWStages * kWStageBytes + 2 * kStageBufBytes + 8 * kBarCount + 16;
   static_assert(kWStages >= 2 && kXStages >= 2, "pipeline too shallow");
   static_assert(kMmaWarps == 1 || kXStages % 2 == 0, "X ring slots must keep their issuer");
   static_assert(kSmemBytes <= 227 * 1024, "shared memory");
@@ -328,77 +322,12 @@ __device__ __forceinline__ void cluster_sync_all() {
   asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 
-// ---- output tile staging + TMA tensor store (decode) --------------------------
-__device__ __forceinline__ void fence_proxy_async_smem() {
-  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-}
-__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, uint32_t smem, int c0, int c1) {
-  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(map),
-               "r"(smem), "r"(c0), "r"(c1)
-               : "memory");
-}
-__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void bulk_wait_read() {
-  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
-}
-// 16 scaled values of output row n (tile row rr), columns m0 + c0 .. + 15,
-// into the staged tile in the tensor map's box layout: Y_MN box [BN][128]
-// (n fastest), Y_NM box [128][BN] (m fastest); element type = y_dtype.
-template <int BN>
-__device__ __forceinline__ void ystage_put(const GemmArgs& a, uint32_t buf, int rr, int c0, const float (&v)[16],
-                                           float fs) {
-  if (a.y_layout == LPQT_Y_NM) {
-    const uint32_t row = buf + rr * BN * (a.y_dtype == LPQT_F32 ? 4 : 2) + c0 * (a.y_dtype == LPQT_F32 ? 4 : 2);
-    if (a.y_dtype == LPQT_F32) {
-#pragma unroll
-      for (int j = 0; j < 16; j += 4)
-        asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(row + j * 4), "f"(v[j] * fs),
-                     "f"(v[j + 1] * fs), "f"(v[j + 2] * fs), "f"(v[j + 3] * fs)
-                     : "memory");
-    } else {
-      uint32_t h[8];
-#pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        if (a.y_dtype == LPQT_F16) {
-          const __half2 t = __floats2half2_rn(v[2 * j] * fs, v[2 * j + 1] * fs);
-          h[j] = *reinterpret_cast<const uint32_t*>(&t);
-        } else {
-          const __nv_bfloat162 t = __floats2bfloat162_rn(v[2 * j] * fs, v[2 * j + 1] * fs);
-          h[j] = *reinterpret_cast<const uint32_t*>(&t);
-        }
-      }
-      asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(row), "r"(h[0]), "r"(h[1]), "r"(h[2]),
-                   "r"(h[3])
-                   : "memory");
-      asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(row + 16), "r"(h[4]), "r"(h[5]), "r"(h[6]),
-                   "r"(h[7])
-                   : "memory");
-    }
-  } else {
-    if (a.y_dtype == LPQT_F32) {
-#pragma unroll
-      for (int j = 0; j < 16; ++j)
-        asm volatile("st.shared.f32 [%0], %1;" ::"r"(buf + ((c0 + j) * kTileN + rr) * 4), "f"(v[j] * fs)
-                     : "memory");
-    } else {
-#pragma unroll
-      for (int j = 0; j < 16; ++j) {
-        const uint16_t hv = a.y_dtype == LPQT_F16 ? __half_as_ushort(__float2half_rn(v[j] * fs))
-                                                  : __bfloat16_as_ushort(__float2bfloat16_rn(v[j] * fs));
-        asm volatile("st.shared.u16 [%0], %1;" ::"r"(buf + ((c0 + j) * kTileN + rr) * 2), "h"(hv) : "memory");
-      }
-    }
-  }
-}
-
 // RAGGED: some stage holds fewer than kKStep tiles (the last k-step of a
 // tile when k_tiles % kKStep != 0, or an odd cluster split-K k-range); only
 // then do the dequant warps walk the stage sequence to learn tile counts.
 template <int BN, bool CSK, bool RAGGED>
 __global__ void __launch_bounds__(kThreads, 1)
-    w6a16_tcgen05_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constant__ CUtensorMap tmap_y,
-                         const GemmArgs a) {
+    w6a16_tcgen05_kernel(const __grid_constant__ CUtensorMap tmap_x, const GemmArgs a) {
   using C = Cfg<BN, CSK>;
   constexpr int KS = C::kKStep;
   using Sched = typename std::conditional<CSK, CskSched, SkSched>::type;
@@ -409,8 +338,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint8_t* smem_x = smem_raw;                                           // kXStages x kXStageBytes
   uint8_t* smem_w = smem_x + C::kXStages * C::kXStageBytes;             // kWStages x kWStageBytes
   uint8_t* smem_stg = smem_w + C::kWStages * C::kWStageBytes;           // CSK: 2 x [BN/4][128] float4
-  uint8_t* smem_y = smem_stg + 2 * C::kStageBufBytes;                  // 2 x Y tile (TMA store source)
-  uint64_t* full_w = reinterpret_cast<uint64_t*>(smem_y + 2 * C::kYBufBytes);
+  uint64_t* full_w = reinterpret_cast<uint64_t*>(smem_stg + 2 * C::kStageBufBytes);
   uint64_t* empty_w = full_w + C::kWStages;
   uint64_t* full_x = empty_w + C::kWStages;
   uint64_t* empty_x = full_x + C::kXStages;
@@ -698,10 +626,6 @@ __global__ void __launch_bounds__(kThreads, 1)
     // CSK, one bit per staging buffer: barrier phases to wait for, and
     // whether the buffer has been sent from before
     uint32_t pf_bits = 0u, sf_bits = 0u, sent_bits = 0u;
-    // Y tiles: staged in smem and written by the TMA tensor store (decode),
-    // else stored directly; ys_n counts staged tiles (buffer = ys_n & 1)
-    const bool ytma = C::kYBufBytes > 0 && a.y_tma;
-    int ys_n = 0;
     for (int i0 = 0; sc.template seg_at<KS>(a, i0, sg); i0 += sg.len, ++lu) {
       const int d = lu % C::kDBufs;
       const uint32_t dph = (lu / C::kDBufs) & 1;
@@ -710,35 +634,6 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int m0 = m_tile * BN;
       const float fs = n < a.N ? __half2float(__ushort_as_half(a.scales[n])) : 0.f;
       const uint32_t t_d = t_lane + d * C::kDCols;
-      const uint32_t ybuf = smem_u32(smem_y) + (ys_n & 1) * C::kYBufBytes;
-      auto y_begin = [&]() {  // the staging buffer must have been read by its last TMA store
-        if (ytma && ys_n >= 2) {
-          if (warp == kWarpEpi0 && lane == 0) bulk_wait_read<1>();
-          named_bar_sync(1, kNumEpiWarps * 32);
-        }
-      };
-      auto y_chunk = [&](int c0, const float (&v)[16]) {
-        if (ytma) {
-          ystage_put<BN>(a, ybuf, rr, c0, v, fs);
-        } else {
-#pragma unroll
-          for (int j = 0; j < 16; ++j) store_y(a, n, m0 + c0 + j, v[j] * fs);
-        }
-      };
-      auto y_end = [&]() {
-        if (!ytma) return;
-        fence_proxy_async_smem();
-        named_bar_sync(1, kNumEpiWarps * 32);
-        if (warp == kWarpEpi0 && lane == 0) {
-          if (a.y_layout == LPQT_Y_NM) {
-            tma_store_2d(&tmap_y, ybuf, m_tile * BN, n_tile * kTileN);
-          } else {
-            tma_store_2d(&tmap_y, ybuf, n_tile * kTileN, m_tile * BN);
-          }
-          bulk_commit();
-        }
-        ++ys_n;
-      };
       // accumulators written for this segment: both issuers when it spans >= 2
       // stages, else only the issuer of the single stage's parity
       const int nacc = min(C::kNAcc, sg.len);
@@ -797,7 +692,6 @@ __global__ void __launch_bounds__(kThreads, 1)
             mbar_wait_cluster(smem_u32(&part_full[b]), (pf_bits >> b) & 1u);
             pf_bits ^= 1u << b;
           }
-          y_begin();
 #pragma unroll
           for (int c0 = 0; c0 < BN; c0 += 16) {
             float sum[16];
@@ -820,9 +714,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                 }
               }
             }
-            y_chunk(c0, sum);
+#pragma unroll
+            for (int j = 0; j < 16; ++j) store_y(a, n, m0 + c0 + j, sum[j] * fs);
           }
-          y_end();
           if (sc.C > 1) {
             // the senders' staging buffers are read: hand them back
             named_bar_sync(1, kNumEpiWarps * 32);
@@ -831,7 +725,6 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
       } else if (sg.full) {
-        y_begin();
 #pragma unroll 1
         for (int c0 = 0; c0 < BN; c0 += 16) {
           float acc[16];
@@ -841,9 +734,9 @@ __global__ void __launch_bounds__(kThreads, 1)
             __syncwarp();
             if (lane == 0) mbar_arrive(&dempty[d]);
           }
-          y_chunk(c0, acc);
+#pragma unroll
+          for (int j = 0; j < 16; ++j) store_y(a, n, m0 + c0 + j, acc[j] * fs);
         }
-        y_end();
       } else {
         // ---- stream-K partial tile
         float* part = a.partials + (((int64_t)blockIdx.x * 2 + sg.pidx) * kTileN + rr) * BN;
@@ -878,7 +771,6 @@ __global__ void __launch_bounds__(kThreads, 1)
           // range before the tile (slot 1 = its last segment); every later
           // contributor starts inside the tile (slot 0 = its first segment)
           const int idx_first = (sk_begin(a, c_first) >= p_first) ? 0 : 1;
-          y_begin();
 #pragma unroll 1
           for (int c0 = 0; c0 < BN; c0 += 16) {
             float acc[16];
@@ -917,16 +809,15 @@ __global__ void __launch_bounds__(kThreads, 1)
                 }
               }
             }
-            y_chunk(c0, acc);
+#pragma unroll
+            for (int j = 0; j < 16; ++j) store_y(a, n, m0 + c0 + j, acc[j] * fs);
           }
-          y_end();
           if (warp == kWarpEpi0 && lane == 0) a.counters[sg.tile] = 0;
           if (last_seg && warp == kWarpEpi0 && lane == 0) CTA_STAMP(11);
         }
         named_bar_sync(1, kNumEpiWarps * 32);
       }
     }
-    if (ytma && warp == kWarpEpi0 && lane == 0) bulk_wait_read<0>();  // smem stays valid until read
     if (warp == kWarpEpi0 && lane == 0) CTA_STAMP(5);
   }
 
@@ -1173,29 +1064,7 @@ static int launch_impl(const Plan& p, const GemmArgs& args, const uint16_t* Xt, 
   cfg.numAttrs = na;
   GemmArgs a2 = args;
   a2.csk_c = CSK ? p.cluster : 0;
-  // Y tensor map for the TMA store epilogue (decode tiles); shapes the TMA
-  // cannot describe (unaligned base / row stride) keep the direct stores
-  CUtensorMap ymap;
-  memset(&ymap, 0, sizeof(ymap));
-  a2.y_tma = 0;
-  if (Cfg<BN, CSK>::kYBufBytes > 0) {
-    const int es = args.y_dtype == LPQT_F32 ? 4 : 2;
-    const CUtensorMapDataType dt = args.y_dtype == LPQT_F32   ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32
-                                   : args.y_dtype == LPQT_F16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16
-                                                              : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
-    const bool nm = args.y_layout == LPQT_Y_NM;
-    const cuuint64_t ydims[2] = {static_cast<cuuint64_t>(nm ? args.M : args.N),
-                                 static_cast<cuuint64_t>(nm ? args.N : args.M)};
-    const cuuint64_t ystr[1] = {static_cast<cuuint64_t>(args.ldy) * es};
-    const cuuint32_t ybox[2] = {static_cast<cuuint32_t>(nm ? BN : kTileN), static_cast<cuuint32_t>(nm ? kTileN : BN)};
-    const bool ok = (reinterpret_cast<uintptr_t>(args.y) % 16 == 0) && (ystr[0] % 16 == 0) &&
-                    ((cuuint64_t)ybox[0] * es) % 16 == 0 && ydims[1] > 1;
-    if (ok && enc(&ymap, dt, 2, args.y, ydims, ystr, ybox, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                  CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
-                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS)
-      a2.y_tma = 1;
-  }
-  if (cudaLaunchKernelEx(&cfg, kern, map, ymap, a2) != cudaSuccess) return LPQT_E_CUDA;
+  if (cudaLaunchKernelEx(&cfg, kern, map, a2) != cudaSuccess) return LPQT_E_CUDA;
   note_launch();
   return check_launch();
 }
