@@ -1038,21 +1038,26 @@ static Plan make_plan(int64_t M, int64_t N, int64_t K, int split_k, int flags, i
       best_c = split_k > 0 ? split_k : 1;
       best_c = std::min(best_c, std::min(kMaxCluster, p.k_tiles));
     } else if (split_k == 0) {
-      // Time model of one launch (us, measured on B200, tools/abx.py): a CTA
-      // streams its weights at ~40 GB/s; stream-K pays ~6 us of cross-CTA
-      // fixups on its tail when tiles are split, cluster split-K ~1.5 us of
-      // DSMEM reduction per round.  Only C = 2 is chosen automatically:
-      // larger clusters measured slower than this model predicts.
-      const double tile_us = (double)kTileBytes / 40e3;   // one 128x128 weight tile
-      const double sk_splits = (double)p.tiles * p.k_tiles / sms;  // k-tiles per CTA
-      const bool sk_partial = (p.tiles % sms) != 0;
-      const double sk_us = sk_splits * tile_us + (sk_partial ? 6.0 : 0.0);
-      const int c = 2;
-      if (p.k_tiles >= c) {
+      // Time model of one launch (us; fitted to B200 measurements of both
+      // schedules on the LLaMA shapes, tools/abx.py, profiles/): a CTA
+      // streams one 128x128 FP6 tile in ~0.31 us; stream-K pays ~3-6 us of
+      // cross-CTA fixups on its tail when tiles are split; cluster split-K
+      // ~0.7 us of DSMEM reduction per round plus ~0.5 us of cluster
+      // launch/sync.  Only C <= 2 is chosen automatically (larger clusters
+      // measured slower than the model predicts).
+      const double tile_us = 0.31;
+      const double sk_kt = (double)p.tiles * p.k_tiles / sms;  // k-tiles per CTA
+      const bool sk_partial = ((int64_t)p.tiles * p.k_tiles) % sms != 0 || p.tiles % sms != 0;
+      // (long per-CTA ranges hide part of the fixup tail)
+      double best = sk_kt * tile_us + (sk_partial ? (sk_kt < 64.0 ? 6.0 : 3.0) : 0.0);
+      for (int c = 1; c <= 2 && c <= p.k_tiles; ++c) {
         const int64_t ncl = std::min<int64_t>(max_clusters_bn(p.bn, c), p.tiles);
         const int64_t rounds = (p.tiles + ncl - 1) / ncl;
-        const double csk_us = rounds * (((p.k_tiles + c - 1) / c) * tile_us + 1.5);
-        if (csk_us < sk_us) best_c = c;
+        const double us = rounds * (((p.k_tiles + c - 1) / c) * tile_us + (c > 1 ? 0.7 : 0.0)) + (c > 1 ? 0.5 : 0.0);
+        if (us < best) {
+          best = us;
+          best_c = c;
+        }
       }
     }
   }
