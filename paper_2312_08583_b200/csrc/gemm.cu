@@ -625,6 +625,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       ac.adv2(C::kASlots);
     }
     if (warp == 0 && lane == 0) CTA_STAMP(3);
+    if (warp == 8 && lane == 0) CTA_STAMP(16);
   } else if (warp < kWarpEpi0) {
     // ------------------------------------------------------------ MMA issue
     // issuer mw takes the local stages of parity mw into accumulator mw; a
@@ -684,14 +685,28 @@ __global__ void __launch_bounds__(kThreads, 1)
         ++lu;
       }
       if (mw == 0 && lane == 0) CTA_STAMP(4);
+      if (mw == 1 && lane == 0) CTA_STAMP(15);
     }
   } else {
     // ------------------------------------------------------------ epilogue
     setmaxnreg_dec<72>();
-    if constexpr (CSK) cluster_wait();
-    pdl_wait();  // Y / workspace writes: the preceding grid must be complete
     const int lg = warp & 3;
     const int rr = lg * 32 + lane;  // row inside the 128-row tile (= TMEM lane)
+    // Row scales are weights (never written by the preceding kernel): the
+    // first segment's is loaded before any wait, each next one a segment
+    // ahead, so no global load sits on the epilogue's critical path (a cold
+    // load behind the weight stream costs microseconds).
+    auto scale_of = [&](const Seg& g) -> uint16_t {
+      const int nn = (g.tile / a.m_tiles) * kTileN + rr;
+      return nn < a.N ? __ldg(a.scales + nn) : static_cast<uint16_t>(0);
+    };
+    Seg sg_next;
+    bool have_next = sc.template seg_at<KS>(a, 0, sg_next);
+    uint16_t fs_next = have_next ? scale_of(sg_next) : static_cast<uint16_t>(0);
+    if constexpr (CSK) cluster_wait();
+    if (warp == kWarpEpi0 && lane == 0) CTA_STAMP(17);
+    pdl_wait();  // Y / workspace writes: the preceding grid must be complete
+    if (warp == kWarpEpi0 && lane == 0) CTA_STAMP(18);
     const uint32_t t_lane = tmem_d0 + (static_cast<uint32_t>(lg * 32) << 16);
     Seg sg;
     int lu = 0;
@@ -702,13 +717,16 @@ __global__ void __launch_bounds__(kThreads, 1)
     // else stored directly; ys_n counts staged tiles (buffer = ys_n & 1)
     const bool ytma = C::kYBufBytes > 0 && a.y_tma;
     int ys_n = 0;
-    for (int i0 = 0; sc.template seg_at<KS>(a, i0, sg); i0 += sg.len, ++lu) {
+    for (; have_next; ++lu) {
+      sg = sg_next;
+      const float fs = __half2float(__ushort_as_half(fs_next));
+      have_next = sc.template seg_at<KS>(a, sg.i0 + sg.len, sg_next);
+      if (have_next) fs_next = scale_of(sg_next);
       const int d = lu % C::kDBufs;
       const uint32_t dph = (lu / C::kDBufs) & 1;
       const int n_tile = sg.tile / a.m_tiles, m_tile = sg.tile % a.m_tiles;
       const int n = n_tile * kTileN + rr;
       const int m0 = m_tile * BN;
-      const float fs = n < a.N ? __half2float(__ushort_as_half(a.scales[n])) : 0.f;
       const uint32_t t_d = t_lane + d * C::kDCols;
       const uint32_t ybuf = smem_u32(smem_y) + (ys_n & 1) * C::kYBufBytes;
       auto y_begin = [&]() {  // the staging buffer must have been read by its last TMA store
