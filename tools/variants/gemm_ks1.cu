@@ -57,7 +57,7 @@
 #include <mutex>
 #include <type_traits>
 
-#include "common.cuh"
+#include "../../paper_2312_08583_b200/csrc/common.cuh"
 
 namespace lpqt {
 
@@ -94,7 +94,7 @@ struct GemmArgs {
 
 template <int BN, bool CSK>
 struct Cfg {
-  static constexpr int kKStep = BN <= 32 ? 2 : 1;           // 128-k tiles per pipeline stage
+  static constexpr int kKStep = BN <= 32 && BN != 16 ? 2 : 1;
   static constexpr int kXTileBytes = BN * kTileK * 2;       // X for one tile: two SW128 blocks
   static constexpr int kWStageBytes = kKStep * kTileBytes;
   static constexpr int kXStageBytes = kKStep * kXTileBytes;
@@ -593,33 +593,15 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     if (warp == 0 && lane == 0) CTA_STAMP(12);
     for (int i = grp; i < n_st; i += 2) {
-      // the first segment is rebuilt before the wait for the TMEM slot, so
-      // half the ALU work overlaps the MMAs still reading the slot
-      const bool act = KS == 1 || tl < nt_cur;
-      uint32_t r[32];
-#ifndef LPQT_EXP_NO_REBUILD
-      if (act) {
-        fp6x32_cvt_f16x32_fma(q[0], r, sm);
-        fp6x32_cvt_f16x32_fma(q[0] + 6, r + 16, sm);
-      }
-#else
-#pragma unroll
-      for (int j = 0; j < 32; ++j) r[j] = q[0][j % 12];
-#endif
       mbar_wait_u32(ae0 + 8 * ac.idx, ac.ph ^ 1u);
       tc_fence_after();
-      if (act) {
+      if (KS == 1 || tl < nt_cur) {
         const uint32_t ta = t_lane + ac.idx * (KS * kAColsPerBuf);
-        tmem_st_x32(ta, r);
 #pragma unroll
-        for (int h = 1; h < kSegs; ++h) {
-#ifndef LPQT_EXP_NO_REBUILD
+        for (int h = 0; h < kSegs; ++h) {
+          uint32_t r[32];
           fp6x32_cvt_f16x32_fma(q[h], r, sm);
           fp6x32_cvt_f16x32_fma(q[h] + 6, r + 16, sm);
-#else
-#pragma unroll
-          for (int j = 0; j < 32; ++j) r[j] = q[h][j % 12];
-#endif
           tmem_st_x32(ta + h * 32, r);
         }
       }
@@ -687,13 +669,8 @@ __global__ void __launch_bounds__(kThreads, 1)
               for (int j = 0; j < kTileK / 16; ++j) {
                 const uint32_t off = (t * C::kXTileBytes + (j >> 2) * (BN * 128) + (j & 3) * 32) >> 4;
                 const bool init = first && t == 0 && j == 0;
-#ifndef LPQT_EXP_NO_MMA
                 mma_f16_ts_if(e, d_tmem, ta + t * kAColsPerBuf + j * 8, bd_lo + off, bd_hi, idesc,
                               init ? 0u : 1u);
-#else
-                (void)off;
-                (void)init;
-#endif
               }
             }
           }
