@@ -530,21 +530,30 @@ def main():
     # (CUDA events over the timed region, launches back to back)
     achieved = step_bytes(layers, m) / world / t_step / 1e9
     traffic = None
+    traffic_note = None
     tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tp):
         with open(tp) as f:
-            traffic = json.load(f).get(f"{args.model}_m{m}")
+            tr = json.load(f).get(f"{args.model}_m{m}")
+        if tr:
+            # DRAM bytes (read + write) of the step's launches from one
+            # ncu --set full capture, per step like `achieved`
+            traffic = tr["bytes_per_step"] // world
+            traffic_note = {"traffic_over_algorithmic": tr["ratio"], "source": "profiles/ncu_traffic.json: " +
+                            tr["source"]}
     if rank != 0:
         return
     line = {
         "metric": METRIC, "value": round(res["value"], 2), "unit": "GB/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(t_step * 1e3, 5),
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
-        "dtype": "fp16 x fp6(e3m2) -> fp32 accumulate", "data": "synthetic (random-init weights, N(0,1) fp16 X)",
+        "dtype": "fp16", "dtype_detail": "fp6 e3m2 weights rebuilt to fp16, fp16 activations, fp32 accumulate",
+        "data": "synthetic (random-init weights, N(0,1) fp16 X)",
         "config": config,
         "tflops": round(flops / t_step / 1e12, 3),
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peaks["hbm_gbs"], "unit": "GB/s",
                      "frac": round(achieved / peaks["hbm_gbs"], 4), "traffic": traffic,
+                     "traffic_unit": "bytes per step (DRAM read + write, ncu)", "traffic_detail": traffic_note,
                      "peak_source": peaks["source"],
                      "kernel": "w6a16_tcgen05_kernel<16> (all 4 launches of the step, timed region)",
                      "per_launch_serialised": res["per_layer"]},

@@ -1,0 +1,1381 @@
+// gemm.cu — K4/K5/K6: the W6A16 linear on tcgen05 (gemm.py:65-94 CGQ path).
+//
+//   Y[n, m] = S[n] * sum_k V[n, k] * X[m, k]
+//
+// exactly the reference's CGQ algorithm (raw code values V = value_table[c],
+// row scale applied once after the fp32 accumulation, gemm.py:84-88), up to
+// fp32 summation order.  V is rebuilt in registers by the hardware e3m2
+// converter from the tile layout (common.cuh); the paper's bias-shift
+// identity compose[c] * (S * 2^12) == V * S (dequant.py:33-69) means the same
+// result as the folded-scale formulation, bit for bit per element.
+//
+// Output tiles are 128 weight rows x BN batch columns; the contraction runs
+// over "stages" of kKStep 128-k weight tiles.  Two work schedules:
+//
+//  * stream-K (SK): the (tile, k-step) space is cut into gridDim.x equal
+//    contiguous ranges, one per persistent CTA (1 per SM).  A tile cut
+//    between CTAs is finished by whichever contributor arrives last (global
+//    fp32 partials + an acq_rel tile counter), summing the partials in a fixed
+//    order.  Perfect balance; the cross-CTA fixups cost global round trips.
+//    Used when there are many tiles (prefill, big N).
+//  * cluster split-K (CSK): CTAs form clusters of C (C <= 8); cluster j
+//    takes tiles j, j + #clusters, ... ("rounds"), and rank r of the cluster
+//    contracts k-tiles [r KT / C, (r + 1) KT / C) of each.  The C partial
+//    accumulators of a tile meet in shared memory over DSMEM: every
+//    non-reducer stages its fp32 partial in its own smem and signals the
+//    round's reducer (rank round % C) through a cluster-scope mbarrier; the
+//    reducer reads the partials with ld.shared::cluster, sums them in rank
+//    order (deterministic), scales and stores Y, and hands the staging
+//    buffers back.  No global atomics, no L2 round trips on the tail.  Used
+//    for decode when the tile count is small.
+//
+// Per CTA (768 threads), warp-specialised:
+//   warp 16     W producer: per stage one 1-D bulk copy of the stage's
+//               consecutive 12288-B weight tiles (evict-first); starts at
+//               once, before the preceding kernel finishes (PDL).
+//   warp 17     X producer: 2-D TMA boxes of X (64 k x BN rows, 128-B
+//               swizzle; rows >= M, k >= K read 0) after griddepcontrol.wait.
+//   warps 0-15  dequant (DQ): two groups of 8 warps on alternate stages;
+//               LDS of the tile layout -> FP6->FP16 rebuild (hardware e3m2
+//               converter + spare-bit gather) -> tcgen05.st into the stage's
+//               TMEM A slot (128 lanes = weight rows, 64 half2 columns per
+//               128-k tile).
+//   warps 18-19 MMA issuers (2 for N <= 64, alternate stages, one
+//               accumulator each): tcgen05.mma.kind::f16, A in TMEM ("TS"),
+//               B = X from SMEM, D (fp32, 128 x BN) in TMEM.
+//   warps 20-23 epilogue: tcgen05.ld D (accumulators summed in fixed order)
+//               -> x S -> Y, or the split-K reduction.
+// Pipelines: W ring (W producer <-> DQ), X ring (X producer <-> MMA commit),
+// TMEM-A ring (DQ <-> MMA commit), TMEM-D ring (MMA <-> epilogue).  Rings
+// are even-sized where two parties alternate stages, so every slot is always
+// consumed by the same party in stage order and no parity wait can skip a
+// phase.
+#include <stdlib.h>
+#include <string.h>
+
+#include <algorithm>
+#include <mutex>
+#include <type_traits>
+
+#include "../../paper_2312_08583_b200/csrc/common.cuh"
+
+namespace lpqt {
+
+constexpr int kNumDqWarps = 16;
+constexpr int kNumEpiWarps = 4;
+constexpr int kMaxMmaWarps = 2;
+constexpr int kWarpTmaW = kNumDqWarps;       // weight-tile producer
+constexpr int kWarpTmaX = kNumDqWarps + 1;   // activation producer
+constexpr int kWarpMma0 = kNumDqWarps + 2;
+constexpr int kWarpEpi0 = kWarpMma0 + kMaxMmaWarps;
+constexpr int kThreads = (kWarpEpi0 + kNumEpiWarps) * 32;  // 768
+constexpr int kAColsPerBuf = kTileK / 2;  // 64 columns of packed half2
+constexpr int kTmemCols = 512;
+constexpr int kSmemBudget = 216 * 1024;
+constexpr int64_t kMaxCounters = 65536;   // stream-K tile counters (256 KiB)
+constexpr int kMaxCluster = 8;
+
+struct GemmArgs {
+  const uint8_t* tiles;
+  const uint16_t* scales;
+  void* y;
+  float* partials;    // SK: [gridDim.x][2][128][BN] fp32 (first / last segment of each CTA)
+  int* counters;      // SK: [tiles] k-steps contributed so far (self-resetting)
+  long long* trace;   // LPQT_TRACE builds only: per-CTA %globaltimer stamps
+  int64_t ldy;
+  int64_t total;      // SK: tiles * ksteps, the stream-K iteration space
+  int M, N;
+  int k_tiles, ksteps, n_tiles, m_tiles, tile_count;
+  int y_dtype, y_layout;
+  int csk_c;          // CSK: cluster size C (k-split factor)
+  int y_tma;          // Y tiles leave through the TMA tensor store (tmap_y valid)
+  ShiftMuls sm;       // 2^26, 2^28, 2^30: right shifts on the FMA pipe (common.cuh)
+};
+
+template <int BN, bool CSK>
+struct Cfg {
+  static constexpr int kKStep = BN <= 32 ? 2 : 1;           // 128-k tiles per pipeline stage
+  static constexpr int kXTileBytes = BN * kTileK * 2;       // X for one tile: two SW128 blocks
+  static constexpr int kWStageBytes = kKStep * kTileBytes;
+  static constexpr int kXStageBytes = kKStep * kXTileBytes;
+  static constexpr int kXStages = BN <= 16 ? (CSK ? 4 : 6) : (BN <= 128 ? 4 : 2);
+  // CSK: two partial staging buffers of 128 x BN fp32 (rounds alternate)
+  static constexpr int kStageBufBytes = CSK ? kTileN * BN * 4 : 0;
+  // decode: output tiles staged in smem (two 128 x BN buffers, fp32-sized) and
+  // written by the TMA tensor store, off the epilogue's critical path
+  static constexpr int kYBufBytes = BN <= 32 ? kTileN * BN * 4 : 0;
+  static constexpr int kWStagesRaw =
+      (kSmemBudget - kXStages * kXStageBytes - 2 * kStageBufBytes - 2 * kYBufBytes) / kWStageBytes;
+  static constexpr int kWStages = (kWStagesRaw > 12 ? 12 : kWStagesRaw) & ~1;  // even: see header
+  static constexpr int kStages = kWStages;                  // reported by the plan
+  static constexpr int kDBufs = BN <= 128 ? 2 : 1;
+  // MMA issue: at small N a tcgen05.mma executes in ~9 cycles while its
+  // single-lane issue sequence takes several times that, so two warps issue
+  // alternate stages, each into its own accumulator; the epilogue sums them
+  // in a fixed order.  Prefill MMAs (N >= 128) are long enough for one.
+#ifdef LPQT_EXP_ONE_ISSUER
+  static constexpr int kMmaWarps = (BN <= 64 && BN != 16) ? 2 : 1;
+#else
+  static constexpr int kMmaWarps = BN <= 64 ? 2 : 1;
+#endif
+  static constexpr int kNAcc = kMmaWarps;
+  static constexpr int kDCols = BN * kNAcc;
+  static constexpr int kACols = kTmemCols - kDBufs * kDCols;
+  // even when two issuers alternate stages (each slot keeps its issuer);
+  // with one issuer MMAs complete in stage order and any depth is safe
+  static constexpr int kASlots = kMmaWarps == 2 ? ((kACols / kAColsPerBuf) / kKStep) & ~1
+                                                : (kACols / kAColsPerBuf) / kKStep;
+  static constexpr int kBarCount = 2 * kWStages + 2 * kXStages + 2 * kASlots + 2 * kDBufs + 4;
+  static constexpr int kSmemBytes = kXStages * kXStageBytes + kWStages * kWStageBytes + 2 * kStageBufBytes +
+                                    2 * kYBufBytes + 8 * kBarCount + 16;
+  static_assert(kWStages >= 2 && kXStages >= 2, "pipeline too shallow");
+  static_assert(kMmaWarps == 1 || kXStages % 2 == 0, "X ring slots must keep their issuer");
+  static_assert(kSmemBytes <= 227 * 1024, "shared memory");
+  static_assert(kASlots >= 2, "A ring too shallow");
+  static_assert(!CSK || BN <= 32, "cluster split-K is the decode schedule");
+};
+
+#ifdef LPQT_TRACE
+// per-CTA %globaltimer stamps: trace[cta * 24 + ev]
+#define CTA_STAMP(ev)                                                   \
+  do {                                                                  \
+    if (a.trace && blockIdx.x < 256) {                                  \
+      uint64_t gt;                                                      \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));            \
+      a.trace[blockIdx.x * 24 + (ev)] = (long long)gt;                  \
+    }                                                                   \
+  } while (0)
+#else
+#define CTA_STAMP(ev) \
+  do {                \
+  } while (0)
+#endif
+constexpr int kTraceLen = 256 * 24;
+
+// ---------------------------------------------------------------------------
+// Work schedules.  Both present the CTA's work as a sequence of segments
+// (one tile, a contiguous k-tile range [kt0, kt1), `len` stages whose local
+// indices start at i0); every role walks the same sequence.
+// ---------------------------------------------------------------------------
+struct Seg {
+  int tile, i0, len, kt0, kt1;
+  bool full;  // SK: the whole tile, no other contributor
+  int pidx;   // SK: partial slot (0 = tile holding the range start, 1 = last tile)
+  int red;    // CSK: reducer rank of this round
+};
+
+// ---- stream-K ------------------------------------------------------------------
+__device__ __forceinline__ int64_t sk_begin(const GemmArgs& a, int c) {
+  return (int64_t)c * a.total / (int64_t)gridDim.x;
+}
+// CTA whose range holds global k-step position p
+__device__ __forceinline__ int sk_cta_of(const GemmArgs& a, int64_t p) {
+  return static_cast<int>(((p + 1) * (int64_t)gridDim.x - 1) / a.total);
+}
+
+// A CTA's stream-K range [beg, end) in natural order; segments never
+// straddle a tile.
+struct SkSched {
+  int64_t beg, end;
+  int n;
+  __device__ __forceinline__ void init(const GemmArgs& a) {
+    beg = sk_begin(a, blockIdx.x);
+    end = sk_begin(a, blockIdx.x + 1);
+    n = static_cast<int>(end - beg);
+  }
+  template <int KS>
+  __device__ __forceinline__ bool seg_at(const GemmArgs& a, int i, Seg& sg) const {
+    if (i >= n) return false;
+    const int64_t p = beg + i;
+    const int t = static_cast<int>(p / a.ksteps);
+    const int s0 = static_cast<int>(p - (int64_t)t * a.ksteps);
+    const int64_t rem = end - p;
+    const int len = rem < (int64_t)(a.ksteps - s0) ? static_cast<int>(rem) : a.ksteps - s0;
+    sg.tile = t;
+    sg.i0 = i;
+    sg.len = len;
+    sg.kt0 = s0 * KS;
+    sg.kt1 = min((s0 + len) * KS, a.k_tiles);
+    sg.full = (s0 == 0 && len == a.ksteps);
+    sg.pidx = (beg >= (int64_t)t * a.ksteps) ? 0 : 1;
+    sg.red = 0;
+    return true;
+  }
+};
+
+// ---- cluster split-K ------------------------------------------------------------
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+
+struct CskSched {
+  int C, rank, cid, ncl, kt0, kt1, len, rounds, n;
+  __device__ __forceinline__ void init(const GemmArgs& a, int ks) {
+    C = a.csk_c;
+    rank = static_cast<int>(cluster_rank());
+    cid = static_cast<int>(blockIdx.x) / C;
+    ncl = static_cast<int>(gridDim.x) / C;
+    kt0 = rank * a.k_tiles / C;
+    kt1 = (rank + 1) * a.k_tiles / C;
+    len = (kt1 - kt0 + ks - 1) / ks;
+    rounds = cid < a.tile_count ? (a.tile_count - 1 - cid) / ncl + 1 : 0;
+    n = rounds * len;
+  }
+  template <int KS>
+  __device__ __forceinline__ bool seg_at(const GemmArgs& a, int i, Seg& sg) const {
+    if (i >= n) return false;
+    const int q = i / len;
+    sg.tile = cid + q * ncl;
+    sg.i0 = i;
+    sg.len = len;
+    sg.kt0 = kt0;
+    sg.kt1 = kt1;
+    sg.full = (C == 1);
+    sg.pidx = 0;
+    sg.red = q % C;
+    return true;
+  }
+};
+
+// Stage walker over the segment sequence (divisions only at segment starts)
+template <class S, int KS>
+struct StageIter {
+  Seg sg;
+  int s;  // stage inside the segment
+  bool ok;
+  __device__ __forceinline__ void start(const GemmArgs& a, const S& sc, int i) {
+    ok = sc.template seg_at<KS>(a, 0, sg);
+    s = 0;
+    while (ok && i >= sg.i0 + sg.len) ok = sc.template seg_at<KS>(a, sg.i0 + sg.len, sg);
+    if (ok) s = i - sg.i0;
+  }
+  __device__ __forceinline__ void next(const GemmArgs& a, const S& sc) {
+    if (++s == sg.len) {
+      ok = sc.template seg_at<KS>(a, sg.i0 + sg.len, sg);
+      s = 0;
+    }
+  }
+  __device__ __forceinline__ int kt() const { return sg.kt0 + s * KS; }
+  __device__ __forceinline__ int nt() const { return min(KS, sg.kt1 - kt()); }
+};
+
+__device__ __forceinline__ int atom_add_acq_rel_gpu(int* p, int v) {
+  int old;
+  asm volatile("atom.add.acq_rel.gpu.s32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+  return old;
+}
+
+__device__ __forceinline__ void store_y(const GemmArgs& a, int n, int m, float v) {
+  if (n >= a.N || m >= a.M) return;
+  const int64_t off = a.y_layout == LPQT_Y_NM ? (int64_t)n * a.ldy + m : (int64_t)m * a.ldy + n;
+  if (a.y_dtype == LPQT_F32) {
+    static_cast<float*>(a.y)[off] = v;
+  } else if (a.y_dtype == LPQT_F16) {
+    static_cast<__half*>(a.y)[off] = __float2half_rn(v);
+  } else {
+    static_cast<__nv_bfloat16*>(a.y)[off] = __float2bfloat16_rn(v);
+  }
+}
+
+// Sum the first `nacc` accumulators over 16 columns [c0, c0+16) (fixed order).
+template <int BN>
+__device__ __forceinline__ void load_acc16(uint32_t t_d, int c0, int q0, int nacc, float (&acc)[16]) {
+  uint32_t v[16];
+  tmem_ld_x16(t_d + q0 * BN + c0, v);
+  tmem_wait_ld();
+#pragma unroll
+  for (int j = 0; j < 16; ++j) acc[j] = __uint_as_float(v[j]);
+#pragma unroll 1
+  for (int q = q0 + 1; q < q0 + nacc; ++q) {
+    tmem_ld_x16(t_d + q * BN + c0, v);
+    tmem_wait_ld();
+#pragma unroll
+    for (int j = 0; j < 16; ++j) acc[j] += __uint_as_float(v[j]);
+  }
+}
+
+// ---- DSMEM / cluster primitives ----------------------------------------------------
+__device__ __forceinline__ uint32_t mapa_shared(uint32_t addr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ float4 ld_dsmem_f4(uint32_t addr) {
+  float4 v;
+  asm volatile("ld.shared::cluster.v4.f32 {%0, %1, %2, %3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "r"(addr)
+               : "memory");
+  return v;
+}
+// arrive (release, cluster scope) on an mbarrier of another CTA of the cluster
+__device__ __forceinline__ void mbar_arrive_remote(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+__device__ __forceinline__ void mbar_wait_cluster(uint32_t addr, uint32_t parity) {
+  uint32_t ok = 0, spins = 0;
+  do {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(addr), "r"(parity)
+        : "memory");
+    if (++spins == (1u << 30)) __trap();
+  } while (!ok);
+}
+__device__ __forceinline__ void cluster_arrive() {
+  asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void cluster_wait() { asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory"); }
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
+// ---- output tile staging + TMA tensor store (decode) --------------------------
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, uint32_t smem, int c0, int c1) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(map),
+               "r"(smem), "r"(c0), "r"(c1)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+// 16 scaled values of output row n (tile row rr), columns m0 + c0 .. + 15,
+// into the staged tile in the tensor map's box layout: Y_MN box [BN][128]
+// (n fastest), Y_NM box [128][BN] (m fastest); element type = y_dtype.
+template <int BN>
+__device__ __forceinline__ void ystage_put(const GemmArgs& a, uint32_t buf, int rr, int c0, const float (&v)[16],
+                                           float fs) {
+  if (a.y_layout == LPQT_Y_NM) {
+    const uint32_t row = buf + rr * BN * (a.y_dtype == LPQT_F32 ? 4 : 2) + c0 * (a.y_dtype == LPQT_F32 ? 4 : 2);
+    if (a.y_dtype == LPQT_F32) {
+#pragma unroll
+      for (int j = 0; j < 16; j += 4)
+        asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(row + j * 4), "f"(v[j] * fs),
+                     "f"(v[j + 1] * fs), "f"(v[j + 2] * fs), "f"(v[j + 3] * fs)
+                     : "memory");
+    } else {
+      uint32_t h[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        if (a.y_dtype == LPQT_F16) {
+          const __half2 t = __floats2half2_rn(v[2 * j] * fs, v[2 * j + 1] * fs);
+          h[j] = *reinterpret_cast<const uint32_t*>(&t);
+        } else {
+          const __nv_bfloat162 t = __floats2bfloat162_rn(v[2 * j] * fs, v[2 * j + 1] * fs);
+          h[j] = *reinterpret_cast<const uint32_t*>(&t);
+        }
+      }
+      asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(row), "r"(h[0]), "r"(h[1]), "r"(h[2]),
+                   "r"(h[3])
+                   : "memory");
+      asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(row + 16), "r"(h[4]), "r"(h[5]), "r"(h[6]),
+                   "r"(h[7])
+                   : "memory");
+    }
+  } else {
+    if (a.y_dtype == LPQT_F32) {
+#pragma unroll
+      for (int j = 0; j < 16; ++j)
+        asm volatile("st.shared.f32 [%0], %1;" ::"r"(buf + ((c0 + j) * kTileN + rr) * 4), "f"(v[j] * fs)
+                     : "memory");
+    } else {
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        const uint16_t hv = a.y_dtype == LPQT_F16 ? __half_as_ushort(__float2half_rn(v[j] * fs))
+                                                  : __bfloat16_as_ushort(__float2bfloat16_rn(v[j] * fs));
+        asm volatile("st.shared.u16 [%0], %1;" ::"r"(buf + ((c0 + j) * kTileN + rr) * 2), "h"(hv) : "memory");
+      }
+    }
+  }
+}
+
+// RAGGED: some stage holds fewer than kKStep tiles (the last k-step of a
+// tile when k_tiles % kKStep != 0, or an odd cluster split-K k-range); only
+// then do the dequant warps walk the stage sequence to learn tile counts.
+template <int BN, bool CSK, bool RAGGED>
+__global__ void __launch_bounds__(kThreads, 1)
+    w6a16_tcgen05_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constant__ CUtensorMap tmap_y,
+                         const GemmArgs a) {
+  using C = Cfg<BN, CSK>;
+  constexpr int KS = C::kKStep;
+  using Sched = typename std::conditional<CSK, CskSched, SkSched>::type;
+  // The dynamic shared window starts 1024-aligned (as CUTLASS also assumes
+  // for SW128 operands; checked below), so every address is a constant offset
+  // from the symbol.
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem_x = smem_raw;                                           // kXStages x kXStageBytes
+  uint8_t* smem_w = smem_x + C::kXStages * C::kXStageBytes;             // kWStages x kWStageBytes
+  uint8_t* smem_stg = smem_w + C::kWStages * C::kWStageBytes;           // CSK: 2 x [BN/4][128] float4
+  uint8_t* smem_y = smem_stg + 2 * C::kStageBufBytes;                  // 2 x Y tile (TMA store source)
+  uint64_t* full_w = reinterpret_cast<uint64_t*>(smem_y + 2 * C::kYBufBytes);
+  uint64_t* empty_w = full_w + C::kWStages;
+  uint64_t* full_x = empty_w + C::kWStages;
+  uint64_t* empty_x = full_x + C::kXStages;
+  uint64_t* afull = empty_x + C::kXStages;
+  uint64_t* aempty = afull + C::kASlots;
+  uint64_t* dfull = aempty + C::kASlots;
+  uint64_t* dempty = dfull + C::kDBufs;
+  uint64_t* part_full = dempty + C::kDBufs;  // CSK [2]: this CTA's round partials from the senders
+  uint64_t* stg_free = part_full + 2;        // CSK [2]: this CTA's staging buffer read by the reducer
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(stg_free + 2);
+  volatile int* last_flag = reinterpret_cast<volatile int*>(tmem_slot + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    CTA_STAMP(0);
+    if (smem_u32(smem_raw) & 1023u) __trap();  // SW128 descriptors need 1024-B alignment
+  }
+  Sched sc;
+  if constexpr (CSK) {
+    sc.init(a, KS);
+  } else {
+    sc.init(a);
+  }
+  const int n_st = sc.n;
+
+  // Setup.  The W producer initialises every mbarrier and starts streaming
+  // weight tiles at once (weights never depend on the preceding kernel, see
+  // LPQT_LAUNCH_PDL); the other warps meet on named barrier 2 (the producer
+  // only arrives), so the TMEM allocation overlaps the first weight loads.
+  if (warp == kWarpTmaW) {
+    if (lane == 0) {
+      for (int s = 0; s < C::kWStages; ++s) {
+        mbar_init(&full_w[s], 1);
+        mbar_init(&empty_w[s], kNumDqWarps / 2);  // the dequant group owning the slot
+      }
+      for (int s = 0; s < C::kXStages; ++s) {
+        mbar_init(&full_x[s], 1);
+        mbar_init(&empty_x[s], 1);  // MMA commit
+      }
+      for (int b = 0; b < C::kASlots; ++b) {
+        mbar_init(&afull[b], kNumDqWarps / 2);
+        mbar_init(&aempty[b], 1);   // MMA commit
+      }
+      for (int d = 0; d < C::kDBufs; ++d) {
+        mbar_init(&dfull[d], C::kMmaWarps);
+        mbar_init(&dempty[d], kNumEpiWarps);
+      }
+      if constexpr (CSK) {
+        for (int b = 0; b < 2; ++b) {
+          mbar_init(&part_full[b], sc.C > 1 ? sc.C - 1 : 1);  // one remote arrive per sender
+          mbar_init(&stg_free[b], 1);                         // one remote arrive by the reducer
+        }
+      }
+      fence_mbar_init();
+      pdl_launch_dependents();  // the next kernel may queue for this SM as soon as it frees
+    }
+    __syncwarp();
+    named_bar_arrive(2, kThreads);
+  } else {
+    if (warp == kWarpMma0) {
+      tmem_alloc(tmem_slot, kTmemCols);
+      tmem_relinquish();
+    }
+    if (warp == kWarpTmaX && lane == 0) prefetch_tmap(&tmap_x);
+    tc_fence_before();
+    named_bar_sync(2, kThreads);
+    tc_fence_after();
+  }
+  // CSK: every thread arrives on the cluster barrier once its CTA's barriers
+  // are initialised; the epilogue (the only remote user) waits before its
+  // first DSMEM access, every other warp just before the exit sync
+  if constexpr (CSK) cluster_arrive();
+  // warp-uniform (not read by the W producer, which may pass before the alloc)
+  const uint32_t tmem_base = warp == kWarpTmaW ? 0u : __shfl_sync(0xffffffffu, *tmem_slot, 0);
+  const uint32_t tmem_d0 = tmem_base + C::kACols;                       // D buffers above the A ring
+  if (threadIdx.x == 0) {
+    CTA_STAMP(1);
+#ifdef LPQT_TRACE
+    uint32_t smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    if (a.trace && blockIdx.x < 256) a.trace[blockIdx.x * 24 + 7] = smid;
+#endif
+  }
+
+  // Register split (launch: 768 x 80): each role's warpgroup re-sizes its
+  // registers on entry — dequant 88, producer/MMA 48, epilogue 72
+  // (4 x 128 x 88 + 128 x 48 + 128 x 72 <= 768 x 80).
+  if (warp == kWarpTmaW || warp == kWarpTmaX) {
+    // ------------------------------------------------------------ producers
+    setmaxnreg_dec<48>();
+    const bool is_w = (warp == kWarpTmaW);
+    if (!is_w) pdl_wait();  // X is the preceding kernel's output
+    if (!is_w && lane == 0) CTA_STAMP(13);
+    const uint64_t pol = l2_evict_first_policy();
+    StageIter<Sched, KS> it;
+    it.start(a, sc, 0);
+    for (int i = 0; i < n_st; ++i, it.next(a, sc)) {
+      const int kt = it.kt(), nt = it.nt();
+      const int n_tile = it.sg.tile / a.m_tiles, m_tile = it.sg.tile - n_tile * a.m_tiles;
+      if (is_w) {
+        const int s = i % C::kWStages;
+        mbar_wait(&empty_w[s], ((i / C::kWStages) & 1) ^ 1);
+        const uint8_t* src = a.tiles + ((int64_t)n_tile * a.k_tiles + kt) * kTileBytes;
+        const uint32_t bytes = static_cast<uint32_t>(nt * kTileBytes);
+        const uint32_t e = elect_one();
+        mbar_arrive_expect_tx_if(e, &full_w[s], bytes);
+        bulk_g2s_if(e, smem_w + s * C::kWStageBytes, src, bytes, &full_w[s], pol);
+      } else {
+        const int s = i % C::kXStages;
+        mbar_wait(&empty_x[s], ((i / C::kXStages) & 1) ^ 1);
+        uint8_t* xs = smem_x + s * C::kXStageBytes;
+        const uint32_t e = elect_one();
+        mbar_arrive_expect_tx_if(e, &full_x[s], static_cast<uint32_t>(nt * C::kXTileBytes));
+        for (int j = 0; j < nt; ++j) {
+          tma_load_2d_if(e, xs + j * C::kXTileBytes, &tmap_x, &full_x[s], (kt + j) * kTileK, m_tile * BN);
+          tma_load_2d_if(e, xs + j * C::kXTileBytes + BN * 128, &tmap_x, &full_x[s], (kt + j) * kTileK + 64,
+                         m_tile * BN);
+        }
+      }
+    }
+    if (is_w && lane == 0) CTA_STAMP(2);
+  } else if (warp < kNumDqWarps) {
+    // ------------------------------------------------------------ dequant
+    // Two groups of 8 warps take alternate stages (one group's barrier waits
+    // overlap the other's ALU work); in a group warp w owns TMEM lane group
+    // w % 4 (rows 32 (w % 4) ..) and, for kKStep 2, tile tl = (w / 4) % 2 of
+    // the stage (its whole 128-k row: two 64-weight segments), for kKStep 1
+    // k-half tl of the stage's tile.
+    setmaxnreg_inc<88>();
+    constexpr int kSegs = KS == 2 ? 2 : 1;
+    const int lg = warp & 3, grp = warp >> 3, tl = (warp >> 2) & 1;
+    const int row = lg * 32 + lane;
+    const uint32_t w_src = smem_u32(smem_w) + static_cast<uint32_t>(row * 16 + (KS == 2 ? tl * kTileBytes
+                                                                                         : tl * 3 * kTileN * 16));
+    const uint32_t t_lane = tmem_base + (static_cast<uint32_t>(lg * 32) << 16) +
+                            static_cast<uint32_t>(KS == 2 ? tl * kAColsPerBuf : tl * 32);
+    const uint32_t fw0 = smem_u32(full_w), ew0 = smem_u32(empty_w);
+    const uint32_t af0 = smem_u32(afull), ae0 = smem_u32(aempty);
+    const ShiftMuls sm = a.sm;
+    // the group's stages are i = grp, grp + 2, ...: cursors step by two slots
+    struct Cur {
+      uint32_t idx, ph;
+      __device__ __forceinline__ void adv2(uint32_t n) {
+        idx += 2;
+        if (idx >= n) {
+          idx -= n;
+          ph ^= 1u;
+        }
+      }
+    };
+    Cur wc{static_cast<uint32_t>(grp), 0u};   // W ring
+    Cur ac{static_cast<uint32_t>(grp), 0u};   // A ring
+    StageIter<Sched, KS> it;
+    if constexpr (RAGGED) it.start(a, sc, grp);
+    auto stage_nt = [&]() -> int {
+      if constexpr (RAGGED) {
+        return it.nt();
+      } else {
+        return KS;
+      }
+    };
+    uint32_t q[kSegs][6 * 2];
+    auto load_words = [&](int nt) {
+      mbar_wait_u32(fw0 + 8 * wc.idx, wc.ph);
+      if (KS == 1 || tl < nt) {
+        const uint32_t src = w_src + wc.idx * C::kWStageBytes;
+#pragma unroll
+        for (int h = 0; h < kSegs; ++h) {
+          const uint32_t sh = src + h * 3 * kTileN * 16;
+          const uint4 v0 = lds128_u32(sh), v1 = lds128_u32(sh + kTileN * 16), v2 = lds128_u32(sh + 2 * kTileN * 16);
+          q[h][0] = v0.x; q[h][1] = v0.y; q[h][2] = v0.z; q[h][3] = v0.w; q[h][4] = v1.x; q[h][5] = v1.y;
+          q[h][6] = v1.z; q[h][7] = v1.w; q[h][8] = v2.x; q[h][9] = v2.y; q[h][10] = v2.z; q[h][11] = v2.w;
+        }
+      }
+    };
+    int nt_cur = 0;
+    if (grp < n_st) {
+      nt_cur = stage_nt();
+      load_words(nt_cur);
+    }
+    if (warp == 0 && lane == 0) CTA_STAMP(12);
+    for (int i = grp; i < n_st; i += 2) {
+      // the first segment is rebuilt before the wait for the TMEM slot, so
+      // half the ALU work overlaps the MMAs still reading the slot
+      const bool act = KS == 1 || tl < nt_cur;
+      uint32_t r[32];
+#ifndef LPQT_EXP_NO_REBUILD
+      if (act) {
+        fp6x32_cvt_f16x32_fma(q[0], r, sm);
+        fp6x32_cvt_f16x32_fma(q[0] + 6, r + 16, sm);
+      }
+#else
+#pragma unroll
+      for (int j = 0; j < 32; ++j) r[j] = q[0][j % 12];
+#endif
+      mbar_wait_u32(ae0 + 8 * ac.idx, ac.ph ^ 1u);
+      tc_fence_after();
+      if (act) {
+        const uint32_t ta = t_lane + ac.idx * (KS * kAColsPerBuf);
+        tmem_st_x32(ta, r);
+#pragma unroll
+        for (int h = 1; h < kSegs; ++h) {
+#ifndef LPQT_EXP_NO_REBUILD
+          fp6x32_cvt_f16x32_fma(q[h], r, sm);
+          fp6x32_cvt_f16x32_fma(q[h] + 6, r + 16, sm);
+#else
+#pragma unroll
+          for (int j = 0; j < 32; ++j) r[j] = q[h][j % 12];
+#endif
+          tmem_st_x32(ta + h * 32, r);
+        }
+      }
+      // the stage's words are consumed: hand the W slot back to the producer
+      __syncwarp();
+      if (lane == 0) mbar_arrive_u32(ew0 + 8 * wc.idx);
+      wc.adv2(C::kWStages);
+      // prefetch the group's next stage while the TMEM stores drain
+      if (i + 2 < n_st) {
+        if constexpr (RAGGED) {
+          it.next(a, sc);
+          it.next(a, sc);
+        }
+        nt_cur = stage_nt();
+        load_words(nt_cur);
+      }
+      tmem_wait_st();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_u32(af0 + 8 * ac.idx);
+      ac.adv2(C::kASlots);
+    }
+    if (warp == 0 && lane == 0) CTA_STAMP(3);
+    if (warp == 8 && lane == 0) CTA_STAMP(16);
+  } else if (warp < kWarpEpi0) {
+    // ------------------------------------------------------------ MMA issue
+    // issuer mw takes the local stages of parity mw into accumulator mw; a
+    // one-stage segment leaves one issuer without work: it then arrives on
+    // dfull without a commit, and the epilogue sums only the accumulators
+    // that were written.
+    setmaxnreg_dec<48>();
+    const int mw = warp - kWarpMma0;
+    if (mw < C::kMmaWarps) {
+      constexpr uint32_t idesc = idesc_f16_m128(BN);
+      Seg sg;
+      int lu = 0;
+      for (int i0 = 0; sc.template seg_at<KS>(a, i0, sg); i0 += sg.len) {
+        const int d = lu % C::kDBufs;
+        const uint32_t dph = (lu / C::kDBufs) & 1;
+        mbar_wait(&dempty[d], dph ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_d0 + d * C::kDCols + mw * BN;
+        const int s_first = C::kMmaWarps == 2 ? ((mw - sg.i0) & 1) : 0;
+        for (int s = s_first; s < sg.len; s += C::kMmaWarps) {
+          const int it = sg.i0 + s;
+          const int kt = sg.kt0 + s * KS;
+          const int nt = min(KS, sg.kt1 - kt);
+          const int xs = it % C::kXStages;
+          const int slot = it % C::kASlots;
+          mbar_wait(&full_x[xs], (it / C::kXStages) & 1);
+          if (it == mw && lane == 0) CTA_STAMP(14);
+          mbar_wait(&afull[slot], (it / C::kASlots) & 1);
+          tc_fence_after();
+          const uint32_t e = elect_one();
+          // descriptor of X block 0 of this stage; every other operand is a
+          // compile-time offset from it (start address field = addr >> 4)
+          const uint64_t bd0 = sdesc_kmajor_sw128(smem_u32(smem_x + xs * C::kXStageBytes));
+          const uint32_t bd_lo = static_cast<uint32_t>(bd0), bd_hi = static_cast<uint32_t>(bd0 >> 32);
+          const uint32_t ta = tmem_base + slot * (KS * kAColsPerBuf);
+          const bool first = (s == s_first);
+#pragma unroll
+          for (int t = 0; t < KS; ++t) {
+            if (t < nt) {
+#pragma unroll
+              for (int j = 0; j < kTileK / 16; ++j) {
+                const uint32_t off = (t * C::kXTileBytes + (j >> 2) * (BN * 128) + (j & 3) * 32) >> 4;
+                const bool init = first && t == 0 && j == 0;
+#ifndef LPQT_EXP_NO_MMA
+                mma_f16_ts_if(e, d_tmem, ta + t * kAColsPerBuf + j * 8, bd_lo + off, bd_hi, idesc,
+                              init ? 0u : 1u);
+#else
+                (void)off;
+                (void)init;
+#endif
+              }
+            }
+          }
+          tc_commit_if(e, &empty_x[xs]);
+          tc_commit_if(e, &aempty[slot]);
+        }
+        if (s_first < sg.len) {
+          tc_commit_elect(&dfull[d]);
+        } else if (lane == 0) {
+          mbar_arrive(&dfull[d]);  // no MMA of this issuer in the segment
+        }
+        ++lu;
+      }
+      if (mw == 0 && lane == 0) CTA_STAMP(4);
+      if (mw == 1 && lane == 0) CTA_STAMP(15);
+    }
+  } else {
+    // ------------------------------------------------------------ epilogue
+    setmaxnreg_dec<72>();
+    const int lg = warp & 3;
+    const int rr = lg * 32 + lane;  // row inside the 128-row tile (= TMEM lane)
+    // Row scales are weights (never written by the preceding kernel): the
+    // first segment's is loaded before any wait, each next one a segment
+    // ahead, so no global load sits on the epilogue's critical path (a cold
+    // load behind the weight stream costs microseconds).
+    auto scale_of = [&](const Seg& g) -> uint16_t {
+      const int nn = (g.tile / a.m_tiles) * kTileN + rr;
+      return nn < a.N ? __ldg(a.scales + nn) : static_cast<uint16_t>(0);
+    };
+    Seg sg_next;
+    bool have_next = sc.template seg_at<KS>(a, 0, sg_next);
+    uint16_t fs_next = have_next ? scale_of(sg_next) : static_cast<uint16_t>(0);
+    if constexpr (CSK) cluster_wait();
+    if (warp == kWarpEpi0 && lane == 0) CTA_STAMP(17);
+    pdl_wait();  // Y / workspace writes: the preceding grid must be complete
+    if (warp == kWarpEpi0 && lane == 0) CTA_STAMP(18);
+    const uint32_t t_lane = tmem_d0 + (static_cast<uint32_t>(lg * 32) << 16);
+    Seg sg;
+    int lu = 0;
+    // CSK, one bit per staging buffer: barrier phases to wait for, and
+    // whether the buffer has been sent from before
+    uint32_t pf_bits = 0u, sf_bits = 0u, sent_bits = 0u;
+    // Y tiles: staged in smem and written by the TMA tensor store (decode),
+    // else stored directly; ys_n counts staged tiles (buffer = ys_n & 1)
+    const bool ytma = C::kYBufBytes > 0 && a.y_tma;
+    int ys_n = 0;
+    for (; have_next; ++lu) {
+      sg = sg_next;
+      const float fs = __half2float(__ushort_as_half(fs_next));
+      have_next = sc.template seg_at<KS>(a, sg.i0 + sg.len, sg_next);
+      if (have_next) fs_next = scale_of(sg_next);
+      const int d = lu % C::kDBufs;
+      const uint32_t dph = (lu / C::kDBufs) & 1;
+      const int n_tile = sg.tile / a.m_tiles, m_tile = sg.tile % a.m_tiles;
+      const int n = n_tile * kTileN + rr;
+      const int m0 = m_tile * BN;
+      const uint32_t t_d = t_lane + d * C::kDCols;
+      const uint32_t ybuf = smem_u32(smem_y) + (ys_n & 1) * C::kYBufBytes;
+      auto y_begin = [&]() {  // the staging buffer must have been read by its last TMA store
+        if (ytma && ys_n >= 2) {
+          if (warp == kWarpEpi0 && lane == 0) bulk_wait_read<1>();
+          named_bar_sync(1, kNumEpiWarps * 32);
+        }
+      };
+      auto y_chunk = [&](int c0, const float (&v)[16]) {
+        if (ytma) {
+          ystage_put<BN>(a, ybuf, rr, c0, v, fs);
+        } else {
+#pragma unroll
+          for (int j = 0; j < 16; ++j) store_y(a, n, m0 + c0 + j, v[j] * fs);
+        }
+      };
+      auto y_end = [&]() {
+        if (!ytma) return;
+        fence_proxy_async_smem();
+        named_bar_sync(1, kNumEpiWarps * 32);
+        if (warp == kWarpEpi0 && lane == 0) {
+          if (a.y_layout == LPQT_Y_NM) {
+            tma_store_2d(&tmap_y, ybuf, m_tile * BN, n_tile * kTileN);
+          } else {
+            tma_store_2d(&tmap_y, ybuf, n_tile * kTileN, m_tile * BN);
+          }
+          bulk_commit();
+        }
+        ++ys_n;
+      };
+      // accumulators written for this segment: both issuers when it spans >= 2
+      // stages, else only the issuer of the single stage's parity
+      const int nacc = min(C::kNAcc, sg.len);
+      const int q0 = (nacc < C::kNAcc) ? (sg.i0 & 1) : 0;
+      const bool last_seg = sg.i0 + sg.len >= n_st;
+      mbar_wait(&dfull[d], dph);
+      if (last_seg && warp == kWarpEpi0 && lane == 0) CTA_STAMP(8);
+      tc_fence_after();
+      if constexpr (CSK) {
+        // ---- cluster split-K: reduce the C partials of this tile over DSMEM
+        const int b = lu & 1;  // staging buffer / barrier of this round
+        // staging layout [BN / 4][128] float4: thread rr writes column chunk
+        // j at (j * 128 + rr) * 16 (conflict-free)
+        const uint32_t stg = smem_u32(smem_stg) + b * C::kStageBufBytes + rr * 16;
+        if (sc.C > 1 && sc.rank != sg.red) {
+          // sender: wait until the reducer that read this buffer last is
+          // done with it, stage the partial, signal this round's reducer
+          if ((sent_bits >> b) & 1u) {
+            mbar_wait_cluster(smem_u32(&stg_free[b]), (sf_bits >> b) & 1u);
+            sf_bits ^= 1u << b;
+          }
+          sent_bits |= 1u << b;
+#pragma unroll 1
+          for (int c0 = 0; c0 < BN; c0 += 16) {
+            float acc[16];
+            load_acc16<BN>(t_d, c0, q0, nacc, acc);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(stg + (c0 / 4 + j) * 128 * 16),
+                           "f"(acc[4 * j]), "f"(acc[4 * j + 1]), "f"(acc[4 * j + 2]), "f"(acc[4 * j + 3])
+                           : "memory");
+            }
+          }
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&dempty[d]);
+          named_bar_sync(1, kNumEpiWarps * 32);
+          if (warp == kWarpEpi0 && lane == 0)
+            mbar_arrive_remote(mapa_shared(smem_u32(&part_full[b]), static_cast<uint32_t>(sg.red)));
+        } else {
+          // reducer: own partial into registers and the D buffer straight
+          // back to the MMA (the reduction below must not stall the
+          // pipeline), then wait for the C - 1 partials and sum in rank order
+          float own[BN];
+#pragma unroll
+          for (int c0 = 0; c0 < BN; c0 += 16) {
+            float t16[16];
+            load_acc16<BN>(t_d, c0, q0, nacc, t16);
+#pragma unroll
+            for (int j = 0; j < 16; ++j) own[c0 + j] = t16[j];
+          }
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&dempty[d]);
+          if (sc.C > 1) {
+            mbar_wait_cluster(smem_u32(&part_full[b]), (pf_bits >> b) & 1u);
+            pf_bits ^= 1u << b;
+          }
+          y_begin();
+#pragma unroll
+          for (int c0 = 0; c0 < BN; c0 += 16) {
+            float sum[16];
+#pragma unroll
+            for (int j = 0; j < 16; ++j) sum[j] = 0.f;
+#pragma unroll 1
+            for (int r = 0; r < sc.C; ++r) {
+              if (r == sc.rank) {
+#pragma unroll
+                for (int j = 0; j < 16; ++j) sum[j] += own[c0 + j];
+              } else {
+                const uint32_t src = mapa_shared(stg + (c0 / 4) * 128 * 16, static_cast<uint32_t>(r));
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                  const float4 v = ld_dsmem_f4(src + j * 128 * 16);
+                  sum[4 * j] += v.x;
+                  sum[4 * j + 1] += v.y;
+                  sum[4 * j + 2] += v.z;
+                  sum[4 * j + 3] += v.w;
+                }
+              }
+            }
+            y_chunk(c0, sum);
+          }
+          y_end();
+          if (sc.C > 1) {
+            // the senders' staging buffers are read: hand them back
+            named_bar_sync(1, kNumEpiWarps * 32);
+            if (warp == kWarpEpi0 && lane < sc.C && lane != sc.rank)
+              mbar_arrive_remote(mapa_shared(smem_u32(&stg_free[b]), static_cast<uint32_t>(lane)));
+          }
+        }
+      } else if (sg.full) {
+        y_begin();
+#pragma unroll 1
+        for (int c0 = 0; c0 < BN; c0 += 16) {
+          float acc[16];
+          load_acc16<BN>(t_d, c0, q0, nacc, acc);
+          if (c0 + 16 >= BN) {  // last chunk read: hand the D buffer back to the MMA warp
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&dempty[d]);
+          }
+          y_chunk(c0, acc);
+        }
+        y_end();
+      } else {
+        // ---- stream-K partial tile
+        float* part = a.partials + (((int64_t)blockIdx.x * 2 + sg.pidx) * kTileN + rr) * BN;
+#pragma unroll 1
+        for (int c0 = 0; c0 < BN; c0 += 16) {
+          float acc[16];
+          load_acc16<BN>(t_d, c0, q0, nacc, acc);
+          if (c0 + 16 >= BN) {
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&dempty[d]);
+          }
+#pragma unroll
+          for (int j = 0; j < 16; j += 4) {
+            __stcg(reinterpret_cast<float4*>(part + c0 + j), make_float4(acc[j], acc[j + 1], acc[j + 2], acc[j + 3]));
+          }
+        }
+        // publish: CTA barrier, then one gpu-scope acq_rel atomic (release our
+        // partial, acquire the other contributors' partials if we are last)
+        named_bar_sync(1, kNumEpiWarps * 32);
+        if (warp == kWarpEpi0 && lane == 0) {
+          const int k_done = sg.len;
+          const int prev = atom_add_acq_rel_gpu(&a.counters[sg.tile], k_done);
+          *last_flag = (prev + k_done == a.ksteps) ? 1 : 0;
+        }
+        named_bar_sync(1, kNumEpiWarps * 32);
+        if (*last_flag) {
+          const int64_t p_first = (int64_t)sg.tile * a.ksteps;
+          const int c_first = sk_cta_of(a, p_first);
+          const int c_last = sk_cta_of(a, p_first + a.ksteps - 1);
+          // partial slot of contributor c: only c_first can have started its
+          // range before the tile (slot 1 = its last segment); every later
+          // contributor starts inside the tile (slot 0 = its first segment)
+          const int idx_first = (sk_begin(a, c_first) >= p_first) ? 0 : 1;
+          y_begin();
+#pragma unroll 1
+          for (int c0 = 0; c0 < BN; c0 += 16) {
+            float acc[16];
+#pragma unroll
+            for (int j = 0; j < 16; ++j) acc[j] = 0.f;
+            // contributors in k order (fixed summation order: deterministic);
+            // kFix of them are loaded at once so their L2 round trips
+            // overlap.  Plain (weak) loads: the acquire above ordered them
+            // after every contributor's release.
+            constexpr int kFix = 2;
+#pragma unroll 1
+            for (int cb = c_first; cb <= c_last; cb += kFix) {
+              float4 v[kFix][4];
+#pragma unroll
+              for (int u = 0; u < kFix; ++u) {
+                const int c = cb + u;
+                if (c <= c_last) {
+                  const int idx = c == c_first ? idx_first : 0;
+                  const float4* src =
+                      reinterpret_cast<const float4*>(a.partials + (((int64_t)c * 2 + idx) * kTileN + rr) * BN + c0);
+#pragma unroll
+                  for (int j = 0; j < 4; ++j) v[u][j] = src[j];
+                } else {
+#pragma unroll
+                  for (int j = 0; j < 4; ++j) v[u][j] = make_float4(0.f, 0.f, 0.f, 0.f);
+                }
+              }
+#pragma unroll
+              for (int u = 0; u < kFix; ++u) {
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                  acc[4 * j + 0] += v[u][j].x;
+                  acc[4 * j + 1] += v[u][j].y;
+                  acc[4 * j + 2] += v[u][j].z;
+                  acc[4 * j + 3] += v[u][j].w;
+                }
+              }
+            }
+            y_chunk(c0, acc);
+          }
+          y_end();
+          if (warp == kWarpEpi0 && lane == 0) a.counters[sg.tile] = 0;
+          if (last_seg && warp == kWarpEpi0 && lane == 0) CTA_STAMP(11);
+        }
+        named_bar_sync(1, kNumEpiWarps * 32);
+      }
+    }
+    if (ytma && warp == kWarpEpi0 && lane == 0) bulk_wait_read<0>();  // smem stays valid until read
+    if (warp == kWarpEpi0 && lane == 0) CTA_STAMP(5);
+  }
+
+  if constexpr (CSK) {
+    if (warp < kWarpEpi0) cluster_wait();  // the setup phase (epilogue waited already)
+  }
+  tc_fence_before();
+  __syncthreads();
+  // CSK: no CTA may leave while a peer can still read its staging buffer or
+  // arrive on its barriers
+  if constexpr (CSK) cluster_sync_all();
+  if (threadIdx.x == 0) CTA_STAMP(6);
+  if (warp == kWarpMma0) {
+    tc_fence_after();
+    tmem_dealloc(tmem_base, kTmemCols);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// host side: plan, tensor map, launch
+// ---------------------------------------------------------------------------
+struct Plan {
+  int bn, grid, n_tiles, m_tiles, k_tiles, ksteps, stages, smem, kstep;
+  int64_t tiles, total, ws_bytes, counters_bytes;
+  bool partials;
+  bool csk;
+  int cluster;  // CSK cluster size
+  int splits;   // max CTAs contributing to one tile
+};
+
+static int pick_bn(int64_t M) {
+  if (M <= 16) return 16;
+  if (M <= 32) return 32;
+  if (M <= 64) return 64;
+  if (M <= 128) return 128;
+  return 256;
+}
+
+template <int BN, bool CSK>
+static void cfg_of(Plan& p) {
+  p.stages = Cfg<BN, CSK>::kStages;
+  p.smem = Cfg<BN, CSK>::kSmemBytes;
+  p.kstep = Cfg<BN, CSK>::kKStep;
+}
+
+static int num_sms() {
+  static int sms = 0;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || sms <= 0) sms = 148;
+  });
+  return sms;
+}
+
+// Co-resident clusters of c CTAs for the decode kernel (GPC packing; 1 CTA
+// per SM).  Queried once per c from the driver; the fallback is a 148-SM
+// B200 as measured (tools/cluster_occ.cu).
+template <int BN>
+static int max_clusters(int c) {
+  static int cache[kMaxCluster + 1] = {0};
+  static std::mutex mu;
+  std::lock_guard<std::mutex> lock(mu);
+  if (cache[c] > 0) return cache[c];
+  static const int fallback[kMaxCluster + 1] = {0, 148, 74, 45, 33, 26, 22, 15, 15};
+  int n = 0;
+  auto kern = w6a16_tcgen05_kernel<BN, true, true>;
+  constexpr int smem = Cfg<BN, true>::kSmemBytes;
+  int dev = 0;
+  if (cudaGetDevice(&dev) == cudaSuccess &&
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) == cudaSuccess) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(c * 64);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = smem;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = c;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    if (cudaOccupancyMaxActiveClusters(&n, kern, &cfg) != cudaSuccess) n = 0;
+  }
+  cudaGetLastError();  // a failed query must not poison later launches
+  if (n <= 0) n = fallback[c];
+  cache[c] = n;
+  return n;
+}
+
+static int max_clusters_bn(int bn, int c) { return bn <= 16 ? max_clusters<16>(c) : max_clusters<32>(c); }
+
+// split_k == 0: automatic schedule.  With LPQT_SCHED_CLUSTER: cluster
+// split-K with C = split_k (>= 1).  Otherwise split_k > 0 is stream-K with
+// about split_k CTAs per tile (testing / tuning hooks).
+static Plan make_plan(int64_t M, int64_t N, int64_t K, int split_k, int flags, int sms) {
+  Plan p{};
+  p.bn = pick_bn(M);
+  p.n_tiles = static_cast<int>((N + kTileN - 1) / kTileN);
+  p.m_tiles = static_cast<int>((M + p.bn - 1) / p.bn);
+  p.k_tiles = static_cast<int>((K + kTileK - 1) / kTileK);
+  p.tiles = (int64_t)p.n_tiles * p.m_tiles;
+  // ---- schedule choice (decode, BN <= 32, may use cluster split-K)
+  const bool csk_ok = p.bn <= 32 && p.tiles < ((int64_t)1 << 30);
+  int best_c = 0;
+  if (csk_ok && !(flags & LPQT_SCHED_STREAMK)) {
+    if (flags & LPQT_SCHED_CLUSTER) {
+      best_c = split_k > 0 ? split_k : 1;
+      best_c = std::min(best_c, std::min(kMaxCluster, p.k_tiles));
+    } else if (split_k == 0) {
+      // Time model of one launch (us; fitted to B200 measurements of both
+      // schedules on the LLaMA shapes, tools/abx.py, profiles/): a CTA
+      // streams one 128x128 FP6 tile in ~0.31 us; stream-K pays ~3-6 us of
+      // cross-CTA fixups on its tail when tiles are split; cluster split-K
+      // ~0.7 us of DSMEM reduction per round plus ~0.5 us of cluster
+      // launch/sync.  Only C <= 2 is chosen automatically (larger clusters
+      // measured slower than the model predicts).
+      const double tile_us = 0.31;
+      const double sk_kt = (double)p.tiles * p.k_tiles / sms;  // k-tiles per CTA
+      const bool sk_partial = ((int64_t)p.tiles * p.k_tiles) % sms != 0 || p.tiles % sms != 0;
+      // (long per-CTA ranges hide part of the fixup tail)
+      double best = sk_kt * tile_us + (sk_partial ? (sk_kt < 64.0 ? 6.0 : 3.0) : 0.0);
+      for (int c = 1; c <= 2 && c <= p.k_tiles; ++c) {
+        const int64_t ncl = std::min<int64_t>(max_clusters_bn(p.bn, c), p.tiles);
+        const int64_t rounds = (p.tiles + ncl - 1) / ncl;
+        const double us = rounds * (((p.k_tiles + c - 1) / c) * tile_us + (c > 1 ? 0.7 : 0.0)) + (c > 1 ? 0.5 : 0.0);
+        if (us < best) {
+          best = us;
+          best_c = c;
+        }
+      }
+    }
+  }
+  if (best_c > 0) {
+    p.csk = true;
+    p.cluster = best_c;
+    if (p.bn <= 16) {
+      cfg_of<16, true>(p);
+    } else {
+      cfg_of<32, true>(p);
+    }
+    const int64_t ncl = std::min<int64_t>(max_clusters_bn(p.bn, best_c), p.tiles);
+    p.grid = static_cast<int>(ncl * best_c);
+    p.ksteps = (p.k_tiles + p.kstep - 1) / p.kstep;
+    p.splits = best_c;
+    return p;
+  }
+  switch (p.bn) {
+    case 16: cfg_of<16, false>(p); break;
+    case 32: cfg_of<32, false>(p); break;
+    case 64: cfg_of<64, false>(p); break;
+    case 128: cfg_of<128, false>(p); break;
+    default: cfg_of<256, false>(p); break;
+  }
+  p.ksteps = (p.k_tiles + p.kstep - 1) / p.kstep;
+  p.total = p.tiles * p.ksteps;
+  int64_t g = split_k > 0 ? p.tiles * split_k : sms;
+  if (g > p.total) g = p.total;
+  if (p.tiles > kMaxCounters) g = p.tiles;  // one whole tile per CTA: no counters needed
+  if (g < 1) g = 1;
+  p.grid = static_cast<int>(g);
+  // partial tiles exist unless every CTA range is a whole number of tiles
+  p.partials = !(p.total % g == 0 && (p.total / g) % p.ksteps == 0);
+  if (p.partials) {
+    p.counters_bytes = kMaxCounters * 4;  // fixed region, zeroed once, self-resetting
+    p.ws_bytes = p.counters_bytes + (int64_t)p.grid * 2 * kTileN * p.bn * 4;
+  }
+  const int64_t per = p.total / p.grid;  // k-steps per CTA (floor)
+  p.splits = p.partials ? static_cast<int>((p.ksteps + (per > 0 ? per : 1) - 1) / (per > 0 ? per : 1) + 1) : 1;
+  return p;
+}
+
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  });
+  return fn;
+}
+
+#ifdef LPQT_TRACE
+// kTraceSlots trace records; launch n writes record n % kTraceSlots (graph
+// captures bake the record index in at capture time)
+constexpr int kTraceSlots = 16;
+static long long* trace_buffer() {
+  static long long* buf = nullptr;
+  if (!buf) {
+    cudaMalloc(&buf, (size_t)kTraceSlots * kTraceLen * sizeof(long long));
+    cudaMemset(buf, 0, (size_t)kTraceSlots * kTraceLen * sizeof(long long));
+  }
+  return buf;
+}
+static int g_trace_n = 0;  // launches traced so far
+static int trace_next_slot() { return g_trace_n++ % kTraceSlots; }
+#endif
+
+template <int BN, bool CSK, bool RAGGED>
+static int launch_impl(const Plan& p, const GemmArgs& args, const uint16_t* Xt, int64_t ldx, int64_t M,
+                       cudaStream_t stream, int flags) {
+  EncodeTiledFn enc = encode_fn();
+  if (!enc) return LPQT_E_CUDA;
+  CUtensorMap map;
+  const cuuint64_t dims[2] = {static_cast<cuuint64_t>(ldx), static_cast<cuuint64_t>(M)};
+  const cuuint64_t strides[1] = {static_cast<cuuint64_t>(ldx) * 2};
+  const cuuint32_t box[2] = {64, static_cast<cuuint32_t>(BN)};
+  const cuuint32_t estr[2] = {1, 1};
+  if (enc(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, const_cast<uint16_t*>(Xt), dims, strides, box, estr,
+          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+    return LPQT_E_INVALID_INPUT;
+  auto kern = w6a16_tcgen05_kernel<BN, CSK, RAGGED>;
+  constexpr int smem = Cfg<BN, CSK>::kSmemBytes;
+  static std::once_flag once;
+  static cudaError_t attr_err = cudaSuccess;
+  std::call_once(once, [&] {
+    attr_err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  });
+  if (attr_err != cudaSuccess) return LPQT_E_CUDA;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(p.grid);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[2];
+  int na = 0;
+  if (flags & LPQT_LAUNCH_PDL) {
+    attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[na].val.programmaticStreamSerializationAllowed = 1;
+    ++na;
+  }
+  if (CSK) {
+    attr[na].id = cudaLaunchAttributeClusterDimension;
+    attr[na].val.clusterDim.x = p.cluster;
+    attr[na].val.clusterDim.y = 1;
+    attr[na].val.clusterDim.z = 1;
+    ++na;
+  }
+  cfg.attrs = attr;
+  cfg.numAttrs = na;
+  GemmArgs a2 = args;
+  a2.csk_c = CSK ? p.cluster : 0;
+  // Y tensor map for the TMA store epilogue (decode tiles); shapes the TMA
+  // cannot describe (unaligned base / row stride) keep the direct stores
+  CUtensorMap ymap;
+  memset(&ymap, 0, sizeof(ymap));
+  a2.y_tma = 0;
+  if (Cfg<BN, CSK>::kYBufBytes > 0) {
+    const int es = args.y_dtype == LPQT_F32 ? 4 : 2;
+    const CUtensorMapDataType dt = args.y_dtype == LPQT_F32   ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32
+                                   : args.y_dtype == LPQT_F16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16
+                                                              : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
+    const bool nm = args.y_layout == LPQT_Y_NM;
+    const cuuint64_t ydims[2] = {static_cast<cuuint64_t>(nm ? args.M : args.N),
+                                 static_cast<cuuint64_t>(nm ? args.N : args.M)};
+    const cuuint64_t ystr[1] = {static_cast<cuuint64_t>(args.ldy) * es};
+    const cuuint32_t ybox[2] = {static_cast<cuuint32_t>(nm ? BN : kTileN), static_cast<cuuint32_t>(nm ? kTileN : BN)};
+    const bool ok = (reinterpret_cast<uintptr_t>(args.y) % 16 == 0) && (ystr[0] % 16 == 0) &&
+                    ((cuuint64_t)ybox[0] * es) % 16 == 0 && ydims[1] > 1;
+    if (ok && enc(&ymap, dt, 2, args.y, ydims, ystr, ybox, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                  CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS)
+      a2.y_tma = 1;
+  }
+  if (cudaLaunchKernelEx(&cfg, kern, map, ymap, a2) != cudaSuccess) return LPQT_E_CUDA;
+  note_launch();
+  return check_launch();
+}
+
+}  // namespace lpqt
+
+using namespace lpqt;
+
+extern "C" {
+
+#ifdef LPQT_TRACE
+int lpqt_trace_dump(long long* host) {  // the last launch's record
+  cudaDeviceSynchronize();
+  const int slot = (g_trace_n + kTraceSlots - 1) % kTraceSlots;
+  return cudaMemcpy(host, trace_buffer() + (size_t)slot * kTraceLen, kTraceLen * sizeof(long long),
+                    cudaMemcpyDeviceToHost) == cudaSuccess
+             ? 0
+             : -1;
+}
+// all kTraceSlots records (launch n -> record n % kTraceSlots); returns the
+// number of launches traced so far
+int lpqt_trace_dump_all(long long* host, int* n_launches) {
+  cudaDeviceSynchronize();
+  if (n_launches) *n_launches = g_trace_n;
+  return cudaMemcpy(host, trace_buffer(), (size_t)kTraceSlots * kTraceLen * sizeof(long long),
+                    cudaMemcpyDeviceToHost) == cudaSuccess
+             ? 0
+             : -1;
+}
+#endif
+
+int64_t lpqt_w6a16_workspace_bytes(int64_t M, int64_t N, int64_t K, int split_k) {
+  if (M <= 0 || N <= 0 || K <= 0) return 0;
+  // the largest any schedule of this shape may need (auto or forced stream-K)
+  const Plan p0 = make_plan(M, N, K, split_k, 0, num_sms());
+  const Plan p1 = make_plan(M, N, K, split_k, LPQT_SCHED_STREAMK, num_sms());
+  return p0.ws_bytes > p1.ws_bytes ? p0.ws_bytes : p1.ws_bytes;
+}
+
+int lpqt_w6a16_plan_ex(int64_t M, int64_t N, int64_t K, int split_k, int flags, int* out, int n_out) {
+  if (M <= 0 || N <= 0 || K <= 0) return LPQT_E_SHAPE;
+  if ((flags & LPQT_SCHED_STREAMK) && (flags & LPQT_SCHED_CLUSTER)) return LPQT_E_INVALID_INPUT;
+  const Plan p = make_plan(M, N, K, split_k, flags, num_sms());
+  const int v[6] = {p.bn, p.splits, p.grid, p.stages, p.csk ? 1 : 0, p.csk ? p.cluster : 0};
+  for (int i = 0; i < n_out && i < 6; ++i) out[i] = v[i];
+  return LPQT_OK;
+}
+
+// Reports the plan: block_n = MMA N, splits = max CTAs sharing one tile,
+// grid = CTAs, stages = smem pipeline depth.
+int lpqt_w6a16_plan(int64_t M, int64_t N, int64_t K, int split_k, int* block_n, int* splits, int* grid, int* stages) {
+  int v[4];
+  const int st = lpqt_w6a16_plan_ex(M, N, K, split_k, 0, v, 4);
+  if (st != LPQT_OK) return st;
+  if (block_n) *block_n = v[0];
+  if (splits) *splits = v[1];
+  if (grid) *grid = v[2];
+  if (stages) *stages = v[3];
+  return LPQT_OK;
+}
+
+int lpqt_w6a16_linear(const uint8_t* tiles, const uint16_t* scales, const uint16_t* Xt, int64_t ldx, int64_t M,
+                      int64_t N, int64_t K, void* Y, int y_dtype, int y_layout, int64_t ldy, int split_k,
+                      void* workspace, int64_t workspace_bytes, void* stream) {
+  return lpqt_w6a16_linear_ex(tiles, scales, Xt, ldx, M, N, K, Y, y_dtype, y_layout, ldy, split_k, workspace,
+                              workspace_bytes, 0, stream);
+}
+
+int lpqt_w6a16_linear_ex(const uint8_t* tiles, const uint16_t* scales, const uint16_t* Xt, int64_t ldx, int64_t M,
+                         int64_t N, int64_t K, void* Y, int y_dtype, int y_layout, int64_t ldy, int split_k,
+                         void* workspace, int64_t workspace_bytes, int flags, void* stream) {
+  if (flags & ~(LPQT_LAUNCH_PDL | LPQT_SCHED_STREAMK | LPQT_SCHED_CLUSTER)) return LPQT_E_INVALID_INPUT;
+  if ((flags & LPQT_SCHED_STREAMK) && (flags & LPQT_SCHED_CLUSTER)) return LPQT_E_INVALID_INPUT;
+  if (M < 0 || N < 0 || K < 0) return LPQT_E_SHAPE;
+  if (M == 0 || N == 0) return LPQT_OK;
+  if (K == 0) return LPQT_E_SHAPE;  // callers zero-fill (gemm.py:74-75)
+  if (ldx < K || ldx % 8 != 0 || (reinterpret_cast<uintptr_t>(Xt) & 15)) return LPQT_E_SHAPE;
+  if (y_dtype != LPQT_F32 && y_dtype != LPQT_F16 && y_dtype != LPQT_BF16) return LPQT_E_UNSUPPORTED;
+  if (y_layout != LPQT_Y_NM && y_layout != LPQT_Y_MN) return LPQT_E_UNSUPPORTED;
+  if (y_layout == LPQT_Y_NM ? ldy < M : ldy < N) return LPQT_E_SHAPE;
+  if (split_k < 0) return LPQT_E_INVALID_INPUT;
+  if (N > (int64_t)1 << 30 || M > (int64_t)1 << 30 || K > (int64_t)1 << 30) return LPQT_E_SHAPE;
+  const Plan p = make_plan(M, N, K, split_k, flags, num_sms());
+  if (p.ws_bytes > 0 && (workspace == nullptr || workspace_bytes < p.ws_bytes)) return LPQT_E_WORKSPACE;
+  GemmArgs args{};
+#ifdef LPQT_TRACE
+  args.trace = trace_buffer() + (size_t)trace_next_slot() * kTraceLen;
+#endif
+  args.tiles = tiles;
+  args.scales = scales;
+  args.y = Y;
+  args.counters = static_cast<int*>(workspace);
+  args.partials = reinterpret_cast<float*>(static_cast<uint8_t*>(workspace) + p.counters_bytes);
+  args.ldy = ldy;
+  args.total = p.total;
+  args.M = static_cast<int>(M);
+  args.N = static_cast<int>(N);
+  args.k_tiles = p.k_tiles;
+  args.ksteps = p.ksteps;
+  args.n_tiles = p.n_tiles;
+  args.m_tiles = p.m_tiles;
+  args.tile_count = static_cast<int>(p.tiles);
+  args.y_dtype = y_dtype;
+  args.y_layout = y_layout;
+  args.sm = ShiftMuls{1u << 26, 1u << 28, 1u << 30};
+  cudaStream_t st = as_stream(stream);
+  bool ragged = p.k_tiles % p.kstep != 0;
+  if (p.csk) {
+    for (int r = 0; r < p.cluster; ++r)  // k-range of rank r must be a whole number of stages
+      ragged |= ((r + 1) * p.k_tiles / p.cluster - r * p.k_tiles / p.cluster) % p.kstep != 0;
+    if (p.bn <= 16)
+      return ragged ? launch_impl<16, true, true>(p, args, Xt, ldx, M, st, flags)
+                    : launch_impl<16, true, false>(p, args, Xt, ldx, M, st, flags);
+    return ragged ? launch_impl<32, true, true>(p, args, Xt, ldx, M, st, flags)
+                  : launch_impl<32, true, false>(p, args, Xt, ldx, M, st, flags);
+  }
+  switch (p.bn) {
+    case 16:
+      return ragged ? launch_impl<16, false, true>(p, args, Xt, ldx, M, st, flags)
+                    : launch_impl<16, false, false>(p, args, Xt, ldx, M, st, flags);
+    case 32:
+      return ragged ? launch_impl<32, false, true>(p, args, Xt, ldx, M, st, flags)
+                    : launch_impl<32, false, false>(p, args, Xt, ldx, M, st, flags);
+    case 64: return launch_impl<64, false, false>(p, args, Xt, ldx, M, st, flags);
+    case 128: return launch_impl<128, false, false>(p, args, Xt, ldx, M, st, flags);
+    default: return launch_impl<256, false, false>(p, args, Xt, ldx, M, st, flags);
+  }
+}
+
+}  // extern "C"
