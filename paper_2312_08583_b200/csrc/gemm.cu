@@ -260,6 +260,15 @@ __device__ __forceinline__ int atom_add_acq_rel_gpu(int* p, int v) {
   return old;
 }
 
+__device__ __forceinline__ int ld_acquire_gpu(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void prefetch_l1(const void* p) {
+  asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
+}
+
 __device__ __forceinline__ void store_y(const GemmArgs& a, int n, int m, float v) {
   if (n >= a.N || m >= a.M) return;
   const int64_t off = a.y_layout == LPQT_Y_NM ? (int64_t)n * a.ldy + m : (int64_t)m * a.ldy + n;
@@ -785,6 +794,41 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int nacc = min(C::kNAcc, sg.len);
       const int q0 = (nacc < C::kNAcc) ? (sg.i0 & 1) : 0;
       const bool last_seg = sg.i0 + sg.len >= n_st;
+      // stream-K partial tile: if every other contributor has already
+      // published (acquire-load of the tile counter), this CTA is the last
+      // arriver — it skips publishing its own partial and the atomic, and
+      // pulls the others' partials into L1 while its MMAs finish
+      bool sk_last = false;
+      int64_t p_first = 0;
+      int c_first = 0, c_last = 0, idx_first = 0;
+      // contributors of a split tile (64-bit divisions: only when needed)
+      auto contributors = [&]() {
+        p_first = (int64_t)sg.tile * a.ksteps;
+        c_first = sk_cta_of(a, p_first);
+        c_last = sk_cta_of(a, p_first + a.ksteps - 1);
+        // partial slot of contributor c: only c_first can have started its
+        // range before the tile (slot 1 = its last segment); every later
+        // contributor starts inside the tile (slot 0 = its first segment)
+        idx_first = (sk_begin(a, c_first) >= p_first) ? 0 : 1;
+      };
+      // worth a look only where it usually succeeds: this CTA's last
+      // segment opening a tile (this CTA = its first contributor) shared
+      // with just the next CTA, which contracted its part first thing
+      if (!CSK && !sg.full && last_seg && sg.kt0 == 0) {
+        contributors();
+        if (c_first == static_cast<int>(blockIdx.x) && c_last == c_first + 1) {
+          if (warp == kWarpEpi0 && lane == 0)
+            *last_flag = (ld_acquire_gpu(&a.counters[sg.tile]) + sg.len == a.ksteps) ? 1 : 0;
+          named_bar_sync(1, kNumEpiWarps * 32);
+          sk_last = *last_flag != 0;
+          if (sk_last) {
+            const float* src = a.partials + (((int64_t)c_last * 2 + 0) * kTileN + rr) * BN;
+#pragma unroll
+            for (int c0 = 0; c0 < BN; c0 += 32) prefetch_l1(src + c0);
+          }
+          named_bar_sync(1, kNumEpiWarps * 32);  // last_flag is reused below
+        }
+      }
       mbar_wait(&dfull[d], dph);
       if (last_seg && warp == kWarpEpi0 && lane == 0) CTA_STAMP(8);
       tc_fence_after();
@@ -887,48 +931,71 @@ __global__ void __launch_bounds__(kThreads, 1)
         y_end();
       } else {
         // ---- stream-K partial tile
-        float* part = a.partials + (((int64_t)blockIdx.x * 2 + sg.pidx) * kTileN + rr) * BN;
+        if (!sk_last) {
+          float* part = a.partials + (((int64_t)blockIdx.x * 2 + sg.pidx) * kTileN + rr) * BN;
 #pragma unroll 1
-        for (int c0 = 0; c0 < BN; c0 += 16) {
-          float acc[16];
-          load_acc16<BN>(t_d, c0, q0, nacc, acc);
-          if (c0 + 16 >= BN) {
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&dempty[d]);
-          }
+          for (int c0 = 0; c0 < BN; c0 += 16) {
+            float acc[16];
+            load_acc16<BN>(t_d, c0, q0, nacc, acc);
+            if (c0 + 16 >= BN) {
+              tc_fence_before();
+              __syncwarp();
+              if (lane == 0) mbar_arrive(&dempty[d]);
+            }
 #pragma unroll
-          for (int j = 0; j < 16; j += 4) {
-            __stcg(reinterpret_cast<float4*>(part + c0 + j), make_float4(acc[j], acc[j + 1], acc[j + 2], acc[j + 3]));
+            for (int j = 0; j < 16; j += 4) {
+              __stcg(reinterpret_cast<float4*>(part + c0 + j),
+                     make_float4(acc[j], acc[j + 1], acc[j + 2], acc[j + 3]));
+            }
           }
+          // publish: CTA barrier, then one gpu-scope acq_rel atomic (release
+          // our partial, acquire the other contributors' partials if last)
+          named_bar_sync(1, kNumEpiWarps * 32);
+          if (warp == kWarpEpi0 && lane == 0) {
+            const int k_done = sg.len;
+            const int prev = atom_add_acq_rel_gpu(&a.counters[sg.tile], k_done);
+            *last_flag = (prev + k_done == a.ksteps) ? 1 : 0;
+          }
+          named_bar_sync(1, kNumEpiWarps * 32);
         }
-        // publish: CTA barrier, then one gpu-scope acq_rel atomic (release our
-        // partial, acquire the other contributors' partials if we are last)
-        named_bar_sync(1, kNumEpiWarps * 32);
-        if (warp == kWarpEpi0 && lane == 0) {
-          const int k_done = sg.len;
-          const int prev = atom_add_acq_rel_gpu(&a.counters[sg.tile], k_done);
-          *last_flag = (prev + k_done == a.ksteps) ? 1 : 0;
-        }
-        named_bar_sync(1, kNumEpiWarps * 32);
-        if (*last_flag) {
-          const int64_t p_first = (int64_t)sg.tile * a.ksteps;
-          const int c_first = sk_cta_of(a, p_first);
-          const int c_last = sk_cta_of(a, p_first + a.ksteps - 1);
-          // partial slot of contributor c: only c_first can have started its
-          // range before the tile (slot 1 = its last segment); every later
-          // contributor starts inside the tile (slot 0 = its first segment)
-          const int idx_first = (sk_begin(a, c_first) >= p_first) ? 0 : 1;
+        if (sk_last) {
+          // fast path: two contributors, this CTA first in k order
+          y_begin();
+#pragma unroll 1
+          for (int c0 = 0; c0 < BN; c0 += 16) {
+            float acc[16];
+            load_acc16<BN>(t_d, c0, q0, nacc, acc);
+            if (c0 + 16 >= BN) {
+              tc_fence_before();
+              __syncwarp();
+              if (lane == 0) mbar_arrive(&dempty[d]);
+            }
+            const float4* src =
+                reinterpret_cast<const float4*>(a.partials + (((int64_t)c_last * 2 + 0) * kTileN + rr) * BN + c0);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              const float4 v = src[j];
+              // (0 + own) + other: the canonical contributor-order sum
+              acc[4 * j + 0] = (0.f + acc[4 * j + 0]) + v.x;
+              acc[4 * j + 1] = (0.f + acc[4 * j + 1]) + v.y;
+              acc[4 * j + 2] = (0.f + acc[4 * j + 2]) + v.z;
+              acc[4 * j + 3] = (0.f + acc[4 * j + 3]) + v.w;
+            }
+            y_chunk(c0, acc);
+          }
+          y_end();
+        } else if (*last_flag) {
+          contributors();
           y_begin();
 #pragma unroll 1
           for (int c0 = 0; c0 < BN; c0 += 16) {
             float acc[16];
 #pragma unroll
             for (int j = 0; j < 16; ++j) acc[j] = 0.f;
-            // contributors in k order (fixed summation order: deterministic);
-            // kFix of them are loaded at once so their L2 round trips
-            // overlap.  Plain (weak) loads: the acquire above ordered them
-            // after every contributor's release.
+            // contributors in k order (fixed summation order, whichever CTA
+            // arrives last: deterministic); kFix of them are loaded at once
+            // so their L2 round trips overlap.  Plain (weak) loads: the
+            // acquire above ordered them after every contributor's release.
             constexpr int kFix = 2;
 #pragma unroll 1
             for (int cb = c_first; cb <= c_last; cb += kFix) {
@@ -961,6 +1028,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             y_chunk(c0, acc);
           }
           y_end();
+        }
+        if (sk_last || *last_flag) {
           if (warp == kWarpEpi0 && lane == 0) a.counters[sg.tile] = 0;
           if (last_seg && warp == kWarpEpi0 && lane == 0) CTA_STAMP(11);
         }
@@ -1089,8 +1158,11 @@ static Plan make_plan(int64_t M, int64_t N, int64_t K, int split_k, int flags, i
       const double tile_us = 0.31;
       const double sk_kt = (double)p.tiles * p.k_tiles / sms;  // k-tiles per CTA
       const bool sk_partial = ((int64_t)p.tiles * p.k_tiles) % sms != 0 || p.tiles % sms != 0;
-      // (long per-CTA ranges hide part of the fixup tail)
-      double best = sk_kt * tile_us + (sk_partial ? (sk_kt < 64.0 ? 6.0 : 3.0) : 0.0);
+      // (a range spanning whole tiles splits each tile between two CTAs,
+      // whose fixup takes the last-arriver fast path; long ranges hide part
+      // of the tail)
+      const double sk_tail = sk_kt >= p.k_tiles ? 2.0 : (sk_kt < 64.0 ? 6.0 : 3.0);
+      double best = sk_kt * tile_us + (sk_partial ? sk_tail : 0.0);
       for (int c = 1; c <= 2 && c <= p.k_tiles; ++c) {
         const int64_t ncl = std::min<int64_t>(max_clusters_bn(p.bn, c), p.tiles);
         const int64_t rounds = (p.tiles + ncl - 1) / ncl;
