@@ -71,7 +71,10 @@ constexpr int kWarpEpi0 = kWarpMma0 + kMaxMmaWarps;
 constexpr int kThreads = (kWarpEpi0 + kNumEpiWarps) * 32;  // 768
 constexpr int kAColsPerBuf = kTileK / 2;  // 64 columns of packed half2
 constexpr int kTmemCols = 512;
-constexpr int kSmemBudget = 216 * 1024;
+#ifndef LPQT_SMEM_BUDGET_KB
+#define LPQT_SMEM_BUDGET_KB 216
+#endif
+constexpr int kSmemBudget = LPQT_SMEM_BUDGET_KB * 1024;
 constexpr int64_t kMaxCounters = 65536;   // stream-K tile counters (256 KiB)
 constexpr int kMaxCluster = 8;
 
@@ -88,6 +91,7 @@ struct GemmArgs {
   int k_tiles, ksteps, n_tiles, m_tiles, tile_count;
   int y_dtype, y_layout;
   int csk_c;          // CSK: cluster size C (k-split factor)
+  int n_fastest;      // tile index order: 0 = batch tile fastest, 1 = weight-row tile fastest
   int y_tma;          // Y tiles leave through the TMA tensor store (tmap_y valid)
   ShiftMuls sm;       // 2^26, 2^28, 2^30: right shifts on the FMA pipe (common.cuh)
 };
@@ -98,14 +102,17 @@ struct Cfg {
   static constexpr int kXTileBytes = BN * kTileK * 2;       // X for one tile: two SW128 blocks
   static constexpr int kWStageBytes = kKStep * kTileBytes;
   static constexpr int kXStageBytes = kKStep * kXTileBytes;
-  static constexpr int kXStages = BN <= 16 ? (CSK ? 4 : 6) : (BN <= 128 ? 4 : 2);
+  // prefill (BN = 256): an X stage is 64 KB and covers ~1000 MMA cycles, so
+  // three stages keep the L2 latency of X hidden (2 W stages of 12 KB suffice)
+  static constexpr int kXStages = BN <= 16 ? (CSK ? 4 : 6) : (BN <= 128 ? 4 : 3);
   // CSK: two partial staging buffers of 128 x BN fp32 (rounds alternate)
   static constexpr int kStageBufBytes = CSK ? kTileN * BN * 4 : 0;
   // decode: output tiles staged in smem (two 128 x BN buffers, fp32-sized) and
   // written by the TMA tensor store, off the epilogue's critical path
   static constexpr int kYBufBytes = BN <= 32 ? kTileN * BN * 4 : 0;
+  static constexpr int kBudget = BN >= 256 ? 221 * 1024 : kSmemBudget;
   static constexpr int kWStagesRaw =
-      (kSmemBudget - kXStages * kXStageBytes - 2 * kStageBufBytes - 2 * kYBufBytes) / kWStageBytes;
+      (kBudget - kXStages * kXStageBytes - 2 * kStageBufBytes - 2 * kYBufBytes) / kWStageBytes;
   static constexpr int kWStages = (kWStagesRaw > 12 ? 12 : kWStagesRaw) & ~1;  // even: see header
   static constexpr int kStages = kWStages;                  // reported by the plan
   static constexpr int kDBufs = BN <= 128 ? 2 : 1;
@@ -253,6 +260,20 @@ struct StageIter {
   __device__ __forceinline__ int kt() const { return sg.kt0 + s * KS; }
   __device__ __forceinline__ int nt() const { return min(KS, sg.kt1 - kt()); }
 };
+
+// Output tile t -> (weight-row tile, batch tile).  Decode and moderate
+// prefill run the batch tiles of one weight tile back to back (the weight
+// tile is shared in L2); when X itself outgrows L2 the weight-row tiles of
+// one batch tile run back to back instead, so the X tile stays resident.
+__device__ __forceinline__ void tile_nm(const GemmArgs& a, int t, int& n_tile, int& m_tile) {
+  if (a.n_fastest) {
+    m_tile = t / a.n_tiles;
+    n_tile = t - m_tile * a.n_tiles;
+  } else {
+    n_tile = t / a.m_tiles;
+    m_tile = t - n_tile * a.m_tiles;
+  }
+}
 
 __device__ __forceinline__ int atom_add_acq_rel_gpu(int* p, int v) {
   int old;
@@ -513,12 +534,15 @@ __global__ void __launch_bounds__(kThreads, 1)
     const bool is_w = (warp == kWarpTmaW);
     if (!is_w) pdl_wait();  // X is the preceding kernel's output
     if (!is_w && lane == 0) CTA_STAMP(13);
-    const uint64_t pol = l2_evict_first_policy();
+    // decode streams every weight byte once (evict-first); with several
+    // batch tiles (prefill) the same weight tile is re-read per batch tile
+    const uint64_t pol = (a.m_tiles > 1 && !a.n_fastest) ? l2_evict_last_policy() : l2_evict_first_policy();
     StageIter<Sched, KS> it;
     it.start(a, sc, 0);
     for (int i = 0; i < n_st; ++i, it.next(a, sc)) {
       const int kt = it.kt(), nt = it.nt();
-      const int n_tile = it.sg.tile / a.m_tiles, m_tile = it.sg.tile - n_tile * a.m_tiles;
+      int n_tile, m_tile;
+      tile_nm(a, it.sg.tile, n_tile, m_tile);
       if (is_w) {
         const int s = i % C::kWStages;
         mbar_wait(&empty_w[s], ((i / C::kWStages) & 1) ^ 1);
@@ -729,7 +753,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     // ahead, so no global load sits on the epilogue's critical path (a cold
     // load behind the weight stream costs microseconds).
     auto scale_of = [&](const Seg& g) -> uint16_t {
-      const int nn = (g.tile / a.m_tiles) * kTileN + rr;
+      int nt, mt;
+      tile_nm(a, g.tile, nt, mt);
+      const int nn = nt * kTileN + rr;
       return nn < a.N ? __ldg(a.scales + nn) : static_cast<uint16_t>(0);
     };
     Seg sg_next;
@@ -756,7 +782,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (have_next) fs_next = scale_of(sg_next);
       const int d = lu % C::kDBufs;
       const uint32_t dph = (lu / C::kDBufs) & 1;
-      const int n_tile = sg.tile / a.m_tiles, m_tile = sg.tile % a.m_tiles;
+      int n_tile, m_tile;
+      tile_nm(a, sg.tile, n_tile, m_tile);
       const int n = n_tile * kTileN + rr;
       const int m0 = m_tile * BN;
       const uint32_t t_d = t_lane + d * C::kDCols;
@@ -1067,11 +1094,14 @@ struct Plan {
   int splits;   // max CTAs contributing to one tile
 };
 
+#ifndef LPQT_MAX_BN
+#define LPQT_MAX_BN 256
+#endif
 static int pick_bn(int64_t M) {
   if (M <= 16) return 16;
   if (M <= 32) return 32;
   if (M <= 64) return 64;
-  if (M <= 128) return 128;
+  if (M <= 128 || LPQT_MAX_BN == 128) return 128;
   return 256;
 }
 
@@ -1416,6 +1446,8 @@ int lpqt_w6a16_linear_ex(const uint8_t* tiles, const uint16_t* scales, const uin
   args.n_tiles = p.n_tiles;
   args.m_tiles = p.m_tiles;
   args.tile_count = static_cast<int>(p.tiles);
+  // X larger than ~1/3 of L2 (126 MB): keep each batch tile's X resident
+  args.n_fastest = (p.m_tiles > 1 && M * K * 2 > (int64_t)40 << 20) ? 1 : 0;
   args.y_dtype = y_dtype;
   args.y_layout = y_layout;
   args.sm = ShiftMuls{1u << 26, 1u << 28, 1u << 30};

@@ -320,3 +320,16 @@ def test_chained_layers_read_previous_output():
         assert normwise_rel(y1.double().cpu().numpy(), r1.cpu().numpy()) <= 1e-3
         r2 = (L.dequantize_tensor(L.quantize_tensor(W2, CGQ, bias_shift=True), "bias_shift") @ y1.double().T).T
         assert normwise_rel(y2.double().cpu().numpy(), r2.cpu().numpy()) <= 1e-3
+
+
+def test_prefill_large_x_weight_row_fastest_order():
+    """M x K x 2 B > 40 MB switches the tile order (weight-row tiles of one
+    batch tile back to back); results must not change."""
+    g = torch.Generator(device="cuda").manual_seed(17)
+    n, k, m = 640, 8192, 2600
+    W = (torch.randn(n, k, generator=g, device="cuda") * 0.02).half()
+    X = torch.randn(k, m, generator=g, device="cuda").half()
+    q = L.quantize_tensor(W, CGQ, bias_shift=True)
+    Y = L.gemm_quantized(q, X)
+    Y_ref = (L.dequantize_tensor(q, "bias_shift") @ X.double()).float()
+    assert normwise_rel(Y.cpu().numpy(), Y_ref.cpu().numpy()) <= REL_TOL
