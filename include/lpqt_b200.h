@@ -90,7 +90,8 @@ int lpqt_fp6_dequant_naive(const uint8_t* codes, const uint16_t* scales,
  * W[N, K] row-major with row stride ldw (elements), any LPQT_* dtype.
  * Writes scales[N] (f16 bits), folded[N] when bias_shift, and the canonical
  * planes seg4/seg2 of the row-major code stream (flat index r*K + k).
- * `codes_ws` (N*K bytes) is needed only when K % 8 != 0, else may be NULL. */
+ * `codes_ws` is ignored (ABI v1 argument; pass NULL).  Two launches: row
+ * scales, then encode + pack (8 codes per thread). */
 int lpqt_fp6_quantize_pack(const void* W, int dtype, int64_t N, int64_t K,
                            int64_t ldw, int bias_shift, uint16_t* scales,
                            uint16_t* folded, uint8_t* seg4, uint8_t* seg2,
@@ -113,6 +114,14 @@ int lpqt_fp6_dequantize_tensor(const uint8_t* seg4, const uint8_t* seg2,
 int64_t lpqt_fp6_tiles_bytes(int64_t N, int64_t K);
 int lpqt_fp6_prepack(const uint8_t* seg4, const uint8_t* seg2, int64_t N,
                      int64_t K, uint8_t* tiles, void* stream);
+/* quantize_tensor (quantizer.py:189-248) straight into the tile layout:
+ * scales[N] (+ folded[N] when bias_shift) exactly as lpqt_fp6_quantize_pack,
+ * and tiles (lpqt_fp6_tiles_bytes(N, K) bytes) equal to
+ * prepack(quantize_pack(W)) byte for byte, without the canonical planes. */
+int lpqt_fp6_quantize_tiles(const void* W, int dtype, int64_t N, int64_t K,
+                            int64_t ldw, int bias_shift, uint16_t* scales,
+                            uint16_t* folded, uint8_t* tiles,
+                            uint32_t* dev_flags, void* stream);
 int lpqt_fp6_unprepack(const uint8_t* tiles, int64_t N, int64_t K,
                        uint8_t* codes, void* stream);
 /* Standalone transform (the GEMM's register dequant): tiles -> out[N, K]

@@ -54,6 +54,7 @@ SIGNATURES = {
     "lpqt_fp6_dequantize_tensor": (_I32, [_P, _P, _P, _I32, _I64, _I64, _P, _I32, _P]),
     "lpqt_fp6_tiles_bytes": (_I64, [_I64, _I64]),
     "lpqt_fp6_prepack": (_I32, [_P, _P, _I64, _I64, _P, _P]),
+    "lpqt_fp6_quantize_tiles": (_I32, [_P, _I32, _I64, _I64, _I64, _I32, _P, _P, _P, _P, _P]),
     "lpqt_fp6_unprepack": (_I32, [_P, _I64, _I64, _P, _P]),
     "lpqt_fp6_tiles_dequant": (_I32, [_P, _P, _I64, _I64, _P, _P]),
     "lpqt_stage_activations": (_I32, [_P, _I32, _I64, _I64, _I64, _P, _I64, _P]),

@@ -75,87 +75,274 @@ __global__ void encode_kernel(const void* __restrict__ x, int64_t n, uint8_t* __
   if (bad) atomicOr(flags, LPQT_F_NONFINITE);
 }
 
-// ---- K1: fused per-row quantize ----------------------------------------------
-// One CTA per row (grid-stride): pass 1 row max|w| + finiteness, pass 2
-// encode + pack.  K % 8 == 0: each thread packs 8 codes -> 4 seg4 bytes
-// (one u32) + 2 seg2 bytes (one u16), rows are byte aligned.  Otherwise codes
-// go to `codes_ws` and the flat pack kernel runs afterwards.
+// ---- fast exact encode for binary16 / bfloat16 inputs ------------------------
+// For w in f16 or bf16 and S a binary16 scale, the exact quotient q = |w| / S
+// is never closer than 2^-15 (relative) to a grid midpoint m unless it equals
+// it: w - m*S is a nonzero multiple of a granularity >= 2^-15 * m*S (w has
+// <= 11 significant bits, m*S <= 15).  So RN_f32(q) lands on the same side of
+// every midpoint as q (and on m exactly iff q == m), the reference's f64
+// quotient does too (quantizer.py:228), and the hardware RNE conversion to
+// e3m2 (cvt.rn.satfinite.e3m2x2.f32) reproduces searchsorted(mids, q, 'right')
+// with the ties-to-even fix-up (codec.py:125-129): ties go to the even
+// mantissa = the even grid index, and q > 26 saturates to 28 (idx 31).  The
+// sign is applied separately so -0.0 -> code 0 (codec.py:130).
+// f32 / f64 inputs keep the literal f64 path (fp6_encode above).
+__device__ __forceinline__ uint32_t fp6_encode2_cvt(float w0, float w1, float S) {
+  const float q0 = __fdiv_rn(fabsf(w0), S), q1 = __fdiv_rn(fabsf(w1), S);
+  uint16_t r;
+  asm("cvt.rn.satfinite.e3m2x2.f32 %0, %1, %2;" : "=h"(r) : "f"(q1), "f"(q0));
+  return static_cast<uint32_t>(r) | (w0 < 0.f ? 0x20u : 0u) | (w1 < 0.f ? 0x2000u : 0u);
+}
+
 template <int DT>
-__global__ void __launch_bounds__(256) quantize_rows_kernel(const void* __restrict__ W, int64_t N, int64_t K,
-                                                            int64_t ldw, int bias_shift, uint16_t* __restrict__ scales,
-                                                            uint16_t* __restrict__ folded, uint8_t* __restrict__ seg4,
-                                                            uint8_t* __restrict__ seg2, uint8_t* __restrict__ codes_ws,
-                                                            uint32_t* __restrict__ flags) {
-  __shared__ double mids[32];
-  __shared__ double red[8];
-  __shared__ double s_scale;
-  load_mids(mids);
-  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  const bool fused = (K % 8) == 0;
-  for (int64_t r = blockIdx.x; r < N; r += gridDim.x) {
-    const char* row = static_cast<const char*>(W);
-    const int64_t base = r * ldw;
-    // pass 1: peak (quantizer.py:225) and finiteness (quantizer.py:200)
-    double peak = 0.0;
+struct InTraits {
+  using Acc = float;
+  static constexpr bool kCvt = true;
+};
+template <>
+struct InTraits<LPQT_F32> {
+  using Acc = float;
+  static constexpr bool kCvt = false;
+};
+template <>
+struct InTraits<LPQT_F64> {
+  using Acc = double;
+  static constexpr bool kCvt = false;
+};
+
+// 8 consecutive elements from a 16-byte aligned address, widened exactly
+template <int DT>
+__device__ __forceinline__ void load8(const void* p, typename InTraits<DT>::Acc v[8]) {
+  const uint4* q = static_cast<const uint4*>(p);
+  if constexpr (DT == LPQT_F16 || DT == LPQT_BF16) {
+    const uint4 u = __ldg(q);
+    const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      if constexpr (DT == LPQT_F16) {
+        const float2 f = __half22float2(*reinterpret_cast<const __half2*>(&w[i]));
+        v[2 * i] = f.x;
+        v[2 * i + 1] = f.y;
+      } else {
+        v[2 * i] = __uint_as_float(w[i] << 16);
+        v[2 * i + 1] = __uint_as_float(w[i] & 0xFFFF0000u);
+      }
+    }
+  } else if constexpr (DT == LPQT_F32) {
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      const float4 f = __ldg(reinterpret_cast<const float4*>(q) + i);
+      v[4 * i] = f.x, v[4 * i + 1] = f.y, v[4 * i + 2] = f.z, v[4 * i + 3] = f.w;
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const double2 d = __ldg(reinterpret_cast<const double2*>(q) + i);
+      v[2 * i] = d.x, v[2 * i + 1] = d.y;
+    }
+  }
+}
+template <int DT>
+__device__ __forceinline__ typename InTraits<DT>::Acc load1(const void* p, int64_t i) {
+  if constexpr (DT == LPQT_F64) return static_cast<const double*>(p)[i];
+  else return static_cast<float>(load_as_double<DT>(p, i));
+}
+template <int DT>
+__device__ __forceinline__ int elem_bytes() {
+  return DT == LPQT_F64 ? 8 : DT == LPQT_F32 ? 4 : 2;
+}
+
+// 8 codes -> one u64 (byte j = code of element j)
+template <int DT>
+__device__ __forceinline__ uint64_t encode8(const typename InTraits<DT>::Acc v[8], float Sf, double Sd,
+                                            const double* __restrict__ mids) {
+  uint64_t c = 0;
+  if constexpr (InTraits<DT>::kCvt) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) c |= static_cast<uint64_t>(fp6_encode2_cvt(v[2 * i], v[2 * i + 1], Sf)) << (16 * i);
+  } else {
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+      c |= static_cast<uint64_t>(fp6_encode(static_cast<double>(v[i]) / Sd, mids)) << (8 * i);
+  }
+  return c;
+}
+
+template <int DT>
+__device__ __forceinline__ uint32_t encode1(typename InTraits<DT>::Acc v, float S, const double* __restrict__ mids) {
+  if constexpr (InTraits<DT>::kCvt) return fp6_encode2_cvt(v, 0.f, S) & 0xFFu;
+  else return fp6_encode(static_cast<double>(v) / static_cast<double>(S), mids);
+}
+
+// ---- K1a: per-row scales (quantizer.py:200-201, :225-227, _round_scales_f16
+// :142-153; fold dequant.py:61-69).  One warp per row, 16-byte loads.
+template <int DT>
+__global__ void __launch_bounds__(256) row_scales_kernel(const void* __restrict__ W, int64_t N, int64_t K,
+                                                         int64_t ldw, int vec, int bias_shift,
+                                                         uint16_t* __restrict__ scales, uint16_t* __restrict__ folded,
+                                                         uint32_t* __restrict__ flags) {
+  using Acc = typename InTraits<DT>::Acc;
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  uint32_t f = 0;
+  for (int64_t r = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); r < N; r += warps) {
+    const char* row = static_cast<const char*>(W) + r * ldw * elem_bytes<DT>();
+    Acc peak = 0;
     bool bad = false;
-    for (int64_t k = tid; k < K; k += blockDim.x) {
-      const double v = load_as_double<DT>(row, base + k);
-      if (!isfinite(v)) bad = true;
+    const int64_t k8 = vec ? K / 8 * 8 : 0;
+    for (int64_t k = 8 * lane; k < k8; k += 256) {
+      Acc v[8];
+      load8<DT>(row + k * elem_bytes<DT>(), v);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        bad |= !isfinite(v[j]);
+        peak = fmax(peak, fabs(v[j]));
+      }
+    }
+    for (int64_t k = k8 + lane; k < K; k += 32) {
+      const Acc v = load1<DT>(row, k);
+      bad |= !isfinite(v);
       peak = fmax(peak, fabs(v));
     }
-    if (__syncthreads_or(bad)) {
-      if (tid == 0) atomicOr(flags, LPQT_F_NONFINITE);
-    }
+    if (__any_sync(0xffffffffu, bad)) f |= LPQT_F_NONFINITE;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) peak = fmax(peak, __shfl_xor_sync(0xffffffffu, peak, o));
-    if (lane == 0) red[wid] = peak;
-    __syncthreads();
-    if (tid == 0) {
-      double p = red[0];
-      for (int i = 1; i < (int)(blockDim.x >> 5); ++i) p = fmax(p, red[i]);
-      // quantizer.py:227 + _round_scales_f16 (:142-153)
+    if (lane == 0) {
+      const double p = static_cast<double>(peak);
       const double raw = (p == 0.0) ? 1.0 : p / 28.0;
-      __half s = __double2half(raw);
-      uint16_t sb = __half_as_ushort(s);
-      if ((sb & 0x7FFFu) == 0x7C00u) {
-        atomicOr(flags, LPQT_F_SCALE_INF);
-      }
+      uint16_t sb = __half_as_ushort(__double2half(raw));
+      if ((sb & 0x7FFFu) == 0x7C00u) f |= LPQT_F_SCALE_INF;
       if ((sb & 0x7FFFu) == 0) sb = 0x0001u;  // underflow clamps to 2^-24
       scales[r] = sb;
-      const double sd = static_cast<double>(__half2float(__ushort_as_half(sb)));
       if (bias_shift) {
-        // dequant.py:61-69: folded = S * 2^12, overflow above 65504
-        const double f = sd * 4096.0;
-        if (f > 65504.0) atomicOr(flags, LPQT_F_FOLD_OVERFLOW);
-        folded[r] = (f > 65504.0) ? (uint16_t)0x7C00u : __half_as_ushort(__double2half(f));
+        const double fv = static_cast<double>(__half2float(__ushort_as_half(sb))) * 4096.0;
+        if (fv > 65504.0) f |= LPQT_F_FOLD_OVERFLOW;
+        folded[r] = (fv > 65504.0) ? (uint16_t)0x7C00u : __half_as_ushort(__double2half(fv));
       }
-      s_scale = sd;
     }
-    __syncthreads();
-    const double S = s_scale;
-    // pass 2: codes = encode(W / S) (quantizer.py:228-229, f64 division)
-    if (fused) {
-      const int64_t groups = K / 8;
-      for (int64_t g = tid; g < groups; g += blockDim.x) {
-        uint32_t c[8];
+  }
+  if (f) atomicOr(flags, f);
+}
+
+__device__ __forceinline__ void load_mids_f64(double* smem_mids) {
+  for (int i = threadIdx.x; i < 32; i += blockDim.x)
+    smem_mids[i] = i < 31 ? 0.5 * (fp6_magnitude(i) + fp6_magnitude(i + 1)) : 1e300;
+  __syncthreads();
+}
+
+// ---- K1b: codes -> canonical planes (quantizer.py:228-229, packing.py:63-90).
+// Thread per 8 consecutive codes of the flat row-major stream: one u32 of
+// seg4 and one u16 of seg2 (groups are 8-aligned in the flat index, so this
+// holds for any K; the last group pads with code 0 like packing.py:73).
+template <int DT>
+__global__ void __launch_bounds__(256) encode_planes_kernel(const void* __restrict__ W, int64_t N, int64_t K,
+                                                            int64_t ldw, int vec,
+                                                            const uint16_t* __restrict__ scales,
+                                                            uint8_t* __restrict__ seg4, uint8_t* __restrict__ seg2) {
+  using Acc = typename InTraits<DT>::Acc;
+  __shared__ double mids[32];
+  if constexpr (!InTraits<DT>::kCvt) load_mids_f64(mids);
+  const int64_t total = N * K, groups = (total + 7) / 8;
+  for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < groups; g += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i0 = 8 * g;
+    uint64_t c = 0;
+    if (vec) {  // vec => K % 8 == 0: the whole group lies in one row
+      const int64_t r = i0 / K, k = i0 - r * K;
+      Acc v[8];
+      load8<DT>(static_cast<const char*>(W) + (r * ldw + k) * elem_bytes<DT>(), v);
+      const float s = __half2float(__ushort_as_half(scales[r]));
+      c = encode8<DT>(v, s, static_cast<double>(s), mids);
+    } else {
+      int64_t r = i0 / K, k = i0 - r * K;
 #pragma unroll
-        for (int j = 0; j < 8; ++j) c[j] = fp6_encode(load_as_double<DT>(row, base + g * 8 + j) / S, mids);
-        uint32_t s4 = 0, s2 = 0;
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          s4 |= (c[j] >> 2) << (4 * j);
-          s2 |= (c[j] & 3u) << (2 * j);
+      for (int j = 0; j < 8; ++j) {
+        if (i0 + j < total) {
+          const Acc v = load1<DT>(W, r * ldw + k);
+          const float s = __half2float(__ushort_as_half(scales[r]));
+          c |= static_cast<uint64_t>(encode1<DT>(v, s, mids)) << (8 * j);
         }
-        const int64_t i0 = r * K + g * 8;
-        *reinterpret_cast<uint32_t*>(seg4 + i0 / 2) = s4;
-        *reinterpret_cast<uint16_t*>(seg2 + i0 / 4) = static_cast<uint16_t>(s2);
+        if (++k == K) k = 0, ++r;
+      }
+    }
+    uint32_t s4 = 0, s2 = 0;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const uint32_t cj = static_cast<uint32_t>(c >> (8 * j)) & 0x3Fu;
+      s4 |= (cj >> 2) << (4 * j);
+      s2 |= (cj & 3u) << (2 * j);
+    }
+    *reinterpret_cast<uint32_t*>(seg4 + 4 * g) = s4;
+    *reinterpret_cast<uint16_t*>(seg2 + 2 * g) = static_cast<uint16_t>(s2);
+  }
+}
+
+// ---- K1c: codes straight into the GEMM tile layout (no canonical planes).
+// Thread per (row n < Np, 64-weight half of a 128-k tile): 8 x 16 B loads,
+// 64 codes, 12 words (fp6x32 layout v2, common.cuh), 3 x 16 B stores.  Rows
+// are the fastest thread index so every warp store writes 512 contiguous
+// bytes of one [khalf][quad] plane.  Padding rows / columns get code 0
+// (exactly what prepack writes).
+__device__ __forceinline__ void pack_words_from_bytes(const uint32_t cw[8], uint32_t w[6]) {
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    w[i] = cw[i] | (((cw[6] >> (2 * i)) & 0x03030303u) << 6);
+    w[3 + i] = cw[3 + i] | (((cw[7] >> (2 * i)) & 0x03030303u) << 6);
+  }
+}
+
+template <int DT>
+__global__ void __launch_bounds__(256) encode_tiles_kernel(const void* __restrict__ W, int64_t N, int64_t K,
+                                                           int64_t ldw, int vec, const uint16_t* __restrict__ scales,
+                                                           int64_t Np, int64_t k_tiles, uint8_t* __restrict__ tiles) {
+  using Acc = typename InTraits<DT>::Acc;
+  __shared__ double mids[32];
+  if constexpr (!InTraits<DT>::kCvt) load_mids_f64(mids);
+  const int64_t total = Np * k_tiles * 2;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+    const int rr = static_cast<int>(t & 127);
+    const int64_t s = t >> 7;
+    const int kh = static_cast<int>(s & 1);
+    const int64_t tile = s >> 1;  // rt * k_tiles + kt
+    const int64_t rt = tile / k_tiles, kt = tile - rt * k_tiles;
+    const int64_t n = rt * kTileN + rr, k0 = kt * kTileK + kh * 64;
+    uint32_t cw[16];
+    if (n < N) {
+      const float Sf = __half2float(__ushort_as_half(scales[n]));
+      const double Sd = static_cast<double>(Sf);
+      const char* row = static_cast<const char*>(W) + n * ldw * elem_bytes<DT>();
+      if (vec && k0 + 64 <= K) {
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          Acc v[8];
+          load8<DT>(row + (k0 + 8 * q) * elem_bytes<DT>(), v);
+          const uint64_t c = encode8<DT>(v, Sf, Sd, mids);
+          cw[2 * q] = static_cast<uint32_t>(c);
+          cw[2 * q + 1] = static_cast<uint32_t>(c >> 32);
+        }
+      } else {
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          Acc v[8];
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const int64_t k = k0 + 8 * q + j;
+            v[j] = k < K ? load1<DT>(row, k) : Acc(0);
+          }
+          const uint64_t c = encode8<DT>(v, Sf, Sd, mids);
+          cw[2 * q] = static_cast<uint32_t>(c);
+          cw[2 * q + 1] = static_cast<uint32_t>(c >> 32);
+        }
       }
     } else {
-      for (int64_t k = tid; k < K; k += blockDim.x) {
-        codes_ws[r * K + k] = static_cast<uint8_t>(fp6_encode(load_as_double<DT>(row, base + k) / S, mids));
-      }
+#pragma unroll
+      for (int i = 0; i < 16; ++i) cw[i] = 0;
     }
-    __syncthreads();
+    uint32_t w[12];
+    pack_words_from_bytes(cw, w);
+    pack_words_from_bytes(cw + 8, w + 6);
+    uint4* dst = reinterpret_cast<uint4*>(tiles + tile * kTileBytes) + (kh * 3) * kTileN + rr;
+#pragma unroll
+    for (int q = 0; q < 3; ++q) dst[q * kTileN] = make_uint4(w[4 * q], w[4 * q + 1], w[4 * q + 2], w[4 * q + 3]);
   }
 }
 
@@ -349,20 +536,56 @@ int lpqt_fp6_dequant_naive(const uint8_t* codes, const uint16_t* scales, int64_t
   return check_launch();
 }
 
+static int quantize_scales(const void* W, int dtype, int64_t N, int64_t K, int64_t ldw, int vec, int bias_shift,
+                           uint16_t* scales, uint16_t* folded, uint32_t* dev_flags, cudaStream_t st) {
+  const int g = static_cast<int>((N + 7) / 8 < 148 * 8 ? (N + 7) / 8 : 148 * 8);
+  LPQT_DISPATCH_DT(dtype, row_scales_kernel<DT><<<g, 256, 0, st>>>(W, N, K, ldw, vec, bias_shift, scales, folded,
+                                                                    dev_flags));
+  note_launch();
+  return check_launch();
+}
+
+static int rows_vectorizable(const void* W, int64_t ldw) {
+  return (reinterpret_cast<uintptr_t>(W) % 16 == 0) && (ldw % 8 == 0);
+}
+
 int lpqt_fp6_quantize_pack(const void* W, int dtype, int64_t N, int64_t K, int64_t ldw, int bias_shift,
                            uint16_t* scales, uint16_t* folded, uint8_t* seg4, uint8_t* seg2, uint8_t* codes_ws,
                            uint32_t* dev_flags, void* stream) {
+  (void)codes_ws;  // no longer needed (ABI v1 argument)
   if (N < 0 || K < 0 || ldw < K) return LPQT_E_SHAPE;
   if (N == 0 || K == 0) return LPQT_OK;
-  if (K % 8 != 0 && codes_ws == nullptr) return LPQT_E_WORKSPACE;
   if (bias_shift && folded == nullptr) return LPQT_E_INVALID_INPUT;
-  const int g = static_cast<int>(N < 148 * 16 ? N : 148 * 16);
-  LPQT_DISPATCH_DT(dtype, quantize_rows_kernel<DT><<<g, 256, 0, as_stream(stream)>>>(
-                              W, N, K, ldw, bias_shift, scales, folded, seg4, seg2, codes_ws, dev_flags));
+  if (dtype < LPQT_F64 || dtype > LPQT_BF16) return LPQT_E_UNSUPPORTED;
+  const cudaStream_t st = as_stream(stream);
+  const int vec = rows_vectorizable(W, ldw);
+  int rc = quantize_scales(W, dtype, N, K, ldw, vec, bias_shift, scales, folded, dev_flags, st);
+  if (rc != LPQT_OK) return rc;
+  const int64_t groups = (N * K + 7) / 8;
+  const int pv = vec && (K % 8 == 0);
+  LPQT_DISPATCH_DT(dtype, encode_planes_kernel<DT><<<grid_for(groups, 256), 256, 0, st>>>(W, N, K, ldw, pv, scales,
+                                                                                         seg4, seg2));
   note_launch();
-  int st = check_launch();
-  if (st != LPQT_OK || K % 8 == 0) return st;
-  return lpqt_fp6_pack(codes_ws, N * K, seg4, seg2, dev_flags, stream);
+  return check_launch();
+}
+
+int lpqt_fp6_quantize_tiles(const void* W, int dtype, int64_t N, int64_t K, int64_t ldw, int bias_shift,
+                            uint16_t* scales, uint16_t* folded, uint8_t* tiles, uint32_t* dev_flags, void* stream) {
+  if (N < 0 || K < 0 || ldw < K) return LPQT_E_SHAPE;
+  if (N == 0 || K == 0) return LPQT_OK;
+  if (bias_shift && folded == nullptr) return LPQT_E_INVALID_INPUT;
+  if (dtype < LPQT_F64 || dtype > LPQT_BF16) return LPQT_E_UNSUPPORTED;
+  if (tiles == nullptr || scales == nullptr) return LPQT_E_INVALID_INPUT;
+  const cudaStream_t st = as_stream(stream);
+  const int vec = rows_vectorizable(W, ldw);
+  int rc = quantize_scales(W, dtype, N, K, ldw, vec, bias_shift, scales, folded, dev_flags, st);
+  if (rc != LPQT_OK) return rc;
+  const int64_t Np = (N + kTileN - 1) / kTileN * kTileN, k_tiles = (K + kTileK - 1) / kTileK;
+  const int64_t threads = Np * k_tiles * 2;
+  LPQT_DISPATCH_DT(dtype, encode_tiles_kernel<DT><<<grid_for(threads, 256), 256, 0, st>>>(W, N, K, ldw, vec, scales,
+                                                                                         Np, k_tiles, tiles));
+  note_launch();
+  return check_launch();
 }
 
 int lpqt_fp6_dequantize_tensor(const uint8_t* seg4, const uint8_t* seg2, const uint16_t* row_scale, int path,

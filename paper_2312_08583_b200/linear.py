@@ -57,12 +57,23 @@ class Fp6Weight:
 
     @classmethod
     def quantize(cls, W, bias_shift: bool = True) -> "Fp6Weight":
-        """RTN per-row FP6 quantize on the GPU (quantizer.py:189-248), then prepack."""
-        from .quantizer import _weights_to_device, quantize_device
+        """RTN per-row FP6 quantize on the GPU (quantizer.py:189-248) straight
+        into the tile layout (`lpqt_fp6_quantize_tiles`; byte-identical to
+        prepack of the canonical planes)."""
+        from .quantizer import _weights_to_device
         w, _ = _weights_to_device(W)
         n, k = (int(v) for v in w.shape)
-        d = quantize_device(w, bias_shift)
-        return cls.from_planes(d["seg4"], d["seg2"], d["scales"], n, k, d["folded"])
+        t = _lib.torch()
+        dev = w.device
+        tiles = t.empty(int(_lib.load().lpqt_fp6_tiles_bytes(n, k)), dtype=t.uint8, device=dev)
+        scales = t.empty(n, dtype=t.float16, device=dev)
+        folded = t.empty(n, dtype=t.float16, device=dev) if bias_shift else None
+        flags = _lib.Flags()
+        _lib.check(_lib.load().lpqt_fp6_quantize_tiles(
+            w.data_ptr(), _lib.dtype_code(w.dtype), n, k, int(w.stride(0)) if n else k, int(bool(bias_shift)),
+            scales.data_ptr(), _lib.ptr(folded), tiles.data_ptr(), flags.ptr, _lib.stream_ptr()), "quantize_tiles")
+        flags.raise_if_set()
+        return cls(tiles, scales, n, k, folded, static=True)
 
     @classmethod
     def from_quantized(cls, q) -> "Fp6Weight":

@@ -170,11 +170,10 @@ def quantize_device(w, bias_shift: bool = True):
     if seg4.numel():
         seg4[-4:].zero_()
         seg2[-4:].zero_()
-    ws = t.empty(nk, dtype=t.uint8, device=dev) if k % 8 else None
     flags = _lib.Flags()
     _lib.check(_lib.load().lpqt_fp6_quantize_pack(
         w.data_ptr(), _lib.dtype_code(w.dtype), n, k, k, int(bool(bias_shift)), scales.data_ptr(),
-        _lib.ptr(folded), seg4.data_ptr(), seg2.data_ptr(), _lib.ptr(ws), flags.ptr, _lib.stream_ptr()),
+        _lib.ptr(folded), seg4.data_ptr(), seg2.data_ptr(), None, flags.ptr, _lib.stream_ptr()),
         "quantize_tensor")
     flags.raise_if_set()
     return {"scales": scales, "folded": folded, "seg4": seg4, "seg2": seg2}

@@ -94,6 +94,113 @@ def test_quantize_llama_shape_codes_match_oracle():
     assert np.array_equal(q.payload.seg_tail.cpu().numpy(), o["seg2"])
 
 
+_TORCH_DT = {"f64": torch.float64, "f32": torch.float32, "f16": torch.float16, "bf16": torch.bfloat16}
+
+
+def _planes_then_prepack(Wt):
+    q = L.quantize_tensor(Wt, CGQ, bias_shift=True)
+    n, k = Wt.shape
+    return L.Fp6Weight.from_planes(q.payload.seg4, q.payload.seg_tail, q.scales, n, k, q.folded_scales), q
+
+
+def _oracle_of(Wt):
+    # bf16 / f16 / f32 widen to f64 exactly; the reference quantizes in f64
+    return O.quantize_tensor(Wt.double().cpu().numpy(), bias_shift=True)
+
+
+@pytest.mark.parametrize("dt", ["f16", "bf16", "f32", "f64"])
+@pytest.mark.parametrize("shape", [(1, 1), (3, 5), (130, 300), (129, 1000), (256, 4096)])
+def test_quantize_tiles_equals_prepacked_planes(dt, shape):
+    """lpqt_fp6_quantize_tiles == prepack(lpqt_fp6_quantize_pack) byte for
+    byte, and both agree with the oracle (quantizer.py:189-248)."""
+    g = torch.Generator().manual_seed(hash((dt, shape)) % 2**31)
+    Wt = (torch.randn(shape, generator=g, dtype=torch.float64) * 0.05).to(_TORCH_DT[dt])
+    Wt[torch.rand(shape, generator=g) < 0.03] = 0
+    Wt = Wt.cuda()
+    fused = L.Fp6Weight.quantize(Wt)
+    ref, q = _planes_then_prepack(Wt)
+    assert torch.equal(fused.tiles, ref.tiles)
+    assert torch.equal(fused.scales.view(torch.int16), ref.scales.view(torch.int16))
+    assert torch.equal(fused.folded.view(torch.int16), q.folded_scales.view(torch.int16))
+    o = _oracle_of(Wt)
+    assert np.array_equal(q.scales.cpu().numpy().view(np.uint16), o["scales"].view(np.uint16))
+    assert np.array_equal(q.payload.seg4.cpu().numpy(), o["seg4"])
+    assert np.array_equal(q.payload.seg_tail.cpu().numpy(), o["seg2"])
+
+
+def _adversarial_rows(dt):
+    """Rows whose scale is pinned (peak = 28 * S0 exactly) and whose entries
+    sit exactly on every grid midpoint m_i * S0, one ulp of the input dtype
+    either side of it, on -0.0, on tiny negatives and near saturation."""
+    tdt = _TORCH_DT[dt]
+    ibits = {torch.float16: torch.int16, torch.bfloat16: torch.int16,
+             torch.float32: torch.int32, torch.float64: torch.int64}[tdt]
+    rows = []
+    for s0 in (2.0 ** -7, 1.5 * 2 ** -9, 1.25 * 2 ** -3, 1.75 * 2 ** -12, 0.0123, 3.0e-5):
+        s0 = float(np.float16(s0))
+        row = [28.0 * s0, -28.0 * s0, -0.0, 0.0, -1e-30, 1e-30, 27.9 * s0, -26.0 * s0]
+        for m in O.grid_midpoints():
+            v = torch.tensor([m * s0], dtype=torch.float64).to(tdt)
+            b = v.view(ibits)
+            for x in (v, (b + 1).view(tdt), (b - 1).view(tdt)):
+                row += [float(x), -float(x)]
+        rows.append(row)
+    W = torch.zeros((len(rows), max(len(r) for r in rows)), dtype=torch.float64)
+    for i, r in enumerate(rows):
+        W[i, :len(r)] = torch.tensor(r, dtype=torch.float64)
+    return W.to(tdt)
+
+
+@pytest.mark.parametrize("dt", ["f16", "bf16", "f32", "f64"])
+def test_quantize_midpoint_ties_and_signs_vs_oracle(dt):
+    Wt = _adversarial_rows(dt).cuda()
+    fused = L.Fp6Weight.quantize(Wt)
+    ref, q = _planes_then_prepack(Wt)
+    o = _oracle_of(Wt)
+    assert np.array_equal(q.scales.cpu().numpy().view(np.uint16), o["scales"].view(np.uint16))
+    assert np.array_equal(q.payload.seg4.cpu().numpy(), o["seg4"])
+    assert np.array_equal(q.payload.seg_tail.cpu().numpy(), o["seg2"])
+    assert torch.equal(fused.tiles, ref.tiles)
+    assert torch.equal(fused.codes().cpu(), torch.from_numpy(O.unpack(o["seg4"], o["seg2"], Wt.numel())
+                                                             .reshape(Wt.shape)))
+
+
+@pytest.mark.parametrize("offset", [0, 8, 3])
+def test_quantize_tiles_strided_rows(offset):
+    """ldw > K and 16-byte-misaligned rows go through the scalar path with
+    the same result."""
+    n, k, ldw = 200, 520, 600
+    g = torch.Generator().manual_seed(5)
+    big = (torch.randn((n, ldw), generator=g) * 0.1).half().cuda()
+    view = big[:, offset:offset + k]
+    want = L.Fp6Weight.quantize(view.contiguous())
+    from paper_2312_08583_b200 import _lib
+    lib = _lib.load()
+    tiles = torch.empty(lib.lpqt_fp6_tiles_bytes(n, k), dtype=torch.uint8, device="cuda")
+    scales = torch.empty(n, dtype=torch.float16, device="cuda")
+    flags = _lib.Flags()
+    st = lib.lpqt_fp6_quantize_tiles(view.data_ptr(), _lib.F16, n, k, ldw, 0, scales.data_ptr(), None,
+                                     tiles.data_ptr(), flags.ptr, _lib.stream_ptr())
+    assert st == 0
+    flags.raise_if_set()
+    assert torch.equal(tiles, want.tiles)
+    assert torch.equal(scales.view(torch.int16), want.scales.view(torch.int16))
+
+
+def test_quantize_tiles_errors():
+    W = torch.ones((4, 8), dtype=torch.float16, device="cuda")
+    W[1, 3] = float("nan")
+    with pytest.raises(L.InvalidInput):
+        L.Fp6Weight.quantize(W)
+    W = torch.full((2, 8), 3.0e38, dtype=torch.bfloat16, device="cuda")
+    with pytest.raises(L.InvalidInput):
+        L.Fp6Weight.quantize(W)   # S = peak / 28 overflows binary16
+    W = torch.full((2, 8), 60000.0, dtype=torch.float16, device="cuda")
+    with pytest.raises(L.ScaleOverflow):
+        L.Fp6Weight.quantize(W)   # S * 2^12 > 65504 (bias shift)
+    assert L.Fp6Weight.quantize(W, bias_shift=False).folded is None
+
+
 def test_empty_inputs():
     q = L.quantize_tensor(np.zeros((0, 5)), CGQ, bias_shift=True)
     assert q.scales.size == 0 and q.payload.code_count == 0
