@@ -182,6 +182,29 @@ int lpqt_w6a16_linear_ex(const uint8_t* tiles, const uint16_t* scales,
                          int64_t ldy, int split_k, void* workspace,
                          int64_t workspace_bytes, int flags, void* stream);
 
+/* The linear that will run next on the same stream (decode chains: QKV ->
+ * O -> gate_up -> down -> next block's QKV).  With it, each CTA of this
+ * launch, once it has requested its last weight tile, issues bulk L2
+ * prefetches (cp.async.bulk.prefetch.L2) of the first `bytes_per_cta`
+ * bytes that the matching CTA of the next launch will stream (derived from
+ * that launch's plan; 0 = 64 KiB).  Weights are static, so this only moves
+ * HBM reads earlier: HBM keeps streaming through this launch's drain and
+ * the next one's start-up.  Ignored when the next launch has more than one
+ * batch tile (prefill).  Not a reference interface (no counterpart). */
+typedef struct lpqt_next_linear {
+  const uint8_t* tiles;   /* next weight, tile layout */
+  int64_t M, N, K;        /* next problem (plan inputs) */
+  int split_k, flags;     /* next launch's split_k / schedule flags */
+  int64_t bytes_per_cta;  /* prefetch depth per next-launch CTA */
+} lpqt_next_linear;
+
+int lpqt_w6a16_linear_pf(const uint8_t* tiles, const uint16_t* scales,
+                         const uint16_t* Xt, int64_t ldx, int64_t M, int64_t N,
+                         int64_t K, void* Y, int y_dtype, int y_layout,
+                         int64_t ldy, int split_k, void* workspace,
+                         int64_t workspace_bytes, int flags,
+                         const lpqt_next_linear* next, void* stream);
+
 /* Number of kernel launches performed by this library since load (for the
  * bench's gpu_launches claim). */
 int64_t lpqt_launch_count(void);

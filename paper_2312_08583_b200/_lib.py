@@ -38,6 +38,14 @@ _P = ctypes.c_void_p
 _I64 = ctypes.c_int64
 _I32 = ctypes.c_int
 
+
+
+class NextLinear(ctypes.Structure):
+    """lpqt_next_linear (include/lpqt_b200.h): the launch that follows on the stream."""
+    _fields_ = [("tiles", ctypes.c_void_p), ("M", ctypes.c_int64), ("N", ctypes.c_int64), ("K", ctypes.c_int64),
+                ("split_k", ctypes.c_int), ("flags", ctypes.c_int), ("bytes_per_cta", ctypes.c_int64)]
+
+
 # name -> (restype, argtypes); every symbol declared in include/lpqt_b200.h
 SIGNATURES = {
     "lpqt_strerror": (ctypes.c_char_p, [_I32]),
@@ -64,6 +72,8 @@ SIGNATURES = {
     "lpqt_w6a16_linear": (_I32, [_P, _P, _P, _I64, _I64, _I64, _I64, _P, _I32, _I32, _I64, _I32, _P, _I64, _P]),
     "lpqt_w6a16_linear_ex": (_I32, [_P, _P, _P, _I64, _I64, _I64, _I64, _P, _I32, _I32, _I64, _I32, _P, _I64, _I32,
                                     _P]),
+    "lpqt_w6a16_linear_pf": (_I32, [_P, _P, _P, _I64, _I64, _I64, _I64, _P, _I32, _I32, _I64, _I32, _P, _I64, _I32,
+                                    ctypes.POINTER(NextLinear), _P]),
     "lpqt_launch_count": (_I64, []),
 }
 

@@ -96,6 +96,17 @@ struct GemmArgs {
   ShiftMuls sm;       // 2^26, 2^28, 2^30: right shifts on the FMA pipe (common.cuh)
 };
 
+// Cross-launch L2 prefetch of the NEXT linear's weights (lpqt_w6a16_linear_pf):
+// slice c = the first bytes the next launch's CTA c streams, derived from
+// that launch's plan (total > 0: stream-K, else cluster split-K).  A separate
+// kernel parameter: growing GemmArgs perturbs the epilogue's register budget.
+struct L2Prefetch {
+  const uint8_t* base;
+  int64_t total, bytes;
+  int count, ksteps, kstep, k_tiles, c, tiles;
+  uint32_t chunk;
+};
+
 template <int BN, bool CSK>
 struct Cfg {
   static constexpr int kKStep = BN <= 32 ? 2 : 1;           // 128-k tiles per pipeline stage
@@ -125,7 +136,7 @@ struct Cfg {
   static constexpr int kDCols = BN * kNAcc;
   static constexpr int kACols = kTmemCols - kDBufs * kDCols;
   static constexpr int kASlots = ((kACols / kAColsPerBuf) / kKStep) & ~1;  // even
-  static constexpr int kBarCount = 2 * kWStages + 2 * kXStages + 2 * kASlots + 2 * kDBufs + 4;
+  static constexpr int kBarCount = 2 * kWStages + 2 * kXStages + 2 * kASlots + 2 * kDBufs + 5;
   static constexpr int kSmemBytes = kXStages * kXStageBytes + kWStages * kWStageBytes + 2 * kStageBufBytes +
                                     2 * kYBufBytes + 8 * kBarCount + 16;
   static_assert(kWStages >= 2 && kXStages >= 2, "pipeline too shallow");
@@ -136,13 +147,20 @@ struct Cfg {
 };
 
 #ifdef LPQT_TRACE
-// per-CTA %globaltimer stamps: trace[cta * 24 + ev]
+// per-CTA stamps: trace[cta * 32 + ev] = %clock64 (cheap, SM-local); the
+// entry (ev 0) and exit (ev 6) stamps also record %globaltimer in slots 30
+// and 31 so the host maps cycles to a chip-wide time axis.  (A %globaltimer
+// read per stamp costs up to ~1 us and distorted dense stamp sequences.)
 #define CTA_STAMP(ev)                                                   \
   do {                                                                  \
     if (a.trace && blockIdx.x < 256) {                                  \
-      uint64_t gt;                                                      \
-      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));            \
-      a.trace[blockIdx.x * 24 + (ev)] = (long long)gt;                  \
+      long long ck = clock64();                                         \
+      a.trace[blockIdx.x * 32 + (ev)] = ck;                             \
+      if ((ev) == 0 || (ev) == 6) {                                     \
+        uint64_t gt;                                                    \
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));          \
+        a.trace[blockIdx.x * 32 + ((ev) == 0 ? 30 : 31)] = (long long)gt; \
+      }                                                                 \
     }                                                                   \
   } while (0)
 #else
@@ -150,7 +168,7 @@ struct Cfg {
   do {                \
   } while (0)
 #endif
-constexpr int kTraceLen = 256 * 24;
+constexpr int kTraceLen = 256 * 32;
 
 // ---------------------------------------------------------------------------
 // Work schedules.  Both present the CTA's work as a sequence of segments
@@ -176,12 +194,11 @@ __device__ __forceinline__ int sk_cta_of(const GemmArgs& a, int64_t p) {
 // A CTA's stream-K range [beg, end) in natural order; segments never
 // straddle a tile.
 struct SkSched {
-  int64_t beg, end;
+  int64_t beg;  // (the range end is beg + n: one 64-bit value kept live, not two)
   int n;
   __device__ __forceinline__ void init(const GemmArgs& a) {
     beg = sk_begin(a, blockIdx.x);
-    end = sk_begin(a, blockIdx.x + 1);
-    n = static_cast<int>(end - beg);
+    n = static_cast<int>(sk_begin(a, blockIdx.x + 1) - beg);
   }
   template <int KS>
   __device__ __forceinline__ bool seg_at(const GemmArgs& a, int i, Seg& sg) const {
@@ -189,8 +206,8 @@ struct SkSched {
     const int64_t p = beg + i;
     const int t = static_cast<int>(p / a.ksteps);
     const int s0 = static_cast<int>(p - (int64_t)t * a.ksteps);
-    const int64_t rem = end - p;
-    const int len = rem < (int64_t)(a.ksteps - s0) ? static_cast<int>(rem) : a.ksteps - s0;
+    const int rem = n - i;
+    const int len = rem < a.ksteps - s0 ? rem : a.ksteps - s0;
     sg.tile = t;
     sg.i0 = i;
     sg.len = len;
@@ -319,6 +336,19 @@ __device__ __forceinline__ void load_acc16(uint32_t t_d, int c0, int q0, int nac
   }
 }
 
+// Stream-K partial tile of contributor slot `blk` (= cta * 2 + idx): 128 x BN
+// fp32.  BN 16 stores it chunk-major (float4 chunk j of row r at [j][r]): a
+// warp's accesses to one chunk are 512 contiguous bytes, coalesced in global
+// and conflict-free once gathered into shared memory.  BN 32 keeps rows
+// contiguous (the chunk-major index math costs its epilogue registers).
+template <int BN>
+struct PartLayout {
+  static constexpr int kJStride = BN <= 16 ? kTileN : 1;  // float4 stride between chunks of a row
+  __device__ __forceinline__ static int64_t f4(int64_t blk, int j, int rr) {  // float4 index
+    return blk * (kTileN * BN / 4) + (BN <= 16 ? rr : rr * (BN / 4)) + (int64_t)j * kJStride;
+  }
+};
+
 // ---- DSMEM / cluster primitives ----------------------------------------------------
 __device__ __forceinline__ uint32_t mapa_shared(uint32_t addr, uint32_t rank) {
   uint32_t r;
@@ -359,6 +389,9 @@ __device__ __forceinline__ void cluster_sync_all() {
 }
 
 // ---- output tile staging + TMA tensor store (decode) --------------------------
+__device__ __forceinline__ void fence_proxy_async_global() {
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+}
 __device__ __forceinline__ void fence_proxy_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
@@ -428,7 +461,7 @@ __device__ __forceinline__ void ystage_put(const GemmArgs& a, uint32_t buf, int 
 template <int BN, bool CSK, bool RAGGED>
 __global__ void __launch_bounds__(kThreads, 1)
     w6a16_tcgen05_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constant__ CUtensorMap tmap_y,
-                         const GemmArgs a) {
+                         const GemmArgs a, const L2Prefetch pf) {
   using C = Cfg<BN, CSK>;
   constexpr int KS = C::kKStep;
   using Sched = typename std::conditional<CSK, CskSched, SkSched>::type;
@@ -450,7 +483,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* dempty = dfull + C::kDBufs;
   uint64_t* part_full = dempty + C::kDBufs;  // CSK [2]: this CTA's round partials from the senders
   uint64_t* stg_free = part_full + 2;        // CSK [2]: this CTA's staging buffer read by the reducer
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(stg_free + 2);
+  uint64_t* fix_bar = stg_free + 2;          // SK: partials gathered by bulk copy (last segment)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(fix_bar + 1);
   volatile int* last_flag = reinterpret_cast<volatile int*>(tmem_slot + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -493,9 +527,12 @@ __global__ void __launch_bounds__(kThreads, 1)
           mbar_init(&part_full[b], sc.C > 1 ? sc.C - 1 : 1);  // one remote arrive per sender
           mbar_init(&stg_free[b], 1);                         // one remote arrive by the reducer
         }
+      } else {
+        mbar_init(fix_bar, 1);
       }
       fence_mbar_init();
       pdl_launch_dependents();  // the next kernel may queue for this SM as soon as it frees
+      CTA_STAMP(19);
     }
     __syncwarp();
     named_bar_arrive(2, kThreads);
@@ -503,6 +540,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (warp == kWarpMma0) {
       tmem_alloc(tmem_slot, kTmemCols);
       tmem_relinquish();
+      if (lane == 0) CTA_STAMP(21);
     }
     if (warp == kWarpTmaX && lane == 0) prefetch_tmap(&tmap_x);
     tc_fence_before();
@@ -521,7 +559,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #ifdef LPQT_TRACE
     uint32_t smid;
     asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
-    if (a.trace && blockIdx.x < 256) a.trace[blockIdx.x * 24 + 7] = smid;
+    if (a.trace && blockIdx.x < 256) a.trace[blockIdx.x * 32 + 7] = smid;
 #endif
   }
 
@@ -551,6 +589,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t e = elect_one();
         mbar_arrive_expect_tx_if(e, &full_w[s], bytes);
         bulk_g2s_if(e, smem_w + s * C::kWStageBytes, src, bytes, &full_w[s], pol);
+        if (i == 0 && lane == 0) CTA_STAMP(20);
       } else {
         const int s = i % C::kXStages;
         mbar_wait(&empty_x[s], ((i / C::kXStages) & 1) ^ 1);
@@ -564,7 +603,29 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
     }
-    if (is_w && lane == 0) CTA_STAMP(2);
+    if (is_w && lane == 0) {
+      CTA_STAMP(2);
+      // every weight byte of this CTA is requested: hand HBM the next
+      // linear's first bytes so it keeps streaming through this launch's
+      // drain and the next one's start-up
+      if (pf.base) {
+        for (int c = blockIdx.x; c < pf.count; c += gridDim.x) {
+          int64_t kt_lin;  // tile-linear k-tile index = byte offset / kTileBytes
+          if (pf.total > 0) {
+            const int64_t q = (int64_t)c * pf.total / pf.count;
+            const int64_t t = q / pf.ksteps;
+            kt_lin = t * pf.k_tiles + (q - t * pf.ksteps) * pf.kstep;
+          } else {
+            const int cid = c / pf.c, r = c - cid * pf.c;
+            if (cid >= pf.tiles) continue;
+            kt_lin = (int64_t)cid * pf.k_tiles + r * pf.k_tiles / pf.c;
+          }
+          const int64_t off = kt_lin * kTileBytes;
+          const int64_t len = min((int64_t)pf.chunk, pf.bytes - off);
+          if (len > 0) prefetch_l2_bulk(pf.base + off, static_cast<uint32_t>(len));
+        }
+      }
+    }
   } else if (warp < kNumDqWarps) {
     // ------------------------------------------------------------ dequant
     // Two groups of 8 warps take alternate stages (one group's barrier waits
@@ -573,6 +634,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     // the stage (its whole 128-k row: two 64-weight segments), for kKStep 1
     // k-half tl of the stage's tile.
     setmaxnreg_inc<88>();
+    if (warp == 0 && lane == 0) CTA_STAMP(22);
     constexpr int kSegs = KS == 2 ? 2 : 1;
     const int lg = warp & 3, grp = warp >> 3, tl = (warp >> 2) & 1;
     const int row = lg * 32 + lane;
@@ -838,25 +900,58 @@ __global__ void __launch_bounds__(kThreads, 1)
         // contributor starts inside the tile (slot 0 = its first segment)
         idx_first = (sk_begin(a, c_first) >= p_first) ? 0 : 1;
       };
-      // worth a look only where it usually succeeds: this CTA's last
-      // segment opening a tile (this CTA = its first contributor) shared
-      // with just the next CTA, which contracted its part first thing
-      if (!CSK && !sg.full && last_seg && sg.kt0 == 0) {
-        contributors();
-        if (c_first == static_cast<int>(blockIdx.x) && c_last == c_first + 1) {
+      // BN 16: a CTA's last segment of a shared tile peeks (acquire) at the
+      // tile counter before and after its MMAs; a hit means every other
+      // contributor has published, so this CTA reduces without publishing its
+      // own partial or taking the atomic, gathering the others by bulk copy
+      // into the W ring (free once the last segment's MMAs are done).
+      // BN 32: only the first-contributor / two-CTA case (register budget).
+      constexpr int kPartBytes = kTileN * BN * 4;
+      if constexpr (BN <= 16) {
+        bool peek_ok = false;
+        auto peek = [&]() {
           if (warp == kWarpEpi0 && lane == 0)
             *last_flag = (ld_acquire_gpu(&a.counters[sg.tile]) + sg.len == a.ksteps) ? 1 : 0;
           named_bar_sync(1, kNumEpiWarps * 32);
           sk_last = *last_flag != 0;
-          if (sk_last) {
-            const float* src = a.partials + (((int64_t)c_last * 2 + 0) * kTileN + rr) * BN;
-#pragma unroll
-            for (int c0 = 0; c0 < BN; c0 += 32) prefetch_l1(src + c0);
-          }
           named_bar_sync(1, kNumEpiWarps * 32);  // last_flag is reused below
+        };
+        if (!CSK && !sg.full && last_seg) {
+          // any contributor whose last segment this is may turn out to be
+          // the tile's last arriver; it then needs no publish and no atomic
+          contributors();
+          peek_ok = (int64_t)(c_last - c_first + 1) * kPartBytes <= (int64_t)C::kWStages * C::kWStageBytes;
+          if (peek_ok) {
+            peek();
+            if (sk_last && c_last == c_first + 1 && c_first == static_cast<int>(blockIdx.x)) {
+              const float4* src = reinterpret_cast<const float4*>(a.partials);
+#pragma unroll
+              for (int j = 0; j < BN / 4; j += (BN <= 16 ? 1 : 8)) prefetch_l1(src + PartLayout<BN>::f4((int64_t)c_last * 2, j, rr));
+            }
+          }
         }
+        mbar_wait(&dfull[d], dph);
+        // second look once the MMAs are done: the other contributors usually
+        // finished meanwhile, and a hit skips publishing + the acq_rel atomic
+        if (peek_ok && !sk_last) peek();
+      } else {
+        if (!CSK && !sg.full && last_seg && sg.kt0 == 0) {
+          contributors();
+          if (c_first == static_cast<int>(blockIdx.x) && c_last == c_first + 1) {
+            if (warp == kWarpEpi0 && lane == 0)
+              *last_flag = (ld_acquire_gpu(&a.counters[sg.tile]) + sg.len == a.ksteps) ? 1 : 0;
+            named_bar_sync(1, kNumEpiWarps * 32);
+            sk_last = *last_flag != 0;
+            if (sk_last) {
+              const float4* src = reinterpret_cast<const float4*>(a.partials);
+#pragma unroll
+              for (int j = 0; j < BN / 4; j += (BN <= 16 ? 1 : 8)) prefetch_l1(src + PartLayout<BN>::f4((int64_t)c_last * 2, j, rr));
+            }
+            named_bar_sync(1, kNumEpiWarps * 32);  // last_flag is reused below
+          }
+        }
+        mbar_wait(&dfull[d], dph);
       }
-      mbar_wait(&dfull[d], dph);
       if (last_seg && warp == kWarpEpi0 && lane == 0) CTA_STAMP(8);
       tc_fence_after();
       if constexpr (CSK) {
@@ -959,7 +1054,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       } else {
         // ---- stream-K partial tile
         if (!sk_last) {
-          float* part = a.partials + (((int64_t)blockIdx.x * 2 + sg.pidx) * kTileN + rr) * BN;
+          float4* part = reinterpret_cast<float4*>(a.partials) + PartLayout<BN>::f4((int64_t)blockIdx.x * 2 + sg.pidx, 0, rr);
 #pragma unroll 1
           for (int c0 = 0; c0 < BN; c0 += 16) {
             float acc[16];
@@ -971,8 +1066,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
 #pragma unroll
             for (int j = 0; j < 16; j += 4) {
-              __stcg(reinterpret_cast<float4*>(part + c0 + j),
-                     make_float4(acc[j], acc[j + 1], acc[j + 2], acc[j + 3]));
+              __stcg(part + ((c0 + j) / 4) * PartLayout<BN>::kJStride, make_float4(acc[j], acc[j + 1], acc[j + 2], acc[j + 3]));
             }
           }
           // publish: CTA barrier, then one gpu-scope acq_rel atomic (release
@@ -980,12 +1074,69 @@ __global__ void __launch_bounds__(kThreads, 1)
           named_bar_sync(1, kNumEpiWarps * 32);
           if (warp == kWarpEpi0 && lane == 0) {
             const int k_done = sg.len;
+            if (last_seg) CTA_STAMP(9);
             const int prev = atom_add_acq_rel_gpu(&a.counters[sg.tile], k_done);
             *last_flag = (prev + k_done == a.ksteps) ? 1 : 0;
+            if (last_seg) CTA_STAMP(10);
           }
           named_bar_sync(1, kNumEpiWarps * 32);
         }
-        if (sk_last) {
+        if (BN <= 16 && sk_last && !(c_last == c_first + 1 && c_first == static_cast<int>(blockIdx.x))) {
+          // last arriver found by the peek (any position in k order): the
+          // other contributors' partials arrive by bulk copy in one round
+          // trip (slot c - c_first of the free W ring), own stays in TMEM
+          const int me = static_cast<int>(blockIdx.x);
+          if (warp == kWarpEpi0 && lane == 0) {
+            fence_proxy_async_global();  // generic-proxy partials (acquired above) -> bulk-copy reads
+            mbar_arrive_expect_tx(fix_bar, static_cast<uint32_t>(c_last - c_first) * kPartBytes);
+            for (int c = c_first; c <= c_last; ++c) {
+              if (c == me) continue;
+              const int idx = c == c_first ? idx_first : 0;
+              bulk_g2s_plain(smem_w + (c - c_first) * kPartBytes, a.partials + ((int64_t)c * 2 + idx) * (kTileN * BN),
+                             kPartBytes, fix_bar);
+            }
+          }
+          y_begin();
+          mbar_wait(fix_bar, 0);
+          if (warp == kWarpEpi0 && lane == 0) CTA_STAMP(23);
+          const uint32_t base = smem_u32(smem_w) + static_cast<uint32_t>(rr * 16);  // chunk-major rows
+#pragma unroll 1
+          for (int c0 = 0; c0 < BN; c0 += 16) {
+            float own[16], acc[16];
+            load_acc16<BN>(t_d, c0, q0, nacc, own);
+            if (warp == kWarpEpi0 && lane == 0) CTA_STAMP(26);
+            if (c0 + 16 >= BN) {
+              tc_fence_before();
+              __syncwarp();
+              if (lane == 0) mbar_arrive(&dempty[d]);
+            }
+#pragma unroll
+            for (int j = 0; j < 16; ++j) acc[j] = 0.f;
+            // contributors in k order, own partial in its place
+#pragma unroll 1
+            for (int c = c_first; c <= c_last; ++c) {
+              if (c == me) {
+#pragma unroll
+                for (int j = 0; j < 16; ++j) acc[j] += own[j];
+              } else {
+                const uint32_t src = base + (c - c_first) * kPartBytes + (c0 / 4) * kTileN * 16;
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                  const float4 v = lds128_f32(src + j * kTileN * 16);
+                  acc[4 * j + 0] += v.x;
+                  acc[4 * j + 1] += v.y;
+                  acc[4 * j + 2] += v.z;
+                  acc[4 * j + 3] += v.w;
+                }
+              }
+            }
+            if (warp == kWarpEpi0 && lane == 0) CTA_STAMP(27);
+            y_chunk(c0, acc);
+          }
+          if (warp == kWarpEpi0 && lane == 0) CTA_STAMP(24);
+          y_end();
+          if (warp == kWarpEpi0 && lane == 0) CTA_STAMP(25);
+        } else if (sk_last) {
           // fast path: two contributors, this CTA first in k order
           y_begin();
 #pragma unroll 1
@@ -997,16 +1148,57 @@ __global__ void __launch_bounds__(kThreads, 1)
               __syncwarp();
               if (lane == 0) mbar_arrive(&dempty[d]);
             }
-            const float4* src =
-                reinterpret_cast<const float4*>(a.partials + (((int64_t)c_last * 2 + 0) * kTileN + rr) * BN + c0);
+            const float4* src = reinterpret_cast<const float4*>(a.partials) + PartLayout<BN>::f4((int64_t)c_last * 2, c0 / 4, rr);
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
-              const float4 v = src[j];
+              const float4 v = src[j * PartLayout<BN>::kJStride];
               // (0 + own) + other: the canonical contributor-order sum
               acc[4 * j + 0] = (0.f + acc[4 * j + 0]) + v.x;
               acc[4 * j + 1] = (0.f + acc[4 * j + 1]) + v.y;
               acc[4 * j + 2] = (0.f + acc[4 * j + 2]) + v.z;
               acc[4 * j + 3] = (0.f + acc[4 * j + 3]) + v.w;
+            }
+            y_chunk(c0, acc);
+          }
+          y_end();
+        } else if (BN <= 16 && *last_flag && last_seg &&
+                   (int64_t)(sk_cta_of(a, (int64_t)sg.tile * a.ksteps + a.ksteps - 1) -
+                             sk_cta_of(a, (int64_t)sg.tile * a.ksteps) + 1) * (kTileN * BN * 4) <=
+                       (int64_t)C::kWStages * C::kWStageBytes) {
+          // last segment, last arriver: every W stage has been consumed, so
+          // the ring takes all contributors' partials in ONE round trip (one
+          // bulk copy each, in flight together) instead of a chain of L2
+          // loads at the very end of the kernel
+          contributors();
+          if (warp == kWarpEpi0 && lane == 0) {
+            fence_proxy_async_global();  // generic-proxy partials (acquired above) -> bulk-copy reads
+            mbar_arrive_expect_tx(fix_bar, static_cast<uint32_t>(c_last - c_first + 1) * kPartBytes);
+            for (int c = c_first; c <= c_last; ++c) {
+              const int idx = c == c_first ? idx_first : 0;
+              bulk_g2s_plain(smem_w + (c - c_first) * kPartBytes, a.partials + ((int64_t)c * 2 + idx) * (kTileN * BN),
+                             kPartBytes, fix_bar);
+            }
+          }
+          y_begin();
+          mbar_wait(fix_bar, 0);
+          if (warp == kWarpEpi0 && lane == 0) CTA_STAMP(23);
+          const uint32_t base = smem_u32(smem_w) + static_cast<uint32_t>(rr * 16);  // chunk-major rows
+#pragma unroll 1
+          for (int c0 = 0; c0 < BN; c0 += 16) {
+            float acc[16];
+#pragma unroll
+            for (int j = 0; j < 16; ++j) acc[j] = 0.f;
+#pragma unroll 1
+            for (int c = 0; c <= c_last - c_first; ++c) {
+              const uint32_t src = base + c * kPartBytes + (c0 / 4) * kTileN * 16;
+#pragma unroll
+              for (int j = 0; j < 4; ++j) {
+                const float4 v = lds128_f32(src + j * kTileN * 16);
+                acc[4 * j + 0] += v.x;
+                acc[4 * j + 1] += v.y;
+                acc[4 * j + 2] += v.z;
+                acc[4 * j + 3] += v.w;
+              }
             }
             y_chunk(c0, acc);
           }
@@ -1032,10 +1224,17 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const int c = cb + u;
                 if (c <= c_last) {
                   const int idx = c == c_first ? idx_first : 0;
-                  const float4* src =
-                      reinterpret_cast<const float4*>(a.partials + (((int64_t)c * 2 + idx) * kTileN + rr) * BN + c0);
+                  if constexpr (BN <= 16) {
+                    const float4* src = reinterpret_cast<const float4*>(a.partials) +
+                                        PartLayout<BN>::f4((int64_t)c * 2 + idx, c0 / 4, rr);
 #pragma unroll
-                  for (int j = 0; j < 4; ++j) v[u][j] = src[j];
+                    for (int j = 0; j < 4; ++j) v[u][j] = src[j * PartLayout<BN>::kJStride];
+                  } else {  // rows contiguous (same address as PartLayout<BN>::f4)
+                    const float4* src = reinterpret_cast<const float4*>(
+                        a.partials + (((int64_t)c * 2 + idx) * kTileN + rr) * BN + c0);
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) v[u][j] = src[j];
+                  }
                 } else {
 #pragma unroll
                   for (int j = 0; j < 4; ++j) v[u][j] = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -1277,8 +1476,8 @@ static int trace_next_slot() { return g_trace_n++ % kTraceSlots; }
 #endif
 
 template <int BN, bool CSK, bool RAGGED>
-static int launch_impl(const Plan& p, const GemmArgs& args, const uint16_t* Xt, int64_t ldx, int64_t M,
-                       cudaStream_t stream, int flags) {
+static int launch_impl(const Plan& p, const GemmArgs& args, const L2Prefetch& pf, const uint16_t* Xt, int64_t ldx,
+                       int64_t M, cudaStream_t stream, int flags) {
   EncodeTiledFn enc = encode_fn();
   if (!enc) return LPQT_E_CUDA;
   CUtensorMap map;
@@ -1343,7 +1542,7 @@ static int launch_impl(const Plan& p, const GemmArgs& args, const uint16_t* Xt, 
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS)
       a2.y_tma = 1;
   }
-  if (cudaLaunchKernelEx(&cfg, kern, map, ymap, a2) != cudaSuccess) return LPQT_E_CUDA;
+  if (cudaLaunchKernelEx(&cfg, kern, map, ymap, a2, pf) != cudaSuccess) return LPQT_E_CUDA;
   note_launch();
   return check_launch();
 }
@@ -1415,6 +1614,14 @@ int lpqt_w6a16_linear(const uint8_t* tiles, const uint16_t* scales, const uint16
 int lpqt_w6a16_linear_ex(const uint8_t* tiles, const uint16_t* scales, const uint16_t* Xt, int64_t ldx, int64_t M,
                          int64_t N, int64_t K, void* Y, int y_dtype, int y_layout, int64_t ldy, int split_k,
                          void* workspace, int64_t workspace_bytes, int flags, void* stream) {
+  return lpqt_w6a16_linear_pf(tiles, scales, Xt, ldx, M, N, K, Y, y_dtype, y_layout, ldy, split_k, workspace,
+                              workspace_bytes, flags, nullptr, stream);
+}
+
+int lpqt_w6a16_linear_pf(const uint8_t* tiles, const uint16_t* scales, const uint16_t* Xt, int64_t ldx, int64_t M,
+                         int64_t N, int64_t K, void* Y, int y_dtype, int y_layout, int64_t ldy, int split_k,
+                         void* workspace, int64_t workspace_bytes, int flags, const lpqt_next_linear* next,
+                         void* stream) {
   if (flags & ~(LPQT_LAUNCH_PDL | LPQT_SCHED_STREAMK | LPQT_SCHED_CLUSTER)) return LPQT_E_INVALID_INPUT;
   if ((flags & LPQT_SCHED_STREAMK) && (flags & LPQT_SCHED_CLUSTER)) return LPQT_E_INVALID_INPUT;
   if (M < 0 || N < 0 || K < 0) return LPQT_E_SHAPE;
@@ -1429,6 +1636,7 @@ int lpqt_w6a16_linear_ex(const uint8_t* tiles, const uint16_t* scales, const uin
   const Plan p = make_plan(M, N, K, split_k, flags, num_sms());
   if (p.ws_bytes > 0 && (workspace == nullptr || workspace_bytes < p.ws_bytes)) return LPQT_E_WORKSPACE;
   GemmArgs args{};
+  L2Prefetch pfa{};
 #ifdef LPQT_TRACE
   args.trace = trace_buffer() + (size_t)trace_next_slot() * kTraceLen;
 #endif
@@ -1451,27 +1659,46 @@ int lpqt_w6a16_linear_ex(const uint8_t* tiles, const uint16_t* scales, const uin
   args.y_dtype = y_dtype;
   args.y_layout = y_layout;
   args.sm = ShiftMuls{1u << 26, 1u << 28, 1u << 30};
+  if (next && next->tiles && next->M > 0 && next->N > 0 && next->K > 0 && next->bytes_per_cta >= 0) {
+    // the next launch's plan tells which bytes each of its CTAs needs first
+    // (decode shapes: one batch tile, tile index = weight row tile)
+    if ((next->flags & LPQT_SCHED_STREAMK) && (next->flags & LPQT_SCHED_CLUSTER)) return LPQT_E_INVALID_INPUT;
+    const Plan q = make_plan(next->M, next->N, next->K, next->split_k, next->flags, num_sms());
+    const int64_t chunk = next->bytes_per_cta > 0 ? next->bytes_per_cta : (int64_t)64 << 10;
+    if (q.m_tiles == 1) {
+      pfa.base = next->tiles;
+      pfa.bytes = (int64_t)q.n_tiles * q.k_tiles * kTileBytes;
+      pfa.count = q.grid;
+      pfa.total = q.csk ? 0 : q.total;
+      pfa.ksteps = q.ksteps;
+      pfa.kstep = q.kstep;
+      pfa.k_tiles = q.k_tiles;
+      pfa.c = q.csk ? q.cluster : 1;
+      pfa.tiles = static_cast<int>(q.tiles);
+      pfa.chunk = static_cast<uint32_t>(std::min<int64_t>(chunk, (int64_t)1 << 30) / 16 * 16);
+    }
+  }
   cudaStream_t st = as_stream(stream);
   bool ragged = p.k_tiles % p.kstep != 0;
   if (p.csk) {
     for (int r = 0; r < p.cluster; ++r)  // k-range of rank r must be a whole number of stages
       ragged |= ((r + 1) * p.k_tiles / p.cluster - r * p.k_tiles / p.cluster) % p.kstep != 0;
     if (p.bn <= 16)
-      return ragged ? launch_impl<16, true, true>(p, args, Xt, ldx, M, st, flags)
-                    : launch_impl<16, true, false>(p, args, Xt, ldx, M, st, flags);
-    return ragged ? launch_impl<32, true, true>(p, args, Xt, ldx, M, st, flags)
-                  : launch_impl<32, true, false>(p, args, Xt, ldx, M, st, flags);
+      return ragged ? launch_impl<16, true, true>(p, args, pfa, Xt, ldx, M, st, flags)
+                    : launch_impl<16, true, false>(p, args, pfa, Xt, ldx, M, st, flags);
+    return ragged ? launch_impl<32, true, true>(p, args, pfa, Xt, ldx, M, st, flags)
+                  : launch_impl<32, true, false>(p, args, pfa, Xt, ldx, M, st, flags);
   }
   switch (p.bn) {
     case 16:
-      return ragged ? launch_impl<16, false, true>(p, args, Xt, ldx, M, st, flags)
-                    : launch_impl<16, false, false>(p, args, Xt, ldx, M, st, flags);
+      return ragged ? launch_impl<16, false, true>(p, args, pfa, Xt, ldx, M, st, flags)
+                    : launch_impl<16, false, false>(p, args, pfa, Xt, ldx, M, st, flags);
     case 32:
-      return ragged ? launch_impl<32, false, true>(p, args, Xt, ldx, M, st, flags)
-                    : launch_impl<32, false, false>(p, args, Xt, ldx, M, st, flags);
-    case 64: return launch_impl<64, false, false>(p, args, Xt, ldx, M, st, flags);
-    case 128: return launch_impl<128, false, false>(p, args, Xt, ldx, M, st, flags);
-    default: return launch_impl<256, false, false>(p, args, Xt, ldx, M, st, flags);
+      return ragged ? launch_impl<32, false, true>(p, args, pfa, Xt, ldx, M, st, flags)
+                    : launch_impl<32, false, false>(p, args, pfa, Xt, ldx, M, st, flags);
+    case 64: return launch_impl<64, false, false>(p, args, pfa, Xt, ldx, M, st, flags);
+    case 128: return launch_impl<128, false, false>(p, args, pfa, Xt, ldx, M, st, flags);
+    default: return launch_impl<256, false, false>(p, args, pfa, Xt, ldx, M, st, flags);
   }
 }
 

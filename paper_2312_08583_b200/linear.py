@@ -10,6 +10,8 @@ scales.  `w6a16_linear` is the torch-facing call (x[M, K] fp16 -> y[M, N]);
 
 from __future__ import annotations
 
+import ctypes
+
 import numpy as np
 
 from . import _lib
@@ -137,15 +139,19 @@ def plan(m: int, n: int, k: int, split_k: int = 0, sched: str = "auto") -> dict:
 
 
 def _launch(weight: Fp6Weight, xt, ldx: int, m: int, y, y_dtype: int, y_layout: int, ldy: int, split_k: int,
-            sched: str = "auto"):
+            sched: str = "auto", prefetch: "Fp6Weight | None" = None, prefetch_bytes: int = 0):
     lib = _lib.load()
     ws_bytes = int(lib.lpqt_w6a16_workspace_bytes(m, weight.n, weight.k, split_k))
     ws = _lib.Workspace.get(ws_bytes) if ws_bytes else None
     flags = (_lib.LAUNCH_PDL if weight.static else 0) | _sched_flags(sched)
-    _lib.check(lib.lpqt_w6a16_linear_ex(
+    nxt = None
+    if prefetch is not None:
+        # the next launch is assumed to use the same batch and the automatic schedule
+        nxt = _lib.NextLinear(prefetch.tiles.data_ptr(), m, prefetch.n, prefetch.k, 0, 0, int(prefetch_bytes))
+    _lib.check(lib.lpqt_w6a16_linear_pf(
         weight.tiles.data_ptr(), weight.scales.data_ptr(), xt.data_ptr(), ldx, m, weight.n, weight.k,
         y.data_ptr(), y_dtype, y_layout, ldy, split_k, _lib.ptr(ws), ws.numel() if ws is not None else 0,
-        flags, _lib.stream_ptr()), "w6a16_linear")
+        flags, None if nxt is None else ctypes.byref(nxt), _lib.stream_ptr()), "w6a16_linear")
 
 
 def stage_activations(X, k: int):
@@ -175,12 +181,15 @@ def gemm_nm(weight: Fp6Weight, xt, ldx: int, m: int, out=None, split_k: int = 0,
     return y
 
 
-def w6a16_linear(x, weight: Fp6Weight, out=None, out_dtype=None, split_k: int = 0, sched: str = "auto"):
+def w6a16_linear(x, weight: Fp6Weight, out=None, out_dtype=None, split_k: int = 0, sched: str = "auto",
+                 prefetch: "Fp6Weight | None" = None, prefetch_bytes: int = 0):
     """y = x @ W_hat^T for x[..., K] (CUDA, fp16 preferred) -> y[..., N].
 
     x is the K-major B operand as is when it is contiguous fp16 with K % 8 ==
     0; otherwise it is cast / padded once.  out_dtype: fp16 (default for
-    fp16 x), bf16 or fp32.
+    fp16 x), bf16 or fp32.  prefetch: the weight of the linear that runs
+    next on this stream (same batch); this launch's drain pulls its first
+    bytes into L2 (lpqt_w6a16_linear_pf).
     """
     t = _lib.torch()
     if x.shape[-1] != weight.k:
@@ -204,7 +213,7 @@ def w6a16_linear(x, weight: Fp6Weight, out=None, out_dtype=None, split_k: int = 
         if weight.k == 0:
             y.zero_()
         else:
-            _launch(weight, x2, ldx, m, y, code, _lib.Y_MN, weight.n, split_k, sched)
+            _launch(weight, x2, ldx, m, y, code, _lib.Y_MN, weight.n, split_k, sched, prefetch, prefetch_bytes)
     return y.reshape(*lead, weight.n)
 
 

@@ -440,3 +440,37 @@ def test_prefill_large_x_weight_row_fastest_order():
     Y = L.gemm_quantized(q, X)
     Y_ref = (L.dequantize_tensor(q, "bias_shift") @ X.double()).float()
     assert normwise_rel(Y.cpu().numpy(), Y_ref.cpu().numpy()) <= REL_TOL
+
+
+@pytest.mark.parametrize("m", [1, 16, 512])
+def test_prefetch_next_linear_is_transparent(m):
+    """lpqt_w6a16_linear_pf: naming the next launch's weight (stream-K and
+    cluster-split next plans, any depth) leaves every result bit-identical."""
+    g = torch.Generator(device="cuda").manual_seed(3)
+    shapes = [(12288, 4096), (4096, 4096), (4096, 11008), (640, 256)]
+    ws = [L.Fp6Weight.quantize((torch.randn(n, k, device="cuda", generator=g) * 0.02).half()) for n, k in shapes]
+    xs = [torch.randn(m, k, device="cuda", generator=g).half() for _, k in shapes]
+    want = [L.w6a16_linear(x, w) for x, w in zip(xs, ws)]
+    for depth in (0, 16, 12288, 1 << 20):
+        for i, (x, w) in enumerate(zip(xs, ws)):
+            nxt = ws[(i + 1) % len(ws)]
+            got = L.w6a16_linear(x, w, prefetch=nxt, prefetch_bytes=depth)
+            assert torch.equal(got, want[i]), (i, depth)
+    torch.cuda.synchronize()
+
+
+@pytest.mark.parametrize("n,k,m", [(4096, 11008, 16), (4096, 11008, 1), (1024, 16384, 8), (4096, 11008, 32)])
+def test_streamk_fixup_paths_bit_identical(n, k, m):
+    """Stream-K tiles shared by 2..N CTAs close through whichever path the
+    timing picks (last-arriver peek + bulk gather, two-contributor fast path,
+    publish + atomic): every path sums the contributors in k order, so
+    repeated launches are bit-identical and match the oracle within tolerance."""
+    g = torch.Generator(device="cuda").manual_seed(9)
+    W = (torch.randn(n, k, generator=g, device="cuda") * 0.02).half()
+    w = L.Fp6Weight.quantize(W)
+    x = torch.randn(m, k, generator=g, device="cuda").half()
+    ys = [L.w6a16_linear(x, w, out_dtype=torch.float32, sched="streamk") for _ in range(20)]
+    for y in ys[1:]:
+        assert torch.equal(y.view(torch.int32), ys[0].view(torch.int32))
+    ref = (w.dequantize_f16().double() @ x.double().t()).t()
+    assert normwise_rel(ys[0].cpu().numpy(), ref.cpu().numpy()) <= REL_TOL

@@ -27,12 +27,12 @@ for _ in range(4):
     ts.append(e0.elapsed_time(e1) * 1e3)
 lib = _lib.load()
 BASE = 0
-buf = (ctypes.c_longlong * (256 * 24 + 12 * 64 + 16 * 3 * 64))()
+buf = (ctypes.c_longlong * (256 * 32 + 12 * 64 + 16 * 3 * 64))()
 lib.lpqt_trace_dump(buf)
 t = np.frombuffer(buf, dtype=np.int64)
 plan = L.plan(a.m, a.n, a.k, a.split)
 print("shape", a.n, a.k, a.m, "out", a.out, os.environ.get("LPQT_LIB", ""), "plan", plan, "event us (eager, last 3):", [round(v, 2) for v in ts[1:]])
-cta = t[BASE:BASE + 256 * 24].reshape(256, 24)[: plan["grid"]].astype(np.float64)
+cta = t[BASE:BASE + 256 * 32].reshape(256, 32)[: plan["grid"]].astype(np.float64)
 t0 = cta[:, 0].min()
 cols = [0, 1, 12, 13, 14, 2, 3, 4, 8, 9, 10, 16, 17, 18, 19, 11, 5, 6]
 names = ["entry", "setup", "dq_1st_data", "x_pdl_ok", "mma_1st_x", "prodW_done", "dq0_done", "mma_done",
@@ -52,7 +52,7 @@ print("slowest CTAs: cta smid | " + " ".join(f"{n[:9]:>9}" for n in names))
 for c in order:
     print(f"{c:4d} {int(cta[c, 7]):4d} | " + " ".join(f"{v:9.2f}" for v in rel[c]))
 
-ev = t[256 * 24:256 * 24 + 12 * 64].reshape(12, 64)
+ev = t[256 * 32:256 * 32 + 12 * 64].reshape(12, 64)
 enames = ["W_issue", "dq_top", "dq_aempty", "dq_sttm", "dq_pre", "dq_waitst", "dq_had_nx", "mma_x_ok", "mma_a_ok",
           "mma_commit"]
 base = ev[ev > 0].min() if (ev > 0).any() else 0
@@ -62,7 +62,7 @@ for i in range(min(40, 64)):
     row = [(ev[e, i] - base) if ev[e, i] > 0 else -1 for e in range(10)]
     print(f"{i:2d} " + " ".join(f"{v:10d}" for v in row))
 
-wt = t[256 * 24 + 12 * 64:].reshape(16, 3, 64)
+wt = t[256 * 32 + 12 * 64:].reshape(16, 3, 64)
 print("DQ warps, stages 20..27: (aempty_ok, sttm_issued, afull_arrived) relative to warp 0 aempty_ok of the stage")
 for i in range(20, 28):
     b = wt[0, 0, i]
