@@ -26,6 +26,7 @@ distinct copies (302 MB > 2 x 126 MB L2), so every step reads cold weights.
 from __future__ import annotations
 
 import argparse
+import ctypes
 import json
 import os
 import statistics
@@ -199,20 +200,27 @@ def run_ours(args, world, rank):
     yfull = [torch.empty(n, m, device="cuda", dtype=torch.float16) for _, n, _ in layers]
     lib = _lib.load()
 
-    def launch(i, w):
+    def next_of(c, i):
+        # the linear that runs next on the stream: the step's next layer, or
+        # the first layer of the next step (the next weight copy)
+        return sets[c][i + 1] if i + 1 < len(layers) else sets[(c + 1) % copies][0]
+
+    def launch(i, w, nxt=None):
         # reference layout Y[N_p, M] (gemm.py:65), fp16 out
         ws_bytes = int(lib.lpqt_w6a16_workspace_bytes(m, w.n, w.k, 0))
         ws = _lib.Workspace.get(ws_bytes) if ws_bytes else None
         # programmatic dependent launch: the weights are static, so each GEMM
-        # streams its weight tiles while the previous layer's kernel drains
-        _lib.check(lib.lpqt_w6a16_linear_ex(w.tiles.data_ptr(), w.scales.data_ptr(), xts[i].data_ptr(), w.k, m,
+        # streams its weight tiles while the previous layer's kernel drains;
+        # and its drain pulls the next linear's first weight bytes into L2
+        pf = None if nxt is None else _lib.NextLinear(nxt.tiles.data_ptr(), m, nxt.n, nxt.k, 0, 0, 0)
+        _lib.check(lib.lpqt_w6a16_linear_pf(w.tiles.data_ptr(), w.scales.data_ptr(), xts[i].data_ptr(), w.k, m,
                                             w.n, w.k, ys[i].data_ptr(), _lib.F16, _lib.Y_NM, m, 0, _lib.ptr(ws),
                                             ws.numel() if ws is not None else 0, _lib.LAUNCH_PDL,
-                                            _lib.stream_ptr()))
+                                            None if pf is None else ctypes.byref(pf), _lib.stream_ptr()))
 
     def step(c):
         for i, w in enumerate(sets[c]):
-            launch(i, w)
+            launch(i, w, next_of(c, i))
             if world > 1:
                 import torch.distributed as dist
                 dist.all_gather_into_tensor(yfull[i], ys[i])
@@ -232,7 +240,7 @@ def run_ours(args, world, rank):
             for i, w in enumerate(sets[c]):
                 if with_events:
                     evs[i].record()
-                launch(i, w)
+                launch(i, w, None if with_events else next_of(c, i))
                 if world > 1:
                     import torch.distributed as dist
                     dist.all_gather_into_tensor(yfull[i], ys[i])
@@ -366,11 +374,12 @@ def time_e2e(layers, wset, world, rank, m, args):
         for i, w in enumerate(wset):
             x = xd[int(xoff[i]):int(xoff[i + 1])].view(m, ks[i])
             y = yd[int(yoff[i]):int(yoff[i + 1])].view(m, ns[i])
+            nxt = wset[(i + 1) % len(wset)]    # the next linear on the stream (L2 prefetch hint)
             if world == 1:
-                w6a16_linear(x, w, out=y)
+                w6a16_linear(x, w, out=y, prefetch=nxt)
             else:
                 import torch.distributed as dist
-                w6a16_linear(x, w, out=ys_local[i])
+                w6a16_linear(x, w, out=ys_local[i], prefetch=nxt)
                 # column shards gathered along N: [P, M, N/P] -> y[M, N]
                 parts = torch.empty(world, m, w.n, dtype=torch.float16, device="cuda")
                 dist.all_gather_into_tensor(parts, ys_local[i])
