@@ -131,11 +131,19 @@ struct Cfg {
   // single-lane issue sequence takes several times that, so two warps issue
   // alternate stages, each into its own accumulator; the epilogue sums them
   // in a fixed order.  Prefill MMAs (N >= 128) are long enough for one.
+#ifdef LPQT_MMA1
+  static constexpr int kMmaWarps = 1;
+#else
   static constexpr int kMmaWarps = BN <= 64 ? 2 : 1;
+#endif
   static constexpr int kNAcc = kMmaWarps;
   static constexpr int kDCols = BN * kNAcc;
   static constexpr int kACols = kTmemCols - kDBufs * kDCols;
-  static constexpr int kASlots = ((kACols / kAColsPerBuf) / kKStep) & ~1;  // even
+  // even with two MMA issuers (each slot then always belongs to the same
+  // issuer, which waits on it in stage order: no parity wait can skip a
+  // phase); one issuer may use every whole slot TMEM holds
+  static constexpr int kASlots =
+      kMmaWarps == 1 ? (kACols / kAColsPerBuf) / kKStep : ((kACols / kAColsPerBuf) / kKStep) & ~1;
   static constexpr int kBarCount = 2 * kWStages + 2 * kXStages + 2 * kASlots + 2 * kDBufs + 5;
   static constexpr int kSmemBytes = kXStages * kXStageBytes + kWStages * kWStageBytes + 2 * kStageBufBytes +
                                     2 * kYBufBytes + 8 * kBarCount + 16;
