@@ -152,7 +152,8 @@ int64_t lpqt_w6a16_workspace_bytes(int64_t M, int64_t N, int64_t K, int split_k)
 int lpqt_w6a16_plan(int64_t M, int64_t N, int64_t K, int split_k,
                     int* block_n, int* splits, int* grid, int* stages);
 /* Plan with schedule flags: out[0..5] = block_n, splits, grid, stages,
- * schedule (0 stream-K, 1 cluster split-K), cluster size (n_out <= 6). */
+ * schedule (0 stream-K, 1 cluster split-K, 2 whole tiles round-robin —
+ * prefill whose activations outgrow L2), cluster size (n_out <= 6). */
 int lpqt_w6a16_plan_ex(int64_t M, int64_t N, int64_t K, int split_k, int flags,
                        int* out, int n_out);
 int lpqt_w6a16_linear(const uint8_t* tiles, const uint16_t* scales,

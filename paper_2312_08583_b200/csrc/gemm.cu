@@ -93,6 +93,7 @@ struct GemmArgs {
   int csk_c;          // CSK: cluster size C (k-split factor)
   int n_fastest;      // tile index order: 0 = batch tile fastest, 1 = weight-row tile fastest
   int y_tma;          // Y tiles leave through the TMA tensor store (tmap_y valid)
+  int dp;             // prefill (BN >= 64): whole tiles round-robin, CTA c takes c, c + grid, ...
   ShiftMuls sm;       // 2^26, 2^28, 2^30: right shifts on the FMA pipe (common.cuh)
 };
 
@@ -121,12 +122,15 @@ struct Cfg {
   // decode: output tiles staged in smem (two 128 x BN buffers, fp32-sized) and
   // written by the TMA tensor store, off the epilogue's critical path
   static constexpr int kYBufBytes = BN <= 32 ? kTileN * BN * 4 : 0;
-  static constexpr int kBudget = BN >= 256 ? 221 * 1024 : kSmemBudget;
+  static constexpr int kBudget = BN >= 192 ? 221 * 1024 : kSmemBudget;
   static constexpr int kWStagesRaw =
       (kBudget - kXStages * kXStageBytes - 2 * kStageBufBytes - 2 * kYBufBytes) / kWStageBytes;
   static constexpr int kWStages = (kWStagesRaw > 12 ? 12 : kWStagesRaw) & ~1;  // even: see header
   static constexpr int kStages = kWStages;                  // reported by the plan
-  static constexpr int kDBufs = BN <= 128 ? 2 : 1;
+  // two accumulators in flight (the epilogue drains one while the next
+  // tile's MMAs fill the other) up to BN 192: 2 x 192 + a 2-slot A ring = 512
+  // TMEM columns; BN 256 has room for one
+  static constexpr int kDBufs = BN <= 192 ? 2 : 1;
   // MMA issue: at small N a tcgen05.mma executes in ~9 cycles while its
   // single-lane issue sequence takes several times that, so two warps issue
   // alternate stages, each into its own accumulator; the epilogue sums them
@@ -201,16 +205,41 @@ __device__ __forceinline__ int sk_cta_of(const GemmArgs& a, int64_t p) {
 
 // A CTA's stream-K range [beg, end) in natural order; segments never
 // straddle a tile.
+//
+// Prefill (KS 1, a.dp): whole tiles round-robin instead — CTA c takes tiles c,
+// c + grid, c + 2 grid, ... so the CTAs in flight always work on ~grid
+// consecutive tiles: with the weight-row-fastest order they share one or two
+// batch tiles of X, which stays in L2 (contiguous stream-K ranges would spread
+// the CTAs over every batch tile at once and stream X from HBM repeatedly).
 struct SkSched {
   int64_t beg;  // (the range end is beg + n: one 64-bit value kept live, not two)
   int n;
+  template <int KS>
   __device__ __forceinline__ void init(const GemmArgs& a) {
+    if (KS == 1 && a.dp) {
+      const int c = static_cast<int>(blockIdx.x);
+      n = c < a.tile_count ? ((a.tile_count - 1 - c) / static_cast<int>(gridDim.x) + 1) * a.ksteps : 0;
+      beg = 0;
+      return;
+    }
     beg = sk_begin(a, blockIdx.x);
     n = static_cast<int>(sk_begin(a, blockIdx.x + 1) - beg);
   }
   template <int KS>
   __device__ __forceinline__ bool seg_at(const GemmArgs& a, int i, Seg& sg) const {
     if (i >= n) return false;
+    if (KS == 1 && a.dp) {
+      const int j = i / a.ksteps;
+      sg.tile = static_cast<int>(blockIdx.x) + j * static_cast<int>(gridDim.x);
+      sg.i0 = j * a.ksteps;
+      sg.len = a.ksteps;
+      sg.kt0 = 0;
+      sg.kt1 = a.k_tiles;
+      sg.full = true;
+      sg.pidx = 0;
+      sg.red = 0;
+      return true;
+    }
     const int64_t p = beg + i;
     const int t = static_cast<int>(p / a.ksteps);
     const int s0 = static_cast<int>(p - (int64_t)t * a.ksteps);
@@ -311,9 +340,6 @@ __device__ __forceinline__ int ld_acquire_gpu(const int* p) {
   asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
-__device__ __forceinline__ void prefetch_l1(const void* p) {
-  asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
-}
 
 __device__ __forceinline__ void store_y(const GemmArgs& a, int n, int m, float v) {
   if (n >= a.N || m >= a.M) return;
@@ -344,16 +370,20 @@ __device__ __forceinline__ void load_acc16(uint32_t t_d, int c0, int q0, int nac
   }
 }
 
+// Partials are read with ld.global.cg / bulk copies (L2), never through L1:
+// with programmatic dependent launch an SM's L1 may still hold the same
+// workspace lines from a previous launch of another shape.
 // Stream-K partial tile of contributor slot `blk` (= cta * 2 + idx): 128 x BN
-// fp32.  BN 16 stores it chunk-major (float4 chunk j of row r at [j][r]): a
-// warp's accesses to one chunk are 512 contiguous bytes, coalesced in global
-// and conflict-free once gathered into shared memory.  BN 32 keeps rows
+// fp32, stored chunk-major (float4 chunk j of row r at [j][r]): a warp's
+// accesses to one chunk are 512 contiguous bytes, coalesced in global and
+// conflict-free once gathered into shared memory.  BN 32 keeps rows
 // contiguous (the chunk-major index math costs its epilogue registers).
 template <int BN>
 struct PartLayout {
-  static constexpr int kJStride = BN <= 16 ? kTileN : 1;  // float4 stride between chunks of a row
+  static constexpr bool kChunkMajor = BN != 32;
+  static constexpr int kJStride = kChunkMajor ? kTileN : 1;  // float4 stride between chunks of a row
   __device__ __forceinline__ static int64_t f4(int64_t blk, int j, int rr) {  // float4 index
-    return blk * (kTileN * BN / 4) + (BN <= 16 ? rr : rr * (BN / 4)) + (int64_t)j * kJStride;
+    return blk * (kTileN * BN / 4) + (kChunkMajor ? rr : rr * (BN / 4)) + (int64_t)j * kJStride;
   }
 };
 
@@ -504,7 +534,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   if constexpr (CSK) {
     sc.init(a, KS);
   } else {
-    sc.init(a);
+    sc.template init<KS>(a);
   }
   const int n_st = sc.n;
 
@@ -893,8 +923,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const bool last_seg = sg.i0 + sg.len >= n_st;
       // stream-K partial tile: if every other contributor has already
       // published (acquire-load of the tile counter), this CTA is the last
-      // arriver — it skips publishing its own partial and the atomic, and
-      // pulls the others' partials into L1 while its MMAs finish
+      // arriver — it skips publishing its own partial and the atomic
       bool sk_last = false;
       int64_t p_first = 0;
       int c_first = 0, c_last = 0, idx_first = 0;
@@ -908,14 +937,98 @@ __global__ void __launch_bounds__(kThreads, 1)
         // contributor starts inside the tile (slot 0 = its first segment)
         idx_first = (sk_begin(a, c_first) >= p_first) ? 0 : 1;
       };
+      // Tail reduction (BN >= 128, last segment: every X and W stage has been
+      // consumed).  Contributors c_first..c_last in k order; batches of
+      // kSlots partials land by bulk copy in [smem_x, smem_x + X ring + W
+      // ring); the running sum lives in the other TMEM accumulator (idle: no
+      // MMA follows).  Summation order = every other path's: 0 + p0 + p1 + ...
+      auto tail_reduce = [&](bool own_in_tmem) {
+        constexpr int kFree = C::kXStages * C::kXStageBytes + C::kWStages * C::kWStageBytes;
+        constexpr int kSlots = kFree / (kTileN * BN * 4) > 0 ? kFree / (kTileN * BN * 4) : 1;
+        constexpr uint32_t kPB = kTileN * BN * 4;
+        const int me = static_cast<int>(blockIdx.x);
+        const uint32_t t_acc = t_lane + (1 - d) * C::kDCols;   // the idle accumulator (this warp's lanes)
+        const uint32_t sbase = smem_u32(smem_x) + static_cast<uint32_t>(rr * 16);
+        uint32_t fph = 0;
+        y_begin();
+        for (int b0 = c_first; b0 <= c_last; b0 += kSlots) {
+          const int b1 = min(c_last, b0 + kSlots - 1);
+          if (warp == kWarpEpi0 && lane == 0) {
+            uint32_t bytes = 0;
+            for (int c = b0; c <= b1; ++c) bytes += (own_in_tmem && c == me) ? 0u : kPB;
+            fence_proxy_async_global();  // generic-proxy partials (acquired) -> bulk-copy reads
+            mbar_arrive_expect_tx(fix_bar, bytes);
+            for (int c = b0; c <= b1; ++c) {
+              if (own_in_tmem && c == me) continue;
+              const int idx = c == c_first ? idx_first : 0;
+              bulk_g2s_plain(smem_x + (c - b0) * kPB, a.partials + ((int64_t)c * 2 + idx) * (kTileN * BN), kPB,
+                             fix_bar);
+            }
+          }
+          mbar_wait(fix_bar, fph);
+          fph ^= 1u;
+          const bool last_batch = b1 == c_last;
+#pragma unroll 1
+          for (int c0 = 0; c0 < BN; c0 += 16) {
+            float acc[16];
+            if (b0 == c_first) {
+#pragma unroll
+              for (int j = 0; j < 16; ++j) acc[j] = 0.f;
+            } else {
+              uint32_t v[16];
+              tmem_ld_x16(t_acc + c0, v);
+              tmem_wait_ld();
+#pragma unroll
+              for (int j = 0; j < 16; ++j) acc[j] = __uint_as_float(v[j]);
+            }
+#pragma unroll 1
+            for (int c = b0; c <= b1; ++c) {
+              if (own_in_tmem && c == me) {
+                float own[16];
+                load_acc16<BN>(t_d, c0, q0, nacc, own);
+#pragma unroll
+                for (int j = 0; j < 16; ++j) acc[j] += own[j];
+              } else {
+                const uint32_t src = sbase + (c - b0) * kPB + (c0 / 4) * kTileN * 16;
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                  const float4 v = lds128_f32(src + j * kTileN * 16);
+                  acc[4 * j + 0] += v.x;
+                  acc[4 * j + 1] += v.y;
+                  acc[4 * j + 2] += v.z;
+                  acc[4 * j + 3] += v.w;
+                }
+              }
+            }
+            if (last_batch) {
+              y_chunk(c0, acc);
+            } else {
+              uint32_t v[16];
+#pragma unroll
+              for (int j = 0; j < 16; ++j) v[j] = __float_as_uint(acc[j]);
+              tmem_st_x16(t_acc + c0, v);
+            }
+          }
+          tmem_wait_st();
+          // every thread is done with this batch's slots before the next copies
+          named_bar_sync(1, kNumEpiWarps * 32);
+        }
+        if (own_in_tmem) {  // (a published partial already handed its D buffer back)
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&dempty[d]);
+        }
+        y_end();
+      };
       // BN 16: a CTA's last segment of a shared tile peeks (acquire) at the
       // tile counter before and after its MMAs; a hit means every other
       // contributor has published, so this CTA reduces without publishing its
       // own partial or taking the atomic, gathering the others by bulk copy
       // into the W ring (free once the last segment's MMAs are done).
+      // BN >= 128 gathers in batches through the free X + W rings (below).
       // BN 32: only the first-contributor / two-CTA case (register budget).
       constexpr int kPartBytes = kTileN * BN * 4;
-      if constexpr (BN <= 16) {
+      if constexpr (BN <= 16 || BN >= 128) {
         bool peek_ok = false;
         auto peek = [&]() {
           if (warp == kWarpEpi0 && lane == 0)
@@ -928,14 +1041,10 @@ __global__ void __launch_bounds__(kThreads, 1)
           // any contributor whose last segment this is may turn out to be
           // the tile's last arriver; it then needs no publish and no atomic
           contributors();
-          peek_ok = (int64_t)(c_last - c_first + 1) * kPartBytes <= (int64_t)C::kWStages * C::kWStageBytes;
+          peek_ok = BN >= 128 ||
+                    (int64_t)(c_last - c_first + 1) * kPartBytes <= (int64_t)C::kWStages * C::kWStageBytes;
           if (peek_ok) {
             peek();
-            if (sk_last && c_last == c_first + 1 && c_first == static_cast<int>(blockIdx.x)) {
-              const float4* src = reinterpret_cast<const float4*>(a.partials);
-#pragma unroll
-              for (int j = 0; j < BN / 4; j += (BN <= 16 ? 1 : 8)) prefetch_l1(src + PartLayout<BN>::f4((int64_t)c_last * 2, j, rr));
-            }
           }
         }
         mbar_wait(&dfull[d], dph);
@@ -950,11 +1059,6 @@ __global__ void __launch_bounds__(kThreads, 1)
               *last_flag = (ld_acquire_gpu(&a.counters[sg.tile]) + sg.len == a.ksteps) ? 1 : 0;
             named_bar_sync(1, kNumEpiWarps * 32);
             sk_last = *last_flag != 0;
-            if (sk_last) {
-              const float4* src = reinterpret_cast<const float4*>(a.partials);
-#pragma unroll
-              for (int j = 0; j < BN / 4; j += (BN <= 16 ? 1 : 8)) prefetch_l1(src + PartLayout<BN>::f4((int64_t)c_last * 2, j, rr));
-            }
             named_bar_sync(1, kNumEpiWarps * 32);  // last_flag is reused below
           }
         }
@@ -1089,7 +1193,15 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
           named_bar_sync(1, kNumEpiWarps * 32);
         }
-        if (BN <= 16 && sk_last && !(c_last == c_first + 1 && c_first == static_cast<int>(blockIdx.x))) {
+        if (BN >= 128 && C::kDBufs == 2 && last_seg && (sk_last || *last_flag)) {
+          // ---- stream-K tail, BN >= 128: the other contributors' 128 x BN
+          // partials come by bulk copy, in batches through the free X + W
+          // rings, summed in k order into the idle second TMEM accumulator
+          // (own partial in place: from TMEM when the peek spared publishing
+          // it, else from the workspace like the others)
+          contributors();
+          tail_reduce(sk_last);
+        } else if (BN <= 16 && sk_last && !(c_last == c_first + 1 && c_first == static_cast<int>(blockIdx.x))) {
           // last arriver found by the peek (any position in k order): the
           // other contributors' partials arrive by bulk copy in one round
           // trip (slot c - c_first of the free W ring), own stays in TMEM
@@ -1159,7 +1271,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             const float4* src = reinterpret_cast<const float4*>(a.partials) + PartLayout<BN>::f4((int64_t)c_last * 2, c0 / 4, rr);
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
-              const float4 v = src[j * PartLayout<BN>::kJStride];
+              const float4 v = __ldcg(src + j * PartLayout<BN>::kJStride);
               // (0 + own) + other: the canonical contributor-order sum
               acc[4 * j + 0] = (0.f + acc[4 * j + 0]) + v.x;
               acc[4 * j + 1] = (0.f + acc[4 * j + 1]) + v.y;
@@ -1232,16 +1344,16 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const int c = cb + u;
                 if (c <= c_last) {
                   const int idx = c == c_first ? idx_first : 0;
-                  if constexpr (BN <= 16) {
+                  if constexpr (PartLayout<BN>::kChunkMajor) {
                     const float4* src = reinterpret_cast<const float4*>(a.partials) +
                                         PartLayout<BN>::f4((int64_t)c * 2 + idx, c0 / 4, rr);
 #pragma unroll
-                    for (int j = 0; j < 4; ++j) v[u][j] = src[j * PartLayout<BN>::kJStride];
+                    for (int j = 0; j < 4; ++j) v[u][j] = __ldcg(src + j * PartLayout<BN>::kJStride);
                   } else {  // rows contiguous (same address as PartLayout<BN>::f4)
                     const float4* src = reinterpret_cast<const float4*>(
                         a.partials + (((int64_t)c * 2 + idx) * kTileN + rr) * BN + c0);
 #pragma unroll
-                    for (int j = 0; j < 4; ++j) v[u][j] = src[j];
+                    for (int j = 0; j < 4; ++j) v[u][j] = __ldcg(src + j);
                   }
                 } else {
 #pragma unroll
@@ -1297,19 +1409,28 @@ struct Plan {
   int64_t tiles, total, ws_bytes, counters_bytes;
   bool partials;
   bool csk;
+  bool dp;      // prefill: whole tiles round-robin (SkSched DP mode)
   int cluster;  // CSK cluster size
   int splits;   // max CTAs contributing to one tile
 };
 
-#ifndef LPQT_MAX_BN
-#define LPQT_MAX_BN 256
+// Prefill MMA N (M > 128).  192 keeps two accumulators in TMEM (the epilogue
+// of one tile overlaps the next tile's MMAs) and its MMA time per k-tile
+// (~770 cycles) still covers the 128-row dequant (~600); 256 has a single
+// accumulator (the tensor pipe idles through every epilogue) and 128 is
+// dequant-bound.  Measured: profiles/r01_v8_probe_prefill_bn192.txt.
+#ifndef LPQT_PREFILL_BN
+#define LPQT_PREFILL_BN 192
+#endif
+#ifndef LPQT_SK_SPLIT_WIDE
+#define LPQT_SK_SPLIT_WIDE 0  // > 0: fixed cap on CTAs per tile for BN >= 64 (tuning hook)
 #endif
 static int pick_bn(int64_t M) {
   if (M <= 16) return 16;
   if (M <= 32) return 32;
   if (M <= 64) return 64;
-  if (M <= 128 || LPQT_MAX_BN == 128) return 128;
-  return 256;
+  if (M <= 128 || LPQT_PREFILL_BN == 128) return 128;
+  return LPQT_PREFILL_BN;
 }
 
 template <int BN, bool CSK>
@@ -1430,11 +1551,20 @@ static Plan make_plan(int64_t M, int64_t N, int64_t K, int split_k, int flags, i
     case 32: cfg_of<32, false>(p); break;
     case 64: cfg_of<64, false>(p); break;
     case 128: cfg_of<128, false>(p); break;
+    case 192: cfg_of<192, false>(p); break;
     default: cfg_of<256, false>(p); break;
   }
   p.ksteps = (p.k_tiles + p.kstep - 1) / p.kstep;
   p.total = p.tiles * p.ksteps;
   int64_t g = split_k > 0 ? p.tiles * split_k : sms;
+  // BN >= 64: splitting a tile costs a 128 x BN fp32 partial round trip per
+  // contributor; it pays only when each CTA still contracts >= ~24 k-tiles
+  // (measured, profiles/r01_v8_abx_split_cap.jsonl: no split at K = 4096, two
+  // at 8192, three at 11008, four at 28672)
+  if (split_k == 0 && p.kstep == 1) {
+    const int64_t cap = LPQT_SK_SPLIT_WIDE > 0 ? LPQT_SK_SPLIT_WIDE : std::min(4, std::max(1, p.k_tiles / 24));
+    if (g > p.tiles * cap) g = p.tiles * cap;
+  }
   if (g > p.total) g = p.total;
   if (p.tiles > kMaxCounters) g = p.tiles;  // one whole tile per CTA: no counters needed
   if (g < 1) g = 1;
@@ -1444,6 +1574,18 @@ static Plan make_plan(int64_t M, int64_t N, int64_t K, int split_k, int flags, i
   if (p.partials) {
     p.counters_bytes = kMaxCounters * 4;  // fixed region, zeroed once, self-resetting
     p.ws_bytes = p.counters_bytes + (int64_t)p.grid * 2 * kTileN * p.bn * 4;
+  }
+  // prefill whose X outgrows L2 (see args.n_fastest): round-robin whole tiles
+  // keep the CTAs in flight on consecutive tiles, sharing X in L2
+  if (p.kstep == 1 && p.m_tiles > 1 && M * K * 2 > ((int64_t)40 << 20) && p.tiles >= 2 * (int64_t)sms &&
+      p.tiles < ((int64_t)1 << 30) && split_k == 0 && !(flags & LPQT_SCHED_STREAMK)) {
+    p.dp = true;
+    p.grid = sms;
+    p.partials = false;
+    p.counters_bytes = 0;
+    p.ws_bytes = 0;
+    p.splits = 1;
+    return p;
   }
   const int64_t per = p.total / p.grid;  // k-steps per CTA (floor)
   p.splits = p.partials ? static_cast<int>((p.ksteps + (per > 0 ? per : 1) - 1) / (per > 0 ? per : 1) + 1) : 1;
@@ -1594,7 +1736,7 @@ int lpqt_w6a16_plan_ex(int64_t M, int64_t N, int64_t K, int split_k, int flags, 
   if (M <= 0 || N <= 0 || K <= 0) return LPQT_E_SHAPE;
   if ((flags & LPQT_SCHED_STREAMK) && (flags & LPQT_SCHED_CLUSTER)) return LPQT_E_INVALID_INPUT;
   const Plan p = make_plan(M, N, K, split_k, flags, num_sms());
-  const int v[6] = {p.bn, p.splits, p.grid, p.stages, p.csk ? 1 : 0, p.csk ? p.cluster : 0};
+  const int v[6] = {p.bn, p.splits, p.grid, p.stages, p.csk ? 1 : (p.dp ? 2 : 0), p.csk ? p.cluster : 0};
   for (int i = 0; i < n_out && i < 6; ++i) out[i] = v[i];
   return LPQT_OK;
 }
@@ -1664,6 +1806,7 @@ int lpqt_w6a16_linear_pf(const uint8_t* tiles, const uint16_t* scales, const uin
   args.tile_count = static_cast<int>(p.tiles);
   // X larger than ~1/3 of L2 (126 MB): keep each batch tile's X resident
   args.n_fastest = (p.m_tiles > 1 && M * K * 2 > (int64_t)40 << 20) ? 1 : 0;
+  args.dp = p.dp ? 1 : 0;
   args.y_dtype = y_dtype;
   args.y_layout = y_layout;
   args.sm = ShiftMuls{1u << 26, 1u << 28, 1u << 30};
@@ -1706,6 +1849,7 @@ int lpqt_w6a16_linear_pf(const uint8_t* tiles, const uint16_t* scales, const uin
                     : launch_impl<32, false, false>(p, args, pfa, Xt, ldx, M, st, flags);
     case 64: return launch_impl<64, false, false>(p, args, pfa, Xt, ldx, M, st, flags);
     case 128: return launch_impl<128, false, false>(p, args, pfa, Xt, ldx, M, st, flags);
+    case 192: return launch_impl<192, false, false>(p, args, pfa, Xt, ldx, M, st, flags);
     default: return launch_impl<256, false, false>(p, args, pfa, Xt, ldx, M, st, flags);
   }
 }

@@ -442,6 +442,22 @@ def test_prefill_large_x_weight_row_fastest_order():
     assert normwise_rel(Y.cpu().numpy(), Y_ref.cpu().numpy()) <= REL_TOL
 
 
+def test_prefill_round_robin_tiles_match_stream_k():
+    """X > 40 MB with >= 2 waves of tiles: whole tiles round-robin over the
+    CTAs (plan schedule "roundrobin"); same result as forced stream-K within
+    the fp32 summation tolerance, and within REL_TOL of the f64 reference."""
+    g = torch.Generator(device="cuda").manual_seed(23)
+    n, k, m = 4096, 8192, 2600
+    assert L.plan(m, n, k)["schedule"] == "roundrobin"
+    w = L.Fp6Weight.quantize((torch.randn(n, k, generator=g, device="cuda") * 0.02).half())
+    x = torch.randn(m, k, generator=g, device="cuda").half()
+    y = L.w6a16_linear(x, w, out_dtype=torch.float32)
+    y_sk = L.w6a16_linear(x, w, out_dtype=torch.float32, sched="streamk")
+    assert normwise_rel(y.cpu().numpy(), y_sk.cpu().numpy()) <= 1e-5
+    ref = (x.double() @ w.dequantize_f16().double().t())
+    assert normwise_rel(y.cpu().numpy(), ref.cpu().numpy()) <= REL_TOL
+
+
 @pytest.mark.parametrize("m", [1, 16, 512])
 def test_prefetch_next_linear_is_transparent(m):
     """lpqt_w6a16_linear_pf: naming the next launch's weight (stream-K and
@@ -474,3 +490,20 @@ def test_streamk_fixup_paths_bit_identical(n, k, m):
         assert torch.equal(y.view(torch.int32), ys[0].view(torch.int32))
     ref = (w.dequantize_f16().double() @ x.double().t()).t()
     assert normwise_rel(ys[0].cpu().numpy(), ref.cpu().numpy()) <= REL_TOL
+
+
+def test_split_k_workspace_shared_across_shapes_is_exact():
+    """Launches of different shapes back to back (PDL) reuse the same split-K
+    workspace slots; every result must equal its own first run bit for bit
+    (partials are read through L2 only — an L1 line left by the previous
+    shape's launch must never be seen)."""
+    g = torch.Generator(device="cuda").manual_seed(31)
+    shapes = [(4096, 11008, 1), (640, 256, 1), (4096, 11008, 16), (1024, 8192, 3), (8192, 8192, 128),
+              (4096, 4096, 300)]
+    ws = [L.Fp6Weight.quantize((torch.randn(n, k, device="cuda", generator=g) * 0.02).half()) for n, k, _ in shapes]
+    xs = [torch.randn(m, k, device="cuda", generator=g).half() for _, k, m in shapes]
+    want = [L.w6a16_linear(x, w, out_dtype=torch.float32) for x, w in zip(xs, ws)]
+    for r in range(30):
+        for i in (range(len(shapes)) if r % 2 else reversed(range(len(shapes)))):
+            y = L.w6a16_linear(xs[i], ws[i], out_dtype=torch.float32, prefetch=ws[(i + 1) % len(ws)])
+            assert torch.equal(y, want[i]), (r, shapes[i])
