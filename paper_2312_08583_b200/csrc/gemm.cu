@@ -502,6 +502,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                          const GemmArgs a, const L2Prefetch pf) {
   using C = Cfg<BN, CSK>;
   constexpr int KS = C::kKStep;
+  // barrier waits: decode (BN <= 32) parks in the hardware try_wait (woken on
+  // the phase flip); prefill re-polls every LPQT_WAIT_HINT_NS (measured,
+  // profiles/r01_v9_abx_wait_modes.jsonl)
+  constexpr int WM = BN <= 32 ? 0 : LPQT_WAIT_MODE;
   using Sched = typename std::conditional<CSK, CskSched, SkSched>::type;
   // The dynamic shared window starts 1024-aligned (as CUTLASS also assumes
   // for SW128 operands; checked below), so every address is a constant offset
@@ -621,7 +625,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       tile_nm(a, it.sg.tile, n_tile, m_tile);
       if (is_w) {
         const int s = i % C::kWStages;
-        mbar_wait(&empty_w[s], ((i / C::kWStages) & 1) ^ 1);
+        mbar_wait<WM>(&empty_w[s], ((i / C::kWStages) & 1) ^ 1);
         const uint8_t* src = a.tiles + ((int64_t)n_tile * a.k_tiles + kt) * kTileBytes;
         const uint32_t bytes = static_cast<uint32_t>(nt * kTileBytes);
         const uint32_t e = elect_one();
@@ -630,7 +634,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (i == 0 && lane == 0) CTA_STAMP(20);
       } else {
         const int s = i % C::kXStages;
-        mbar_wait(&empty_x[s], ((i / C::kXStages) & 1) ^ 1);
+        mbar_wait<WM>(&empty_x[s], ((i / C::kXStages) & 1) ^ 1);
         uint8_t* xs = smem_x + s * C::kXStageBytes;
         const uint32_t e = elect_one();
         mbar_arrive_expect_tx_if(e, &full_x[s], static_cast<uint32_t>(nt * C::kXTileBytes));
@@ -707,7 +711,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     };
     uint32_t q[kSegs][6 * 2];
     auto load_words = [&](int nt) {
-      mbar_wait_u32(fw0 + 8 * wc.idx, wc.ph);
+      mbar_wait_u32<WM>(fw0 + 8 * wc.idx, wc.ph);
       if (KS == 1 || tl < nt) {
         const uint32_t src = w_src + wc.idx * C::kWStageBytes;
 #pragma unroll
@@ -739,7 +743,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
       for (int j = 0; j < 32; ++j) r[j] = q[0][j % 12];
 #endif
-      mbar_wait_u32(ae0 + 8 * ac.idx, ac.ph ^ 1u);
+      mbar_wait_u32<WM>(ae0 + 8 * ac.idx, ac.ph ^ 1u);
       tc_fence_after();
       if (act) {
         const uint32_t ta = t_lane + ac.idx * (KS * kAColsPerBuf);
@@ -792,7 +796,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int i0 = 0; sc.template seg_at<KS>(a, i0, sg); i0 += sg.len) {
         const int d = lu % C::kDBufs;
         const uint32_t dph = (lu / C::kDBufs) & 1;
-        mbar_wait(&dempty[d], dph ^ 1);
+        mbar_wait<WM>(&dempty[d], dph ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_d0 + d * C::kDCols + mw * BN;
         const int s_first = C::kMmaWarps == 2 ? ((mw - sg.i0) & 1) : 0;
@@ -802,9 +806,9 @@ __global__ void __launch_bounds__(kThreads, 1)
           const int nt = min(KS, sg.kt1 - kt);
           const int xs = it % C::kXStages;
           const int slot = it % C::kASlots;
-          mbar_wait(&full_x[xs], (it / C::kXStages) & 1);
+          mbar_wait<WM>(&full_x[xs], (it / C::kXStages) & 1);
           if (it == mw && lane == 0) CTA_STAMP(14);
-          mbar_wait(&afull[slot], (it / C::kASlots) & 1);
+          mbar_wait<WM>(&afull[slot], (it / C::kASlots) & 1);
           tc_fence_after();
           const uint32_t e = elect_one();
           // descriptor of X block 0 of this stage; every other operand is a
@@ -965,7 +969,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                              fix_bar);
             }
           }
-          mbar_wait(fix_bar, fph);
+          mbar_wait<WM>(fix_bar, fph);
           fph ^= 1u;
           const bool last_batch = b1 == c_last;
 #pragma unroll 1
@@ -1047,7 +1051,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             peek();
           }
         }
-        mbar_wait(&dfull[d], dph);
+        mbar_wait<WM>(&dfull[d], dph);
         // second look once the MMAs are done: the other contributors usually
         // finished meanwhile, and a hit skips publishing + the acq_rel atomic
         if (peek_ok && !sk_last) peek();
@@ -1062,7 +1066,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             named_bar_sync(1, kNumEpiWarps * 32);  // last_flag is reused below
           }
         }
-        mbar_wait(&dfull[d], dph);
+        mbar_wait<WM>(&dfull[d], dph);
       }
       if (last_seg && warp == kWarpEpi0 && lane == 0) CTA_STAMP(8);
       tc_fence_after();
@@ -1217,7 +1221,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
           }
           y_begin();
-          mbar_wait(fix_bar, 0);
+          mbar_wait<WM>(fix_bar, 0);
           if (warp == kWarpEpi0 && lane == 0) CTA_STAMP(23);
           const uint32_t base = smem_u32(smem_w) + static_cast<uint32_t>(rr * 16);  // chunk-major rows
 #pragma unroll 1
@@ -1300,7 +1304,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
           }
           y_begin();
-          mbar_wait(fix_bar, 0);
+          mbar_wait<WM>(fix_bar, 0);
           if (warp == kWarpEpi0 && lane == 0) CTA_STAMP(23);
           const uint32_t base = smem_u32(smem_w) + static_cast<uint32_t>(rr * 16);  // chunk-major rows
 #pragma unroll 1
