@@ -25,6 +25,7 @@ ap.add_argument("--m", type=int, default=16)
 ap.add_argument("--depths", default="-1,16384,32768,65536,131072,262144")
 ap.add_argument("--steps", type=int, default=50)
 ap.add_argument("--rounds", type=int, default=5)
+ap.add_argument("--plans", default="", help="per-layer sched:split overrides, e.g. cluster:2,auto:0,streamk:0,auto:0")
 a = ap.parse_args()
 shapes = SHAPES[a.model]
 l2 = torch.cuda.get_device_properties(0).L2_cache_size
@@ -43,12 +44,16 @@ xs = [torch.randn(m, k, device="cuda").half() for _, k in shapes]
 ys = [torch.empty(m, n, device="cuda", dtype=torch.float16) for n, _ in shapes]
 
 
+plans = [(p.split(":")[0], int(p.split(":")[1])) for p in a.plans.split(",")] if a.plans else [("auto", 0)] * len(shapes)
+
+
 def step(c, depth):
     for i, w in enumerate(sets[c]):
         nxt = None
         if depth >= 0:
             nxt = sets[c][i + 1] if i + 1 < len(shapes) else sets[(c + 1) % copies][0]
-        L.w6a16_linear(xs[i], w, out=ys[i], prefetch=nxt, prefetch_bytes=max(depth, 0))
+        L.w6a16_linear(xs[i], w, out=ys[i], prefetch=nxt, prefetch_bytes=max(depth, 0), sched=plans[i][0],
+                       split_k=plans[i][1])
 
 
 depths = [int(v) for v in a.depths.split(",")]
@@ -80,5 +85,5 @@ for r in range(a.rounds):
 byt = sum(w.stream_bytes() for w in base) + sum(2 * m * k + 2 * m * n for n, k in shapes)
 for d in depths:
     t = sorted(times[d])[len(times[d]) // 2]
-    print(json.dumps({"model": a.model, "m": m, "prefetch_bytes_per_cta": d, "us_per_step": round(t, 2),
+    print(json.dumps({"model": a.model, "m": m, "plans": a.plans or "auto", "prefetch_bytes_per_cta": d, "us_per_step": round(t, 2),
                       "min": round(min(times[d]), 2), "GBps": round(byt / t / 1e3, 1)}), flush=True)
