@@ -206,6 +206,39 @@ int lpqt_w6a16_linear_pf(const uint8_t* tiles, const uint16_t* scales,
                          int64_t workspace_bytes, int flags,
                          const lpqt_next_linear* next, void* stream);
 
+/* ---- FGQ x FP6 (quantizer.py FGQ blocks :91-115, gemm.py:96-110) ---------
+ * One binary16 scale per (row, block of `block` columns), stored row-major
+ * (index r * ceil(K / block) + j); block <= 0 or >= K is CGQ (one per row),
+ * identical to the entries above.  Quantize / dequantize accept any block
+ * size; the GEMM takes blocks of whole 128-k tiles (block % 128 == 0, else
+ * LPQT_E_UNSUPPORTED) and applies each block's scale to the rebuilt binary16
+ * weights before the MMA (the binary16 dequant of dequant.py:72-79). */
+int lpqt_fp6_quantize_pack_blocks(const void* W, int dtype, int64_t N,
+                                  int64_t K, int64_t ldw, int64_t block,
+                                  int bias_shift, uint16_t* scales,
+                                  uint16_t* folded, uint8_t* seg4,
+                                  uint8_t* seg2, uint32_t* dev_flags,
+                                  void* stream);
+int lpqt_fp6_quantize_tiles_blocks(const void* W, int dtype, int64_t N,
+                                   int64_t K, int64_t ldw, int64_t block,
+                                   int bias_shift, uint16_t* scales,
+                                   uint16_t* folded, uint8_t* tiles,
+                                   uint32_t* dev_flags, void* stream);
+int lpqt_fp6_dequantize_tensor_blocks(const uint8_t* seg4, const uint8_t* seg2,
+                                      const uint16_t* block_scale, int path,
+                                      int64_t N, int64_t K, int64_t block,
+                                      void* out, int out_dtype, void* stream);
+int lpqt_fp6_tiles_dequant_blocks(const uint8_t* tiles, const uint16_t* scales,
+                                  int64_t N, int64_t K, int64_t block,
+                                  uint16_t* out, void* stream);
+int lpqt_w6a16_linear_blocks(const uint8_t* tiles, const uint16_t* scales,
+                             int64_t block, const uint16_t* Xt, int64_t ldx,
+                             int64_t M, int64_t N, int64_t K, void* Y,
+                             int y_dtype, int y_layout, int64_t ldy,
+                             int split_k, void* workspace,
+                             int64_t workspace_bytes, int flags,
+                             const lpqt_next_linear* next, void* stream);
+
 /* Number of kernel launches performed by this library since load (for the
  * bench's gpu_launches claim). */
 int64_t lpqt_launch_count(void);

@@ -74,6 +74,12 @@ SIGNATURES = {
                                     _P]),
     "lpqt_w6a16_linear_pf": (_I32, [_P, _P, _P, _I64, _I64, _I64, _I64, _P, _I32, _I32, _I64, _I32, _P, _I64, _I32,
                                     ctypes.POINTER(NextLinear), _P]),
+    "lpqt_fp6_quantize_pack_blocks": (_I32, [_P, _I32, _I64, _I64, _I64, _I64, _I32, _P, _P, _P, _P, _P, _P]),
+    "lpqt_fp6_quantize_tiles_blocks": (_I32, [_P, _I32, _I64, _I64, _I64, _I64, _I32, _P, _P, _P, _P, _P]),
+    "lpqt_fp6_dequantize_tensor_blocks": (_I32, [_P, _P, _P, _I32, _I64, _I64, _I64, _P, _I32, _P]),
+    "lpqt_fp6_tiles_dequant_blocks": (_I32, [_P, _P, _I64, _I64, _I64, _P, _P]),
+    "lpqt_w6a16_linear_blocks": (_I32, [_P, _P, _I64, _P, _I64, _I64, _I64, _I64, _P, _I32, _I32, _I64, _I32, _P,
+                                        _I64, _I32, ctypes.POINTER(NextLinear), _P]),
     "lpqt_launch_count": (_I64, []),
 }
 

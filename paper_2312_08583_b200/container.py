@@ -61,11 +61,6 @@ def write_lpqt(q: QuantizedTensor) -> bytes:
                        scheme.block_size if scheme.granularity is Granularity.FGQ else 0,
                        q.rows, q.cols, int(bool(q.bias_shift)), bytes(7))]
 
-    def section(raw: bytes, length_prefix: bool = False) -> None:
-        if length_prefix:
-            parts.append(struct.pack("<Q", len(raw)))
-        parts.append(raw)
-
     sections = [np.ascontiguousarray(_host(q.scales), dtype="<f2").tobytes()]
     if scheme.fmt is TensorFormat.INT4_ASYM:
         sections.append(np.ascontiguousarray(_host(q.zero_points), dtype="<f2").tobytes())
@@ -217,21 +212,22 @@ def load_lpqt(data: bytes):
     The stream is validated on the host (header fields, section lengths, the
     reference's scale checks), copied to the GPU once from pinned memory, and
     `lpqt_fp6_prepack` reads the canonical planes in place from the device
-    copy.  Only CGQ x FP6 (the path this library accelerates) loads; other
-    schemes raise InvalidScheme like quantize_tensor does.
+    copy.  FP6 under CGQ or FGQ (the formats this library runs) loads;
+    other schemes raise InvalidScheme like quantize_tensor does.
     """
     from .linear import Fp6Weight
-    from .quantizer import _require_path
+    from .quantizer import _require_path, scale_block
     hdr, _, off = _parse(data)
     _require_path(hdr["scheme"])
     t = _lib.torch()
     rows, cols = hdr["rows"], hdr["cols"]
+    nb = num_blocks(rows, cols, hdr["scheme"])
     host = t.frombuffer(bytearray(data), dtype=t.uint8).pin_memory()
     blob = host.to(_lib.device(), non_blocking=True)
-    scales = blob[off["scales"]:off["scales"] + 2 * rows].view(t.float16)
-    folded = blob[off["folded"]:off["folded"] + 2 * rows].view(t.float16) if hdr["bias_shift"] else None
+    scales = blob[off["scales"]:off["scales"] + 2 * nb].view(t.float16)
+    folded = blob[off["folded"]:off["folded"] + 2 * nb].view(t.float16) if hdr["bias_shift"] else None
     seg4 = blob[off["seg4"]:off["seg4"] + seg4_length(rows * cols)]
     tail = blob[off["tail"]:off["tail"] + tail_length(hdr["scheme"].fmt.minifloat, rows * cols)]
     # scales / folded are kept as views into the device copy of the stream;
     # the planes are only read by the prepack
-    return Fp6Weight.from_planes(seg4, tail, scales, rows, cols, folded)
+    return Fp6Weight.from_planes(seg4, tail, scales, rows, cols, folded, block=scale_block(hdr["scheme"]))

@@ -97,6 +97,21 @@ struct GemmArgs {
   ShiftMuls sm;       // 2^26, 2^28, 2^30: right shifts on the FMA pipe (common.cuh)
 };
 
+// FGQ (block scales, quantizer.py FGQ x FP6; gemm.py:96-110): scales are one
+// f16 per (row, block of bkt 128-k tiles), bpr per row; the dequant warps
+// multiply each rebuilt f16 weight by its block's scale before the MMA (the
+// binary16 dequant of dequant.py:72-79), the epilogue applies none.
+struct FgqArgs {
+  int bpr, bkt;
+};
+__device__ __forceinline__ void scale_f16x2(uint32_t (&r)[32], uint32_t s2) {
+#pragma unroll
+  for (int j = 0; j < 32; ++j) {
+    __half2 v = __hmul2(*reinterpret_cast<const __half2*>(&r[j]), *reinterpret_cast<const __half2*>(&s2));
+    r[j] = *reinterpret_cast<const uint32_t*>(&v);
+  }
+}
+
 // Cross-launch L2 prefetch of the NEXT linear's weights (lpqt_w6a16_linear_pf):
 // slice c = the first bytes the next launch's CTA c streams, derived from
 // that launch's plan (total > 0: stream-K, else cluster split-K).  A separate
@@ -496,10 +511,11 @@ __device__ __forceinline__ void ystage_put(const GemmArgs& a, uint32_t buf, int 
 // RAGGED: some stage holds fewer than kKStep tiles (the last k-step of a
 // tile when k_tiles % kKStep != 0, or an odd cluster split-K k-range); only
 // then do the dequant warps walk the stage sequence to learn tile counts.
-template <int BN, bool CSK, bool RAGGED>
+template <int BN, bool CSK, bool RAGGED, bool FGQ = false>
 __global__ void __launch_bounds__(kThreads, 1)
     w6a16_tcgen05_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constant__ CUtensorMap tmap_y,
-                         const GemmArgs a, const L2Prefetch pf) {
+                         const GemmArgs a, const L2Prefetch pf, const FgqArgs fg) {
+  static_assert(!FGQ || (RAGGED && !CSK), "FGQ walks the stage sequence (RAGGED) and uses no cluster split");
   using C = Cfg<BN, CSK>;
   constexpr int KS = C::kKStep;
   // barrier waits: decode (BN <= 32) parks in the hardware try_wait (woken on
@@ -710,7 +726,16 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     };
     uint32_t q[kSegs][6 * 2];
+    uint32_t fs2 = 0;  // FGQ: this stage's block scale as f16x2
     auto load_words = [&](int nt) {
+      if constexpr (FGQ) {
+        int n_tile, m_tile;
+        tile_nm(a, it.sg.tile, n_tile, m_tile);
+        const int n = n_tile * kTileN + row;
+        const int kt = it.kt() + (KS == 2 ? tl : 0);
+        const uint16_t sb = n < a.N ? __ldg(a.scales + (int64_t)n * fg.bpr + kt / fg.bkt) : static_cast<uint16_t>(0);
+        fs2 = static_cast<uint32_t>(sb) * 0x10001u;
+      }
       mbar_wait_u32<WM>(fw0 + 8 * wc.idx, wc.ph);
       if (KS == 1 || tl < nt) {
         const uint32_t src = w_src + wc.idx * C::kWStageBytes;
@@ -738,6 +763,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (act) {
         fp6x32_cvt_f16x32_fma(q[0], r, sm);
         fp6x32_cvt_f16x32_fma(q[0] + 6, r + 16, sm);
+        if constexpr (FGQ) scale_f16x2(r, fs2);
       }
 #else
 #pragma unroll
@@ -753,6 +779,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #ifndef LPQT_EXP_NO_REBUILD
           fp6x32_cvt_f16x32_fma(q[h], r, sm);
           fp6x32_cvt_f16x32_fma(q[h] + 6, r + 16, sm);
+          if constexpr (FGQ) scale_f16x2(r, fs2);
 #else
 #pragma unroll
           for (int j = 0; j < 32; ++j) r[j] = q[h][j % 12];
@@ -860,6 +887,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       int nt, mt;
       tile_nm(a, g.tile, nt, mt);
       const int nn = nt * kTileN + rr;
+      if constexpr (FGQ) return nn < a.N ? static_cast<uint16_t>(0x3C00u) : static_cast<uint16_t>(0);  // (in A)
       return nn < a.N ? __ldg(a.scales + nn) : static_cast<uint16_t>(0);
     };
     Seg sg_next;
@@ -1495,7 +1523,7 @@ static int max_clusters_bn(int bn, int c) { return bn <= 16 ? max_clusters<16>(c
 // split_k == 0: automatic schedule.  With LPQT_SCHED_CLUSTER: cluster
 // split-K with C = split_k (>= 1).  Otherwise split_k > 0 is stream-K with
 // about split_k CTAs per tile (testing / tuning hooks).
-static Plan make_plan(int64_t M, int64_t N, int64_t K, int split_k, int flags, int sms) {
+static Plan make_plan(int64_t M, int64_t N, int64_t K, int split_k, int flags, int sms, bool fgq = false) {
   Plan p{};
   p.bn = pick_bn(M);
   p.n_tiles = static_cast<int>((N + kTileN - 1) / kTileN);
@@ -1503,7 +1531,7 @@ static Plan make_plan(int64_t M, int64_t N, int64_t K, int split_k, int flags, i
   p.k_tiles = static_cast<int>((K + kTileK - 1) / kTileK);
   p.tiles = (int64_t)p.n_tiles * p.m_tiles;
   // ---- schedule choice (decode, BN <= 32, may use cluster split-K)
-  const bool csk_ok = p.bn <= 32 && p.tiles < ((int64_t)1 << 30);
+  const bool csk_ok = !fgq && p.bn <= 32 && p.tiles < ((int64_t)1 << 30);  // (FGQ: stream-K / round-robin only)
   int best_c = 0;
   if (csk_ok && !(flags & LPQT_SCHED_STREAMK)) {
     if (flags & LPQT_SCHED_CLUSTER) {
@@ -1629,8 +1657,9 @@ static int g_trace_n = 0;  // launches traced so far
 static int trace_next_slot() { return g_trace_n++ % kTraceSlots; }
 #endif
 
-template <int BN, bool CSK, bool RAGGED>
-static int launch_impl(const Plan& p, const GemmArgs& args, const L2Prefetch& pf, const uint16_t* Xt, int64_t ldx,
+template <int BN, bool CSK, bool RAGGED, bool FGQ = false>
+static int launch_impl(const Plan& p, const GemmArgs& args, const L2Prefetch& pf, const FgqArgs& fg,
+                       const uint16_t* Xt, int64_t ldx,
                        int64_t M, cudaStream_t stream, int flags) {
   EncodeTiledFn enc = encode_fn();
   if (!enc) return LPQT_E_CUDA;
@@ -1643,7 +1672,7 @@ static int launch_impl(const Plan& p, const GemmArgs& args, const L2Prefetch& pf
           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
     return LPQT_E_INVALID_INPUT;
-  auto kern = w6a16_tcgen05_kernel<BN, CSK, RAGGED>;
+  auto kern = w6a16_tcgen05_kernel<BN, CSK, RAGGED, FGQ>;
   constexpr int smem = Cfg<BN, CSK>::kSmemBytes;
   static std::once_flag once;
   static cudaError_t attr_err = cudaSuccess;
@@ -1696,7 +1725,7 @@ static int launch_impl(const Plan& p, const GemmArgs& args, const L2Prefetch& pf
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS)
       a2.y_tma = 1;
   }
-  if (cudaLaunchKernelEx(&cfg, kern, map, ymap, a2, pf) != cudaSuccess) return LPQT_E_CUDA;
+  if (cudaLaunchKernelEx(&cfg, kern, map, ymap, a2, pf, fg) != cudaSuccess) return LPQT_E_CUDA;
   note_launch();
   return check_launch();
 }
@@ -1776,7 +1805,24 @@ int lpqt_w6a16_linear_pf(const uint8_t* tiles, const uint16_t* scales, const uin
                          int64_t N, int64_t K, void* Y, int y_dtype, int y_layout, int64_t ldy, int split_k,
                          void* workspace, int64_t workspace_bytes, int flags, const lpqt_next_linear* next,
                          void* stream) {
+  return lpqt_w6a16_linear_blocks(tiles, scales, 0, Xt, ldx, M, N, K, Y, y_dtype, y_layout, ldy, split_k, workspace,
+                                  workspace_bytes, flags, next, stream);
+}
+
+int lpqt_w6a16_linear_blocks(const uint8_t* tiles, const uint16_t* scales, int64_t block, const uint16_t* Xt,
+                             int64_t ldx, int64_t M, int64_t N, int64_t K, void* Y, int y_dtype, int y_layout,
+                             int64_t ldy, int split_k, void* workspace, int64_t workspace_bytes, int flags,
+                             const lpqt_next_linear* next, void* stream) {
   if (flags & ~(LPQT_LAUNCH_PDL | LPQT_SCHED_STREAMK | LPQT_SCHED_CLUSTER)) return LPQT_E_INVALID_INPUT;
+  // FGQ: blocks of B columns (B = K, or block <= 0: one scale per row)
+  const bool fgq = block > 0 && block < K;
+  if (fgq && block % kTileK != 0) return LPQT_E_UNSUPPORTED;   // block scales at 128-k tile granularity
+  if (fgq && (flags & LPQT_SCHED_CLUSTER)) return LPQT_E_UNSUPPORTED;
+  FgqArgs fga{};
+  if (fgq) {
+    fga.bpr = static_cast<int>((K + block - 1) / block);
+    fga.bkt = static_cast<int>(block / kTileK);
+  }
   if ((flags & LPQT_SCHED_STREAMK) && (flags & LPQT_SCHED_CLUSTER)) return LPQT_E_INVALID_INPUT;
   if (M < 0 || N < 0 || K < 0) return LPQT_E_SHAPE;
   if (M == 0 || N == 0) return LPQT_OK;
@@ -1787,7 +1833,7 @@ int lpqt_w6a16_linear_pf(const uint8_t* tiles, const uint16_t* scales, const uin
   if (y_layout == LPQT_Y_NM ? ldy < M : ldy < N) return LPQT_E_SHAPE;
   if (split_k < 0) return LPQT_E_INVALID_INPUT;
   if (N > (int64_t)1 << 30 || M > (int64_t)1 << 30 || K > (int64_t)1 << 30) return LPQT_E_SHAPE;
-  const Plan p = make_plan(M, N, K, split_k, flags, num_sms());
+  Plan p = make_plan(M, N, K, split_k, flags, num_sms(), fgq);
   if (p.ws_bytes > 0 && (workspace == nullptr || workspace_bytes < p.ws_bytes)) return LPQT_E_WORKSPACE;
   GemmArgs args{};
   L2Prefetch pfa{};
@@ -1834,27 +1880,37 @@ int lpqt_w6a16_linear_pf(const uint8_t* tiles, const uint16_t* scales, const uin
     }
   }
   cudaStream_t st = as_stream(stream);
+  if (fgq) {  // the dequant warps walk the stage sequence for the block scales (RAGGED instantiation)
+    switch (p.bn) {
+      case 16: return launch_impl<16, false, true, true>(p, args, pfa, fga, Xt, ldx, M, st, flags);
+      case 32: return launch_impl<32, false, true, true>(p, args, pfa, fga, Xt, ldx, M, st, flags);
+      case 64: return launch_impl<64, false, true, true>(p, args, pfa, fga, Xt, ldx, M, st, flags);
+      case 128: return launch_impl<128, false, true, true>(p, args, pfa, fga, Xt, ldx, M, st, flags);
+      case 192: return launch_impl<192, false, true, true>(p, args, pfa, fga, Xt, ldx, M, st, flags);
+      default: return LPQT_E_UNSUPPORTED;
+    }
+  }
   bool ragged = p.k_tiles % p.kstep != 0;
   if (p.csk) {
     for (int r = 0; r < p.cluster; ++r)  // k-range of rank r must be a whole number of stages
       ragged |= ((r + 1) * p.k_tiles / p.cluster - r * p.k_tiles / p.cluster) % p.kstep != 0;
     if (p.bn <= 16)
-      return ragged ? launch_impl<16, true, true>(p, args, pfa, Xt, ldx, M, st, flags)
-                    : launch_impl<16, true, false>(p, args, pfa, Xt, ldx, M, st, flags);
-    return ragged ? launch_impl<32, true, true>(p, args, pfa, Xt, ldx, M, st, flags)
-                  : launch_impl<32, true, false>(p, args, pfa, Xt, ldx, M, st, flags);
+      return ragged ? launch_impl<16, true, true>(p, args, pfa, fga, Xt, ldx, M, st, flags)
+                    : launch_impl<16, true, false>(p, args, pfa, fga, Xt, ldx, M, st, flags);
+    return ragged ? launch_impl<32, true, true>(p, args, pfa, fga, Xt, ldx, M, st, flags)
+                  : launch_impl<32, true, false>(p, args, pfa, fga, Xt, ldx, M, st, flags);
   }
   switch (p.bn) {
     case 16:
-      return ragged ? launch_impl<16, false, true>(p, args, pfa, Xt, ldx, M, st, flags)
-                    : launch_impl<16, false, false>(p, args, pfa, Xt, ldx, M, st, flags);
+      return ragged ? launch_impl<16, false, true>(p, args, pfa, fga, Xt, ldx, M, st, flags)
+                    : launch_impl<16, false, false>(p, args, pfa, fga, Xt, ldx, M, st, flags);
     case 32:
-      return ragged ? launch_impl<32, false, true>(p, args, pfa, Xt, ldx, M, st, flags)
-                    : launch_impl<32, false, false>(p, args, pfa, Xt, ldx, M, st, flags);
-    case 64: return launch_impl<64, false, false>(p, args, pfa, Xt, ldx, M, st, flags);
-    case 128: return launch_impl<128, false, false>(p, args, pfa, Xt, ldx, M, st, flags);
-    case 192: return launch_impl<192, false, false>(p, args, pfa, Xt, ldx, M, st, flags);
-    default: return launch_impl<256, false, false>(p, args, pfa, Xt, ldx, M, st, flags);
+      return ragged ? launch_impl<32, false, true>(p, args, pfa, fga, Xt, ldx, M, st, flags)
+                    : launch_impl<32, false, false>(p, args, pfa, fga, Xt, ldx, M, st, flags);
+    case 64: return launch_impl<64, false, false>(p, args, pfa, fga, Xt, ldx, M, st, flags);
+    case 128: return launch_impl<128, false, false>(p, args, pfa, fga, Xt, ldx, M, st, flags);
+    case 192: return launch_impl<192, false, false>(p, args, pfa, fga, Xt, ldx, M, st, flags);
+    default: return launch_impl<256, false, false>(p, args, pfa, fga, Xt, ldx, M, st, flags);
   }
 }
 

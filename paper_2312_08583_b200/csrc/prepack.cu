@@ -65,22 +65,25 @@ __global__ void unprepack_kernel(const uint8_t* __restrict__ tiles, int64_t N, i
 }
 
 // K3: tiles -> out[N, K] binary16 = value_f16[c] * S[n] (the GEMM's transform)
+// scales: one per (row, block of B columns), B = K for CGQ
 __global__ void tiles_dequant_kernel(const uint8_t* __restrict__ tiles, const uint16_t* __restrict__ scales,
-                                     int64_t N, int64_t K, int64_t Kp, uint16_t* __restrict__ out) {
+                                     int64_t N, int64_t K, int64_t Kp, int64_t B, int64_t bpr,
+                                     uint16_t* __restrict__ out) {
   const int64_t groups = Kp / 32, total = N * groups, k_tiles = Kp / kTileK;
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
     const int64_t n = t / groups, g = t % groups;
     uint32_t w[6], h[16];
     load_group(tiles, n, g, k_tiles, w);
     fp6x32_cvt_f16x32(w, h);
-    const __half2 f2 = __half2half2(__ushort_as_half(scales[n]));
 #pragma unroll
     for (int j = 0; j < 16; ++j) {
-      __half2 v = *reinterpret_cast<const __half2*>(&h[j]);
-      v = __hmul2(v, f2);
+      const __half2 v = *reinterpret_cast<const __half2*>(&h[j]);
       const int64_t k = g * 32 + 2 * j;
-      if (k < K) out[n * K + k] = __half_as_ushort(__low2half(v));
-      if (k + 1 < K) out[n * K + k + 1] = __half_as_ushort(__high2half(v));
+      if (k < K)
+        out[n * K + k] = __half_as_ushort(__hmul(__low2half(v), __ushort_as_half(scales[n * bpr + k / B])));
+      if (k + 1 < K)
+        out[n * K + k + 1] =
+            __half_as_ushort(__hmul(__high2half(v), __ushort_as_half(scales[n * bpr + (k + 1) / B])));
     }
   }
 }
@@ -116,14 +119,21 @@ int lpqt_fp6_unprepack(const uint8_t* tiles, int64_t N, int64_t K, uint8_t* code
   return check_launch();
 }
 
-int lpqt_fp6_tiles_dequant(const uint8_t* tiles, const uint16_t* scales, int64_t N, int64_t K, uint16_t* out,
-                           void* stream) {
+int lpqt_fp6_tiles_dequant_blocks(const uint8_t* tiles, const uint16_t* scales, int64_t N, int64_t K, int64_t block,
+                                  uint16_t* out, void* stream) {
   if (N < 0 || K < 0) return LPQT_E_SHAPE;
   if (N == 0 || K == 0) return LPQT_OK;
   const int64_t Kp = round_up(K, kTileK);
-  tiles_dequant_kernel<<<grid_for(N * (Kp / 32), 256), 256, 0, as_stream(stream)>>>(tiles, scales, N, K, Kp, out);
+  const int64_t B = (block <= 0 || block >= K) ? K : block, bpr = (K + B - 1) / B;
+  tiles_dequant_kernel<<<grid_for(N * (Kp / 32), 256), 256, 0, as_stream(stream)>>>(tiles, scales, N, K, Kp, B, bpr,
+                                                                                     out);
   note_launch();
   return check_launch();
+}
+
+int lpqt_fp6_tiles_dequant(const uint8_t* tiles, const uint16_t* scales, int64_t N, int64_t K, uint16_t* out,
+                           void* stream) {
+  return lpqt_fp6_tiles_dequant_blocks(tiles, scales, N, K, 0, out, stream);
 }
 
 }  // extern "C"

@@ -174,32 +174,37 @@ __device__ __forceinline__ uint32_t encode1(typename InTraits<DT>::Acc v, float 
   else return fp6_encode(static_cast<double>(v) / static_cast<double>(S), mids);
 }
 
-// ---- K1a: per-row scales (quantizer.py:200-201, :225-227, _round_scales_f16
-// :142-153; fold dequant.py:61-69).  One warp per row, 16-byte loads.
+// ---- K1a: per-block scales (quantizer.py:200-201, :224-227 with the FGQ
+// blocks of :91-115, _round_scales_f16 :142-153; fold dequant.py:61-69).  One
+// warp per (row, block of B columns) — B = K for CGQ (one block per row) —
+// scales stored row-major per block (r * bpr + j); 16-byte loads.
 template <int DT>
-__global__ void __launch_bounds__(256) row_scales_kernel(const void* __restrict__ W, int64_t N, int64_t K,
-                                                         int64_t ldw, int vec, int bias_shift,
-                                                         uint16_t* __restrict__ scales, uint16_t* __restrict__ folded,
-                                                         uint32_t* __restrict__ flags) {
+__global__ void __launch_bounds__(256) block_scales_kernel(const void* __restrict__ W, int64_t N, int64_t K,
+                                                           int64_t ldw, int64_t B, int64_t bpr, int vec,
+                                                           int bias_shift, uint16_t* __restrict__ scales,
+                                                           uint16_t* __restrict__ folded,
+                                                           uint32_t* __restrict__ flags) {
   using Acc = typename InTraits<DT>::Acc;
   const int lane = threadIdx.x & 31;
   const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
   uint32_t f = 0;
-  for (int64_t r = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); r < N; r += warps) {
+  for (int64_t u = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); u < N * bpr; u += warps) {
+    const int64_t r = u / bpr, j = u - r * bpr;
+    const int64_t k0 = j * B, k1 = k0 + B < K ? k0 + B : K;
     const char* row = static_cast<const char*>(W) + r * ldw * elem_bytes<DT>();
     Acc peak = 0;
     bool bad = false;
-    const int64_t k8 = vec ? K / 8 * 8 : 0;
-    for (int64_t k = 8 * lane; k < k8; k += 256) {
+    const int64_t k8 = (vec && k0 % 8 == 0) ? k0 + (k1 - k0) / 8 * 8 : k0;
+    for (int64_t k = k0 + 8 * lane; k < k8; k += 256) {
       Acc v[8];
       load8<DT>(row + k * elem_bytes<DT>(), v);
 #pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        bad |= !isfinite(v[j]);
-        peak = fmax(peak, fabs(v[j]));
+      for (int q = 0; q < 8; ++q) {
+        bad |= !isfinite(v[q]);
+        peak = fmax(peak, fabs(v[q]));
       }
     }
-    for (int64_t k = k8 + lane; k < K; k += 32) {
+    for (int64_t k = k8 + lane; k < k1; k += 32) {
       const Acc v = load1<DT>(row, k);
       bad |= !isfinite(v);
       peak = fmax(peak, fabs(v));
@@ -213,15 +218,21 @@ __global__ void __launch_bounds__(256) row_scales_kernel(const void* __restrict_
       uint16_t sb = __half_as_ushort(__double2half(raw));
       if ((sb & 0x7FFFu) == 0x7C00u) f |= LPQT_F_SCALE_INF;
       if ((sb & 0x7FFFu) == 0) sb = 0x0001u;  // underflow clamps to 2^-24
-      scales[r] = sb;
+      scales[u] = sb;
       if (bias_shift) {
         const double fv = static_cast<double>(__half2float(__ushort_as_half(sb))) * 4096.0;
         if (fv > 65504.0) f |= LPQT_F_FOLD_OVERFLOW;
-        folded[r] = (fv > 65504.0) ? (uint16_t)0x7C00u : __half_as_ushort(__double2half(fv));
+        folded[u] = (fv > 65504.0) ? (uint16_t)0x7C00u : __half_as_ushort(__double2half(fv));
       }
     }
   }
   if (f) atomicOr(flags, f);
+}
+
+// scale of element (r, k) under B-column blocks (B = K: the row's scale)
+__device__ __forceinline__ float block_scale(const uint16_t* __restrict__ scales, int64_t r, int64_t k, int64_t B,
+                                             int64_t bpr) {
+  return __half2float(__ushort_as_half(scales[r * bpr + k / B]));
 }
 
 __device__ __forceinline__ void load_mids_f64(double* smem_mids) {
@@ -236,7 +247,7 @@ __device__ __forceinline__ void load_mids_f64(double* smem_mids) {
 // holds for any K; the last group pads with code 0 like packing.py:73).
 template <int DT>
 __global__ void __launch_bounds__(256) encode_planes_kernel(const void* __restrict__ W, int64_t N, int64_t K,
-                                                            int64_t ldw, int vec,
+                                                            int64_t ldw, int vec, int64_t B, int64_t bpr,
                                                             const uint16_t* __restrict__ scales,
                                                             uint8_t* __restrict__ seg4, uint8_t* __restrict__ seg2) {
   using Acc = typename InTraits<DT>::Acc;
@@ -246,11 +257,11 @@ __global__ void __launch_bounds__(256) encode_planes_kernel(const void* __restri
   for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < groups; g += (int64_t)gridDim.x * blockDim.x) {
     const int64_t i0 = 8 * g;
     uint64_t c = 0;
-    if (vec) {  // vec => K % 8 == 0: the whole group lies in one row
+    if (vec) {  // vec => K % 8 == 0 and B % 8 == 0: one row, one block
       const int64_t r = i0 / K, k = i0 - r * K;
       Acc v[8];
       load8<DT>(static_cast<const char*>(W) + (r * ldw + k) * elem_bytes<DT>(), v);
-      const float s = __half2float(__ushort_as_half(scales[r]));
+      const float s = block_scale(scales, r, k, B, bpr);
       c = encode8<DT>(v, s, static_cast<double>(s), mids);
     } else {
       int64_t r = i0 / K, k = i0 - r * K;
@@ -258,8 +269,7 @@ __global__ void __launch_bounds__(256) encode_planes_kernel(const void* __restri
       for (int j = 0; j < 8; ++j) {
         if (i0 + j < total) {
           const Acc v = load1<DT>(W, r * ldw + k);
-          const float s = __half2float(__ushort_as_half(scales[r]));
-          c |= static_cast<uint64_t>(encode1<DT>(v, s, mids)) << (8 * j);
+          c |= static_cast<uint64_t>(encode1<DT>(v, block_scale(scales, r, k, B, bpr), mids)) << (8 * j);
         }
         if (++k == K) k = 0, ++r;
       }
@@ -292,8 +302,9 @@ __device__ __forceinline__ void pack_words_from_bytes(const uint32_t cw[8], uint
 
 template <int DT>
 __global__ void __launch_bounds__(256) encode_tiles_kernel(const void* __restrict__ W, int64_t N, int64_t K,
-                                                           int64_t ldw, int vec, const uint16_t* __restrict__ scales,
-                                                           int64_t Np, int64_t k_tiles, uint8_t* __restrict__ tiles) {
+                                                           int64_t ldw, int vec, int64_t B, int64_t bpr,
+                                                           const uint16_t* __restrict__ scales, int64_t Np,
+                                                           int64_t k_tiles, uint8_t* __restrict__ tiles) {
   using Acc = typename InTraits<DT>::Acc;
   __shared__ double mids[32];
   if constexpr (!InTraits<DT>::kCvt) load_mids_f64(mids);
@@ -307,28 +318,32 @@ __global__ void __launch_bounds__(256) encode_tiles_kernel(const void* __restric
     const int64_t n = rt * kTileN + rr, k0 = kt * kTileK + kh * 64;
     uint32_t cw[16];
     if (n < N) {
-      const float Sf = __half2float(__ushort_as_half(scales[n]));
-      const double Sd = static_cast<double>(Sf);
       const char* row = static_cast<const char*>(W) + n * ldw * elem_bytes<DT>();
-      if (vec && k0 + 64 <= K) {
+      if (vec && k0 + 64 <= K) {  // vec => B % 8 == 0: one scale per 8 columns
+        int64_t j = k0 / B, kb = (j + 1) * B;  // block of the current 8-group, its end
+        float Sf = __half2float(__ushort_as_half(scales[n * bpr + j]));
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
+          if (k0 + 8 * q >= kb) {
+            ++j, kb += B;
+            Sf = __half2float(__ushort_as_half(scales[n * bpr + j]));
+          }
           Acc v[8];
           load8<DT>(row + (k0 + 8 * q) * elem_bytes<DT>(), v);
-          const uint64_t c = encode8<DT>(v, Sf, Sd, mids);
+          const uint64_t c = encode8<DT>(v, Sf, static_cast<double>(Sf), mids);
           cw[2 * q] = static_cast<uint32_t>(c);
           cw[2 * q + 1] = static_cast<uint32_t>(c >> 32);
         }
       } else {
-#pragma unroll
+#pragma unroll 1
         for (int q = 0; q < 8; ++q) {
-          Acc v[8];
+          uint64_t c = 0;
 #pragma unroll
-          for (int j = 0; j < 8; ++j) {
-            const int64_t k = k0 + 8 * q + j;
-            v[j] = k < K ? load1<DT>(row, k) : Acc(0);
+          for (int e = 0; e < 8; ++e) {
+            const int64_t k = k0 + 8 * q + e;
+            if (k < K) c |= static_cast<uint64_t>(encode1<DT>(load1<DT>(row, k), block_scale(scales, n, k, B, bpr),
+                                                                mids)) << (8 * e);
           }
-          const uint64_t c = encode8<DT>(v, Sf, Sd, mids);
           cw[2 * q] = static_cast<uint32_t>(c);
           cw[2 * q + 1] = static_cast<uint32_t>(c >> 32);
         }
@@ -429,13 +444,13 @@ __global__ void dequant_naive_kernel(const uint8_t* __restrict__ codes, const ui
 template <int OUT>
 __global__ void dequantize_tensor_kernel(const uint8_t* __restrict__ seg4, const uint8_t* __restrict__ seg2,
                                          const uint16_t* __restrict__ row_scale, int path, int64_t N, int64_t K,
-                                         void* __restrict__ out) {
+                                         int64_t B, int64_t bpr, void* __restrict__ out) {
   const int64_t total = N * K;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
     const uint32_t c = canon_code(seg4, seg2, i);
-    const int64_t r = i / K;
+    const int64_t r = i / K, k = i - r * K;
     const __half comp = __ushort_as_half(fp6_compose_bits(c));
-    const __half s = __ushort_as_half(row_scale[r]);
+    const __half s = __ushort_as_half(row_scale[r * bpr + k / B]);  // the element's block (B = K: its row)
     if (OUT == LPQT_F64) {
       double v = static_cast<double>(__half2float(comp));
       if (path == 0) v *= 4096.0;
@@ -536,11 +551,13 @@ int lpqt_fp6_dequant_naive(const uint8_t* codes, const uint16_t* scales, int64_t
   return check_launch();
 }
 
-static int quantize_scales(const void* W, int dtype, int64_t N, int64_t K, int64_t ldw, int vec, int bias_shift,
-                           uint16_t* scales, uint16_t* folded, uint32_t* dev_flags, cudaStream_t st) {
-  const int g = static_cast<int>((N + 7) / 8 < 148 * 8 ? (N + 7) / 8 : 148 * 8);
-  LPQT_DISPATCH_DT(dtype, row_scales_kernel<DT><<<g, 256, 0, st>>>(W, N, K, ldw, vec, bias_shift, scales, folded,
-                                                                    dev_flags));
+static int quantize_scales(const void* W, int dtype, int64_t N, int64_t K, int64_t ldw, int64_t B, int64_t bpr,
+                           int vec, int bias_shift, uint16_t* scales, uint16_t* folded, uint32_t* dev_flags,
+                           cudaStream_t st) {
+  const int64_t units = N * bpr;
+  const int g = static_cast<int>((units + 7) / 8 < 148 * 8 ? (units + 7) / 8 : 148 * 8);
+  LPQT_DISPATCH_DT(dtype, block_scales_kernel<DT><<<g, 256, 0, st>>>(W, N, K, ldw, B, bpr, vec, bias_shift, scales,
+                                                                      folded, dev_flags));
   note_launch();
   return check_launch();
 }
@@ -549,60 +566,100 @@ static int rows_vectorizable(const void* W, int64_t ldw) {
   return (reinterpret_cast<uintptr_t>(W) % 16 == 0) && (ldw % 8 == 0);
 }
 
+// block <= 0 or >= K: CGQ (one block per row)
+static void block_geometry(int64_t K, int64_t block, int64_t& B, int64_t& bpr) {
+  B = (block <= 0 || block >= K) ? K : block;
+  bpr = (K + B - 1) / B;
+}
+
+static int check_quantize_args(const void* W, int dtype, int64_t N, int64_t K, int64_t ldw, int bias_shift,
+                               const uint16_t* folded) {
+  (void)W;
+  if (N < 0 || K < 0 || ldw < K) return LPQT_E_SHAPE;
+  if (bias_shift && folded == nullptr) return LPQT_E_INVALID_INPUT;
+  if (dtype < LPQT_F64 || dtype > LPQT_BF16) return LPQT_E_UNSUPPORTED;
+  return LPQT_OK;
+}
+
+int lpqt_fp6_quantize_pack_blocks(const void* W, int dtype, int64_t N, int64_t K, int64_t ldw, int64_t block,
+                                  int bias_shift, uint16_t* scales, uint16_t* folded, uint8_t* seg4, uint8_t* seg2,
+                                  uint32_t* dev_flags, void* stream) {
+  int rc = check_quantize_args(W, dtype, N, K, ldw, bias_shift, folded);
+  if (rc != LPQT_OK || N == 0 || K == 0) return rc;
+  const cudaStream_t st = as_stream(stream);
+  int64_t B, bpr;
+  block_geometry(K, block, B, bpr);
+  const int vec = rows_vectorizable(W, ldw);
+  rc = quantize_scales(W, dtype, N, K, ldw, B, bpr, vec, bias_shift, scales, folded, dev_flags, st);
+  if (rc != LPQT_OK) return rc;
+  const int64_t groups = (N * K + 7) / 8;
+  const int pv = vec && (K % 8 == 0) && (B % 8 == 0);
+  LPQT_DISPATCH_DT(dtype, encode_planes_kernel<DT><<<grid_for(groups, 256), 256, 0, st>>>(W, N, K, ldw, pv, B, bpr,
+                                                                                         scales, seg4, seg2));
+  note_launch();
+  return check_launch();
+}
+
 int lpqt_fp6_quantize_pack(const void* W, int dtype, int64_t N, int64_t K, int64_t ldw, int bias_shift,
                            uint16_t* scales, uint16_t* folded, uint8_t* seg4, uint8_t* seg2, uint8_t* codes_ws,
                            uint32_t* dev_flags, void* stream) {
   (void)codes_ws;  // no longer needed (ABI v1 argument)
-  if (N < 0 || K < 0 || ldw < K) return LPQT_E_SHAPE;
-  if (N == 0 || K == 0) return LPQT_OK;
-  if (bias_shift && folded == nullptr) return LPQT_E_INVALID_INPUT;
-  if (dtype < LPQT_F64 || dtype > LPQT_BF16) return LPQT_E_UNSUPPORTED;
+  return lpqt_fp6_quantize_pack_blocks(W, dtype, N, K, ldw, 0, bias_shift, scales, folded, seg4, seg2, dev_flags,
+                                       stream);
+}
+
+int lpqt_fp6_quantize_tiles_blocks(const void* W, int dtype, int64_t N, int64_t K, int64_t ldw, int64_t block,
+                                   int bias_shift, uint16_t* scales, uint16_t* folded, uint8_t* tiles,
+                                   uint32_t* dev_flags, void* stream) {
+  int rc = check_quantize_args(W, dtype, N, K, ldw, bias_shift, folded);
+  if (rc != LPQT_OK || N == 0 || K == 0) return rc;
+  if (tiles == nullptr || scales == nullptr) return LPQT_E_INVALID_INPUT;
   const cudaStream_t st = as_stream(stream);
+  int64_t B, bpr;
+  block_geometry(K, block, B, bpr);
   const int vec = rows_vectorizable(W, ldw);
-  int rc = quantize_scales(W, dtype, N, K, ldw, vec, bias_shift, scales, folded, dev_flags, st);
+  rc = quantize_scales(W, dtype, N, K, ldw, B, bpr, vec, bias_shift, scales, folded, dev_flags, st);
   if (rc != LPQT_OK) return rc;
-  const int64_t groups = (N * K + 7) / 8;
-  const int pv = vec && (K % 8 == 0);
-  LPQT_DISPATCH_DT(dtype, encode_planes_kernel<DT><<<grid_for(groups, 256), 256, 0, st>>>(W, N, K, ldw, pv, scales,
-                                                                                         seg4, seg2));
+  const int64_t Np = (N + kTileN - 1) / kTileN * kTileN, k_tiles = (K + kTileK - 1) / kTileK;
+  const int64_t threads = Np * k_tiles * 2;
+  const int tv = vec && (B % 8 == 0);
+  LPQT_DISPATCH_DT(dtype, encode_tiles_kernel<DT><<<grid_for(threads, 256), 256, 0, st>>>(W, N, K, ldw, tv, B, bpr,
+                                                                                         scales, Np, k_tiles, tiles));
   note_launch();
   return check_launch();
 }
 
 int lpqt_fp6_quantize_tiles(const void* W, int dtype, int64_t N, int64_t K, int64_t ldw, int bias_shift,
                             uint16_t* scales, uint16_t* folded, uint8_t* tiles, uint32_t* dev_flags, void* stream) {
-  if (N < 0 || K < 0 || ldw < K) return LPQT_E_SHAPE;
-  if (N == 0 || K == 0) return LPQT_OK;
-  if (bias_shift && folded == nullptr) return LPQT_E_INVALID_INPUT;
-  if (dtype < LPQT_F64 || dtype > LPQT_BF16) return LPQT_E_UNSUPPORTED;
-  if (tiles == nullptr || scales == nullptr) return LPQT_E_INVALID_INPUT;
-  const cudaStream_t st = as_stream(stream);
-  const int vec = rows_vectorizable(W, ldw);
-  int rc = quantize_scales(W, dtype, N, K, ldw, vec, bias_shift, scales, folded, dev_flags, st);
-  if (rc != LPQT_OK) return rc;
-  const int64_t Np = (N + kTileN - 1) / kTileN * kTileN, k_tiles = (K + kTileK - 1) / kTileK;
-  const int64_t threads = Np * k_tiles * 2;
-  LPQT_DISPATCH_DT(dtype, encode_tiles_kernel<DT><<<grid_for(threads, 256), 256, 0, st>>>(W, N, K, ldw, vec, scales,
-                                                                                         Np, k_tiles, tiles));
+  return lpqt_fp6_quantize_tiles_blocks(W, dtype, N, K, ldw, 0, bias_shift, scales, folded, tiles, dev_flags,
+                                        stream);
+}
+
+int lpqt_fp6_dequantize_tensor_blocks(const uint8_t* seg4, const uint8_t* seg2, const uint16_t* block_scale,
+                                      int path, int64_t N, int64_t K, int64_t block, void* out, int out_dtype,
+                                      void* stream) {
+  if (N < 0 || K < 0) return LPQT_E_SHAPE;
+  if (path != 0 && path != 1) return LPQT_E_INVALID_INPUT;
+  if (N * K == 0) return LPQT_OK;
+  int64_t B, bpr;
+  block_geometry(K, block, B, bpr);
+  const int g = grid_for(N * K, 256);
+  if (out_dtype == LPQT_F64) {
+    dequantize_tensor_kernel<LPQT_F64><<<g, 256, 0, as_stream(stream)>>>(seg4, seg2, block_scale, path, N, K, B, bpr,
+                                                                          out);
+  } else if (out_dtype == LPQT_F16) {
+    dequantize_tensor_kernel<LPQT_F16><<<g, 256, 0, as_stream(stream)>>>(seg4, seg2, block_scale, path, N, K, B, bpr,
+                                                                          out);
+  } else {
+    return LPQT_E_UNSUPPORTED;
+  }
   note_launch();
   return check_launch();
 }
 
 int lpqt_fp6_dequantize_tensor(const uint8_t* seg4, const uint8_t* seg2, const uint16_t* row_scale, int path,
                                int64_t N, int64_t K, void* out, int out_dtype, void* stream) {
-  if (N < 0 || K < 0) return LPQT_E_SHAPE;
-  if (path != 0 && path != 1) return LPQT_E_INVALID_INPUT;
-  if (N * K == 0) return LPQT_OK;
-  const int g = grid_for(N * K, 256);
-  if (out_dtype == LPQT_F64) {
-    dequantize_tensor_kernel<LPQT_F64><<<g, 256, 0, as_stream(stream)>>>(seg4, seg2, row_scale, path, N, K, out);
-  } else if (out_dtype == LPQT_F16) {
-    dequantize_tensor_kernel<LPQT_F16><<<g, 256, 0, as_stream(stream)>>>(seg4, seg2, row_scale, path, N, K, out);
-  } else {
-    return LPQT_E_UNSUPPORTED;
-  }
-  note_launch();
-  return check_launch();
+  return lpqt_fp6_dequantize_tensor_blocks(seg4, seg2, row_scale, path, N, K, 0, out, out_dtype, stream);
 }
 
 int lpqt_stage_activations(const void* X, int dtype, int64_t K, int64_t M, int64_t ldx, uint16_t* Xt, int64_t Kp,

@@ -18,7 +18,7 @@ import numpy as np
 from . import _lib
 from .errors import PayloadMismatch, ShapeError
 from .linear import Fp6Weight, gemm_nm, stage_activations
-from .quantizer import ErrorReport, QuantizedTensor, error_report, num_blocks
+from .quantizer import ErrorReport, QuantizedTensor, _require_gemm_path, error_report, num_blocks
 
 
 def _check_activation(X, k: int) -> None:
@@ -29,12 +29,16 @@ def _check_activation(X, k: int) -> None:
 
 
 def gemm_quantized(wq: QuantizedTensor, X, split_k: int = 0, sched: str = "auto"):
-    """Y = W_hat @ X for a CGQ FP6 tensor (N x K) and X (K x M) -> f32 (N x M).
+    """Y = W_hat @ X for an FP6 tensor (N x K; CGQ, or FGQ with blocks of
+    whole 128-k tiles) and X (K x M) -> f32 (N x M).
 
     `split_k` / `sched` are B200 tuning hooks (default: automatic schedule);
-    the result is the same up to fp32 summation order."""
+    the result is the same up to fp32 summation order (FGQ: the block scale
+    is applied to the binary16 rebuilt weight, gemm.py:96-110 applies it to
+    the fp32 block partial)."""
     if wq.num_blocks != num_blocks(wq.rows, wq.cols, wq.scheme):
         raise PayloadMismatch("block parameter count does not match the scheme")
+    _require_gemm_path(wq.scheme, wq.cols)
     torch_in = _lib.is_torch(X)
     Xa = X if torch_in else np.asarray(X)
     _check_activation(Xa, wq.cols)

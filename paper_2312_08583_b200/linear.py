@@ -38,12 +38,16 @@ def prepack(seg4, seg2, n: int, k: int):
 class Fp6Weight:
     """An N x K FP6 (e3m2) weight resident in HBM in the GEMM's tile layout."""
 
-    def __init__(self, tiles, scales, n: int, k: int, folded=None, static: bool = False):
+    def __init__(self, tiles, scales, n: int, k: int, folded=None, static: bool = False, block: int = 0):
         self.tiles = tiles
-        self.scales = scales          # f16 [N]  (S; the GEMM folds S * 2^12 in-register)
-        self.folded = folded          # f16 [N] or None (bias-shift artifact, API parity)
+        # f16 scales: one per row (CGQ, block 0; the GEMM multiplies the fp32
+        # accumulator by S) or one per (row, block of `block` columns), FGQ,
+        # row-major (the GEMM scales the rebuilt weights per 128-k tile)
+        self.scales = scales
+        self.folded = folded          # f16 or None (bias-shift artifact, API parity)
         self.n = int(n)
         self.k = int(k)
+        self.block = int(block) if block and int(block) < int(k) else 0
         # static: tiles/scales are complete and never rewritten, so the GEMM
         # may be launched with programmatic dependent launch (it prefetches
         # weights before the preceding kernel on the stream has finished).
@@ -51,41 +55,45 @@ class Fp6Weight:
 
     # -- construction -------------------------------------------------------
     @classmethod
-    def from_planes(cls, seg4, seg2, scales, n: int, k: int, folded=None) -> "Fp6Weight":
+    def from_planes(cls, seg4, seg2, scales, n: int, k: int, folded=None, block: int = 0) -> "Fp6Weight":
         tiles = prepack(seg4, seg2, n, k)
         # one-time: the weights are complete before any GEMM can overlap them
         _lib.torch().cuda.current_stream().synchronize()
-        return cls(tiles, scales, n, k, folded, static=True)
+        return cls(tiles, scales, n, k, folded, static=True, block=block)
 
     @classmethod
-    def quantize(cls, W, bias_shift: bool = True) -> "Fp6Weight":
-        """RTN per-row FP6 quantize on the GPU (quantizer.py:189-248) straight
-        into the tile layout (`lpqt_fp6_quantize_tiles`; byte-identical to
-        prepack of the canonical planes)."""
+    def quantize(cls, W, bias_shift: bool = True, block: int = 0) -> "Fp6Weight":
+        """RTN FP6 quantize on the GPU (quantizer.py:189-248) straight into
+        the tile layout (`lpqt_fp6_quantize_tiles_blocks`; byte-identical to
+        prepack of the canonical planes).  block: 0 = one scale per row
+        (CGQ), else FGQ blocks of `block` columns."""
         from .quantizer import _weights_to_device
         w, _ = _weights_to_device(W)
         n, k = (int(v) for v in w.shape)
+        block = int(block) if block and int(block) < k else 0
+        nb = n * (-(-k // block) if block else 1)
         t = _lib.torch()
         dev = w.device
         tiles = t.empty(int(_lib.load().lpqt_fp6_tiles_bytes(n, k)), dtype=t.uint8, device=dev)
-        scales = t.empty(n, dtype=t.float16, device=dev)
-        folded = t.empty(n, dtype=t.float16, device=dev) if bias_shift else None
+        scales = t.empty(nb, dtype=t.float16, device=dev)
+        folded = t.empty(nb, dtype=t.float16, device=dev) if bias_shift else None
         flags = _lib.Flags()
-        _lib.check(_lib.load().lpqt_fp6_quantize_tiles(
-            w.data_ptr(), _lib.dtype_code(w.dtype), n, k, int(w.stride(0)) if n else k, int(bool(bias_shift)),
-            scales.data_ptr(), _lib.ptr(folded), tiles.data_ptr(), flags.ptr, _lib.stream_ptr()), "quantize_tiles")
+        _lib.check(_lib.load().lpqt_fp6_quantize_tiles_blocks(
+            w.data_ptr(), _lib.dtype_code(w.dtype), n, k, int(w.stride(0)) if n else k, block,
+            int(bool(bias_shift)), scales.data_ptr(), _lib.ptr(folded), tiles.data_ptr(), flags.ptr,
+            _lib.stream_ptr()), "quantize_tiles")
         flags.raise_if_set()
-        return cls(tiles, scales, n, k, folded, static=True)
+        return cls(tiles, scales, n, k, folded, static=True, block=block)
 
     @classmethod
     def from_quantized(cls, q) -> "Fp6Weight":
-        from .quantizer import _require_path, device_planes
+        from .quantizer import _require_path, device_planes, scale_block
         _require_path(q.scheme)
         cache = q.device_cache
         if cache is not None and "weight" in cache:
             return cache["weight"]
         s4, s2, sc = device_planes(q)
-        w = cls.from_planes(s4, s2, sc, q.rows, q.cols)
+        w = cls.from_planes(s4, s2, sc, q.rows, q.cols, block=scale_block(q.scheme))
         if cache is not None:
             cache["weight"] = w
         return w
@@ -96,9 +104,9 @@ class Fp6Weight:
         return int(self.tiles.numel() + 2 * self.scales.numel())
 
     def stream_bytes(self) -> int:
-        """Algorithmic weight bytes per GEMM: 0.75 B/weight + 2 B/row (cli.py:75-80)."""
+        """Algorithmic weight bytes per GEMM: 0.75 B/weight + 2 B per scale (cli.py:75-80)."""
         nk = self.n * self.k
-        return seg4_length(nk) + _round_up((2 * nk + 7) // 8, 4) + 2 * self.n
+        return seg4_length(nk) + _round_up((2 * nk + 7) // 8, 4) + 2 * int(self.scales.numel())
 
     def codes(self):
         """Row-major codes [N, K] recovered from the tile layout (test hook)."""
@@ -114,8 +122,9 @@ class Fp6Weight:
         compose[c] * folded (dequant.py:82-86)."""
         t = _lib.torch()
         out = t.empty((self.n, self.k), dtype=t.float16, device=self.tiles.device)
-        _lib.check(_lib.load().lpqt_fp6_tiles_dequant(self.tiles.data_ptr(), self.scales.data_ptr(), self.n, self.k,
-                                                      out.data_ptr(), _lib.stream_ptr()), "tiles_dequant")
+        _lib.check(_lib.load().lpqt_fp6_tiles_dequant_blocks(self.tiles.data_ptr(), self.scales.data_ptr(), self.n,
+                                                             self.k, self.block, out.data_ptr(), _lib.stream_ptr()),
+                   "tiles_dequant")
         return out
 
 
@@ -148,8 +157,11 @@ def _launch(weight: Fp6Weight, xt, ldx: int, m: int, y, y_dtype: int, y_layout: 
     if prefetch is not None:
         # the next launch is assumed to use the same batch and the automatic schedule
         nxt = _lib.NextLinear(prefetch.tiles.data_ptr(), m, prefetch.n, prefetch.k, 0, 0, int(prefetch_bytes))
-    _lib.check(lib.lpqt_w6a16_linear_pf(
-        weight.tiles.data_ptr(), weight.scales.data_ptr(), xt.data_ptr(), ldx, m, weight.n, weight.k,
+    if weight.block and weight.block % TILE:
+        from .errors import InvalidScheme
+        raise InvalidScheme(f"FGQ block_size {weight.block} is not a multiple of 128: outside the B200 GEMM path")
+    _lib.check(lib.lpqt_w6a16_linear_blocks(
+        weight.tiles.data_ptr(), weight.scales.data_ptr(), weight.block, xt.data_ptr(), ldx, m, weight.n, weight.k,
         y.data_ptr(), y_dtype, y_layout, ldy, split_k, _lib.ptr(ws), ws.numel() if ws is not None else 0,
         flags, None if nxt is None else ctypes.byref(nxt), _lib.stream_ptr()), "w6a16_linear")
 

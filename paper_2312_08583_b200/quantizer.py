@@ -5,7 +5,9 @@ weight row) runs as one fused GPU kernel (`lpqt_fp6_quantize_pack`): row
 max|w|, S = RN_f16(peak/28), fold S*2^12, RTN codes of W/S and the canonical
 4+2 planes, bit-exact with the reference for f64/f32/f16/bf16 input.
 `dequantize_tensor` is the GPU `lpqt_fp6_dequantize_tensor` (f64 exact).
-FGQ, FP5 and INT4 schemes are outside this path and raise InvalidScheme.
+FP6 quantizes under CGQ (one scale per output row) or FGQ (one per block of
+block_size columns; the GEMM needs blocks of whole 128-k tiles); FP5 and
+INT4 are outside this path and raise InvalidScheme.
 """
 
 from __future__ import annotations
@@ -92,11 +94,25 @@ def _validate_scheme(scheme: QuantScheme) -> None:
 
 
 def _require_path(scheme: QuantScheme) -> None:
+    """CGQ or FGQ x FP6_E3M2 (the formats this library runs on the GPU)."""
     _validate_scheme(scheme)
-    if scheme.fmt is not TensorFormat.FP6_E3M2 or scheme.granularity is not Granularity.CGQ:
+    if scheme.fmt is not TensorFormat.FP6_E3M2:
         raise InvalidScheme(
-            f"{scheme.granularity.name} x {scheme.fmt.name} is outside the B200 path "
-            "(per-output-channel CGQ x FP6_E3M2 only)")
+            f"{scheme.granularity.name} x {scheme.fmt.name} is outside the B200 path (FP6_E3M2, CGQ or FGQ)")
+
+
+def scale_block(scheme: QuantScheme) -> int:
+    """Columns per scale for the kernels: 0 = one scale per row (CGQ)."""
+    return scheme.block_size if scheme.granularity is Granularity.FGQ else 0
+
+
+def _require_gemm_path(scheme: QuantScheme, cols: int) -> None:
+    """The GEMM applies FGQ scales per 128-k weight tile: blocks must be
+    whole tiles (or span the row)."""
+    _require_path(scheme)
+    b = scale_block(scheme)
+    if b and b < cols and b % 128:
+        raise InvalidScheme(f"FGQ block_size {b} is not a multiple of 128: outside the B200 GEMM path")
 
 
 def blocks_per_row(cols: int, scheme: QuantScheme) -> int:
@@ -156,14 +172,16 @@ def _weights_to_device(W):
     return _lib.to_device(a), False
 
 
-def quantize_device(w, bias_shift: bool = True):
+def quantize_device(w, bias_shift: bool = True, block: int = 0):
     """GPU quantize of a 2-D CUDA tensor -> dict of CUDA tensors
-    {scales, folded, seg4, seg2} (canonical planes, flat index r*K + k)."""
+    {scales, folded, seg4, seg2} (canonical planes, flat index r*K + k;
+    scales one per row, or per block of `block` columns row-major)."""
     t = _lib.torch()
     n, k = (int(v) for v in w.shape)
     dev = w.device
-    scales = t.empty(n, dtype=t.float16, device=dev)
-    folded = t.empty(n, dtype=t.float16, device=dev) if bias_shift else None
+    nb = n * (-(-k // block) if block and block < k else 1)
+    scales = t.empty(nb, dtype=t.float16, device=dev)
+    folded = t.empty(nb, dtype=t.float16, device=dev) if bias_shift else None
     nk = n * k
     seg4 = t.empty(seg4_length(nk), dtype=t.uint8, device=dev)
     seg2 = t.empty(tail_length(FP6_E3M2, nk), dtype=t.uint8, device=dev)
@@ -171,10 +189,9 @@ def quantize_device(w, bias_shift: bool = True):
         seg4[-4:].zero_()
         seg2[-4:].zero_()
     flags = _lib.Flags()
-    _lib.check(_lib.load().lpqt_fp6_quantize_pack(
-        w.data_ptr(), _lib.dtype_code(w.dtype), n, k, k, int(bool(bias_shift)), scales.data_ptr(),
-        _lib.ptr(folded), seg4.data_ptr(), seg2.data_ptr(), None, flags.ptr, _lib.stream_ptr()),
-        "quantize_tensor")
+    _lib.check(_lib.load().lpqt_fp6_quantize_pack_blocks(
+        w.data_ptr(), _lib.dtype_code(w.dtype), n, k, k, int(block), int(bool(bias_shift)), scales.data_ptr(),
+        _lib.ptr(folded), seg4.data_ptr(), seg2.data_ptr(), flags.ptr, _lib.stream_ptr()), "quantize_tensor")
     flags.raise_if_set()
     return {"scales": scales, "folded": folded, "seg4": seg4, "seg2": seg2}
 
@@ -204,7 +221,7 @@ def quantize_tensor(W, scheme: QuantScheme, bias_shift: bool = False) -> Quantiz
         e8 = np.zeros(0, dtype=np.uint8)
         return QuantizedTensor(n, k, scheme, e16, None, PackedSegments(e8, e8.copy(), 0), bias_shift,
                                e16.copy() if bias_shift else None)
-    d = quantize_device(w, bias_shift)
+    d = quantize_device(w, bias_shift, scale_block(scheme))
     cache = {"scales": d["scales"], "seg4": d["seg4"], "seg2": d["seg2"]}
     if torch_in:
         return QuantizedTensor(n, k, scheme, d["scales"], None, PackedSegments(d["seg4"], d["seg2"], n * k),
@@ -270,9 +287,9 @@ def dequantize_tensor(q: QuantizedTensor, path: str = "naive"):
     else:
         raise ValueError(f"unknown dequantization path {path!r}")
     out = t.empty((q.rows, q.cols), dtype=t.float64, device=s4.device)
-    _lib.check(_lib.load().lpqt_fp6_dequantize_tensor(
-        s4.data_ptr(), s2.data_ptr(), row_scale.data_ptr(), p, q.rows, q.cols, out.data_ptr(), _lib.F64,
-        _lib.stream_ptr()), "dequantize_tensor")
+    _lib.check(_lib.load().lpqt_fp6_dequantize_tensor_blocks(
+        s4.data_ptr(), s2.data_ptr(), row_scale.data_ptr(), p, q.rows, q.cols, scale_block(q.scheme), out.data_ptr(),
+        _lib.F64, _lib.stream_ptr()), "dequantize_tensor")
     return out if torch_in else out.cpu().numpy()
 
 

@@ -9,6 +9,7 @@ gemm_tolerance = 4 eps32 K max|W_hat| max|X|, gemm.py:118-122).
 """
 
 import hashlib
+import os
 
 import numpy as np
 import pytest
@@ -507,3 +508,60 @@ def test_split_k_workspace_shared_across_shapes_is_exact():
         for i in (range(len(shapes)) if r % 2 else reversed(range(len(shapes)))):
             y = L.w6a16_linear(xs[i], ws[i], out_dtype=torch.float32, prefetch=ws[(i + 1) % len(ws)])
             assert torch.equal(y, want[i]), (r, shapes[i])
+
+
+# ---------------------------------------------------------------- FGQ x FP6
+FGQ_GOLD = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "golden_fgq.npz")
+
+
+def test_fgq_quantize_dequantize_vs_reference():
+    """FGQ quantize on the GPU == the reference's bytes for every block size
+    (16, 7, 64, 128, 256, ragged last blocks, an all-zero block)."""
+    g = np.load(FGQ_GOLD)
+    for name in [str(s) for s in g["f_names"]]:
+        W, b = g[f"f/{name}/W"], int(g[f"f/{name}/block"])
+        q = L.quantize_tensor(W, L.QuantScheme(L.Granularity.FGQ, L.TensorFormat.FP6_E3M2, b), bias_shift=True)
+        assert np.array_equal(q.scales.view(np.uint16), g[f"f/{name}/scales"]), name
+        assert np.array_equal(q.folded_scales.view(np.uint16), g[f"f/{name}/folded"]), name
+        assert np.array_equal(q.payload.seg4, g[f"f/{name}/seg4"]), name
+        assert np.array_equal(q.payload.seg_tail, g[f"f/{name}/seg2"]), name
+        for path in ("naive", "bias_shift"):
+            assert np.array_equal(L.dequantize_tensor(q, path), g[f"f/{name}/deq"]), (name, path)
+        if b % 128 == 0 or b >= W.shape[1]:
+            Y = L.gemm_quantized(q, g[f"f/{name}/X"])
+            assert normwise_rel(Y, g[f"f/{name}/Y"]) <= REL_TOL, name
+
+
+@pytest.mark.parametrize("dt", ["f16", "bf16", "f32"])
+@pytest.mark.parametrize("n,k,block", [(300, 1000, 128), (256, 4096, 256), (130, 640, 384), (129, 777, 40)])
+def test_fgq_quantize_tiles_equals_prepacked_planes(dt, n, k, block):
+    gen = torch.Generator().manual_seed(n + k + block)
+    Wt = (torch.randn((n, k), generator=gen, dtype=torch.float64) * 0.05).to(_TORCH_DT[dt]).cuda()
+    scheme = L.QuantScheme(L.Granularity.FGQ, L.TensorFormat.FP6_E3M2, block)
+    q = L.quantize_tensor(Wt, scheme, bias_shift=True)
+    fused = L.Fp6Weight.quantize(Wt, block=block)
+    ref = L.Fp6Weight.from_planes(q.payload.seg4, q.payload.seg_tail, q.scales, n, k, q.folded_scales, block=block)
+    assert torch.equal(fused.tiles, ref.tiles)
+    assert torch.equal(fused.scales.view(torch.int16), q.scales.view(torch.int16))
+    o = O.quantize_tensor_fgq(Wt.double().cpu().numpy(), block, bias_shift=True)
+    assert np.array_equal(q.scales.cpu().numpy().view(np.uint16), o["scales"].view(np.uint16))
+    assert np.array_equal(q.payload.seg4.cpu().numpy(), o["seg4"])
+
+
+@pytest.mark.parametrize("m", [1, 16, 33, 300])
+@pytest.mark.parametrize("n,k,block", [(512, 1024, 128), (1000, 4096, 512), (384, 1000, 256), (4096, 4096, 128)])
+def test_fgq_gemm_vs_oracle(n, k, block, m):
+    """Block scales applied to the rebuilt binary16 weights before the MMA:
+    within the fp32 tolerance of the reference's block-partial GEMM
+    (gemm.py:96-110) on the same fp16 activations, for every batch-tile
+    width (BN 16 / 32 / 64 / 192) and ragged last blocks."""
+    gen = torch.Generator(device="cuda").manual_seed(n * 7 + k + m)
+    W = (torch.randn(n, k, generator=gen, device="cuda") * 0.02).half()
+    w = L.Fp6Weight.quantize(W, block=block)
+    x = torch.randn(m, k, generator=gen, device="cuda").half()
+    y = L.w6a16_linear(x, w, out_dtype=torch.float32)
+    codes = w.codes().cpu().numpy()
+    Yo = O.gemm_quantized_fgq(codes.ravel(), w.scales.cpu().numpy(), n, k, block, x.t().float().cpu().numpy())
+    assert normwise_rel(y.t().cpu().numpy(), Yo) <= REL_TOL
+    y2 = L.w6a16_linear(x, w, out_dtype=torch.float32, sched="streamk", split_k=3)
+    assert normwise_rel(y2.cpu().numpy(), y.cpu().numpy()) <= 1e-5
