@@ -102,7 +102,7 @@ struct GemmArgs {
 // multiply each rebuilt f16 weight by its block's scale before the MMA (the
 // binary16 dequant of dequant.py:72-79), the epilogue applies none.
 struct FgqArgs {
-  int bpr, bkt;
+  int bpr, bkt, bkt_shift;  // bkt_shift >= 0: bkt == 1 << bkt_shift
 };
 __device__ __forceinline__ void scale_f16x2(uint32_t (&r)[32], uint32_t s2) {
 #pragma unroll
@@ -733,7 +733,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         tile_nm(a, it.sg.tile, n_tile, m_tile);
         const int n = n_tile * kTileN + row;
         const int kt = it.kt() + (KS == 2 ? tl : 0);
-        const uint16_t sb = n < a.N ? __ldg(a.scales + (int64_t)n * fg.bpr + kt / fg.bkt) : static_cast<uint16_t>(0);
+        const int blk = fg.bkt_shift >= 0 ? (kt >> fg.bkt_shift) : kt / fg.bkt;
+        const uint16_t sb = n < a.N ? __ldg(a.scales + (int64_t)n * fg.bpr + blk) : static_cast<uint16_t>(0);
         fs2 = static_cast<uint32_t>(sb) * 0x10001u;
       }
       mbar_wait_u32<WM>(fw0 + 8 * wc.idx, wc.ph);
@@ -1822,6 +1823,7 @@ int lpqt_w6a16_linear_blocks(const uint8_t* tiles, const uint16_t* scales, int64
   if (fgq) {
     fga.bpr = static_cast<int>((K + block - 1) / block);
     fga.bkt = static_cast<int>(block / kTileK);
+    fga.bkt_shift = (fga.bkt & (fga.bkt - 1)) == 0 ? __builtin_ctz(static_cast<unsigned>(fga.bkt)) : -1;
   }
   if ((flags & LPQT_SCHED_STREAMK) && (flags & LPQT_SCHED_CLUSTER)) return LPQT_E_INVALID_INPUT;
   if (M < 0 || N < 0 || K < 0) return LPQT_E_SHAPE;
