@@ -150,11 +150,7 @@ struct Cfg {
   // single-lane issue sequence takes several times that, so two warps issue
   // alternate stages, each into its own accumulator; the epilogue sums them
   // in a fixed order.  Prefill MMAs (N >= 128) are long enough for one.
-#ifdef LPQT_MMA1
-  static constexpr int kMmaWarps = 1;
-#else
   static constexpr int kMmaWarps = BN <= 64 ? 2 : 1;
-#endif
   static constexpr int kNAcc = kMmaWarps;
   static constexpr int kDCols = BN * kNAcc;
   static constexpr int kACols = kTmemCols - kDBufs * kDCols;
@@ -760,16 +756,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       // half the ALU work overlaps the MMAs still reading the slot
       const bool act = KS == 1 || tl < nt_cur;
       uint32_t r[32];
-#ifndef LPQT_EXP_NO_REBUILD
       if (act) {
         fp6x32_cvt_f16x32_fma(q[0], r, sm);
         fp6x32_cvt_f16x32_fma(q[0] + 6, r + 16, sm);
         if constexpr (FGQ) scale_f16x2(r, fs2);
       }
-#else
-#pragma unroll
-      for (int j = 0; j < 32; ++j) r[j] = q[0][j % 12];
-#endif
       mbar_wait_u32<WM>(ae0 + 8 * ac.idx, ac.ph ^ 1u);
       tc_fence_after();
       if (act) {
@@ -777,14 +768,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         tmem_st_x32(ta, r);
 #pragma unroll
         for (int h = 1; h < kSegs; ++h) {
-#ifndef LPQT_EXP_NO_REBUILD
           fp6x32_cvt_f16x32_fma(q[h], r, sm);
           fp6x32_cvt_f16x32_fma(q[h] + 6, r + 16, sm);
           if constexpr (FGQ) scale_f16x2(r, fs2);
-#else
-#pragma unroll
-          for (int j = 0; j < 32; ++j) r[j] = q[h][j % 12];
-#endif
           tmem_st_x32(ta + h * 32, r);
         }
       }
@@ -852,13 +838,8 @@ __global__ void __launch_bounds__(kThreads, 1)
               for (int j = 0; j < kTileK / 16; ++j) {
                 const uint32_t off = (t * C::kXTileBytes + (j >> 2) * (BN * 128) + (j & 3) * 32) >> 4;
                 const bool init = first && t == 0 && j == 0;
-#ifndef LPQT_EXP_NO_MMA
                 mma_f16_ts_if(e, d_tmem, ta + t * kAColsPerBuf + j * 8, bd_lo + off, bd_hi, idesc,
                               init ? 0u : 1u);
-#else
-                (void)off;
-                (void)init;
-#endif
               }
             }
           }
