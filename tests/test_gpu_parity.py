@@ -500,8 +500,10 @@ def test_split_k_workspace_shared_across_shapes_is_exact():
     shape's launch must never be seen)."""
     g = torch.Generator(device="cuda").manual_seed(31)
     shapes = [(4096, 11008, 1), (640, 256, 1), (4096, 11008, 16), (1024, 8192, 3), (8192, 8192, 128),
-              (4096, 4096, 300)]
-    ws = [L.Fp6Weight.quantize((torch.randn(n, k, device="cuda", generator=g) * 0.02).half()) for n, k, _ in shapes]
+              (4096, 4096, 300), (2048, 4096, 40), (1024, 8192, 24), (4096, 11008, 64)]
+    blocks = [0, 0, 0, 128, 0, 256, 0, 128, 0]     # FGQ launches interleaved with CGQ ones
+    ws = [L.Fp6Weight.quantize((torch.randn(n, k, device="cuda", generator=g) * 0.02).half(), block=b)
+          for (n, k, _), b in zip(shapes, blocks)]
     xs = [torch.randn(m, k, device="cuda", generator=g).half() for _, k, m in shapes]
     want = [L.w6a16_linear(x, w, out_dtype=torch.float32) for x, w in zip(xs, ws)]
     for r in range(30):

@@ -98,6 +98,9 @@ int main() {
     run<64, 0, 2>(ctas);
     run<64, 1, 2>(ctas);
     run<128, 0, 1>(ctas);
+    run<128, 1, 1>(ctas);
+    run<192, 0, 1>(ctas);
+    run<192, 1, 1>(ctas);
     run<256, 0, 1>(ctas);
     run<256, 1, 1>(ctas);
   }
