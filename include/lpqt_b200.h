@@ -239,6 +239,36 @@ int lpqt_w6a16_linear_blocks(const uint8_t* tiles, const uint16_t* scales,
                              int64_t workspace_bytes, int flags,
                              const lpqt_next_linear* next, void* stream);
 
+/* ---- FP5 e3m1 (codec.py FP5_E3M1, packing.py 4 + 1 split) ----------------
+ * Same contracts as the FP6 entries with seg4 = c >> 1 (align4(ceil(n/2)) B)
+ * and a one-bit tail (lpqt_fp5_tail_length(n) = align4(ceil(n/8)) B, little-
+ * endian bit order).  Scales are peak / 24 (max_value).  FP5 weights run the
+ * GEMM through the FP6 tile layout (lpqt_fp5_prepack: every e3m1 value is an
+ * e3m2 value), i.e. at FP6's 0.75 B per weight. */
+int64_t lpqt_fp5_tail_length(int64_t n);
+int lpqt_fp5_encode_rtn(const void* x, int dtype, int64_t n, uint8_t* codes,
+                        uint32_t* dev_flags, void* stream);
+int lpqt_fp5_pack(const uint8_t* codes, int64_t n, uint8_t* seg4,
+                  uint8_t* seg1, uint32_t* dev_flags, void* stream);
+int lpqt_fp5_unpack(const uint8_t* seg4, const uint8_t* seg1, int64_t n,
+                    uint8_t* codes, void* stream);
+int lpqt_fp5_quantize_pack_blocks(const void* W, int dtype, int64_t N,
+                                  int64_t K, int64_t ldw, int64_t block,
+                                  int bias_shift, uint16_t* scales,
+                                  uint16_t* folded, uint8_t* seg4,
+                                  uint8_t* seg1, uint32_t* dev_flags,
+                                  void* stream);
+int lpqt_fp5_dequantize_tensor_blocks(const uint8_t* seg4, const uint8_t* seg1,
+                                      const uint16_t* block_scale, int path,
+                                      int64_t N, int64_t K, int64_t block,
+                                      void* out, int out_dtype, void* stream);
+int lpqt_fp5_dequant_bias_shift(const uint8_t* codes, const uint16_t* folded,
+                                int64_t n, uint16_t* out, void* stream);
+int lpqt_fp5_dequant_naive(const uint8_t* codes, const uint16_t* scales,
+                           int64_t n, uint16_t* out, void* stream);
+int lpqt_fp5_prepack(const uint8_t* seg4, const uint8_t* seg1, int64_t N,
+                     int64_t K, uint8_t* tiles, void* stream);
+
 /* Number of kernel launches performed by this library since load (for the
  * bench's gpu_launches claim). */
 int64_t lpqt_launch_count(void);

@@ -80,6 +80,15 @@ SIGNATURES = {
     "lpqt_fp6_tiles_dequant_blocks": (_I32, [_P, _P, _I64, _I64, _I64, _P, _P]),
     "lpqt_w6a16_linear_blocks": (_I32, [_P, _P, _I64, _P, _I64, _I64, _I64, _I64, _P, _I32, _I32, _I64, _I32, _P,
                                         _I64, _I32, ctypes.POINTER(NextLinear), _P]),
+    "lpqt_fp5_tail_length": (_I64, [_I64]),
+    "lpqt_fp5_encode_rtn": (_I32, [_P, _I32, _I64, _P, _P, _P]),
+    "lpqt_fp5_pack": (_I32, [_P, _I64, _P, _P, _P, _P]),
+    "lpqt_fp5_unpack": (_I32, [_P, _P, _I64, _P, _P]),
+    "lpqt_fp5_quantize_pack_blocks": (_I32, [_P, _I32, _I64, _I64, _I64, _I64, _I32, _P, _P, _P, _P, _P, _P]),
+    "lpqt_fp5_dequantize_tensor_blocks": (_I32, [_P, _P, _P, _I32, _I64, _I64, _I64, _P, _I32, _P]),
+    "lpqt_fp5_dequant_bias_shift": (_I32, [_P, _P, _I64, _P, _P]),
+    "lpqt_fp5_dequant_naive": (_I32, [_P, _P, _I64, _P, _P]),
+    "lpqt_fp5_prepack": (_I32, [_P, _P, _I64, _I64, _P, _P]),
     "lpqt_launch_count": (_I64, []),
 }
 

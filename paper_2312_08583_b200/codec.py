@@ -46,14 +46,22 @@ class MiniFloatFormat:
 
 
 FP6_E3M2 = MiniFloatFormat("FP6_E3M2", 3, 2, 3, 6, 28.0)
-# Declared for API compatibility; FP5 is outside the B200 path.
 FP5_E3M1 = MiniFloatFormat("FP5_E3M1", 3, 1, 3, 5, 24.0)
 MINIFLOAT_FORMATS = (FP6_E3M2, FP5_E3M1)
 
 
+def kernel_prefix(fmt: MiniFloatFormat) -> str:
+    """C-ABI family of a format: lpqt_fp6_* (4 + 2) or lpqt_fp5_* (4 + 1)."""
+    if fmt == FP6_E3M2:
+        return "lpqt_fp6"
+    if fmt == FP5_E3M1:
+        return "lpqt_fp5"
+    raise InvalidScheme(f"{fmt.name} is not a format of this library (FP6_E3M2, FP5_E3M1)")
+
+
 def require_fp6(fmt: MiniFloatFormat) -> None:
     if fmt != FP6_E3M2:
-        raise InvalidScheme(f"{fmt.name} is outside the B200 FP6 path (only FP6_E3M2 is accelerated)")
+        raise InvalidScheme(f"{fmt.name} is outside this operation (FP6_E3M2 only)")
 
 
 def decode(fmt: MiniFloatFormat, code: int) -> float:
@@ -94,12 +102,13 @@ def codebook(fmt: MiniFloatFormat) -> list[tuple[int, float]]:
 def encode_rtn_array(fmt: MiniFloatFormat, x):
     """Round-to-nearest encode on the GPU (codec.py:116-132).
 
-    Ties go to the even magnitude index, values beyond +-28 saturate, -0.0
+    Ties go to the even magnitude index, values beyond the format's max_value
+    (28 FP6, 24 FP5) saturate, -0.0
     encodes to code 0.  numpy / array-like in -> numpy uint8 out; a torch
     tensor in -> a uint8 tensor on the GPU.  Non-finite input raises
     InvalidInput.
     """
-    require_fp6(fmt)
+    prefix = kernel_prefix(fmt)
     t = _lib.torch()
     torch_in = _lib.is_torch(x)
     if torch_in:
@@ -118,7 +127,7 @@ def encode_rtn_array(fmt: MiniFloatFormat, x):
     codes = t.empty(n, dtype=t.uint8, device=src.device)
     if n:
         flags = _lib.Flags()
-        _lib.check(_lib.load().lpqt_fp6_encode_rtn(
+        _lib.check(getattr(_lib.load(), prefix + "_encode_rtn")(
             src.data_ptr(), _lib.dtype_code(src.dtype), n, codes.data_ptr(), flags.ptr, _lib.stream_ptr()),
             "encode_rtn_array")
         if flags.value():

@@ -230,4 +230,5 @@ def load_lpqt(data: bytes):
     tail = blob[off["tail"]:off["tail"] + tail_length(hdr["scheme"].fmt.minifloat, rows * cols)]
     # scales / folded are kept as views into the device copy of the stream;
     # the planes are only read by the prepack
-    return Fp6Weight.from_planes(seg4, tail, scales, rows, cols, folded, block=scale_block(hdr["scheme"]))
+    fmt = "fp5" if hdr["scheme"].fmt.minifloat.mantissa_bits == 1 else "fp6"
+    return Fp6Weight.from_planes(seg4, tail, scales, rows, cols, folded, block=scale_block(hdr["scheme"]), fmt=fmt)

@@ -88,6 +88,32 @@ __global__ void tiles_dequant_kernel(const uint8_t* __restrict__ tiles, const ui
   }
 }
 
+
+// FP5 e3m1 planes (seg4 = c >> 1, one tail bit per code) -> the FP6 tile
+// layout: e3m1 code (s, e, m) is the e3m2 code (s, e, m << 1) of the same value
+__global__ void prepack_fp5_kernel(const uint8_t* __restrict__ seg4, const uint8_t* __restrict__ seg1, int64_t N,
+                                   int64_t K, int64_t Np, int64_t Kp, uint8_t* __restrict__ tiles) {
+  const int64_t groups = Kp / 32, total = Np * groups, k_tiles = Kp / kTileK;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t n = t / groups, g = t % groups;
+    uint8_t c[32];
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+      const int64_t k = g * 32 + j, i = n * K + k;
+      uint32_t c6 = 0;
+      if (n < N && k < K) {
+        const uint32_t c5 = (((seg4[i >> 1] >> (4 * (i & 1))) & 15u) << 1) | ((seg1[i >> 3] >> (i & 7)) & 1u);
+        c6 = ((c5 & 0x10u) << 1) | (((c5 >> 1) & 7u) << 2) | ((c5 & 1u) << 1);
+      }
+      c[j] = static_cast<uint8_t>(c6);
+    }
+    uint32_t w[6];
+    fp6x32_pack_words(c, w);
+#pragma unroll
+    for (int i = 0; i < 6; ++i) *reinterpret_cast<uint32_t*>(tiles + tile_word_addr(n, g, i, k_tiles)) = w[i];
+  }
+}
+
 }  // namespace lpqt
 
 using namespace lpqt;
@@ -134,6 +160,16 @@ int lpqt_fp6_tiles_dequant_blocks(const uint8_t* tiles, const uint16_t* scales, 
 int lpqt_fp6_tiles_dequant(const uint8_t* tiles, const uint16_t* scales, int64_t N, int64_t K, uint16_t* out,
                            void* stream) {
   return lpqt_fp6_tiles_dequant_blocks(tiles, scales, N, K, 0, out, stream);
+}
+
+
+int lpqt_fp5_prepack(const uint8_t* seg4, const uint8_t* seg1, int64_t N, int64_t K, uint8_t* tiles, void* stream) {
+  if (N < 0 || K < 0) return LPQT_E_SHAPE;
+  if (N == 0 || K == 0) return LPQT_OK;
+  const int64_t Np = round_up(N, kTileN), Kp = round_up(K, kTileK);
+  prepack_fp5_kernel<<<grid_for(Np * (Kp / 32), 256), 256, 0, as_stream(stream)>>>(seg4, seg1, N, K, Np, Kp, tiles);
+  note_launch();
+  return check_launch();
 }
 
 }  // extern "C"

@@ -181,7 +181,8 @@ __device__ __forceinline__ uint32_t encode1(typename InTraits<DT>::Acc v, float 
 template <int DT>
 __global__ void __launch_bounds__(256) block_scales_kernel(const void* __restrict__ W, int64_t N, int64_t K,
                                                            int64_t ldw, int64_t B, int64_t bpr, int vec,
-                                                           int bias_shift, uint16_t* __restrict__ scales,
+                                                           double maxv, int bias_shift,
+                                                           uint16_t* __restrict__ scales,
                                                            uint16_t* __restrict__ folded,
                                                            uint32_t* __restrict__ flags) {
   using Acc = typename InTraits<DT>::Acc;
@@ -214,7 +215,7 @@ __global__ void __launch_bounds__(256) block_scales_kernel(const void* __restric
     for (int o = 16; o > 0; o >>= 1) peak = fmax(peak, __shfl_xor_sync(0xffffffffu, peak, o));
     if (lane == 0) {
       const double p = static_cast<double>(peak);
-      const double raw = (p == 0.0) ? 1.0 : p / 28.0;
+      const double raw = (p == 0.0) ? 1.0 : p / maxv;  // max_value: 28 (FP6), 24 (FP5)
       uint16_t sb = __half_as_ushort(__double2half(raw));
       if ((sb & 0x7FFFu) == 0x7C00u) f |= LPQT_F_SCALE_INF;
       if ((sb & 0x7FFFu) == 0) sb = 0x0001u;  // underflow clamps to 2^-24
@@ -482,6 +483,160 @@ __global__ void stage_activations_kernel(const void* __restrict__ X, int64_t K, 
   }
 }
 
+
+// ---------------------------------------------------------------------------
+// FP5 e3m1 (codec.py FP5_E3M1: 3 exponent bits, 1 mantissa bit, bias 3, max
+// 24) with the 4 + 1 split (packing.py:84-85, :112-113): seg4 holds c >> 1
+// like FP6, the tail one mantissa bit per code (little-endian bit order).
+// Codes are the literal f64 search (midpoints of the 16-value grid, ties to
+// the even index, sign from the input).  The GEMM runs FP5 weights through
+// the FP6 tile layout: every e3m1 value is the e3m2 value with mantissa m<<1.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ double fp5_magnitude(int i) {
+  const int e = i >> 1, m = i & 1;
+  return e == 0 ? 0.125 * m : (1.0 + 0.5 * m) * ldexp(1.0, e - 3);
+}
+__device__ __forceinline__ void load_mids_fp5(double* smem_mids) {
+  for (int i = threadIdx.x; i < 16; i += blockDim.x)
+    smem_mids[i] = i < 15 ? 0.5 * (fp5_magnitude(i) + fp5_magnitude(i + 1)) : 1e300;
+  __syncthreads();
+}
+__device__ __forceinline__ uint32_t fp5_encode(double x, const double* __restrict__ mids) {
+  const double a = fabs(x);
+  int idx = 0;
+#pragma unroll
+  for (int step = 8; step >= 1; step >>= 1) {
+    if (idx + step <= 15 && mids[idx + step - 1] <= a) idx += step;
+  }
+  if (idx > 0 && (idx & 1) && a == mids[idx - 1]) idx -= 1;
+  return (x < 0.0 ? 0x10u : 0u) | static_cast<uint32_t>(idx);
+}
+__device__ __forceinline__ uint32_t fp5_code(const uint8_t* __restrict__ seg4, const uint8_t* __restrict__ seg1,
+                                             int64_t i) {
+  const uint32_t hi = (seg4[i >> 1] >> (4 * (i & 1))) & 15u;
+  const uint32_t lo = (seg1[i >> 3] >> (i & 7)) & 1u;
+  return (hi << 1) | lo;
+}
+// binary16 bits of the bias-shift compose (dequant.py:33-43 with mantissa_bits 1)
+__device__ __forceinline__ uint16_t fp5_compose_bits(uint32_t c) {
+  return static_cast<uint16_t>(((c & 0x10u) << 11) | (((c >> 1) & 7u) << 10) | ((c & 1u) << 9));
+}
+
+template <int DT>
+__global__ void fp5_encode_kernel(const void* __restrict__ x, int64_t n, uint8_t* __restrict__ codes,
+                                  uint32_t* __restrict__ flags) {
+  __shared__ double mids[16];
+  load_mids_fp5(mids);
+  bool bad = false;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const double v = load_as_double<DT>(x, i);
+    if (!isfinite(v)) {
+      bad = true;
+      codes[i] = 0;
+      continue;
+    }
+    codes[i] = static_cast<uint8_t>(fp5_encode(v, mids));
+  }
+  if (bad) atomicOr(flags, LPQT_F_NONFINITE);
+}
+
+// thread per 8 codes: 4 bytes of seg4, 1 byte of the tail
+__device__ __forceinline__ void fp5_put8(const uint32_t (&c)[8], int64_t g, int64_t len4, int64_t len1,
+                                         uint8_t* __restrict__ seg4, uint8_t* __restrict__ seg1) {
+  uint32_t s4 = 0, s1 = 0;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    s4 |= ((c[j] >> 1) & 15u) << (4 * j);
+    s1 |= (c[j] & 1u) << j;
+  }
+#pragma unroll
+  for (int b = 0; b < 4; ++b)
+    if (4 * g + b < len4) seg4[4 * g + b] = static_cast<uint8_t>(s4 >> (8 * b));
+  if (g < len1) seg1[g] = static_cast<uint8_t>(s1);
+}
+
+__global__ void fp5_pack_kernel(const uint8_t* __restrict__ codes, int64_t n, int64_t len4, int64_t len1,
+                                uint8_t* __restrict__ seg4, uint8_t* __restrict__ seg1, uint32_t* __restrict__ flags) {
+  bool bad = false;
+  const int64_t groups = (len4 * 2 + 7) / 8 > len1 ? (len4 * 2 + 7) / 8 : len1;
+  for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < groups; g += (int64_t)gridDim.x * blockDim.x) {
+    uint32_t c[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int64_t i = 8 * g + j;
+      c[j] = i < n ? codes[i] : 0u;
+      if (c[j] > 31u) bad = true;
+    }
+    fp5_put8(c, g, len4, len1, seg4, seg1);
+  }
+  if (bad) atomicOr(flags, LPQT_F_BAD_CODE);
+}
+
+__global__ void fp5_unpack_kernel(const uint8_t* __restrict__ seg4, const uint8_t* __restrict__ seg1, int64_t n,
+                                  uint8_t* __restrict__ codes) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    codes[i] = static_cast<uint8_t>(fp5_code(seg4, seg1, i));
+}
+
+// quantize_tensor minifloat branch for FP5 (quantizer.py:224-231): codes of
+// W / S (f64 quotient, literal search) packed 4 + 1; thread per 8 flat codes
+template <int DT>
+__global__ void fp5_encode_planes_kernel(const void* __restrict__ W, int64_t N, int64_t K, int64_t ldw, int64_t B,
+                                         int64_t bpr, const uint16_t* __restrict__ scales, int64_t len4, int64_t len1,
+                                         uint8_t* __restrict__ seg4, uint8_t* __restrict__ seg1) {
+  __shared__ double mids[16];
+  load_mids_fp5(mids);
+  const int64_t total = N * K, groups = (total + 7) / 8;
+  for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < groups; g += (int64_t)gridDim.x * blockDim.x) {
+    int64_t r = (8 * g) / K, k = 8 * g - r * K;
+    uint32_t c[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      c[j] = 0;
+      if (8 * g + j < total) {
+        const double v = load_as_double<DT>(W, r * ldw + k);
+        const double S = static_cast<double>(__half2float(__ushort_as_half(scales[r * bpr + k / B])));
+        c[j] = fp5_encode(v / S, mids);
+      }
+      if (++k == K) k = 0, ++r;
+    }
+    fp5_put8(c, g, len4, len1, seg4, seg1);
+  }
+}
+
+// dequantize_tensor (quantizer.py:269-299) for FP5 planes, per-block scales
+template <int OUT>
+__global__ void fp5_dequantize_tensor_kernel(const uint8_t* __restrict__ seg4, const uint8_t* __restrict__ seg1,
+                                             const uint16_t* __restrict__ bscale, int path, int64_t N, int64_t K,
+                                             int64_t B, int64_t bpr, void* __restrict__ out) {
+  const int64_t total = N * K;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t c = fp5_code(seg4, seg1, i);
+    const int64_t r = i / K, k = i - r * K;
+    const __half comp = __ushort_as_half(fp5_compose_bits(c));
+    const __half s = __ushort_as_half(bscale[r * bpr + k / B]);
+    if (OUT == LPQT_F64) {
+      double v = static_cast<double>(__half2float(comp));
+      if (path == 0) v *= 4096.0;
+      static_cast<double*>(out)[i] = v * static_cast<double>(__half2float(s));
+    } else {
+      __half v = comp;
+      if (path == 0) v = __float2half_rn(__half2float(comp) * 4096.0f);
+      static_cast<uint16_t*>(out)[i] = __half_as_ushort(__hmul(v, s));
+    }
+  }
+}
+
+// elementwise binary16 dequant of FP5 codes (dequant.py:72-86)
+__global__ void fp5_dequant_kernel(const uint8_t* __restrict__ codes, const uint16_t* __restrict__ scale, int path,
+                                   int64_t n, uint16_t* __restrict__ out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const __half comp = __ushort_as_half(fp5_compose_bits(codes[i]));
+    const __half v = path == 1 ? comp : __float2half_rn(__half2float(comp) * 4096.0f);
+    out[i] = __half_as_ushort(__hmul(v, __ushort_as_half(scale[i])));
+  }
+}
+
 }  // namespace lpqt
 
 using namespace lpqt;
@@ -553,11 +708,11 @@ int lpqt_fp6_dequant_naive(const uint8_t* codes, const uint16_t* scales, int64_t
 
 static int quantize_scales(const void* W, int dtype, int64_t N, int64_t K, int64_t ldw, int64_t B, int64_t bpr,
                            int vec, int bias_shift, uint16_t* scales, uint16_t* folded, uint32_t* dev_flags,
-                           cudaStream_t st) {
+                           cudaStream_t st, double maxv = 28.0) {
   const int64_t units = N * bpr;
   const int g = static_cast<int>((units + 7) / 8 < 148 * 8 ? (units + 7) / 8 : 148 * 8);
-  LPQT_DISPATCH_DT(dtype, block_scales_kernel<DT><<<g, 256, 0, st>>>(W, N, K, ldw, B, bpr, vec, bias_shift, scales,
-                                                                      folded, dev_flags));
+  LPQT_DISPATCH_DT(dtype, block_scales_kernel<DT><<<g, 256, 0, st>>>(W, N, K, ldw, B, bpr, vec, maxv, bias_shift,
+                                                                      scales, folded, dev_flags));
   note_launch();
   return check_launch();
 }
@@ -668,6 +823,94 @@ int lpqt_stage_activations(const void* X, int dtype, int64_t K, int64_t M, int64
   if (M * Kp == 0) return LPQT_OK;
   const int g = grid_for(M * Kp, 256);
   LPQT_DISPATCH_DT(dtype, stage_activations_kernel<DT><<<g, 256, 0, as_stream(stream)>>>(X, K, M, ldx, Xt, Kp));
+  note_launch();
+  return check_launch();
+}
+
+
+// ---- FP5 e3m1 (4 + 1) --------------------------------------------------------
+int64_t lpqt_fp5_tail_length(int64_t n) { return ((n + 7) / 8 + 3) / 4 * 4; }
+
+int lpqt_fp5_encode_rtn(const void* x, int dtype, int64_t n, uint8_t* codes, uint32_t* dev_flags, void* stream) {
+  if (n < 0) return LPQT_E_SHAPE;
+  if (n == 0) return LPQT_OK;
+  LPQT_DISPATCH_DT(dtype, fp5_encode_kernel<DT><<<grid_for(n, 256), 256, 0, as_stream(stream)>>>(x, n, codes,
+                                                                                                  dev_flags));
+  note_launch();
+  return check_launch();
+}
+
+int lpqt_fp5_pack(const uint8_t* codes, int64_t n, uint8_t* seg4, uint8_t* seg1, uint32_t* dev_flags, void* stream) {
+  if (n < 0) return LPQT_E_SHAPE;
+  const int64_t len4 = lpqt_fp6_seg4_length(n), len1 = lpqt_fp5_tail_length(n);
+  if (len4 == 0) return LPQT_OK;
+  const int64_t groups = (len4 * 2 + 7) / 8 > len1 ? (len4 * 2 + 7) / 8 : len1;
+  fp5_pack_kernel<<<grid_for(groups, 256), 256, 0, as_stream(stream)>>>(codes, n, len4, len1, seg4, seg1, dev_flags);
+  note_launch();
+  return check_launch();
+}
+
+int lpqt_fp5_unpack(const uint8_t* seg4, const uint8_t* seg1, int64_t n, uint8_t* codes, void* stream) {
+  if (n < 0) return LPQT_E_SHAPE;
+  if (n == 0) return LPQT_OK;
+  fp5_unpack_kernel<<<grid_for(n, 256), 256, 0, as_stream(stream)>>>(seg4, seg1, n, codes);
+  note_launch();
+  return check_launch();
+}
+
+int lpqt_fp5_quantize_pack_blocks(const void* W, int dtype, int64_t N, int64_t K, int64_t ldw, int64_t block,
+                                  int bias_shift, uint16_t* scales, uint16_t* folded, uint8_t* seg4, uint8_t* seg1,
+                                  uint32_t* dev_flags, void* stream) {
+  int rc = check_quantize_args(W, dtype, N, K, ldw, bias_shift, folded);
+  if (rc != LPQT_OK || N == 0 || K == 0) return rc;
+  const cudaStream_t st = as_stream(stream);
+  int64_t B, bpr;
+  block_geometry(K, block, B, bpr);
+  rc = quantize_scales(W, dtype, N, K, ldw, B, bpr, rows_vectorizable(W, ldw), bias_shift, scales, folded, dev_flags,
+                       st, 24.0);
+  if (rc != LPQT_OK) return rc;
+  const int64_t len4 = lpqt_fp6_seg4_length(N * K), len1 = lpqt_fp5_tail_length(N * K);
+  const int64_t groups = (N * K + 7) / 8;
+  LPQT_DISPATCH_DT(dtype, fp5_encode_planes_kernel<DT><<<grid_for(groups, 256), 256, 0, st>>>(
+                              W, N, K, ldw, B, bpr, scales, len4, len1, seg4, seg1));
+  note_launch();
+  return check_launch();
+}
+
+int lpqt_fp5_dequantize_tensor_blocks(const uint8_t* seg4, const uint8_t* seg1, const uint16_t* block_scale, int path,
+                                      int64_t N, int64_t K, int64_t block, void* out, int out_dtype, void* stream) {
+  if (N < 0 || K < 0) return LPQT_E_SHAPE;
+  if (path != 0 && path != 1) return LPQT_E_INVALID_INPUT;
+  if (N * K == 0) return LPQT_OK;
+  int64_t B, bpr;
+  block_geometry(K, block, B, bpr);
+  const int g = grid_for(N * K, 256);
+  if (out_dtype == LPQT_F64) {
+    fp5_dequantize_tensor_kernel<LPQT_F64><<<g, 256, 0, as_stream(stream)>>>(seg4, seg1, block_scale, path, N, K, B,
+                                                                              bpr, out);
+  } else if (out_dtype == LPQT_F16) {
+    fp5_dequantize_tensor_kernel<LPQT_F16><<<g, 256, 0, as_stream(stream)>>>(seg4, seg1, block_scale, path, N, K, B,
+                                                                              bpr, out);
+  } else {
+    return LPQT_E_UNSUPPORTED;
+  }
+  note_launch();
+  return check_launch();
+}
+
+int lpqt_fp5_dequant_bias_shift(const uint8_t* codes, const uint16_t* folded, int64_t n, uint16_t* out,
+                                void* stream) {
+  if (n < 0) return LPQT_E_SHAPE;
+  if (n == 0) return LPQT_OK;
+  fp5_dequant_kernel<<<grid_for(n, 256), 256, 0, as_stream(stream)>>>(codes, folded, 1, n, out);
+  note_launch();
+  return check_launch();
+}
+
+int lpqt_fp5_dequant_naive(const uint8_t* codes, const uint16_t* scales, int64_t n, uint16_t* out, void* stream) {
+  if (n < 0) return LPQT_E_SHAPE;
+  if (n == 0) return LPQT_OK;
+  fp5_dequant_kernel<<<grid_for(n, 256), 256, 0, as_stream(stream)>>>(codes, scales, 0, n, out);
   note_launch();
   return check_launch();
 }

@@ -12,7 +12,7 @@ from functools import lru_cache
 import numpy as np
 
 from . import _lib
-from .codec import MiniFloatFormat, require_fp6
+from .codec import MiniFloatFormat, kernel_prefix
 from .errors import InvalidInput
 from .packing import PackedSegments, unpack
 
@@ -40,8 +40,9 @@ def _as_f16_device(x):
 
 def fold_scale_array(fmt: MiniFloatFormat, scales):
     """folded = S * 2^12 exactly; InvalidInput for non-positive / non-finite
-    scales, ScaleOverflow above 65504 (dequant.py:61-69)."""
-    require_fp6(fmt)
+    scales, ScaleOverflow above 65504 (dequant.py:61-69; the fold constant is
+    2^12 for both formats: bias 15 - 3)."""
+    kernel_prefix(fmt)
     t = _lib.torch()
     s, torch_in = _as_f16_device(scales)
     shape = tuple(s.shape)
@@ -82,14 +83,12 @@ def _elementwise(fn_name: str, codes, scale):
 
 def dequant_naive_array(fmt: MiniFloatFormat, codes, scale):
     """value_f16[c] * S in binary16 (dequant.py:72-79); broadcasts."""
-    require_fp6(fmt)
-    return _elementwise("lpqt_fp6_dequant_naive", codes, scale)
+    return _elementwise(kernel_prefix(fmt) + "_dequant_naive", codes, scale)
 
 
 def dequant_bias_shift_array(fmt: MiniFloatFormat, codes, folded):
     """compose[c] * folded in binary16 (dequant.py:82-86); broadcasts."""
-    require_fp6(fmt)
-    return _elementwise("lpqt_fp6_dequant_bias_shift", codes, folded)
+    return _elementwise(kernel_prefix(fmt) + "_dequant_bias_shift", codes, folded)
 
 
 def dequant_naive(fmt: MiniFloatFormat, code: int, scale) -> np.float16:

@@ -25,13 +25,15 @@ def _round_up(x: int, m: int) -> int:
     return (x + m - 1) // m * m
 
 
-def prepack(seg4, seg2, n: int, k: int):
-    """Canonical planes (CUDA uint8) -> tile layout (CUDA uint8)."""
+def prepack(seg4, seg2, n: int, k: int, fmt: str = "fp6"):
+    """Canonical planes (CUDA uint8) -> tile layout (CUDA uint8).  fmt "fp5":
+    4 + 1 planes, converted to the FP6 tile layout (every e3m1 value is an
+    e3m2 value) — FP5 weights stream at FP6's 0.75 B per weight."""
     t = _lib.torch()
     nbytes = int(_lib.load().lpqt_fp6_tiles_bytes(n, k))
     tiles = t.empty(nbytes, dtype=t.uint8, device=seg4.device)
-    _lib.check(_lib.load().lpqt_fp6_prepack(seg4.data_ptr(), seg2.data_ptr(), n, k, tiles.data_ptr(),
-                                            _lib.stream_ptr()), "prepack")
+    fn = _lib.load().lpqt_fp5_prepack if fmt == "fp5" else _lib.load().lpqt_fp6_prepack
+    _lib.check(fn(seg4.data_ptr(), seg2.data_ptr(), n, k, tiles.data_ptr(), _lib.stream_ptr()), "prepack")
     return tiles
 
 
@@ -55,8 +57,9 @@ class Fp6Weight:
 
     # -- construction -------------------------------------------------------
     @classmethod
-    def from_planes(cls, seg4, seg2, scales, n: int, k: int, folded=None, block: int = 0) -> "Fp6Weight":
-        tiles = prepack(seg4, seg2, n, k)
+    def from_planes(cls, seg4, seg2, scales, n: int, k: int, folded=None, block: int = 0,
+                    fmt: str = "fp6") -> "Fp6Weight":
+        tiles = prepack(seg4, seg2, n, k, fmt)
         # one-time: the weights are complete before any GEMM can overlap them
         _lib.torch().cuda.current_stream().synchronize()
         return cls(tiles, scales, n, k, folded, static=True, block=block)
@@ -93,7 +96,8 @@ class Fp6Weight:
         if cache is not None and "weight" in cache:
             return cache["weight"]
         s4, s2, sc = device_planes(q)
-        w = cls.from_planes(s4, s2, sc, q.rows, q.cols, block=scale_block(q.scheme))
+        fmt = "fp5" if q.scheme.fmt.minifloat.mantissa_bits == 1 else "fp6"
+        w = cls.from_planes(s4, s2, sc, q.rows, q.cols, block=scale_block(q.scheme), fmt=fmt)
         if cache is not None:
             cache["weight"] = w
         return w

@@ -14,7 +14,7 @@ from dataclasses import dataclass
 import numpy as np
 
 from . import _lib
-from .codec import MiniFloatFormat, require_fp6
+from .codec import FP6_E3M2, MiniFloatFormat, kernel_prefix
 from .errors import InvalidCode, InvalidScheme, PayloadMismatch
 
 
@@ -67,35 +67,35 @@ def _codes_to_device(fmt: MiniFloatFormat, codes):
     return _lib.to_device(a), False
 
 
-def pack_device(codes_dev, n: int):
-    """codes (uint8 CUDA tensor, n) -> (seg4, seg2) CUDA tensors."""
+def pack_device(codes_dev, n: int, fmt: MiniFloatFormat = FP6_E3M2):
+    """codes (uint8 CUDA tensor, n) -> (seg4, tail) CUDA tensors."""
     t = _lib.torch()
     seg4 = t.empty(seg4_length(n), dtype=t.uint8, device=codes_dev.device)
-    seg2 = t.empty(_align4((2 * n + 7) // 8), dtype=t.uint8, device=codes_dev.device)
-    if seg2.numel():
+    tail = t.empty(tail_length(fmt, n), dtype=t.uint8, device=codes_dev.device)
+    if tail.numel():
         flags = _lib.Flags()
-        _lib.check(_lib.load().lpqt_fp6_pack(codes_dev.data_ptr(), n, seg4.data_ptr(), seg2.data_ptr(),
-                                             flags.ptr, _lib.stream_ptr()), "pack")
+        _lib.check(getattr(_lib.load(), kernel_prefix(fmt) + "_pack")(
+            codes_dev.data_ptr(), n, seg4.data_ptr(), tail.data_ptr(), flags.ptr, _lib.stream_ptr()), "pack")
         if flags.value():
-            raise InvalidCode("codes must fit 6 bits")
-    return seg4, seg2
+            raise InvalidCode(f"codes must fit {fmt.total_bits} bits")
+    return seg4, tail
 
 
-def unpack_device(seg4, seg2, n: int):
+def unpack_device(seg4, tail, n: int, fmt: MiniFloatFormat = FP6_E3M2):
     t = _lib.torch()
     codes = t.empty(n, dtype=t.uint8, device=seg4.device)
     if n:
-        _lib.check(_lib.load().lpqt_fp6_unpack(seg4.data_ptr(), seg2.data_ptr(), n, codes.data_ptr(),
-                                               _lib.stream_ptr()), "unpack")
+        _lib.check(getattr(_lib.load(), kernel_prefix(fmt) + "_unpack")(
+            seg4.data_ptr(), tail.data_ptr(), n, codes.data_ptr(), _lib.stream_ptr()), "unpack")
     return codes
 
 
 def pack(fmt: MiniFloatFormat, codes) -> PackedSegments:
     """Pack a code stream into the canonical planes (packing.py:63-90)."""
-    require_fp6(fmt)
+    kernel_prefix(fmt)
     c, torch_in = _codes_to_device(fmt, codes)
     n = c.numel()
-    seg4, seg2 = pack_device(c, n)
+    seg4, seg2 = pack_device(c, n, fmt)
     if torch_in:
         return PackedSegments(seg4, seg2, n)
     return PackedSegments(seg4.cpu().numpy(), seg2.cpu().numpy(), n)
@@ -103,7 +103,7 @@ def pack(fmt: MiniFloatFormat, codes) -> PackedSegments:
 
 def unpack(fmt: MiniFloatFormat, segments: PackedSegments):
     """Recover the first `code_count` codes; pad bits ignored (packing.py:93-118)."""
-    require_fp6(fmt)
+    kernel_prefix(fmt)
     n = int(segments.code_count)
     torch_in = _lib.is_torch(segments.seg4)
     s4 = segments.seg4 if torch_in else np.asarray(segments.seg4, dtype=np.uint8)
@@ -114,7 +114,7 @@ def unpack(fmt: MiniFloatFormat, segments: PackedSegments):
         raise PayloadMismatch(f"segment lengths ({n4}, {n2}) inconsistent with code count {n}")
     d4 = _lib.to_device(s4).reshape(-1)
     d2 = _lib.to_device(s2).reshape(-1)
-    codes = unpack_device(d4, d2, n)
+    codes = unpack_device(d4, d2, n, fmt)
     return codes if torch_in else codes.cpu().numpy()
 
 

@@ -5,9 +5,9 @@ weight row) runs as one fused GPU kernel (`lpqt_fp6_quantize_pack`): row
 max|w|, S = RN_f16(peak/28), fold S*2^12, RTN codes of W/S and the canonical
 4+2 planes, bit-exact with the reference for f64/f32/f16/bf16 input.
 `dequantize_tensor` is the GPU `lpqt_fp6_dequantize_tensor` (f64 exact).
-FP6 quantizes under CGQ (one scale per output row) or FGQ (one per block of
-block_size columns; the GEMM needs blocks of whole 128-k tiles); FP5 and
-INT4 are outside this path and raise InvalidScheme.
+FP6 (4+2) and FP5 (4+1) quantize under CGQ (one scale per output row) or FGQ
+(one per block of block_size columns; the GEMM needs blocks of whole 128-k
+tiles); INT4 is outside this path and raises InvalidScheme.
 """
 
 from __future__ import annotations
@@ -18,7 +18,7 @@ from enum import Enum
 import numpy as np
 
 from . import _lib
-from .codec import FP5_E3M1, FP6_E3M2, MiniFloatFormat
+from .codec import FP5_E3M1, FP6_E3M2, MiniFloatFormat, kernel_prefix
 from .errors import (InvalidInput, InvalidScheme, PathUnavailable, PayloadMismatch,
                      ShapeError)
 from .packing import PackedSegments, seg4_length, tail_length
@@ -94,11 +94,11 @@ def _validate_scheme(scheme: QuantScheme) -> None:
 
 
 def _require_path(scheme: QuantScheme) -> None:
-    """CGQ or FGQ x FP6_E3M2 (the formats this library runs on the GPU)."""
+    """CGQ or FGQ x FP6_E3M2 / FP5_E3M1 (the formats this library runs on the GPU)."""
     _validate_scheme(scheme)
-    if scheme.fmt is not TensorFormat.FP6_E3M2:
+    if scheme.fmt.minifloat is None:
         raise InvalidScheme(
-            f"{scheme.granularity.name} x {scheme.fmt.name} is outside the B200 path (FP6_E3M2, CGQ or FGQ)")
+            f"{scheme.granularity.name} x {scheme.fmt.name} is outside the B200 path (FP6 / FP5, CGQ or FGQ)")
 
 
 def scale_block(scheme: QuantScheme) -> int:
@@ -172,7 +172,7 @@ def _weights_to_device(W):
     return _lib.to_device(a), False
 
 
-def quantize_device(w, bias_shift: bool = True, block: int = 0):
+def quantize_device(w, bias_shift: bool = True, block: int = 0, fmt: MiniFloatFormat = FP6_E3M2):
     """GPU quantize of a 2-D CUDA tensor -> dict of CUDA tensors
     {scales, folded, seg4, seg2} (canonical planes, flat index r*K + k;
     scales one per row, or per block of `block` columns row-major)."""
@@ -184,12 +184,12 @@ def quantize_device(w, bias_shift: bool = True, block: int = 0):
     folded = t.empty(nb, dtype=t.float16, device=dev) if bias_shift else None
     nk = n * k
     seg4 = t.empty(seg4_length(nk), dtype=t.uint8, device=dev)
-    seg2 = t.empty(tail_length(FP6_E3M2, nk), dtype=t.uint8, device=dev)
+    seg2 = t.empty(tail_length(fmt, nk), dtype=t.uint8, device=dev)
     if seg4.numel():
         seg4[-4:].zero_()
         seg2[-4:].zero_()
     flags = _lib.Flags()
-    _lib.check(_lib.load().lpqt_fp6_quantize_pack_blocks(
+    _lib.check(getattr(_lib.load(), kernel_prefix(fmt) + "_quantize_pack_blocks")(
         w.data_ptr(), _lib.dtype_code(w.dtype), n, k, k, int(block), int(bool(bias_shift)), scales.data_ptr(),
         _lib.ptr(folded), seg4.data_ptr(), seg2.data_ptr(), flags.ptr, _lib.stream_ptr()), "quantize_tensor")
     flags.raise_if_set()
@@ -221,7 +221,7 @@ def quantize_tensor(W, scheme: QuantScheme, bias_shift: bool = False) -> Quantiz
         e8 = np.zeros(0, dtype=np.uint8)
         return QuantizedTensor(n, k, scheme, e16, None, PackedSegments(e8, e8.copy(), 0), bias_shift,
                                e16.copy() if bias_shift else None)
-    d = quantize_device(w, bias_shift, scale_block(scheme))
+    d = quantize_device(w, bias_shift, scale_block(scheme), scheme.fmt.minifloat)
     cache = {"scales": d["scales"], "seg4": d["seg4"], "seg2": d["seg2"]}
     if torch_in:
         return QuantizedTensor(n, k, scheme, d["scales"], None, PackedSegments(d["seg4"], d["seg2"], n * k),
@@ -233,12 +233,12 @@ def quantize_tensor(W, scheme: QuantScheme, bias_shift: bool = False) -> Quantiz
 
 def compute_scale_fp(values, fmt: MiniFloatFormat) -> BlockParams:
     """Max-abs scale of one block (quantizer.py:156-163), via the GPU quantizer."""
-    if fmt != FP6_E3M2:
-        raise InvalidScheme(f"{fmt.name} is outside the B200 FP6 path")
+    kernel_prefix(fmt)
     v = np.asarray(values, dtype=np.float64).ravel()
     if v.size == 0:
         raise InvalidInput("block must be non-empty")
-    q = quantize_tensor(v.reshape(1, -1), CGQ_FP6, bias_shift=False)
+    tf = TensorFormat.FP6_E3M2 if fmt == FP6_E3M2 else TensorFormat.FP5_E3M1
+    q = quantize_tensor(v.reshape(1, -1), QuantScheme(Granularity.CGQ, tf), bias_shift=False)
     return BlockParams(scale=np.float16(q.scales[0]))
 
 
@@ -256,7 +256,7 @@ def device_planes(q: QuantizedTensor):
         raise PayloadMismatch("payload does not hold rows*cols codes")
     s4 = _lib.to_device(q.payload.seg4).reshape(-1)
     s2 = _lib.to_device(q.payload.seg_tail).reshape(-1)
-    if s4.numel() != seg4_length(n) or s2.numel() != tail_length(FP6_E3M2, n):
+    if s4.numel() != seg4_length(n) or s2.numel() != tail_length(q.scheme.fmt.minifloat, n):
         raise PayloadMismatch("segment lengths inconsistent with rows*cols")
     t = _lib.torch()
     sc = q.scales if _lib.is_torch(q.scales) else np.asarray(q.scales, dtype=np.float16)
@@ -287,7 +287,7 @@ def dequantize_tensor(q: QuantizedTensor, path: str = "naive"):
     else:
         raise ValueError(f"unknown dequantization path {path!r}")
     out = t.empty((q.rows, q.cols), dtype=t.float64, device=s4.device)
-    _lib.check(_lib.load().lpqt_fp6_dequantize_tensor_blocks(
+    _lib.check(getattr(_lib.load(), kernel_prefix(q.scheme.fmt.minifloat) + "_dequantize_tensor_blocks")(
         s4.data_ptr(), s2.data_ptr(), row_scale.data_ptr(), p, q.rows, q.cols, scale_block(q.scheme), out.data_ptr(),
         _lib.F64, _lib.stream_ptr()), "dequantize_tensor")
     return out if torch_in else out.cpu().numpy()

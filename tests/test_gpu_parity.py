@@ -567,3 +567,59 @@ def test_fgq_gemm_vs_oracle(n, k, block, m):
     assert normwise_rel(y.t().cpu().numpy(), Yo) <= REL_TOL
     y2 = L.w6a16_linear(x, w, out_dtype=torch.float32, sched="streamk", split_k=3)
     assert normwise_rel(y2.cpu().numpy(), y.cpu().numpy()) <= 1e-5
+
+
+# ---------------------------------------------------------------- FP5 e3m1 (4 + 1)
+FP5_GOLD = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "golden_fp5.npz")
+
+
+def test_fp5_codec_pack_dequant_vs_reference():
+    g = np.load(FP5_GOLD)
+    F5 = L.FP5_E3M1
+    assert np.array_equal(L.encode_rtn_array(F5, g["enc/x"]), g["enc/codes"])
+    for n in g["p_lens"]:
+        seg = L.pack(F5, g[f"p/{n}/codes"])
+        assert np.array_equal(seg.seg4, g[f"p/{n}/seg4"]) and np.array_equal(seg.seg_tail, g[f"p/{n}/seg1"]), n
+        assert np.array_equal(L.unpack(F5, seg), g[f"p/{n}/codes"]), n
+    s = g["dq/scales"].view(np.float16)
+    codes = np.arange(32, dtype=np.uint8)
+    f = L.fold_scale_array(F5, s)
+    assert np.array_equal(L.dequant_bias_shift_array(F5, codes[:, None], f[None, :]).view(np.uint16), g["dq/bias"])
+    assert np.array_equal(L.dequant_naive_array(F5, codes[:, None], s[None, :]).view(np.uint16), g["dq/naive"])
+
+
+def test_fp5_quantize_dequantize_gemm_container_vs_reference():
+    """FP5 CGQ / FGQ quantize on the GPU == the reference's scales, folded
+    scales, 4 + 1 planes and .lpqt bytes; dequantize exact; the GEMM (through
+    the FP6 tile layout) within the normwise bar of the reference's GEMM."""
+    g = np.load(FP5_GOLD)
+    for name in [str(s) for s in g["q_names"]]:
+        W, b = g[f"q/{name}/W"], int(g[f"q/{name}/block"])
+        gran = L.Granularity.FGQ if b else L.Granularity.CGQ
+        q = L.quantize_tensor(W, L.QuantScheme(gran, L.TensorFormat.FP5_E3M1, b), bias_shift=True)
+        assert np.array_equal(q.scales.view(np.uint16), g[f"q/{name}/scales"]), name
+        assert np.array_equal(q.folded_scales.view(np.uint16), g[f"q/{name}/folded"]), name
+        assert np.array_equal(q.payload.seg4, g[f"q/{name}/seg4"]), name
+        assert np.array_equal(q.payload.seg_tail, g[f"q/{name}/seg1"]), name
+        assert L.write_lpqt(q) == g[f"q/{name}/container"].tobytes(), name
+        for path in ("naive", "bias_shift"):
+            assert np.array_equal(L.dequantize_tensor(q, path), g[f"q/{name}/deq"]), (name, path)
+        if b == 0 or b % 128 == 0:
+            Y = L.gemm_quantized(q, g[f"q/{name}/X"])
+            assert normwise_rel(Y, g[f"q/{name}/Y"]) <= REL_TOL, name
+            w = L.load_lpqt(g[f"q/{name}/container"].tobytes())
+            y = L.w6a16_linear(torch.from_numpy(g[f"q/{name}/X"].T.copy()).cuda().half(), w, out_dtype=torch.float32)
+            assert normwise_rel(y.t().cpu().numpy(), g[f"q/{name}/Y"]) <= REL_TOL, name
+
+
+@pytest.mark.parametrize("n,k,m", [(512, 1024, 16), (1000, 4096, 300), (4096, 4096, 1)])
+def test_fp5_gemm_vs_oracle_large(n, k, m):
+    rng = np.random.default_rng(n + k + m)
+    W = (rng.standard_normal((n, k)) * 0.02).astype(np.float16)
+    X = rng.standard_normal((k, m)).astype(np.float16)
+    q = L.quantize_tensor(W, L.QuantScheme(L.Granularity.CGQ, L.TensorFormat.FP5_E3M1), bias_shift=True)
+    o = O.quantize_tensor_fp5(W, True)
+    assert np.array_equal(q.payload.seg4, o["seg4"]) and np.array_equal(q.payload.seg_tail, o["seg1"])
+    Y = L.gemm_quantized(q, X)
+    What = O.fp5_value_table()[o["codes"].reshape(n, k)] * o["scales"].astype(np.float64)[:, None]
+    assert normwise_rel(Y, What @ X.astype(np.float64)) <= REL_TOL
