@@ -269,6 +269,23 @@ int lpqt_fp5_dequant_naive(const uint8_t* codes, const uint16_t* scales,
 int lpqt_fp5_prepack(const uint8_t* seg4, const uint8_t* seg1, int64_t N,
                      int64_t K, uint8_t* tiles, void* stream);
 
+/* ---- INT4 asymmetric, CGQ / FGQ (quantizer.py:232-244, packing.py:121-141)
+ * The paper's comparator format: per block zero point RN_f16(min) and scale
+ * RN_f16((max - min) / 15), levels clip(rint((w - Z) / S), 0, 15), two per
+ * byte (ceil(n / 2) bytes, even index low nibble); dequantize = Z + S * level
+ * in f64.  The comparator GEMM dequantizes and calls a library GEMM. */
+int lpqt_int4_quantize_blocks(const void* W, int dtype, int64_t N, int64_t K,
+                              int64_t ldw, int64_t block, uint16_t* scales,
+                              uint16_t* zeros, uint8_t* nibbles,
+                              uint32_t* dev_flags, void* stream);
+int lpqt_int4_pack(const uint8_t* levels, int64_t n, uint8_t* nibbles,
+                   uint32_t* dev_flags, void* stream);
+int lpqt_int4_unpack(const uint8_t* nibbles, int64_t n, uint8_t* levels,
+                     void* stream);
+int lpqt_int4_dequantize_blocks(const uint8_t* nibbles, const uint16_t* scales,
+                                const uint16_t* zeros, int64_t N, int64_t K,
+                                int64_t block, double* out, void* stream);
+
 /* Number of kernel launches performed by this library since load (for the
  * bench's gpu_launches claim). */
 int64_t lpqt_launch_count(void);

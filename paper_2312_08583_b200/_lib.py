@@ -89,6 +89,10 @@ SIGNATURES = {
     "lpqt_fp5_dequant_bias_shift": (_I32, [_P, _P, _I64, _P, _P]),
     "lpqt_fp5_dequant_naive": (_I32, [_P, _P, _I64, _P, _P]),
     "lpqt_fp5_prepack": (_I32, [_P, _P, _I64, _I64, _P, _P]),
+    "lpqt_int4_quantize_blocks": (_I32, [_P, _I32, _I64, _I64, _I64, _I64, _P, _P, _P, _P, _P]),
+    "lpqt_int4_pack": (_I32, [_P, _I64, _P, _P, _P]),
+    "lpqt_int4_unpack": (_I32, [_P, _I64, _P, _P]),
+    "lpqt_int4_dequantize_blocks": (_I32, [_P, _P, _P, _I64, _I64, _I64, _P, _P]),
     "lpqt_launch_count": (_I64, []),
 }
 

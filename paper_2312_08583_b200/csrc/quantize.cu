@@ -637,6 +637,108 @@ __global__ void fp5_dequant_kernel(const uint8_t* __restrict__ codes, const uint
   }
 }
 
+
+// ---------------------------------------------------------------------------
+// INT4 asymmetric (quantizer.py:232-244, packing.py:121-141): per block
+// zero point Z = RN_f16(min), scale S = RN_f16((max - min) / 15) (1.0 for a
+// constant block, 0 -> 2^-24, inf -> InvalidInput), levels =
+// clip(rint((w - Z) / S), 0, 15) in f64, two levels per byte (even index in
+// the low nibble, ceil(n / 2) bytes).  The comparator path of SURVEY §8 f4.
+// ---------------------------------------------------------------------------
+template <int DT>
+__global__ void __launch_bounds__(256) int4_block_params_kernel(const void* __restrict__ W, int64_t N, int64_t K,
+                                                                int64_t ldw, int64_t B, int64_t bpr,
+                                                                uint16_t* __restrict__ scales,
+                                                                uint16_t* __restrict__ zeros,
+                                                                uint32_t* __restrict__ flags) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  uint32_t f = 0;
+  for (int64_t u = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); u < N * bpr; u += warps) {
+    const int64_t r = u / bpr, j = u - r * bpr;
+    const int64_t k0 = j * B, k1 = k0 + B < K ? k0 + B : K;
+    double lo = 1e308, hi = -1e308;
+    bool bad = false;
+    for (int64_t k = k0 + lane; k < k1; k += 32) {
+      const double v = load_as_double<DT>(W, r * ldw + k);
+      bad |= !isfinite(v);
+      lo = fmin(lo, v);
+      hi = fmax(hi, v);
+    }
+    if (__any_sync(0xffffffffu, bad)) f |= LPQT_F_NONFINITE;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      lo = fmin(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+      hi = fmax(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+    }
+    if (lane == 0) {
+      const uint16_t zb = __half_as_ushort(__double2half(lo));
+      if ((zb & 0x7FFFu) == 0x7C00u) f |= LPQT_F_SCALE_INF;  // zero point overflows binary16
+      const double span = hi - lo;
+      uint16_t sb = __half_as_ushort(__double2half(span == 0.0 ? 1.0 : span / 15.0));
+      if ((sb & 0x7FFFu) == 0x7C00u) f |= LPQT_F_SCALE_INF;
+      if ((sb & 0x7FFFu) == 0) sb = 0x0001u;
+      zeros[u] = zb;
+      scales[u] = sb;
+    }
+  }
+  if (f) atomicOr(flags, f);
+}
+
+__device__ __forceinline__ double h2d(uint16_t b) { return static_cast<double>(__half2float(__ushort_as_half(b))); }
+
+template <int DT>
+__global__ void int4_encode_kernel(const void* __restrict__ W, int64_t N, int64_t K, int64_t ldw, int64_t B,
+                                   int64_t bpr, const uint16_t* __restrict__ scales,
+                                   const uint16_t* __restrict__ zeros, int64_t len, uint8_t* __restrict__ nib) {
+  const int64_t total = N * K, groups = (total + 7) / 8;
+  for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < groups; g += (int64_t)gridDim.x * blockDim.x) {
+    int64_t r = (8 * g) / K, k = 8 * g - r * K;
+    uint32_t word = 0;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      if (8 * g + j < total) {
+        const int64_t b = r * bpr + k / B;
+        const double lvl = rint((load_as_double<DT>(W, r * ldw + k) - h2d(zeros[b])) / h2d(scales[b]));
+        word |= static_cast<uint32_t>(fmin(fmax(lvl, 0.0), 15.0)) << (4 * j);
+      }
+      if (++k == K) k = 0, ++r;
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      if (4 * g + q < len) nib[4 * g + q] = static_cast<uint8_t>(word >> (8 * q));
+  }
+}
+
+__global__ void int4_pack_kernel(const uint8_t* __restrict__ lv, int64_t n, uint8_t* __restrict__ nib,
+                                 uint32_t* __restrict__ flags) {
+  bool bad = false;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < (n + 1) / 2;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t a = lv[2 * i], b = 2 * i + 1 < n ? lv[2 * i + 1] : 0u;
+    bad |= a > 15u || b > 15u;
+    nib[i] = static_cast<uint8_t>((a & 15u) | ((b & 15u) << 4));
+  }
+  if (bad) atomicOr(flags, LPQT_F_BAD_CODE);
+}
+
+__global__ void int4_unpack_kernel(const uint8_t* __restrict__ nib, int64_t n, uint8_t* __restrict__ lv) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    lv[i] = static_cast<uint8_t>((nib[i >> 1] >> (4 * (i & 1))) & 15u);
+}
+
+// dequantize_tensor INT4 (quantizer.py:296-298): Z + S * level in f64
+__global__ void int4_dequantize_kernel(const uint8_t* __restrict__ nib, const uint16_t* __restrict__ scales,
+                                       const uint16_t* __restrict__ zeros, int64_t N, int64_t K, int64_t B,
+                                       int64_t bpr, double* __restrict__ out) {
+  const int64_t total = N * K;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / K, k = i - r * K, b = r * bpr + k / B;
+    const double lvl = static_cast<double>((nib[i >> 1] >> (4 * (i & 1))) & 15u);
+    out[i] = h2d(zeros[b]) + h2d(scales[b]) * lvl;
+  }
+}
+
 }  // namespace lpqt
 
 using namespace lpqt;
@@ -911,6 +1013,59 @@ int lpqt_fp5_dequant_naive(const uint8_t* codes, const uint16_t* scales, int64_t
   if (n < 0) return LPQT_E_SHAPE;
   if (n == 0) return LPQT_OK;
   fp5_dequant_kernel<<<grid_for(n, 256), 256, 0, as_stream(stream)>>>(codes, scales, 0, n, out);
+  note_launch();
+  return check_launch();
+}
+
+
+// ---- INT4 asymmetric (comparator path) --------------------------------------
+int lpqt_int4_quantize_blocks(const void* W, int dtype, int64_t N, int64_t K, int64_t ldw, int64_t block,
+                              uint16_t* scales, uint16_t* zeros, uint8_t* nibbles, uint32_t* dev_flags,
+                              void* stream) {
+  if (N < 0 || K < 0 || ldw < K) return LPQT_E_SHAPE;
+  if (dtype < LPQT_F64 || dtype > LPQT_BF16) return LPQT_E_UNSUPPORTED;
+  if (N == 0 || K == 0) return LPQT_OK;
+  const cudaStream_t st = as_stream(stream);
+  int64_t B, bpr;
+  block_geometry(K, block, B, bpr);
+  const int64_t units = N * bpr;
+  const int g = static_cast<int>((units + 7) / 8 < 148 * 8 ? (units + 7) / 8 : 148 * 8);
+  LPQT_DISPATCH_DT(dtype, int4_block_params_kernel<DT><<<g, 256, 0, st>>>(W, N, K, ldw, B, bpr, scales, zeros,
+                                                                           dev_flags));
+  note_launch();
+  int rc = check_launch();
+  if (rc != LPQT_OK) return rc;
+  const int64_t len = (N * K + 1) / 2, groups = (N * K + 7) / 8;
+  LPQT_DISPATCH_DT(dtype, int4_encode_kernel<DT><<<grid_for(groups, 256), 256, 0, st>>>(W, N, K, ldw, B, bpr, scales,
+                                                                                       zeros, len, nibbles));
+  note_launch();
+  return check_launch();
+}
+
+int lpqt_int4_pack(const uint8_t* levels, int64_t n, uint8_t* nibbles, uint32_t* dev_flags, void* stream) {
+  if (n < 0) return LPQT_E_SHAPE;
+  if (n == 0) return LPQT_OK;
+  int4_pack_kernel<<<grid_for((n + 1) / 2, 256), 256, 0, as_stream(stream)>>>(levels, n, nibbles, dev_flags);
+  note_launch();
+  return check_launch();
+}
+
+int lpqt_int4_unpack(const uint8_t* nibbles, int64_t n, uint8_t* levels, void* stream) {
+  if (n < 0) return LPQT_E_SHAPE;
+  if (n == 0) return LPQT_OK;
+  int4_unpack_kernel<<<grid_for(n, 256), 256, 0, as_stream(stream)>>>(nibbles, n, levels);
+  note_launch();
+  return check_launch();
+}
+
+int lpqt_int4_dequantize_blocks(const uint8_t* nibbles, const uint16_t* scales, const uint16_t* zeros, int64_t N,
+                                int64_t K, int64_t block, double* out, void* stream) {
+  if (N < 0 || K < 0) return LPQT_E_SHAPE;
+  if (N * K == 0) return LPQT_OK;
+  int64_t B, bpr;
+  block_geometry(K, block, B, bpr);
+  int4_dequantize_kernel<<<grid_for(N * K, 256), 256, 0, as_stream(stream)>>>(nibbles, scales, zeros, N, K, B, bpr,
+                                                                              out);
   note_launch();
   return check_launch();
 }

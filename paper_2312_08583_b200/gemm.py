@@ -18,7 +18,8 @@ import numpy as np
 from . import _lib
 from .errors import PayloadMismatch, ShapeError
 from .linear import Fp6Weight, gemm_nm, stage_activations
-from .quantizer import ErrorReport, QuantizedTensor, _require_gemm_path, error_report, num_blocks
+from .quantizer import (ErrorReport, QuantizedTensor, TensorFormat, _require_gemm_path, dequantize_tensor,
+                        error_report, num_blocks)
 
 
 def _check_activation(X, k: int) -> None:
@@ -38,6 +39,8 @@ def gemm_quantized(wq: QuantizedTensor, X, split_k: int = 0, sched: str = "auto"
     the fp32 block partial)."""
     if wq.num_blocks != num_blocks(wq.rows, wq.cols, wq.scheme):
         raise PayloadMismatch("block parameter count does not match the scheme")
+    if wq.scheme.fmt is TensorFormat.INT4_ASYM:
+        return _gemm_int4_comparator(wq, X)
     _require_gemm_path(wq.scheme, wq.cols)
     torch_in = _lib.is_torch(X)
     Xa = X if torch_in else np.asarray(X)
@@ -69,6 +72,19 @@ def _dense(W, X, dtype):
     finally:
         t.backends.cuda.matmul.allow_tf32 = prev
     return Y if torch_in else Y.cpu().numpy()
+
+
+def _gemm_int4_comparator(wq: QuantizedTensor, X):
+    """INT4 (the paper's comparator format): the GPU dequantizes
+    (Z + S * level, exact f64) and a library fp32 GEMM multiplies — the
+    reference's dequantize-then-matmul comparator (gemm.py:84-110 INT4 terms),
+    not a fused W4A16 kernel."""
+    torch_in = _lib.is_torch(X)
+    Xa = X if torch_in else np.asarray(X)
+    _check_activation(Xa, wq.cols)
+    W_hat = dequantize_tensor(wq)
+    Y = _dense(W_hat, Xa, _lib.torch().float32)
+    return Y
 
 
 def gemm_reference(W, X):

@@ -119,10 +119,42 @@ def unpack(fmt: MiniFloatFormat, segments: PackedSegments):
 
 
 def pack_int4(levels):
-    """INT4 nibbles (packing.py:121-129): outside the B200 FP6 path."""
-    raise InvalidScheme("INT4 packing is outside the B200 FP6 path")
+    """INT4 levels -> nibbles, two per byte, even index in the low nibble
+    (packing.py:121-129), on the GPU.  InvalidCode outside [0, 15]."""
+    t = _lib.torch()
+    torch_in = _lib.is_torch(levels)
+    if torch_in:
+        lv = levels.reshape(-1)
+        if lv.numel() and (int(lv.min()) < 0 or int(lv.max()) > 15):
+            raise InvalidCode("INT4 levels must lie in [0, 15]")
+        lv = lv.to(_lib.device()).to(t.uint8).contiguous()
+    else:
+        a = np.asarray(levels).reshape(-1)
+        if a.size and (a.min() < 0 or a.max() > 15):
+            raise InvalidCode("INT4 levels must lie in [0, 15]")
+        lv = _lib.to_device(a.astype(np.uint8))
+    n = lv.numel()
+    out = t.empty((n + 1) // 2, dtype=t.uint8, device=lv.device)
+    if n:
+        flags = _lib.Flags()
+        _lib.check(_lib.load().lpqt_int4_pack(lv.data_ptr(), n, out.data_ptr(), flags.ptr, _lib.stream_ptr()),
+                   "pack_int4")
+        if flags.value():
+            raise InvalidCode("INT4 levels must lie in [0, 15]")
+    return out if torch_in else out.cpu().numpy()
 
 
 def unpack_int4(data, count: int):
-    """INT4 nibbles (packing.py:132-141): outside the B200 FP6 path."""
-    raise InvalidScheme("INT4 packing is outside the B200 FP6 path")
+    """Recover `count` INT4 levels from a nibble array (packing.py:132-141)."""
+    t = _lib.torch()
+    torch_in = _lib.is_torch(data)
+    d = data.reshape(-1) if torch_in else np.asarray(data, dtype=np.uint8).reshape(-1)
+    size = d.numel() if torch_in else d.size
+    if size != (count + 1) // 2:
+        raise PayloadMismatch(f"nibble array of {size} bytes cannot hold {count} levels")
+    dd = _lib.to_device(d).to(t.uint8).contiguous()
+    out = t.empty(count, dtype=t.uint8, device=dd.device)
+    if count:
+        _lib.check(_lib.load().lpqt_int4_unpack(dd.data_ptr(), count, out.data_ptr(), _lib.stream_ptr()),
+                   "unpack_int4")
+    return out if torch_in else out.cpu().numpy()

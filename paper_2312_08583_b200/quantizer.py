@@ -207,6 +207,8 @@ def quantize_tensor(W, scheme: QuantScheme, bias_shift: bool = False) -> Quantiz
     _validate_scheme(scheme)
     if bias_shift and scheme.fmt.minifloat is None:
         raise InvalidScheme("bias shift applies to minifloat formats only")
+    if scheme.fmt is TensorFormat.INT4_ASYM:
+        return _quantize_int4(W, scheme)
     _require_path(scheme)
     w, torch_in = _weights_to_device(W)
     n, k = (int(v) for v in w.shape)
@@ -242,8 +244,35 @@ def compute_scale_fp(values, fmt: MiniFloatFormat) -> BlockParams:
     return BlockParams(scale=np.float16(q.scales[0]))
 
 
+def _quantize_int4(W, scheme: QuantScheme) -> QuantizedTensor:
+    """INT4 asymmetric (quantizer.py:232-244) on the GPU: per block zero
+    point / scale, levels packed two per byte — the paper's comparator."""
+    w, torch_in = _weights_to_device(W)
+    n, k = (int(v) for v in w.shape)
+    t = _lib.torch()
+    block = scale_block(scheme)
+    nb = num_blocks(n, k, scheme)
+    scales = t.empty(nb, dtype=t.float16, device=w.device)
+    zeros = t.empty(nb, dtype=t.float16, device=w.device)
+    nib = t.zeros((n * k + 1) // 2, dtype=t.uint8, device=w.device)
+    if n and k:
+        flags = _lib.Flags()
+        _lib.check(_lib.load().lpqt_int4_quantize_blocks(
+            w.data_ptr(), _lib.dtype_code(w.dtype), n, k, k, block, scales.data_ptr(), zeros.data_ptr(),
+            nib.data_ptr(), flags.ptr, _lib.stream_ptr()), "quantize_tensor")
+        flags.raise_if_set()
+    if torch_in:
+        return QuantizedTensor(n, k, scheme, scales, zeros, nib, False, None)
+    return QuantizedTensor(n, k, scheme, scales.cpu().numpy(), zeros.cpu().numpy(), nib.cpu().numpy(), False, None)
+
+
 def compute_affine_params_int4(values) -> BlockParams:
-    raise InvalidScheme("INT4 is outside the B200 FP6 path")
+    """Zero point / scale of one INT4 block (quantizer.py:166-177), via the GPU quantizer."""
+    v = np.asarray(values, dtype=np.float64).ravel()
+    if v.size == 0:
+        raise InvalidInput("block must be non-empty")
+    q = _quantize_int4(v.reshape(1, -1), QuantScheme(Granularity.CGQ, TensorFormat.INT4_ASYM))
+    return BlockParams(scale=np.float16(q.scales[0]), zero_point=np.float16(q.zero_points[0]))
 
 
 def device_planes(q: QuantizedTensor):
@@ -273,6 +302,19 @@ def dequantize_tensor(q: QuantizedTensor, path: str = "naive"):
             else np.zeros((q.rows, q.cols), dtype=np.float64)
     if q.num_blocks != num_blocks(q.rows, q.cols, q.scheme):
         raise PayloadMismatch("block parameter count does not match the scheme")
+    if q.scheme.fmt is TensorFormat.INT4_ASYM:   # zero_point + scale * level, f64 (quantizer.py:296-298)
+        nib = q.payload if _lib.is_torch(q.payload) else np.asarray(q.payload, dtype=np.uint8)
+        if (nib.numel() if _lib.is_torch(nib) else nib.size) != (q.rows * q.cols + 1) // 2:
+            raise PayloadMismatch("payload does not hold rows*cols levels")
+        dn = _lib.to_device(nib).reshape(-1).to(t.uint8)
+        ds = _lib.to_device(q.scales if _lib.is_torch(q.scales) else np.asarray(q.scales, np.float16)).to(t.float16)
+        dz = _lib.to_device(q.zero_points if _lib.is_torch(q.zero_points)
+                            else np.asarray(q.zero_points, np.float16)).to(t.float16)
+        out = t.empty((q.rows, q.cols), dtype=t.float64, device=dn.device)
+        _lib.check(_lib.load().lpqt_int4_dequantize_blocks(
+            dn.data_ptr(), ds.data_ptr(), dz.data_ptr(), q.rows, q.cols, scale_block(q.scheme), out.data_ptr(),
+            _lib.stream_ptr()), "dequantize_tensor")
+        return out if torch_in else out.cpu().numpy()
     _require_path(q.scheme)
     if path == "naive":
         s4, s2, row_scale = device_planes(q)

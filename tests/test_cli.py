@@ -95,9 +95,13 @@ def test_quantize_inspect_dequantize_stats(tmp_path, weights_file, capsys):
     rc, so, _ = run(capsys, ["stats", "--input", str(out), "--reference", str(p), "--shape", "64x96"])
     d = kv(so)
     assert rc == 0 and float(d["sqnr_db"]) > 20.0
-    rc, _, err = run(capsys, ["quantize", "--input", str(p), "--shape", "64x96", "--format", "int4",
+    rc, _, err = run(capsys, ["quantize", "--input", str(p), "--shape", "64x96", "--format", "int4", "--bias-shift",
                               "--output", str(out)])
-    assert rc == 1 and err.startswith("error=InvalidScheme ")
+    assert rc == 1 and err.startswith("error=InvalidScheme ")      # cli tests test_int4_with_bias_shift_rejected
+    rc, so, _ = run(capsys, ["quantize", "--input", str(p), "--shape", "64x96", "--format", "int4", "--scheme", "fgq",
+                             "--block-size", "32", "--output", str(out)])
+    d = kv(so)
+    assert rc == 0 and d["blocks"] == str(64 * 3) and int(d["payload_bytes"]) == 64 * 96 // 2
 
 
 @pytest.mark.gpu
@@ -123,5 +127,5 @@ def test_bench_preset_smoke(capsys):
     assert rc == 0
     lines = [ln for ln in so.splitlines() if ln.startswith("path=")]
     assert [ln.split()[0] for ln in lines] == ["path=fp16_dense", "path=fp6_w6a16", "path=fp6_dequant_naive",
-                                               "path=fp6_dequant_bias_shift"]
+                                               "path=fp6_dequant_bias_shift", "path=int4_fgq"]
     assert "weight_bytes=8465152" in lines[1]   # 5504 x 2048 x 0.75 + 2 x 5504

@@ -623,3 +623,30 @@ def test_fp5_gemm_vs_oracle_large(n, k, m):
     Y = L.gemm_quantized(q, X)
     What = O.fp5_value_table()[o["codes"].reshape(n, k)] * o["scales"].astype(np.float64)[:, None]
     assert normwise_rel(Y, What @ X.astype(np.float64)) <= REL_TOL
+
+
+# ---------------------------------------------------------------- INT4 comparator
+INT4_GOLD = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "golden_int4.npz")
+
+
+def test_int4_quantize_pack_dequant_gemm_vs_reference():
+    """INT4 asymmetric CGQ / FGQ (any block size) on the GPU == the
+    reference's zero points, scales, nibbles, container bytes and f64
+    dequant; the comparator GEMM within the normwise bar."""
+    g = np.load(INT4_GOLD)
+    assert np.array_equal(L.pack_int4(g["p/levels"]), g["p/nibbles"])
+    assert np.array_equal(L.unpack_int4(g["p/nibbles"], g["p/levels"].size), g["p/levels"])
+    with pytest.raises(L.InvalidCode):
+        L.pack_int4([3, 16])
+    for name in [str(s) for s in g["q_names"]]:
+        W, b = g[f"q/{name}/W"], int(g[f"q/{name}/block"])
+        gran = L.Granularity.FGQ if b else L.Granularity.CGQ
+        q = L.quantize_tensor(W, L.QuantScheme(gran, L.TensorFormat.INT4_ASYM, b))
+        assert np.array_equal(q.scales.view(np.uint16), g[f"q/{name}/scales"]), name
+        assert np.array_equal(q.zero_points.view(np.uint16), g[f"q/{name}/zeros"]), name
+        assert np.array_equal(q.payload, g[f"q/{name}/nibbles"]), name
+        assert L.write_lpqt(q) == g[f"q/{name}/container"].tobytes(), name
+        assert np.array_equal(L.dequantize_tensor(q), g[f"q/{name}/deq"]), name
+        assert normwise_rel(L.gemm_quantized(q, g[f"q/{name}/X"]), g[f"q/{name}/Y"]) <= REL_TOL, name
+    with pytest.raises(L.InvalidScheme):
+        L.quantize_tensor(np.ones((2, 4)), L.QuantScheme(L.Granularity.CGQ, L.TensorFormat.INT4_ASYM), bias_shift=True)
