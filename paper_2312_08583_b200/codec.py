@@ -1,8 +1,8 @@
-"""FP6 (e3m2) code space — reference codec.py:20-151.
+"""FP6 (e3m2) and FP5 (e3m1) code spaces — reference codec.py:20-151.
 
-Format descriptors and the 64-entry value tables are static metadata and are
-built here; the RTN encoder (`encode_rtn_array`, the quantizer's inner loop,
-codec.py:116-132) runs on the GPU (`lpqt_fp6_encode_rtn`).
+Format descriptors and the value tables are static metadata and are built
+here; the RTN encoder (`encode_rtn_array`, the quantizer's inner loop,
+codec.py:116-132) runs on the GPU (`lpqt_fp6_encode_rtn` / `lpqt_fp5_encode_rtn`).
 """
 
 from __future__ import annotations
@@ -58,10 +58,6 @@ def kernel_prefix(fmt: MiniFloatFormat) -> str:
         return "lpqt_fp5"
     raise InvalidScheme(f"{fmt.name} is not a format of this library (FP6_E3M2, FP5_E3M1)")
 
-
-def require_fp6(fmt: MiniFloatFormat) -> None:
-    if fmt != FP6_E3M2:
-        raise InvalidScheme(f"{fmt.name} is outside this operation (FP6_E3M2 only)")
 
 
 def decode(fmt: MiniFloatFormat, code: int) -> float:

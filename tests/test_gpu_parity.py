@@ -650,3 +650,21 @@ def test_int4_quantize_pack_dequant_gemm_vs_reference():
         assert normwise_rel(L.gemm_quantized(q, g[f"q/{name}/X"]), g[f"q/{name}/Y"]) <= REL_TOL, name
     with pytest.raises(L.InvalidScheme):
         L.quantize_tensor(np.ones((2, 4)), L.QuantScheme(L.Granularity.CGQ, L.TensorFormat.INT4_ASYM), bias_shift=True)
+
+
+def test_random_shape_fuzz():
+    """Seeded fuzz over shapes / batch / scheme: every launch within the
+    normwise bar of the f64 product of the kernel's own binary16 weights,
+    bit-identical on relaunch (whatever path the timing picks)."""
+    rng = np.random.default_rng(20261017)
+    for _ in range(40):
+        n = int(rng.choice([128, 256, 384, 640, 1000, 2048, 4224]))
+        k = int(rng.choice([128, 256, 520, 1024, 3000, 4096, 8192]))
+        m = int(rng.choice([1, 2, 5, 16, 17, 31, 32, 40, 64, 96, 128, 129, 200, 300]))
+        block = int(rng.choice([0, 0, 128, 256])) if k > 256 else 0
+        w = L.Fp6Weight.quantize((torch.randn(n, k, device="cuda") * 0.02).half(), block=block)
+        x = torch.randn(m, k, device="cuda").half()
+        y = L.w6a16_linear(x, w, out_dtype=torch.float32)
+        assert torch.equal(y, L.w6a16_linear(x, w, out_dtype=torch.float32)), (n, k, m, block)
+        ref = x.double() @ w.dequantize_f16().double().t()
+        assert normwise_rel(y.cpu().numpy(), ref.cpu().numpy()) <= REL_TOL, (n, k, m, block)
