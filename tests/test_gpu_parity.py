@@ -657,7 +657,7 @@ def test_random_shape_fuzz():
     normwise bar of the f64 product of the kernel's own binary16 weights,
     bit-identical on relaunch (whatever path the timing picks)."""
     rng = np.random.default_rng(20261017)
-    for _ in range(40):
+    for _ in range(int(os.environ.get("LPQT_FUZZ_ITERS", "40"))):
         n = int(rng.choice([128, 256, 384, 640, 1000, 2048, 4224]))
         k = int(rng.choice([128, 256, 520, 1024, 3000, 4096, 8192]))
         m = int(rng.choice([1, 2, 5, 16, 17, 31, 32, 40, 64, 96, 128, 129, 200, 300]))
