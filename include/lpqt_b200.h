@@ -286,6 +286,23 @@ int lpqt_int4_dequantize_blocks(const uint8_t* nibbles, const uint16_t* scales,
                                 const uint16_t* zeros, int64_t N, int64_t K,
                                 int64_t block, double* out, void* stream);
 
+/* W4A16 comparator GEMM: INT4 tiles (lpqt_int4_tiles_bytes(N, K) bytes,
+ * lpqt_int4_prepack of the nibble payload), per-block f16 scales and zero
+ * points (block <= 0 or >= K: one per row, else a multiple of 128); the
+ * binary16 weight Z + S * level is rebuilt in registers and runs the same
+ * tcgen05 pipeline as the FP6 GEMM (flags: LPQT_LAUNCH_PDL,
+ * LPQT_SCHED_STREAMK). */
+int64_t lpqt_int4_tiles_bytes(int64_t N, int64_t K);
+int lpqt_int4_prepack(const uint8_t* nibbles, int64_t N, int64_t K,
+                      uint8_t* tiles, void* stream);
+int lpqt_w4a16_linear_blocks(const uint8_t* tiles, const uint16_t* scales,
+                             const uint16_t* zeros, int64_t block,
+                             const uint16_t* Xt, int64_t ldx, int64_t M,
+                             int64_t N, int64_t K, void* Y, int y_dtype,
+                             int y_layout, int64_t ldy, int split_k,
+                             void* workspace, int64_t workspace_bytes,
+                             int flags, void* stream);
+
 /* Number of kernel launches performed by this library since load (for the
  * bench's gpu_launches claim). */
 int64_t lpqt_launch_count(void);

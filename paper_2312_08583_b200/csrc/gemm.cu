@@ -103,7 +103,26 @@ struct GemmArgs {
 // binary16 dequant of dequant.py:72-79), the epilogue applies none.
 struct FgqArgs {
   int bpr, bkt, bkt_shift;  // bkt_shift >= 0: bkt == 1 << bkt_shift
+  const uint16_t* zeros;    // INT4: per-block zero points (same indexing as the scales)
 };
+// INT4 rebuild, 64 weights (8 words; nibble p of word w holds weight
+// 8w + 2(p & 3) + (p >> 2)): OR the nibble pair into the mantissa of
+// binary16 1024 (exact 1024 + level), subtract 1024 (exact), then
+// level * S + Z with one binary16 rounding (HFMA2).
+__device__ __forceinline__ void int4x64_to_f16(const uint32_t (&w)[12], uint32_t (&r)[32], uint32_t s2, uint32_t z2) {
+  const __half2 k1024 = __halves2half2(__ushort_as_half(0x6400u), __ushort_as_half(0x6400u));
+  const __half2 S = *reinterpret_cast<const __half2*>(&s2), Z = *reinterpret_cast<const __half2*>(&z2);
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+#pragma unroll
+    for (int p = 0; p < 4; ++p) {
+      const uint32_t h = lop3_sel(w[i] >> (4 * p), 0x64006400u, 0x000F000Fu);  // (w >> 4p) & 0x000F000F | 0x64006400
+      const __half2 lv = __hsub2(*reinterpret_cast<const __half2*>(&h), k1024);
+      const __half2 v = __hfma2(lv, S, Z);
+      r[4 * i + p] = *reinterpret_cast<const uint32_t*>(&v);
+    }
+  }
+}
 __device__ __forceinline__ void scale_f16x2(uint32_t (&r)[32], uint32_t s2) {
 #pragma unroll
   for (int j = 0; j < 32; ++j) {
@@ -123,11 +142,16 @@ struct L2Prefetch {
   uint32_t chunk;
 };
 
-template <int BN, bool CSK>
+// WB: weight bits, 6 (FP6 e3m2 tiles, 12288 B) or 4 (INT4 tiles, 8192 B:
+// [k-half 2][quad 2][row 128][16 B], nibbles pre-permuted for the
+// magic-number rebuild; the INT4 comparator of SURVEY §8 f4)
+template <int BN, bool CSK, int WB = 6>
 struct Cfg {
+  static constexpr int kTileB = WB == 6 ? kTileBytes : kTileN * kTileK / 2;
+  static constexpr int kQuads = WB == 6 ? 3 : 2;             // 16-B quads per (row, k-half)
   static constexpr int kKStep = BN <= 32 ? 2 : 1;           // 128-k tiles per pipeline stage
   static constexpr int kXTileBytes = BN * kTileK * 2;       // X for one tile: two SW128 blocks
-  static constexpr int kWStageBytes = kKStep * kTileBytes;
+  static constexpr int kWStageBytes = kKStep * kTileB;
   static constexpr int kXStageBytes = kKStep * kXTileBytes;
   // prefill (BN = 256): an X stage is 64 KB and covers ~1000 MMA cycles, so
   // three stages keep the L2 latency of X hidden (2 W stages of 12 KB suffice)
@@ -507,12 +531,13 @@ __device__ __forceinline__ void ystage_put(const GemmArgs& a, uint32_t buf, int 
 // RAGGED: some stage holds fewer than kKStep tiles (the last k-step of a
 // tile when k_tiles % kKStep != 0, or an odd cluster split-K k-range); only
 // then do the dequant warps walk the stage sequence to learn tile counts.
-template <int BN, bool CSK, bool RAGGED, bool FGQ = false>
+template <int BN, bool CSK, bool RAGGED, bool FGQ = false, int WB = 6>
 __global__ void __launch_bounds__(kThreads, 1)
     w6a16_tcgen05_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constant__ CUtensorMap tmap_y,
                          const GemmArgs a, const L2Prefetch pf, const FgqArgs fg) {
   static_assert(!FGQ || (RAGGED && !CSK), "FGQ walks the stage sequence (RAGGED) and uses no cluster split");
-  using C = Cfg<BN, CSK>;
+  static_assert(WB == 6 || FGQ, "INT4 weights carry per-block scales and zero points (FGQ path)");
+  using C = Cfg<BN, CSK, WB>;
   constexpr int KS = C::kKStep;
   // barrier waits: decode (BN <= 32) parks in the hardware try_wait (woken on
   // the phase flip); prefill re-polls every LPQT_WAIT_HINT_NS (measured,
@@ -638,8 +663,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (is_w) {
         const int s = i % C::kWStages;
         mbar_wait<WM>(&empty_w[s], ((i / C::kWStages) & 1) ^ 1);
-        const uint8_t* src = a.tiles + ((int64_t)n_tile * a.k_tiles + kt) * kTileBytes;
-        const uint32_t bytes = static_cast<uint32_t>(nt * kTileBytes);
+        const uint8_t* src = a.tiles + ((int64_t)n_tile * a.k_tiles + kt) * C::kTileB;
+        const uint32_t bytes = static_cast<uint32_t>(nt * C::kTileB);
         const uint32_t e = elect_one();
         mbar_arrive_expect_tx_if(e, &full_w[s], bytes);
         bulk_g2s_if(e, smem_w + s * C::kWStageBytes, src, bytes, &full_w[s], pol);
@@ -692,8 +717,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     constexpr int kSegs = KS == 2 ? 2 : 1;
     const int lg = warp & 3, grp = warp >> 3, tl = (warp >> 2) & 1;
     const int row = lg * 32 + lane;
-    const uint32_t w_src = smem_u32(smem_w) + static_cast<uint32_t>(row * 16 + (KS == 2 ? tl * kTileBytes
-                                                                                         : tl * 3 * kTileN * 16));
+    const uint32_t w_src = smem_u32(smem_w) + static_cast<uint32_t>(row * 16 + (KS == 2 ? tl * C::kTileB
+                                                                                         : tl * C::kQuads * kTileN * 16));
     const uint32_t t_lane = tmem_base + (static_cast<uint32_t>(lg * 32) << 16) +
                             static_cast<uint32_t>(KS == 2 ? tl * kAColsPerBuf : tl * 32);
     const uint32_t fw0 = smem_u32(full_w), ew0 = smem_u32(empty_w);
@@ -723,6 +748,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     };
     uint32_t q[kSegs][6 * 2];
     uint32_t fs2 = 0;  // FGQ: this stage's block scale as f16x2
+    uint32_t fz2 = 0;  // INT4: this stage's block zero point as f16x2
     auto load_words = [&](int nt) {
       if constexpr (FGQ) {
         int n_tile, m_tile;
@@ -732,16 +758,24 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int blk = fg.bkt_shift >= 0 ? (kt >> fg.bkt_shift) : kt / fg.bkt;
         const uint16_t sb = n < a.N ? __ldg(a.scales + (int64_t)n * fg.bpr + blk) : static_cast<uint16_t>(0);
         fs2 = static_cast<uint32_t>(sb) * 0x10001u;
+        if constexpr (WB == 4) {
+          const uint16_t zb = n < a.N ? __ldg(fg.zeros + (int64_t)n * fg.bpr + blk) : static_cast<uint16_t>(0);
+          fz2 = static_cast<uint32_t>(zb) * 0x10001u;
+        }
       }
       mbar_wait_u32<WM>(fw0 + 8 * wc.idx, wc.ph);
       if (KS == 1 || tl < nt) {
         const uint32_t src = w_src + wc.idx * C::kWStageBytes;
 #pragma unroll
         for (int h = 0; h < kSegs; ++h) {
-          const uint32_t sh = src + h * 3 * kTileN * 16;
-          const uint4 v0 = lds128_u32(sh), v1 = lds128_u32(sh + kTileN * 16), v2 = lds128_u32(sh + 2 * kTileN * 16);
+          const uint32_t sh = src + h * C::kQuads * kTileN * 16;
+          const uint4 v0 = lds128_u32(sh), v1 = lds128_u32(sh + kTileN * 16);
           q[h][0] = v0.x; q[h][1] = v0.y; q[h][2] = v0.z; q[h][3] = v0.w; q[h][4] = v1.x; q[h][5] = v1.y;
-          q[h][6] = v1.z; q[h][7] = v1.w; q[h][8] = v2.x; q[h][9] = v2.y; q[h][10] = v2.z; q[h][11] = v2.w;
+          q[h][6] = v1.z; q[h][7] = v1.w;
+          if constexpr (WB == 6) {
+            const uint4 v2 = lds128_u32(sh + 2 * kTileN * 16);
+            q[h][8] = v2.x; q[h][9] = v2.y; q[h][10] = v2.z; q[h][11] = v2.w;
+          }
         }
       }
     };
@@ -757,9 +791,13 @@ __global__ void __launch_bounds__(kThreads, 1)
       const bool act = KS == 1 || tl < nt_cur;
       uint32_t r[32];
       if (act) {
-        fp6x32_cvt_f16x32_fma(q[0], r, sm);
-        fp6x32_cvt_f16x32_fma(q[0] + 6, r + 16, sm);
-        if constexpr (FGQ) scale_f16x2(r, fs2);
+        if constexpr (WB == 4) {
+          int4x64_to_f16(q[0], r, fs2, fz2);
+        } else {
+          fp6x32_cvt_f16x32_fma(q[0], r, sm);
+          fp6x32_cvt_f16x32_fma(q[0] + 6, r + 16, sm);
+          if constexpr (FGQ) scale_f16x2(r, fs2);
+        }
       }
       mbar_wait_u32<WM>(ae0 + 8 * ac.idx, ac.ph ^ 1u);
       tc_fence_after();
@@ -768,9 +806,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         tmem_st_x32(ta, r);
 #pragma unroll
         for (int h = 1; h < kSegs; ++h) {
-          fp6x32_cvt_f16x32_fma(q[h], r, sm);
-          fp6x32_cvt_f16x32_fma(q[h] + 6, r + 16, sm);
-          if constexpr (FGQ) scale_f16x2(r, fs2);
+          if constexpr (WB == 4) {
+            int4x64_to_f16(q[h], r, fs2, fz2);
+          } else {
+            fp6x32_cvt_f16x32_fma(q[h], r, sm);
+            fp6x32_cvt_f16x32_fma(q[h] + 6, r + 16, sm);
+            if constexpr (FGQ) scale_f16x2(r, fs2);
+          }
           tmem_st_x32(ta + h * 32, r);
         }
       }
@@ -1426,6 +1468,7 @@ struct Plan {
   bool dp;      // prefill: whole tiles round-robin (SkSched DP mode)
   int cluster;  // CSK cluster size
   int splits;   // max CTAs contributing to one tile
+  int64_t K;    // X's k extent: TMA zero-fills columns K .. ldx (W4A16 pads with Z, not 0)
 };
 
 // Prefill MMA N (M > 128).  192 keeps two accumulators in TMEM (the epilogue
@@ -1510,6 +1553,7 @@ static Plan make_plan(int64_t M, int64_t N, int64_t K, int split_k, int flags, i
   p.bn = pick_bn(M);
   p.n_tiles = static_cast<int>((N + kTileN - 1) / kTileN);
   p.m_tiles = static_cast<int>((M + p.bn - 1) / p.bn);
+  p.K = K;
   p.k_tiles = static_cast<int>((K + kTileK - 1) / kTileK);
   p.tiles = (int64_t)p.n_tiles * p.m_tiles;
   // ---- schedule choice (decode, BN <= 32, may use cluster split-K)
@@ -1639,14 +1683,14 @@ static int g_trace_n = 0;  // launches traced so far
 static int trace_next_slot() { return g_trace_n++ % kTraceSlots; }
 #endif
 
-template <int BN, bool CSK, bool RAGGED, bool FGQ = false>
+template <int BN, bool CSK, bool RAGGED, bool FGQ = false, int WB = 6>
 static int launch_impl(const Plan& p, const GemmArgs& args, const L2Prefetch& pf, const FgqArgs& fg,
                        const uint16_t* Xt, int64_t ldx,
                        int64_t M, cudaStream_t stream, int flags) {
   EncodeTiledFn enc = encode_fn();
   if (!enc) return LPQT_E_CUDA;
   CUtensorMap map;
-  const cuuint64_t dims[2] = {static_cast<cuuint64_t>(ldx), static_cast<cuuint64_t>(M)};
+  const cuuint64_t dims[2] = {static_cast<cuuint64_t>(p.K), static_cast<cuuint64_t>(M)};
   const cuuint64_t strides[1] = {static_cast<cuuint64_t>(ldx) * 2};
   const cuuint32_t box[2] = {64, static_cast<cuuint32_t>(BN)};
   const cuuint32_t estr[2] = {1, 1};
@@ -1654,8 +1698,8 @@ static int launch_impl(const Plan& p, const GemmArgs& args, const L2Prefetch& pf
           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
     return LPQT_E_INVALID_INPUT;
-  auto kern = w6a16_tcgen05_kernel<BN, CSK, RAGGED, FGQ>;
-  constexpr int smem = Cfg<BN, CSK>::kSmemBytes;
+  auto kern = w6a16_tcgen05_kernel<BN, CSK, RAGGED, FGQ, WB>;
+  constexpr int smem = Cfg<BN, CSK, WB>::kSmemBytes;
   static std::once_flag once;
   static cudaError_t attr_err = cudaSuccess;
   std::call_once(once, [&] {
@@ -1690,7 +1734,7 @@ static int launch_impl(const Plan& p, const GemmArgs& args, const L2Prefetch& pf
   CUtensorMap ymap;
   memset(&ymap, 0, sizeof(ymap));
   a2.y_tma = 0;
-  if (Cfg<BN, CSK>::kYBufBytes > 0) {
+  if (Cfg<BN, CSK, WB>::kYBufBytes > 0) {
     const int es = args.y_dtype == LPQT_F32 ? 4 : 2;
     const CUtensorMapDataType dt = args.y_dtype == LPQT_F32   ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32
                                    : args.y_dtype == LPQT_F16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16
@@ -1894,6 +1938,69 @@ int lpqt_w6a16_linear_blocks(const uint8_t* tiles, const uint16_t* scales, int64
     case 128: return launch_impl<128, false, false>(p, args, pfa, fga, Xt, ldx, M, st, flags);
     case 192: return launch_impl<192, false, false>(p, args, pfa, fga, Xt, ldx, M, st, flags);
     default: return launch_impl<256, false, false>(p, args, pfa, fga, Xt, ldx, M, st, flags);
+  }
+}
+
+
+// W4A16 (the INT4 comparator): INT4 tiles (lpqt_int4_prepack),
+// per-block f16 scales and zero points (block <= 0 or >= K: one per row; else
+// a multiple of 128), the rebuilt binary16 weight = Z + S * level feeds the same
+// tcgen05 pipeline (stream-K / round-robin schedules).
+int lpqt_w4a16_linear_blocks(const uint8_t* tiles, const uint16_t* scales, const uint16_t* zeros, int64_t block,
+                             const uint16_t* Xt, int64_t ldx, int64_t M, int64_t N, int64_t K, void* Y, int y_dtype,
+                             int y_layout, int64_t ldy, int split_k, void* workspace, int64_t workspace_bytes,
+                             int flags, void* stream) {
+  if (flags & ~(LPQT_LAUNCH_PDL | LPQT_SCHED_STREAMK)) return LPQT_E_INVALID_INPUT;
+  if (M < 0 || N < 0 || K < 0) return LPQT_E_SHAPE;
+  if (M == 0 || N == 0) return LPQT_OK;
+  if (K == 0) return LPQT_E_SHAPE;
+  if (ldx < K || ldx % 8 != 0 || (reinterpret_cast<uintptr_t>(Xt) & 15)) return LPQT_E_SHAPE;
+  if (y_dtype != LPQT_F32 && y_dtype != LPQT_F16 && y_dtype != LPQT_BF16) return LPQT_E_UNSUPPORTED;
+  if (y_layout != LPQT_Y_NM && y_layout != LPQT_Y_MN) return LPQT_E_UNSUPPORTED;
+  if (y_layout == LPQT_Y_NM ? ldy < M : ldy < N) return LPQT_E_SHAPE;
+  if (split_k < 0 || zeros == nullptr) return LPQT_E_INVALID_INPUT;
+  if (N > (int64_t)1 << 30 || M > (int64_t)1 << 30 || K > (int64_t)1 << 30) return LPQT_E_SHAPE;
+  const bool per_row = block <= 0 || block >= K;
+  if (!per_row && block % kTileK != 0) return LPQT_E_UNSUPPORTED;
+  const Plan p = make_plan(M, N, K, split_k, flags, num_sms(), true);
+  if (p.ws_bytes > 0 && (workspace == nullptr || workspace_bytes < p.ws_bytes)) return LPQT_E_WORKSPACE;
+  FgqArgs fga{};
+  fga.bpr = per_row ? 1 : static_cast<int>((K + block - 1) / block);
+  fga.bkt = per_row ? p.k_tiles : static_cast<int>(block / kTileK);
+  fga.bkt_shift = (fga.bkt & (fga.bkt - 1)) == 0 ? __builtin_ctz(static_cast<unsigned>(fga.bkt)) : -1;
+  fga.zeros = zeros;
+  GemmArgs args{};
+  L2Prefetch pfa{};
+#ifdef LPQT_TRACE
+  args.trace = trace_buffer() + (size_t)trace_next_slot() * kTraceLen;
+#endif
+  args.tiles = tiles;
+  args.scales = scales;
+  args.y = Y;
+  args.counters = static_cast<int*>(workspace);
+  args.partials = reinterpret_cast<float*>(static_cast<uint8_t*>(workspace) + p.counters_bytes);
+  args.ldy = ldy;
+  args.total = p.total;
+  args.M = static_cast<int>(M);
+  args.N = static_cast<int>(N);
+  args.k_tiles = p.k_tiles;
+  args.ksteps = p.ksteps;
+  args.n_tiles = p.n_tiles;
+  args.m_tiles = p.m_tiles;
+  args.tile_count = static_cast<int>(p.tiles);
+  args.n_fastest = (p.m_tiles > 1 && M * K * 2 > (int64_t)40 << 20) ? 1 : 0;
+  args.dp = p.dp ? 1 : 0;
+  args.y_dtype = y_dtype;
+  args.y_layout = y_layout;
+  args.sm = ShiftMuls{1u << 26, 1u << 28, 1u << 30};
+  cudaStream_t st = as_stream(stream);
+  switch (p.bn) {
+    case 16: return launch_impl<16, false, true, true, 4>(p, args, pfa, fga, Xt, ldx, M, st, flags);
+    case 32: return launch_impl<32, false, true, true, 4>(p, args, pfa, fga, Xt, ldx, M, st, flags);
+    case 64: return launch_impl<64, false, true, true, 4>(p, args, pfa, fga, Xt, ldx, M, st, flags);
+    case 128: return launch_impl<128, false, true, true, 4>(p, args, pfa, fga, Xt, ldx, M, st, flags);
+    case 192: return launch_impl<192, false, true, true, 4>(p, args, pfa, fga, Xt, ldx, M, st, flags);
+    default: return LPQT_E_UNSUPPORTED;
   }
 }
 

@@ -114,6 +114,34 @@ __global__ void prepack_fp5_kernel(const uint8_t* __restrict__ seg4, const uint8
   }
 }
 
+
+// INT4 nibbles (row-major, two per byte, packing.py:121-129) -> INT4 tiles:
+// 128 x 128 tiles of 8192 B, [k-half 2][quad 2][row 128][16 B]; word w of a
+// (row, k-half) holds weights 8w .. 8w + 7 with weight 8w + j in nibble
+// (j >> 1) + 4 (j & 1), the order the magic-number rebuild produces pairs in.
+__global__ void prepack_int4_kernel(const uint8_t* __restrict__ nib, int64_t N, int64_t K, int64_t Np, int64_t Kp,
+                                    uint8_t* __restrict__ tiles) {
+  const int64_t words = Kp / 8, total = Np * words, k_tiles = Kp / kTileK;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t n = t / words, w8 = t % words;
+    uint32_t word = 0;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int64_t k = w8 * 8 + j;
+      uint32_t lv = 0;
+      if (n < N && k < K) {
+        const int64_t i = n * K + k;
+        lv = (nib[i >> 1] >> (4 * (i & 1))) & 15u;
+      }
+      word |= lv << (4 * ((j >> 1) + 4 * (j & 1)));
+    }
+    const int64_t kt = w8 / 16, rr = n % kTileN, rt = n / kTileN;
+    const int wi = static_cast<int>(w8 % 16), khalf = wi / 8, quad = (wi % 8) / 4, wq = wi % 4;
+    const int64_t off = (rt * k_tiles + kt) * (kTileN * kTileK / 2) + ((int64_t)(khalf * 2 + quad) * kTileN + rr) * 16 + wq * 4;
+    *reinterpret_cast<uint32_t*>(tiles + off) = word;
+  }
+}
+
 }  // namespace lpqt
 
 using namespace lpqt;
@@ -168,6 +196,21 @@ int lpqt_fp5_prepack(const uint8_t* seg4, const uint8_t* seg1, int64_t N, int64_
   if (N == 0 || K == 0) return LPQT_OK;
   const int64_t Np = round_up(N, kTileN), Kp = round_up(K, kTileK);
   prepack_fp5_kernel<<<grid_for(Np * (Kp / 32), 256), 256, 0, as_stream(stream)>>>(seg4, seg1, N, K, Np, Kp, tiles);
+  note_launch();
+  return check_launch();
+}
+
+
+int64_t lpqt_int4_tiles_bytes(int64_t N, int64_t K) {
+  if (N <= 0 || K <= 0) return 0;
+  return round_up(N, kTileN) / kTileN * (round_up(K, kTileK) / kTileK) * (kTileN * kTileK / 2);
+}
+
+int lpqt_int4_prepack(const uint8_t* nibbles, int64_t N, int64_t K, uint8_t* tiles, void* stream) {
+  if (N < 0 || K < 0) return LPQT_E_SHAPE;
+  if (N == 0 || K == 0) return LPQT_OK;
+  const int64_t Np = round_up(N, kTileN), Kp = round_up(K, kTileK);
+  prepack_int4_kernel<<<grid_for(Np * (Kp / 8), 256), 256, 0, as_stream(stream)>>>(nibbles, N, K, Np, Kp, tiles);
   note_launch();
   return check_launch();
 }

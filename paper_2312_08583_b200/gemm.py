@@ -17,7 +17,7 @@ import numpy as np
 
 from . import _lib
 from .errors import PayloadMismatch, ShapeError
-from .linear import Fp6Weight, gemm_nm, stage_activations
+from .linear import Fp6Weight, Int4Weight, gemm_nm, stage_activations
 from .quantizer import (ErrorReport, QuantizedTensor, TensorFormat, _require_gemm_path, dequantize_tensor,
                         error_report, num_blocks)
 
@@ -30,8 +30,10 @@ def _check_activation(X, k: int) -> None:
 
 
 def gemm_quantized(wq: QuantizedTensor, X, split_k: int = 0, sched: str = "auto"):
-    """Y = W_hat @ X for an FP6 tensor (N x K; CGQ, or FGQ with blocks of
-    whole 128-k tiles) and X (K x M) -> f32 (N x M).
+    """Y = W_hat @ X for an FP6 / FP5 / INT4 tensor (N x K; CGQ, or FGQ with
+    blocks of whole 128-k tiles) and X (K x M) -> f32 (N x M).  INT4 runs the
+    W4A16 variant of the kernel: W_hat = Z + S * level rebuilt in binary16
+    (one rounding; the reference sums S * sum(level x) + Z * sum(x) in fp32).
 
     `split_k` / `sched` are B200 tuning hooks (default: automatic schedule);
     the result is the same up to fp32 summation order (FGQ: the block scale
@@ -39,9 +41,13 @@ def gemm_quantized(wq: QuantizedTensor, X, split_k: int = 0, sched: str = "auto"
     the fp32 block partial)."""
     if wq.num_blocks != num_blocks(wq.rows, wq.cols, wq.scheme):
         raise PayloadMismatch("block parameter count does not match the scheme")
-    if wq.scheme.fmt is TensorFormat.INT4_ASYM:
-        return _gemm_int4_comparator(wq, X)
-    _require_gemm_path(wq.scheme, wq.cols)
+    int4 = wq.scheme.fmt is TensorFormat.INT4_ASYM
+    if int4:
+        b = wq.scheme.block_size if wq.scheme.granularity.name == "FGQ" else 0
+        if b and b < wq.cols and b % 128:
+            return _gemm_int4_comparator(wq, X)
+    else:
+        _require_gemm_path(wq.scheme, wq.cols)
     torch_in = _lib.is_torch(X)
     Xa = X if torch_in else np.asarray(X)
     _check_activation(Xa, wq.cols)
@@ -51,7 +57,7 @@ def gemm_quantized(wq: QuantizedTensor, X, split_k: int = 0, sched: str = "auto"
         if torch_in:
             return t.zeros((n, m), dtype=t.float32, device=_lib.device())
         return np.zeros((n, m), dtype=np.float32)
-    weight = Fp6Weight.from_quantized(wq)
+    weight = Int4Weight.from_quantized(wq) if int4 else Fp6Weight.from_quantized(wq)
     xt, kp = stage_activations(Xa, k)
     y = gemm_nm(weight, xt, kp, m, split_k=split_k, sched=sched)
     return y if torch_in else y.cpu().numpy()
@@ -75,10 +81,10 @@ def _dense(W, X, dtype):
 
 
 def _gemm_int4_comparator(wq: QuantizedTensor, X):
-    """INT4 (the paper's comparator format): the GPU dequantizes
-    (Z + S * level, exact f64) and a library fp32 GEMM multiplies — the
-    reference's dequantize-then-matmul comparator (gemm.py:84-110 INT4 terms),
-    not a fused W4A16 kernel."""
+    """INT4 with FGQ blocks that are not whole 128-k tiles: the GPU
+    dequantizes (Z + S * level, exact f64) and a library fp32 GEMM multiplies
+    (gemm.py:84-110 INT4 terms).  CGQ and tile-aligned FGQ INT4 run the fused
+    W4A16 tcgen05 kernel (`Int4Weight`)."""
     torch_in = _lib.is_torch(X)
     Xa = X if torch_in else np.asarray(X)
     _check_activation(Xa, wq.cols)

@@ -132,6 +132,61 @@ class Fp6Weight:
         return out
 
 
+class Int4Weight:
+    """An N x K INT4 asymmetric weight (the paper's comparator format,
+    quantizer.py:232-244) in the W4A16 tile layout (128 x 128 tiles of 8192 B,
+    `lpqt_int4_prepack`) with f16 scales and zero points per row (CGQ) or per
+    block of `block` columns (FGQ, a multiple of 128).  The GEMM rebuilds
+    Z + S * level in binary16 and runs the FP6 kernel's tcgen05 pipeline."""
+
+    static = True
+
+    def __init__(self, tiles, scales, zeros, n: int, k: int, block: int = 0):
+        self.tiles = tiles
+        self.scales = scales
+        self.zeros = zeros
+        self.n = int(n)
+        self.k = int(k)
+        self.block = int(block) if block and int(block) < int(k) else 0
+
+    @classmethod
+    def from_quantized(cls, q) -> "Int4Weight":
+        from .errors import InvalidScheme, PayloadMismatch
+        from .quantizer import scale_block
+        block = scale_block(q.scheme)
+        if block and block < q.cols and block % TILE:
+            raise InvalidScheme(f"FGQ block_size {block} is not a multiple of 128: outside the B200 GEMM path")
+        cache = q.device_cache
+        if cache is not None and "weight" in cache:
+            return cache["weight"]
+        t = _lib.torch()
+        nib = _lib.to_device(q.payload if _lib.is_torch(q.payload) else np.asarray(q.payload, np.uint8))
+        nib = nib.reshape(-1).to(t.uint8)
+        if nib.numel() != (q.rows * q.cols + 1) // 2:
+            raise PayloadMismatch("payload does not hold rows*cols levels")
+
+        def f16(a):
+            return _lib.to_device(a if _lib.is_torch(a) else np.asarray(a, np.float16)).reshape(-1).to(t.float16)
+
+        lib = _lib.load()
+        tiles = t.empty(int(lib.lpqt_int4_tiles_bytes(q.rows, q.cols)), dtype=t.uint8, device=nib.device)
+        _lib.check(lib.lpqt_int4_prepack(nib.data_ptr(), q.rows, q.cols, tiles.data_ptr(), _lib.stream_ptr()),
+                   "int4_prepack")
+        t.cuda.current_stream().synchronize()
+        w = cls(tiles, f16(q.scales), f16(q.zero_points), q.rows, q.cols, block)
+        if cache is not None:
+            cache["weight"] = w
+        return w
+
+    @property
+    def nbytes(self) -> int:
+        return int(self.tiles.numel() + 2 * self.scales.numel() + 2 * self.zeros.numel())
+
+    def stream_bytes(self) -> int:
+        """Algorithmic weight bytes per GEMM: 0.5 B/weight + 4 B per block."""
+        return (self.n * self.k + 1) // 2 + 4 * int(self.scales.numel())
+
+
 _SCHED_FLAGS = {"auto": 0, "streamk": 2, "cluster": 4}
 
 
@@ -157,6 +212,14 @@ def _launch(weight: Fp6Weight, xt, ldx: int, m: int, y, y_dtype: int, y_layout: 
     ws_bytes = int(lib.lpqt_w6a16_workspace_bytes(m, weight.n, weight.k, split_k))
     ws = _lib.Workspace.get(ws_bytes) if ws_bytes else None
     flags = (_lib.LAUNCH_PDL if weight.static else 0) | _sched_flags(sched)
+    if isinstance(weight, Int4Weight):
+        if sched == "cluster":
+            raise ValueError("the W4A16 GEMM runs the stream-K / round-robin schedules only")
+        _lib.check(lib.lpqt_w4a16_linear_blocks(
+            weight.tiles.data_ptr(), weight.scales.data_ptr(), weight.zeros.data_ptr(), weight.block, xt.data_ptr(),
+            ldx, m, weight.n, weight.k, y.data_ptr(), y_dtype, y_layout, ldy, split_k, _lib.ptr(ws),
+            ws.numel() if ws is not None else 0, flags, _lib.stream_ptr()), "w4a16_linear")
+        return
     nxt = None
     if prefetch is not None:
         # the next launch is assumed to use the same batch and the automatic schedule

@@ -652,6 +652,34 @@ def test_int4_quantize_pack_dequant_gemm_vs_reference():
         L.quantize_tensor(np.ones((2, 4)), L.QuantScheme(L.Granularity.CGQ, L.TensorFormat.INT4_ASYM), bias_shift=True)
 
 
+@pytest.mark.parametrize("n,k,m,block", [(128, 128, 1, 0), (1000, 3000, 16, 0), (4096, 4096, 16, 128),
+                                         (4224, 1024, 96, 256), (640, 8192, 300, 0), (2048, 2048, 2, 512)])
+def test_w4a16_gemm_vs_oracle(n, k, m, block):
+    """Fused W4A16 tcgen05 GEMM (INT4 tiles, per-row / per-128k-block zero
+    points and scales): within the normwise bar of the reference f64 product,
+    and within 1e-5 of the f64 product of its own binary16 rebuild; ragged
+    N / K, every BN bucket; bit-identical on relaunch."""
+    rng = np.random.default_rng(n * 7 + k + m + block)
+    W = (rng.standard_normal((n, k)) * 0.02 + rng.standard_normal((n, 1)) * 0.01).astype(np.float32)
+    X = rng.standard_normal((k, m)).astype(np.float16)
+    gran = L.Granularity.FGQ if block else L.Granularity.CGQ
+    q = L.quantize_tensor(W, L.QuantScheme(gran, L.TensorFormat.INT4_ASYM, block))
+    o = O.quantize_tensor_int4(W, block)
+    assert np.array_equal(q.payload, o["nibbles"]) and np.array_equal(q.scales.view(np.uint16),
+                                                                        o["scales"].view(np.uint16))
+    Y = L.gemm_quantized(q, X)
+    assert np.array_equal(Y, L.gemm_quantized(q, X))
+    deq = O.dequantize_int4(o["levels"], o["scales"], o["zeros"], n, k, block)
+    assert normwise_rel(Y, deq @ X.astype(np.float64)) <= REL_TOL
+    # the kernel's binary16 weight RN_f16(Z + S * level): one rounding (HFMA2) of the exact f64 value
+    W16 = deq.astype(np.float16).astype(np.float64)
+    assert normwise_rel(Y, W16 @ X.astype(np.float64)) <= 1e-5
+    # torch-facing call with fp16 output through the same weight
+    w = L.Int4Weight.from_quantized(q)
+    y = L.w6a16_linear(torch.from_numpy(X.T.copy()).cuda(), w, out_dtype=torch.float32)
+    assert torch.equal(y.t().cpu(), torch.from_numpy(Y))
+
+
 def test_random_shape_fuzz():
     """Seeded fuzz over shapes / batch / scheme: every launch within the
     normwise bar of the f64 product of the kernel's own binary16 weights,
