@@ -109,17 +109,35 @@ struct FgqArgs {
 // 8w + 2(p & 3) + (p >> 2)): OR the nibble pair into the mantissa of
 // binary16 1024 (exact 1024 + level), subtract 1024 (exact), then
 // level * S + Z with one binary16 rounding (HFMA2).
+// (a & IMM) | c in one LOP3 (IMM the immediate, c a register: LOP3 takes one
+// immediate, so two constant operands would cost a second LOP3)
+template <uint32_t IMM>
+__device__ __forceinline__ uint32_t and_or(uint32_t a, uint32_t c) {
+  uint32_t d;
+  asm("lop3.b32 %0, %1, %2, %3, 0xEA;" : "=r"(d) : "r"(a), "n"(IMM), "r"(c));
+  return d;
+}
+// 64 INT4 levels (8 words, weight 8i + j in nibble (j >> 1) + 4 (j & 1) of
+// word i) -> 32 f16x2 Z + S * level with one rounding (HFMA2 of the exact
+// level).  Nibbles 0/4 and 2/6 OR into 1024.0 (0x6400: ulp 1), nibbles 1/5
+// and 3/7 in place into 64.0 (0x5400: ulp 1/16), so a pair costs one LOP3,
+// one HADD2 (exact: the level) and one HFMA2, plus a shift per two pairs.
 __device__ __forceinline__ void int4x64_to_f16(const uint32_t (&w)[12], uint32_t (&r)[32], uint32_t s2, uint32_t z2) {
+  uint32_t m1024 = 0x64006400u, m64 = 0x54005400u;
+  asm volatile("" : "+r"(m1024), "+r"(m64));  // keep the magic numbers in registers
   const __half2 k1024 = __halves2half2(__ushort_as_half(0x6400u), __ushort_as_half(0x6400u));
+  const __half2 k64 = __halves2half2(__ushort_as_half(0x5400u), __ushort_as_half(0x5400u));
   const __half2 S = *reinterpret_cast<const __half2*>(&s2), Z = *reinterpret_cast<const __half2*>(&z2);
 #pragma unroll
   for (int i = 0; i < 8; ++i) {
 #pragma unroll
-    for (int p = 0; p < 4; ++p) {
-      const uint32_t h = lop3_sel(w[i] >> (4 * p), 0x64006400u, 0x000F000Fu);  // (w >> 4p) & 0x000F000F | 0x64006400
-      const __half2 lv = __hsub2(*reinterpret_cast<const __half2*>(&h), k1024);
-      const __half2 v = __hfma2(lv, S, Z);
-      r[4 * i + p] = *reinterpret_cast<const uint32_t*>(&v);
+    for (int hp = 0; hp < 2; ++hp) {
+      const uint32_t y = w[i] >> (8 * hp);
+      const uint32_t h0 = and_or<0x000F000Fu>(y, m1024), h1 = and_or<0x00F000F0u>(y, m64);
+      const __half2 v0 = __hfma2(__hsub2(*reinterpret_cast<const __half2*>(&h0), k1024), S, Z);
+      const __half2 v1 = __hfma2(__hsub2(*reinterpret_cast<const __half2*>(&h1), k64), S, Z);
+      r[4 * i + 2 * hp] = *reinterpret_cast<const uint32_t*>(&v0);
+      r[4 * i + 2 * hp + 1] = *reinterpret_cast<const uint32_t*>(&v1);
     }
   }
 }
