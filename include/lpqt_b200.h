@@ -59,7 +59,7 @@ extern "C" {
 #define LPQT_Y_MN  1   /* Y[m, n] (torch.nn.Linear layout)                     */
 
 const char* lpqt_strerror(int status);
-int lpqt_abi_version(void);               /* bumps on any signature change (3: _ex, plan_ex) */
+int lpqt_abi_version(void);               /* bumps on any signature change (4: FGQ stage params) */
 
 /* codec.py:116-132 encode_rtn_array: x[n] (dtype) -> codes[n] (u8). */
 int lpqt_fp6_encode_rtn(const void* x, int dtype, int64_t n, uint8_t* codes,
@@ -212,7 +212,10 @@ int lpqt_w6a16_linear_pf(const uint8_t* tiles, const uint16_t* scales,
  * identical to the entries above.  Quantize / dequantize accept any block
  * size; the GEMM takes blocks of whole 128-k tiles (block % 128 == 0, else
  * LPQT_E_UNSUPPORTED) and applies each block's scale to the rebuilt binary16
- * weights before the MMA (the binary16 dequant of dequant.py:72-79). */
+ * weights before the MMA (the binary16 dequant of dequant.py:72-79).
+ * lpqt_w6a16_linear_blocks with 0 < block < K reads `scales` as the
+ * STAGE-ORDERED block scales (lpqt_fgq_stage_params, below), not the
+ * row-major array; with block <= 0 or >= K they are the per-row scales. */
 int lpqt_fp6_quantize_pack_blocks(const void* W, int dtype, int64_t N,
                                   int64_t K, int64_t ldw, int64_t block,
                                   int bias_shift, uint16_t* scales,
@@ -286,22 +289,33 @@ int lpqt_int4_dequantize_blocks(const uint8_t* nibbles, const uint16_t* scales,
                                 const uint16_t* zeros, int64_t N, int64_t K,
                                 int64_t block, double* out, void* stream);
 
+/* FGQ / INT4 block parameters in GEMM stage order: for weight tile (row tile
+ * rt, k tile kt) the 128 rows' f16 scale (with_zeros / INT4: scale | zero
+ * << 16, u32) of the block holding kt.  Built once per weight from the
+ * row-major per-block arrays (block <= 0 or >= K: one per row, else a
+ * multiple of 128); the GEMM's weight producer copies them next to the
+ * weight bytes of each stage.  lpqt_fgq_stage_bytes(N, K, with_zeros) bytes. */
+int64_t lpqt_fgq_stage_bytes(int64_t N, int64_t K, int with_zeros);
+int lpqt_fgq_stage_params(const uint16_t* scales, const uint16_t* zeros,
+                          int64_t N, int64_t K, int64_t block, void* out,
+                          void* stream);
+
 /* W4A16 comparator GEMM: INT4 tiles (lpqt_int4_tiles_bytes(N, K) bytes,
- * lpqt_int4_prepack of the nibble payload), per-block f16 scales and zero
- * points (block <= 0 or >= K: one per row, else a multiple of 128); the
- * binary16 weight Z + S * level is rebuilt in registers and runs the same
- * tcgen05 pipeline as the FP6 GEMM (flags: LPQT_LAUNCH_PDL,
- * LPQT_SCHED_STREAMK). */
+ * lpqt_int4_prepack of the nibble payload) and the stage-ordered scale |
+ * zero words (lpqt_fgq_stage_params with zeros); the binary16 weight
+ * Z + S * level is rebuilt in registers and runs the same tcgen05 pipeline
+ * as the FP6 GEMM (flags: LPQT_LAUNCH_PDL, LPQT_SCHED_STREAMK,
+ * LPQT_SCHED_CLUSTER).  block: the parameters' block size (validated). */
 int64_t lpqt_int4_tiles_bytes(int64_t N, int64_t K);
 int lpqt_int4_prepack(const uint8_t* nibbles, int64_t N, int64_t K,
                       uint8_t* tiles, void* stream);
-int lpqt_w4a16_linear_blocks(const uint8_t* tiles, const uint16_t* scales,
-                             const uint16_t* zeros, int64_t block,
-                             const uint16_t* Xt, int64_t ldx, int64_t M,
-                             int64_t N, int64_t K, void* Y, int y_dtype,
-                             int y_layout, int64_t ldy, int split_k,
-                             void* workspace, int64_t workspace_bytes,
-                             int flags, void* stream);
+int lpqt_w4a16_linear_blocks(const uint8_t* tiles, const uint32_t* params,
+                             int64_t block, const uint16_t* Xt, int64_t ldx,
+                             int64_t M, int64_t N, int64_t K, void* Y,
+                             int y_dtype, int y_layout, int64_t ldy,
+                             int split_k, void* workspace,
+                             int64_t workspace_bytes, int flags,
+                             void* stream);
 
 /* Number of kernel launches performed by this library since load (for the
  * bench's gpu_launches claim). */

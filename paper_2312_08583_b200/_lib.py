@@ -95,8 +95,10 @@ SIGNATURES = {
     "lpqt_int4_dequantize_blocks": (_I32, [_P, _P, _P, _I64, _I64, _I64, _P, _P]),
     "lpqt_int4_tiles_bytes": (_I64, [_I64, _I64]),
     "lpqt_int4_prepack": (_I32, [_P, _I64, _I64, _P, _P]),
-    "lpqt_w4a16_linear_blocks": (_I32, [_P, _P, _P, _I64, _P, _I64, _I64, _I64, _I64, _P, _I32, _I32, _I64, _I32, _P,
+    "lpqt_w4a16_linear_blocks": (_I32, [_P, _P, _I64, _P, _I64, _I64, _I64, _I64, _P, _I32, _I32, _I64, _I32, _P,
                                         _I64, _I32, _P]),
+    "lpqt_fgq_stage_bytes": (_I64, [_I64, _I64, _I32]),
+    "lpqt_fgq_stage_params": (_I32, [_P, _P, _I64, _I64, _I64, _P, _P]),
     "lpqt_launch_count": (_I64, []),
 }
 

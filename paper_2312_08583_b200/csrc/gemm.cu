@@ -97,13 +97,16 @@ struct GemmArgs {
   ShiftMuls sm;       // 2^26, 2^28, 2^30: right shifts on the FMA pipe (common.cuh)
 };
 
-// FGQ (block scales, quantizer.py FGQ x FP6; gemm.py:96-110): scales are one
-// f16 per (row, block of bkt 128-k tiles), bpr per row; the dequant warps
-// multiply each rebuilt f16 weight by its block's scale before the MMA (the
-// binary16 dequant of dequant.py:72-79), the epilogue applies none.
+// FGQ (block scales, quantizer.py FGQ x FP6; gemm.py:96-110) and INT4: the
+// block parameters are re-laid out once per weight in stage order
+// (lpqt_fgq_stage_params): for weight tile (row tile rt, k tile kt), the 128
+// rows' f16 scale (INT4: f16 scale | f16 zero << 16) of the block holding kt,
+// at ((rt * k_tiles) + kt) * kSBytes.  The W producer copies them into the
+// stage next to the weight bytes (same mbarrier), so a dequant thread reads
+// its row's parameter with one LDS; the rebuilt f16 weight carries the block
+// scale (the binary16 dequant of dequant.py:72-79) and the epilogue applies none.
 struct FgqArgs {
-  int bpr, bkt, bkt_shift;  // bkt_shift >= 0: bkt == 1 << bkt_shift
-  const uint16_t* zeros;    // INT4: per-block zero points (same indexing as the scales)
+  const uint8_t* stage;  // stage-ordered block parameters (null: CGQ FP6)
 };
 // INT4 rebuild, 64 weights (8 words; nibble p of word w holds weight
 // 8w + 2(p & 3) + (p >> 2)): OR the nibble pair into the mantissa of
@@ -163,13 +166,15 @@ struct L2Prefetch {
 // WB: weight bits, 6 (FP6 e3m2 tiles, 12288 B) or 4 (INT4 tiles, 8192 B:
 // [k-half 2][quad 2][row 128][16 B], nibbles pre-permuted for the
 // magic-number rebuild; the INT4 comparator of SURVEY §8 f4)
-template <int BN, bool CSK, int WB = 6>
+template <int BN, bool CSK, int WB = 6, bool FGQ = false>
 struct Cfg {
   static constexpr int kTileB = WB == 6 ? kTileBytes : kTileN * kTileK / 2;
+  // FGQ / INT4: a stage carries its tiles' block parameters after the weights
+  static constexpr int kSBytes = FGQ ? kTileN * (WB == 4 ? 4 : 2) : 0;
   static constexpr int kQuads = WB == 6 ? 3 : 2;             // 16-B quads per (row, k-half)
   static constexpr int kKStep = BN <= 32 ? 2 : 1;           // 128-k tiles per pipeline stage
   static constexpr int kXTileBytes = BN * kTileK * 2;       // X for one tile: two SW128 blocks
-  static constexpr int kWStageBytes = kKStep * kTileB;
+  static constexpr int kWStageBytes = kKStep * (kTileB + kSBytes);
   static constexpr int kXStageBytes = kKStep * kXTileBytes;
   // prefill (BN = 256): an X stage is 64 KB and covers ~1000 MMA cycles, so
   // three stages keep the L2 latency of X hidden (2 W stages of 12 KB suffice)
@@ -553,9 +558,8 @@ template <int BN, bool CSK, bool RAGGED, bool FGQ = false, int WB = 6>
 __global__ void __launch_bounds__(kThreads, 1)
     w6a16_tcgen05_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constant__ CUtensorMap tmap_y,
                          const GemmArgs a, const L2Prefetch pf, const FgqArgs fg) {
-  static_assert(!FGQ || (RAGGED && !CSK), "FGQ walks the stage sequence (RAGGED) and uses no cluster split");
   static_assert(WB == 6 || FGQ, "INT4 weights carry per-block scales and zero points (FGQ path)");
-  using C = Cfg<BN, CSK, WB>;
+  using C = Cfg<BN, CSK, WB, FGQ>;
   constexpr int KS = C::kKStep;
   // barrier waits: decode (BN <= 32) parks in the hardware try_wait (woken on
   // the phase flip); prefill re-polls every LPQT_WAIT_HINT_NS (measured,
@@ -684,8 +688,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint8_t* src = a.tiles + ((int64_t)n_tile * a.k_tiles + kt) * C::kTileB;
         const uint32_t bytes = static_cast<uint32_t>(nt * C::kTileB);
         const uint32_t e = elect_one();
-        mbar_arrive_expect_tx_if(e, &full_w[s], bytes);
+        mbar_arrive_expect_tx_if(e, &full_w[s], bytes + static_cast<uint32_t>(nt * C::kSBytes));
         bulk_g2s_if(e, smem_w + s * C::kWStageBytes, src, bytes, &full_w[s], pol);
+        if constexpr (FGQ) {
+          const uint8_t* sp = fg.stage + ((int64_t)n_tile * a.k_tiles + kt) * C::kSBytes;
+          bulk_g2s_if(e, smem_w + s * C::kWStageBytes + KS * C::kTileB, sp, static_cast<uint32_t>(nt * C::kSBytes),
+                      &full_w[s], pol);
+        }
         if (i == 0 && lane == 0) CTA_STAMP(20);
       } else {
         const int s = i % C::kXStages;
@@ -767,22 +776,21 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint32_t q[kSegs][6 * 2];
     uint32_t fs2 = 0;  // FGQ: this stage's block scale as f16x2
     uint32_t fz2 = 0;  // INT4: this stage's block zero point as f16x2
+    // this thread's block parameter in the stage (after the KS weight tiles)
+    const uint32_t s_src = smem_u32(smem_w) + KS * C::kTileB + (KS == 2 ? tl : 0) * C::kSBytes +
+                           row * (WB == 4 ? 4 : 2);
     auto load_words = [&](int nt) {
-      if constexpr (FGQ) {
-        int n_tile, m_tile;
-        tile_nm(a, it.sg.tile, n_tile, m_tile);
-        const int n = n_tile * kTileN + row;
-        const int kt = it.kt() + (KS == 2 ? tl : 0);
-        const int blk = fg.bkt_shift >= 0 ? (kt >> fg.bkt_shift) : kt / fg.bkt;
-        const uint16_t sb = n < a.N ? __ldg(a.scales + (int64_t)n * fg.bpr + blk) : static_cast<uint16_t>(0);
-        fs2 = static_cast<uint32_t>(sb) * 0x10001u;
-        if constexpr (WB == 4) {
-          const uint16_t zb = n < a.N ? __ldg(fg.zeros + (int64_t)n * fg.bpr + blk) : static_cast<uint16_t>(0);
-          fz2 = static_cast<uint32_t>(zb) * 0x10001u;
-        }
-      }
       mbar_wait_u32<WM>(fw0 + 8 * wc.idx, wc.ph);
       if (KS == 1 || tl < nt) {
+        if constexpr (FGQ) {
+          if constexpr (WB == 4) {
+            const uint32_t sz = lds_u32(s_src + wc.idx * C::kWStageBytes);
+            fs2 = __byte_perm(sz, 0u, 0x1010);
+            fz2 = __byte_perm(sz, 0u, 0x3232);
+          } else {
+            fs2 = __byte_perm(lds_u16(s_src + wc.idx * C::kWStageBytes), 0u, 0x1010);
+          }
+        }
         const uint32_t src = w_src + wc.idx * C::kWStageBytes;
 #pragma unroll
         for (int h = 0; h < kSegs; ++h) {
@@ -1575,7 +1583,7 @@ static Plan make_plan(int64_t M, int64_t N, int64_t K, int split_k, int flags, i
   p.k_tiles = static_cast<int>((K + kTileK - 1) / kTileK);
   p.tiles = (int64_t)p.n_tiles * p.m_tiles;
   // ---- schedule choice (decode, BN <= 32, may use cluster split-K)
-  const bool csk_ok = !fgq && p.bn <= 32 && p.tiles < ((int64_t)1 << 30);  // (FGQ: stream-K / round-robin only)
+  const bool csk_ok = p.bn <= 32 && p.tiles < ((int64_t)1 << 30);
   int best_c = 0;
   if (csk_ok && !(flags & LPQT_SCHED_STREAMK)) {
     if (flags & LPQT_SCHED_CLUSTER) {
@@ -1717,7 +1725,7 @@ static int launch_impl(const Plan& p, const GemmArgs& args, const L2Prefetch& pf
           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
     return LPQT_E_INVALID_INPUT;
   auto kern = w6a16_tcgen05_kernel<BN, CSK, RAGGED, FGQ, WB>;
-  constexpr int smem = Cfg<BN, CSK, WB>::kSmemBytes;
+  constexpr int smem = Cfg<BN, CSK, WB, FGQ>::kSmemBytes;
   static std::once_flag once;
   static cudaError_t attr_err = cudaSuccess;
   std::call_once(once, [&] {
@@ -1752,7 +1760,7 @@ static int launch_impl(const Plan& p, const GemmArgs& args, const L2Prefetch& pf
   CUtensorMap ymap;
   memset(&ymap, 0, sizeof(ymap));
   a2.y_tma = 0;
-  if (Cfg<BN, CSK, WB>::kYBufBytes > 0) {
+  if (Cfg<BN, CSK, WB, FGQ>::kYBufBytes > 0) {
     const int es = args.y_dtype == LPQT_F32 ? 4 : 2;
     const CUtensorMapDataType dt = args.y_dtype == LPQT_F32   ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32
                                    : args.y_dtype == LPQT_F16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16
@@ -1777,6 +1785,36 @@ static int launch_impl(const Plan& p, const GemmArgs& args, const L2Prefetch& pf
 }  // namespace lpqt
 
 using namespace lpqt;
+
+// Schedule / stage-shape dispatch shared by the FP6 (CGQ, FGQ) and INT4 entries.
+template <bool FGQ, int WB>
+static int dispatch(const Plan& p, const GemmArgs& args, const L2Prefetch& pfa, const FgqArgs& fga,
+                    const uint16_t* Xt, int64_t ldx, int64_t M, cudaStream_t st, int flags) {
+  bool ragged = p.k_tiles % p.kstep != 0;
+  if (p.csk) {
+    for (int r = 0; r < p.cluster; ++r)  // k-range of rank r must be a whole number of stages
+      ragged |= ((r + 1) * p.k_tiles / p.cluster - r * p.k_tiles / p.cluster) % p.kstep != 0;
+    if (p.bn <= 16)
+      return ragged ? launch_impl<16, true, true, FGQ, WB>(p, args, pfa, fga, Xt, ldx, M, st, flags)
+                    : launch_impl<16, true, false, FGQ, WB>(p, args, pfa, fga, Xt, ldx, M, st, flags);
+    return ragged ? launch_impl<32, true, true, FGQ, WB>(p, args, pfa, fga, Xt, ldx, M, st, flags)
+                  : launch_impl<32, true, false, FGQ, WB>(p, args, pfa, fga, Xt, ldx, M, st, flags);
+  }
+  switch (p.bn) {
+    case 16:
+      return ragged ? launch_impl<16, false, true, FGQ, WB>(p, args, pfa, fga, Xt, ldx, M, st, flags)
+                    : launch_impl<16, false, false, FGQ, WB>(p, args, pfa, fga, Xt, ldx, M, st, flags);
+    case 32:
+      return ragged ? launch_impl<32, false, true, FGQ, WB>(p, args, pfa, fga, Xt, ldx, M, st, flags)
+                    : launch_impl<32, false, false, FGQ, WB>(p, args, pfa, fga, Xt, ldx, M, st, flags);
+    case 64: return launch_impl<64, false, false, FGQ, WB>(p, args, pfa, fga, Xt, ldx, M, st, flags);
+    case 128: return launch_impl<128, false, false, FGQ, WB>(p, args, pfa, fga, Xt, ldx, M, st, flags);
+    case 192: return launch_impl<192, false, false, FGQ, WB>(p, args, pfa, fga, Xt, ldx, M, st, flags);
+    default:
+      if constexpr (FGQ) return LPQT_E_UNSUPPORTED;  // (BN 256 only by LPQT_PREFILL_BN override)
+      else return launch_impl<256, false, false, FGQ, WB>(p, args, pfa, fga, Xt, ldx, M, st, flags);
+  }
+}
 
 extern "C" {
 
@@ -1861,13 +1899,8 @@ int lpqt_w6a16_linear_blocks(const uint8_t* tiles, const uint16_t* scales, int64
   // FGQ: blocks of B columns (B = K, or block <= 0: one scale per row)
   const bool fgq = block > 0 && block < K;
   if (fgq && block % kTileK != 0) return LPQT_E_UNSUPPORTED;   // block scales at 128-k tile granularity
-  if (fgq && (flags & LPQT_SCHED_CLUSTER)) return LPQT_E_UNSUPPORTED;
   FgqArgs fga{};
-  if (fgq) {
-    fga.bpr = static_cast<int>((K + block - 1) / block);
-    fga.bkt = static_cast<int>(block / kTileK);
-    fga.bkt_shift = (fga.bkt & (fga.bkt - 1)) == 0 ? __builtin_ctz(static_cast<unsigned>(fga.bkt)) : -1;
-  }
+  if (fgq) fga.stage = reinterpret_cast<const uint8_t*>(scales);  // stage-ordered (lpqt_fgq_stage_params)
   if ((flags & LPQT_SCHED_STREAMK) && (flags & LPQT_SCHED_CLUSTER)) return LPQT_E_INVALID_INPUT;
   if (M < 0 || N < 0 || K < 0) return LPQT_E_SHAPE;
   if (M == 0 || N == 0) return LPQT_OK;
@@ -1925,38 +1958,8 @@ int lpqt_w6a16_linear_blocks(const uint8_t* tiles, const uint16_t* scales, int64
     }
   }
   cudaStream_t st = as_stream(stream);
-  if (fgq) {  // the dequant warps walk the stage sequence for the block scales (RAGGED instantiation)
-    switch (p.bn) {
-      case 16: return launch_impl<16, false, true, true>(p, args, pfa, fga, Xt, ldx, M, st, flags);
-      case 32: return launch_impl<32, false, true, true>(p, args, pfa, fga, Xt, ldx, M, st, flags);
-      case 64: return launch_impl<64, false, true, true>(p, args, pfa, fga, Xt, ldx, M, st, flags);
-      case 128: return launch_impl<128, false, true, true>(p, args, pfa, fga, Xt, ldx, M, st, flags);
-      case 192: return launch_impl<192, false, true, true>(p, args, pfa, fga, Xt, ldx, M, st, flags);
-      default: return LPQT_E_UNSUPPORTED;
-    }
-  }
-  bool ragged = p.k_tiles % p.kstep != 0;
-  if (p.csk) {
-    for (int r = 0; r < p.cluster; ++r)  // k-range of rank r must be a whole number of stages
-      ragged |= ((r + 1) * p.k_tiles / p.cluster - r * p.k_tiles / p.cluster) % p.kstep != 0;
-    if (p.bn <= 16)
-      return ragged ? launch_impl<16, true, true>(p, args, pfa, fga, Xt, ldx, M, st, flags)
-                    : launch_impl<16, true, false>(p, args, pfa, fga, Xt, ldx, M, st, flags);
-    return ragged ? launch_impl<32, true, true>(p, args, pfa, fga, Xt, ldx, M, st, flags)
-                  : launch_impl<32, true, false>(p, args, pfa, fga, Xt, ldx, M, st, flags);
-  }
-  switch (p.bn) {
-    case 16:
-      return ragged ? launch_impl<16, false, true>(p, args, pfa, fga, Xt, ldx, M, st, flags)
-                    : launch_impl<16, false, false>(p, args, pfa, fga, Xt, ldx, M, st, flags);
-    case 32:
-      return ragged ? launch_impl<32, false, true>(p, args, pfa, fga, Xt, ldx, M, st, flags)
-                    : launch_impl<32, false, false>(p, args, pfa, fga, Xt, ldx, M, st, flags);
-    case 64: return launch_impl<64, false, false>(p, args, pfa, fga, Xt, ldx, M, st, flags);
-    case 128: return launch_impl<128, false, false>(p, args, pfa, fga, Xt, ldx, M, st, flags);
-    case 192: return launch_impl<192, false, false>(p, args, pfa, fga, Xt, ldx, M, st, flags);
-    default: return launch_impl<256, false, false>(p, args, pfa, fga, Xt, ldx, M, st, flags);
-  }
+  return fgq ? dispatch<true, 6>(p, args, pfa, fga, Xt, ldx, M, st, flags)
+             : dispatch<false, 6>(p, args, pfa, fga, Xt, ldx, M, st, flags);
 }
 
 
@@ -1964,11 +1967,11 @@ int lpqt_w6a16_linear_blocks(const uint8_t* tiles, const uint16_t* scales, int64
 // per-block f16 scales and zero points (block <= 0 or >= K: one per row; else
 // a multiple of 128), the rebuilt binary16 weight = Z + S * level feeds the same
 // tcgen05 pipeline (stream-K / round-robin schedules).
-int lpqt_w4a16_linear_blocks(const uint8_t* tiles, const uint16_t* scales, const uint16_t* zeros, int64_t block,
+int lpqt_w4a16_linear_blocks(const uint8_t* tiles, const uint32_t* params, int64_t block,
                              const uint16_t* Xt, int64_t ldx, int64_t M, int64_t N, int64_t K, void* Y, int y_dtype,
                              int y_layout, int64_t ldy, int split_k, void* workspace, int64_t workspace_bytes,
                              int flags, void* stream) {
-  if (flags & ~(LPQT_LAUNCH_PDL | LPQT_SCHED_STREAMK)) return LPQT_E_INVALID_INPUT;
+  if (flags & ~(LPQT_LAUNCH_PDL | LPQT_SCHED_STREAMK | LPQT_SCHED_CLUSTER)) return LPQT_E_INVALID_INPUT;
   if (M < 0 || N < 0 || K < 0) return LPQT_E_SHAPE;
   if (M == 0 || N == 0) return LPQT_OK;
   if (K == 0) return LPQT_E_SHAPE;
@@ -1976,24 +1979,22 @@ int lpqt_w4a16_linear_blocks(const uint8_t* tiles, const uint16_t* scales, const
   if (y_dtype != LPQT_F32 && y_dtype != LPQT_F16 && y_dtype != LPQT_BF16) return LPQT_E_UNSUPPORTED;
   if (y_layout != LPQT_Y_NM && y_layout != LPQT_Y_MN) return LPQT_E_UNSUPPORTED;
   if (y_layout == LPQT_Y_NM ? ldy < M : ldy < N) return LPQT_E_SHAPE;
-  if (split_k < 0 || zeros == nullptr) return LPQT_E_INVALID_INPUT;
+  if (split_k < 0 || params == nullptr) return LPQT_E_INVALID_INPUT;
+  if ((flags & LPQT_SCHED_STREAMK) && (flags & LPQT_SCHED_CLUSTER)) return LPQT_E_INVALID_INPUT;
   if (N > (int64_t)1 << 30 || M > (int64_t)1 << 30 || K > (int64_t)1 << 30) return LPQT_E_SHAPE;
   const bool per_row = block <= 0 || block >= K;
   if (!per_row && block % kTileK != 0) return LPQT_E_UNSUPPORTED;
   const Plan p = make_plan(M, N, K, split_k, flags, num_sms(), true);
   if (p.ws_bytes > 0 && (workspace == nullptr || workspace_bytes < p.ws_bytes)) return LPQT_E_WORKSPACE;
   FgqArgs fga{};
-  fga.bpr = per_row ? 1 : static_cast<int>((K + block - 1) / block);
-  fga.bkt = per_row ? p.k_tiles : static_cast<int>(block / kTileK);
-  fga.bkt_shift = (fga.bkt & (fga.bkt - 1)) == 0 ? __builtin_ctz(static_cast<unsigned>(fga.bkt)) : -1;
-  fga.zeros = zeros;
+  fga.stage = reinterpret_cast<const uint8_t*>(params);
   GemmArgs args{};
   L2Prefetch pfa{};
 #ifdef LPQT_TRACE
   args.trace = trace_buffer() + (size_t)trace_next_slot() * kTraceLen;
 #endif
   args.tiles = tiles;
-  args.scales = scales;
+  args.scales = nullptr;
   args.y = Y;
   args.counters = static_cast<int*>(workspace);
   args.partials = reinterpret_cast<float*>(static_cast<uint8_t*>(workspace) + p.counters_bytes);
@@ -2011,15 +2012,7 @@ int lpqt_w4a16_linear_blocks(const uint8_t* tiles, const uint16_t* scales, const
   args.y_dtype = y_dtype;
   args.y_layout = y_layout;
   args.sm = ShiftMuls{1u << 26, 1u << 28, 1u << 30};
-  cudaStream_t st = as_stream(stream);
-  switch (p.bn) {
-    case 16: return launch_impl<16, false, true, true, 4>(p, args, pfa, fga, Xt, ldx, M, st, flags);
-    case 32: return launch_impl<32, false, true, true, 4>(p, args, pfa, fga, Xt, ldx, M, st, flags);
-    case 64: return launch_impl<64, false, true, true, 4>(p, args, pfa, fga, Xt, ldx, M, st, flags);
-    case 128: return launch_impl<128, false, true, true, 4>(p, args, pfa, fga, Xt, ldx, M, st, flags);
-    case 192: return launch_impl<192, false, true, true, 4>(p, args, pfa, fga, Xt, ldx, M, st, flags);
-    default: return LPQT_E_UNSUPPORTED;
-  }
+  return dispatch<true, 4>(p, args, pfa, fga, Xt, ldx, M, as_stream(stream), flags);
 }
 
 }  // extern "C"

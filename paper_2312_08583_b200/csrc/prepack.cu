@@ -142,6 +142,25 @@ __global__ void prepack_int4_kernel(const uint8_t* __restrict__ nib, int64_t N, 
   }
 }
 
+
+// Block parameters in GEMM stage order (FgqArgs, gemm.cu): entry
+// (rt * k_tiles + kt) * 128 + r = the f16 scale (INT4: scale | zero << 16) of
+// row rt * 128 + r in the block holding k tile kt; rows past N are 0.
+__global__ void fgq_stage_params_kernel(const uint16_t* __restrict__ scales, const uint16_t* __restrict__ zeros,
+                                        int64_t N, int64_t bpr, int64_t bkt, int64_t k_tiles, int64_t total,
+                                        void* __restrict__ out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i % kTileN, t = i / kTileN, kt = t % k_tiles, n = (t / k_tiles) * kTileN + r;
+    const int64_t b = n * bpr + kt / bkt;
+    const uint32_t sc = n < N ? scales[b] : 0u;
+    if (zeros) {
+      static_cast<uint32_t*>(out)[i] = sc | (n < N ? static_cast<uint32_t>(zeros[b]) << 16 : 0u);
+    } else {
+      static_cast<uint16_t*>(out)[i] = static_cast<uint16_t>(sc);
+    }
+  }
+}
+
 }  // namespace lpqt
 
 using namespace lpqt;
@@ -211,6 +230,28 @@ int lpqt_int4_prepack(const uint8_t* nibbles, int64_t N, int64_t K, uint8_t* til
   if (N == 0 || K == 0) return LPQT_OK;
   const int64_t Np = round_up(N, kTileN), Kp = round_up(K, kTileK);
   prepack_int4_kernel<<<grid_for(Np * (Kp / 8), 256), 256, 0, as_stream(stream)>>>(nibbles, N, K, Np, Kp, tiles);
+  note_launch();
+  return check_launch();
+}
+
+
+int64_t lpqt_fgq_stage_bytes(int64_t N, int64_t K, int with_zeros) {
+  if (N <= 0 || K <= 0) return 0;
+  return round_up(N, kTileN) * (round_up(K, kTileK) / kTileK) * (with_zeros ? 4 : 2);
+}
+
+int lpqt_fgq_stage_params(const uint16_t* scales, const uint16_t* zeros, int64_t N, int64_t K, int64_t block,
+                          void* out, void* stream) {
+  if (N < 0 || K < 0) return LPQT_E_SHAPE;
+  if (N == 0 || K == 0) return LPQT_OK;
+  const bool per_row = block <= 0 || block >= K;
+  if (!per_row && block % kTileK != 0) return LPQT_E_UNSUPPORTED;
+  const int64_t k_tiles = round_up(K, kTileK) / kTileK;
+  const int64_t bpr = per_row ? 1 : (K + block - 1) / block;
+  const int64_t bkt = per_row ? k_tiles : block / kTileK;
+  const int64_t total = round_up(N, kTileN) * k_tiles;
+  fgq_stage_params_kernel<<<grid_for(total, 256), 256, 0, as_stream(stream)>>>(scales, zeros, N, bpr, bkt, k_tiles,
+                                                                               total, out);
   note_launch();
   return check_launch();
 }

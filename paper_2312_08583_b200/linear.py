@@ -25,6 +25,18 @@ def _round_up(x: int, m: int) -> int:
     return (x + m - 1) // m * m
 
 
+def stage_params(scales, zeros, n: int, k: int, block: int):
+    """Row-major per-block f16 scales (and INT4 zero points) -> the GEMM's
+    stage-ordered block parameters (`lpqt_fgq_stage_params`): built once per
+    weight, read by the W producer next to each stage's weight bytes."""
+    t = _lib.torch()
+    lib = _lib.load()
+    out = t.empty(int(lib.lpqt_fgq_stage_bytes(n, k, int(zeros is not None))), dtype=t.uint8, device=scales.device)
+    _lib.check(lib.lpqt_fgq_stage_params(scales.data_ptr(), _lib.ptr(zeros), n, k, block, out.data_ptr(),
+                                         _lib.stream_ptr()), "fgq_stage_params")
+    return out
+
+
 def prepack(seg4, seg2, n: int, k: int, fmt: str = "fp6"):
     """Canonical planes (CUDA uint8) -> tile layout (CUDA uint8).  fmt "fp5":
     4 + 1 planes, converted to the FP6 tile layout (every e3m1 value is an
@@ -50,6 +62,10 @@ class Fp6Weight:
         self.n = int(n)
         self.k = int(k)
         self.block = int(block) if block and int(block) < int(k) else 0
+        # FGQ: the GEMM's stage-ordered copy of the block scales (built once here)
+        # (blocks that are not whole 128-k tiles dequantize but do not run the GEMM)
+        self._stage = (stage_params(scales, None, self.n, self.k, self.block)
+                       if self.block and self.block % TILE == 0 else None)
         # static: tiles/scales are complete and never rewritten, so the GEMM
         # may be launched with programmatic dependent launch (it prefetches
         # weights before the preceding kernel on the stream has finished).
@@ -102,6 +118,11 @@ class Fp6Weight:
             cache["weight"] = w
         return w
 
+    def gemm_scales(self):
+        """The scale operand of the GEMM: the per-row scales (CGQ) or the
+        stage-ordered block scales (FGQ)."""
+        return self._stage if self.block else self.scales
+
     # -- inspection -----------------------------------------------------------
     @property
     def nbytes(self) -> int:
@@ -148,6 +169,7 @@ class Int4Weight:
         self.n = int(n)
         self.k = int(k)
         self.block = int(block) if block and int(block) < int(k) else 0
+        self.params = stage_params(scales, zeros, self.n, self.k, self.block)
 
     @classmethod
     def from_quantized(cls, q) -> "Int4Weight":
@@ -213,10 +235,8 @@ def _launch(weight: Fp6Weight, xt, ldx: int, m: int, y, y_dtype: int, y_layout: 
     ws = _lib.Workspace.get(ws_bytes) if ws_bytes else None
     flags = (_lib.LAUNCH_PDL if weight.static else 0) | _sched_flags(sched)
     if isinstance(weight, Int4Weight):
-        if sched == "cluster":
-            raise ValueError("the W4A16 GEMM runs the stream-K / round-robin schedules only")
         _lib.check(lib.lpqt_w4a16_linear_blocks(
-            weight.tiles.data_ptr(), weight.scales.data_ptr(), weight.zeros.data_ptr(), weight.block, xt.data_ptr(),
+            weight.tiles.data_ptr(), weight.params.data_ptr(), weight.block, xt.data_ptr(),
             ldx, m, weight.n, weight.k, y.data_ptr(), y_dtype, y_layout, ldy, split_k, _lib.ptr(ws),
             ws.numel() if ws is not None else 0, flags, _lib.stream_ptr()), "w4a16_linear")
         return
@@ -228,7 +248,8 @@ def _launch(weight: Fp6Weight, xt, ldx: int, m: int, y, y_dtype: int, y_layout: 
         from .errors import InvalidScheme
         raise InvalidScheme(f"FGQ block_size {weight.block} is not a multiple of 128: outside the B200 GEMM path")
     _lib.check(lib.lpqt_w6a16_linear_blocks(
-        weight.tiles.data_ptr(), weight.scales.data_ptr(), weight.block, xt.data_ptr(), ldx, m, weight.n, weight.k,
+        weight.tiles.data_ptr(), weight.gemm_scales().data_ptr(), weight.block, xt.data_ptr(), ldx, m, weight.n,
+        weight.k,
         y.data_ptr(), y_dtype, y_layout, ldy, split_k, _lib.ptr(ws), ws.numel() if ws is not None else 0,
         flags, None if nxt is None else ctypes.byref(nxt), _lib.stream_ptr()), "w6a16_linear")
 

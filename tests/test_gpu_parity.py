@@ -680,6 +680,34 @@ def test_w4a16_gemm_vs_oracle(n, k, m, block):
     assert torch.equal(y.t().cpu(), torch.from_numpy(Y))
 
 
+@pytest.mark.parametrize("sched,split_k", [("streamk", 0), ("streamk", 3), ("cluster", 1), ("cluster", 2),
+                                           ("cluster", 3), ("cluster", 4)])
+@pytest.mark.parametrize("fmt", ["fp6_fgq", "int4_cgq", "int4_fgq"])
+def test_block_params_every_schedule(fmt, sched, split_k):
+    """Stage-ordered block parameters (FGQ scales, INT4 scale | zero) under
+    stream-K and cluster split-K, ragged K (odd k-tile counts split unevenly
+    over the cluster ranks): within the bar of the f64 product of the
+    kernel's binary16 weights, deterministic."""
+    n, k = 1000, 3000 if fmt != "fp6_fgq" else 3072
+    rng = np.random.default_rng(hash((fmt, sched, split_k)) % 2**32)
+    W = (rng.standard_normal((n, k)) * 0.02).astype(np.float16)
+    for m in (1, 16, 24):
+        x = torch.from_numpy(rng.standard_normal((m, k)).astype(np.float16)).cuda()
+        if fmt == "fp6_fgq":
+            w = L.Fp6Weight.quantize(torch.from_numpy(W).cuda(), block=256)
+            Wh = w.dequantize_f16().double()
+        else:
+            block = 256 if fmt == "int4_fgq" else 0
+            gran = L.Granularity.FGQ if block else L.Granularity.CGQ
+            q = L.quantize_tensor(W, L.QuantScheme(gran, L.TensorFormat.INT4_ASYM, block))
+            w = L.Int4Weight.from_quantized(q)
+            Wh = torch.from_numpy(np.asarray(L.dequantize_tensor(q)).astype(np.float16).astype(np.float64)).cuda()
+        y = L.w6a16_linear(x, w, out_dtype=torch.float32, split_k=split_k, sched=sched)
+        assert torch.equal(y, L.w6a16_linear(x, w, out_dtype=torch.float32, split_k=split_k, sched=sched))
+        ref = x.double() @ Wh.t()
+        assert normwise_rel(y.cpu().numpy(), ref.cpu().numpy()) <= 1e-5, (m, fmt, sched, split_k)
+
+
 def test_random_shape_fuzz():
     """Seeded fuzz over shapes / batch / scheme: every launch within the
     normwise bar of the f64 product of the kernel's own binary16 weights,
