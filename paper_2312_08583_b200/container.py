@@ -207,28 +207,33 @@ def read_raw(data: bytes, rows: int, cols: int, dtype: str) -> np.ndarray:
 
 # ------------------------------------------------------------------ device loader
 def load_lpqt(data: bytes):
-    """Container stream -> Fp6Weight resident in HBM in the tile layout.
+    """Container stream -> weight resident in HBM in the GEMM's tile layout.
 
     The stream is validated on the host (header fields, section lengths, the
     reference's scale checks), copied to the GPU once from pinned memory, and
-    `lpqt_fp6_prepack` reads the canonical planes in place from the device
-    copy.  FP6 under CGQ or FGQ (the formats this library runs) loads;
-    other schemes raise InvalidScheme like quantize_tensor does.
+    the prepack kernel reads the payload in place from the device copy:
+    FP6 / FP5 (CGQ or FGQ) -> `Fp6Weight` (`lpqt_fp6_prepack` /
+    `lpqt_fp5_prepack`), INT4 -> `Int4Weight` (`lpqt_int4_prepack`).
     """
-    from .linear import Fp6Weight
+    from .linear import Fp6Weight, Int4Weight
     from .quantizer import _require_path, scale_block
     hdr, _, off = _parse(data)
-    _require_path(hdr["scheme"])
+    scheme = hdr["scheme"]
     t = _lib.torch()
     rows, cols = hdr["rows"], hdr["cols"]
-    nb = num_blocks(rows, cols, hdr["scheme"])
+    nb = num_blocks(rows, cols, scheme)
     host = t.frombuffer(bytearray(data), dtype=t.uint8).pin_memory()
     blob = host.to(_lib.device(), non_blocking=True)
+    # scales / zeros / folded are kept as views into the device copy of the
+    # stream; the payload is only read by the prepack
     scales = blob[off["scales"]:off["scales"] + 2 * nb].view(t.float16)
+    if scheme.fmt is TensorFormat.INT4_ASYM:
+        zeros = blob[off["zeros"]:off["zeros"] + 2 * nb].view(t.float16)
+        nib = blob[off["nibbles"]:off["nibbles"] + (rows * cols + 1) // 2]
+        return Int4Weight.from_nibbles(nib, scales, zeros, rows, cols, block=scale_block(scheme))
+    _require_path(scheme)
     folded = blob[off["folded"]:off["folded"] + 2 * nb].view(t.float16) if hdr["bias_shift"] else None
     seg4 = blob[off["seg4"]:off["seg4"] + seg4_length(rows * cols)]
-    tail = blob[off["tail"]:off["tail"] + tail_length(hdr["scheme"].fmt.minifloat, rows * cols)]
-    # scales / folded are kept as views into the device copy of the stream;
-    # the planes are only read by the prepack
-    fmt = "fp5" if hdr["scheme"].fmt.minifloat.mantissa_bits == 1 else "fp6"
-    return Fp6Weight.from_planes(seg4, tail, scales, rows, cols, folded, block=scale_block(hdr["scheme"]), fmt=fmt)
+    tail = blob[off["tail"]:off["tail"] + tail_length(scheme.fmt.minifloat, rows * cols)]
+    fmt = "fp5" if scheme.fmt.minifloat.mantissa_bits == 1 else "fp6"
+    return Fp6Weight.from_planes(seg4, tail, scales, rows, cols, folded, block=scale_block(scheme), fmt=fmt)

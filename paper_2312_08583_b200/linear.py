@@ -169,7 +169,9 @@ class Int4Weight:
         self.n = int(n)
         self.k = int(k)
         self.block = int(block) if block and int(block) < int(k) else 0
-        self.params = stage_params(scales, zeros, self.n, self.k, self.block)
+        # (blocks that are not whole 128-k tiles dequantize but do not run the GEMM)
+        self.params = (stage_params(scales, zeros, self.n, self.k, self.block)
+                       if self.n and self.k and self.block % TILE == 0 else None)
 
     @classmethod
     def from_quantized(cls, q) -> "Int4Weight":
@@ -190,14 +192,21 @@ class Int4Weight:
         def f16(a):
             return _lib.to_device(a if _lib.is_torch(a) else np.asarray(a, np.float16)).reshape(-1).to(t.float16)
 
-        lib = _lib.load()
-        tiles = t.empty(int(lib.lpqt_int4_tiles_bytes(q.rows, q.cols)), dtype=t.uint8, device=nib.device)
-        _lib.check(lib.lpqt_int4_prepack(nib.data_ptr(), q.rows, q.cols, tiles.data_ptr(), _lib.stream_ptr()),
-                   "int4_prepack")
-        t.cuda.current_stream().synchronize()
-        w = cls(tiles, f16(q.scales), f16(q.zero_points), q.rows, q.cols, block)
+        w = cls.from_nibbles(nib, f16(q.scales), f16(q.zero_points), q.rows, q.cols, block)
         if cache is not None:
             cache["weight"] = w
+        return w
+
+    @classmethod
+    def from_nibbles(cls, nib, scales, zeros, n: int, k: int, block: int = 0) -> "Int4Weight":
+        """CUDA nibble payload (packing.py INT4 order) + f16 scales / zero
+        points -> tile layout (`lpqt_int4_prepack`)."""
+        t = _lib.torch()
+        lib = _lib.load()
+        tiles = t.empty(int(lib.lpqt_int4_tiles_bytes(n, k)), dtype=t.uint8, device=nib.device)
+        _lib.check(lib.lpqt_int4_prepack(nib.data_ptr(), n, k, tiles.data_ptr(), _lib.stream_ptr()), "int4_prepack")
+        w = cls(tiles, scales, zeros, n, k, block)
+        t.cuda.current_stream().synchronize()
         return w
 
     @property
@@ -234,6 +243,9 @@ def _launch(weight: Fp6Weight, xt, ldx: int, m: int, y, y_dtype: int, y_layout: 
     ws_bytes = int(lib.lpqt_w6a16_workspace_bytes(m, weight.n, weight.k, split_k))
     ws = _lib.Workspace.get(ws_bytes) if ws_bytes else None
     flags = (_lib.LAUNCH_PDL if weight.static else 0) | _sched_flags(sched)
+    if weight.block and weight.block % TILE:
+        from .errors import InvalidScheme
+        raise InvalidScheme(f"FGQ block_size {weight.block} is not a multiple of 128: outside the B200 GEMM path")
     if isinstance(weight, Int4Weight):
         _lib.check(lib.lpqt_w4a16_linear_blocks(
             weight.tiles.data_ptr(), weight.params.data_ptr(), weight.block, xt.data_ptr(),
