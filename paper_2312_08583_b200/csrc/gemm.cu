@@ -166,13 +166,16 @@ struct L2Prefetch {
 // WB: weight bits, 6 (FP6 e3m2 tiles, 12288 B) or 4 (INT4 tiles, 8192 B:
 // [k-half 2][quad 2][row 128][16 B], nibbles pre-permuted for the
 // magic-number rebuild; the INT4 comparator of SURVEY §8 f4)
+#ifndef LPQT_DECODE_KSTEP
+#define LPQT_DECODE_KSTEP 2  // decode (BN <= 32): 128-k tiles per stage
+#endif
 template <int BN, bool CSK, int WB = 6, bool FGQ = false>
 struct Cfg {
   static constexpr int kTileB = WB == 6 ? kTileBytes : kTileN * kTileK / 2;
   // FGQ / INT4: a stage carries its tiles' block parameters after the weights
   static constexpr int kSBytes = FGQ ? kTileN * (WB == 4 ? 4 : 2) : 0;
   static constexpr int kQuads = WB == 6 ? 3 : 2;             // 16-B quads per (row, k-half)
-  static constexpr int kKStep = BN <= 32 ? 2 : 1;           // 128-k tiles per pipeline stage
+  static constexpr int kKStep = BN <= 32 ? LPQT_DECODE_KSTEP : 1;  // 128-k tiles per pipeline stage
   static constexpr int kXTileBytes = BN * kTileK * 2;       // X for one tile: two SW128 blocks
   static constexpr int kWStageBytes = kKStep * (kTileB + kSBytes);
   static constexpr int kXStageBytes = kKStep * kXTileBytes;
