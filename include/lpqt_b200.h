@@ -199,6 +199,37 @@ typedef struct lpqt_next_linear {
   int64_t bytes_per_cta;  /* prefetch depth per next-launch CTA */
 } lpqt_next_linear;
 
+/* Fused GEMM + all-gather over peer memory (column-parallel TP).
+ * Every rank runs its row shard's GEMM and its epilogue stores each output
+ * element straight into every peer's (NVLink P2P / symmetric) copy of the
+ * full Y: y[p] is peer p's Y buffer already offset to this rank's block (NM
+ * layout: + row0 * ldy, MN layout: + row0), same dtype / layout / ldy on all
+ * peers.  Completion is part of the same kernel: each CTA fences its stores
+ * at system scope and counts itself in `done` (a zeroed int the caller owns,
+ * reset by the kernel); the last CTA writes `epoch` into slot `rank` of every
+ * peer's flag array (flags[p], LPQT_MAX_PEERS u32, zeroed once) and waits
+ * until its own array holds >= epoch from every peer.  When the kernel
+ * completes, Y is whole on this GPU.  epoch: strictly increasing per call
+ * (wrapping compare); the caller must not reuse a Y buffer a slower peer
+ * may still be reading (the Python wrapper alternates two).  npeers = 1
+ * (y[0] = own buffer) is a plain launch plus the counter. */
+#define LPQT_MAX_PEERS 8
+typedef struct lpqt_peer_out {
+  void* y[LPQT_MAX_PEERS];
+  uint32_t* flags[LPQT_MAX_PEERS];
+  int npeers, rank;
+  uint32_t epoch;
+  int* done;
+} lpqt_peer_out;
+
+int lpqt_w6a16_linear_gather(const uint8_t* tiles, const uint16_t* scales,
+                             int64_t block, const uint16_t* Xt, int64_t ldx,
+                             int64_t M, int64_t N, int64_t K, int y_dtype,
+                             int y_layout, int64_t ldy, int split_k,
+                             void* workspace, int64_t workspace_bytes,
+                             int flags, const lpqt_peer_out* peers,
+                             void* stream);
+
 int lpqt_w6a16_linear_pf(const uint8_t* tiles, const uint16_t* scales,
                          const uint16_t* Xt, int64_t ldx, int64_t M, int64_t N,
                          int64_t K, void* Y, int y_dtype, int y_layout,

@@ -40,6 +40,16 @@ _I32 = ctypes.c_int
 
 
 
+MAX_PEERS = 8
+
+
+class PeerOut(ctypes.Structure):
+    """lpqt_peer_out (include/lpqt_b200.h): fused GEMM + all-gather targets."""
+    _fields_ = [("y", ctypes.c_void_p * MAX_PEERS), ("flags", ctypes.c_void_p * MAX_PEERS),
+                ("npeers", ctypes.c_int), ("rank", ctypes.c_int), ("epoch", ctypes.c_uint32),
+                ("done", ctypes.c_void_p)]
+
+
 class NextLinear(ctypes.Structure):
     """lpqt_next_linear (include/lpqt_b200.h): the launch that follows on the stream."""
     _fields_ = [("tiles", ctypes.c_void_p), ("M", ctypes.c_int64), ("N", ctypes.c_int64), ("K", ctypes.c_int64),
@@ -98,6 +108,8 @@ SIGNATURES = {
     "lpqt_w4a16_linear_blocks": (_I32, [_P, _P, _I64, _P, _I64, _I64, _I64, _I64, _P, _I32, _I32, _I64, _I32, _P,
                                         _I64, _I32, _P]),
     "lpqt_fgq_stage_bytes": (_I64, [_I64, _I64, _I32]),
+    "lpqt_w6a16_linear_gather": (_I32, [_P, _P, _I64, _P, _I64, _I64, _I64, _I64, _I32, _I32, _I64, _I32, _P,
+                                        _I64, _I32, _P, _P]),
     "lpqt_fgq_stage_params": (_I32, [_P, _P, _I64, _I64, _I64, _P, _P]),
     "lpqt_launch_count": (_I64, []),
 }

@@ -414,6 +414,60 @@ __device__ __forceinline__ void store_y(const GemmArgs& a, int n, int m, float v
   }
 }
 
+// Fused all-gather (lpqt_w6a16_linear_gather): the same element into every
+// peer's Y (each y[p] already offset to this rank's block).
+__device__ __forceinline__ void store_y_peers(const GemmArgs& a, const lpqt_peer_out& po, int n, int m, float v) {
+  if (n >= a.N || m >= a.M) return;
+  const int64_t off = a.y_layout == LPQT_Y_NM ? (int64_t)n * a.ldy + m : (int64_t)m * a.ldy + n;
+  // (static peer indices: the pointers stay in the constant bank, no local copy)
+  if (a.y_dtype == LPQT_F32) {
+#pragma unroll
+    for (int p = 0; p < LPQT_MAX_PEERS; ++p)
+      if (p < po.npeers) static_cast<float*>(po.y[p])[off] = v;
+  } else if (a.y_dtype == LPQT_F16) {
+    const __half h = __float2half_rn(v);
+#pragma unroll
+    for (int p = 0; p < LPQT_MAX_PEERS; ++p)
+      if (p < po.npeers) static_cast<__half*>(po.y[p])[off] = h;
+  } else {
+    const __nv_bfloat16 h = __float2bfloat16_rn(v);
+#pragma unroll
+    for (int p = 0; p < LPQT_MAX_PEERS; ++p)
+      if (p < po.npeers) static_cast<__nv_bfloat16*>(po.y[p])[off] = h;
+  }
+}
+__device__ __forceinline__ void st_release_sys_u32(uint32_t* p, uint32_t v) {
+  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t ld_acquire_sys_u32(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+// Last CTA of this rank's launch (all CTAs fenced their peer stores at system
+// scope before counting in): signal every peer, then wait for every peer's
+// signal of this epoch (>= in wrapping order: a faster peer may already have
+// signalled the next one), then re-arm the counter for the next launch.
+__device__ __forceinline__ void peer_complete(const lpqt_peer_out& po) {
+  const int prev = atom_add_acq_rel_gpu(po.done, 1);
+  if (prev != static_cast<int>(gridDim.x) - 1) return;
+  __threadfence_system();
+  const uint32_t* mine = nullptr;
+#pragma unroll
+  for (int p = 0; p < LPQT_MAX_PEERS; ++p) {
+    if (p < po.npeers) st_release_sys_u32(po.flags[p] + po.rank, po.epoch);
+    if (p == po.rank) mine = po.flags[p];
+  }
+  for (int q = 0; q < po.npeers; ++q) {
+    // a peer that never launches is a caller bug: fail loudly (~10 s) rather than hang
+    for (uint32_t spin = 0; static_cast<int32_t>(ld_acquire_sys_u32(mine + q) - po.epoch) < 0; ++spin) {
+      if (spin > (1u << 26)) __trap();
+      __nanosleep(128);
+    }
+  }
+  *po.done = 0;
+}
+
 // Sum the first `nacc` accumulators over 16 columns [c0, c0+16) (fixed order).
 template <int BN>
 __device__ __forceinline__ void load_acc16(uint32_t t_d, int c0, int q0, int nacc, float (&acc)[16]) {
@@ -557,10 +611,11 @@ __device__ __forceinline__ void ystage_put(const GemmArgs& a, uint32_t buf, int 
 // RAGGED: some stage holds fewer than kKStep tiles (the last k-step of a
 // tile when k_tiles % kKStep != 0, or an odd cluster split-K k-range); only
 // then do the dequant warps walk the stage sequence to learn tile counts.
-template <int BN, bool CSK, bool RAGGED, bool FGQ = false, int WB = 6>
+template <int BN, bool CSK, bool RAGGED, bool FGQ = false, int WB = 6, bool PEERS = false>
 __global__ void __launch_bounds__(kThreads, 1)
     w6a16_tcgen05_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constant__ CUtensorMap tmap_y,
-                         const GemmArgs a, const L2Prefetch pf, const FgqArgs fg) {
+                         const GemmArgs a, const L2Prefetch pf, const FgqArgs fg,
+                         const __grid_constant__ lpqt_peer_out po) {
   static_assert(WB == 6 || FGQ, "INT4 weights carry per-block scales and zero points (FGQ path)");
   using C = Cfg<BN, CSK, WB, FGQ>;
   constexpr int KS = C::kKStep;
@@ -958,7 +1013,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint32_t pf_bits = 0u, sf_bits = 0u, sent_bits = 0u;
     // Y tiles: staged in smem and written by the TMA tensor store (decode),
     // else stored directly; ys_n counts staged tiles (buffer = ys_n & 1)
-    const bool ytma = C::kYBufBytes > 0 && a.y_tma;
+    const bool ytma = !PEERS && C::kYBufBytes > 0 && a.y_tma;
     int ys_n = 0;
     for (; have_next; ++lu) {
       sg = sg_next;
@@ -983,8 +1038,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (ytma) {
           ystage_put<BN>(a, ybuf, rr, c0, v, fs);
         } else {
+          if constexpr (PEERS) {
+#pragma unroll 1
+            for (int j = 0; j < 16; ++j) store_y_peers(a, po, n, m0 + c0 + j, v[j] * fs);
+          } else {
 #pragma unroll
-          for (int j = 0; j < 16; ++j) store_y(a, n, m0 + c0 + j, v[j] * fs);
+            for (int j = 0; j < 16; ++j) store_y(a, n, m0 + c0 + j, v[j] * fs);
+          }
         }
       };
       auto y_end = [&]() {
@@ -1474,8 +1534,14 @@ __global__ void __launch_bounds__(kThreads, 1)
   if constexpr (CSK) {
     if (warp < kWarpEpi0) cluster_wait();  // the setup phase (epilogue waited already)
   }
+  if constexpr (PEERS) {
+    if (warp >= kWarpEpi0) __threadfence_system();  // peer Y stores before the count
+  }
   tc_fence_before();
   __syncthreads();
+  if constexpr (PEERS) {
+    if (threadIdx.x == 0) peer_complete(po);
+  }
   // CSK: no CTA may leave while a peer can still read its staging buffer or
   // arrive on its barriers
   if constexpr (CSK) cluster_sync_all();
@@ -1712,10 +1778,10 @@ static int g_trace_n = 0;  // launches traced so far
 static int trace_next_slot() { return g_trace_n++ % kTraceSlots; }
 #endif
 
-template <int BN, bool CSK, bool RAGGED, bool FGQ = false, int WB = 6>
+template <int BN, bool CSK, bool RAGGED, bool FGQ = false, int WB = 6, bool PEERS = false>
 static int launch_impl(const Plan& p, const GemmArgs& args, const L2Prefetch& pf, const FgqArgs& fg,
                        const uint16_t* Xt, int64_t ldx,
-                       int64_t M, cudaStream_t stream, int flags) {
+                       int64_t M, cudaStream_t stream, int flags, const lpqt_peer_out* peers = nullptr) {
   EncodeTiledFn enc = encode_fn();
   if (!enc) return LPQT_E_CUDA;
   CUtensorMap map;
@@ -1727,7 +1793,7 @@ static int launch_impl(const Plan& p, const GemmArgs& args, const L2Prefetch& pf
           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
     return LPQT_E_INVALID_INPUT;
-  auto kern = w6a16_tcgen05_kernel<BN, CSK, RAGGED, FGQ, WB>;
+  auto kern = w6a16_tcgen05_kernel<BN, CSK, RAGGED, FGQ, WB, PEERS>;
   constexpr int smem = Cfg<BN, CSK, WB, FGQ>::kSmemBytes;
   static std::once_flag once;
   static cudaError_t attr_err = cudaSuccess;
@@ -1763,7 +1829,10 @@ static int launch_impl(const Plan& p, const GemmArgs& args, const L2Prefetch& pf
   CUtensorMap ymap;
   memset(&ymap, 0, sizeof(ymap));
   a2.y_tma = 0;
-  if (Cfg<BN, CSK, WB, FGQ>::kYBufBytes > 0) {
+  lpqt_peer_out po;
+  memset(&po, 0, sizeof(po));
+  if (peers) po = *peers;
+  if (Cfg<BN, CSK, WB, FGQ>::kYBufBytes > 0 && !PEERS) {
     const int es = args.y_dtype == LPQT_F32 ? 4 : 2;
     const CUtensorMapDataType dt = args.y_dtype == LPQT_F32   ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32
                                    : args.y_dtype == LPQT_F16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16
@@ -1780,7 +1849,7 @@ static int launch_impl(const Plan& p, const GemmArgs& args, const L2Prefetch& pf
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS)
       a2.y_tma = 1;
   }
-  if (cudaLaunchKernelEx(&cfg, kern, map, ymap, a2, pf, fg) != cudaSuccess) return LPQT_E_CUDA;
+  if (cudaLaunchKernelEx(&cfg, kern, map, ymap, a2, pf, fg, po) != cudaSuccess) return LPQT_E_CUDA;
   note_launch();
   return check_launch();
 }
@@ -1790,32 +1859,33 @@ static int launch_impl(const Plan& p, const GemmArgs& args, const L2Prefetch& pf
 using namespace lpqt;
 
 // Schedule / stage-shape dispatch shared by the FP6 (CGQ, FGQ) and INT4 entries.
-template <bool FGQ, int WB>
+template <bool FGQ, int WB, bool PEERS = false>
 static int dispatch(const Plan& p, const GemmArgs& args, const L2Prefetch& pfa, const FgqArgs& fga,
-                    const uint16_t* Xt, int64_t ldx, int64_t M, cudaStream_t st, int flags) {
+                    const uint16_t* Xt, int64_t ldx, int64_t M, cudaStream_t st, int flags,
+                    const lpqt_peer_out* po = nullptr) {
   bool ragged = p.k_tiles % p.kstep != 0;
   if (p.csk) {
     for (int r = 0; r < p.cluster; ++r)  // k-range of rank r must be a whole number of stages
       ragged |= ((r + 1) * p.k_tiles / p.cluster - r * p.k_tiles / p.cluster) % p.kstep != 0;
     if (p.bn <= 16)
-      return ragged ? launch_impl<16, true, true, FGQ, WB>(p, args, pfa, fga, Xt, ldx, M, st, flags)
-                    : launch_impl<16, true, false, FGQ, WB>(p, args, pfa, fga, Xt, ldx, M, st, flags);
-    return ragged ? launch_impl<32, true, true, FGQ, WB>(p, args, pfa, fga, Xt, ldx, M, st, flags)
-                  : launch_impl<32, true, false, FGQ, WB>(p, args, pfa, fga, Xt, ldx, M, st, flags);
+      return ragged ? launch_impl<16, true, true, FGQ, WB, PEERS>(p, args, pfa, fga, Xt, ldx, M, st, flags, po)
+                    : launch_impl<16, true, false, FGQ, WB, PEERS>(p, args, pfa, fga, Xt, ldx, M, st, flags, po);
+    return ragged ? launch_impl<32, true, true, FGQ, WB, PEERS>(p, args, pfa, fga, Xt, ldx, M, st, flags, po)
+                  : launch_impl<32, true, false, FGQ, WB, PEERS>(p, args, pfa, fga, Xt, ldx, M, st, flags, po);
   }
   switch (p.bn) {
     case 16:
-      return ragged ? launch_impl<16, false, true, FGQ, WB>(p, args, pfa, fga, Xt, ldx, M, st, flags)
-                    : launch_impl<16, false, false, FGQ, WB>(p, args, pfa, fga, Xt, ldx, M, st, flags);
+      return ragged ? launch_impl<16, false, true, FGQ, WB, PEERS>(p, args, pfa, fga, Xt, ldx, M, st, flags, po)
+                    : launch_impl<16, false, false, FGQ, WB, PEERS>(p, args, pfa, fga, Xt, ldx, M, st, flags, po);
     case 32:
-      return ragged ? launch_impl<32, false, true, FGQ, WB>(p, args, pfa, fga, Xt, ldx, M, st, flags)
-                    : launch_impl<32, false, false, FGQ, WB>(p, args, pfa, fga, Xt, ldx, M, st, flags);
-    case 64: return launch_impl<64, false, false, FGQ, WB>(p, args, pfa, fga, Xt, ldx, M, st, flags);
-    case 128: return launch_impl<128, false, false, FGQ, WB>(p, args, pfa, fga, Xt, ldx, M, st, flags);
-    case 192: return launch_impl<192, false, false, FGQ, WB>(p, args, pfa, fga, Xt, ldx, M, st, flags);
+      return ragged ? launch_impl<32, false, true, FGQ, WB, PEERS>(p, args, pfa, fga, Xt, ldx, M, st, flags, po)
+                    : launch_impl<32, false, false, FGQ, WB, PEERS>(p, args, pfa, fga, Xt, ldx, M, st, flags, po);
+    case 64: return launch_impl<64, false, false, FGQ, WB, PEERS>(p, args, pfa, fga, Xt, ldx, M, st, flags, po);
+    case 128: return launch_impl<128, false, false, FGQ, WB, PEERS>(p, args, pfa, fga, Xt, ldx, M, st, flags, po);
+    case 192: return launch_impl<192, false, false, FGQ, WB, PEERS>(p, args, pfa, fga, Xt, ldx, M, st, flags, po);
     default:
       if constexpr (FGQ) return LPQT_E_UNSUPPORTED;  // (BN 256 only by LPQT_PREFILL_BN override)
-      else return launch_impl<256, false, false, FGQ, WB>(p, args, pfa, fga, Xt, ldx, M, st, flags);
+      else return launch_impl<256, false, false, FGQ, WB, PEERS>(p, args, pfa, fga, Xt, ldx, M, st, flags, po);
   }
 }
 
@@ -1894,10 +1964,10 @@ int lpqt_w6a16_linear_pf(const uint8_t* tiles, const uint16_t* scales, const uin
                                   workspace_bytes, flags, next, stream);
 }
 
-int lpqt_w6a16_linear_blocks(const uint8_t* tiles, const uint16_t* scales, int64_t block, const uint16_t* Xt,
+static int w6a16_blocks_impl(const uint8_t* tiles, const uint16_t* scales, int64_t block, const uint16_t* Xt,
                              int64_t ldx, int64_t M, int64_t N, int64_t K, void* Y, int y_dtype, int y_layout,
                              int64_t ldy, int split_k, void* workspace, int64_t workspace_bytes, int flags,
-                             const lpqt_next_linear* next, void* stream) {
+                             const lpqt_next_linear* next, void* stream, const lpqt_peer_out* po) {
   if (flags & ~(LPQT_LAUNCH_PDL | LPQT_SCHED_STREAMK | LPQT_SCHED_CLUSTER)) return LPQT_E_INVALID_INPUT;
   // FGQ: blocks of B columns (B = K, or block <= 0: one scale per row)
   const bool fgq = block > 0 && block < K;
@@ -1961,8 +2031,33 @@ int lpqt_w6a16_linear_blocks(const uint8_t* tiles, const uint16_t* scales, int64
     }
   }
   cudaStream_t st = as_stream(stream);
+  if (po)
+    return fgq ? dispatch<true, 6, true>(p, args, pfa, fga, Xt, ldx, M, st, flags, po)
+               : dispatch<false, 6, true>(p, args, pfa, fga, Xt, ldx, M, st, flags, po);
   return fgq ? dispatch<true, 6>(p, args, pfa, fga, Xt, ldx, M, st, flags)
              : dispatch<false, 6>(p, args, pfa, fga, Xt, ldx, M, st, flags);
+}
+
+int lpqt_w6a16_linear_blocks(const uint8_t* tiles, const uint16_t* scales, int64_t block, const uint16_t* Xt,
+                             int64_t ldx, int64_t M, int64_t N, int64_t K, void* Y, int y_dtype, int y_layout,
+                             int64_t ldy, int split_k, void* workspace, int64_t workspace_bytes, int flags,
+                             const lpqt_next_linear* next, void* stream) {
+  return w6a16_blocks_impl(tiles, scales, block, Xt, ldx, M, N, K, Y, y_dtype, y_layout, ldy, split_k, workspace,
+                           workspace_bytes, flags, next, stream, nullptr);
+}
+
+int lpqt_w6a16_linear_gather(const uint8_t* tiles, const uint16_t* scales, int64_t block, const uint16_t* Xt,
+                             int64_t ldx, int64_t M, int64_t N, int64_t K, int y_dtype, int y_layout, int64_t ldy,
+                             int split_k, void* workspace, int64_t workspace_bytes, int flags,
+                             const lpqt_peer_out* peers, void* stream) {
+  if (!peers || peers->npeers < 1 || peers->npeers > LPQT_MAX_PEERS || peers->rank < 0 ||
+      peers->rank >= peers->npeers || peers->done == nullptr)
+    return LPQT_E_INVALID_INPUT;
+  for (int p = 0; p < peers->npeers; ++p)
+    if (peers->y[p] == nullptr || peers->flags[p] == nullptr) return LPQT_E_INVALID_INPUT;
+  if (M == 0 || N == 0) return LPQT_E_SHAPE;  // every rank must launch (the barrier counts CTAs)
+  return w6a16_blocks_impl(tiles, scales, block, Xt, ldx, M, N, K, peers->y[peers->rank], y_dtype, y_layout, ldy,
+                           split_k, workspace, workspace_bytes, flags, nullptr, stream, peers);
 }
 
 

@@ -8,6 +8,11 @@ its shard's GEMM into Y_p (reference N x M layout: a contiguous row block)
 and one NCCL all-gather (torch.distributed, ProcessGroupNCCL over NVLink /
 NVSwitch) assembles Y = [Y_0; ...; Y_{P-1}] with no permute.
 
+`FusedColumnParallelFp6Linear` is the B200 variant with no collective call:
+the GEMM's epilogue stores each rank's block straight into every peer's
+symmetric-memory Y and the same kernel ends with a flag barrier
+(`lpqt_w6a16_linear_gather`, SURVEY §8e "fused variant").
+
 The per-rank compute is pluggable (`local_gemm`) so the sharding + gather
 logic is exercised by world_size-2 gloo tests on CPU with the oracle as the
 local compute; the product path uses the tcgen05 kernel.
@@ -15,6 +20,7 @@ local compute; the product path uses the tcgen05 kernel.
 
 from __future__ import annotations
 
+import ctypes
 from typing import Callable
 
 from . import _lib
@@ -102,3 +108,108 @@ class ColumnParallelFp6Linear:
             out[a:a + sz] = buf[r * mx: r * mx + sz]
             a += sz
         return out
+
+
+# ---------------------------------------------------------------- fused all-gather
+def block_offset(sizes: list[int], rank: int, m: int, layout: str) -> int:
+    """Element offset of `rank`'s output block inside the full Y: rows
+    [row0, row0 + N_p) of Y[N, M] ("nm", ldy = M) or columns of Y[M, N]
+    ("mn", ldy = N)."""
+    row0 = sum(sizes[:rank])
+    return row0 * m if layout == "nm" else row0
+
+
+def gather_linear(weight, xt, ldx: int, m: int, peer_y: list[int], peer_flags: list[int], rank: int, epoch: int,
+                  done, y_dtype: int, layout: str, ldy: int, row0: int, split_k: int = 0, sched: str = "auto",
+                  workspace=None) -> None:
+    """One fused GEMM + all-gather launch (`lpqt_w6a16_linear_gather`): this
+    rank's shard GEMM stores its block straight into every peer's Y
+    (`peer_y[p]` = peer p's Y base address; the block offset is added here)
+    and the same kernel completes only when every peer's block has landed in
+    this GPU's Y (flag barrier, `peer_flags[p]` = peer p's flag array).
+    All ranks must call it with the same epoch.  row0: this rank's first
+    output row (`shard_rows`).  workspace: split-K scratch (default: the
+    per-device one; launches that may run concurrently need their own)."""
+    from .linear import _sched_flags
+    lib = _lib.load()
+    npeers = len(peer_y)
+    if not 1 <= npeers <= _lib.MAX_PEERS or len(peer_flags) != npeers:
+        raise ValueError(f"1..{_lib.MAX_PEERS} peers with one flag array each")
+    es = 4 if y_dtype == _lib.F32 else 2
+    off = row0 * m if layout == "nm" else row0
+    po = _lib.PeerOut()
+    for p in range(npeers):
+        po.y[p] = int(peer_y[p]) + off * es
+        po.flags[p] = int(peer_flags[p])
+    po.npeers, po.rank, po.epoch, po.done = npeers, rank, epoch & 0xFFFFFFFF, done.data_ptr()
+    ws_bytes = int(lib.lpqt_w6a16_workspace_bytes(m, weight.n, weight.k, split_k))
+    ws = workspace if workspace is not None else (_lib.Workspace.get(ws_bytes) if ws_bytes else None)
+    if ws is not None and ws.numel() < ws_bytes:
+        raise ValueError(f"workspace of {ws.numel()} B, the plan needs {ws_bytes}")
+    flags = (_lib.LAUNCH_PDL if weight.static else 0) | _sched_flags(sched)
+    _lib.check(lib.lpqt_w6a16_linear_gather(
+        weight.tiles.data_ptr(), weight.gemm_scales().data_ptr(), weight.block, xt.data_ptr(), ldx, m, weight.n,
+        weight.k, y_dtype, _lib.Y_NM if layout == "nm" else _lib.Y_MN, ldy, split_k, _lib.ptr(ws),
+        ws.numel() if ws is not None else 0, flags, ctypes.byref(po), _lib.stream_ptr()), "w6a16_linear_gather")
+
+
+class FusedColumnParallelFp6Linear:
+    """y[M, N] = x[M, K] @ W_hat^T with W's rows sharded over the group and
+    the all-gather fused into the GEMM: every rank's epilogue writes its
+    columns of y straight into every peer's symmetric-memory copy of y over
+    NVLink / NVSwitch, and the kernel's last CTA runs a flag barrier with the
+    peers (no NCCL call on the data path).  Buffers come from
+    `torch.distributed._symmetric_memory` (P2P-mapped on every peer); two
+    output buffers alternate, so a returned y stays valid until the call after
+    next (clone it to keep it longer)."""
+
+    def __init__(self, weight_shard, n: int, k: int, m_max: int, group=None, out_dtype=None):
+        import torch.distributed as dist
+        import torch.distributed._symmetric_memory as symm
+        t = _lib.torch()
+        self.group = group or dist.group.WORLD
+        self.world, self.rank = dist.get_world_size(self.group), dist.get_rank(self.group)
+        if self.world > _lib.MAX_PEERS:
+            raise ValueError(f"at most {_lib.MAX_PEERS} ranks")
+        self.n, self.k, self.m_max = int(n), int(k), int(m_max)
+        self.sizes = shard_sizes(self.n, self.world)
+        self.weight = weight_shard
+        self.dtype = out_dtype or t.float16
+        dev = weight_shard.tiles.device
+        gname = self.group.group_name
+        self.bufs = [symm.empty((self.m_max, self.n), dtype=self.dtype, device=dev) for _ in range(2)]
+        self.buf_h = [symm.rendezvous(b, gname) for b in self.bufs]
+        self.flag_t = symm.empty((_lib.MAX_PEERS,), dtype=t.int32, device=dev)
+        self.flag_t.zero_()
+        self.flag_h = symm.rendezvous(self.flag_t, gname)
+        self.done = t.zeros(1, dtype=t.int32, device=dev)
+        self.epoch = 0
+        dist.barrier(group=self.group)   # every rank's flags are zero before the first signal
+
+    @classmethod
+    def quantize_shard(cls, W_full, m_max: int, group=None, bias_shift: bool = True, out_dtype=None):
+        import torch.distributed as dist
+        from .linear import Fp6Weight
+        world, rank = dist.get_world_size(group), dist.get_rank(group)
+        n, k = int(W_full.shape[0]), int(W_full.shape[1])
+        a, b = shard_rows(n, world, rank)
+        return cls(Fp6Weight.quantize(W_full[a:b], bias_shift), n, k, m_max, group, out_dtype)
+
+    def __call__(self, x):
+        """x[M, K] fp16, replicated on every rank -> y[M, N] on every rank."""
+        t = _lib.torch()
+        m = int(x.shape[0])
+        if m > self.m_max:
+            raise ValueError(f"batch {m} exceeds m_max {self.m_max}")
+        x2 = x if (x.dtype == t.float16 and x.is_contiguous() and self.k % 8 == 0) else None
+        if x2 is None:
+            kp = (self.k + 7) // 8 * 8
+            x2 = t.zeros((m, kp), dtype=t.float16, device=x.device)
+            x2[:, :self.k] = x
+        ldx = int(x2.shape[1])
+        self.epoch += 1
+        i = self.epoch & 1
+        code = {t.float32: _lib.F32, t.float16: _lib.F16, t.bfloat16: _lib.BF16}[self.dtype]
+        gather_linear(self.weight, x2, ldx, m, list(self.buf_h[i].buffer_ptrs), list(self.flag_h.buffer_ptrs),
+                      self.rank, self.epoch, self.done, code, "mn", self.n, sum(self.sizes[:self.rank]))
+        return self.bufs[i][:m]
