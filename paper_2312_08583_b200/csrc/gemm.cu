@@ -414,6 +414,22 @@ __device__ __forceinline__ void store_y(const GemmArgs& a, int n, int m, float v
   }
 }
 
+// Fused all-gather, decode tiles: one Y tensor map per peer (the staged tile
+// leaves by one TMA store per peer); other kernels carry an empty struct.
+struct PeerMaps {
+  CUtensorMap m[LPQT_MAX_PEERS];
+};
+struct NoPeerMaps {};
+template <bool PEERS>
+using PeerMapsOf = typename std::conditional<PEERS, PeerMaps, NoPeerMaps>::type;
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+
+#ifndef LPQT_EXP_PEERS_LOCAL
+#define LPQT_EXP_PEERS_LOCAL 0  // experiment: gather launch stores only locally
+#endif
+#ifndef LPQT_EXP_PEERS_NOSYNC
+#define LPQT_EXP_PEERS_NOSYNC 0  // experiment: gather launch without the completion barrier
+#endif
 // Fused all-gather (lpqt_w6a16_linear_gather): the same element into every
 // peer's Y (each y[p] already offset to this rank's block).
 __device__ __forceinline__ void store_y_peers(const GemmArgs& a, const lpqt_peer_out& po, int n, int m, float v) {
@@ -444,10 +460,14 @@ __device__ __forceinline__ uint32_t ld_acquire_sys_u32(const uint32_t* p) {
   asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
-// Last CTA of this rank's launch (all CTAs fenced their peer stores at system
-// scope before counting in): signal every peer, then wait for every peer's
-// signal of this epoch (>= in wrapping order: a faster peer may already have
-// signalled the next one), then re-arm the counter for the next launch.
+// Called by one thread per CTA after the CTA barrier that follows its
+// epilogue's peer stores.  The count is a gpu-scope release (cumulative over
+// the CTA's stores through bar.sync); the last CTA's acquire of it and its
+// system-scope release stores of the flag carry every CTA's stores to the
+// peers (the same release/acquire chain custom NVLink all-reduce barriers
+// use; a per-thread fence.sc.sys cost ~10 us per launch).  Then wait for
+// every peer's signal of this epoch (>= in wrapping order: a faster peer may
+// already have signalled the next one) and re-arm the counter.
 __device__ __forceinline__ void peer_complete(const lpqt_peer_out& po) {
   const int prev = atom_add_acq_rel_gpu(po.done, 1);
   if (prev != static_cast<int>(gridDim.x) - 1) return;
@@ -615,7 +635,8 @@ template <int BN, bool CSK, bool RAGGED, bool FGQ = false, int WB = 6, bool PEER
 __global__ void __launch_bounds__(kThreads, 1)
     w6a16_tcgen05_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constant__ CUtensorMap tmap_y,
                          const GemmArgs a, const L2Prefetch pf, const FgqArgs fg,
-                         const __grid_constant__ lpqt_peer_out po) {
+                         const __grid_constant__ lpqt_peer_out po,
+                         const __grid_constant__ PeerMapsOf<PEERS> pmaps) {
   static_assert(WB == 6 || FGQ, "INT4 weights carry per-block scales and zero points (FGQ path)");
   using C = Cfg<BN, CSK, WB, FGQ>;
   constexpr int KS = C::kKStep;
@@ -1013,7 +1034,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint32_t pf_bits = 0u, sf_bits = 0u, sent_bits = 0u;
     // Y tiles: staged in smem and written by the TMA tensor store (decode),
     // else stored directly; ys_n counts staged tiles (buffer = ys_n & 1)
-    const bool ytma = !PEERS && C::kYBufBytes > 0 && a.y_tma;
+    const bool ytma = C::kYBufBytes > 0 && a.y_tma;
     int ys_n = 0;
     for (; have_next; ++lu) {
       sg = sg_next;
@@ -1038,7 +1059,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (ytma) {
           ystage_put<BN>(a, ybuf, rr, c0, v, fs);
         } else {
-          if constexpr (PEERS) {
+          if constexpr (PEERS && C::kYBufBytes == 0 && !LPQT_EXP_PEERS_LOCAL) {
+            // (decode tiles always leave by the per-peer TMA stores: the host
+            // refuses peer buffers the tensor maps cannot describe)
 #pragma unroll 1
             for (int j = 0; j < 16; ++j) store_y_peers(a, po, n, m0 + c0 + j, v[j] * fs);
           } else {
@@ -1052,10 +1075,14 @@ __global__ void __launch_bounds__(kThreads, 1)
         fence_proxy_async_smem();
         named_bar_sync(1, kNumEpiWarps * 32);
         if (warp == kWarpEpi0 && lane == 0) {
-          if (a.y_layout == LPQT_Y_NM) {
-            tma_store_2d(&tmap_y, ybuf, m_tile * BN, n_tile * kTileN);
+          const int yc0 = a.y_layout == LPQT_Y_NM ? m_tile * BN : n_tile * kTileN;
+          const int yc1 = a.y_layout == LPQT_Y_NM ? n_tile * kTileN : m_tile * BN;
+          if constexpr (PEERS) {
+#pragma unroll
+            for (int p = 0; p < LPQT_MAX_PEERS; ++p)
+              if (p < po.npeers) tma_store_2d(&pmaps.m[p], ybuf, yc0, yc1);
           } else {
-            tma_store_2d(&tmap_y, ybuf, n_tile * kTileN, m_tile * BN);
+            tma_store_2d(&tmap_y, ybuf, yc0, yc1);
           }
           bulk_commit();
         }
@@ -1527,19 +1554,23 @@ __global__ void __launch_bounds__(kThreads, 1)
         named_bar_sync(1, kNumEpiWarps * 32);
       }
     }
-    if (ytma && warp == kWarpEpi0 && lane == 0) bulk_wait_read<0>();  // smem stays valid until read
+    if (ytma && warp == kWarpEpi0 && lane == 0) {
+      if constexpr (PEERS) {
+        bulk_wait_all();  // the peer stores are complete before this CTA counts in
+        asm volatile("fence.proxy.async.global;" ::: "memory");
+      } else {
+        bulk_wait_read<0>();  // smem stays valid until read
+      }
+    }
     if (warp == kWarpEpi0 && lane == 0) CTA_STAMP(5);
   }
 
   if constexpr (CSK) {
     if (warp < kWarpEpi0) cluster_wait();  // the setup phase (epilogue waited already)
   }
-  if constexpr (PEERS) {
-    if (warp >= kWarpEpi0) __threadfence_system();  // peer Y stores before the count
-  }
   tc_fence_before();
   __syncthreads();
-  if constexpr (PEERS) {
+  if constexpr (PEERS && !LPQT_EXP_PEERS_NOSYNC) {
     if (threadIdx.x == 0) peer_complete(po);
   }
   // CSK: no CTA may leave while a peer can still read its staging buffer or
@@ -1832,7 +1863,9 @@ static int launch_impl(const Plan& p, const GemmArgs& args, const L2Prefetch& pf
   lpqt_peer_out po;
   memset(&po, 0, sizeof(po));
   if (peers) po = *peers;
-  if (Cfg<BN, CSK, WB, FGQ>::kYBufBytes > 0 && !PEERS) {
+  PeerMapsOf<PEERS> pmaps;
+  memset(&pmaps, 0, sizeof(pmaps));
+  if (Cfg<BN, CSK, WB, FGQ>::kYBufBytes > 0) {
     const int es = args.y_dtype == LPQT_F32 ? 4 : 2;
     const CUtensorMapDataType dt = args.y_dtype == LPQT_F32   ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32
                                    : args.y_dtype == LPQT_F16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16
@@ -1843,13 +1876,20 @@ static int launch_impl(const Plan& p, const GemmArgs& args, const L2Prefetch& pf
     const cuuint64_t ystr[1] = {static_cast<cuuint64_t>(args.ldy) * es};
     const cuuint32_t ybox[2] = {static_cast<cuuint32_t>(nm ? BN : kTileN), static_cast<cuuint32_t>(nm ? kTileN : BN)};
     const bool ok = (reinterpret_cast<uintptr_t>(args.y) % 16 == 0) && (ystr[0] % 16 == 0) &&
-                    ((cuuint64_t)ybox[0] * es) % 16 == 0 && ydims[1] > 1;
-    if (ok && enc(&ymap, dt, 2, args.y, ydims, ystr, ybox, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                  CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
-                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS)
-      a2.y_tma = 1;
+                    ((cuuint64_t)ybox[0] * es) % 16 == 0 && (PEERS || ydims[1] > 1);
+    auto encode_y = [&](void* base, CUtensorMap* out) {
+      return ok && reinterpret_cast<uintptr_t>(base) % 16 == 0 &&
+             enc(out, dt, 2, base, ydims, ystr, ybox, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                 CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+    };
+    bool all = encode_y(args.y, &ymap);
+    if constexpr (PEERS) {
+      for (int q = 0; q < po.npeers; ++q) all = all && encode_y(po.y[q], &pmaps.m[q]);
+    }
+    if (all) a2.y_tma = 1;
+    if (PEERS && !all) return LPQT_E_SHAPE;  // peer Y base / row stride not 16-byte aligned
   }
-  if (cudaLaunchKernelEx(&cfg, kern, map, ymap, a2, pf, fg, po) != cudaSuccess) return LPQT_E_CUDA;
+  if (cudaLaunchKernelEx(&cfg, kern, map, ymap, a2, pf, fg, po, pmaps) != cudaSuccess) return LPQT_E_CUDA;
   note_launch();
   return check_launch();
 }

@@ -32,7 +32,8 @@ def test_block_offsets_tile_the_output():
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("n,k,m,layout,dt", [(2048, 4096, 16, "nm", "f32"), (1920, 3000, 3, "mn", "f16"),
-                                             (4096, 1024, 64, "mn", "bf16"), (1024, 8192, 1, "nm", "f16")])
+                                             (4096, 1024, 64, "mn", "bf16"), (1024, 8192, 1, "mn", "f16"),
+                                             (2048, 2048, 200, "nm", "f16")])
 def test_fused_gather_two_ranks_one_gpu(n, k, m, layout, dt):
     import torch
     tdt = {"f32": torch.float32, "f16": torch.float16, "bf16": torch.bfloat16}[dt]
@@ -84,3 +85,8 @@ def test_fused_gather_single_rank_is_a_plain_launch():
         assert torch.equal(y, L.w6a16_linear(x, w))
     with pytest.raises(L.InvalidInput):
         tp.gather_linear(w, x, 2048, 16, [y.data_ptr()], [flags.data_ptr()], 1, 4, done, _lib.F16, "mn", 1024, 0)
+    # decode tiles leave by per-peer TMA stores: a Y row stride the tensor map
+    # cannot describe (reference layout Y[N, 1] in fp16: 2-byte rows) is refused
+    y1 = torch.empty(1024, 1, dtype=torch.float16, device="cuda")
+    with pytest.raises(L.ShapeError):
+        tp.gather_linear(w, x[:1], 2048, 1, [y1.data_ptr()], [flags.data_ptr()], 0, 5, done, _lib.F16, "nm", 1, 0)

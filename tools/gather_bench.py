@@ -1,7 +1,7 @@
 """Fused GEMM + all-gather epilogue cost on one GPU (dev tool): the 70B TP=8
 shard shapes at decode, plain launch vs `lpqt_w6a16_linear_gather` with one
 peer (the own buffer: direct stores + system fence + counter + flag barrier),
-eager back-to-back launches, weights rotated over > 2x L2.
+back-to-back launches in a CUDA graph, weights rotated over > 2x L2.
 
 python tools/gather_bench.py [--m 16]
 """
@@ -45,12 +45,15 @@ for shape in a.shapes.split(","):
         for i in range(copies):
             fn(i)
         torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            for i in range(40):
+                fn(i)
         ts = []
         for _ in range(5):
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record()
-            for i in range(40):
-                fn(i)
+            g.replay()
             e1.record()
             torch.cuda.synchronize()
             ts.append(e0.elapsed_time(e1) * 1e3 / 40)
