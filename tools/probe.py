@@ -18,6 +18,9 @@ import paper_2312_08583_b200 as L  # noqa: E402
 SHAPES = {
     "7b": [(12288, 4096), (4096, 4096), (22016, 4096), (4096, 11008)],
     "70b": [(10240, 8192), (8192, 8192), (57344, 8192), (8192, 28672)],
+    # BASELINE configs[2]: LLaMA-2-13B and StarCoder-15B (MQA, MLP 24576)
+    "13b": [(15360, 5120), (5120, 5120), (27648, 5120), (5120, 13824)],
+    "sc15b": [(6400, 6144), (6144, 6144), (24576, 6144), (6144, 24576)],
 }
 
 
@@ -51,22 +54,23 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--shapes", default="all")
     ap.add_argument("--m", default="1,16")
-    ap.add_argument("--split", type=int, default=0)
+    ap.add_argument("--split", default="0", help="comma list of split_k values (0 = automatic plan)")
     args = ap.parse_args()
-    shapes = SHAPES["7b"] + SHAPES["70b"] if args.shapes == "all" else SHAPES[args.shapes]
+    shapes = SHAPES["7b"] + SHAPES["70b"] if args.shapes == "all" else sum((SHAPES[s] for s in args.shapes.split(",")), [])
+    splits = [int(v) for v in args.split.split(",")]
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device="cuda")
     for n, k in shapes:
         W = (torch.randn(n, k, device="cuda") * 0.02).half()
         lin = L.Fp6Linear.from_dense(W)
-        for m in (int(v) for v in args.m.split(",")):
+        for m, split in ((int(v), sp) for v in args.m.split(",") for sp in splits):
             x = torch.randn(m, k, device="cuda").half()
             y = torch.empty(m, n, device="cuda", dtype=torch.float16)
-            t6 = time_fn(lambda: L.w6a16_linear(x, lin.weight, out=y, split_k=args.split), flush=flush)
+            t6 = time_fn(lambda: L.w6a16_linear(x, lin.weight, out=y, split_k=split), flush=flush)
             t16 = time_fn(lambda: torch.matmul(x, W.t()), flush=flush)
             ref = (x.float() @ W.float().t())
             err = float((y.float() - ref).abs().max() / ref.abs().max())
             wbytes = lin.weight.stream_bytes() + 2 * m * k + 2 * m * n
-            print(json.dumps({"n": n, "k": k, "m": m, "plan": L.plan(m, n, k, args.split),
+            print(json.dumps({"n": n, "k": k, "m": m, "split_k": split, "plan": L.plan(m, n, k, split),
                               "us_fp6": round(t6 * 1e6, 2), "us_cublas": round(t16 * 1e6, 2),
                               "speedup": round(t16 / t6, 3), "GBps": round(wbytes / t6 / 1e9, 1),
                               "TFLOPS": round(2 * m * n * k / t6 / 1e12, 2), "err_vs_fp16W": err}), flush=True)
