@@ -424,12 +424,6 @@ template <bool PEERS>
 using PeerMapsOf = typename std::conditional<PEERS, PeerMaps, NoPeerMaps>::type;
 __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 
-#ifndef LPQT_EXP_PEERS_LOCAL
-#define LPQT_EXP_PEERS_LOCAL 0  // experiment: gather launch stores only locally
-#endif
-#ifndef LPQT_EXP_PEERS_NOSYNC
-#define LPQT_EXP_PEERS_NOSYNC 0  // experiment: gather launch without the completion barrier
-#endif
 // Fused all-gather (lpqt_w6a16_linear_gather): the same element into every
 // peer's Y (each y[p] already offset to this rank's block).
 __device__ __forceinline__ void store_y_peers(const GemmArgs& a, const lpqt_peer_out& po, int n, int m, float v) {
@@ -1059,7 +1053,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (ytma) {
           ystage_put<BN>(a, ybuf, rr, c0, v, fs);
         } else {
-          if constexpr (PEERS && C::kYBufBytes == 0 && !LPQT_EXP_PEERS_LOCAL) {
+          if constexpr (PEERS && C::kYBufBytes == 0) {
             // (decode tiles always leave by the per-peer TMA stores: the host
             // refuses peer buffers the tensor maps cannot describe)
 #pragma unroll 1
@@ -1570,7 +1564,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
   tc_fence_before();
   __syncthreads();
-  if constexpr (PEERS && !LPQT_EXP_PEERS_NOSYNC) {
+  if constexpr (PEERS) {
     if (threadIdx.x == 0) peer_complete(po);
   }
   // CSK: no CTA may leave while a peer can still read its staging buffer or
