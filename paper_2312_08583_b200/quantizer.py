@@ -7,7 +7,8 @@ max|w|, S = RN_f16(peak/28), fold S*2^12, RTN codes of W/S and the canonical
 `dequantize_tensor` is the GPU `lpqt_fp6_dequantize_tensor` (f64 exact).
 FP6 (4+2) and FP5 (4+1) quantize under CGQ (one scale per output row) or FGQ
 (one per block of block_size columns; the GEMM needs blocks of whole 128-k
-tiles); INT4 is outside this path and raises InvalidScheme.
+tiles); INT4 asymmetric (the paper's comparator) quantizes per row or block
+too, with zero points, and runs the fused W4A16 GEMM (`linear.Int4Weight`).
 """
 
 from __future__ import annotations
