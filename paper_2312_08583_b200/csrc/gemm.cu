@@ -169,6 +169,9 @@ struct L2Prefetch {
 #ifndef LPQT_DECODE_KSTEP
 #define LPQT_DECODE_KSTEP 2  // decode (BN <= 32): 128-k tiles per stage
 #endif
+#ifndef LPQT_TILE_RING
+#define LPQT_TILE_RING 1
+#endif
 template <int BN, bool CSK, int WB = 6, bool FGQ = false>
 struct Cfg {
   static constexpr int kTileB = WB == 6 ? kTileBytes : kTileN * kTileK / 2;
@@ -209,7 +212,13 @@ struct Cfg {
   // phase); one issuer may use every whole slot TMEM holds
   static constexpr int kASlots =
       kMmaWarps == 1 ? (kACols / kAColsPerBuf) / kKStep : ((kACols / kAColsPerBuf) / kKStep) & ~1;
-  static constexpr int kBarCount = 2 * kWStages + 2 * kXStages + 2 * kASlots + 2 * kDBufs + 5;
+  // decode (2 k-tiles per stage, 2 issuers): instead of one 2-tile slot per
+  // issuer, each issuer / dequant-group pair owns a ring of 3 single-tile
+  // slots used in order, so a group may write the next stage's first tile
+  // while the MMAs still read the current stage's second one
+  static constexpr bool kTileRing = LPQT_TILE_RING && kKStep == 2 && kMmaWarps == 2 && kACols / kAColsPerBuf >= 6;
+  static constexpr int kABars = kTileRing ? 6 : kASlots;
+  static constexpr int kBarCount = 2 * kWStages + 2 * kXStages + 2 * kABars + 2 * kDBufs + 5;
   static constexpr int kSmemBytes = kXStages * kXStageBytes + kWStages * kWStageBytes + 2 * kStageBufBytes +
                                     2 * kYBufBytes + 8 * kBarCount + 16;
   static_assert(kWStages >= 2 && kXStages >= 2, "pipeline too shallow");
@@ -652,8 +661,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* full_x = empty_w + C::kWStages;
   uint64_t* empty_x = full_x + C::kXStages;
   uint64_t* afull = empty_x + C::kXStages;
-  uint64_t* aempty = afull + C::kASlots;
-  uint64_t* dfull = aempty + C::kASlots;
+  uint64_t* aempty = afull + C::kABars;
+  uint64_t* dfull = aempty + C::kABars;
   uint64_t* dempty = dfull + C::kDBufs;
   uint64_t* part_full = dempty + C::kDBufs;  // CSK [2]: this CTA's round partials from the senders
   uint64_t* stg_free = part_full + 2;        // CSK [2]: this CTA's staging buffer read by the reducer
@@ -688,8 +697,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_init(&full_x[s], 1);
         mbar_init(&empty_x[s], 1);  // MMA commit
       }
-      for (int b = 0; b < C::kASlots; ++b) {
-        mbar_init(&afull[b], kNumDqWarps / 2);
+      for (int b = 0; b < C::kABars; ++b) {
+        mbar_init(&afull[b], C::kTileRing ? kNumDqWarps / 4 : kNumDqWarps / 2);  // one tile's / stage's warps
         mbar_init(&aempty[b], 1);   // MMA commit
       }
       for (int d = 0; d < C::kDBufs; ++d) {
@@ -836,7 +845,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     };
     Cur wc{static_cast<uint32_t>(grp), 0u};   // W ring
-    Cur ac{static_cast<uint32_t>(grp), 0u};   // A ring
+    // A ring: slot grp of the 2-slot ring, or (tile ring) position tl of the
+    // group's own 3-slot ring (barriers grp * 3 + idx)
+    Cur ac{static_cast<uint32_t>(C::kTileRing ? tl : grp), 0u};
+    const uint32_t a_bar0 = C::kTileRing ? static_cast<uint32_t>(grp * 3) : 0u;
+    const uint32_t t_row = tmem_base + (static_cast<uint32_t>(lg * 32) << 16);
     StageIter<Sched, KS> it;
     if constexpr (RAGGED) it.start(a, sc, grp);
     auto stage_nt = [&]() -> int {
@@ -898,10 +911,11 @@ __global__ void __launch_bounds__(kThreads, 1)
           if constexpr (FGQ) scale_f16x2(r, fs2);
         }
       }
-      mbar_wait_u32<WM>(ae0 + 8 * ac.idx, ac.ph ^ 1u);
+      mbar_wait_u32<WM>(ae0 + 8 * (a_bar0 + ac.idx), ac.ph ^ 1u);
       tc_fence_after();
       if (act) {
-        const uint32_t ta = t_lane + ac.idx * (KS * kAColsPerBuf);
+        const uint32_t ta = C::kTileRing ? t_row + (a_bar0 + ac.idx) * kAColsPerBuf
+                                         : t_lane + ac.idx * (KS * kAColsPerBuf);
         tmem_st_x32(ta, r);
 #pragma unroll
         for (int h = 1; h < kSegs; ++h) {
@@ -931,8 +945,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       tmem_wait_st();
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive_u32(af0 + 8 * ac.idx);
-      ac.adv2(C::kASlots);
+      if (lane == 0) mbar_arrive_u32(af0 + 8 * (a_bar0 + ac.idx));
+      ac.adv2(C::kTileRing ? 3u : static_cast<uint32_t>(C::kASlots));
     }
     if (warp == 0 && lane == 0) CTA_STAMP(3);
     if (warp == 8 && lane == 0) CTA_STAMP(16);
@@ -963,7 +977,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           const int slot = it % C::kASlots;
           mbar_wait<WM>(&full_x[xs], (it / C::kXStages) & 1);
           if (it == mw && lane == 0) CTA_STAMP(14);
-          mbar_wait<WM>(&afull[slot], (it / C::kASlots) & 1);
+          if constexpr (!C::kTileRing) mbar_wait<WM>(&afull[slot], (it / C::kASlots) & 1);
           tc_fence_after();
           const uint32_t e = elect_one();
           // descriptor of X block 0 of this stage; every other operand is a
@@ -974,18 +988,28 @@ __global__ void __launch_bounds__(kThreads, 1)
           const bool first = (s == s_first);
 #pragma unroll
           for (int t = 0; t < KS; ++t) {
+            uint32_t ta_t = ta + t * kAColsPerBuf;
+            int tb = 0;
+            if constexpr (C::kTileRing) {
+              // position 2 * (it >> 1) + t of this issuer's 3-slot ring
+              const int pos = 2 * (it >> 1) + t, sl = pos % 3;
+              tb = mw * 3 + sl;
+              mbar_wait<WM>(&afull[tb], (pos / 3) & 1);
+              tc_fence_after();
+              ta_t = tmem_base + tb * kAColsPerBuf;
+            }
             if (t < nt) {
 #pragma unroll
               for (int j = 0; j < kTileK / 16; ++j) {
                 const uint32_t off = (t * C::kXTileBytes + (j >> 2) * (BN * 128) + (j & 3) * 32) >> 4;
                 const bool init = first && t == 0 && j == 0;
-                mma_f16_ts_if(e, d_tmem, ta + t * kAColsPerBuf + j * 8, bd_lo + off, bd_hi, idesc,
-                              init ? 0u : 1u);
+                mma_f16_ts_if(e, d_tmem, ta_t + j * 8, bd_lo + off, bd_hi, idesc, init ? 0u : 1u);
               }
             }
+            if constexpr (C::kTileRing) tc_commit_if(e, &aempty[tb]);  // this tile's slot is free once read
           }
           tc_commit_if(e, &empty_x[xs]);
-          tc_commit_if(e, &aempty[slot]);
+          if constexpr (!C::kTileRing) tc_commit_if(e, &aempty[slot]);
         }
         if (s_first < sg.len) {
           tc_commit_elect(&dfull[d]);
