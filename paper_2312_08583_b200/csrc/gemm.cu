@@ -474,7 +474,6 @@ __device__ __forceinline__ uint32_t ld_acquire_sys_u32(const uint32_t* p) {
 __device__ __forceinline__ void peer_complete(const lpqt_peer_out& po) {
   const int prev = atom_add_acq_rel_gpu(po.done, 1);
   if (prev != static_cast<int>(gridDim.x) - 1) return;
-  __threadfence_system();
   const uint32_t* mine = nullptr;
 #pragma unroll
   for (int p = 0; p < LPQT_MAX_PEERS; ++p) {
