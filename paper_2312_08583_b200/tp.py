@@ -153,6 +153,14 @@ def gather_linear(weight, xt, ldx: int, m: int, peer_y: list[int], peer_flags: l
         ws.numel() if ws is not None else 0, flags, ctypes.byref(po), _lib.stream_ptr()), "w6a16_linear_gather")
 
 
+def _peer_ptrs(handle, local, rank: int) -> list[int]:
+    """Every peer's address of `local` (a tensor inside a symmetric
+    allocation): the peer's allocation base plus this tensor's offset in it."""
+    base = list(handle.buffer_ptrs)
+    off = local.data_ptr() - base[rank]
+    return [b + off for b in base]
+
+
 class FusedColumnParallelFp6Linear:
     """y[M, N] = x[M, K] @ W_hat^T with W's rows sharded over the group and
     the all-gather fused into the GEMM: every rank's epilogue writes its
@@ -210,6 +218,7 @@ class FusedColumnParallelFp6Linear:
         self.epoch += 1
         i = self.epoch & 1
         code = {t.float32: _lib.F32, t.float16: _lib.F16, t.bfloat16: _lib.BF16}[self.dtype]
-        gather_linear(self.weight, x2, ldx, m, list(self.buf_h[i].buffer_ptrs), list(self.flag_h.buffer_ptrs),
-                      self.rank, self.epoch, self.done, code, "mn", self.n, sum(self.sizes[:self.rank]))
+        gather_linear(self.weight, x2, ldx, m, _peer_ptrs(self.buf_h[i], self.bufs[i], self.rank),
+                      _peer_ptrs(self.flag_h, self.flag_t, self.rank), self.rank, self.epoch, self.done, code, "mn",
+                      self.n, sum(self.sizes[:self.rank]))
         return self.bufs[i][:m]
