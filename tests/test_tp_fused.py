@@ -90,3 +90,29 @@ def test_fused_gather_single_rank_is_a_plain_launch():
     y1 = torch.empty(1024, 1, dtype=torch.float16, device="cuda")
     with pytest.raises(L.ShapeError):
         tp.gather_linear(w, x[:1], 2048, 1, [y1.data_ptr()], [flags.data_ptr()], 0, 5, done, _lib.F16, "nm", 1, 0)
+
+
+@pytest.mark.gpu
+def test_fused_layer_world1_symmetric_memory():
+    """FusedColumnParallelFp6Linear end to end on a one-rank NCCL group:
+    torch symmetric memory for y and the flags, four calls (both output
+    buffers twice), equal to the plain launch."""
+    import os
+    import socket
+
+    import torch
+    import torch.distributed as dist
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda:0"))
+    try:
+        W = (torch.randn(2048, 4096, device="cuda") * 0.02).half()
+        layer = tp.FusedColumnParallelFp6Linear.quantize_shard(W, m_max=32)
+        for m in (1, 16, 32, 5):
+            x = torch.randn(m, 4096, device="cuda").half()
+            y = layer(x)
+            assert torch.equal(y, L.w6a16_linear(x, layer.weight)), m
+    finally:
+        dist.destroy_process_group()
