@@ -1765,10 +1765,11 @@ static Plan make_plan(int64_t M, int64_t N, int64_t K, int split_k, int flags, i
   if (split_k == 0 && p.kstep == 1) {
     const int64_t cap = LPQT_SK_SPLIT_WIDE > 0 ? LPQT_SK_SPLIT_WIDE : std::min(4, std::max(1, p.k_tiles / 24));
     if (g > p.tiles * cap) g = p.tiles * cap;
-    // prefill tiles that fit one wave: one whole tile per CTA beats spreading
-    // them over every SM (the BN >= 128 partial reduction costs more than
-    // the idle SMs; profiles/r01_v14_probe_prefill_split.jsonl)
-    if (p.bn >= 128 && p.tiles <= sms) g = p.tiles;
+    // prefill (BN 192) tiles that fit one wave: one whole tile per CTA beats
+    // spreading them over every SM (the 128 x 192 partial reduction costs
+    // more than the idle SMs); at BN 128 splitting still wins
+    // (profiles/r01_v14_probe_prefill_split.jsonl, _onewave_bn192.jsonl)
+    if (p.bn >= 192 && p.tiles <= sms) g = p.tiles;
   }
   if (g > p.total) g = p.total;
   if (p.tiles > kMaxCounters) g = p.tiles;  // one whole tile per CTA: no counters needed
