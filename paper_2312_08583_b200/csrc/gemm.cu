@@ -1630,7 +1630,12 @@ static int pick_bn(int64_t M) {
   if (M <= 32) return 32;
   if (M <= 64) return 64;
   if (M <= 128 || LPQT_PREFILL_BN == 128) return 128;
-  return LPQT_PREFILL_BN;
+  if (LPQT_PREFILL_BN != 192) return LPQT_PREFILL_BN;
+  // per 128-k step a 128-row weight tile costs ~600 cycles at N = 128 (the
+  // dequant bound) and ~768 at N = 192 (the MMA bound): take the width whose
+  // batch tiles cover M in the fewest cycles (M = 256: 2 x 128, not 2 x 192)
+  const int64_t c128 = (M + 127) / 128 * 600, c192 = (M + 191) / 192 * 768;
+  return c128 < c192 ? 128 : 192;
 }
 
 template <int BN, bool CSK>
