@@ -1774,7 +1774,10 @@ static Plan make_plan(int64_t M, int64_t N, int64_t K, int split_k, int flags, i
     // spreading them over every SM (the 128 x 192 partial reduction costs
     // more than the idle SMs); at BN 128 splitting still wins
     // (profiles/r01_v14_probe_prefill_split.jsonl, _onewave_bn192.jsonl)
-    if (p.bn >= 192 && p.tiles <= sms) g = p.tiles;
+    // (BN 128 with several batch tiles: only when the wave is >= 3/4 full;
+    // profiles/r01_v14_abx_onewave_bn128.jsonl)
+    if ((p.bn >= 192 || (p.bn == 128 && p.m_tiles > 1 && 4 * p.tiles >= 3 * (int64_t)sms)) && p.tiles <= sms)
+      g = p.tiles;
   }
   if (g > p.total) g = p.total;
   if (p.tiles > kMaxCounters) g = p.tiles;  // one whole tile per CTA: no counters needed
