@@ -1,17 +1,21 @@
 """bench.py — W6A16 (FP6 e3m2 weight, FP16 activation) linear on B200.
 
-Workload (N=1, BASELINE.json configs[1]): one LLaMA-2-7B decoder block's four
-linear layers (QKV 12288x4096, O 4096x4096, gate_up 22016x4096, down
-4096x11008) at decode batch M (default 16).  A "step" = those four W6A16
-GEMMs over one batch.  Synthetic data: random-init N(0, 0.02) weights
-quantized on the GPU, N(0, 1) fp16 activations.
+Workload (N=1, the north-star target, BASELINE.json configs[3] at TP=1): one
+LLaMA-2-70B decoder block's four linear layers (QKV 10240x8192, O 8192x8192,
+gate_up 57344x8192, down 8192x28672) at decode batch M (default 16).  A
+"step" = those four W6A16 GEMMs over one batch.  Synthetic data: random-init
+N(0, 0.02) weights quantized on the GPU, N(0, 1) fp16 activations.  Extra
+device-timed lines ride along: the same step at M = 1 and the LLaMA-2-7B step
+(configs[1]) at M = 16 (`--no-extras` skips them; `--model llama2-7b` makes
+7B the headline).
 
 Metric (BASELINE.json): "W6A16 linear TFLOPS & weight HBM GB/s vs roofline
 and cuBLAS FP16, batch 1-512" -> value = algorithmic HBM GB/s of the step
 (FP6 planes 0.75 B/weight + 2 B/row scales + fp16 X + fp16 Y); TFLOPS,
 cuBLAS fp16 and the roofline fraction ride along.
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--m 16] [--impl ours|reference]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--m 16] [--model llama2-70b|llama2-7b]
+                  [--impl ours|reference]
 
 N>1 (torchrun): column-sharded tensor parallelism: every rank
 holds N/P rows of every layer, runs its shard GEMM, and one NCCL
@@ -19,8 +23,10 @@ all_gather_into_tensor per layer assembles Y[N, M] -> "scaling": "strong".
 
 Timing: W untimed warm-up steps, then EXACTLY K steps replayed from CUDA
 graphs, bracketed by barrier + synchronize, device-timed with CUDA events,
-max over ranks.  L2: the step's weights (151 MB FP6) are rotated over two
-distinct copies (302 MB > 2 x 126 MB L2), so every step reads cold weights.
+max over ranks.  L2: the step's weights (646 MB FP6 at 70B, 151 MB at 7B) are
+rotated over >= 2 distinct copies (> 2 x 126 MB L2), so every step reads cold
+weights.  cpu_baseline / --impl reference: the reference package itself
+(baseline/_ref, tools/install_reference.sh) on a bounded row sample.
 """
 
 from __future__ import annotations
@@ -67,6 +73,12 @@ def step_bytes(layers, m):
         seg2 = ((2 * nk + 7) // 8 + 3) // 4 * 4
         tot += seg4 + seg2 + 2 * n + 2 * m * k + 2 * m * n
     return tot
+
+
+def sample_bytes(layers, m, rows):
+    """The share of the step's algorithmic bytes a row sample covers: each
+    layer's bytes x rows / N (X and the scales amortised with the rows)."""
+    return sum(layer_bytes(n, k, m) * min(rows, n) / n for _, n, k in layers)
 
 
 def layer_bytes(n, k, m):
@@ -179,14 +191,11 @@ def build_layers(layers, world, rank, copies, seed=0):
     return sets
 
 
-def run_ours(args, world, rank):
+def run_ours(args, world, rank, layers, m, e2e=True, burn_in=None):
     import torch
     import paper_2312_08583_b200 as L
     from paper_2312_08583_b200 import _lib
-    from paper_2312_08583_b200.linear import gemm_nm
 
-    layers = LAYERS_7B if args.model == "llama2-7b" else LAYERS_70B
-    m = args.m
     l2 = torch.cuda.get_device_properties(0).L2_cache_size
     fp6_set = step_bytes(layers, 0) // world
     copies = max(2, -(-2 * l2 // max(fp6_set, 1)))
@@ -256,7 +265,7 @@ def run_ours(args, world, rank):
     # burn-in so the clock sampler sees the part under load, then the timed region
     launches_before = _lib.launch_count()
     with ClockSampler(int(os.environ.get("LOCAL_RANK", "0"))) as clk:
-        t_end = time.time() + args.burn_in
+        t_end = time.time() + (args.burn_in if burn_in is None else burn_in)
         while time.time() < t_end:
             for c in range(copies):
                 graphs[c].replay()
@@ -299,7 +308,10 @@ def run_ours(args, world, rank):
     if rank == 0 or world > 1:
         res["cublas"] = time_cublas(layers, world, rank, m, args)
     # e2e through the public API with host buffers
-    res["e2e"] = time_e2e(layers, sets[0], world, rank, m, args)
+    if e2e:
+        res["e2e"] = time_e2e(layers, sets[0], world, rank, m, args)
+    del sets, graphs
+    torch.cuda.empty_cache()
     return res
 
 
@@ -435,45 +447,112 @@ def time_e2e(layers, wset, world, rank, m, args):
 
 
 # ---------------------------------------------------------------------------
-def cpu_baseline(layers, m, budget_s=12.0):
-    """Oracle port of the reference CPU path (gemm.py:65-94: unpack -> value
-    table -> ascending-k fp32 loop -> row scale), timed on this host, 1 core,
-    on a bounded sample: the full step's layers, each restricted to its first
-    R rows (sample), repeated until `budget_s` elapsed."""
-    from oracle import lpqt_oracle as O
-    rng = np.random.default_rng(0)
-    rows = 256
-    sample = []
-    for _, n, k in layers:
-        W = (rng.standard_normal((rows, k)) * 0.02).astype(np.float16)
-        q = O.quantize_tensor(W, bias_shift=True)
-        X = rng.standard_normal((k, m)).astype(np.float16)
-        sample.append((q, rows, k, X))
-    nbytes = step_bytes([("", rows, k) for _, _, k in layers], m)
+REF_DIR = os.path.join(ROOT, "baseline", "_ref")
+
+
+def load_reference():
+    """The UNMODIFIED reference package (lpqt 0.1.0) installed in baseline/_ref
+    by tools/install_reference.sh (pip --target; git-ignored, travels to the
+    GPU box).  None when it is not staged (then the oracle port stands in)."""
+    if not os.path.isdir(os.path.join(REF_DIR, "lpqt")):
+        return None
+    if REF_DIR not in sys.path:
+        sys.path.insert(0, REF_DIR)
+    import lpqt
+    assert os.path.dirname(os.path.dirname(os.path.abspath(lpqt.__file__))) == REF_DIR, lpqt.__file__
+    return lpqt
+
+
+class _PortAsRef:
+    """The oracle restatement behind the reference's call signatures (used only
+    when baseline/_ref is absent)."""
+
+    def __init__(self):
+        from oracle import lpqt_oracle as O
+        self.O = O
+
+    def quantize(self, W):
+        return self.O.quantize_tensor(W, bias_shift=True)
+
+    def gemm(self, q, X):
+        n = q["scales"].size
+        return self.O.gemm_quantized(q["codes"], q["scales"], n, q["codes"].size // max(n, 1), X)
+
+
+class _Ref:
+    def __init__(self, lpqt):
+        self.lpqt = lpqt
+        self.scheme = lpqt.QuantScheme(lpqt.Granularity.CGQ, lpqt.TensorFormat.FP6_E3M2)
+
+    def quantize(self, W):
+        # BASELINE.md §3: quantize_tensor(W.astype(float64), CGQ FP6, bias_shift=True)
+        return self.lpqt.quantize_tensor(W.astype(np.float64), self.scheme, bias_shift=True)
+
+    def gemm(self, q, X):
+        return self.lpqt.gemm_quantized(q, X)
+
+
+def reference_impl():
+    lp = load_reference()
+    return (_Ref(lp), "reference") if lp is not None else (_PortAsRef(), "port")
+
+
+def _sample_inputs(layers, m, rows, seed):
+    """BASELINE.md §3 inputs on a row sample: W = N(0,1)*0.02 f32 -> fp16 (the
+    first `rows` rows of each layer), X = N(0,1) [K, M] fp16."""
+    out = []
+    for i, (_, n, k) in enumerate(layers):
+        rng = np.random.default_rng(seed + i)
+        W = (rng.standard_normal((rows, k), dtype=np.float32) * 0.02).astype(np.float16)
+        X = np.random.default_rng(seed + 100 + i).standard_normal((k, m)).astype(np.float16)
+        out.append((W, X))
+    return out
+
+
+def cpu_baseline(layers, m, budget_s=15.0):
+    """The reference's own CPU path (baseline/_ref lpqt: quantize_tensor +
+    gemm_quantized, quantizer.py:189-248 / gemm.py:65-94) timed on this
+    host, single process (numpy elementwise, effectively one core), on a
+    bounded sample: the first R rows of each of the step's layers.
+    `value` = algorithmic GB/s of gemm_quantized over the sample (the
+    metric's unit); the quantize rate rides along."""
+    impl, kind = reference_impl()
+    rows = 64
+    sample = _sample_inputs(layers, m, rows, seed=0)
+    t0 = time.perf_counter()
+    qs = [impl.quantize(W) for W, _ in sample]
+    t_quant = time.perf_counter() - t0
+    nbytes = sample_bytes(layers, m, rows)
     reps = 0
     t0 = time.perf_counter()
     while True:
-        for q, r, k, X in sample:
-            O.gemm_quantized(q["codes"], q["scales"], r, k, X)
+        for q, (_, X) in zip(qs, sample):
+            impl.gemm(q, X)
         reps += 1
         if time.perf_counter() - t0 > budget_s:
             break
     t = time.perf_counter() - t0
-    return {"value": round(nbytes * reps / t / 1e9, 5), "unit": "GB/s", "cores": 1, "kind": "port",
-            "sample": f"oracle gemm_quantized on the first {rows} rows of each of the 4 layers at M={m}, "
-                      f"{reps} reps in {t:.1f}s (numpy, single process)"}
+    n_weights = sum(rows * k for _, _, k in layers)
+    return {"value": round(nbytes * reps / t / 1e9, 5), "unit": "GB/s", "cores": 1, "kind": kind,
+            "quantize_weights_per_s": round(n_weights / t_quant, 1),
+            "sample": f"{'reference lpqt 0.1.0 (baseline/_ref)' if kind == 'reference' else 'oracle port'}: "
+                      f"quantize_tensor (CGQ FP6, bias_shift) of the first {rows} rows of each of the "
+                      f"{len(layers)} layers ({n_weights} weights, {t_quant:.2f}s), then gemm_quantized at M={m} "
+                      f"on those rows, {reps} reps in {t:.1f}s; single process, numpy"}
 
 
 def run_reference(args, world, rank):
-    """--impl reference: the reference's CPU algorithm (oracle port) on all host
-    threads, row-parallel over a process pool (SPEC.md:373-375 permits
-    row parallelism), each step a bounded row sample of the workload."""
+    """--impl reference: the reference's own CPU implementation (baseline/_ref
+    lpqt gemm_quantized) on all host threads, row-parallel over a process pool
+    (SPEC.md:373-375 permits row parallelism); each step = every worker's
+    gemm_quantized over its row sample of each layer."""
     import multiprocessing as mp
     layers = LAYERS_7B if args.model == "llama2-7b" else LAYERS_70B
     m = args.m
     cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
-    rows_per_worker = 32
+    rows_per_worker = 16
     with mp.get_context("fork").Pool(cores, initializer=_ref_init, initargs=(layers, m, rows_per_worker)) as pool:
+        kinds = set(pool.map(_ref_kind, range(cores)))
         for _ in range(max(args.warmup, 1)):
             pool.map(_ref_step, range(cores))
         t_budget = 120.0
@@ -485,30 +564,33 @@ def run_reference(args, world, rank):
             if time.perf_counter() - t0 > t_budget:
                 break
         t = time.perf_counter() - t0
-    nbytes = step_bytes([("", rows_per_worker * cores, k) for _, _, k in layers], m)
+    kind = kinds.pop() if len(kinds) == 1 else "port"
+    nbytes = sample_bytes(layers, m, rows_per_worker * cores)
     value = nbytes * steps / t / 1e9
-    sample = (f"oracle gemm_quantized (numpy ascending-k) on {rows_per_worker} rows x {cores} processes of "
-              f"each 7B layer per step, M={m}; {steps} steps timed")
-    return {"value": value, "t": t, "steps": steps, "cores": cores, "sample": sample}
+    sample = (f"{'reference lpqt 0.1.0 (baseline/_ref)' if kind == 'reference' else 'oracle port'} "
+              f"gemm_quantized on {rows_per_worker} rows x {cores} processes of each {args.model} layer per step, "
+              f"M={m}; {steps} steps timed")
+    return {"value": value, "t": t, "steps": steps, "cores": cores, "sample": sample, "kind": kind}
 
 
 _REF = {}
 
 
 def _ref_init(layers, m, rows):
-    from oracle import lpqt_oracle as O
-    rng = np.random.default_rng(os.getpid())
-    _REF["work"] = []
-    for _, n, k in layers:
-        W = (rng.standard_normal((rows, k)) * 0.02).astype(np.float16)
-        q = O.quantize_tensor(W, bias_shift=True)
-        _REF["work"].append((q["codes"], q["scales"], rows, k, rng.standard_normal((k, m)).astype(np.float16)))
+    impl, kind = reference_impl()
+    _REF["impl"], _REF["kind"] = impl, kind
+    sample = _sample_inputs(layers, m, rows, seed=os.getpid())
+    _REF["work"] = [(impl.quantize(W), X) for W, X in sample]
+
+
+def _ref_kind(_):
+    return _REF["kind"]
 
 
 def _ref_step(_):
-    from oracle import lpqt_oracle as O
-    for codes, scales, r, k, X in _REF["work"]:
-        O.gemm_quantized(codes, scales, r, k, X)
+    impl = _REF["impl"]
+    for q, X in _REF["work"]:
+        impl.gemm(q, X)
     return 0
 
 
@@ -516,13 +598,14 @@ def _ref_step(_):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=2000)
+    ap.add_argument("--steps", type=int, default=1000)
     ap.add_argument("--warmup", type=int, default=20)
     ap.add_argument("--m", type=int, default=16, help="decode batch (tokens)")
-    ap.add_argument("--model", default="llama2-7b", choices=["llama2-7b", "llama2-70b"])
+    ap.add_argument("--model", default="llama2-70b", choices=["llama2-7b", "llama2-70b"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--burn-in", type=float, default=1.5, help="seconds of untimed load before timing")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-extras", action="store_true", help="skip the extra M=1 / 7B lines")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -531,6 +614,8 @@ def main():
     layers = LAYERS_7B if args.model == "llama2-7b" else LAYERS_70B
     workload = f"{args.model} decoder-block linears (QKV/O/gate_up/down) decode M={args.m}"
     config = {"workload": workload, "layers": [f"{n}x{k}" for _, n, k in layers], "batch_m": args.m,
+              "baseline_config": "BASELINE.json configs[3] (LLaMA-2-70B shapes; TP degree = n_gpus)"
+              if args.model == "llama2-70b" else "BASELINE.json configs[1] (LLaMA-2-7B shapes)",
               "tensor_parallel": world, "parallelism": f"tp{world} column-sharded + NCCL all-gather"
               if world > 1 else "single GPU", "activations": "fp16", "weights": "FP6 e3m2 (4+2), per-row f16 scale",
               "l2_hygiene": "inputs larger than L2: weights rotated over >=2 distinct copies (>2x L2) per step"}
@@ -544,7 +629,7 @@ def main():
                 "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
                 "data": "synthetic", "config": config, "impl": "reference",
                 "cpu_baseline": {"value": round(r["value"], 6), "unit": "GB/s", "cores": r["cores"],
-                                 "kind": "port", "sample": r["sample"]},
+                                 "kind": r["kind"], "sample": r["sample"]},
                 "e2e": {"value": round(r["value"], 6), "unit": "GB/s", "h2d_bytes_per_step": 0,
                         "d2h_bytes_per_step": 0}}
         print(json.dumps(line), flush=True)
@@ -553,8 +638,8 @@ def main():
     import torch
     world, rank, _ = setup_dist(args)
     peaks = load_peaks()
-    res = run_ours(args, world, rank)
     m = args.m
+    res = run_ours(args, world, rank, layers, m)
     t_step = res["t"] / args.steps
     flops = step_flops(layers, m)
     # roofline of the dominant kernel: the W6A16 GEMM is every launch of the
@@ -573,6 +658,21 @@ def main():
             traffic = tr["bytes_per_step"] // world
             traffic_note = {"traffic_over_algorithmic": tr["ratio"], "source": "profiles/ncu_traffic.json: " +
                             tr["source"]}
+    extras = []
+    if not args.no_extras:
+        # the other north-star decode point (M = 1) and the 7B step (BASELINE
+        # configs[1]); device-timed like the headline, no e2e
+        for model, mx in ((args.model, 1 if m != 1 else 16), ("llama2-7b" if args.model != "llama2-7b"
+                                                                else "llama2-70b", 16)):
+            lx = LAYERS_7B if model == "llama2-7b" else LAYERS_70B
+            rx = run_ours(args, world, rank, lx, mx, e2e=False, burn_in=0.5)
+            tx = rx["t"] / args.steps
+            ax = step_bytes(lx, mx) / world / tx / 1e9
+            extras.append({"workload": f"{model} decoder-block linears decode M={mx}", "value": round(
+                step_bytes(lx, mx) * args.steps / rx["t"] / 1e9, 2), "unit": "GB/s",
+                "ms_per_step": round(tx * 1e3, 5), "roofline_frac": round(ax / peaks["hbm_gbs"], 4),
+                "speedup_vs_cublas_fp16": round(rx["cublas"]["ms_per_step"] / (tx * 1e3), 3),
+                "clocks": rx["clocks"], "per_launch_serialised": rx["per_layer"]})
     if rank != 0:
         return
     line = {
@@ -593,6 +693,7 @@ def main():
         "e2e": res["e2e"],
         "gpu_launches": res["gpu_launches"],
         "clocks": res["clocks"],
+        "extras": extras,
     }
     if world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(layers, m)

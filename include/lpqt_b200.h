@@ -348,6 +348,28 @@ int lpqt_w4a16_linear_blocks(const uint8_t* tiles, const uint32_t* params,
                              int64_t workspace_bytes, int flags,
                              void* stream);
 
+/* Reference-order GEMMs (exact.cu): the reference's loops replayed one
+ * thread per output element, k ascending, every product and sum rounded
+ * separately — bit-identical to the reference on the same inputs.  They run
+ * the reference-API calls the A16 tcgen05 kernel cannot reproduce within the
+ * reference's tolerance: float32 / float64 activations, FGQ blocks of any
+ * width, INT4 (S * sum(level x) + Z * sum(x)).
+ *   lpqt_gemm_exact_quantized — gemm.py:65-110 gemm_quantized: codes [N, K]
+ *     uint8 row-major (fmt 0 FP6 e3m2 codes, 1 FP5 e3m1 codes, 2 INT4
+ *     levels), f16 scales (and INT4 zero points) one per row (block <= 0 or
+ *     >= K) or per block of `block` columns row-major, X [K, M] float32,
+ *     Y [N, M] float32.
+ *   lpqt_gemm_exact_dense — gemm.py:41-51 gemm_dense (dtype LPQT_F32) and
+ *     gemm.py:28-38 gemm_reference (LPQT_F64): W [N, K], X [K, M], Y [N, M]
+ *     in that dtype. */
+int lpqt_gemm_exact_quantized(const uint8_t* codes, int fmt,
+                              const uint16_t* scales, const uint16_t* zeros,
+                              int64_t N, int64_t K, int64_t block,
+                              const float* X, int64_t M, float* Y,
+                              void* stream);
+int lpqt_gemm_exact_dense(const void* W, const void* X, int dtype, int64_t N,
+                          int64_t K, int64_t M, void* Y, void* stream);
+
 /* Number of kernel launches performed by this library since load (for the
  * bench's gpu_launches claim). */
 int64_t lpqt_launch_count(void);

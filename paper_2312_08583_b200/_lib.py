@@ -111,6 +111,8 @@ SIGNATURES = {
     "lpqt_w6a16_linear_gather": (_I32, [_P, _P, _I64, _P, _I64, _I64, _I64, _I64, _I32, _I32, _I64, _I32, _P,
                                         _I64, _I32, _P, _P]),
     "lpqt_fgq_stage_params": (_I32, [_P, _P, _I64, _I64, _I64, _P, _P]),
+    "lpqt_gemm_exact_quantized": (_I32, [_P, _I32, _P, _P, _I64, _I64, _I64, _P, _I64, _P, _P]),
+    "lpqt_gemm_exact_dense": (_I32, [_P, _P, _I32, _I64, _I64, _I64, _P, _P]),
     "lpqt_launch_count": (_I64, []),
 }
 
@@ -239,19 +241,52 @@ class Flags:
 
 
 class Workspace:
-    """Per-device, grow-only, zero-initialised GEMM workspace (split-K
-    partials + self-resetting tile counters)."""
+    """GEMM workspace (split-K partials + self-resetting tile counters),
+    zero-initialised, one grow-only buffer per (device, stream).
 
-    _per_device: dict = {}
+    * Streams never share a buffer, so split-K GEMMs running concurrently on
+      two streams cannot race on each other's tile counters / partials.
+    * A buffer that is outgrown is retired, never freed: a CUDA graph captured
+      earlier keeps pointing at valid, still-zeroed memory.
+    * Inside a graph capture nothing is resized: an adequate buffer of the
+      capturing stream is used as is, else the default stream's (a graph is
+      replayed on the launching stream, normally the default one, and is then
+      serialised with that stream's eager work); otherwise a capture-private
+      buffer is allocated whose zero-fill is a node of the captured graph (so
+      it is zeroed on every replay, and no eager launch ever sees it).
+      Graphs replayed concurrently with split-K GEMMs on other streams should
+      pass their own buffer.
+    Callers may also pass their own zeroed buffer (`workspace=` in linear.py).
+    """
+
+    _per_stream: dict = {}
+    _retired: list = []
+    _captured: list = []
 
     @classmethod
     def get(cls, nbytes: int):
         t = torch()
         dev = device()
-        cur = cls._per_device.get(dev.index)
-        if cur is None or cur.numel() < nbytes:
-            cur = t.zeros(max(nbytes, 1 << 20), dtype=t.uint8, device=dev)
-            cls._per_device[dev.index] = cur
+        stream = t.cuda.current_stream(dev)
+        key = (dev.index, stream.cuda_stream)
+        cur = cls._per_stream.get(key)
+        if cur is not None and cur.numel() >= nbytes:
+            return cur
+        if t.cuda.is_current_stream_capturing():
+            # torch captures on a side stream but a graph replays on the stream
+            # it is launched from — normally the default stream, whose eager
+            # work it is then serialised with: adopt that stream's buffer
+            dflt = cls._per_stream.get((dev.index, t.cuda.default_stream(dev).cuda_stream))
+            if dflt is not None and dflt.numel() >= nbytes:
+                return dflt
+            buf = t.zeros(max(nbytes, 1 << 20), dtype=t.uint8, device=dev)   # memset captured in the graph
+            cls._captured.append(buf)
+            return buf
+        if cur is not None:
+            cls._retired.append(cur)
+        size = max(nbytes, 1 << 20, 2 * cur.numel() if cur is not None else 0)
+        cur = t.zeros(size, dtype=t.uint8, device=dev)
+        cls._per_stream[key] = cur
         return cur
 
 

@@ -106,12 +106,12 @@ class Fp6Weight:
 
     @classmethod
     def from_quantized(cls, q) -> "Fp6Weight":
-        from .quantizer import _require_path, device_planes, scale_block
+        from .quantizer import _require_path, cache_of, device_planes, scale_block
         _require_path(q.scheme)
-        cache = q.device_cache
+        s4, s2, sc = device_planes(q)   # validates lengths / code_count first
+        cache = cache_of(q)
         if cache is not None and "weight" in cache:
             return cache["weight"]
-        s4, s2, sc = device_planes(q)
         fmt = "fp5" if q.scheme.fmt.minifloat.mantissa_bits == 1 else "fp6"
         w = cls.from_planes(s4, s2, sc, q.rows, q.cols, block=scale_block(q.scheme), fmt=fmt)
         if cache is not None:
@@ -176,11 +176,11 @@ class Int4Weight:
     @classmethod
     def from_quantized(cls, q) -> "Int4Weight":
         from .errors import InvalidScheme, PayloadMismatch
-        from .quantizer import scale_block
+        from .quantizer import cache_of, scale_block
         block = scale_block(q.scheme)
         if block and block < q.cols and block % TILE:
             raise InvalidScheme(f"FGQ block_size {block} is not a multiple of 128: outside the B200 GEMM path")
-        cache = q.device_cache
+        cache = cache_of(q)
         if cache is not None and "weight" in cache:
             return cache["weight"]
         t = _lib.torch()
@@ -238,10 +238,18 @@ def plan(m: int, n: int, k: int, split_k: int = 0, sched: str = "auto") -> dict:
 
 
 def _launch(weight: Fp6Weight, xt, ldx: int, m: int, y, y_dtype: int, y_layout: int, ldy: int, split_k: int,
-            sched: str = "auto", prefetch: "Fp6Weight | None" = None, prefetch_bytes: int = 0):
+            sched: str = "auto", prefetch: "Fp6Weight | None" = None, prefetch_bytes: int = 0, workspace=None):
     lib = _lib.load()
     ws_bytes = int(lib.lpqt_w6a16_workspace_bytes(m, weight.n, weight.k, split_k))
-    ws = _lib.Workspace.get(ws_bytes) if ws_bytes else None
+    if workspace is not None:
+        # caller-owned: zero-initialised once by the caller, never shared
+        # between concurrently running GEMMs (the tile counters self-reset)
+        if workspace.numel() * workspace.element_size() < ws_bytes:
+            from .errors import LpqtError
+            raise LpqtError(f"workspace too small: {ws_bytes} bytes needed")
+        ws = workspace.view(_lib.torch().uint8) if ws_bytes else None
+    else:
+        ws = _lib.Workspace.get(ws_bytes) if ws_bytes else None
     flags = (_lib.LAUNCH_PDL if weight.static else 0) | _sched_flags(sched)
     if weight.block and weight.block % TILE:
         from .errors import InvalidScheme
@@ -293,15 +301,23 @@ def gemm_nm(weight: Fp6Weight, xt, ldx: int, m: int, out=None, split_k: int = 0,
     return y
 
 
+def workspace_bytes(m: int, weight, split_k: int = 0) -> int:
+    """Bytes of zeroed scratch a call at batch `m` needs (0: none)."""
+    return int(_lib.load().lpqt_w6a16_workspace_bytes(m, weight.n, weight.k, split_k))
+
+
 def w6a16_linear(x, weight: Fp6Weight, out=None, out_dtype=None, split_k: int = 0, sched: str = "auto",
-                 prefetch: "Fp6Weight | None" = None, prefetch_bytes: int = 0):
+                 prefetch: "Fp6Weight | None" = None, prefetch_bytes: int = 0, workspace=None):
     """y = x @ W_hat^T for x[..., K] (CUDA, fp16 preferred) -> y[..., N].
 
     x is the K-major B operand as is when it is contiguous fp16 with K % 8 ==
     0; otherwise it is cast / padded once.  out_dtype: fp16 (default for
-    fp16 x), bf16 or fp32.  prefetch: the weight of the linear that runs
-    next on this stream (same batch); this launch's drain pulls its first
-    bytes into L2 (lpqt_w6a16_linear_pf).
+    fp16 x), bf16 or fp32; a given `out` must be a contiguous CUDA tensor of
+    shape [..., N] and its dtype decides the output type.  prefetch: the
+    weight of the linear that runs next on this stream (same batch); this
+    launch's drain pulls its first bytes into L2 (lpqt_w6a16_linear_pf).
+    workspace: optional caller-owned zeroed uint8 CUDA buffer of at least
+    `workspace_bytes(m, weight)` bytes (default: one per stream, _lib.Workspace).
     """
     t = _lib.torch()
     if x.shape[-1] != weight.k:
@@ -318,14 +334,29 @@ def w6a16_linear(x, weight: Fp6Weight, out=None, out_dtype=None, split_k: int = 
         x2, ldx = xp, kp
     else:
         ldx = weight.k
-    odt = out_dtype or (x.dtype if x.dtype in (t.float16, t.bfloat16, t.float32) else t.float16)
-    code = {t.float32: _lib.F32, t.float16: _lib.F16, t.bfloat16: _lib.BF16}[odt]
-    y = out if out is not None else t.empty((m, weight.n), dtype=odt, device=x2.device)
+    codes = {t.float32: _lib.F32, t.float16: _lib.F16, t.bfloat16: _lib.BF16}
+    if out is not None:
+        if out.dtype not in codes:
+            raise ShapeError(f"out dtype {out.dtype} unsupported (fp16, bf16, fp32)")
+        if out_dtype is not None and out_dtype != out.dtype:
+            raise ShapeError(f"out dtype {out.dtype} differs from out_dtype {out_dtype}")
+        if tuple(out.shape) not in ((m, weight.n), lead + (weight.n,)) or not out.is_contiguous() \
+                or out.device != x2.device:
+            raise ShapeError(f"out must be a contiguous {tuple(lead) + (weight.n,)} tensor on {x2.device}, "
+                             f"got {tuple(out.shape)}")
+        odt = out.dtype
+        y = out.view(m, weight.n)
+    else:
+        odt = out_dtype or (x.dtype if x.dtype in codes else t.float16)
+        if odt not in codes:
+            raise ShapeError(f"out_dtype {odt} unsupported (fp16, bf16, fp32)")
+        y = t.empty((m, weight.n), dtype=odt, device=x2.device)
     if m and weight.n:
         if weight.k == 0:
             y.zero_()
         else:
-            _launch(weight, x2, ldx, m, y, code, _lib.Y_MN, weight.n, split_k, sched, prefetch, prefetch_bytes)
+            _launch(weight, x2, ldx, m, y, codes[odt], _lib.Y_MN, weight.n, split_k, sched, prefetch,
+                    prefetch_bytes, workspace)
     return y.reshape(*lead, weight.n)
 
 

@@ -225,13 +225,52 @@ def quantize_tensor(W, scheme: QuantScheme, bias_shift: bool = False) -> Quantiz
         return QuantizedTensor(n, k, scheme, e16, None, PackedSegments(e8, e8.copy(), 0), bias_shift,
                                e16.copy() if bias_shift else None)
     d = quantize_device(w, bias_shift, scale_block(scheme), scheme.fmt.minifloat)
-    cache = {"scales": d["scales"], "seg4": d["seg4"], "seg2": d["seg2"]}
     if torch_in:
-        return QuantizedTensor(n, k, scheme, d["scales"], None, PackedSegments(d["seg4"], d["seg2"], n * k),
-                               bias_shift, d["folded"], cache)
-    return QuantizedTensor(n, k, scheme, d["scales"].cpu().numpy(), None,
-                           PackedSegments(d["seg4"].cpu().numpy(), d["seg2"].cpu().numpy(), n * k),
-                           bias_shift, None if d["folded"] is None else d["folded"].cpu().numpy(), cache)
+        payload = PackedSegments(d["seg4"], d["seg2"], n * k)
+        q = QuantizedTensor(n, k, scheme, d["scales"], None, payload, bias_shift, d["folded"], {})
+    else:
+        payload = PackedSegments(_frozen(d["seg4"]), _frozen(d["seg2"]), n * k)
+        q = QuantizedTensor(n, k, scheme, _frozen(d["scales"]), None, payload, bias_shift,
+                            None if d["folded"] is None else _frozen(d["folded"]), {})
+    _bind_cache(q, {"scales": d["scales"], "seg4": d["seg4"], "seg2": d["seg2"]})
+    return q
+
+
+def _frozen(t):
+    """CUDA tensor -> read-only numpy copy: the reference's QuantizedTensor is
+    frozen, and the device cache below relies on host fields never changing
+    in place (callers copy before editing, as the reference tests do)."""
+    a = t.cpu().numpy()
+    a.setflags(write=False)
+    return a
+
+
+def _fields_key(q: QuantizedTensor) -> tuple:
+    """Identity (and, for torch fields, in-place version) of every field the
+    device cache was derived from.  dataclasses.replace() shares the cache
+    dict with the new tensor; its fields differ, so the key does too."""
+    p = q.payload
+    objs = (q.scales, q.zero_points, p, getattr(p, "seg4", None), getattr(p, "seg_tail", None))
+    return (tuple((id(o), getattr(o, "_version", None) if _lib.is_torch(o) else None) for o in objs),
+            q.rows, q.cols, q.scheme, getattr(p, "code_count", None))
+
+
+def _bind_cache(q: QuantizedTensor, entries: dict) -> None:
+    c = q.device_cache
+    c.clear()
+    c.update(entries)
+    c["_key"] = _fields_key(q)
+    # the key holds ids: keep the objects alive so an id cannot be reused
+    c["_refs"] = (q.scales, q.zero_points, q.payload)
+
+
+def cache_of(q: QuantizedTensor) -> dict | None:
+    """The device cache of `q` if it still describes q's fields, else None
+    (a replaced or in-place-modified tensor never sees stale device data)."""
+    c = q.device_cache
+    if c is None or c.get("_key") != _fields_key(q):
+        return None
+    return c
 
 
 def compute_scale_fp(values, fmt: MiniFloatFormat) -> BlockParams:
@@ -263,8 +302,11 @@ def _quantize_int4(W, scheme: QuantScheme) -> QuantizedTensor:
             nib.data_ptr(), flags.ptr, _lib.stream_ptr()), "quantize_tensor")
         flags.raise_if_set()
     if torch_in:
-        return QuantizedTensor(n, k, scheme, scales, zeros, nib, False, None)
-    return QuantizedTensor(n, k, scheme, scales.cpu().numpy(), zeros.cpu().numpy(), nib.cpu().numpy(), False, None)
+        q = QuantizedTensor(n, k, scheme, scales, zeros, nib, False, None, {})
+    else:
+        q = QuantizedTensor(n, k, scheme, _frozen(scales), _frozen(zeros), _frozen(nib), False, None, {})
+    _bind_cache(q, {})
+    return q
 
 
 def compute_affine_params_int4(values) -> BlockParams:
@@ -278,12 +320,12 @@ def compute_affine_params_int4(values) -> BlockParams:
 
 def device_planes(q: QuantizedTensor):
     """(seg4, seg2, scales) of `q` as CUDA tensors (cached when built here)."""
-    if q.device_cache is not None and "seg4" in q.device_cache:
-        c = q.device_cache
-        return c["seg4"], c["seg2"], c["scales"]
     n = q.rows * q.cols
     if not isinstance(q.payload, PackedSegments) or q.payload.code_count != n:
         raise PayloadMismatch("payload does not hold rows*cols codes")
+    c = cache_of(q)
+    if c is not None and "seg4" in c:
+        return c["seg4"], c["seg2"], c["scales"]
     s4 = _lib.to_device(q.payload.seg4).reshape(-1)
     s2 = _lib.to_device(q.payload.seg_tail).reshape(-1)
     if s4.numel() != seg4_length(n) or s2.numel() != tail_length(q.scheme.fmt.minifloat, n):

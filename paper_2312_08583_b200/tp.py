@@ -167,9 +167,17 @@ class FusedColumnParallelFp6Linear:
     columns of y straight into every peer's symmetric-memory copy of y over
     NVLink / NVSwitch, and the kernel's last CTA runs a flag barrier with the
     peers (no NCCL call on the data path).  Buffers come from
-    `torch.distributed._symmetric_memory` (P2P-mapped on every peer); two
-    output buffers alternate, so a returned y stays valid until the call after
-    next (clone it to keep it longer)."""
+    `torch.distributed._symmetric_memory` (P2P-mapped on every peer); three
+    output buffers rotate.  Lifetime of a returned y (epoch e): a peer can
+    overwrite this buffer only in its epoch e + 3 launch, which starts after
+    its e + 2 kernel finished, which waits for THIS rank's e + 2 kernel's
+    signal — and that kernel ends only after everything enqueued on this
+    rank's stream before it.  So y stays valid for every reader enqueued on
+    the stream before this rank's call after next (e + 2); clone it to keep
+    it longer.  (With two buffers a peer's e + 2 stores could land while
+    readers enqueued after this rank's e + 1 call still ran.)"""
+
+    NBUF = 3
 
     def __init__(self, weight_shard, n: int, k: int, m_max: int, group=None, out_dtype=None):
         import torch.distributed as dist
@@ -185,7 +193,7 @@ class FusedColumnParallelFp6Linear:
         self.dtype = out_dtype or t.float16
         dev = weight_shard.tiles.device
         gname = self.group.group_name
-        self.bufs = [symm.empty((self.m_max, self.n), dtype=self.dtype, device=dev) for _ in range(2)]
+        self.bufs = [symm.empty((self.m_max, self.n), dtype=self.dtype, device=dev) for _ in range(self.NBUF)]
         self.buf_h = [symm.rendezvous(b, gname) for b in self.bufs]
         self.flag_t = symm.empty((_lib.MAX_PEERS,), dtype=t.int32, device=dev)
         self.flag_t.zero_()
@@ -216,7 +224,7 @@ class FusedColumnParallelFp6Linear:
             x2[:, :self.k] = x
         ldx = int(x2.shape[1])
         self.epoch += 1
-        i = self.epoch & 1
+        i = self.epoch % self.NBUF
         code = {t.float32: _lib.F32, t.float16: _lib.F16, t.bfloat16: _lib.BF16}[self.dtype]
         gather_linear(self.weight, x2, ldx, m, _peer_ptrs(self.buf_h[i], self.bufs[i], self.rank),
                       _peer_ptrs(self.flag_h, self.flag_t, self.rank), self.rank, self.epoch, self.done, code, "mn",

@@ -13,6 +13,7 @@ GOLDEN = os.path.join(ROOT, "tests", "golden", "golden.npz")
 
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a CUDA device (B200, sm_100a)")
+    config.addinivalue_line("markers", "multigpu: needs >= 2 CUDA devices (one torchrun rank per GPU)")
 
 
 @pytest.fixture(scope="session")

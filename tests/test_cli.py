@@ -58,7 +58,7 @@ def test_errors(tmp_path, capsys):
 
 
 def test_preset_table_is_the_papers():
-    assert cli.BENCH_PRESETS == {"ffn1-1b": (5504, 2048, 8), "ffn2-1b": (2048, 5504, 8),
+    assert {k: (p.rows, p.cols, p.batch) for k, p in cli.BENCH_PRESETS.items()} == {"ffn1-1b": (5504, 2048, 8), "ffn2-1b": (2048, 5504, 8),
                                  "ffn1-13b": (13824, 5120, 8), "ffn2-13b": (5120, 13824, 8),
                                  "ffn1-65b": (22016, 8192, 8), "ffn2-65b": (8192, 22016, 8)}
 
@@ -126,6 +126,6 @@ def test_bench_preset_smoke(capsys):
     rc, so, _ = run(capsys, ["bench", "--preset", "ffn1-1b", "--repeat", "3"])
     assert rc == 0
     lines = [ln for ln in so.splitlines() if ln.startswith("path=")]
-    assert [ln.split()[0] for ln in lines] == ["path=fp16_dense", "path=fp6_w6a16", "path=fp6_dequant_naive",
-                                               "path=fp6_dequant_bias_shift", "path=int4_fgq"]
+    assert [ln.split()[0] for ln in lines] == ["path=fp16_dense", "path=fp6_naive", "path=fp6_bias_shift",
+                                               "path=int4_fgq", "path=fp6_w6a16"]
     assert "weight_bytes=8465152" in lines[1]   # 5504 x 2048 x 0.75 + 2 x 5504
