@@ -212,6 +212,8 @@ def run_ours(args, world, rank, layers, m, e2e=True, burn_in=None):
     def next_of(c, i):
         # the linear that runs next on the stream: the step's next layer, or
         # the first layer of the next step (the next weight copy)
+        if args.no_l2_next:
+            return None
         return sets[c][i + 1] if i + 1 < len(layers) else sets[(c + 1) % copies][0]
 
     def launch(i, w, nxt=None):
@@ -258,8 +260,30 @@ def run_ours(args, world, rank, layers, m, e2e=True, burn_in=None):
         return g, evs
 
     graphs = [capture(c, False)[0] for c in range(copies)]
-    for s in range(args.warmup):
-        graphs[s % copies].replay()
+    # the timed region replays graphs of G consecutive steps (step j uses weight
+    # copy j % copies): PDL edges then also join the last GEMM of a step to
+    # the first of the next inside a graph, as a graph-captured serving loop
+    # does; K = q G + r steps = q replays of the G-step graph + r one-step graphs
+    G = max(copies, args.graph_steps // copies * copies) if args.graph_steps > 1 else 1
+    multi = None
+    if G > 1:
+        multi = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(multi):
+            for j in range(G):
+                for i, w in enumerate(sets[j % copies]):
+                    launch(i, w, next_of(j % copies, i))
+                    if world > 1:
+                        import torch.distributed as dist
+                        dist.all_gather_into_tensor(yfull[i], ys[i])
+
+    def run_steps(k):
+        q, r = (k // G, k % G) if multi is not None else (0, k)
+        for _ in range(q):
+            multi.replay()
+        for s in range(r):
+            graphs[s % copies].replay()
+
+    run_steps(args.warmup)
     torch.cuda.synchronize()
 
     # burn-in so the clock sampler sees the part under load, then the timed region
@@ -267,16 +291,14 @@ def run_ours(args, world, rank, layers, m, e2e=True, burn_in=None):
     with ClockSampler(int(os.environ.get("LOCAL_RANK", "0"))) as clk:
         t_end = time.time() + (args.burn_in if burn_in is None else burn_in)
         while time.time() < t_end:
-            for c in range(copies):
-                graphs[c].replay()
+            run_steps(max(G, copies))
             torch.cuda.synchronize()
         barrier(world)
         torch.cuda.synchronize()
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record()
-        for s in range(args.steps):
-            graphs[s % copies].replay()
+        run_steps(args.steps)
         e1.record()
         torch.cuda.synchronize()
         barrier(world)
@@ -302,7 +324,7 @@ def run_ours(args, world, rank, layers, m, e2e=True, burn_in=None):
     total_bytes = step_bytes(layers, m)       # whole job (all ranks)
     value = total_bytes * args.steps / t / 1e9
     res = {"t": t, "value": value, "per_layer": per_layer, "gpu_launches": gpu_launches,
-           "clocks": clk.summary(), "copies": copies}
+           "clocks": clk.summary(), "copies": copies, "graph_steps": G}
 
     # cuBLAS fp16 comparator on the same step (fp16 weights, same shards)
     if rank == 0 or world > 1:
@@ -606,6 +628,8 @@ def main():
     ap.add_argument("--burn-in", type=float, default=1.5, help="seconds of untimed load before timing")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-extras", action="store_true", help="skip the extra M=1 / 7B lines")
+    ap.add_argument("--graph-steps", type=int, default=8, help="steps per replayed CUDA graph")
+    ap.add_argument("--no-l2-next", action="store_true", help="no next-linear L2 prefetch hint")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -618,7 +642,8 @@ def main():
               if args.model == "llama2-70b" else "BASELINE.json configs[1] (LLaMA-2-7B shapes)",
               "tensor_parallel": world, "parallelism": f"tp{world} column-sharded + NCCL all-gather"
               if world > 1 else "single GPU", "activations": "fp16", "weights": "FP6 e3m2 (4+2), per-row f16 scale",
-              "l2_hygiene": "inputs larger than L2: weights rotated over >=2 distinct copies (>2x L2) per step"}
+              "l2_hygiene": "inputs larger than L2: weights rotated over >=2 distinct copies (>2x L2) per step",
+              "graph_steps": args.graph_steps}
 
     if args.impl == "reference":
         if rank != 0:

@@ -172,12 +172,6 @@ struct L2Prefetch {
 #ifndef LPQT_TILE_RING
 #define LPQT_TILE_RING 1
 #endif
-// decode (BN <= 32): the W producer also keeps LPQT_W_L2PF stages beyond its
-// smem ring requested into L2 (cp.async.bulk.prefetch.L2), so more weight
-// bytes are in flight per SM than the ring holds; 0 = off
-#ifndef LPQT_W_L2PF
-#define LPQT_W_L2PF 0
-#endif
 template <int BN, bool CSK, int WB = 6, bool FGQ = false>
 struct Cfg {
   static constexpr int kTileB = WB == 6 ? kTileBytes : kTileN * kTileK / 2;
@@ -765,29 +759,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint64_t pol = (a.m_tiles > 1 && !a.n_fastest) ? l2_evict_last_policy() : l2_evict_first_policy();
     StageIter<Sched, KS> it;
     it.start(a, sc, 0);
-    constexpr int kPf = (BN <= 32) ? LPQT_W_L2PF : 0;
-    StageIter<Sched, KS> pit;  // kPf > 0: the stage kWStages + kPf - 1 ahead of `it`
-    if constexpr (kPf > 0) {
-      if (is_w) {
-        pit.start(a, sc, 0);
-        for (int j = 0; j < C::kWStages && pit.ok; ++j) pit.next(a, sc);
-      }
-    }
     for (int i = 0; i < n_st; ++i, it.next(a, sc)) {
       const int kt = it.kt(), nt = it.nt();
       int n_tile, m_tile;
       tile_nm(a, it.sg.tile, n_tile, m_tile);
       if (is_w) {
-        if constexpr (kPf > 0) {
-          // before the ring-slot wait: stages i + kWStages .. + kPf - 1 requested into L2
-          for (int r = (i == 0 ? kPf : 1); r > 0 && pit.ok; --r, pit.next(a, sc)) {
-            int pn, pm;
-            tile_nm(a, pit.sg.tile, pn, pm);
-            if (lane == 0)
-              prefetch_l2_bulk(a.tiles + ((int64_t)pn * a.k_tiles + pit.kt()) * C::kTileB,
-                               static_cast<uint32_t>(pit.nt() * C::kTileB));
-          }
-        }
         const int s = i % C::kWStages;
         mbar_wait<WM>(&empty_w[s], ((i / C::kWStages) & 1) ^ 1);
         const uint8_t* src = a.tiles + ((int64_t)n_tile * a.k_tiles + kt) * C::kTileB;
