@@ -172,10 +172,26 @@ struct L2Prefetch {
 #ifndef LPQT_TILE_RING
 #define LPQT_TILE_RING 1
 #endif
+#ifndef LPQT_PD_SLOTS16
+#define LPQT_PD_SLOTS16 4  // FGQ per-block partial slots at BN 16 (TMEM: <= 6)
+#endif
+#ifndef LPQT_PD_WAIT
+#define LPQT_PD_WAIT 0     // the epilogue's partial-ready wait mode (see mbar_try_wait)
+#endif
 template <int BN, bool CSK, int WB = 6, bool FGQ = false>
 struct Cfg {
   static constexpr int kTileB = WB == 6 ? kTileBytes : kTileN * kTileK / 2;
+  // FGQ x FP6 at decode shapes (BN <= 32): "per-block partials" — every 128-k
+  // weight tile's MMAs go into a fresh fp32 partial accumulator (kPSlots ring
+  // in TMEM) and the epilogue adds S_block * partial in fp32, the reference's
+  // FGQ order (gemm.py:96-110).  The dequant thread of each row hands its
+  // block scale to the epilogue through TMEM too (kScaleCols columns, one
+  // per k-tile ordinal mod 32), ordered by the same afull -> MMA -> pfull chain.
+  static constexpr bool kPD = FGQ && WB == 6 && BN <= 32;
+  static constexpr int kScaleCols = kPD ? 32 : 0;
   // FGQ / INT4: a stage carries its tiles' block parameters after the weights
+  // (the dequant warps apply them to the rebuilt binary16 weight, or pass
+  // them on to the epilogue under kPD)
   static constexpr int kSBytes = FGQ ? kTileN * (WB == 4 ? 4 : 2) : 0;
   static constexpr int kQuads = WB == 6 ? 3 : 2;             // 16-B quads per (row, k-half)
   static constexpr int kKStep = BN <= 32 ? LPQT_DECODE_KSTEP : 1;  // 128-k tiles per pipeline stage
@@ -204,9 +220,14 @@ struct Cfg {
   // alternate stages, each into its own accumulator; the epilogue sums them
   // in a fixed order.  Prefill MMAs (N >= 128) are long enough for one.
   static constexpr int kMmaWarps = BN <= 64 ? 2 : 1;
-  static constexpr int kNAcc = kMmaWarps;
+  // (per-block partials: the epilogue writes the segment's scaled sum into a
+  // single D accumulator itself)
+  static constexpr int kNAcc = kPD ? 1 : kMmaWarps;
   static constexpr int kDCols = BN * kNAcc;
-  static constexpr int kACols = kTmemCols - kDBufs * kDCols;
+  // per-k-tile partial accumulators (in-order drains bound every issuer's lead
+  // to kPSlots ordinals, so a slot may alternate issuers without a skipped phase)
+  static constexpr int kPSlots = kPD ? (BN <= 16 ? LPQT_PD_SLOTS16 : 4) : 0;
+  static constexpr int kACols = kTmemCols - kDBufs * kDCols - kPSlots * BN - kScaleCols;
   // even with two MMA issuers (each slot then always belongs to the same
   // issuer, which waits on it in stage order: no parity wait can skip a
   // phase); one issuer may use every whole slot TMEM holds
@@ -218,7 +239,7 @@ struct Cfg {
   // while the MMAs still read the current stage's second one
   static constexpr bool kTileRing = LPQT_TILE_RING && kKStep == 2 && kMmaWarps == 2 && kACols / kAColsPerBuf >= 6;
   static constexpr int kABars = kTileRing ? 6 : kASlots;
-  static constexpr int kBarCount = 2 * kWStages + 2 * kXStages + 2 * kABars + 2 * kDBufs + 5;
+  static constexpr int kBarCount = 2 * kWStages + 2 * kXStages + 2 * kABars + 2 * kDBufs + 5 + 2 * kPSlots;
   static constexpr int kSmemBytes = kXStages * kXStageBytes + kWStages * kWStageBytes + 2 * kStageBufBytes +
                                     2 * kYBufBytes + 8 * kBarCount + 16;
   static_assert(kWStages >= 2 && kXStages >= 2, "pipeline too shallow");
@@ -403,6 +424,10 @@ __device__ __forceinline__ int atom_add_acq_rel_gpu(int* p, int v) {
   int old;
   asm volatile("atom.add.acq_rel.gpu.s32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
   return old;
+}
+
+__device__ __forceinline__ void red_add_release_gpu(int* p, int v) {
+  asm volatile("red.release.gpu.global.add.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
 __device__ __forceinline__ int ld_acquire_gpu(const int* p) {
@@ -666,8 +691,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* part_full = dempty + C::kDBufs;  // CSK [2]: this CTA's round partials from the senders
   uint64_t* stg_free = part_full + 2;        // CSK [2]: this CTA's staging buffer read by the reducer
   uint64_t* fix_bar = stg_free + 2;          // SK: partials gathered by bulk copy (last segment)
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(fix_bar + 1);
-  volatile int* last_flag = reinterpret_cast<volatile int*>(tmem_slot + 1);
+  uint64_t* pfull = fix_bar + 1;             // kPD [kPSlots]: a k-tile's partial is in TMEM
+  uint64_t* pempty = pfull + C::kPSlots;     // kPD [kPSlots]: ... read by the epilogue
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(pempty + C::kPSlots);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
@@ -711,6 +737,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       } else {
         mbar_init(fix_bar, 1);
+      }
+      for (int b = 0; b < C::kPSlots; ++b) {
+        mbar_init(&pfull[b], 1);
+        mbar_init(&pempty[b], kNumEpiWarps);
       }
       fence_mbar_init();
       pdl_launch_dependents();  // the next kernel may queue for this SM as soon as it frees
@@ -907,7 +937,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         } else {
           fp6x32_cvt_f16x32_fma(q[0], r, sm);
           fp6x32_cvt_f16x32_fma(q[0] + 6, r + 16, sm);
-          if constexpr (FGQ) scale_f16x2(r, fs2);
+          if constexpr (FGQ && !C::kPD) scale_f16x2(r, fs2);
         }
       }
       mbar_wait_u32<WM>(ae0 + 8 * (a_bar0 + ac.idx), ac.ph ^ 1u);
@@ -923,9 +953,15 @@ __global__ void __launch_bounds__(kThreads, 1)
           } else {
             fp6x32_cvt_f16x32_fma(q[h], r, sm);
             fp6x32_cvt_f16x32_fma(q[h] + 6, r + 16, sm);
-            if constexpr (FGQ) scale_f16x2(r, fs2);
+            if constexpr (FGQ && !C::kPD) scale_f16x2(r, fs2);
           }
           tmem_st_x32(ta + h * 32, r);
+        }
+        if constexpr (C::kPD) {
+          // this row's block scale of tile ordinal q, for the epilogue (fp32)
+          const uint32_t q = static_cast<uint32_t>(KS * i + (KS == 2 ? tl : 0));
+          tmem_st_x1(t_row + C::kACols + C::kDBufs * C::kDCols + C::kPSlots * BN + (q & 31u),
+                     __float_as_uint(__half2float(__ushort_as_half(static_cast<uint16_t>(fs2)))));
         }
       }
       // the stage's words are consumed: hand the W slot back to the producer
@@ -964,8 +1000,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int i0 = 0; sc.template seg_at<KS>(a, i0, sg); i0 += sg.len) {
         const int d = lu % C::kDBufs;
         const uint32_t dph = (lu / C::kDBufs) & 1;
-        mbar_wait<WM>(&dempty[d], dph ^ 1);
-        tc_fence_after();
+        if constexpr (!C::kPD) {  // (per-block partials: the epilogue owns D)
+          mbar_wait<WM>(&dempty[d], dph ^ 1);
+          tc_fence_after();
+        }
         const uint32_t d_tmem = tmem_d0 + d * C::kDCols + mw * BN;
         const int s_first = C::kMmaWarps == 2 ? ((mw - sg.i0) & 1) : 0;
         for (int s = s_first; s < sg.len; s += C::kMmaWarps) {
@@ -998,11 +1036,26 @@ __global__ void __launch_bounds__(kThreads, 1)
               ta_t = tmem_base + tb * kAColsPerBuf;
             }
             if (t < nt) {
+              if constexpr (C::kPD) {
+                // k-tile ordinal q = KS * stage + t: a fresh partial in slot q % kPSlots
+                // (with two issuers on alternate stages each slot keeps its issuer)
+                const int q = KS * it + t, ps = q % C::kPSlots;
+                mbar_wait<WM>(&pempty[ps], ((q / C::kPSlots) & 1) ^ 1);
+                tc_fence_after();
+                const uint32_t p_tmem = tmem_d0 + C::kDBufs * C::kDCols + ps * BN;
 #pragma unroll
-              for (int j = 0; j < kTileK / 16; ++j) {
-                const uint32_t off = (t * C::kXTileBytes + (j >> 2) * (BN * 128) + (j & 3) * 32) >> 4;
-                const bool init = first && t == 0 && j == 0;
-                mma_f16_ts_if(e, d_tmem, ta_t + j * 8, bd_lo + off, bd_hi, idesc, init ? 0u : 1u);
+                for (int j = 0; j < kTileK / 16; ++j) {
+                  const uint32_t off = (t * C::kXTileBytes + (j >> 2) * (BN * 128) + (j & 3) * 32) >> 4;
+                  mma_f16_ts_if(e, p_tmem, ta_t + j * 8, bd_lo + off, bd_hi, idesc, j == 0 ? 0u : 1u);
+                }
+                tc_commit_if(e, &pfull[ps]);
+              } else {
+#pragma unroll
+                for (int j = 0; j < kTileK / 16; ++j) {
+                  const uint32_t off = (t * C::kXTileBytes + (j >> 2) * (BN * 128) + (j & 3) * 32) >> 4;
+                  const bool init = first && t == 0 && j == 0;
+                  mma_f16_ts_if(e, d_tmem, ta_t + j * 8, bd_lo + off, bd_hi, idesc, init ? 0u : 1u);
+                }
               }
             }
             if constexpr (C::kTileRing) tc_commit_if(e, &aempty[tb]);  // this tile's slot is free once read
@@ -1010,10 +1063,12 @@ __global__ void __launch_bounds__(kThreads, 1)
           tc_commit_if(e, &empty_x[xs]);
           if constexpr (!C::kTileRing) tc_commit_if(e, &aempty[slot]);
         }
-        if (s_first < sg.len) {
-          tc_commit_elect(&dfull[d]);
-        } else if (lane == 0) {
-          mbar_arrive(&dfull[d]);  // no MMA of this issuer in the segment
+        if constexpr (!C::kPD) {
+          if (s_first < sg.len) {
+            tc_commit_elect(&dfull[d]);
+          } else if (lane == 0) {
+            mbar_arrive(&dfull[d]);  // no MMA of this issuer in the segment
+          }
         }
         ++lu;
       }
@@ -1029,16 +1084,22 @@ __global__ void __launch_bounds__(kThreads, 1)
     // first segment's is loaded before any wait, each next one a segment
     // ahead, so no global load sits on the epilogue's critical path (a cold
     // load behind the weight stream costs microseconds).
-    auto scale_of = [&](const Seg& g) -> uint16_t {
+    // FGQ x FP6: the row's power-of-two factor 2^e_r (the block scales are
+    // normalised by it, lpqt_fgq_stage_params); INT4 carries its scale in A
+    auto scale_of = [&](const Seg& g) -> float {
       int nt, mt;
       tile_nm(a, g.tile, nt, mt);
       const int nn = nt * kTileN + rr;
-      if constexpr (FGQ) return nn < a.N ? static_cast<uint16_t>(0x3C00u) : static_cast<uint16_t>(0);  // (in A)
-      return nn < a.N ? __ldg(a.scales + nn) : static_cast<uint16_t>(0);
+      if constexpr (FGQ && WB == 6)
+        return nn < a.N ? __ldg(reinterpret_cast<const float*>(fg.stage + (int64_t)a.n_tiles * a.k_tiles * kTileN * 2) +
+                                nn)
+                        : 0.f;
+      if constexpr (FGQ) return nn < a.N ? 1.f : 0.f;
+      return nn < a.N ? __half2float(__ushort_as_half(__ldg(a.scales + nn))) : 0.f;
     };
     Seg sg_next;
     bool have_next = sc.template seg_at<KS>(a, 0, sg_next);
-    uint16_t fs_next = have_next ? scale_of(sg_next) : static_cast<uint16_t>(0);
+    float fs_next = have_next ? scale_of(sg_next) : 0.f;
     if constexpr (CSK) cluster_wait();
     if (warp == kWarpEpi0 && lane == 0) CTA_STAMP(17);
     pdl_wait();  // Y / workspace writes: the preceding grid must be complete
@@ -1055,7 +1116,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     int ys_n = 0;
     for (; have_next; ++lu) {
       sg = sg_next;
-      const float fs = __half2float(__ushort_as_half(fs_next));
+      const float fs = fs_next;
       have_next = sc.template seg_at<KS>(a, sg.i0 + sg.len, sg_next);
       if (have_next) fs_next = scale_of(sg_next);
       const int d = lu % C::kDBufs;
@@ -1110,10 +1171,6 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int nacc = min(C::kNAcc, sg.len);
       const int q0 = (nacc < C::kNAcc) ? (sg.i0 & 1) : 0;
       const bool last_seg = sg.i0 + sg.len >= n_st;
-      // stream-K partial tile: if every other contributor has already
-      // published (acquire-load of the tile counter), this CTA is the last
-      // arriver — it skips publishing its own partial and the atomic
-      bool sk_last = false;
       int64_t p_first = 0;
       int c_first = 0, c_last = 0, idx_first = 0;
       // contributors of a split tile (64-bit divisions: only when needed)
@@ -1209,48 +1266,67 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         y_end();
       };
-      // BN 16: a CTA's last segment of a shared tile peeks (acquire) at the
-      // tile counter before and after its MMAs; a hit means every other
-      // contributor has published, so this CTA reduces without publishing its
-      // own partial or taking the atomic, gathering the others by bulk copy
-      // into the W ring (free once the last segment's MMAs are done).
-      // BN >= 128 gathers in batches through the free X + W rings (below).
-      // BN 32: only the first-contributor / two-CTA case (register budget).
+      // Stream-K fixup roles (static, so nobody waits for an atomic's reply):
+      // the REDUCER of a split tile is its first contributor in k order,
+      // c_first — the tile's head is the END of c_first's range, so this is
+      // always c_first's last segment and every other contributor's share
+      // (a whole range inside the tile, or the first segment of c_last's)
+      // finishes no later.  The others publish their fp32 partial and count
+      // in with one release reduction (no round trip: they go on, or exit);
+      // the reducer polls the tile counter after its own MMAs, then sums
+      // own + partials in k order (deterministic) and stores Y.
       constexpr int kPartBytes = kTileN * BN * 4;
-      if constexpr (BN <= 16 || BN >= 128) {
-        bool peek_ok = false;
-        auto peek = [&]() {
-          if (warp == kWarpEpi0 && lane == 0)
-            *last_flag = (ld_acquire_gpu(&a.counters[sg.tile]) + sg.len == a.ksteps) ? 1 : 0;
-          named_bar_sync(1, kNumEpiWarps * 32);
-          sk_last = *last_flag != 0;
-          named_bar_sync(1, kNumEpiWarps * 32);  // last_flag is reused below
-        };
-        if (!CSK && !sg.full && last_seg) {
-          // any contributor whose last segment this is may turn out to be
-          // the tile's last arriver; it then needs no publish and no atomic
-          contributors();
-          peek_ok = BN >= 128 ||
-                    (int64_t)(c_last - c_first + 1) * kPartBytes <= (int64_t)C::kWStages * C::kWStageBytes;
-          if (peek_ok) {
-            peek();
+      bool reducer = false;
+      if (!CSK && !sg.full) {
+        contributors();
+        reducer = c_first == static_cast<int>(blockIdx.x);
+      }
+      if constexpr (C::kPD) {
+        // FGQ per-block partials (gemm.py:96-110): for every 128-k tile of the
+        // segment, in k order, acc += S_block * partial (fp32, product and
+        // sum rounded separately like the reference), then the segment's sum
+        // goes to D buffer d, read below like an MMA accumulator
+        float pacc[BN];
+#pragma unroll
+        for (int j = 0; j < BN; ++j) pacc[j] = 0.f;
+        const uint32_t t_p = t_lane + C::kDBufs * C::kDCols;
+        const uint32_t t_sc = t_p + C::kPSlots * BN;  // block scales, column = ordinal mod 32
+#pragma unroll 1
+        for (int s = 0; s < sg.len; ++s) {
+          const int i = sg.i0 + s, kt = sg.kt0 + s * KS, nt = min(KS, sg.kt1 - kt);
+#pragma unroll
+          for (int t = 0; t < KS; ++t) {
+            if (t < nt) {
+              const int q = KS * i + t, ps = q % C::kPSlots;
+              mbar_wait<LPQT_PD_WAIT>(&pfull[ps], (q / C::kPSlots) & 1);
+              tc_fence_after();
+              uint32_t sv;
+              tmem_ld_x1(t_sc + (q & 31), sv);
+#pragma unroll
+              for (int c0 = 0; c0 < BN; c0 += 16) {
+                uint32_t v[16];
+                tmem_ld_x16(t_p + ps * BN + c0, v);
+                tmem_wait_ld();
+                const float scl = __uint_as_float(sv);
+#pragma unroll
+                for (int j = 0; j < 16; ++j)
+                  pacc[c0 + j] = __fadd_rn(pacc[c0 + j], __fmul_rn(scl, __uint_as_float(v[j])));
+              }
+              tc_fence_before();
+              __syncwarp();
+              if (lane == 0) mbar_arrive(&pempty[ps]);
+            }
           }
         }
-        mbar_wait<WM>(&dfull[d], dph);
-        // second look once the MMAs are done: the other contributors usually
-        // finished meanwhile, and a hit skips publishing + the acq_rel atomic
-        if (peek_ok && !sk_last) peek();
+#pragma unroll
+        for (int c0 = 0; c0 < BN; c0 += 16) {
+          uint32_t v[16];
+#pragma unroll
+          for (int j = 0; j < 16; ++j) v[j] = __float_as_uint(pacc[c0 + j]);
+          tmem_st_x16(t_d + c0, v);
+        }
+        tmem_wait_st();
       } else {
-        if (!CSK && !sg.full && last_seg && sg.kt0 == 0) {
-          contributors();
-          if (c_first == static_cast<int>(blockIdx.x) && c_last == c_first + 1) {
-            if (warp == kWarpEpi0 && lane == 0)
-              *last_flag = (ld_acquire_gpu(&a.counters[sg.tile]) + sg.len == a.ksteps) ? 1 : 0;
-            named_bar_sync(1, kNumEpiWarps * 32);
-            sk_last = *last_flag != 0;
-            named_bar_sync(1, kNumEpiWarps * 32);  // last_flag is reused below
-          }
-        }
         mbar_wait<WM>(&dfull[d], dph);
       }
       if (last_seg && warp == kWarpEpi0 && lane == 0) CTA_STAMP(8);
@@ -1354,7 +1430,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         y_end();
       } else {
         // ---- stream-K partial tile
-        if (!sk_last) {
+        if (!reducer) {
           float4* part = reinterpret_cast<float4*>(a.partials) + PartLayout<BN>::f4((int64_t)blockIdx.x * 2 + sg.pidx, 0, rr);
 #pragma unroll 1
           for (int c0 = 0; c0 < BN; c0 += 16) {
@@ -1370,203 +1446,141 @@ __global__ void __launch_bounds__(kThreads, 1)
               __stcg(part + ((c0 + j) / 4) * PartLayout<BN>::kJStride, make_float4(acc[j], acc[j + 1], acc[j + 2], acc[j + 3]));
             }
           }
-          // publish: CTA barrier, then one gpu-scope acq_rel atomic (release
-          // our partial, acquire the other contributors' partials if last)
+          // publish: CTA barrier (cumulativity over the epilogue's stores),
+          // then one gpu-scope release reduction — no reply awaited
           named_bar_sync(1, kNumEpiWarps * 32);
           if (warp == kWarpEpi0 && lane == 0) {
-            const int k_done = sg.len;
             if (last_seg) CTA_STAMP(9);
-            const int prev = atom_add_acq_rel_gpu(&a.counters[sg.tile], k_done);
-            *last_flag = (prev + k_done == a.ksteps) ? 1 : 0;
+            red_add_release_gpu(&a.counters[sg.tile], sg.len);
             if (last_seg) CTA_STAMP(10);
           }
+        } else {
+          // reducer: wait until the other contributors' k-steps are published
+          if (warp == kWarpEpi0 && lane == 0) {
+            const int others = a.ksteps - sg.len;
+            for (uint32_t spin = 0; ld_acquire_gpu(&a.counters[sg.tile]) != others; ++spin) {
+              if (spin > (1u << 26)) __trap();  // a contributor never published: fail loudly
+              __nanosleep(32);
+            }
+            CTA_STAMP(10);
+          }
           named_bar_sync(1, kNumEpiWarps * 32);
-        }
-        if (BN >= 128 && C::kDBufs == 2 && last_seg && (sk_last || *last_flag)) {
-          // ---- stream-K tail, BN >= 128: the other contributors' 128 x BN
-          // partials come by bulk copy, in batches through the free X + W
-          // rings, summed in k order into the idle second TMEM accumulator
-          // (own partial in place: from TMEM when the peek spared publishing
-          // it, else from the workspace like the others)
-          contributors();
-          tail_reduce(sk_last);
-        } else if (BN <= 16 && sk_last && !(c_last == c_first + 1 && c_first == static_cast<int>(blockIdx.x))) {
-          // last arriver found by the peek (any position in k order): the
-          // other contributors' partials arrive by bulk copy in one round
-          // trip (slot c - c_first of the free W ring), own stays in TMEM
-          const int me = static_cast<int>(blockIdx.x);
-          if (warp == kWarpEpi0 && lane == 0) {
-            fence_proxy_async_global();  // generic-proxy partials (acquired above) -> bulk-copy reads
-            mbar_arrive_expect_tx(fix_bar, static_cast<uint32_t>(c_last - c_first) * kPartBytes);
-            for (int c = c_first; c <= c_last; ++c) {
-              if (c == me) continue;
-              const int idx = c == c_first ? idx_first : 0;
-              bulk_g2s_plain(smem_w + (c - c_first) * kPartBytes, a.partials + ((int64_t)c * 2 + idx) * (kTileN * BN),
-                             kPartBytes, fix_bar);
+          if (BN >= 128 && C::kDBufs == 2) {
+            tail_reduce(true);  // (own partial in TMEM, the others by bulk copy in batches)
+          } else if ((int64_t)(c_last - c_first) * kPartBytes <= (int64_t)C::kWStages * C::kWStageBytes) {
+            // last segment: every W stage is consumed, so the ring takes the
+            // other contributors' partials in ONE round trip (one bulk copy
+            // each, in flight together); own partial stays in TMEM
+            if (warp == kWarpEpi0 && lane == 0) {
+              fence_proxy_async_global();  // generic-proxy partials (acquired above) -> bulk-copy reads
+              mbar_arrive_expect_tx(fix_bar, static_cast<uint32_t>(c_last - c_first) * kPartBytes);
+              for (int c = c_first + 1; c <= c_last; ++c)
+                bulk_g2s_plain(smem_w + (c - c_first) * kPartBytes, a.partials + ((int64_t)c * 2) * (kTileN * BN),
+                               kPartBytes, fix_bar);
             }
-          }
-          y_begin();
-          mbar_wait<WM>(fix_bar, 0);
-          if (warp == kWarpEpi0 && lane == 0) CTA_STAMP(23);
-          const uint32_t base = smem_u32(smem_w) + static_cast<uint32_t>(rr * 16);  // chunk-major rows
+            y_begin();
+            mbar_wait<WM>(fix_bar, 0);
+            if (warp == kWarpEpi0 && lane == 0) CTA_STAMP(23);
+            const uint32_t base = smem_u32(smem_w) + static_cast<uint32_t>(rr * 16);  // chunk-major rows
 #pragma unroll 1
-          for (int c0 = 0; c0 < BN; c0 += 16) {
-            float own[16], acc[16];
-            load_acc16<BN>(t_d, c0, q0, nacc, own);
-            if (warp == kWarpEpi0 && lane == 0) CTA_STAMP(26);
-            if (c0 + 16 >= BN) {
-              tc_fence_before();
-              __syncwarp();
-              if (lane == 0) mbar_arrive(&dempty[d]);
-            }
-#pragma unroll
-            for (int j = 0; j < 16; ++j) acc[j] = 0.f;
-            // contributors in k order, own partial in its place
-#pragma unroll 1
-            for (int c = c_first; c <= c_last; ++c) {
-              if (c == me) {
-#pragma unroll
-                for (int j = 0; j < 16; ++j) acc[j] += own[j];
-              } else {
-                const uint32_t src = base + (c - c_first) * kPartBytes + (c0 / 4) * kTileN * 16;
-#pragma unroll
-                for (int j = 0; j < 4; ++j) {
-                  const float4 v = lds128_f32(src + j * kTileN * 16);
-                  acc[4 * j + 0] += v.x;
-                  acc[4 * j + 1] += v.y;
-                  acc[4 * j + 2] += v.z;
-                  acc[4 * j + 3] += v.w;
-                }
+            for (int c0 = 0; c0 < BN; c0 += 16) {
+              float acc[16];
+              load_acc16<BN>(t_d, c0, q0, nacc, acc);
+              if (c0 + 16 >= BN) {
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&dempty[d]);
               }
-            }
-            if (warp == kWarpEpi0 && lane == 0) CTA_STAMP(27);
-            y_chunk(c0, acc);
-          }
-          if (warp == kWarpEpi0 && lane == 0) CTA_STAMP(24);
-          y_end();
-          if (warp == kWarpEpi0 && lane == 0) CTA_STAMP(25);
-        } else if (sk_last) {
-          // fast path: two contributors, this CTA first in k order
-          y_begin();
+              // (0 + own) + p1 + p2 ...: contributors in k order
+#pragma unroll
+              for (int j = 0; j < 16; ++j) acc[j] = 0.f + acc[j];
 #pragma unroll 1
-          for (int c0 = 0; c0 < BN; c0 += 16) {
-            float acc[16];
-            load_acc16<BN>(t_d, c0, q0, nacc, acc);
-            if (c0 + 16 >= BN) {
-              tc_fence_before();
-              __syncwarp();
-              if (lane == 0) mbar_arrive(&dempty[d]);
-            }
-            const float4* src = reinterpret_cast<const float4*>(a.partials) + PartLayout<BN>::f4((int64_t)c_last * 2, c0 / 4, rr);
+              for (int c = 1; c <= c_last - c_first; ++c) {
+                if constexpr (PartLayout<BN>::kChunkMajor) {
+                  const uint32_t src = base + c * kPartBytes + (c0 / 4) * kTileN * 16;
 #pragma unroll
-            for (int j = 0; j < 4; ++j) {
-              const float4 v = __ldcg(src + j * PartLayout<BN>::kJStride);
-              // (0 + own) + other: the canonical contributor-order sum
-              acc[4 * j + 0] = (0.f + acc[4 * j + 0]) + v.x;
-              acc[4 * j + 1] = (0.f + acc[4 * j + 1]) + v.y;
-              acc[4 * j + 2] = (0.f + acc[4 * j + 2]) + v.z;
-              acc[4 * j + 3] = (0.f + acc[4 * j + 3]) + v.w;
-            }
-            y_chunk(c0, acc);
-          }
-          y_end();
-        } else if (BN <= 16 && *last_flag && last_seg &&
-                   (int64_t)(sk_cta_of(a, (int64_t)sg.tile * a.ksteps + a.ksteps - 1) -
-                             sk_cta_of(a, (int64_t)sg.tile * a.ksteps) + 1) * (kTileN * BN * 4) <=
-                       (int64_t)C::kWStages * C::kWStageBytes) {
-          // last segment, last arriver: every W stage has been consumed, so
-          // the ring takes all contributors' partials in ONE round trip (one
-          // bulk copy each, in flight together) instead of a chain of L2
-          // loads at the very end of the kernel
-          contributors();
-          if (warp == kWarpEpi0 && lane == 0) {
-            fence_proxy_async_global();  // generic-proxy partials (acquired above) -> bulk-copy reads
-            mbar_arrive_expect_tx(fix_bar, static_cast<uint32_t>(c_last - c_first + 1) * kPartBytes);
-            for (int c = c_first; c <= c_last; ++c) {
-              const int idx = c == c_first ? idx_first : 0;
-              bulk_g2s_plain(smem_w + (c - c_first) * kPartBytes, a.partials + ((int64_t)c * 2 + idx) * (kTileN * BN),
-                             kPartBytes, fix_bar);
-            }
-          }
-          y_begin();
-          mbar_wait<WM>(fix_bar, 0);
-          if (warp == kWarpEpi0 && lane == 0) CTA_STAMP(23);
-          const uint32_t base = smem_u32(smem_w) + static_cast<uint32_t>(rr * 16);  // chunk-major rows
-#pragma unroll 1
-          for (int c0 = 0; c0 < BN; c0 += 16) {
-            float acc[16];
-#pragma unroll
-            for (int j = 0; j < 16; ++j) acc[j] = 0.f;
-#pragma unroll 1
-            for (int c = 0; c <= c_last - c_first; ++c) {
-              const uint32_t src = base + c * kPartBytes + (c0 / 4) * kTileN * 16;
-#pragma unroll
-              for (int j = 0; j < 4; ++j) {
-                const float4 v = lds128_f32(src + j * kTileN * 16);
-                acc[4 * j + 0] += v.x;
-                acc[4 * j + 1] += v.y;
-                acc[4 * j + 2] += v.z;
-                acc[4 * j + 3] += v.w;
-              }
-            }
-            y_chunk(c0, acc);
-          }
-          y_end();
-        } else if (*last_flag) {
-          contributors();
-          y_begin();
-#pragma unroll 1
-          for (int c0 = 0; c0 < BN; c0 += 16) {
-            float acc[16];
-#pragma unroll
-            for (int j = 0; j < 16; ++j) acc[j] = 0.f;
-            // contributors in k order (fixed summation order, whichever CTA
-            // arrives last: deterministic); kFix of them are loaded at once
-            // so their L2 round trips overlap.  Plain (weak) loads: the
-            // acquire above ordered them after every contributor's release.
-            constexpr int kFix = 2;
-#pragma unroll 1
-            for (int cb = c_first; cb <= c_last; cb += kFix) {
-              float4 v[kFix][4];
-#pragma unroll
-              for (int u = 0; u < kFix; ++u) {
-                const int c = cb + u;
-                if (c <= c_last) {
-                  const int idx = c == c_first ? idx_first : 0;
-                  if constexpr (PartLayout<BN>::kChunkMajor) {
-                    const float4* src = reinterpret_cast<const float4*>(a.partials) +
-                                        PartLayout<BN>::f4((int64_t)c * 2 + idx, c0 / 4, rr);
-#pragma unroll
-                    for (int j = 0; j < 4; ++j) v[u][j] = __ldcg(src + j * PartLayout<BN>::kJStride);
-                  } else {  // rows contiguous (same address as PartLayout<BN>::f4)
-                    const float4* src = reinterpret_cast<const float4*>(
-                        a.partials + (((int64_t)c * 2 + idx) * kTileN + rr) * BN + c0);
-#pragma unroll
-                    for (int j = 0; j < 4; ++j) v[u][j] = __ldcg(src + j);
+                  for (int j = 0; j < 4; ++j) {
+                    const float4 v = lds128_f32(src + j * kTileN * 16);
+                    acc[4 * j + 0] += v.x;
+                    acc[4 * j + 1] += v.y;
+                    acc[4 * j + 2] += v.z;
+                    acc[4 * j + 3] += v.w;
                   }
-                } else {
+                } else {  // rows contiguous
+                  const uint32_t src = smem_u32(smem_w) + c * kPartBytes + (rr * BN + c0) * 4;
 #pragma unroll
-                  for (int j = 0; j < 4; ++j) v[u][j] = make_float4(0.f, 0.f, 0.f, 0.f);
+                  for (int j = 0; j < 4; ++j) {
+                    const float4 v = lds128_f32(src + j * 16);
+                    acc[4 * j + 0] += v.x;
+                    acc[4 * j + 1] += v.y;
+                    acc[4 * j + 2] += v.z;
+                    acc[4 * j + 3] += v.w;
+                  }
                 }
               }
-#pragma unroll
-              for (int u = 0; u < kFix; ++u) {
-#pragma unroll
-                for (int j = 0; j < 4; ++j) {
-                  acc[4 * j + 0] += v[u][j].x;
-                  acc[4 * j + 1] += v[u][j].y;
-                  acc[4 * j + 2] += v[u][j].z;
-                  acc[4 * j + 3] += v[u][j].w;
-                }
-              }
+              y_chunk(c0, acc);
             }
-            y_chunk(c0, acc);
+            if (warp == kWarpEpi0 && lane == 0) CTA_STAMP(24);
+            y_end();
+          } else {
+            // many contributors (partials exceed the W ring): L2 loads in k
+            // order, kFix at a time so their round trips overlap
+            y_begin();
+#pragma unroll 1
+            for (int c0 = 0; c0 < BN; c0 += 16) {
+              float acc[16];
+              load_acc16<BN>(t_d, c0, q0, nacc, acc);
+              if (c0 + 16 >= BN) {
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&dempty[d]);
+              }
+#pragma unroll
+              for (int j = 0; j < 16; ++j) acc[j] = 0.f + acc[j];
+              constexpr int kFix = BN <= 32 ? 1 : 2;  // (decode epilogue: 72 registers)
+#pragma unroll 1
+              for (int cb = c_first + 1; cb <= c_last; cb += kFix) {
+                float4 v[kFix][4];
+#pragma unroll
+                for (int u = 0; u < kFix; ++u) {
+                  const int c = cb + u;
+                  if (c <= c_last) {
+                    if constexpr (PartLayout<BN>::kChunkMajor) {
+                      const float4* src = reinterpret_cast<const float4*>(a.partials) +
+                                          PartLayout<BN>::f4((int64_t)c * 2, c0 / 4, rr);
+#pragma unroll
+                      for (int j = 0; j < 4; ++j) v[u][j] = __ldcg(src + j * PartLayout<BN>::kJStride);
+                    } else {
+                      const float4* src = reinterpret_cast<const float4*>(
+                          a.partials + (((int64_t)c * 2) * kTileN + rr) * BN + c0);
+#pragma unroll
+                      for (int j = 0; j < 4; ++j) v[u][j] = __ldcg(src + j);
+                    }
+                  } else {
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) v[u][j] = make_float4(0.f, 0.f, 0.f, 0.f);
+                  }
+                }
+#pragma unroll
+                for (int u = 0; u < kFix; ++u) {
+#pragma unroll
+                  for (int j = 0; j < 4; ++j) {
+                    acc[4 * j + 0] += v[u][j].x;
+                    acc[4 * j + 1] += v[u][j].y;
+                    acc[4 * j + 2] += v[u][j].z;
+                    acc[4 * j + 3] += v[u][j].w;
+                  }
+                }
+              }
+              y_chunk(c0, acc);
+            }
+            y_end();
           }
-          y_end();
-        }
-        if (sk_last || *last_flag) {
-          if (warp == kWarpEpi0 && lane == 0) a.counters[sg.tile] = 0;
-          if (last_seg && warp == kWarpEpi0 && lane == 0) CTA_STAMP(11);
+          // every partial is read: re-arm the counter for the next launch
+          if (warp == kWarpEpi0 && lane == 0) {
+            a.counters[sg.tile] = 0;
+            if (last_seg) CTA_STAMP(11);
+          }
         }
         named_bar_sync(1, kNumEpiWarps * 32);
       }

@@ -146,9 +146,28 @@ __global__ void prepack_int4_kernel(const uint8_t* __restrict__ nib, int64_t N, 
 // Block parameters in GEMM stage order (FgqArgs, gemm.cu): entry
 // (rt * k_tiles + kt) * 128 + r = the f16 scale (INT4: scale | zero << 16) of
 // row rt * 128 + r in the block holding k tile kt; rows past N are 0.
+// FP6 / FP5 (no zero points): each row's block scales are normalised by a
+// power of two, S'_b = S_b * 2^-e_r with max_b S'_b in [2^10, 2^11), and
+// 2^e_r (f32) is stored per row after the stage-ordered scales.  Exact
+// (binary16 exponent shift) unless S_b < 2^-24 max_b S_b; the GEMM multiplies
+// by 2^e_r in fp32, so the products and sums are the reference's scaled by a
+// power of two (no binary16 under/overflow of v * S_b in the rebuilt weight).
+__global__ void fgq_row_factor_kernel(const uint16_t* __restrict__ scales, int64_t N, int64_t Np, int64_t bpr,
+                                      float* __restrict__ rowf) {
+  for (int64_t n = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; n < Np; n += (int64_t)gridDim.x * blockDim.x) {
+    float mx = 0.f;
+    if (n < N)
+      for (int64_t b = 0; b < bpr; ++b) mx = fmaxf(mx, __half2float(__ushort_as_half(scales[n * bpr + b])));
+    // e = floor(log2(mx)) - 10 (mx a positive binary16 value: frexpf is exact)
+    int ex = 0;
+    frexpf(mx > 0.f ? mx : 1.f, &ex);  // mx = f * 2^ex, f in [0.5, 1)
+    rowf[n] = ldexpf(1.f, ex - 1 - 10);
+  }
+}
+
 __global__ void fgq_stage_params_kernel(const uint16_t* __restrict__ scales, const uint16_t* __restrict__ zeros,
                                         int64_t N, int64_t bpr, int64_t bkt, int64_t k_tiles, int64_t total,
-                                        void* __restrict__ out) {
+                                        const float* __restrict__ rowf, void* __restrict__ out) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t r = i % kTileN, t = i / kTileN, kt = t % k_tiles, n = (t / k_tiles) * kTileN + r;
     const int64_t b = n * bpr + kt / bkt;
@@ -156,7 +175,8 @@ __global__ void fgq_stage_params_kernel(const uint16_t* __restrict__ scales, con
     if (zeros) {
       static_cast<uint32_t*>(out)[i] = sc | (n < N ? static_cast<uint32_t>(zeros[b]) << 16 : 0u);
     } else {
-      static_cast<uint16_t*>(out)[i] = static_cast<uint16_t>(sc);
+      const float v = __half2float(__ushort_as_half(static_cast<uint16_t>(sc))) / rowf[n];  // exact: power of 2
+      static_cast<uint16_t*>(out)[i] = __half_as_ushort(__float2half_rn(v));
     }
   }
 }
@@ -237,7 +257,8 @@ int lpqt_int4_prepack(const uint8_t* nibbles, int64_t N, int64_t K, uint8_t* til
 
 int64_t lpqt_fgq_stage_bytes(int64_t N, int64_t K, int with_zeros) {
   if (N <= 0 || K <= 0) return 0;
-  return round_up(N, kTileN) * (round_up(K, kTileK) / kTileK) * (with_zeros ? 4 : 2);
+  const int64_t stage = round_up(N, kTileN) * (round_up(K, kTileK) / kTileK) * (with_zeros ? 4 : 2);
+  return with_zeros ? stage : stage + round_up(N, kTileN) * 4;  // FP6 / FP5: + f32 row factors
 }
 
 int lpqt_fgq_stage_params(const uint16_t* scales, const uint16_t* zeros, int64_t N, int64_t K, int64_t block,
@@ -249,9 +270,15 @@ int lpqt_fgq_stage_params(const uint16_t* scales, const uint16_t* zeros, int64_t
   const int64_t k_tiles = round_up(K, kTileK) / kTileK;
   const int64_t bpr = per_row ? 1 : (K + block - 1) / block;
   const int64_t bkt = per_row ? k_tiles : block / kTileK;
-  const int64_t total = round_up(N, kTileN) * k_tiles;
+  const int64_t Np = round_up(N, kTileN);
+  const int64_t total = Np * k_tiles;
+  float* rowf = zeros ? nullptr : reinterpret_cast<float*>(static_cast<uint8_t*>(out) + total * 2);
+  if (!zeros) {
+    fgq_row_factor_kernel<<<grid_for(Np, 256), 256, 0, as_stream(stream)>>>(scales, N, Np, bpr, rowf);
+    note_launch();
+  }
   fgq_stage_params_kernel<<<grid_for(total, 256), 256, 0, as_stream(stream)>>>(scales, zeros, N, bpr, bkt, k_tiles,
-                                                                               total, out);
+                                                                               total, rowf, out);
   note_launch();
   return check_launch();
 }

@@ -569,6 +569,41 @@ def test_fgq_gemm_vs_oracle(n, k, block, m):
     assert normwise_rel(y2.cpu().numpy(), y.cpu().numpy()) <= 1e-5
 
 
+@pytest.mark.parametrize("m", [1, 16, 32, 33, 300])
+@pytest.mark.parametrize("n,k,block", [(512, 2048, 128), (384, 4096, 256), (1024, 8192, 128)])
+def test_fgq_block_magnitudes_1e6_to_1_per_row(n, k, block, m):
+    """block magnitudes spanning 1e-6 .. 1 inside every row.
+    Decode widths (M <= 32) scale each 128-k partial in fp32 (the reference's
+    FGQ order, gemm.py:96-110); wider batches rebuild v * S'_b in binary16 with
+    the row's power-of-two factor applied in fp32 (no binary16 underflow).
+    Checked ELEMENTWISE per row against the oracle's block-partial GEMM on the
+    same fp16 activations: |y - y_ref| <= 1e-3 * max_row |y_ref| for every
+    row, and within the reference's own f32 bound (gemm.py:118-122, with the
+    2^-11 binary16-rebuild term for M > 32) of the f64 product of the
+    oracle's W_hat."""
+    rng = np.random.default_rng(n + k + block + m)
+    nb = -(-k // block)
+    mag = 10.0 ** rng.uniform(-6, 0, size=(n, nb))
+    Wn = rng.standard_normal((n, k)) * np.repeat(mag, block, axis=1)[:, :k]
+    W = torch.from_numpy(Wn.astype(np.float32)).cuda()
+    w = L.Fp6Weight.quantize(W, block=block)
+    o = O.quantize_tensor_fgq(Wn.astype(np.float32), block, True)
+    codes = w.codes().cpu().numpy()
+    assert np.array_equal(codes.ravel(), o["codes"]) and np.array_equal(
+        w.scales.cpu().numpy().view(np.uint16), o["scales"].view(np.uint16))
+    x = torch.randn(m, k, device="cuda", generator=torch.Generator(device="cuda").manual_seed(m)).half()
+    X = x.t().float().cpu().numpy()
+    y = L.w6a16_linear(x, w, out_dtype=torch.float32).t().cpu().numpy().astype(np.float64)
+    Yo = O.gemm_quantized_fgq(o["codes"], o["scales"], n, k, block, X).astype(np.float64)
+    row_max = np.maximum(np.abs(Yo).max(axis=1, keepdims=True), 1e-30)
+    assert np.all(np.abs(y - Yo) <= 1e-3 * row_max)
+    W_hat = O.value_table()[o["codes"].reshape(n, k)] * O.block_scale_per_element(o["scales"], n, k, block)
+    Yf64 = W_hat @ X.astype(np.float64)
+    extra = 2.0 ** -11 if m > 32 else 0.0
+    tol = (4 * np.finfo(np.float32).eps + extra) * k * np.abs(W_hat).max(axis=1, keepdims=True) * np.abs(X).max()
+    assert np.all(np.abs(y - Yf64) <= tol)
+
+
 # ---------------------------------------------------------------- FP5 e3m1 (4 + 1)
 FP5_GOLD = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "golden_fp5.npz")
 
@@ -686,8 +721,10 @@ def test_w4a16_gemm_vs_oracle(n, k, m, block):
 def test_block_params_every_schedule(fmt, sched, split_k):
     """Stage-ordered block parameters (FGQ scales, INT4 scale | zero) under
     stream-K and cluster split-K, ragged K (odd k-tile counts split unevenly
-    over the cluster ranks): within the bar of the f64 product of the
-    kernel's binary16 weights, deterministic."""
+    over the cluster ranks): within 1e-5 of the f64 product of the weights
+    the kernel multiplies — the exact v * S_b for FGQ FP6 at decode widths
+    (block scales applied to fp32 per-tile partials), the binary16 rebuild
+    otherwise — and deterministic."""
     n, k = 1000, 3000 if fmt != "fp6_fgq" else 3072
     rng = np.random.default_rng(hash((fmt, sched, split_k)) % 2**32)
     W = (rng.standard_normal((n, k)) * 0.02).astype(np.float16)
@@ -695,7 +732,9 @@ def test_block_params_every_schedule(fmt, sched, split_k):
         x = torch.from_numpy(rng.standard_normal((m, k)).astype(np.float16)).cuda()
         if fmt == "fp6_fgq":
             w = L.Fp6Weight.quantize(torch.from_numpy(W).cuda(), block=256)
-            Wh = w.dequantize_f16().double()
+            q = L.quantize_tensor(torch.from_numpy(W).cuda(), L.QuantScheme(L.Granularity.FGQ,
+                                                                           L.TensorFormat.FP6_E3M2, 256))
+            Wh = L.dequantize_tensor(q) if m <= 32 else w.dequantize_f16().double()
         else:
             block = 256 if fmt == "int4_fgq" else 0
             gran = L.Granularity.FGQ if block else L.Granularity.CGQ
