@@ -172,6 +172,9 @@ struct L2Prefetch {
 #ifndef LPQT_TILE_RING
 #define LPQT_TILE_RING 1
 #endif
+#ifndef LPQT_PREFILL_XSTAGES
+#define LPQT_PREFILL_XSTAGES 3  // BN 192: X stages of 48 KB (W gets the rest of the budget)
+#endif
 #ifndef LPQT_PD_SLOTS16
 #define LPQT_PD_SLOTS16 4  // FGQ per-block partial slots at BN 16 (TMEM: <= 6)
 #endif
@@ -200,7 +203,7 @@ struct Cfg {
   static constexpr int kXStageBytes = kKStep * kXTileBytes;
   // prefill (BN = 256): an X stage is 64 KB and covers ~1000 MMA cycles, so
   // three stages keep the L2 latency of X hidden (2 W stages of 12 KB suffice)
-  static constexpr int kXStages = BN <= 16 ? (CSK ? 4 : 6) : (BN <= 128 ? 4 : 3);
+  static constexpr int kXStages = BN <= 16 ? (CSK ? 4 : 6) : (BN <= 128 ? 4 : (BN == 192 ? LPQT_PREFILL_XSTAGES : 3));
   // CSK: two partial staging buffers of 128 x BN fp32 (rounds alternate)
   static constexpr int kStageBufBytes = CSK ? kTileN * BN * 4 : 0;
   // decode: output tiles staged in smem (two 128 x BN buffers, fp32-sized) and
