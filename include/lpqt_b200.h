@@ -177,6 +177,12 @@ int lpqt_w6a16_linear(const uint8_t* tiles, const uint16_t* scales,
  * (k-split factor, 1..8) for decode batches (M <= 32). */
 #define LPQT_SCHED_STREAMK 2
 #define LPQT_SCHED_CLUSTER 4
+/* Prefill (CGQ, even number of 128-row weight tiles): the CTA-pair kernel
+ * (tcgen05 cta_group::2, M = 256 x N = 256 MMAs, prefill2sm.cu) is picked by
+ * a time model; LPQT_SCHED_PAIR forces it where the shape allows,
+ * LPQT_SCHED_SINGLE forbids it (A/B hooks). */
+#define LPQT_SCHED_SINGLE 8
+#define LPQT_SCHED_PAIR 16
 int lpqt_w6a16_linear_ex(const uint8_t* tiles, const uint16_t* scales,
                          const uint16_t* Xt, int64_t ldx, int64_t M, int64_t N,
                          int64_t K, void* Y, int y_dtype, int y_layout,

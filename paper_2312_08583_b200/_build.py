@@ -17,7 +17,7 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 BUILD = os.path.join(ROOT, "build", "lpqt")
 LIB = os.path.join(PKG, "liblpqt_b200.so")
-SOURCES = ["capi.cu", "quantize.cu", "prepack.cu", "gemm.cu", "exact.cu"]
+SOURCES = ["capi.cu", "quantize.cu", "prepack.cu", "gemm.cu", "exact.cu", "prefill2sm.cu"]
 HEADERS = ["common.cuh"]
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

@@ -591,23 +591,7 @@ __device__ __forceinline__ void cluster_sync_all() {
   asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 
-// ---- output tile staging + TMA tensor store (decode) --------------------------
-__device__ __forceinline__ void fence_proxy_async_global() {
-  asm volatile("fence.proxy.async.global;" ::: "memory");
-}
-__device__ __forceinline__ void fence_proxy_async_smem() {
-  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-}
-__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, uint32_t smem, int c0, int c1) {
-  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(map),
-               "r"(smem), "r"(c0), "r"(c1)
-               : "memory");
-}
-__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void bulk_wait_read() {
-  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
-}
+// ---- output tile staging (decode; the TMA store helpers are in common.cuh) ----
 // 16 scaled values of output row n (tile row rr), columns m0 + c0 .. + 15,
 // into the staged tile in the tensor map's box layout: Y_MN box [BN][128]
 // (n fastest), Y_NM box [128][BN] (m fastest); element type = y_dtype.
@@ -1823,6 +1807,35 @@ static Plan make_plan(int64_t M, int64_t N, int64_t K, int split_k, int flags, i
   return p;
 }
 
+int launch_prefill_2sm(const uint8_t* tiles, const uint16_t* scales, const uint16_t* Xt, int64_t ldx, int64_t M,
+                       int64_t N, int64_t K, void* Y, int y_dtype, int y_layout, int64_t ldy, int flags,
+                       cudaStream_t stream, int* grid_out);  // prefill2sm.cu
+int prefill_2sm_pairs();                                       // prefill2sm.cu
+double prefill_2sm_choose(int64_t M, int64_t N, int64_t K, int* bn_out);  // prefill2sm.cu
+
+// The CTA-pair prefill kernel (prefill2sm.cu) vs this file's single-SM one:
+// per-SM cycle estimates, pair kernel ~1024 cycles per 128-k step of a
+// 256 x 256 unit at ~90 % tensor-pipe efficiency, whole units per pair;
+// single-SM kernel: the BN-192 / 128 step cost over 148 SMs at the measured
+// ~68 % efficiency (profiles/r02_ncu_prefill_m2048.json).
+#ifndef LPQT_PAIR_MIN_M
+#define LPQT_PAIR_MIN_M 129  // (below: decode / small prefill stay single-SM)
+#endif
+static bool use_pair_kernel(int64_t M, int64_t N, int64_t K, int flags) {
+  if (flags & LPQT_SCHED_SINGLE) return false;
+  const int64_t n_tiles = (N + kTileN - 1) / kTileN;
+  if (n_tiles % 2 != 0 || M < 17) return false;
+  if (flags & LPQT_SCHED_PAIR) return true;
+  if (flags & (LPQT_SCHED_STREAMK | LPQT_SCHED_CLUSTER) || M < LPQT_PAIR_MIN_M) return false;
+  const int64_t k_tiles = (K + kTileK - 1) / kTileK;
+  const double t2 = prefill_2sm_choose(M, N, K, nullptr) / 0.8;
+  const int bn = pick_bn(M);
+  const int64_t tiles = n_tiles * ((M + bn - 1) / bn);
+  const double step = bn >= 192 ? 768.0 / 0.68 : 600.0;
+  const double t1 = (double)tiles * k_tiles * step / num_sms();
+  return t2 < t1;
+}
+
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
@@ -2010,6 +2023,14 @@ int64_t lpqt_w6a16_workspace_bytes(int64_t M, int64_t N, int64_t K, int split_k)
 int lpqt_w6a16_plan_ex(int64_t M, int64_t N, int64_t K, int split_k, int flags, int* out, int n_out) {
   if (M <= 0 || N <= 0 || K <= 0) return LPQT_E_SHAPE;
   if ((flags & LPQT_SCHED_STREAMK) && (flags & LPQT_SCHED_CLUSTER)) return LPQT_E_INVALID_INPUT;
+  if (split_k == 0 && use_pair_kernel(M, N, K, flags)) {
+    int bn = 256;
+    prefill_2sm_choose(M, N, K, &bn);
+    const int64_t units = ((N + kTileN - 1) / kTileN / 2) * ((M + bn - 1) / bn);
+    const int v[6] = {bn, 1, 2 * (int)std::min<int64_t>(prefill_2sm_pairs(), units), 6, 3, 2};
+    for (int i = 0; i < n_out && i < 6; ++i) out[i] = v[i];
+    return LPQT_OK;
+  }
   const Plan p = make_plan(M, N, K, split_k, flags, num_sms());
   const int v[6] = {p.bn, p.splits, p.grid, p.stages, p.csk ? 1 : (p.dp ? 2 : 0), p.csk ? p.cluster : 0};
   for (int i = 0; i < n_out && i < 6; ++i) out[i] = v[i];
@@ -2055,7 +2076,8 @@ static int w6a16_blocks_impl(const uint8_t* tiles, const uint16_t* scales, int64
                              int64_t ldx, int64_t M, int64_t N, int64_t K, void* Y, int y_dtype, int y_layout,
                              int64_t ldy, int split_k, void* workspace, int64_t workspace_bytes, int flags,
                              const lpqt_next_linear* next, void* stream, const lpqt_peer_out* po) {
-  if (flags & ~(LPQT_LAUNCH_PDL | LPQT_SCHED_STREAMK | LPQT_SCHED_CLUSTER)) return LPQT_E_INVALID_INPUT;
+  if (flags & ~(LPQT_LAUNCH_PDL | LPQT_SCHED_STREAMK | LPQT_SCHED_CLUSTER | LPQT_SCHED_SINGLE | LPQT_SCHED_PAIR))
+    return LPQT_E_INVALID_INPUT;
   // FGQ: blocks of B columns (B = K, or block <= 0: one scale per row)
   const bool fgq = block > 0 && block < K;
   if (fgq && block % kTileK != 0) return LPQT_E_UNSUPPORTED;   // block scales at 128-k tile granularity
@@ -2071,6 +2093,11 @@ static int w6a16_blocks_impl(const uint8_t* tiles, const uint16_t* scales, int64
   if (y_layout == LPQT_Y_NM ? ldy < M : ldy < N) return LPQT_E_SHAPE;
   if (split_k < 0) return LPQT_E_INVALID_INPUT;
   if (N > (int64_t)1 << 30 || M > (int64_t)1 << 30 || K > (int64_t)1 << 30) return LPQT_E_SHAPE;
+  if (!fgq && !po && split_k == 0 && use_pair_kernel(M, N, K, flags)) {
+    const int st = launch_prefill_2sm(tiles, scales, Xt, ldx, M, N, K, Y, y_dtype, y_layout, ldy, flags,
+                                      as_stream(stream), nullptr);
+    if (st != LPQT_E_UNSUPPORTED) return st;
+  }
   Plan p = make_plan(M, N, K, split_k, flags, num_sms(), fgq);
   if (p.ws_bytes > 0 && (workspace == nullptr || workspace_bytes < p.ws_bytes)) return LPQT_E_WORKSPACE;
   GemmArgs args{};

@@ -1,0 +1,542 @@
+// prefill2sm.cu — the W6A16 GEMM at prefill batch sizes on CTA PAIRS
+// (tcgen05 cta_group::2), gemm.py:65-94 CGQ.
+//
+// Why a second kernel: at prefill the single-SM kernel (gemm.cu, BN 192) feeds
+// each 768-cycle 128 x 192 x 128 MMA step with 48 KB of X from L2 and only
+// three X stages fit next to the weight ring; measured 68 % tensor-pipe
+// activity at M = 2048 with the dequant warps waiting on the MMA
+// (profiles/r02_ncu_prefill_m2048.json).  A CTA pair runs M = 256 x N = 256
+// MMAs: each SM still dequantizes ONE 128-row weight tile per 128-k step into
+// its own TMEM (A operand, "TS" MMA), but loads only HALF of the 256 batch
+// columns of X (its half of B); the pair's MMA reads both halves.  Per SM and
+// k step: 1024 MMA cycles against ~600 dequant cycles and 32 KB of X + 12 KB
+// of weights — X per MMA cycle is half the single-SM kernel's, and four X
+// stages + six weight stages fit in shared memory.
+//
+// Work unit: 2 weight-row tiles (one per CTA: rank r owns row tile 2p + r)
+// x 256 batch columns, the whole K (no split-K: prefill has units for every
+// pair).  Unit u -> (pair, batch tile); cluster c takes u = c, c + #clusters,...
+//
+// Roles per CTA (768 threads): warps 0-15 dequant (two groups of 8 on
+// alternate k steps, warp w: lane group w % 4, k-half (w / 4) % 2), warp 16
+// W producer (1-D bulk copy of the CTA's 12 KB weight tile per step), warp 17
+// X producer (TMA of the CTA's 128 X rows, completing on the LEADER's
+// barrier), warp 18 MMA issuer (leader CTA only: tcgen05.mma.cta_group::2,
+// commits multicast to both CTAs), warps 20-23 epilogue (own 128 rows x 256
+// columns of D from own TMEM, x row scale, Y).  Cross-CTA hand-offs: the
+// follower's dequant and epilogue warps arrive on the leader's afull /
+// dempty barriers (mapa + release.cluster); its X TMA completes on the
+// leader's full_x; the MMA's commits reach both CTAs' empty_x / aempty /
+// dfull (multicast::cluster).
+#include <string.h>
+
+#include <algorithm>
+#include <mutex>
+
+#include "common.cuh"
+
+namespace lpqt {
+namespace p2 {
+
+constexpr int kMaxBN = 256;              // MMA N (batch columns of a unit): a.bn, a multiple of 32 <= 256
+constexpr int kHalf = kMaxBN / 2;        // X rows each CTA loads at most
+constexpr int kDqWarps = 16;
+constexpr int kWarpW = 16, kWarpX = 17, kWarpMma = 18, kWarpEpi0 = 20;
+constexpr int kThreads = 24 * 32;
+constexpr int kXStage = kHalf * kTileK * 2;   // 32 KB: two SW128 boxes of 64 k x 128 rows
+constexpr int kXStages = 4;
+constexpr int kWStages = 6;                   // even: the two dequant groups alternate
+constexpr int kASlots = 4;                    // 64 TMEM columns each (one 128 x 128 f16 tile)
+constexpr int kAColsTile = kTileK / 2;
+constexpr int kDCol0 = kASlots * kAColsTile;  // D: 256 fp32 columns after the A ring
+constexpr int kTmemCols = 512;
+constexpr int kYChunk = 32;                   // epilogue: 32 batch columns per TMA store
+constexpr int kYBuf = kYChunk * kTileN * 2;   // 8 KB staging (16-bit Y), double-buffered
+constexpr int kSmemBytes = kXStages * kXStage + kWStages * kTileBytes + 2 * kYBuf +
+                           8 * (2 * kXStages + 2 * kWStages + 2 * kASlots + 2) + 16;
+static_assert(kSmemBytes <= 227 * 1024, "shared memory");
+
+struct Args {
+  const uint8_t* tiles;
+  const uint16_t* scales;
+  void* y;
+  int64_t ldy;
+  int M, N, k_tiles, n_tiles, m_tiles, units, n_fastest, y_dtype, y_layout;
+  int bn;     // batch columns per unit (MMA N; each CTA loads bn / 2 X rows)
+  int y_tma;  // Y[M, N] 16-bit: the epilogue stages 32-column chunks and TMA-stores them
+  ShiftMuls sm;
+};
+
+__device__ __forceinline__ uint32_t cta_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t mapa(uint32_t addr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
+  return r;
+}
+// arrive on a barrier of either CTA of the pair.  Default (release.cta)
+// semantics: what the consumer needs ordered is TMEM (tcgen05.wait::st /
+// wait::ld + tcgen05.fence::before_thread_sync precede the arrive), not
+// generic memory; a release.cluster arrive costs a MEMBAR per call — measured
+// 44 % of the dequant warps' stall samples (profiles/r02_ncu_pair_m2048.json).
+__device__ __forceinline__ void arrive_cluster(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+__device__ __forceinline__ void wait_cluster(uint32_t addr, uint32_t parity) {
+  uint32_t ok = 0, spins = 0;
+  do {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2, %3;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(addr), "r"(parity), "r"(LPQT_WAIT_HINT_NS)
+        : "memory");
+    if (++spins == (1u << 28)) __trap();  // a pipeline bug fails the launch instead of hanging
+  } while (!ok);
+}
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// X half of this CTA into its own smem; completion counted on the leader's barrier
+__device__ __forceinline__ void tma_x_2sm(uint32_t pred, uint32_t dst, const CUtensorMap* map, uint32_t mbar_cluster,
+                                          int c0, int c1) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\t"
+      "setp.ne.b32 e, %0, 0;\n\t"
+      "@e cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%1], [%2, {%4, "
+      "%5}], [%3];\n\t}" ::"r"(pred),
+      "r"(dst), "l"(map), "r"(mbar_cluster), "r"(c0), "r"(c1)
+      : "memory");
+}
+__device__ __forceinline__ void mma_2sm(uint32_t pred, uint32_t d_tmem, uint32_t a_tmem, uint32_t b_lo, uint32_t b_hi,
+                                        uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\t.reg .b64 bd;\n\t"
+      "setp.ne.b32 e, %0, 0;\n\t"
+      "setp.ne.b32 p, %6, 0;\n\t"
+      "mov.b64 bd, {%3, %4};\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%1], [%2], bd, %5, p;\n\t}" ::"r"(pred),
+      "r"(d_tmem), "r"(a_tmem), "r"(b_lo), "r"(b_hi), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void commit_2sm(uint32_t pred, uint64_t* bar) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\t"
+      "setp.ne.b32 e, %0, 0;\n\t"
+      "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%1], %2;\n\t}" ::"r"(
+          pred),
+      "r"(smem_u32(bar)), "h"(static_cast<uint16_t>(3))
+      : "memory");
+}
+
+// unit u of this cluster's sequence -> (pair, batch tile)
+__device__ __forceinline__ void unit_nm(const Args& a, int u, int& pair, int& mt) {
+  const int n_pairs = a.n_tiles / 2;
+  if (a.n_fastest) {
+    mt = u / n_pairs;
+    pair = u - mt * n_pairs;
+  } else {
+    pair = u / a.m_tiles;
+    mt = u - pair * a.m_tiles;
+  }
+}
+
+__device__ __forceinline__ void store_y(const Args& a, int n, int m, float v) {
+  if (n >= a.N || m >= a.M) return;
+  const int64_t off = a.y_layout == LPQT_Y_NM ? (int64_t)n * a.ldy + m : (int64_t)m * a.ldy + n;
+  if (a.y_dtype == LPQT_F32) {
+    static_cast<float*>(a.y)[off] = v;
+  } else if (a.y_dtype == LPQT_F16) {
+    static_cast<__half*>(a.y)[off] = __float2half_rn(v);
+  } else {
+    static_cast<__nv_bfloat16*>(a.y)[off] = __float2bfloat16_rn(v);
+  }
+}
+
+__global__ void __launch_bounds__(kThreads, 1)
+    w6a16_prefill_2sm_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constant__ CUtensorMap tmap_y,
+                             const Args a) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem_x = smem_raw;
+  uint8_t* smem_w = smem_x + kXStages * kXStage;
+  uint8_t* smem_y = smem_w + kWStages * kTileBytes;
+  uint64_t* full_x = reinterpret_cast<uint64_t*>(smem_y + 2 * kYBuf);
+  uint64_t* empty_x = full_x + kXStages;
+  uint64_t* full_w = empty_x + kXStages;
+  uint64_t* empty_w = full_w + kWStages;
+  uint64_t* afull = empty_w + kWStages;
+  uint64_t* aempty = afull + kASlots;
+  uint64_t* dfull = aempty + kASlots;
+  uint64_t* dempty = dfull + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(dempty + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cta_rank();
+  const bool leader = rank == 0;
+  const int cid = static_cast<int>(blockIdx.x) >> 1, ncl = static_cast<int>(gridDim.x) >> 1;
+  const int my_units = cid < a.units ? (a.units - 1 - cid) / ncl + 1 : 0;
+  const int n_st = my_units * a.k_tiles;
+
+  if (threadIdx.x == 0) {
+    if (smem_u32(smem_raw) & 1023u) __trap();
+    for (int s = 0; s < kXStages; ++s) {
+      mbar_init(&full_x[s], 1);   // leader: its expect_tx arrival (+ both halves' bytes)
+      mbar_init(&empty_x[s], 1);  // MMA commit (multicast)
+    }
+    for (int s = 0; s < kWStages; ++s) {
+      mbar_init(&full_w[s], 1);
+      mbar_init(&empty_w[s], kDqWarps / 2);  // the dequant group owning the slot
+    }
+    for (int b = 0; b < kASlots; ++b) {
+      mbar_init(&afull[b], 2 * (kDqWarps / 2));  // leader: both CTAs' dequant group
+      mbar_init(&aempty[b], 1);                  // MMA commit (multicast)
+    }
+    mbar_init(dfull, 1);
+    mbar_init(dempty, 2 * 4);  // leader: both CTAs' epilogue warps
+    fence_mbar_init();
+  }
+  if (warp == kWarpMma) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(kTmemCols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+  }
+  if (warp == kWarpX && lane == 0) prefetch_tmap(&tmap_x);
+  tc_fence_before();
+  cluster_sync();  // barriers of both CTAs initialised, TMEM allocated
+  tc_fence_after();
+  pdl_launch_dependents();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == kWarpW || warp == kWarpX || warp == kWarpMma || warp == kWarpMma + 1) {
+    setmaxnreg_dec<48>();
+    if (warp == kWarpW) {
+      // ------------------------------------------------ W producer (own row tile)
+      const uint64_t pol = l2_evict_last_policy();  // a weight tile is re-read once per batch tile
+      for (int i = 0; i < n_st; ++i) {
+        const int ul = i / a.k_tiles, kt = i - ul * a.k_tiles;
+        int pair, mt;
+        unit_nm(a, cid + ul * ncl, pair, mt);
+        const int s = i % kWStages;
+        mbar_wait<2>(&empty_w[s], ((i / kWStages) & 1) ^ 1);
+        const uint32_t e = elect_one();
+        mbar_arrive_expect_tx_if(e, &full_w[s], kTileBytes);
+        bulk_g2s_if(e, smem_w + s * kTileBytes,
+                    a.tiles + ((int64_t)(2 * pair + rank) * a.k_tiles + kt) * kTileBytes, kTileBytes, &full_w[s], pol);
+      }
+    } else if (warp == kWarpX) {
+      // ------------------------------------------------ X producer (own half of the batch tile)
+      pdl_wait();  // X is the preceding kernel's output
+      const uint32_t fx_leader = mapa(smem_u32(full_x), 0);
+      for (int i = 0; i < n_st; ++i) {
+        const int ul = i / a.k_tiles, kt = i - ul * a.k_tiles;
+        int pair, mt;
+        unit_nm(a, cid + ul * ncl, pair, mt);
+        const int s = i % kXStages;
+        mbar_wait<2>(&empty_x[s], ((i / kXStages) & 1) ^ 1);
+        const uint32_t e = elect_one();
+        const int half = a.bn >> 1;
+        if (leader) mbar_arrive_expect_tx_if(e, &full_x[s], static_cast<uint32_t>(a.bn * kTileK * 2));
+        const uint32_t dst = smem_u32(smem_x + s * kXStage);
+        const int row = mt * a.bn + static_cast<int>(rank) * half;
+        tma_x_2sm(e, dst, &tmap_x, fx_leader + 8 * s, kt * kTileK, row);
+        tma_x_2sm(e, dst + half * 128, &tmap_x, fx_leader + 8 * s, kt * kTileK + 64, row);
+      }
+    } else if (warp == kWarpMma && leader) {
+      // ------------------------------------------------ MMA issuer (leader only)
+      const uint32_t idesc = (1u << 4) | (static_cast<uint32_t>(a.bn >> 3) << 17) |
+                             (static_cast<uint32_t>(256 >> 4) << 24);
+      const int half = a.bn >> 1;
+      const uint32_t d_tmem = tmem_base + kDCol0;
+      const uint32_t ae_bar = smem_u32(afull), dm_bar = smem_u32(dempty), fx_bar = smem_u32(full_x);
+      for (int ul = 0; ul < my_units; ++ul) {
+        wait_cluster(dm_bar, (ul & 1) ^ 1);  // both CTAs drained D
+        tc_fence_after();
+        for (int kt = 0; kt < a.k_tiles; ++kt) {
+          const int i = ul * a.k_tiles + kt;
+          const int xs = i % kXStages, sl = i % kASlots;
+          wait_cluster(fx_bar + 8 * xs, (i / kXStages) & 1);     // both X halves landed
+          wait_cluster(ae_bar + 8 * sl, (i / kASlots) & 1);      // both A tiles rebuilt
+          tc_fence_after();
+          const uint32_t e = elect_one();
+          const uint64_t bd0 = sdesc_kmajor_sw128(smem_u32(smem_x + xs * kXStage));
+          const uint32_t bd_lo = static_cast<uint32_t>(bd0), bd_hi = static_cast<uint32_t>(bd0 >> 32);
+          const uint32_t ta = tmem_base + sl * kAColsTile;
+#pragma unroll
+          for (int j = 0; j < kTileK / 16; ++j) {
+            const uint32_t off = ((j >> 2) * (half * 128) + (j & 3) * 32) >> 4;
+            mma_2sm(e, d_tmem, ta + j * 8, bd_lo + off, bd_hi, idesc, (kt | j) ? 1u : 0u);
+          }
+          commit_2sm(e, &empty_x[xs]);
+          commit_2sm(e, &aempty[sl]);
+        }
+        commit_2sm(elect_one(), dfull);
+      }
+    }
+  } else if (warp < kDqWarps) {
+    // ------------------------------------------------ dequant (own row tile -> own TMEM A)
+    setmaxnreg_inc<88>();
+    const int lg = warp & 3, grp = warp >> 3, tl = (warp >> 2) & 1;
+    const int row = lg * 32 + lane;
+    const uint32_t w_src = smem_u32(smem_w) + static_cast<uint32_t>(row * 16 + tl * 3 * kTileN * 16);
+    const uint32_t t_lane = tmem_base + (static_cast<uint32_t>(lg * 32) << 16) + static_cast<uint32_t>(tl * 32);
+    const uint32_t af_leader = mapa(smem_u32(afull), 0);
+    const ShiftMuls sm = a.sm;
+    uint32_t q[12];
+    auto load = [&](int i) {
+      const int s = i % kWStages;
+      mbar_wait<2>(&full_w[s], (i / kWStages) & 1);
+      const uint32_t src = w_src + s * kTileBytes;
+      const uint4 v0 = lds128_u32(src), v1 = lds128_u32(src + kTileN * 16), v2 = lds128_u32(src + 2 * kTileN * 16);
+      q[0] = v0.x; q[1] = v0.y; q[2] = v0.z; q[3] = v0.w; q[4] = v1.x; q[5] = v1.y;
+      q[6] = v1.z; q[7] = v1.w; q[8] = v2.x; q[9] = v2.y; q[10] = v2.z; q[11] = v2.w;
+    };
+    if (grp < n_st) load(grp);
+    for (int i = grp; i < n_st; i += 2) {
+      uint32_t r[32];
+      fp6x32_cvt_f16x32_fma(q, r, sm);
+      fp6x32_cvt_f16x32_fma(q + 6, r + 16, sm);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty_w[i % kWStages]);  // words consumed
+      const int sl = i % kASlots;
+      mbar_wait<2>(&aempty[sl], ((i / kASlots) & 1) ^ 1);
+      tc_fence_after();
+      tmem_st_x32(t_lane + sl * kAColsTile, r);
+      if (i + 2 < n_st) load(i + 2);
+      tmem_wait_st();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) arrive_cluster(af_leader + 8 * sl);
+    }
+  } else {
+    // ------------------------------------------------ epilogue (own 128 rows x bn columns)
+    setmaxnreg_dec<72>();
+    const int lg = warp & 3;
+    const int rr = lg * 32 + lane;
+    const uint32_t t_d = tmem_base + kDCol0 + (static_cast<uint32_t>(lg * 32) << 16);
+    const uint32_t dm_leader = mapa(smem_u32(dempty), 0);
+    const bool lead_thread = warp == kWarpEpi0 && lane == 0;
+    int nchunk = 0;  // TMA-stored chunks so far (staging buffer = nchunk & 1)
+    pdl_wait();      // Y writes: the preceding grid must be complete
+    for (int ul = 0; ul < my_units; ++ul) {
+      int pair, mt;
+      unit_nm(a, cid + ul * ncl, pair, mt);
+      const int n0 = (2 * pair + static_cast<int>(rank)) * kTileN, n = n0 + rr;
+      const float fs = n < a.N ? __half2float(__ushort_as_half(__ldg(a.scales + n))) : 0.f;
+      mbar_wait<2>(dfull, ul & 1);
+      tc_fence_after();
+#pragma unroll 1
+      for (int c0 = 0; c0 < a.bn; c0 += kYChunk) {
+        uint32_t v[kYChunk];
+        tmem_ld_x16(t_d + c0, *reinterpret_cast<uint32_t(*)[16]>(v));
+        tmem_ld_x16(t_d + c0 + 16, *reinterpret_cast<uint32_t(*)[16]>(v + 16));
+        tmem_wait_ld();
+        if (c0 + kYChunk >= a.bn) {  // last chunk read: D may be overwritten
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) arrive_cluster(dm_leader);
+        }
+        const int m0 = mt * a.bn + c0;
+        if (a.y_tma) {
+          // [32 m][128 n] 16-bit tile in smem -> one TMA tensor store (clips m >= M, n >= N)
+          const uint32_t buf = smem_u32(smem_y) + (nchunk & 1) * kYBuf;
+          if (nchunk >= 2) {
+            if (lead_thread) bulk_wait_read<1>();  // this buffer's previous store has read it
+            named_bar_sync(1, 4 * 32);
+          }
+#pragma unroll
+          for (int j = 0; j < kYChunk; ++j) {
+            const float f = __uint_as_float(v[j]) * fs;
+            const uint16_t h = a.y_dtype == LPQT_F16 ? __half_as_ushort(__float2half_rn(f))
+                                                     : __bfloat16_as_ushort(__float2bfloat16_rn(f));
+            asm volatile("st.shared.u16 [%0], %1;" ::"r"(buf + (j * kTileN + rr) * 2), "h"(h) : "memory");
+          }
+          fence_proxy_async_smem();
+          named_bar_sync(1, 4 * 32);
+          if (lead_thread) {
+            tma_store_2d(&tmap_y, buf, n0, m0);
+            bulk_commit();
+          }
+          ++nchunk;
+        } else {
+#pragma unroll
+          for (int j = 0; j < kYChunk; ++j) store_y(a, n, m0 + j, __uint_as_float(v[j]) * fs);
+        }
+      }
+    }
+    if (lead_thread) bulk_wait_read<0>();  // staging smem stays valid until the stores read it
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync();  // no CTA leaves while its peer may still signal its barriers / read its TMEM
+  if (warp == kWarpMma) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(kTmemCols) : "memory");
+  }
+}
+
+}  // namespace p2
+
+typedef CUresult (*EncodeTiledFn2)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeTiledFn2 encode_fn_2sm() {
+  static EncodeTiledFn2 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn2>(p);
+  });
+  return fn;
+}
+
+// Co-resident CTA pairs (GPC packing); queried once.
+static int max_pairs() {
+  static int n = 0;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    int v = 0;
+    if (cudaFuncSetAttribute(p2::w6a16_prefill_2sm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             p2::kSmemBytes) == cudaSuccess) {
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(2 * 64);
+      cfg.blockDim = dim3(p2::kThreads);
+      cfg.dynamicSmemBytes = p2::kSmemBytes;
+      cudaLaunchAttribute attr[1];
+      attr[0].id = cudaLaunchAttributeClusterDimension;
+      attr[0].val.clusterDim.x = 2;
+      attr[0].val.clusterDim.y = 1;
+      attr[0].val.clusterDim.z = 1;
+      cfg.attrs = attr;
+      cfg.numAttrs = 1;
+      if (cudaOccupancyMaxActiveClusters(&v, p2::w6a16_prefill_2sm_kernel, &cfg) != cudaSuccess) v = 0;
+    }
+    cudaGetLastError();
+    n = v > 0 ? v : 74;
+  });
+  return n;
+}
+
+int prefill_2sm_pairs() { return max_pairs(); }
+
+// Unit width: the batch columns bn (a multiple of 32, <= 256) that minimise
+// rounds x k-step cost, rounds = ceil(units / co-resident pairs); a k step
+// costs max(4 bn, ~700) cycles (MMA floor M = 256 across the pair:
+// bn / 2 cycles per K = 16; the dequant of one 128 x 128 tile by 16 warps:
+// ~600 + barrier overhead).  Returns the estimated cycles per SM.
+double prefill_2sm_choose(int64_t M, int64_t N, int64_t K, int* bn_out) {
+  const int64_t n_pairs = (N + kTileN - 1) / kTileN / 2;
+  const int64_t k_tiles = (K + kTileK - 1) / kTileK;
+  const int64_t pairs = max_pairs();
+  double best = 1e30;
+  int best_bn = 256;
+  for (int bn = 256; bn >= 128; bn -= 32) {
+    const int64_t units = n_pairs * ((M + bn - 1) / bn);
+    const int64_t rounds = (units + pairs - 1) / pairs;
+    const double step = std::max(4.0 * bn, 700.0);
+    const double t = (double)rounds * (k_tiles * step + 4.0 * bn * 8);  // + the epilogue drain
+    if (t < best * 0.98) {
+      best = t;
+      best_bn = bn;
+    }
+  }
+  if (bn_out) *bn_out = best_bn;
+  return best;
+}
+
+// Host launch of the pair kernel (called from gemm.cu's dispatcher; CGQ FP6,
+// even number of 128-row weight tiles).  Returns LPQT_E_UNSUPPORTED when the
+// shape does not fit (the caller then uses the single-SM kernel).
+int launch_prefill_2sm(const uint8_t* tiles, const uint16_t* scales, const uint16_t* Xt, int64_t ldx, int64_t M,
+                       int64_t N, int64_t K, void* Y, int y_dtype, int y_layout, int64_t ldy, int flags,
+                       cudaStream_t stream, int* grid_out) {
+  const int n_tiles = static_cast<int>((N + kTileN - 1) / kTileN);
+  if (n_tiles % 2 != 0) return LPQT_E_UNSUPPORTED;
+  EncodeTiledFn2 enc = encode_fn_2sm();
+  if (!enc) return LPQT_E_CUDA;
+  int bn = 256;
+  prefill_2sm_choose(M, N, K, &bn);
+  CUtensorMap map;
+  const cuuint64_t dims[2] = {static_cast<cuuint64_t>(K), static_cast<cuuint64_t>(M)};
+  const cuuint64_t strides[1] = {static_cast<cuuint64_t>(ldx) * 2};
+  const cuuint32_t box[2] = {64, static_cast<cuuint32_t>(bn / 2)};
+  const cuuint32_t estr[2] = {1, 1};
+  if (enc(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, const_cast<uint16_t*>(Xt), dims, strides, box, estr,
+          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+    return LPQT_E_INVALID_INPUT;
+  // Y[M, N] with 16-bit elements, 16-B aligned base and row stride: the TMA store epilogue
+  CUtensorMap ymap;
+  memset(&ymap, 0, sizeof(ymap));
+  int y_tma = 0;
+  if (y_layout == LPQT_Y_MN && y_dtype != LPQT_F32 && reinterpret_cast<uintptr_t>(Y) % 16 == 0 &&
+      (ldy * 2) % 16 == 0) {
+    const cuuint64_t ydims[2] = {static_cast<cuuint64_t>(N), static_cast<cuuint64_t>(M)};
+    const cuuint64_t ystr[1] = {static_cast<cuuint64_t>(ldy) * 2};
+    const cuuint32_t ybox[2] = {static_cast<cuuint32_t>(kTileN), static_cast<cuuint32_t>(p2::kYChunk)};
+    if (enc(&ymap, y_dtype == LPQT_F16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, Y,
+            ydims, ystr, ybox, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+            CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS)
+      y_tma = 1;
+  }
+  p2::Args a{};
+  a.tiles = tiles;
+  a.scales = scales;
+  a.y = Y;
+  a.ldy = ldy;
+  a.M = static_cast<int>(M);
+  a.N = static_cast<int>(N);
+  a.k_tiles = static_cast<int>((K + kTileK - 1) / kTileK);
+  a.n_tiles = n_tiles;
+  a.bn = bn;
+  a.y_tma = y_tma;
+  a.m_tiles = static_cast<int>((M + bn - 1) / bn);
+  a.units = (n_tiles / 2) * a.m_tiles;
+  // X larger than ~1/3 of L2: keep each batch tile's X resident (weight-row pairs fastest)
+  a.n_fastest = (a.m_tiles > 1 && M * K * 2 > ((int64_t)40 << 20)) ? 1 : 0;
+  a.y_dtype = y_dtype;
+  a.y_layout = y_layout;
+  a.sm = ShiftMuls{1u << 26, 1u << 28, 1u << 30};
+  const int pairs = std::min(max_pairs(), a.units);
+  static std::once_flag once;
+  static cudaError_t attr_err = cudaSuccess;
+  std::call_once(once, [] {
+    attr_err = cudaFuncSetAttribute(p2::w6a16_prefill_2sm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    p2::kSmemBytes);
+  });
+  if (attr_err != cudaSuccess) return LPQT_E_CUDA;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(2 * pairs);
+  cfg.blockDim = dim3(p2::kThreads);
+  cfg.dynamicSmemBytes = p2::kSmemBytes;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[2];
+  int na = 0;
+  attr[na].id = cudaLaunchAttributeClusterDimension;
+  attr[na].val.clusterDim.x = 2;
+  attr[na].val.clusterDim.y = 1;
+  attr[na].val.clusterDim.z = 1;
+  ++na;
+  if (flags & LPQT_LAUNCH_PDL) {
+    attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[na].val.programmaticStreamSerializationAllowed = 1;
+    ++na;
+  }
+  cfg.attrs = attr;
+  cfg.numAttrs = na;
+  if (grid_out) *grid_out = 2 * pairs;
+  if (cudaLaunchKernelEx(&cfg, p2::w6a16_prefill_2sm_kernel, map, ymap, a) != cudaSuccess) return LPQT_E_CUDA;
+  note_launch();
+  return check_launch();
+}
+
+}  // namespace lpqt

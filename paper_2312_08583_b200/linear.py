@@ -218,7 +218,7 @@ class Int4Weight:
         return (self.n * self.k + 1) // 2 + 4 * int(self.scales.numel())
 
 
-_SCHED_FLAGS = {"auto": 0, "streamk": 2, "cluster": 4}
+_SCHED_FLAGS = {"auto": 0, "streamk": 2, "cluster": 4, "single": 8, "pair": 16}
 
 
 def _sched_flags(sched: str) -> int:
@@ -234,7 +234,7 @@ def plan(m: int, n: int, k: int, split_k: int = 0, sched: str = "auto") -> dict:
     out = (ctypes.c_int * 6)()
     _lib.check(_lib.load().lpqt_w6a16_plan_ex(m, n, k, split_k, _sched_flags(sched), out, 6), "plan")
     return {"block_n": out[0], "splits": out[1], "grid": out[2], "stages": out[3],
-            "schedule": {0: "streamk", 1: "cluster", 2: "roundrobin"}[out[4]], "cluster": out[5]}
+            "schedule": {0: "streamk", 1: "cluster", 2: "roundrobin", 3: "pair"}[out[4]], "cluster": out[5]}
 
 
 def _launch(weight: Fp6Weight, xt, ldx: int, m: int, y, y_dtype: int, y_layout: int, ldy: int, split_k: int,

@@ -1,0 +1,2 @@
+mkdir -p gpurun_out
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:prefill_2sm -s 1 -c 1 -o gpurun_out/r2n_pair_m2048 python tools/profile_pair.py --m 2048 > gpurun_out/r2n_ncu.log 2>&1
