@@ -688,16 +688,27 @@ def main():
         # the other north-star decode point (M = 1) and the 7B step (BASELINE
         # configs[1]); device-timed like the headline, no e2e
         for model, mx in ((args.model, 1 if m != 1 else 16), ("llama2-7b" if args.model != "llama2-7b"
-                                                                else "llama2-70b", 16)):
+                                                                else "llama2-70b", 16), (args.model, 512)):
             lx = LAYERS_7B if model == "llama2-7b" else LAYERS_70B
-            rx = run_ours(args, world, rank, lx, mx, e2e=False, burn_in=0.5)
-            tx = rx["t"] / args.steps
+            import argparse as _ap
+            ax_args = _ap.Namespace(**dict(vars(args), steps=args.steps if mx <= 16 else max(20, args.steps // 20)))
+            rx = run_ours(ax_args, world, rank, lx, mx, e2e=False, burn_in=0.5)
+            tx = rx["t"] / ax_args.steps
             ax = step_bytes(lx, mx) / world / tx / 1e9
-            extras.append({"workload": f"{model} decoder-block linears decode M={mx}", "value": round(
-                step_bytes(lx, mx) * args.steps / rx["t"] / 1e9, 2), "unit": "GB/s",
-                "ms_per_step": round(tx * 1e3, 5), "roofline_frac": round(ax / peaks["hbm_gbs"], 4),
-                "speedup_vs_cublas_fp16": round(rx["cublas"]["ms_per_step"] / (tx * 1e3), 3),
-                "clocks": rx["clocks"], "per_launch_serialised": rx["per_layer"]})
+            ent = {"workload": f"{model} decoder-block linears {'decode' if mx <= 16 else 'prefill'} M={mx}",
+                   "value": round(step_bytes(lx, mx) * ax_args.steps / rx["t"] / 1e9, 2), "unit": "GB/s",
+                   "steps": ax_args.steps, "ms_per_step": round(tx * 1e3, 5),
+                   "roofline_frac": round(ax / peaks["hbm_gbs"], 4),
+                   "tflops": round(step_flops(lx, mx) / world / tx / 1e12, 2),
+                   "speedup_vs_cublas_fp16": round(rx["cublas"]["ms_per_step"] / (tx * 1e3), 3),
+                   "cublas_fp16_tflops": rx["cublas"]["TFLOPS"],
+                   "clocks": rx["clocks"], "per_launch_serialised": rx["per_layer"]}
+            if mx > 16:   # prefill: tensor-pipe bound, roofline against the measured dense bf16 peak
+                ent["roofline"] = {"bound": "tensor", "achieved": ent["tflops"],
+                                   "peak": peaks["bf16_tflops_sustained"], "unit": "TFLOP/s",
+                                   "frac": round(ent["tflops"] / peaks["bf16_tflops_sustained"], 4),
+                                   "peak_source": peaks["source"] + " (sustained)"}
+            extras.append(ent)
     if rank != 0:
         return
     line = {

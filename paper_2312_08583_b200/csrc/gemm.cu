@@ -1817,7 +1817,9 @@ double prefill_2sm_choose(int64_t M, int64_t N, int64_t K, int* bn_out);  // pre
 // per-SM cycle estimates, pair kernel ~1024 cycles per 128-k step of a
 // 256 x 256 unit at ~90 % tensor-pipe efficiency, whole units per pair;
 // single-SM kernel: the BN-192 / 128 step cost over 148 SMs at the measured
-// ~68 % efficiency (profiles/r02_ncu_prefill_m2048.json).
+// ~60 % efficiency (68 % tensor-pipe activity at M = 2048, less with the
+// stream-K fixups at M = 512; profiles/r02_ncu_prefill_m2048.json,
+// r02_abx_pair_vs_single.jsonl).
 #ifndef LPQT_PAIR_MIN_M
 #define LPQT_PAIR_MIN_M 129  // (below: decode / small prefill stay single-SM)
 #endif
@@ -1828,10 +1830,10 @@ static bool use_pair_kernel(int64_t M, int64_t N, int64_t K, int flags) {
   if (flags & LPQT_SCHED_PAIR) return true;
   if (flags & (LPQT_SCHED_STREAMK | LPQT_SCHED_CLUSTER) || M < LPQT_PAIR_MIN_M) return false;
   const int64_t k_tiles = (K + kTileK - 1) / kTileK;
-  const double t2 = prefill_2sm_choose(M, N, K, nullptr) / 0.8;
+  const double t2 = prefill_2sm_choose(M, N, K, nullptr) / 0.9;
   const int bn = pick_bn(M);
   const int64_t tiles = n_tiles * ((M + bn - 1) / bn);
-  const double step = bn >= 192 ? 768.0 / 0.68 : 600.0;
+  const double step = bn >= 192 ? 768.0 / 0.6 : 600.0;
   const double t1 = (double)tiles * k_tiles * step / num_sms();
   return t2 < t1;
 }
