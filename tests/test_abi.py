@@ -73,7 +73,7 @@ def test_host_errors_without_launch(lib):
     assert st == _lib.E_SHAPE          # ldx % 8 != 0
     st = lib.lpqt_w6a16_linear_ex(None, None, None, 8, 1, 128, 8, None, 9, _lib.Y_NM, 1, 0, None, 0, 0, None)
     assert st == _lib.E_UNSUPPORTED    # bad y dtype
-    st = lib.lpqt_w6a16_linear_ex(None, None, None, 8, 1, 128, 8, None, _lib.F32, _lib.Y_NM, 1, 0, None, 0, 8, None)
+    st = lib.lpqt_w6a16_linear_ex(None, None, None, 8, 1, 128, 8, None, _lib.F32, _lib.Y_NM, 1, 0, None, 0, 64, None)
     assert st == _lib.E_INVALID_INPUT  # unknown flag
     assert lib.lpqt_w6a16_linear(None, None, None, 8, 0, 128, 8, None, _lib.F32, _lib.Y_NM, 1, 0, None, 0,
                                  None) == _lib.OK  # M == 0: nothing to do
