@@ -32,6 +32,7 @@
 
 #include <algorithm>
 #include <mutex>
+#include <type_traits>
 
 #include "common.cuh"
 
@@ -63,7 +64,7 @@ struct Args {
   int64_t ldy;
   int M, N, k_tiles, n_tiles, m_tiles, units, n_fastest, y_dtype, y_layout;
   int bn;     // batch columns per unit (MMA N; each CTA loads bn / 2 X rows)
-  int y_tma;  // Y[M, N] 16-bit: the epilogue stages 32-column chunks and TMA-stores them
+  int y_tma;  // 0: element stores; 1: Y[M, N] / 2: Y[N, M] staged in 8-KB chunks, TMA-stored
   ShiftMuls sm;
 };
 
@@ -314,7 +315,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else {
     // ------------------------------------------------ epilogue (own 128 rows x bn columns)
-    setmaxnreg_dec<72>();
+    // (registers: 4 x 128 x 88 dequant + 128 x 48 producers / MMA + 128 x 104 = 64512)
+    setmaxnreg_inc<104>();
     const int lg = warp & 3;
     const int rr = lg * 32 + lane;
     const uint32_t t_d = tmem_base + kDCol0 + (static_cast<uint32_t>(lg * 32) << 16);
@@ -329,43 +331,84 @@ __global__ void __launch_bounds__(kThreads, 1)
       const float fs = n < a.N ? __half2float(__ushort_as_half(__ldg(a.scales + n))) : 0.f;
       mbar_wait<2>(dfull, ul & 1);
       tc_fence_after();
-#pragma unroll 1
-      for (int c0 = 0; c0 < a.bn; c0 += kYChunk) {
-        uint32_t v[kYChunk];
+      // one chunk of CW batch columns (8 KB staged: CW = 32 for 16-bit Y, 16 for f32)
+      auto chunk = [&](auto cw_tag, int c0) {
+        constexpr int CW = decltype(cw_tag)::value;
+        uint32_t v[CW];
         tmem_ld_x16(t_d + c0, *reinterpret_cast<uint32_t(*)[16]>(v));
-        tmem_ld_x16(t_d + c0 + 16, *reinterpret_cast<uint32_t(*)[16]>(v + 16));
+        if constexpr (CW == 32) tmem_ld_x16(t_d + c0 + 16, *reinterpret_cast<uint32_t(*)[16]>(v + 16));
         tmem_wait_ld();
-        if (c0 + kYChunk >= a.bn) {  // last chunk read: D may be overwritten
+        if (c0 + CW >= a.bn) {  // last chunk read: D may be overwritten
           tc_fence_before();
           __syncwarp();
           if (lane == 0) arrive_cluster(dm_leader);
         }
         const int m0 = mt * a.bn + c0;
-        if (a.y_tma) {
-          // [32 m][128 n] 16-bit tile in smem -> one TMA tensor store (clips m >= M, n >= N)
-          const uint32_t buf = smem_u32(smem_y) + (nchunk & 1) * kYBuf;
-          if (nchunk >= 2) {
-            if (lead_thread) bulk_wait_read<1>();  // this buffer's previous store has read it
-            named_bar_sync(1, 4 * 32);
-          }
+        if (!a.y_tma) {
 #pragma unroll
-          for (int j = 0; j < kYChunk; ++j) {
-            const float f = __uint_as_float(v[j]) * fs;
-            const uint16_t h = a.y_dtype == LPQT_F16 ? __half_as_ushort(__float2half_rn(f))
-                                                     : __bfloat16_as_ushort(__float2bfloat16_rn(f));
-            asm volatile("st.shared.u16 [%0], %1;" ::"r"(buf + (j * kTileN + rr) * 2), "h"(h) : "memory");
-          }
-          fence_proxy_async_smem();
+          for (int j = 0; j < CW; ++j) store_y(a, n, m0 + j, __uint_as_float(v[j]) * fs);
+          return;
+        }
+        // staged chunk -> one TMA tensor store (clips m >= M, n >= N).  Y[M, N]: smem
+        // [CW m][128 n] (thread rr writes column rr); Y[N, M]: smem [128 n][CW m]
+        // (thread rr writes its 64-byte row with four 16-byte stores)
+        const uint32_t buf = smem_u32(smem_y) + (nchunk & 1) * kYBuf;
+        if (nchunk >= 2) {
+          if (lead_thread) bulk_wait_read<1>();  // this buffer's previous store has read it
           named_bar_sync(1, 4 * 32);
-          if (lead_thread) {
-            tma_store_2d(&tmap_y, buf, n0, m0);
-            bulk_commit();
+        }
+        uint32_t h[16];  // the chunk's 64 bytes of this row, packed
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          if constexpr (CW == 16) {
+            h[j] = __float_as_uint(__uint_as_float(v[j]) * fs);
+          } else {
+            const float f0 = __uint_as_float(v[2 * j]) * fs, f1 = __uint_as_float(v[2 * j + 1]) * fs;
+            if (a.y_dtype == LPQT_F16) {
+              const __half2 t = __floats2half2_rn(f0, f1);
+              h[j] = *reinterpret_cast<const uint32_t*>(&t);
+            } else {
+              const __nv_bfloat162 t = __floats2bfloat162_rn(f0, f1);
+              h[j] = *reinterpret_cast<const uint32_t*>(&t);
+            }
           }
-          ++nchunk;
+        }
+        if (a.y_tma == 1) {
+#pragma unroll
+          for (int j = 0; j < CW; ++j) {
+            if constexpr (CW == 16) {
+              asm volatile("st.shared.b32 [%0], %1;" ::"r"(buf + (j * kTileN + rr) * 4), "r"(h[j]) : "memory");
+            } else {
+              asm volatile("st.shared.u16 [%0], %1;" ::"r"(buf + (j * kTileN + rr) * 2),
+                           "h"(static_cast<uint16_t>(h[j >> 1] >> (16 * (j & 1))))
+                           : "memory");
+            }
+          }
         } else {
 #pragma unroll
-          for (int j = 0; j < kYChunk; ++j) store_y(a, n, m0 + j, __uint_as_float(v[j]) * fs);
+          for (int j = 0; j < 16; j += 4)
+            asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(buf + rr * 64 + j * 4), "r"(h[j]),
+                         "r"(h[j + 1]), "r"(h[j + 2]), "r"(h[j + 3])
+                         : "memory");
         }
+        fence_proxy_async_smem();
+        named_bar_sync(1, 4 * 32);
+        if (lead_thread) {
+          if (a.y_tma == 1) {
+            tma_store_2d(&tmap_y, buf, n0, m0);
+          } else {
+            tma_store_2d(&tmap_y, buf, m0, n0);
+          }
+          bulk_commit();
+        }
+        ++nchunk;
+      };
+      if (a.y_dtype == LPQT_F32) {
+#pragma unroll 1
+        for (int c0 = 0; c0 < a.bn; c0 += 16) chunk(std::integral_constant<int, 16>{}, c0);
+      } else {
+#pragma unroll 1
+        for (int c0 = 0; c0 < a.bn; c0 += 32) chunk(std::integral_constant<int, 32>{}, c0);
       }
     }
     if (lead_thread) bulk_wait_read<0>();  // staging smem stays valid until the stores read it
@@ -474,19 +517,24 @@ int launch_prefill_2sm(const uint8_t* tiles, const uint16_t* scales, const uint1
           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
     return LPQT_E_INVALID_INPUT;
-  // Y[M, N] with 16-bit elements, 16-B aligned base and row stride: the TMA store epilogue
+  // Y with a 16-B aligned base and row stride: the TMA-store epilogue (8-KB chunks:
+  // 32 batch columns of 16-bit Y or 16 of f32), Y[M, N] or Y[N, M]
   CUtensorMap ymap;
   memset(&ymap, 0, sizeof(ymap));
   int y_tma = 0;
-  if (y_layout == LPQT_Y_MN && y_dtype != LPQT_F32 && reinterpret_cast<uintptr_t>(Y) % 16 == 0 &&
-      (ldy * 2) % 16 == 0) {
-    const cuuint64_t ydims[2] = {static_cast<cuuint64_t>(N), static_cast<cuuint64_t>(M)};
-    const cuuint64_t ystr[1] = {static_cast<cuuint64_t>(ldy) * 2};
-    const cuuint32_t ybox[2] = {static_cast<cuuint32_t>(kTileN), static_cast<cuuint32_t>(p2::kYChunk)};
-    if (enc(&ymap, y_dtype == LPQT_F16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, Y,
-            ydims, ystr, ybox, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+  const int es = y_dtype == LPQT_F32 ? 4 : 2;
+  const cuuint32_t cw = static_cast<cuuint32_t>(p2::kYBuf / (kTileN * es));
+  if (reinterpret_cast<uintptr_t>(Y) % 16 == 0 && (ldy * es) % 16 == 0) {
+    const bool mn = y_layout == LPQT_Y_MN;
+    const cuuint64_t ydims[2] = {static_cast<cuuint64_t>(mn ? N : M), static_cast<cuuint64_t>(mn ? M : N)};
+    const cuuint64_t ystr[1] = {static_cast<cuuint64_t>(ldy) * es};
+    const cuuint32_t ybox[2] = {mn ? static_cast<cuuint32_t>(kTileN) : cw, mn ? cw : static_cast<cuuint32_t>(kTileN)};
+    const CUtensorMapDataType dt = y_dtype == LPQT_F32   ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32
+                                   : y_dtype == LPQT_F16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16
+                                                         : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
+    if (enc(&ymap, dt, 2, Y, ydims, ystr, ybox, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
             CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS)
-      y_tma = 1;
+      y_tma = mn ? 1 : 2;
   }
   p2::Args a{};
   a.tiles = tiles;

@@ -52,6 +52,23 @@ def test_pair_kernel_layouts_and_dtypes(dt):
     assert _rel(Y, y_ref.t()) <= 1e-5
 
 
+@pytest.mark.parametrize("dt", [torch.float16, torch.float32])
+@pytest.mark.parametrize("m", [512, 777])
+def test_pair_kernel_reference_layout(dt, m):
+    """Y[N, M] (the reference layout, gemm_nm): the TMA-store epilogue when the
+    row stride allows it (m = 512), element stores otherwise (m = 777)."""
+    from paper_2312_08583_b200.linear import gemm_nm, _launch
+    from paper_2312_08583_b200 import _lib
+    n, k = 2048, 4096
+    W = (torch.randn(n, k, device="cuda") * 0.02).half()
+    x = torch.randn(m, k, device="cuda").half()
+    w = L.Fp6Weight.quantize(W)
+    ref = L.w6a16_linear(x, w, out_dtype=torch.float32, sched="single").t()
+    y = torch.empty(n, m, dtype=dt, device="cuda")
+    _launch(w, x, k, m, y, _lib.F32 if dt == torch.float32 else _lib.F16, _lib.Y_NM, m, 0, "pair")
+    assert _rel(y.float(), ref) <= (1e-5 if dt == torch.float32 else 1e-2)
+
+
 def test_odd_tile_count_falls_back():
     n, k, m = 1100, 1024, 600          # 9 row tiles: no pairs
     W = (torch.randn(n, k, device="cuda") * 0.02).half()

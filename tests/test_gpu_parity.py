@@ -449,12 +449,15 @@ def test_prefill_round_robin_tiles_match_stream_k():
     the fp32 summation tolerance, and within REL_TOL of the f64 reference."""
     g = torch.Generator(device="cuda").manual_seed(23)
     n, k, m = 4096, 8192, 2600
-    assert L.plan(m, n, k)["schedule"] == "roundrobin"
+    assert L.plan(m, n, k, sched="single")["schedule"] == "roundrobin"   # (auto: the CTA-pair kernel)
     w = L.Fp6Weight.quantize((torch.randn(n, k, generator=g, device="cuda") * 0.02).half())
     x = torch.randn(m, k, generator=g, device="cuda").half()
-    y = L.w6a16_linear(x, w, out_dtype=torch.float32)
+    y = L.w6a16_linear(x, w, out_dtype=torch.float32, sched="single")
     y_sk = L.w6a16_linear(x, w, out_dtype=torch.float32, sched="streamk")
     assert normwise_rel(y.cpu().numpy(), y_sk.cpu().numpy()) <= 1e-5
+    y_pair = L.w6a16_linear(x, w, out_dtype=torch.float32)
+    assert L.plan(m, n, k)["schedule"] == "pair"
+    assert normwise_rel(y_pair.cpu().numpy(), y_sk.cpu().numpy()) <= 1e-5
     ref = (x.double() @ w.dequantize_f16().double().t())
     assert normwise_rel(y.cpu().numpy(), ref.cpu().numpy()) <= REL_TOL
 
