@@ -315,8 +315,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else {
     // ------------------------------------------------ epilogue (own 128 rows x bn columns)
-    // (registers: 4 x 128 x 88 dequant + 128 x 48 producers / MMA + 128 x 104 = 64512)
-    setmaxnreg_inc<104>();
+    // (keeps the launch's 80 registers: setmaxnreg moves registers only inside the
+    // CTA's allocation, 768 x 80, and the producers' 4 x 32 x 32 released by the
+    // decrement above are exactly what the dequant warps' increment to 88 takes —
+    // an increment here would wait forever)
     const int lg = warp & 3;
     const int rr = lg * 32 + lane;
     const uint32_t t_d = tmem_base + kDCol0 + (static_cast<uint32_t>(lg * 32) << 16);
