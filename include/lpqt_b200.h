@@ -59,7 +59,7 @@ extern "C" {
 #define LPQT_Y_MN  1   /* Y[m, n] (torch.nn.Linear layout)                     */
 
 const char* lpqt_strerror(int status);
-int lpqt_abi_version(void);               /* bumps on any signature change (4: FGQ stage params) */
+int lpqt_abi_version(void);               /* bumps on any signature change (5: reference-order kernels, pair-kernel flags, FGQ row factors) */
 
 /* codec.py:116-132 encode_rtn_array: x[n] (dtype) -> codes[n] (u8). */
 int lpqt_fp6_encode_rtn(const void* x, int dtype, int64_t n, uint8_t* codes,
@@ -331,7 +331,10 @@ int lpqt_int4_dequantize_blocks(const uint8_t* nibbles, const uint16_t* scales,
  * << 16, u32) of the block holding kt.  Built once per weight from the
  * row-major per-block arrays (block <= 0 or >= K: one per row, else a
  * multiple of 128); the GEMM's weight producer copies them next to the
- * weight bytes of each stage.  lpqt_fgq_stage_bytes(N, K, with_zeros) bytes. */
+ * weight bytes of each stage.  Without zeros (FP6 / FP5) each row's scales
+ * are normalised by a power of two 2^e_r (max in [2^10, 2^11)) and the f32
+ * row factors 2^e_r follow the stage-ordered scales (the GEMM applies them in
+ * fp32).  lpqt_fgq_stage_bytes(N, K, with_zeros) bytes. */
 int64_t lpqt_fgq_stage_bytes(int64_t N, int64_t K, int with_zeros);
 int lpqt_fgq_stage_params(const uint16_t* scales, const uint16_t* zeros,
                           int64_t N, int64_t K, int64_t block, void* out,
