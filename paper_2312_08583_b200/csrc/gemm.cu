@@ -1722,6 +1722,13 @@ static Plan make_plan(int64_t M, int64_t N, int64_t K, int split_k, int flags, i
       // measured slower than the model predicts).
       const double tile_us = 0.31;
       const double sk_kt = (double)p.tiles * p.k_tiles / sms;  // k-tiles per CTA
+      // Round 2 (stream-K with the static reducer, no atomic round trip on the
+      // tail): stream-K wins once every CTA streams >= 16 k-tiles — 70B O
+      // 8192 x 8192 −6 %, 7B QKV −5 % against the cluster plan, equal on the
+      // rest (profiles/r02_abx_decode_schedules.jsonl); below that (7B O,
+      // 4096 x 4096: 7 k-tiles per CTA) the fixups dominate and the model
+      // below still picks cluster split-K.
+      if (sk_kt >= 16.0) goto done_csk;
       const bool sk_partial = ((int64_t)p.tiles * p.k_tiles) % sms != 0 || p.tiles % sms != 0;
       // (a range spanning whole tiles splits each tile between two CTAs,
       // whose fixup takes the last-arriver fast path; long ranges hide part
@@ -1739,6 +1746,7 @@ static Plan make_plan(int64_t M, int64_t N, int64_t K, int split_k, int flags, i
       }
     }
   }
+done_csk:
   if (best_c > 0) {
     p.csk = true;
     p.cluster = best_c;
