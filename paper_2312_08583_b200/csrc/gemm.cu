@@ -94,6 +94,7 @@ struct GemmArgs {
   int n_fastest;      // tile index order: 0 = batch tile fastest, 1 = weight-row tile fastest
   int y_tma;          // Y tiles leave through the TMA tensor store (tmap_y valid)
   int dp;             // prefill (BN >= 64): whole tiles round-robin, CTA c takes c, c + grid, ...
+  int ramp;           // SK: LPQT_SK_RAMP of this launch (0: equal ranges)
   ShiftMuls sm;       // 2^26, 2^28, 2^30: right shifts on the FMA pipe (common.cuh)
 };
 
@@ -159,7 +160,7 @@ __device__ __forceinline__ void scale_f16x2(uint32_t (&r)[32], uint32_t s2) {
 struct L2Prefetch {
   const uint8_t* base;
   int64_t total, bytes;
-  int count, ksteps, kstep, k_tiles, c, tiles;
+  int count, ksteps, kstep, k_tiles, c, tiles, ramp;
   uint32_t chunk;
 };
 
@@ -289,12 +290,30 @@ struct Seg {
 };
 
 // ---- stream-K ------------------------------------------------------------------
+// LPQT_SK_RAMP (percent, decode BN <= 32): CTA ranges shrink linearly with
+// blockIdx — CTAs are dispatched in blockIdx order, so in a PDL chain the low
+// ones land on the SMs the previous kernel frees first.  Range start of CTA c:
+// total * x (1 + r (1 - x)), x = c / grid (density 1 + r (1 - 2x)).
+#ifndef LPQT_SK_RAMP
+#define LPQT_SK_RAMP 0
+#endif
+__host__ __device__ __forceinline__ int64_t sk_begin_n(int64_t total, int c, int g, int ramp) {
+  if (ramp == 0) return (int64_t)c * total / g;
+  return total * c * (100 * (int64_t)g + ramp * (int64_t)(g - c)) / (100 * (int64_t)g * g);
+}
+__device__ __forceinline__ int sk_ramp(const GemmArgs& a) { return a.dp ? 0 : a.ramp; }
 __device__ __forceinline__ int64_t sk_begin(const GemmArgs& a, int c) {
-  return (int64_t)c * a.total / (int64_t)gridDim.x;
+  return sk_begin_n(a.total, c, static_cast<int>(gridDim.x), sk_ramp(a));
 }
 // CTA whose range holds global k-step position p
 __device__ __forceinline__ int sk_cta_of(const GemmArgs& a, int64_t p) {
-  return static_cast<int>(((p + 1) * (int64_t)gridDim.x - 1) / a.total);
+  if (sk_ramp(a) == 0) return static_cast<int>(((p + 1) * (int64_t)gridDim.x - 1) / a.total);
+  int lo = 0, hi = static_cast<int>(gridDim.x) - 1;  // largest c with begin(c) <= p
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (sk_begin(a, mid) <= p) lo = mid; else hi = mid - 1;
+  }
+  return lo;
 }
 
 // A CTA's stream-K range [beg, end) in natural order; segments never
@@ -699,6 +718,29 @@ __global__ void __launch_bounds__(kThreads, 1)
   // weight tiles at once (weights never depend on the preceding kernel, see
   // LPQT_LAUNCH_PDL); the other warps meet on named barrier 2 (the producer
   // only arrives), so the TMEM allocation overlaps the first weight loads.
+  // W producer: one stage of weight tiles (+ FGQ block parameters) into ring slot i % kWStages
+  const uint64_t w_pol = (a.m_tiles > 1 && !a.n_fastest) ? l2_evict_last_policy() : l2_evict_first_policy();
+  auto issue_w = [&](int i, const StageIter<Sched, KS>& it) {
+    const int kt = it.kt(), nt = it.nt();
+    int n_tile, m_tile;
+    tile_nm(a, it.sg.tile, n_tile, m_tile);
+    const int s = i % C::kWStages;
+    const uint8_t* src = a.tiles + ((int64_t)n_tile * a.k_tiles + kt) * C::kTileB;
+    const uint32_t bytes = static_cast<uint32_t>(nt * C::kTileB);
+    const uint32_t e = elect_one();
+    mbar_arrive_expect_tx_if(e, &full_w[s], bytes + static_cast<uint32_t>(nt * C::kSBytes));
+    bulk_g2s_if(e, smem_w + s * C::kWStageBytes, src, bytes, &full_w[s], w_pol);
+    if constexpr (FGQ) {
+      const uint8_t* sp = fg.stage + ((int64_t)n_tile * a.k_tiles + kt) * C::kSBytes;
+      bulk_g2s_if(e, smem_w + s * C::kWStageBytes + KS * C::kTileB, sp, static_cast<uint32_t>(nt * C::kSBytes),
+                  &full_w[s], w_pol);
+    }
+  };
+  // the first ring's worth of W stages goes out during setup (LPQT_W_PROLOGUE)
+#ifndef LPQT_W_PROLOGUE
+#define LPQT_W_PROLOGUE 0  // measured slower (5-12 %, profiles/r02_abx_w_prologue.jsonl)
+#endif
+  const int w_pro = LPQT_W_PROLOGUE ? min(C::kWStages, n_st) : 0;
   if (warp == kWarpTmaW) {
     if (lane == 0) {
       for (int s = 0; s < C::kWStages; ++s) {
@@ -734,6 +776,15 @@ __global__ void __launch_bounds__(kThreads, 1)
       CTA_STAMP(19);
     }
     __syncwarp();
+    // weights never depend on the preceding kernel: stream the first stages
+    // now, straight after the barrier init (the rest of the setup — TMEM
+    // allocation, register split, named barrier — overlaps their flight)
+    if (w_pro > 0) {
+      StageIter<Sched, KS> it;
+      it.start(a, sc, 0);
+      for (int i = 0; i < w_pro; ++i, it.next(a, sc)) issue_w(i, it);
+      if (lane == 0) CTA_STAMP(20);
+    }
     named_bar_arrive(2, kThreads);
   } else {
     if (warp == kWarpMma0) {
@@ -773,28 +824,20 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (!is_w && lane == 0) CTA_STAMP(13);
     // decode streams every weight byte once (evict-first); with several
     // batch tiles (prefill) the same weight tile is re-read per batch tile
-    const uint64_t pol = (a.m_tiles > 1 && !a.n_fastest) ? l2_evict_last_policy() : l2_evict_first_policy();
+    // (w_pol).  The W producer resumes after its setup prologue.
     StageIter<Sched, KS> it;
-    it.start(a, sc, 0);
-    for (int i = 0; i < n_st; ++i, it.next(a, sc)) {
-      const int kt = it.kt(), nt = it.nt();
-      int n_tile, m_tile;
-      tile_nm(a, it.sg.tile, n_tile, m_tile);
+    const int i0 = is_w ? w_pro : 0;
+    it.start(a, sc, i0);
+    for (int i = i0; i < n_st; ++i, it.next(a, sc)) {
       if (is_w) {
         const int s = i % C::kWStages;
         mbar_wait<WM>(&empty_w[s], ((i / C::kWStages) & 1) ^ 1);
-        const uint8_t* src = a.tiles + ((int64_t)n_tile * a.k_tiles + kt) * C::kTileB;
-        const uint32_t bytes = static_cast<uint32_t>(nt * C::kTileB);
-        const uint32_t e = elect_one();
-        mbar_arrive_expect_tx_if(e, &full_w[s], bytes + static_cast<uint32_t>(nt * C::kSBytes));
-        bulk_g2s_if(e, smem_w + s * C::kWStageBytes, src, bytes, &full_w[s], pol);
-        if constexpr (FGQ) {
-          const uint8_t* sp = fg.stage + ((int64_t)n_tile * a.k_tiles + kt) * C::kSBytes;
-          bulk_g2s_if(e, smem_w + s * C::kWStageBytes + KS * C::kTileB, sp, static_cast<uint32_t>(nt * C::kSBytes),
-                      &full_w[s], pol);
-        }
+        issue_w(i, it);
         if (i == 0 && lane == 0) CTA_STAMP(20);
       } else {
+        const int kt = it.kt(), nt = it.nt();
+        int n_tile, m_tile;
+        tile_nm(a, it.sg.tile, n_tile, m_tile);
         const int s = i % C::kXStages;
         mbar_wait<WM>(&empty_x[s], ((i / C::kXStages) & 1) ^ 1);
         uint8_t* xs = smem_x + s * C::kXStageBytes;
@@ -816,7 +859,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int c = blockIdx.x; c < pf.count; c += gridDim.x) {
           int64_t kt_lin;  // tile-linear k-tile index = byte offset / kTileBytes
           if (pf.total > 0) {
-            const int64_t q = (int64_t)c * pf.total / pf.count;
+            const int64_t q = sk_begin_n(pf.total, c, pf.count, pf.ramp);
             const int64_t t = q / pf.ksteps;
             kt_lin = t * pf.k_tiles + (q - t * pf.ksteps) * pf.kstep;
           } else {
@@ -1612,6 +1655,7 @@ struct Plan {
   bool dp;      // prefill: whole tiles round-robin (SkSched DP mode)
   int cluster;  // CSK cluster size
   int splits;   // max CTAs contributing to one tile
+  int ramp;     // SK range ramp (percent, LPQT_SK_RAMP; decode stream-K only)
   int64_t K;    // X's k extent: TMA zero-fills columns K .. ldx (W4A16 pads with Z, not 0)
 };
 
@@ -1793,7 +1837,8 @@ done_csk:
   if (g < 1) g = 1;
   p.grid = static_cast<int>(g);
   // partial tiles exist unless every CTA range is a whole number of tiles
-  p.partials = !(p.total % g == 0 && (p.total / g) % p.ksteps == 0);
+  p.ramp = (p.bn <= 32 && split_k == 0) ? LPQT_SK_RAMP : 0;
+  p.partials = p.ramp > 0 || !(p.total % g == 0 && (p.total / g) % p.ksteps == 0);
   if (p.partials) {
     p.counters_bytes = kMaxCounters * 4;  // fixed region, zeroed once, self-resetting
     p.ws_bytes = p.counters_bytes + (int64_t)p.grid * 2 * kTileN * p.bn * 4;
@@ -1804,6 +1849,7 @@ done_csk:
       p.tiles < ((int64_t)1 << 30) && split_k == 0 && !(flags & LPQT_SCHED_STREAMK)) {
     p.dp = true;
     p.grid = sms;
+    p.ramp = 0;
     p.partials = false;
     p.counters_bytes = 0;
     p.ws_bytes = 0;
@@ -1817,9 +1863,11 @@ done_csk:
 
 int launch_prefill_2sm(const uint8_t* tiles, const uint16_t* scales, const uint16_t* Xt, int64_t ldx, int64_t M,
                        int64_t N, int64_t K, void* Y, int y_dtype, int y_layout, int64_t ldy, int flags,
-                       cudaStream_t stream, int* grid_out);  // prefill2sm.cu
+                       int force, void* workspace, int64_t workspace_bytes, cudaStream_t stream,
+                       int* grid_out);                         // prefill2sm.cu
 int prefill_2sm_pairs();                                       // prefill2sm.cu
-double prefill_2sm_choose(int64_t M, int64_t N, int64_t K, int* bn_out);  // prefill2sm.cu
+double prefill_2sm_choose(int64_t M, int64_t N, int64_t K, int* bn_out, int* sk_out, int force);  // prefill2sm.cu
+int64_t prefill_2sm_workspace();                                                              // prefill2sm.cu
 
 // The CTA-pair prefill kernel (prefill2sm.cu) vs this file's single-SM one:
 // per-SM cycle estimates, pair kernel ~1024 cycles per 128-k step of a
@@ -1831,6 +1879,13 @@ double prefill_2sm_choose(int64_t M, int64_t N, int64_t K, int* bn_out);  // pre
 #ifndef LPQT_PAIR_MIN_M
 #define LPQT_PAIR_MIN_M 129  // (below: decode / small prefill stay single-SM)
 #endif
+// The pair kernel's schedule choice: split_k 0 = automatic; with
+// LPQT_SCHED_PAIR, split_k 1 / 2 force whole units / whole rounds + a
+// stream-K wave (testing / tuning hooks).  -1: split_k asks for the single-SM kernel.
+static int pair_force(int split_k, int flags) {
+  if (split_k == 0) return 0;
+  return (flags & LPQT_SCHED_PAIR) && split_k <= 2 ? split_k : -1;
+}
 static bool use_pair_kernel(int64_t M, int64_t N, int64_t K, int flags) {
   if (flags & LPQT_SCHED_SINGLE) return false;
   const int64_t n_tiles = (N + kTileN - 1) / kTileN;
@@ -1838,7 +1893,7 @@ static bool use_pair_kernel(int64_t M, int64_t N, int64_t K, int flags) {
   if (flags & LPQT_SCHED_PAIR) return true;
   if (flags & (LPQT_SCHED_STREAMK | LPQT_SCHED_CLUSTER) || M < LPQT_PAIR_MIN_M) return false;
   const int64_t k_tiles = (K + kTileK - 1) / kTileK;
-  const double t2 = prefill_2sm_choose(M, N, K, nullptr) / 0.9;
+  const double t2 = prefill_2sm_choose(M, N, K, nullptr, nullptr, 0) / 0.9;
   const int bn = pick_bn(M);
   const int64_t tiles = n_tiles * ((M + bn - 1) / bn);
   const double step = bn >= 192 ? 768.0 / 0.6 : 600.0;
@@ -2027,17 +2082,21 @@ int64_t lpqt_w6a16_workspace_bytes(int64_t M, int64_t N, int64_t K, int split_k)
   // the largest any schedule of this shape may need (auto or forced stream-K)
   const Plan p0 = make_plan(M, N, K, split_k, 0, num_sms());
   const Plan p1 = make_plan(M, N, K, split_k, LPQT_SCHED_STREAMK, num_sms());
-  return p0.ws_bytes > p1.ws_bytes ? p0.ws_bytes : p1.ws_bytes;
+  // (the pair kernel's stream-K schedule: whenever the pair kernel may run)
+  const int64_t wp = split_k <= 2 && (N + kTileN - 1) / kTileN % 2 == 0 && M >= 17 ? prefill_2sm_workspace() : 0;
+  return std::max(wp, p0.ws_bytes > p1.ws_bytes ? p0.ws_bytes : p1.ws_bytes);
 }
 
 int lpqt_w6a16_plan_ex(int64_t M, int64_t N, int64_t K, int split_k, int flags, int* out, int n_out) {
   if (M <= 0 || N <= 0 || K <= 0) return LPQT_E_SHAPE;
   if ((flags & LPQT_SCHED_STREAMK) && (flags & LPQT_SCHED_CLUSTER)) return LPQT_E_INVALID_INPUT;
-  if (split_k == 0 && use_pair_kernel(M, N, K, flags)) {
-    int bn = 256;
-    prefill_2sm_choose(M, N, K, &bn);
+  if (pair_force(split_k, flags) >= 0 && use_pair_kernel(M, N, K, flags)) {
+    int bn = 256, sk = 0;
+    prefill_2sm_choose(M, N, K, &bn, &sk, pair_force(split_k, flags));
     const int64_t units = ((N + kTileN - 1) / kTileN / 2) * ((M + bn - 1) / bn);
-    const int v[6] = {bn, 1, 2 * (int)std::min<int64_t>(prefill_2sm_pairs(), units), 6, 3, 2};
+    // splits: pairs sharing one unit (stream-K cuts a unit between pairs)
+    const int v[6] = {bn, sk ? 2 : 1, 2 * (int)(sk ? prefill_2sm_pairs() : std::min<int64_t>(prefill_2sm_pairs(), units)),
+                      6, 3, 2};
     for (int i = 0; i < n_out && i < 6; ++i) out[i] = v[i];
     return LPQT_OK;
   }
@@ -2103,9 +2162,10 @@ static int w6a16_blocks_impl(const uint8_t* tiles, const uint16_t* scales, int64
   if (y_layout == LPQT_Y_NM ? ldy < M : ldy < N) return LPQT_E_SHAPE;
   if (split_k < 0) return LPQT_E_INVALID_INPUT;
   if (N > (int64_t)1 << 30 || M > (int64_t)1 << 30 || K > (int64_t)1 << 30) return LPQT_E_SHAPE;
-  if (!fgq && !po && split_k == 0 && use_pair_kernel(M, N, K, flags)) {
+  if (!fgq && !po && pair_force(split_k, flags) >= 0 && use_pair_kernel(M, N, K, flags)) {
     const int st = launch_prefill_2sm(tiles, scales, Xt, ldx, M, N, K, Y, y_dtype, y_layout, ldy, flags,
-                                      as_stream(stream), nullptr);
+                                      pair_force(split_k, flags), workspace, workspace_bytes, as_stream(stream),
+                                      nullptr);
     if (st != LPQT_E_UNSUPPORTED) return st;
   }
   Plan p = make_plan(M, N, K, split_k, flags, num_sms(), fgq);
@@ -2132,6 +2192,7 @@ static int w6a16_blocks_impl(const uint8_t* tiles, const uint16_t* scales, int64
   // X larger than ~1/3 of L2 (126 MB): keep each batch tile's X resident
   args.n_fastest = (p.m_tiles > 1 && M * K * 2 > (int64_t)40 << 20) ? 1 : 0;
   args.dp = p.dp ? 1 : 0;
+  args.ramp = p.ramp;
   args.y_dtype = y_dtype;
   args.y_layout = y_layout;
   args.sm = ShiftMuls{1u << 26, 1u << 28, 1u << 30};
@@ -2151,6 +2212,7 @@ static int w6a16_blocks_impl(const uint8_t* tiles, const uint16_t* scales, int64
       pfa.k_tiles = q.k_tiles;
       pfa.c = q.csk ? q.cluster : 1;
       pfa.tiles = static_cast<int>(q.tiles);
+      pfa.ramp = q.csk ? 0 : q.ramp;
       pfa.chunk = static_cast<uint32_t>(std::min<int64_t>(chunk, (int64_t)1 << 30) / 16 * 16);
     }
   }
@@ -2231,6 +2293,7 @@ int lpqt_w4a16_linear_blocks(const uint8_t* tiles, const uint32_t* params, int64
   args.tile_count = static_cast<int>(p.tiles);
   args.n_fastest = (p.m_tiles > 1 && M * K * 2 > (int64_t)40 << 20) ? 1 : 0;
   args.dp = p.dp ? 1 : 0;
+  args.ramp = p.ramp;
   args.y_dtype = y_dtype;
   args.y_layout = y_layout;
   args.sm = ShiftMuls{1u << 26, 1u << 28, 1u << 30};

@@ -14,8 +14,26 @@
 // stages + six weight stages fit in shared memory.
 //
 // Work unit: 2 weight-row tiles (one per CTA: rank r owns row tile 2p + r)
-// x 256 batch columns, the whole K (no split-K: prefill has units for every
-// pair).  Unit u -> (pair, batch tile); cluster c takes u = c, c + #clusters,...
+// x bn batch columns x the whole K.  Unit u -> (pair, batch tile), in groups
+// of a.group pairs with the pairs fastest inside a group, so the ~P units in
+// flight share a few X tiles and a few weight pairs in L2 (at M = 8192 the
+// pair-fastest order over all 224 gate_up pairs re-streamed every weight pair
+// once per batch tile).  Schedule over the P co-resident pairs:
+//  * whole units round-robin (cluster c takes u = c, c + P, ...) for the
+//    first a.dp_units units (whole rounds);
+//  * stream-K over the rest (a.sk == 1): the (unit, k-tile) space of the
+//    last P .. 2P - 1 units is cut into P equal contiguous ranges, so the last
+//    round's idle pairs are not wasted (70B QKV at M = 512: 80 units on 74
+//    pairs = 2 rounds of whole units, 1.08 rounds with the stream-K wave).  A
+//    unit cut between pairs is reduced by its head's pair (the first
+//    contributor in k order: the head is the END of that pair's range, so it
+//    is its last segment and every other share finishes no later); each other
+//    contributor's share is the first segment of its range: it publishes its
+//    fp32 partial (chunk-major 128 x bn per CTA) and counts in with one
+//    red.release (no reply awaited).  The reducer bulk-copies the partials
+//    into its (drained) X ring one at a time and sums in k order —
+//    deterministic.  Workspace: self-resetting per-(unit, rank) counters +
+//    one partial slot per pair.
 //
 // Roles per CTA (768 threads): warps 0-15 dequant (two groups of 8 on
 // alternate k steps, warp w: lane group w % 4, k-half (w / 4) % 2), warp 16
@@ -31,6 +49,7 @@
 #include <string.h>
 
 #include <algorithm>
+#include <cmath>
 #include <mutex>
 #include <type_traits>
 
@@ -54,8 +73,13 @@ constexpr int kTmemCols = 512;
 constexpr int kYChunk = 32;                   // epilogue: 32 batch columns per TMA store
 constexpr int kYBuf = kYChunk * kTileN * 2;   // 8 KB staging (16-bit Y), double-buffered
 constexpr int kSmemBytes = kXStages * kXStage + kWStages * kTileBytes + 2 * kYBuf +
-                           8 * (2 * kXStages + 2 * kWStages + 2 * kASlots + 2) + 16;
+                           8 * (2 * kXStages + 2 * kWStages + 2 * kASlots + 3) + 16;
 static_assert(kSmemBytes <= 227 * 1024, "shared memory");
+// stream-K: one partial slot per pair and CTA, 128 rows x kMaxBN fp32 (the
+// reducer stages one in its X ring)
+constexpr int kPartFloats = kTileN * kMaxBN;
+static_assert(kPartFloats * 4 <= kXStages * kXStage, "a partial must fit the X ring");
+constexpr int64_t kCounters = 65536;  // per (unit, rank); the region gemm.cu's stream-K uses too
 
 struct Args {
   const uint8_t* tiles;
@@ -65,8 +89,57 @@ struct Args {
   int M, N, k_tiles, n_tiles, m_tiles, units, n_fastest, y_dtype, y_layout;
   int bn;     // batch columns per unit (MMA N; each CTA loads bn / 2 X rows)
   int y_tma;  // 0: element stores; 1: Y[M, N] / 2: Y[N, M] staged in 8-KB chunks, TMA-stored
+  int group;  // pairs per rasterization group
+  int sk;     // stream-K wave over the units past dp_units
+  int dp_units;    // units run whole, round-robin (a multiple of the pair count when sk)
+  int64_t total;   // sk: (units - dp_units) * k_tiles
+  int* counters;   // sk: [units][2] k-tiles published (self-resetting)
+  float* partials; // sk: [pairs][2][kPartFloats], chunk-major float4 [bn / 4][128]
   ShiftMuls sm;
 };
+
+// A pair's walk over its work, step i -> unit u, k tile kt: whole units
+// c, c + P, ... for its first dp_n steps, then its stream-K range (from sk0)
+struct Walk {
+  int u, kt, i;
+  __device__ __forceinline__ void set(const Args& a, int cid, int ncl, int64_t sk0, int dp_n) {
+    if (i < dp_n) {
+      const int ul = i / a.k_tiles;
+      u = cid + ul * ncl;
+      kt = i - ul * a.k_tiles;
+    } else {
+      const int64_t q = sk0 + (i - dp_n);
+      const int64_t us = q / a.k_tiles;
+      u = a.dp_units + static_cast<int>(us);
+      kt = static_cast<int>(q - us * a.k_tiles);
+    }
+  }
+  __device__ __forceinline__ void start(const Args& a, int cid, int ncl, int64_t sk0, int dp_n) {
+    i = 0;
+    set(a, cid, ncl, sk0, dp_n);
+  }
+  __device__ __forceinline__ void adv(const Args& a, int cid, int ncl, int64_t sk0, int dp_n) {
+    if (++i == dp_n) {
+      set(a, cid, ncl, sk0, dp_n);  // into the stream-K range
+    } else if (++kt == a.k_tiles) {
+      kt = 0;
+      u += i < dp_n ? ncl : 1;
+    }
+  }
+};
+__device__ __forceinline__ int64_t sk_beg(const Args& a, int c, int ncl) { return (int64_t)c * a.total / ncl; }
+// pair whose stream-K range holds position q
+__device__ __forceinline__ int sk_pair_of(const Args& a, int64_t q, int ncl) {
+  return static_cast<int>(((q + 1) * (int64_t)ncl - 1) / a.total);
+}
+__device__ __forceinline__ void red_release_gpu(int* p, int v) {
+  asm volatile("red.release.gpu.global.add.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ int ld_acquire(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
 
 __device__ __forceinline__ uint32_t cta_rank() {
   uint32_t r;
@@ -138,8 +211,12 @@ __device__ __forceinline__ void commit_2sm(uint32_t pred, uint64_t* bar) {
 __device__ __forceinline__ void unit_nm(const Args& a, int u, int& pair, int& mt) {
   const int n_pairs = a.n_tiles / 2;
   if (a.n_fastest) {
-    mt = u / n_pairs;
-    pair = u - mt * n_pairs;
+    // groups of a.group pairs x all batch tiles, the group's pairs fastest
+    const int gsz = a.group * a.m_tiles;
+    const int g = u / gsz, r = u - g * gsz;
+    const int gp = min(a.group, n_pairs - g * a.group);  // (the last group may be narrower)
+    mt = r / gp;
+    pair = g * a.group + (r - mt * gp);
   } else {
     pair = u / a.m_tiles;
     mt = u - pair * a.m_tiles;
@@ -173,14 +250,22 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* aempty = afull + kASlots;
   uint64_t* dfull = aempty + kASlots;
   uint64_t* dempty = dfull + 1;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(dempty + 1);
+  uint64_t* fixb = dempty + 1;  // sk reducer: a partial landed in the X ring
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(fixb + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = cta_rank();
   const bool leader = rank == 0;
   const int cid = static_cast<int>(blockIdx.x) >> 1, ncl = static_cast<int>(gridDim.x) >> 1;
-  const int my_units = cid < a.units ? (a.units - 1 - cid) / ncl + 1 : 0;
-  const int n_st = my_units * a.k_tiles;
+  // whole units first (dp_n steps), then the stream-K range [beg, beg + n_st - dp_n)
+  const int my_units = cid < a.dp_units ? (a.dp_units - 1 - cid) / ncl + 1 : 0;
+  const int dp_n = my_units * a.k_tiles;
+  int64_t beg = 0;
+  int n_st = dp_n;
+  if (a.sk) {
+    beg = sk_beg(a, cid, ncl);
+    n_st += static_cast<int>(sk_beg(a, cid + 1, ncl) - beg);
+  }
 
   if (threadIdx.x == 0) {
     if (smem_u32(smem_raw) & 1023u) __trap();
@@ -198,6 +283,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     mbar_init(dfull, 1);
     mbar_init(dempty, 2 * 4);  // leader: both CTAs' epilogue warps
+    mbar_init(fixb, 1);
     fence_mbar_init();
   }
   if (warp == kWarpMma) {
@@ -218,25 +304,29 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (warp == kWarpW) {
       // ------------------------------------------------ W producer (own row tile)
       const uint64_t pol = l2_evict_last_policy();  // a weight tile is re-read once per batch tile
-      for (int i = 0; i < n_st; ++i) {
-        const int ul = i / a.k_tiles, kt = i - ul * a.k_tiles;
+      Walk w;
+      w.start(a, cid, ncl, beg, dp_n);
+      for (int i = 0; i < n_st; ++i, w.adv(a, cid, ncl, beg, dp_n)) {
         int pair, mt;
-        unit_nm(a, cid + ul * ncl, pair, mt);
+        unit_nm(a, w.u, pair, mt);
         const int s = i % kWStages;
         mbar_wait<2>(&empty_w[s], ((i / kWStages) & 1) ^ 1);
         const uint32_t e = elect_one();
         mbar_arrive_expect_tx_if(e, &full_w[s], kTileBytes);
         bulk_g2s_if(e, smem_w + s * kTileBytes,
-                    a.tiles + ((int64_t)(2 * pair + rank) * a.k_tiles + kt) * kTileBytes, kTileBytes, &full_w[s], pol);
+                    a.tiles + ((int64_t)(2 * pair + rank) * a.k_tiles + w.kt) * kTileBytes, kTileBytes, &full_w[s],
+                    pol);
       }
     } else if (warp == kWarpX) {
       // ------------------------------------------------ X producer (own half of the batch tile)
       pdl_wait();  // X is the preceding kernel's output
       const uint32_t fx_leader = mapa(smem_u32(full_x), 0);
-      for (int i = 0; i < n_st; ++i) {
-        const int ul = i / a.k_tiles, kt = i - ul * a.k_tiles;
+      Walk w;
+      w.start(a, cid, ncl, beg, dp_n);
+      for (int i = 0; i < n_st; ++i, w.adv(a, cid, ncl, beg, dp_n)) {
+        const int kt = w.kt;
         int pair, mt;
-        unit_nm(a, cid + ul * ncl, pair, mt);
+        unit_nm(a, w.u, pair, mt);
         const int s = i % kXStages;
         mbar_wait<2>(&empty_x[s], ((i / kXStages) & 1) ^ 1);
         const uint32_t e = elect_one();
@@ -254,28 +344,36 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int half = a.bn >> 1;
       const uint32_t d_tmem = tmem_base + kDCol0;
       const uint32_t ae_bar = smem_u32(afull), dm_bar = smem_u32(dempty), fx_bar = smem_u32(full_x);
-      for (int ul = 0; ul < my_units; ++ul) {
-        wait_cluster(dm_bar, (ul & 1) ^ 1);  // both CTAs drained D
-        tc_fence_after();
-        for (int kt = 0; kt < a.k_tiles; ++kt) {
-          const int i = ul * a.k_tiles + kt;
-          const int xs = i % kXStages, sl = i % kASlots;
-          wait_cluster(fx_bar + 8 * xs, (i / kXStages) & 1);     // both X halves landed
-          wait_cluster(ae_bar + 8 * sl, (i / kASlots) & 1);      // both A tiles rebuilt
+      // a segment = one unit's contiguous k range: fresh accumulator at its
+      // first step, dfull committed after its last
+      Walk w;
+      w.start(a, cid, ncl, beg, dp_n);
+      int seg = 0;
+      for (int i = 0; i < n_st; ++i, w.adv(a, cid, ncl, beg, dp_n)) {
+        const bool s0 = i == 0 || i == dp_n || w.kt == 0;
+        if (s0) {
+          wait_cluster(dm_bar, (seg & 1) ^ 1);  // both CTAs drained D
           tc_fence_after();
-          const uint32_t e = elect_one();
-          const uint64_t bd0 = sdesc_kmajor_sw128(smem_u32(smem_x + xs * kXStage));
-          const uint32_t bd_lo = static_cast<uint32_t>(bd0), bd_hi = static_cast<uint32_t>(bd0 >> 32);
-          const uint32_t ta = tmem_base + sl * kAColsTile;
-#pragma unroll
-          for (int j = 0; j < kTileK / 16; ++j) {
-            const uint32_t off = ((j >> 2) * (half * 128) + (j & 3) * 32) >> 4;
-            mma_2sm(e, d_tmem, ta + j * 8, bd_lo + off, bd_hi, idesc, (kt | j) ? 1u : 0u);
-          }
-          commit_2sm(e, &empty_x[xs]);
-          commit_2sm(e, &aempty[sl]);
         }
-        commit_2sm(elect_one(), dfull);
+        const int xs = i % kXStages, sl = i % kASlots;
+        wait_cluster(fx_bar + 8 * xs, (i / kXStages) & 1);     // both X halves landed
+        wait_cluster(ae_bar + 8 * sl, (i / kASlots) & 1);      // both A tiles rebuilt
+        tc_fence_after();
+        const uint32_t e = elect_one();
+        const uint64_t bd0 = sdesc_kmajor_sw128(smem_u32(smem_x + xs * kXStage));
+        const uint32_t bd_lo = static_cast<uint32_t>(bd0), bd_hi = static_cast<uint32_t>(bd0 >> 32);
+        const uint32_t ta = tmem_base + sl * kAColsTile;
+#pragma unroll
+        for (int j = 0; j < kTileK / 16; ++j) {
+          const uint32_t off = ((j >> 2) * (half * 128) + (j & 3) * 32) >> 4;
+          mma_2sm(e, d_tmem, ta + j * 8, bd_lo + off, bd_hi, idesc, (s0 && j == 0) ? 0u : 1u);
+        }
+        commit_2sm(e, &empty_x[xs]);
+        commit_2sm(e, &aempty[sl]);
+        if (i + 1 == n_st || i + 1 == dp_n || w.kt + 1 == a.k_tiles) {
+          commit_2sm(elect_one(), dfull);
+          ++seg;
+        }
       }
     }
   } else if (warp < kDqWarps) {
@@ -325,26 +423,30 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t dm_leader = mapa(smem_u32(dempty), 0);
     const bool lead_thread = warp == kWarpEpi0 && lane == 0;
     int nchunk = 0;  // TMA-stored chunks so far (staging buffer = nchunk & 1)
-    pdl_wait();      // Y writes: the preceding grid must be complete
-    for (int ul = 0; ul < my_units; ++ul) {
+    uint32_t fph = 0;  // fixb phase
+    pdl_wait();      // Y / workspace writes: the preceding grid must be complete
+    Walk w;
+    w.start(a, cid, ncl, beg, dp_n);
+    for (int seg = 0; w.i < n_st; ++seg) {
+      const int u = w.u, kt0 = w.kt;
+      const int len = min(a.k_tiles - kt0, n_st - w.i);
+      w.i += len;
+      w.set(a, cid, ncl, beg, dp_n);
       int pair, mt;
-      unit_nm(a, cid + ul * ncl, pair, mt);
+      unit_nm(a, u, pair, mt);
       const int n0 = (2 * pair + static_cast<int>(rank)) * kTileN, n = n0 + rr;
       const float fs = n < a.N ? __half2float(__ushort_as_half(__ldg(a.scales + n))) : 0.f;
-      mbar_wait<2>(dfull, ul & 1);
+      mbar_wait<2>(dfull, seg & 1);
       tc_fence_after();
-      // one chunk of CW batch columns (8 KB staged: CW = 32 for 16-bit Y, 16 for f32)
-      auto chunk = [&](auto cw_tag, int c0) {
+      auto d_drained = [&]() {  // D may be overwritten by the next segment's MMAs
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) arrive_cluster(dm_leader);
+      };
+      // one chunk of CW batch columns of fp32 sums -> x row scale -> Y (8 KB
+      // staged: CW = 32 for 16-bit Y, 16 for f32)
+      auto emit = [&](auto cw_tag, int c0, const uint32_t* v) {
         constexpr int CW = decltype(cw_tag)::value;
-        uint32_t v[CW];
-        tmem_ld_x16(t_d + c0, *reinterpret_cast<uint32_t(*)[16]>(v));
-        if constexpr (CW == 32) tmem_ld_x16(t_d + c0 + 16, *reinterpret_cast<uint32_t(*)[16]>(v + 16));
-        tmem_wait_ld();
-        if (c0 + CW >= a.bn) {  // last chunk read: D may be overwritten
-          tc_fence_before();
-          __syncwarp();
-          if (lane == 0) arrive_cluster(dm_leader);
-        }
         const int m0 = mt * a.bn + c0;
         if (!a.y_tma) {
 #pragma unroll
@@ -405,12 +507,96 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         ++nchunk;
       };
-      if (a.y_dtype == LPQT_F32) {
+      // D columns [c0, c0 + CW) of this thread's row
+      auto load_d = [&](auto cw_tag, int c0, uint32_t* v) {
+        constexpr int CW = decltype(cw_tag)::value;
+        tmem_ld_x16(t_d + c0, *reinterpret_cast<uint32_t(*)[16]>(v));
+        if constexpr (CW == 32) tmem_ld_x16(t_d + c0 + 16, *reinterpret_cast<uint32_t(*)[16]>(v + 16));
+        tmem_wait_ld();
+      };
+      auto each_chunk = [&](auto&& body) {
+        if (a.y_dtype == LPQT_F32) {
 #pragma unroll 1
-        for (int c0 = 0; c0 < a.bn; c0 += 16) chunk(std::integral_constant<int, 16>{}, c0);
+          for (int c0 = 0; c0 < a.bn; c0 += 16) body(std::integral_constant<int, 16>{}, c0);
+        } else {
+#pragma unroll 1
+          for (int c0 = 0; c0 < a.bn; c0 += 32) body(std::integral_constant<int, 32>{}, c0);
+        }
+      };
+      if (kt0 == 0 && len == a.k_tiles) {
+        // ---- whole unit
+        each_chunk([&](auto tag, int c0) {
+          uint32_t v[decltype(tag)::value];
+          load_d(tag, c0, v);
+          if (c0 + decltype(tag)::value >= a.bn) d_drained();
+          emit(tag, c0, v);
+        });
+      } else if (kt0 > 0) {
+        // ---- stream-K share (this pair's first segment): publish the fp32
+        // partial, count in, move on
+        float4* part = reinterpret_cast<float4*>(a.partials + ((int64_t)cid * 2 + rank) * kPartFloats) + rr;
+#pragma unroll 1
+        for (int c0 = 0; c0 < a.bn; c0 += 16) {
+          uint32_t v[16];
+          load_d(std::integral_constant<int, 16>{}, c0, v);
+          if (c0 + 16 >= a.bn) d_drained();
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+            __stcg(part + (c0 / 4 + j) * kTileN, make_float4(__uint_as_float(v[4 * j]), __uint_as_float(v[4 * j + 1]),
+                                                            __uint_as_float(v[4 * j + 2]), __uint_as_float(v[4 * j + 3])));
+        }
+        // CTA barrier (cumulativity over the epilogue's stores), then one
+        // gpu-scope release reduction
+        named_bar_sync(1, 4 * 32);
+        if (lead_thread) red_release_gpu(&a.counters[2 * u + rank], len);
       } else {
+        // ---- stream-K head (this pair's last segment): wait for the other
+        // contributors, then own + p(cid + 1) + p(cid + 2) + ... in k order
+        const int c_last = sk_pair_of(a, (int64_t)(u - a.dp_units) * a.k_tiles + a.k_tiles - 1, ncl);
+        if (lead_thread) {
+          const int others = a.k_tiles - len;
+          for (uint32_t spin = 0; ld_acquire(&a.counters[2 * u + rank]) != others; ++spin) {
+            if (spin > (1u << 26)) __trap();  // a contributor never published: fail loudly
+            __nanosleep(64);
+          }
+        }
+        const uint32_t pbytes = static_cast<uint32_t>(kTileN * a.bn * 4);
+        const uint32_t sbase = smem_u32(smem_x) + rr * 16;
 #pragma unroll 1
-        for (int c0 = 0; c0 < a.bn; c0 += 32) chunk(std::integral_constant<int, 32>{}, c0);
+        for (int c = cid + 1; c <= c_last; ++c) {
+          // the X ring is drained (every MMA of this last segment completed)
+          if (lead_thread) {
+            fence_proxy_async_global();  // acquired generic-proxy partials -> bulk-copy reads
+            mbar_arrive_expect_tx(fixb, pbytes);
+            bulk_g2s_plain(smem_x, a.partials + ((int64_t)c * 2 + rank) * kPartFloats, pbytes, fixb);
+          }
+          mbar_wait<2>(fixb, fph);
+          fph ^= 1u;
+          const bool last = c == c_last;
+          each_chunk([&](auto tag, int c0) {
+            constexpr int CW = decltype(tag)::value;
+            uint32_t v[CW];
+            load_d(tag, c0, v);
+#pragma unroll
+            for (int j = 0; j < CW / 4; ++j) {
+              const float4 p = lds128_f32(sbase + (c0 / 4 + j) * kTileN * 16);
+              v[4 * j + 0] = __float_as_uint(__uint_as_float(v[4 * j + 0]) + p.x);
+              v[4 * j + 1] = __float_as_uint(__uint_as_float(v[4 * j + 1]) + p.y);
+              v[4 * j + 2] = __float_as_uint(__uint_as_float(v[4 * j + 2]) + p.z);
+              v[4 * j + 3] = __float_as_uint(__uint_as_float(v[4 * j + 3]) + p.w);
+            }
+            if (last) {
+              if (c0 + CW >= a.bn) d_drained();
+              emit(tag, c0, v);
+            } else {  // running sum back into D
+              tmem_st_x16(t_d + c0, *reinterpret_cast<uint32_t(*)[16]>(v));
+              if constexpr (CW == 32) tmem_st_x16(t_d + c0 + 16, *reinterpret_cast<uint32_t(*)[16]>(v + 16));
+            }
+          });
+          tmem_wait_st();
+          named_bar_sync(1, 4 * 32);  // every thread is done with the staged partial
+        }
+        if (lead_thread) a.counters[2 * u + rank] = 0;  // every partial is read: re-arm
       }
     }
     if (lead_thread) bulk_wait_read<0>();  // staging smem stays valid until the stores read it
@@ -473,43 +659,76 @@ static int max_pairs() {
 
 int prefill_2sm_pairs() { return max_pairs(); }
 
-// Unit width: the batch columns bn (a multiple of 32, <= 256) that minimise
-// rounds x k-step cost, rounds = ceil(units / co-resident pairs); a k step
-// costs max(4 bn, ~700) cycles (MMA floor M = 256 across the pair:
-// bn / 2 cycles per K = 16; the dequant of one 128 x 128 tile by 16 warps:
-// ~600 + barrier overhead).  Returns the estimated cycles per SM.
-double prefill_2sm_choose(int64_t M, int64_t N, int64_t K, int* bn_out) {
+// Unit width and schedule: the batch columns bn (a multiple of 32, <= 256) and
+// whole units vs whole rounds + a stream-K wave that minimise the per-pair
+// cycle estimate.  A k step costs max(4 bn, ~700) cycles (MMA floor M = 256
+// across the pair: bn / 2 cycles per K = 16; the dequant of one 128 x 128
+// tile by 16 warps: ~600 + barrier overhead) and a segment's epilogue drain
+// ~32 bn.  Whole units: ceil(units / P) rounds.  Hybrid: floor(units / P) - 1
+// whole rounds, then the last P + units % P units as stream-K (units * k_tiles
+// / P steps per pair, each unit cut in at most a few pieces) plus a fixup
+// (the publisher's partial store and the reducer's gather, ~2 drains).
+// Returns the estimated cycles per SM.
+// force: 0 = by the estimate, 1 = whole units only, 2 = whole rounds + stream-K wave
+static double choose(int64_t M, int64_t N, int64_t K, int* bn_out, int* dp_units_out, int force = 0) {
   const int64_t n_pairs = (N + kTileN - 1) / kTileN / 2;
   const int64_t k_tiles = (K + kTileK - 1) / kTileK;
   const int64_t pairs = max_pairs();
   double best = 1e30;
   int best_bn = 256;
+  int64_t best_dp = -1;  // -1: whole units only
   for (int bn = 256; bn >= 128; bn -= 32) {
     const int64_t units = n_pairs * ((M + bn - 1) / bn);
     const int64_t rounds = (units + pairs - 1) / pairs;
-    const double step = std::max(4.0 * bn, 700.0);
-    const double t = (double)rounds * (k_tiles * step + 4.0 * bn * 8);  // + the epilogue drain
-    if (t < best * 0.98) {
-      best = t;
+    const double step = std::max(4.0 * bn, 700.0), drain = 4.0 * bn * 8;
+    const double t_dp = (double)rounds * (k_tiles * step + drain);
+    if (force != 2 && t_dp < best * 0.98) {
+      best = t_dp;
       best_bn = bn;
+      best_dp = -1;
+    }
+    if (force == 1 || (force == 0 && units % pairs == 0) || 2 * units > p2::kCounters) continue;
+    const int64_t dp_rounds = units / pairs > 0 ? units / pairs - 1 : 0;
+    const int64_t sk_units = units - dp_rounds * pairs;
+    const double per = (double)sk_units * k_tiles / pairs;
+    if (force == 0 && per < 8.0) continue;  // (every pair streams >= 8 k steps, else the fixups dominate)
+    const double t_sk = dp_rounds * (k_tiles * step + drain) + per * step + (per / k_tiles + 1.0) * drain + 2.0 * drain;
+    if (t_sk < best * 0.98) {
+      best = t_sk;
+      best_bn = bn;
+      best_dp = dp_rounds * pairs;
     }
   }
   if (bn_out) *bn_out = best_bn;
+  if (dp_units_out) *dp_units_out = static_cast<int>(best_dp);
   return best;
 }
+
+double prefill_2sm_choose(int64_t M, int64_t N, int64_t K, int* bn_out, int* sk_out, int force) {
+  int dp = -1;
+  const double t = choose(M, N, K, bn_out, &dp, force);
+  if (sk_out) *sk_out = dp >= 0;
+  return t;
+}
+
+// Workspace of the stream-K schedule: the counters region (shared with
+// gemm.cu's stream-K, self-resetting) + one partial slot per pair and CTA.
+int64_t prefill_2sm_workspace() { return p2::kCounters * 4 + (int64_t)max_pairs() * 2 * p2::kPartFloats * 4; }
 
 // Host launch of the pair kernel (called from gemm.cu's dispatcher; CGQ FP6,
 // even number of 128-row weight tiles).  Returns LPQT_E_UNSUPPORTED when the
 // shape does not fit (the caller then uses the single-SM kernel).
 int launch_prefill_2sm(const uint8_t* tiles, const uint16_t* scales, const uint16_t* Xt, int64_t ldx, int64_t M,
                        int64_t N, int64_t K, void* Y, int y_dtype, int y_layout, int64_t ldy, int flags,
-                       cudaStream_t stream, int* grid_out) {
+                       int force, void* workspace, int64_t workspace_bytes, cudaStream_t stream, int* grid_out) {
   const int n_tiles = static_cast<int>((N + kTileN - 1) / kTileN);
   if (n_tiles % 2 != 0) return LPQT_E_UNSUPPORTED;
   EncodeTiledFn2 enc = encode_fn_2sm();
   if (!enc) return LPQT_E_CUDA;
-  int bn = 256;
-  prefill_2sm_choose(M, N, K, &bn);
+  int bn = 256, dp_units = -1;
+  choose(M, N, K, &bn, &dp_units, force);
+  const int sk = dp_units >= 0;
+  if (sk && (workspace == nullptr || workspace_bytes < prefill_2sm_workspace())) return LPQT_E_WORKSPACE;
   CUtensorMap map;
   const cuuint64_t dims[2] = {static_cast<cuuint64_t>(K), static_cast<cuuint64_t>(M)};
   const cuuint64_t strides[1] = {static_cast<cuuint64_t>(ldx) * 2};
@@ -551,12 +770,36 @@ int launch_prefill_2sm(const uint8_t* tiles, const uint16_t* scales, const uint1
   a.y_tma = y_tma;
   a.m_tiles = static_cast<int>((M + bn - 1) / bn);
   a.units = (n_tiles / 2) * a.m_tiles;
+  a.sk = sk;
+  a.dp_units = sk ? dp_units : a.units;
+  a.total = (int64_t)(a.units - a.dp_units) * a.k_tiles;
+  a.counters = static_cast<int*>(workspace);
+  a.partials = sk ? reinterpret_cast<float*>(static_cast<uint8_t*>(workspace) + p2::kCounters * 4) : nullptr;
   // X larger than ~1/3 of L2: keep each batch tile's X resident (weight-row pairs fastest)
   a.n_fastest = (a.m_tiles > 1 && M * K * 2 > ((int64_t)40 << 20)) ? 1 : 0;
+  // rasterization group: per k step the P units in flight read P / G X slices
+  // (bn x 128 f16) and G weight pairs (2 x 12 KB) — least L2 -> HBM traffic at
+  // G = sqrt(P x X slice / pair slice) (~14 at bn 256)
+  // — a divisor of the pair count when one is within 2x of that (a narrow last
+  // group would put few pairs x many X tiles in flight)
+  {
+    const int np = n_tiles / 2;
+    const double g = std::sqrt((double)max_pairs() * bn * kTileK * 2 / (2.0 * kTileBytes));
+    int best = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(np, std::llround(g))));
+    double off = 1e30;
+    for (int d = 1; d <= np; ++d) {
+      const double o = std::fabs(std::log(d / g));
+      if (np % d == 0 && o < off && o <= std::log(2.0)) {
+        off = o;
+        best = d;
+      }
+    }
+    a.group = best;
+  }
   a.y_dtype = y_dtype;
   a.y_layout = y_layout;
   a.sm = ShiftMuls{1u << 26, 1u << 28, 1u << 30};
-  const int pairs = std::min(max_pairs(), a.units);
+  const int pairs = sk ? max_pairs() : std::min(max_pairs(), a.units);
   static std::once_flag once;
   static cudaError_t attr_err = cudaSuccess;
   std::call_once(once, [] {

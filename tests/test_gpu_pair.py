@@ -77,3 +77,33 @@ def test_odd_tile_count_falls_back():
     assert L.plan(m, n, k, sched="pair")["schedule"] != "pair"
     y = L.w6a16_linear(x, w, out_dtype=torch.float32, sched="pair")
     assert _rel(y, L.w6a16_linear(x, w, out_dtype=torch.float32, sched="single")) <= 1e-5
+
+
+@pytest.mark.parametrize("n,k,m,force", [(2048, 8192, 512, 0), (10240, 8192, 512, 0), (1024, 8192, 300, 0),
+                                         (1024, 4096, 1000, 0), (8192, 4096, 1280, 2), (2048, 4096, 8192, 2),
+                                         (2048, 4096, 8192, 1), (1024, 4096, 600, 2)])
+def test_pair_stream_k(n, k, m, force):
+    """Whole rounds + a stream-K wave over the pairs (units cut between pairs,
+    partials reduced by the unit's head pair in k order), whole units only
+    (force 1), grouped rasterization at M x K x 2 > 40 MB: against the f64
+    product of the same dequantized weights, the single-SM kernel, and
+    bit-identical on repeat.  force: 0 = the planner's choice (stream-K at
+    these shapes), 1 / 2 = split_k hook forcing whole units / stream-K."""
+    plan = L.plan(m, n, k, split_k=force, sched="pair")
+    assert plan["schedule"] == "pair" and plan["splits"] == (1 if force == 1 else 2), plan
+    g = torch.Generator(device="cuda").manual_seed(n + k + m)
+    W = (torch.randn(n, k, generator=g, device="cuda") * 0.02).half()
+    x = torch.randn(m, k, generator=g, device="cuda").half()
+    w = L.Fp6Weight.quantize(W)
+    ref = x.double() @ w.dequantize_f16().double().t()
+    run = lambda dt: L.w6a16_linear(x, w, out_dtype=dt, sched="pair", split_k=force)
+    y2 = run(torch.float32)
+    y1 = L.w6a16_linear(x, w, out_dtype=torch.float32, sched="single")
+    assert _rel(y2, ref) <= 1e-3
+    assert _rel(y2, y1) <= 3e-5   # (a unit may be cut over several pairs: more partial sums)
+    for _ in range(3):
+        assert torch.equal(y2, run(torch.float32))
+    assert _rel(run(torch.float16).float(), y1) <= 1e-2
+    if force == 0:  # the reference layout Y[N, M] through the same schedule
+        Y = L.gemm_quantized(L.quantize_tensor(W, CGQ), x.t().contiguous())
+        assert _rel(Y, y1.t()) <= 3e-5

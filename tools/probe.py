@@ -55,6 +55,7 @@ def main():
     ap.add_argument("--shapes", default="all")
     ap.add_argument("--m", default="1,16")
     ap.add_argument("--split", default="0", help="comma list of split_k values (0 = automatic plan)")
+    ap.add_argument("--sched", default="auto", help="auto / pair / single / streamk / cluster")
     args = ap.parse_args()
     shapes = SHAPES["7b"] + SHAPES["70b"] if args.shapes == "all" else sum((SHAPES[s] for s in args.shapes.split(",")), [])
     splits = [int(v) for v in args.split.split(",")]
@@ -65,12 +66,12 @@ def main():
         for m, split in ((int(v), sp) for v in args.m.split(",") for sp in splits):
             x = torch.randn(m, k, device="cuda").half()
             y = torch.empty(m, n, device="cuda", dtype=torch.float16)
-            t6 = time_fn(lambda: L.w6a16_linear(x, lin.weight, out=y, split_k=split), flush=flush)
+            t6 = time_fn(lambda: L.w6a16_linear(x, lin.weight, out=y, split_k=split, sched=args.sched), flush=flush)
             t16 = time_fn(lambda: torch.matmul(x, W.t()), flush=flush)
             ref = (x.float() @ W.float().t())
             err = float((y.float() - ref).abs().max() / ref.abs().max())
             wbytes = lin.weight.stream_bytes() + 2 * m * k + 2 * m * n
-            print(json.dumps({"n": n, "k": k, "m": m, "split_k": split, "plan": L.plan(m, n, k, split),
+            print(json.dumps({"n": n, "k": k, "m": m, "split_k": split, "plan": L.plan(m, n, k, split, sched=args.sched),
                               "us_fp6": round(t6 * 1e6, 2), "us_cublas": round(t16 * 1e6, 2),
                               "speedup": round(t16 / t6, 3), "GBps": round(wbytes / t6 / 1e9, 1),
                               "TFLOPS": round(2 * m * n * k / t6 / 1e12, 2), "err_vs_fp16W": err}), flush=True)
