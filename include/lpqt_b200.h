@@ -183,6 +183,25 @@ int lpqt_w6a16_linear(const uint8_t* tiles, const uint16_t* scales,
  * LPQT_SCHED_SINGLE forbids it (A/B hooks). */
 #define LPQT_SCHED_SINGLE 8
 #define LPQT_SCHED_PAIR 16
+/* The paper's Bias-Shift ablation ("the same FP6 kernel
+ * without Bias-Shift"), decode batches M <= 16, CGQ FP6 only (else
+ * LPQT_E_UNSUPPORTED).  The product kernel rebuilds weights with the
+ * hardware e3m2 converter and applies S in fp32 after the contraction
+ * (gemm.py:84-88); these flags swap in the paper's software rebuilds, each
+ * followed by the per-weight binary16 scale multiply of the reference's
+ * dequant paths:
+ *   LPQT_REBUILD_BIAS_SHIFT  compose (sign << 15 | eeemm << 8, dequant.py:37-41)
+ *                            x folded scale S * 2^12 (dequant.py:82-86);
+ *   LPQT_REBUILD_NAIVE       exponent + 12, subnormals x 2^12, then x S
+ *                            (dequant_naive_array, dequant.py:72-79).
+ * Both give the binary16 dequantized weight bit for bit (so identical Y).
+ * Folded scales above 65504 (S > 15.99) overflow under BIAS_SHIFT, as in
+ * the reference (ScaleOverflow). */
+#define LPQT_REBUILD_BIAS_SHIFT 32
+#define LPQT_REBUILD_NAIVE 64
+/* `tiles` are native FP5 tiles (lpqt_fp5n_prepack), CGQ; single-SM kernels
+ * (decode and prefill), no pair kernel, no LPQT_REBUILD_* */
+#define LPQT_WEIGHTS_FP5 128
 int lpqt_w6a16_linear_ex(const uint8_t* tiles, const uint16_t* scales,
                          const uint16_t* Xt, int64_t ldx, int64_t M, int64_t N,
                          int64_t K, void* Y, int y_dtype, int y_layout,
@@ -308,6 +327,25 @@ int lpqt_fp5_dequant_naive(const uint8_t* codes, const uint16_t* scales,
                            int64_t n, uint16_t* out, void* stream);
 int lpqt_fp5_prepack(const uint8_t* seg4, const uint8_t* seg1, int64_t N,
                      int64_t K, uint8_t* tiles, void* stream);
+
+/* FP5 e3m1 in its own 4+1 tile layout (0.625 B per weight, vs the FP6 tiles'
+ * 0.75 of lpqt_fp5_prepack): 128 x 128 tiles of 10240 B — a s|eee nibble
+ * plane and a mantissa bit plane per 32-weight group, arranged so the GEMM's
+ * rebuild is two shifts + two logic ops per four weights ahead of the
+ * hardware e3m2 converter (common.cuh).  Planes as packing.py:84-85
+ * (seg4 = c >> 1, seg1 = c & 1).  For lpqt_w6a16_linear_blocks with
+ * LPQT_WEIGHTS_FP5 (CGQ only).  Not a reference interface (a layout change
+ * like lpqt_fp6_prepack). */
+int64_t lpqt_fp5n_tiles_bytes(int64_t N, int64_t K);
+int lpqt_fp5n_prepack(const uint8_t* seg4, const uint8_t* seg1, int64_t N,
+                      int64_t K, uint8_t* tiles, void* stream);
+/* inverse -> row-major e3m1 codes[N, K] (uint8) */
+int lpqt_fp5n_unprepack(const uint8_t* tiles, int64_t N, int64_t K,
+                        uint8_t* codes, void* stream);
+/* tiles -> out[N, K] binary16 = value_f16[c] * S[n] through the GEMM's
+ * rebuild (dequant_naive_array, dequant.py:72-79) */
+int lpqt_fp5n_tiles_dequant(const uint8_t* tiles, const uint16_t* scales,
+                            int64_t N, int64_t K, uint16_t* out, void* stream);
 
 /* ---- INT4 asymmetric, CGQ / FGQ (quantizer.py:232-244, packing.py:121-141)
  * The paper's comparator format: per block zero point RN_f16(min) and scale

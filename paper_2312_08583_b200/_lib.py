@@ -29,6 +29,7 @@ OK = 0
 E_INVALID_INPUT, E_SHAPE, E_SCALE_OVERFLOW, E_PAYLOAD = -1, -2, -3, -4
 E_INVALID_CODE, E_UNSUPPORTED, E_WORKSPACE, E_CUDA = -5, -6, -7, -100
 LAUNCH_PDL = 1
+WEIGHTS_FP5 = 128   # LPQT_WEIGHTS_FP5: native 5-bit tiles
 SCHED_STREAMK, SCHED_CLUSTER = 2, 4
 
 # device flag bits
@@ -99,6 +100,10 @@ SIGNATURES = {
     "lpqt_fp5_dequant_bias_shift": (_I32, [_P, _P, _I64, _P, _P]),
     "lpqt_fp5_dequant_naive": (_I32, [_P, _P, _I64, _P, _P]),
     "lpqt_fp5_prepack": (_I32, [_P, _P, _I64, _I64, _P, _P]),
+    "lpqt_fp5n_tiles_bytes": (_I64, [_I64, _I64]),
+    "lpqt_fp5n_prepack": (_I32, [_P, _P, _I64, _I64, _P, _P]),
+    "lpqt_fp5n_unprepack": (_I32, [_P, _I64, _I64, _P, _P]),
+    "lpqt_fp5n_tiles_dequant": (_I32, [_P, _P, _I64, _I64, _P, _P]),
     "lpqt_int4_quantize_blocks": (_I32, [_P, _I32, _I64, _I64, _I64, _I64, _P, _P, _P, _P, _P]),
     "lpqt_int4_pack": (_I32, [_P, _I64, _P, _P, _P]),
     "lpqt_int4_unpack": (_I32, [_P, _I64, _P, _P]),

@@ -136,6 +136,87 @@ __device__ __forceinline__ void fp6x32_cvt_f16x32_fma(const uint32_t w[6], uint3
   out[14] = cvt_e3m2x2_lo(e1);
   out[15] = cvt_e3m2x2_hi(e1);
 }
+// ---------------------------------------------------------------------------
+// Software rebuilds on the same tile layout, for the paper's ablation
+// (the FP6 kernel with vs without Bias-Shift; selected by
+// LPQT_REBUILD_* launch flags, decode kernels only).  Both produce the
+// binary16 dequantized weight of the reference's two dequant paths
+// (dequant.py:72-86): the epilogue then applies no scale.
+//   bias-shift: h16 = sign << 15 | eeemm << 8 (= value * 2^-12, dequant.py:37-41),
+//               then x folded scale S * 2^12 (HMUL2, one binary16 rounding);
+//   naive:      the exact binary16 value — exponent + 12 for normal codes,
+//               x 2^12 for the subnormal ones (the paper's two-step cast) —
+//               then x S (HMUL2).
+// Both equal value_f16 * S rounded once, so the two ablation kernels give
+// bit-identical Y (tests/test_dequant.py:93-102 of the reference).
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t bias_shift_x2(uint32_t w, uint32_t sel) {
+  const uint32_t p = __byte_perm(w, 0u, sel);  // codes into the high bytes of the two halves
+  return (p & 0x1F001F00u) | ((p << 2) & 0x80008000u);
+}
+__device__ __forceinline__ uint32_t naive_x2(uint32_t w, uint32_t sel) {
+  const uint32_t h = bias_shift_x2(w, sel);
+  const uint32_t t = (h & 0x1C001C00u) + 0x7C007C00u;    // bit 15 / 31: the exponent is non-zero
+  uint32_t m;  // 0xFFFF for the normal halves: PRMT sign-replicate mode (selector msb; __byte_perm masks it off)
+  asm("prmt.b32 %0, %1, 0, 0xBB99;" : "=r"(m) : "r"(t));
+  const uint32_t hn = h + 0x30003000u;                   // exponent + 12 (no carry out of the field)
+  const __half2 hs2 = __hmul2(*reinterpret_cast<const __half2*>(&h), __float2half2_rn(4096.f));  // subnormals x 2^12
+  const uint32_t hs = *reinterpret_cast<const uint32_t*>(&hs2);
+  return (hn & m) | (hs & ~m);
+}
+template <int RB>
+__device__ __forceinline__ void fp6x32_soft_f16x32(const uint32_t w[6], uint32_t out[16], uint32_t s2,
+                                                   const ShiftMuls& sm) {
+  auto one = [&](uint32_t x, uint32_t sel) { return RB == 1 ? bias_shift_x2(x, sel) : naive_x2(x, sel); };
+#pragma unroll
+  for (int i = 0; i < 6; ++i) {
+    out[2 * i] = one(w[i], 0x1404);
+    out[2 * i + 1] = one(w[i], 0x3424);
+  }
+  const uint32_t e0 = spare_gather_fma(w[0], w[1], w[2], sm) & 0x3F3F3F3Fu;
+  const uint32_t e1 = spare_gather_fma(w[3], w[4], w[5], sm) & 0x3F3F3F3Fu;
+  out[12] = one(e0, 0x1404);
+  out[13] = one(e0, 0x3424);
+  out[14] = one(e1, 0x1404);
+  out[15] = one(e1, 0x3424);
+#pragma unroll
+  for (int j = 0; j < 16; ++j) {
+    const __half2 v = __hmul2(*reinterpret_cast<const __half2*>(&out[j]), *reinterpret_cast<const __half2*>(&s2));
+    out[j] = *reinterpret_cast<const uint32_t*>(&v);
+  }
+}
+
+// FP5 native rebuild (layout above): 32 weights -> 16 half2 of the exact
+// binary16 values, k ascending.  Shifts on the FMA pipe (IMAD / IMAD.HI with
+// kernel-argument multipliers, sm.m26 = 2^26 etc.; pass plain powers of two).
+template <int S>
+__device__ __forceinline__ uint32_t mant_bits(uint32_t mw, const ShiftMuls& sm) {
+  // mantissa bit of byte t at bit 8t + S -> bit 8t + 1
+  if constexpr (S == 0) return mw * 2u;
+  else if constexpr (S == 1) return mw;
+  else if constexpr (S == 3) return __umulhi(mw, sm.m30);  // >> 2
+  else if constexpr (S == 5) return __umulhi(mw, sm.m28);  // >> 4
+  else if constexpr (S == 7) return __umulhi(mw, sm.m26);  // >> 6
+  else return mw >> (S - 1);
+}
+__device__ __forceinline__ void fp5x32_cvt_f16x32(const uint32_t nib[4], uint32_t mw, uint32_t out[16],
+                                                  const ShiftMuls& sm) {
+  uint32_t m[8];
+  m[0] = mant_bits<0>(mw, sm); m[1] = mant_bits<1>(mw, sm); m[2] = mant_bits<2>(mw, sm);
+  m[3] = mant_bits<3>(mw, sm); m[4] = mant_bits<4>(mw, sm); m[5] = mant_bits<5>(mw, sm);
+  m[6] = mant_bits<6>(mw, sm); m[7] = mant_bits<7>(mw, sm);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const uint32_t lo = nib[i] * 4u, hi = __umulhi(nib[i], sm.m30);  // << 2 (even nibbles), >> 2 (odd)
+    const uint32_t x0 = (lo & 0x3C3C3C3Cu) | (m[2 * i] & 0x02020202u);
+    const uint32_t x1 = (hi & 0x3C3C3C3Cu) | (m[2 * i + 1] & 0x02020202u);
+    out[4 * i] = cvt_e3m2x2_lo(x0);
+    out[4 * i + 1] = cvt_e3m2x2_hi(x0);
+    out[4 * i + 2] = cvt_e3m2x2_lo(x1);
+    out[4 * i + 3] = cvt_e3m2x2_hi(x1);
+  }
+}
+
 // codes of the 32 weights (inverse of fp6x32_pack_words; used by unprepack)
 __host__ __device__ inline void fp6x32_unpack_codes(const uint32_t w[6], uint8_t c[32]) {
   for (int i = 0; i < 6; ++i)
@@ -232,6 +313,52 @@ __host__ __device__ __forceinline__ int64_t tile_word_addr(int64_t n, int64_t g3
   return (rt * k_tiles + kt) * kTileBytes + ((int64_t)(khalf * 3 + quad) * kTileN + rr) * 16 + wq * 4;
 }
 
+// ---------------------------------------------------------------------------
+// FP5 e3m1 native tiles ("4+1", packing.py:84-85's split: a 4-bit s|eee plane
+// and a 1-bit mantissa plane), 0.625 B per weight.
+//   tile = 128 rows x 128 k = 10240 B, stored [row_tile][k_tile];
+//   inside: nibble quads [khalf 2][grp 2][row 128][16 B] (8192 B), then the
+//   mantissa words [khalf 2][row 128][grp 2][4 B] (2048 B).
+//   32-weight group: nibble word i (0..3) holds s|eee of weight 8i + t in
+//   nibble 2t (t = 0..3) and of weight 8i + 4 + t in nibble 2t + 1; the
+//   mantissa word holds m of weight 8i + 4p + t at bit 8t + 2i + p.
+// Rebuild (fp5x32_cvt_f16x32): the e3m1 code (s, eee, m) is the e3m2 code
+// (s, eee, m0), so per 4 weights one shift of the nibble word + one of the
+// mantissa word (FMA pipe), one AND + one LOP3 build the four e3m2 bytes for
+// two hardware converts (F2FP.E3M2): 16 F2FP + 16 LOP per 32 weights.
+// ---------------------------------------------------------------------------
+constexpr int kTileBytes5 = kTileN * kTileK * 5 / 8;  // 10240
+constexpr int kTile5Nib = kTileN * kTileK / 2;         // 8192: nibble quads, then mantissa words
+
+__host__ __device__ inline void fp5x32_pack_words(const uint8_t c[32], uint32_t nib[4], uint32_t& mw) {
+  mw = 0;
+  for (int i = 0; i < 4; ++i) {
+    nib[i] = 0;
+    for (int p = 0; p < 2; ++p)
+      for (int t = 0; t < 4; ++t) {
+        const uint32_t code = c[8 * i + 4 * p + t] & 0x1Fu;
+        nib[i] |= (code >> 1) << (4 * (2 * t + p));
+        mw |= (code & 1u) << (8 * t + 2 * i + p);
+      }
+  }
+}
+__host__ __device__ inline void fp5x32_unpack_codes(const uint32_t nib[4], uint32_t mw, uint8_t c[32]) {
+  for (int i = 0; i < 4; ++i)
+    for (int p = 0; p < 2; ++p)
+      for (int t = 0; t < 4; ++t)
+        c[8 * i + 4 * p + t] = static_cast<uint8_t>((((nib[i] >> (4 * (2 * t + p))) & 15u) << 1) |
+                                                    ((mw >> (8 * t + 2 * i + p)) & 1u));
+}
+// byte offset of the 32-weight group g32 (k = 32 g32 ..) of row n: nibble word wi (0..3), mantissa word (wi == 4)
+__host__ __device__ __forceinline__ int64_t tile5_word_addr(int64_t n, int64_t g32, int wi, int64_t k_tiles) {
+  const int64_t rt = n / kTileN, rr = n % kTileN;
+  const int64_t kt = g32 / 4;
+  const int gin = static_cast<int>(g32 % 4);
+  const int khalf = gin >> 1, grp = gin & 1;
+  const int64_t base = (rt * k_tiles + kt) * kTileBytes5;
+  if (wi < 4) return base + ((int64_t)(khalf * 2 + grp) * kTileN + rr) * 16 + wi * 4;
+  return base + kTile5Nib + ((int64_t)khalf * kTileN + rr) * 8 + grp * 4;
+}
 // ---------------------------------------------------------------------------
 // PTX wrappers
 // ---------------------------------------------------------------------------

@@ -184,7 +184,7 @@ struct L2Prefetch {
 #endif
 template <int BN, bool CSK, int WB = 6, bool FGQ = false>
 struct Cfg {
-  static constexpr int kTileB = WB == 6 ? kTileBytes : kTileN * kTileK / 2;
+  static constexpr int kTileB = WB == 6 ? kTileBytes : (WB == 5 ? kTileBytes5 : kTileN * kTileK / 2);
   // FGQ x FP6 at decode shapes (BN <= 32): "per-block partials" — every 128-k
   // weight tile's MMAs go into a fresh fp32 partial accumulator (kPSlots ring
   // in TMEM) and the epilogue adds S_block * partial in fp32, the reference's
@@ -664,13 +664,18 @@ __device__ __forceinline__ void ystage_put(const GemmArgs& a, uint32_t buf, int 
 // RAGGED: some stage holds fewer than kKStep tiles (the last k-step of a
 // tile when k_tiles % kKStep != 0, or an odd cluster split-K k-range); only
 // then do the dequant warps walk the stage sequence to learn tile counts.
-template <int BN, bool CSK, bool RAGGED, bool FGQ = false, int WB = 6, bool PEERS = false>
+// RB: weight rebuild — 0 the hardware e3m2 converter (the product path);
+// 1 / 2 the paper's software bias-shift / naive rebuilds x the per-row scale
+// in binary16 (the ablation kernels, common.cuh fp6x32_soft_f16x32)
+template <int BN, bool CSK, bool RAGGED, bool FGQ = false, int WB = 6, bool PEERS = false, int RB = 0>
 __global__ void __launch_bounds__(kThreads, 1)
     w6a16_tcgen05_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constant__ CUtensorMap tmap_y,
                          const GemmArgs a, const L2Prefetch pf, const FgqArgs fg,
                          const __grid_constant__ lpqt_peer_out po,
                          const __grid_constant__ PeerMapsOf<PEERS> pmaps) {
-  static_assert(WB == 6 || FGQ, "INT4 weights carry per-block scales and zero points (FGQ path)");
+  static_assert(WB != 4 || FGQ, "INT4 weights carry per-block scales and zero points (FGQ path)");
+  static_assert(WB != 5 || (!FGQ && !PEERS), "native FP5 tiles: CGQ");
+  static_assert(RB == 0 || (!FGQ && WB == 6 && !PEERS), "ablation rebuilds: CGQ FP6 only");
   using C = Cfg<BN, CSK, WB, FGQ>;
   constexpr int KS = C::kKStep;
   // barrier waits: decode (BN <= 32) parks in the hardware try_wait (woken on
@@ -910,7 +915,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t a_bar0 = C::kTileRing ? static_cast<uint32_t>(grp * 3) : 0u;
     const uint32_t t_row = tmem_base + (static_cast<uint32_t>(lg * 32) << 16);
     StageIter<Sched, KS> it;
-    if constexpr (RAGGED) it.start(a, sc, grp);
+    if constexpr (RAGGED || RB) it.start(a, sc, grp);
     auto stage_nt = [&]() -> int {
       if constexpr (RAGGED) {
         return it.nt();
@@ -919,12 +924,24 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     };
     uint32_t q[kSegs][6 * 2];
+    // WB 5: this row's mantissa words of the tile (after the 8 KB of nibble quads)
+    const uint32_t m_src = smem_u32(smem_w) + static_cast<uint32_t>(kTile5Nib + row * 8 +
+                                                                    (KS == 2 ? tl * C::kTileB : tl * kTileN * 8));
     uint32_t fs2 = 0;  // FGQ: this stage's block scale as f16x2
     uint32_t fz2 = 0;  // INT4: this stage's block zero point as f16x2
     // this thread's block parameter in the stage (after the KS weight tiles)
     const uint32_t s_src = smem_u32(smem_w) + KS * C::kTileB + (KS == 2 ? tl : 0) * C::kSBytes +
                            row * (WB == 4 ? 4 : 2);
     auto load_words = [&](int nt) {
+      if constexpr (RB > 0) {
+        // ablation: this row's scale (bias-shift: folded S * 2^12) for the stage's weight tile
+        int n_tile, m_tile;
+        tile_nm(a, it.sg.tile, n_tile, m_tile);
+        const int n = n_tile * kTileN + row;
+        const __half sc1 = n < a.N ? __ushort_as_half(__ldg(a.scales + n)) : __float2half(0.f);
+        const __half f = RB == 1 ? __hmul(sc1, __float2half(4096.f)) : sc1;
+        fs2 = __byte_perm(__half_as_ushort(f), 0u, 0x1010);
+      }
       mbar_wait_u32<WM>(fw0 + 8 * wc.idx, wc.ph);
       if (KS == 1 || tl < nt) {
         if constexpr (FGQ) {
@@ -946,6 +963,9 @@ __global__ void __launch_bounds__(kThreads, 1)
           if constexpr (WB == 6) {
             const uint4 v2 = lds128_u32(sh + 2 * kTileN * 16);
             q[h][8] = v2.x; q[h][9] = v2.y; q[h][10] = v2.z; q[h][11] = v2.w;
+          } else if constexpr (WB == 5) {
+            const uint2 mv = lds64_u32(m_src + wc.idx * C::kWStageBytes + (KS == 2 ? h * kTileN * 8 : 0));
+            q[h][8] = mv.x; q[h][9] = mv.y;
           }
         }
       }
@@ -964,6 +984,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (act) {
         if constexpr (WB == 4) {
           int4x64_to_f16(q[0], r, fs2, fz2);
+        } else if constexpr (WB == 5) {
+          fp5x32_cvt_f16x32(q[0], q[0][8], r, sm);
+          fp5x32_cvt_f16x32(q[0] + 4, q[0][9], r + 16, sm);
+        } else if constexpr (RB > 0) {
+          fp6x32_soft_f16x32<RB>(q[0], r, fs2, sm);
+          fp6x32_soft_f16x32<RB>(q[0] + 6, r + 16, fs2, sm);
         } else {
           fp6x32_cvt_f16x32_fma(q[0], r, sm);
           fp6x32_cvt_f16x32_fma(q[0] + 6, r + 16, sm);
@@ -980,6 +1006,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int h = 1; h < kSegs; ++h) {
           if constexpr (WB == 4) {
             int4x64_to_f16(q[h], r, fs2, fz2);
+          } else if constexpr (WB == 5) {
+            fp5x32_cvt_f16x32(q[h], q[h][8], r, sm);
+            fp5x32_cvt_f16x32(q[h] + 4, q[h][9], r + 16, sm);
+          } else if constexpr (RB > 0) {
+            fp6x32_soft_f16x32<RB>(q[h], r, fs2, sm);
+            fp6x32_soft_f16x32<RB>(q[h] + 6, r + 16, fs2, sm);
           } else {
             fp6x32_cvt_f16x32_fma(q[h], r, sm);
             fp6x32_cvt_f16x32_fma(q[h] + 6, r + 16, sm);
@@ -1000,7 +1032,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       wc.adv2(C::kWStages);
       // prefetch the group's next stage while the TMEM stores drain
       if (i + 2 < n_st) {
-        if constexpr (RAGGED) {
+        if constexpr (RAGGED || RB) {
           it.next(a, sc);
           it.next(a, sc);
         }
@@ -1124,7 +1156,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         return nn < a.N ? __ldg(reinterpret_cast<const float*>(fg.stage + (int64_t)a.n_tiles * a.k_tiles * kTileN * 2) +
                                 nn)
                         : 0.f;
-      if constexpr (FGQ) return nn < a.N ? 1.f : 0.f;
+      if constexpr (FGQ || RB > 0) return nn < a.N ? 1.f : 0.f;  // (the scale is in A)
       return nn < a.N ? __half2float(__ushort_as_half(__ldg(a.scales + nn))) : 0.f;
     };
     Seg sg_next;
@@ -1876,8 +1908,13 @@ int64_t prefill_2sm_workspace();                                                
 // ~60 % efficiency (68 % tensor-pipe activity at M = 2048, less with the
 // stream-K fixups at M = 512; profiles/r02_ncu_prefill_m2048.json,
 // r02_abx_pair_vs_single.jsonl).
+// Automatic choice: the pair kernel from M = LPQT_PAIR_MIN_M up whenever the
+// weight has an even number of 128-row tiles.  Measured on the 7B / 70B
+// shapes (profiles/r02_probe_pair_vs_single_small_m.jsonl): at M = 128 / 256
+// the pair kernel takes 0.55-0.85x the single-SM kernel's time (whose BN-128
+// stream-K fixups of 64-KB partials dominate), and above that it wins by more.
 #ifndef LPQT_PAIR_MIN_M
-#define LPQT_PAIR_MIN_M 129  // (below: decode / small prefill stay single-SM)
+#define LPQT_PAIR_MIN_M 65  // (below: decode / small prefill stay single-SM)
 #endif
 // The pair kernel's schedule choice: split_k 0 = automatic; with
 // LPQT_SCHED_PAIR, split_k 1 / 2 force whole units / whole rounds + a
@@ -1887,18 +1924,12 @@ static int pair_force(int split_k, int flags) {
   return (flags & LPQT_SCHED_PAIR) && split_k <= 2 ? split_k : -1;
 }
 static bool use_pair_kernel(int64_t M, int64_t N, int64_t K, int flags) {
+  (void)K;
   if (flags & LPQT_SCHED_SINGLE) return false;
   const int64_t n_tiles = (N + kTileN - 1) / kTileN;
   if (n_tiles % 2 != 0 || M < 17) return false;
   if (flags & LPQT_SCHED_PAIR) return true;
-  if (flags & (LPQT_SCHED_STREAMK | LPQT_SCHED_CLUSTER) || M < LPQT_PAIR_MIN_M) return false;
-  const int64_t k_tiles = (K + kTileK - 1) / kTileK;
-  const double t2 = prefill_2sm_choose(M, N, K, nullptr, nullptr, 0) / 0.9;
-  const int bn = pick_bn(M);
-  const int64_t tiles = n_tiles * ((M + bn - 1) / bn);
-  const double step = bn >= 192 ? 768.0 / 0.6 : 600.0;
-  const double t1 = (double)tiles * k_tiles * step / num_sms();
-  return t2 < t1;
+  return !(flags & (LPQT_SCHED_STREAMK | LPQT_SCHED_CLUSTER)) && M >= LPQT_PAIR_MIN_M;
 }
 
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
@@ -1934,7 +1965,7 @@ static int g_trace_n = 0;  // launches traced so far
 static int trace_next_slot() { return g_trace_n++ % kTraceSlots; }
 #endif
 
-template <int BN, bool CSK, bool RAGGED, bool FGQ = false, int WB = 6, bool PEERS = false>
+template <int BN, bool CSK, bool RAGGED, bool FGQ = false, int WB = 6, bool PEERS = false, int RB = 0>
 static int launch_impl(const Plan& p, const GemmArgs& args, const L2Prefetch& pf, const FgqArgs& fg,
                        const uint16_t* Xt, int64_t ldx,
                        int64_t M, cudaStream_t stream, int flags, const lpqt_peer_out* peers = nullptr) {
@@ -1949,7 +1980,7 @@ static int launch_impl(const Plan& p, const GemmArgs& args, const L2Prefetch& pf
           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
     return LPQT_E_INVALID_INPUT;
-  auto kern = w6a16_tcgen05_kernel<BN, CSK, RAGGED, FGQ, WB, PEERS>;
+  auto kern = w6a16_tcgen05_kernel<BN, CSK, RAGGED, FGQ, WB, PEERS, RB>;
   constexpr int smem = Cfg<BN, CSK, WB, FGQ>::kSmemBytes;
   static std::once_flag once;
   static cudaError_t attr_err = cudaSuccess;
@@ -2054,6 +2085,22 @@ static int dispatch(const Plan& p, const GemmArgs& args, const L2Prefetch& pfa, 
   }
 }
 
+// The ablation rebuilds (LPQT_REBUILD_*): decode batch tile (BN 16), CGQ FP6.
+template <int RB>
+static int dispatch_rebuild(const Plan& p, const GemmArgs& args, const L2Prefetch& pfa, const FgqArgs& fga,
+                            const uint16_t* Xt, int64_t ldx, int64_t M, cudaStream_t st, int flags) {
+  if (p.bn != 16) return LPQT_E_UNSUPPORTED;
+  bool ragged = p.k_tiles % p.kstep != 0;
+  if (p.csk) {
+    for (int r = 0; r < p.cluster; ++r)
+      ragged |= ((r + 1) * p.k_tiles / p.cluster - r * p.k_tiles / p.cluster) % p.kstep != 0;
+    return ragged ? launch_impl<16, true, true, false, 6, false, RB>(p, args, pfa, fga, Xt, ldx, M, st, flags)
+                  : launch_impl<16, true, false, false, 6, false, RB>(p, args, pfa, fga, Xt, ldx, M, st, flags);
+  }
+  return ragged ? launch_impl<16, false, true, false, 6, false, RB>(p, args, pfa, fga, Xt, ldx, M, st, flags)
+                : launch_impl<16, false, false, false, 6, false, RB>(p, args, pfa, fga, Xt, ldx, M, st, flags);
+}
+
 extern "C" {
 
 #ifdef LPQT_TRACE
@@ -2083,14 +2130,20 @@ int64_t lpqt_w6a16_workspace_bytes(int64_t M, int64_t N, int64_t K, int split_k)
   const Plan p0 = make_plan(M, N, K, split_k, 0, num_sms());
   const Plan p1 = make_plan(M, N, K, split_k, LPQT_SCHED_STREAMK, num_sms());
   // (the pair kernel's stream-K schedule: whenever the pair kernel may run)
-  const int64_t wp = split_k <= 2 && (N + kTileN - 1) / kTileN % 2 == 0 && M >= 17 ? prefill_2sm_workspace() : 0;
+  // (the pair kernel's stream-K wave, when its planner picks it — or split_k 2 forces it with LPQT_SCHED_PAIR)
+  int pair_sk = 0;
+  if ((N + kTileN - 1) / kTileN % 2 == 0 && M >= 17) {
+    if (split_k == 0) prefill_2sm_choose(M, N, K, nullptr, &pair_sk, 0);
+    if (split_k == 2) pair_sk = 1;
+  }
+  const int64_t wp = pair_sk ? prefill_2sm_workspace() : 0;
   return std::max(wp, p0.ws_bytes > p1.ws_bytes ? p0.ws_bytes : p1.ws_bytes);
 }
 
 int lpqt_w6a16_plan_ex(int64_t M, int64_t N, int64_t K, int split_k, int flags, int* out, int n_out) {
   if (M <= 0 || N <= 0 || K <= 0) return LPQT_E_SHAPE;
   if ((flags & LPQT_SCHED_STREAMK) && (flags & LPQT_SCHED_CLUSTER)) return LPQT_E_INVALID_INPUT;
-  if (pair_force(split_k, flags) >= 0 && use_pair_kernel(M, N, K, flags)) {
+  if (!(flags & LPQT_WEIGHTS_FP5) && pair_force(split_k, flags) >= 0 && use_pair_kernel(M, N, K, flags)) {
     int bn = 256, sk = 0;
     prefill_2sm_choose(M, N, K, &bn, &sk, pair_force(split_k, flags));
     const int64_t units = ((N + kTileN - 1) / kTileN / 2) * ((M + bn - 1) / bn);
@@ -2145,8 +2198,15 @@ static int w6a16_blocks_impl(const uint8_t* tiles, const uint16_t* scales, int64
                              int64_t ldx, int64_t M, int64_t N, int64_t K, void* Y, int y_dtype, int y_layout,
                              int64_t ldy, int split_k, void* workspace, int64_t workspace_bytes, int flags,
                              const lpqt_next_linear* next, void* stream, const lpqt_peer_out* po) {
-  if (flags & ~(LPQT_LAUNCH_PDL | LPQT_SCHED_STREAMK | LPQT_SCHED_CLUSTER | LPQT_SCHED_SINGLE | LPQT_SCHED_PAIR))
+  if (flags & ~(LPQT_LAUNCH_PDL | LPQT_SCHED_STREAMK | LPQT_SCHED_CLUSTER | LPQT_SCHED_SINGLE | LPQT_SCHED_PAIR |
+                LPQT_REBUILD_BIAS_SHIFT | LPQT_REBUILD_NAIVE | LPQT_WEIGHTS_FP5))
     return LPQT_E_INVALID_INPUT;
+  const int rebuild = (flags & LPQT_REBUILD_BIAS_SHIFT) ? 1 : ((flags & LPQT_REBUILD_NAIVE) ? 2 : 0);
+  const bool fp5 = (flags & LPQT_WEIGHTS_FP5) != 0;
+  if (fp5 && (rebuild || po || (block > 0 && block < K))) return LPQT_E_UNSUPPORTED;
+  if ((flags & LPQT_REBUILD_BIAS_SHIFT) && (flags & LPQT_REBUILD_NAIVE)) return LPQT_E_INVALID_INPUT;
+  if (rebuild && (block > 0 && block < K)) return LPQT_E_UNSUPPORTED;
+  if (rebuild && (po || M > 16)) return LPQT_E_UNSUPPORTED;
   // FGQ: blocks of B columns (B = K, or block <= 0: one scale per row)
   const bool fgq = block > 0 && block < K;
   if (fgq && block % kTileK != 0) return LPQT_E_UNSUPPORTED;   // block scales at 128-k tile granularity
@@ -2162,7 +2222,7 @@ static int w6a16_blocks_impl(const uint8_t* tiles, const uint16_t* scales, int64
   if (y_layout == LPQT_Y_NM ? ldy < M : ldy < N) return LPQT_E_SHAPE;
   if (split_k < 0) return LPQT_E_INVALID_INPUT;
   if (N > (int64_t)1 << 30 || M > (int64_t)1 << 30 || K > (int64_t)1 << 30) return LPQT_E_SHAPE;
-  if (!fgq && !po && pair_force(split_k, flags) >= 0 && use_pair_kernel(M, N, K, flags)) {
+  if (!fgq && !po && !fp5 && pair_force(split_k, flags) >= 0 && use_pair_kernel(M, N, K, flags)) {
     const int st = launch_prefill_2sm(tiles, scales, Xt, ldx, M, N, K, Y, y_dtype, y_layout, ldy, flags,
                                       pair_force(split_k, flags), workspace, workspace_bytes, as_stream(stream),
                                       nullptr);
@@ -2217,6 +2277,12 @@ static int w6a16_blocks_impl(const uint8_t* tiles, const uint16_t* scales, int64
     }
   }
   cudaStream_t st = as_stream(stream);
+  if (fp5) {
+    pfa = L2Prefetch{};  // (the next linear's bytes are located by the FP6 tile size)
+    return dispatch<false, 5>(p, args, pfa, fga, Xt, ldx, M, st, flags);
+  }
+  if (rebuild == 1) return dispatch_rebuild<1>(p, args, pfa, fga, Xt, ldx, M, st, flags);
+  if (rebuild == 2) return dispatch_rebuild<2>(p, args, pfa, fga, Xt, ldx, M, st, flags);
   if (po)
     return fgq ? dispatch<true, 6, true>(p, args, pfa, fga, Xt, ldx, M, st, flags, po)
                : dispatch<false, 6, true>(p, args, pfa, fga, Xt, ldx, M, st, flags, po);

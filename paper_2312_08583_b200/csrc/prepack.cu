@@ -115,6 +115,73 @@ __global__ void prepack_fp5_kernel(const uint8_t* __restrict__ seg4, const uint8
 }
 
 
+// FP5 e3m1 planes -> the native 5-bit tiles (common.cuh: 0.625 B per weight)
+__global__ void prepack_fp5n_kernel(const uint8_t* __restrict__ seg4, const uint8_t* __restrict__ seg1, int64_t N,
+                                    int64_t K, int64_t Np, int64_t Kp, uint8_t* __restrict__ tiles) {
+  const int64_t groups = Kp / 32, total = Np * groups, k_tiles = Kp / kTileK;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t n = t / groups, g = t % groups;
+    uint8_t c[32];
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+      const int64_t k = g * 32 + j, i = n * K + k;
+      c[j] = (n < N && k < K) ? static_cast<uint8_t>((((seg4[i >> 1] >> (4 * (i & 1))) & 15u) << 1) |
+                                                     ((seg1[i >> 3] >> (i & 7)) & 1u))
+                              : 0;
+    }
+    uint32_t nib[4], mw;
+    fp5x32_pack_words(c, nib, mw);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) *reinterpret_cast<uint32_t*>(tiles + tile5_word_addr(n, g, i, k_tiles)) = nib[i];
+    *reinterpret_cast<uint32_t*>(tiles + tile5_word_addr(n, g, 4, k_tiles)) = mw;
+  }
+}
+
+__device__ __forceinline__ void load_group5(const uint8_t* __restrict__ tiles, int64_t n, int64_t g, int64_t k_tiles,
+                                            uint32_t nib[4], uint32_t& mw) {
+#pragma unroll
+  for (int i = 0; i < 4; ++i) nib[i] = *reinterpret_cast<const uint32_t*>(tiles + tile5_word_addr(n, g, i, k_tiles));
+  mw = *reinterpret_cast<const uint32_t*>(tiles + tile5_word_addr(n, g, 4, k_tiles));
+}
+
+// native FP5 tiles -> row-major e3m1 codes[N, K]
+__global__ void unprepack_fp5n_kernel(const uint8_t* __restrict__ tiles, int64_t N, int64_t K, int64_t Kp,
+                                      uint8_t* __restrict__ codes) {
+  const int64_t groups = Kp / 32, total = N * groups, k_tiles = Kp / kTileK;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t n = t / groups, g = t % groups;
+    uint32_t nib[4], mw;
+    uint8_t c[32];
+    load_group5(tiles, n, g, k_tiles, nib, mw);
+    fp5x32_unpack_codes(nib, mw, c);
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+      const int64_t k = g * 32 + j;
+      if (k < K) codes[n * K + k] = c[j];
+    }
+  }
+}
+
+// native FP5 tiles -> out[N, K] binary16 = value_f16[c] * S[n] through the GEMM's rebuild
+__global__ void tiles5_dequant_kernel(const uint8_t* __restrict__ tiles, const uint16_t* __restrict__ scales,
+                                      int64_t N, int64_t K, int64_t Kp, uint16_t* __restrict__ out, ShiftMuls sm) {
+  const int64_t groups = Kp / 32, total = N * groups, k_tiles = Kp / kTileK;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t n = t / groups, g = t % groups;
+    uint32_t nib[4], mw, h[16];
+    load_group5(tiles, n, g, k_tiles, nib, mw);
+    fp5x32_cvt_f16x32(nib, mw, h, sm);
+    const __half S = __ushort_as_half(scales[n]);
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      const __half2 v = *reinterpret_cast<const __half2*>(&h[j]);
+      const int64_t k = g * 32 + 2 * j;
+      if (k < K) out[n * K + k] = __half_as_ushort(__hmul(__low2half(v), S));
+      if (k + 1 < K) out[n * K + k + 1] = __half_as_ushort(__hmul(__high2half(v), S));
+    }
+  }
+}
+
 // INT4 nibbles (row-major, two per byte, packing.py:121-129) -> INT4 tiles:
 // 128 x 128 tiles of 8192 B, [k-half 2][quad 2][row 128][16 B]; word w of a
 // (row, k-half) holds weights 8w .. 8w + 7 with weight 8w + j in nibble
@@ -235,6 +302,41 @@ int lpqt_fp5_prepack(const uint8_t* seg4, const uint8_t* seg1, int64_t N, int64_
   if (N == 0 || K == 0) return LPQT_OK;
   const int64_t Np = round_up(N, kTileN), Kp = round_up(K, kTileK);
   prepack_fp5_kernel<<<grid_for(Np * (Kp / 32), 256), 256, 0, as_stream(stream)>>>(seg4, seg1, N, K, Np, Kp, tiles);
+  note_launch();
+  return check_launch();
+}
+
+
+int64_t lpqt_fp5n_tiles_bytes(int64_t N, int64_t K) {
+  if (N <= 0 || K <= 0) return 0;
+  return round_up(N, kTileN) / kTileN * (round_up(K, kTileK) / kTileK) * kTileBytes5;
+}
+
+int lpqt_fp5n_prepack(const uint8_t* seg4, const uint8_t* seg1, int64_t N, int64_t K, uint8_t* tiles, void* stream) {
+  if (N < 0 || K < 0) return LPQT_E_SHAPE;
+  if (N == 0 || K == 0) return LPQT_OK;
+  const int64_t Np = round_up(N, kTileN), Kp = round_up(K, kTileK);
+  prepack_fp5n_kernel<<<grid_for(Np * (Kp / 32), 256), 256, 0, as_stream(stream)>>>(seg4, seg1, N, K, Np, Kp, tiles);
+  note_launch();
+  return check_launch();
+}
+
+int lpqt_fp5n_unprepack(const uint8_t* tiles, int64_t N, int64_t K, uint8_t* codes, void* stream) {
+  if (N < 0 || K < 0) return LPQT_E_SHAPE;
+  if (N == 0 || K == 0) return LPQT_OK;
+  const int64_t Kp = round_up(K, kTileK);
+  unprepack_fp5n_kernel<<<grid_for(N * (Kp / 32), 256), 256, 0, as_stream(stream)>>>(tiles, N, K, Kp, codes);
+  note_launch();
+  return check_launch();
+}
+
+int lpqt_fp5n_tiles_dequant(const uint8_t* tiles, const uint16_t* scales, int64_t N, int64_t K, uint16_t* out,
+                            void* stream) {
+  if (N < 0 || K < 0) return LPQT_E_SHAPE;
+  if (N == 0 || K == 0) return LPQT_OK;
+  const int64_t Kp = round_up(K, kTileK);
+  tiles5_dequant_kernel<<<grid_for(N * (Kp / 32), 256), 256, 0, as_stream(stream)>>>(
+      tiles, scales, N, K, Kp, out, ShiftMuls{1u << 26, 1u << 28, 1u << 30});
   note_launch();
   return check_launch();
 }

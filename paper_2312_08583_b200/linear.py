@@ -38,22 +38,29 @@ def stage_params(scales, zeros, n: int, k: int, block: int):
 
 
 def prepack(seg4, seg2, n: int, k: int, fmt: str = "fp6"):
-    """Canonical planes (CUDA uint8) -> tile layout (CUDA uint8).  fmt "fp5":
-    4 + 1 planes, converted to the FP6 tile layout (every e3m1 value is an
-    e3m2 value) — FP5 weights stream at FP6's 0.75 B per weight."""
+    """Canonical planes (CUDA uint8) -> tile layout (CUDA uint8).
+    fmt "fp6": 4 + 2 planes -> FP6 tiles (0.75 B per weight);
+    "fp5n": 4 + 1 planes -> native FP5 tiles (0.625 B per weight, CGQ GEMM);
+    "fp5": 4 + 1 planes -> FP6 tiles (every e3m1 value is an e3m2 value; the
+    FGQ FP5 GEMM streams these at 0.75 B per weight)."""
     t = _lib.torch()
-    nbytes = int(_lib.load().lpqt_fp6_tiles_bytes(n, k))
+    lib = _lib.load()
+    nbytes = int(lib.lpqt_fp5n_tiles_bytes(n, k) if fmt == "fp5n" else lib.lpqt_fp6_tiles_bytes(n, k))
     tiles = t.empty(nbytes, dtype=t.uint8, device=seg4.device)
-    fn = _lib.load().lpqt_fp5_prepack if fmt == "fp5" else _lib.load().lpqt_fp6_prepack
+    fn = {"fp6": lib.lpqt_fp6_prepack, "fp5": lib.lpqt_fp5_prepack, "fp5n": lib.lpqt_fp5n_prepack}[fmt]
     _lib.check(fn(seg4.data_ptr(), seg2.data_ptr(), n, k, tiles.data_ptr(), _lib.stream_ptr()), "prepack")
     return tiles
 
 
 class Fp6Weight:
-    """An N x K FP6 (e3m2) weight resident in HBM in the GEMM's tile layout."""
+    """An N x K FP6 (e3m2) weight resident in HBM in the GEMM's tile layout
+    (wbits 6), or an FP5 (e3m1) CGQ weight in the native 5-bit tile layout
+    (wbits 5, `lpqt_fp5n_prepack`; the GEMM runs with LPQT_WEIGHTS_FP5)."""
 
-    def __init__(self, tiles, scales, n: int, k: int, folded=None, static: bool = False, block: int = 0):
+    def __init__(self, tiles, scales, n: int, k: int, folded=None, static: bool = False, block: int = 0,
+                 wbits: int = 6):
         self.tiles = tiles
+        self.wbits = int(wbits)
         # f16 scales: one per row (CGQ, block 0; the GEMM multiplies the fp32
         # accumulator by S) or one per (row, block of `block` columns), FGQ,
         # row-major (the GEMM scales the rebuilt weights per 128-k tile)
@@ -75,10 +82,13 @@ class Fp6Weight:
     @classmethod
     def from_planes(cls, seg4, seg2, scales, n: int, k: int, folded=None, block: int = 0,
                     fmt: str = "fp6") -> "Fp6Weight":
+        cgq = not block or int(block) >= int(k)
+        if fmt == "fp5" and cgq:
+            fmt = "fp5n"  # CGQ FP5 streams its own 5-bit tiles
         tiles = prepack(seg4, seg2, n, k, fmt)
         # one-time: the weights are complete before any GEMM can overlap them
         _lib.torch().cuda.current_stream().synchronize()
-        return cls(tiles, scales, n, k, folded, static=True, block=block)
+        return cls(tiles, scales, n, k, folded, static=True, block=block, wbits=5 if fmt == "fp5n" else 6)
 
     @classmethod
     def quantize(cls, W, bias_shift: bool = True, block: int = 0) -> "Fp6Weight":
@@ -129,16 +139,20 @@ class Fp6Weight:
         return int(self.tiles.numel() + 2 * self.scales.numel())
 
     def stream_bytes(self) -> int:
-        """Algorithmic weight bytes per GEMM: 0.75 B/weight + 2 B per scale (cli.py:75-80)."""
+        """Algorithmic weight bytes per GEMM: 0.75 B/weight (FP5 native: 0.625)
+        + 2 B per scale (cli.py:75-80)."""
         nk = self.n * self.k
-        return seg4_length(nk) + _round_up((2 * nk + 7) // 8, 4) + 2 * int(self.scales.numel())
+        tail = (self.wbits - 4) * nk
+        return seg4_length(nk) + _round_up((tail + 7) // 8, 4) + 2 * int(self.scales.numel())
 
     def codes(self):
-        """Row-major codes [N, K] recovered from the tile layout (test hook)."""
+        """Row-major codes [N, K] recovered from the tile layout (test hook):
+        e3m2 codes of FP6 tiles, e3m1 codes of native FP5 tiles."""
         t = _lib.torch()
         out = t.empty((self.n, self.k), dtype=t.uint8, device=self.tiles.device)
-        _lib.check(_lib.load().lpqt_fp6_unprepack(self.tiles.data_ptr(), self.n, self.k, out.data_ptr(),
-                                                  _lib.stream_ptr()), "unprepack")
+        lib = _lib.load()
+        fn = lib.lpqt_fp5n_unprepack if self.wbits == 5 else lib.lpqt_fp6_unprepack
+        _lib.check(fn(self.tiles.data_ptr(), self.n, self.k, out.data_ptr(), _lib.stream_ptr()), "unprepack")
         return out
 
     def dequantize_f16(self):
@@ -147,6 +161,10 @@ class Fp6Weight:
         compose[c] * folded (dequant.py:82-86)."""
         t = _lib.torch()
         out = t.empty((self.n, self.k), dtype=t.float16, device=self.tiles.device)
+        if self.wbits == 5:
+            _lib.check(_lib.load().lpqt_fp5n_tiles_dequant(self.tiles.data_ptr(), self.scales.data_ptr(), self.n,
+                                                           self.k, out.data_ptr(), _lib.stream_ptr()), "tiles_dequant")
+            return out
         _lib.check(_lib.load().lpqt_fp6_tiles_dequant_blocks(self.tiles.data_ptr(), self.scales.data_ptr(), self.n,
                                                              self.k, self.block, out.data_ptr(), _lib.stream_ptr()),
                    "tiles_dequant")
@@ -219,6 +237,10 @@ class Int4Weight:
 
 
 _SCHED_FLAGS = {"auto": 0, "streamk": 2, "cluster": 4, "single": 8, "pair": 16}
+# weight rebuild in the GEMM: "cvt" = the hardware e3m2 converter (the product
+# path); "bias_shift" / "naive" = the paper's software rebuilds with the
+# per-weight binary16 scale (the Bias-Shift ablation; M <= 16)
+_REBUILD_FLAGS = {"cvt": 0, "bias_shift": 32, "naive": 64}
 
 
 def _sched_flags(sched: str) -> int:
@@ -238,7 +260,8 @@ def plan(m: int, n: int, k: int, split_k: int = 0, sched: str = "auto") -> dict:
 
 
 def _launch(weight: Fp6Weight, xt, ldx: int, m: int, y, y_dtype: int, y_layout: int, ldy: int, split_k: int,
-            sched: str = "auto", prefetch: "Fp6Weight | None" = None, prefetch_bytes: int = 0, workspace=None):
+            sched: str = "auto", prefetch: "Fp6Weight | None" = None, prefetch_bytes: int = 0, workspace=None,
+            rebuild: str = "cvt"):
     lib = _lib.load()
     ws_bytes = int(lib.lpqt_w6a16_workspace_bytes(m, weight.n, weight.k, split_k))
     if workspace is not None:
@@ -250,7 +273,11 @@ def _launch(weight: Fp6Weight, xt, ldx: int, m: int, y, y_dtype: int, y_layout: 
         ws = workspace.view(_lib.torch().uint8) if ws_bytes else None
     else:
         ws = _lib.Workspace.get(ws_bytes) if ws_bytes else None
-    flags = (_lib.LAUNCH_PDL if weight.static else 0) | _sched_flags(sched)
+    if rebuild not in _REBUILD_FLAGS:
+        raise ValueError(f"rebuild must be one of {sorted(_REBUILD_FLAGS)}")
+    flags = (_lib.LAUNCH_PDL if weight.static else 0) | _sched_flags(sched) | _REBUILD_FLAGS[rebuild]
+    if getattr(weight, "wbits", 6) == 5:
+        flags |= _lib.WEIGHTS_FP5
     if weight.block and weight.block % TILE:
         from .errors import InvalidScheme
         raise InvalidScheme(f"FGQ block_size {weight.block} is not a multiple of 128: outside the B200 GEMM path")
@@ -261,7 +288,7 @@ def _launch(weight: Fp6Weight, xt, ldx: int, m: int, y, y_dtype: int, y_layout: 
             ws.numel() if ws is not None else 0, flags, _lib.stream_ptr()), "w4a16_linear")
         return
     nxt = None
-    if prefetch is not None:
+    if prefetch is not None and getattr(prefetch, "wbits", 6) == 6:
         # the next launch is assumed to use the same batch and the automatic schedule
         nxt = _lib.NextLinear(prefetch.tiles.data_ptr(), m, prefetch.n, prefetch.k, 0, 0, int(prefetch_bytes))
     if weight.block and weight.block % TILE:
@@ -307,7 +334,7 @@ def workspace_bytes(m: int, weight, split_k: int = 0) -> int:
 
 
 def w6a16_linear(x, weight: Fp6Weight, out=None, out_dtype=None, split_k: int = 0, sched: str = "auto",
-                 prefetch: "Fp6Weight | None" = None, prefetch_bytes: int = 0, workspace=None):
+                 prefetch: "Fp6Weight | None" = None, prefetch_bytes: int = 0, workspace=None, rebuild: str = "cvt"):
     """y = x @ W_hat^T for x[..., K] (CUDA, fp16 preferred) -> y[..., N].
 
     x is the K-major B operand as is when it is contiguous fp16 with K % 8 ==
@@ -318,6 +345,9 @@ def w6a16_linear(x, weight: Fp6Weight, out=None, out_dtype=None, split_k: int = 
     launch's drain pulls its first bytes into L2 (lpqt_w6a16_linear_pf).
     workspace: optional caller-owned zeroed uint8 CUDA buffer of at least
     `workspace_bytes(m, weight)` bytes (default: one per stream, _lib.Workspace).
+    rebuild: "cvt" (default, hardware e3m2 converter, S applied in fp32 after
+    the contraction) or the paper's ablation rebuilds "bias_shift" / "naive"
+    (software rebuild x per-weight binary16 scale; CGQ FP6, M <= 16).
     """
     t = _lib.torch()
     if x.shape[-1] != weight.k:
@@ -356,7 +386,7 @@ def w6a16_linear(x, weight: Fp6Weight, out=None, out_dtype=None, split_k: int = 
             y.zero_()
         else:
             _launch(weight, x2, ldx, m, y, codes[odt], _lib.Y_MN, weight.n, split_k, sched, prefetch,
-                    prefetch_bytes, workspace)
+                    prefetch_bytes, workspace, rebuild)
     return y.reshape(*lead, weight.n)
 
 

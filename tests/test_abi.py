@@ -73,8 +73,14 @@ def test_host_errors_without_launch(lib):
     assert st == _lib.E_SHAPE          # ldx % 8 != 0
     st = lib.lpqt_w6a16_linear_ex(None, None, None, 8, 1, 128, 8, None, 9, _lib.Y_NM, 1, 0, None, 0, 0, None)
     assert st == _lib.E_UNSUPPORTED    # bad y dtype
-    st = lib.lpqt_w6a16_linear_ex(None, None, None, 8, 1, 128, 8, None, _lib.F32, _lib.Y_NM, 1, 0, None, 0, 64, None)
+    st = lib.lpqt_w6a16_linear_ex(None, None, None, 8, 1, 128, 8, None, _lib.F32, _lib.Y_NM, 1, 0, None, 0, 4096, None)
     assert st == _lib.E_INVALID_INPUT  # unknown flag
+    st = lib.lpqt_w6a16_linear_ex(None, None, None, 8, 1, 128, 8, None, _lib.F32, _lib.Y_NM, 1, 0, None, 0, 32 | 64, None)
+    assert st == _lib.E_INVALID_INPUT  # both ablation rebuilds
+    st = lib.lpqt_w6a16_linear_ex(None, None, None, 8, 17, 128, 8, None, _lib.F32, _lib.Y_NM, 17, 0, None, 0, 64, None)
+    assert st == _lib.E_UNSUPPORTED    # ablation rebuilds are decode-only (M <= 16)
+    st = lib.lpqt_w6a16_linear_ex(None, None, None, 8, 1, 128, 8, None, _lib.F32, _lib.Y_NM, 1, 0, None, 0, 128 | 32, None)
+    assert st == _lib.E_UNSUPPORTED    # native FP5 tiles run the hardware rebuild only
     assert lib.lpqt_w6a16_linear(None, None, None, 8, 0, 128, 8, None, _lib.F32, _lib.Y_NM, 1, 0, None, 0,
                                  None) == _lib.OK  # M == 0: nothing to do
 
