@@ -187,29 +187,34 @@ __device__ __forceinline__ void fp6x32_soft_f16x32(const uint32_t w[6], uint32_t
 }
 
 // FP5 native rebuild (layout above): 32 weights -> 16 half2 of the exact
-// binary16 values, k ascending.  Shifts on the FMA pipe (IMAD / IMAD.HI with
-// kernel-argument multipliers, sm.m26 = 2^26 etc.; pass plain powers of two).
-template <int S>
-__device__ __forceinline__ uint32_t mant_bits(uint32_t mw, const ShiftMuls& sm) {
-  // mantissa bit of byte t at bit 8t + S -> bit 8t + 1
-  if constexpr (S == 0) return mw * 2u;
-  else if constexpr (S == 1) return mw;
-  else if constexpr (S == 3) return __umulhi(mw, sm.m30);  // >> 2
-  else if constexpr (S == 5) return __umulhi(mw, sm.m28);  // >> 4
-  else if constexpr (S == 7) return __umulhi(mw, sm.m26);  // >> 6
-  else return mw >> (S - 1);
+// binary16 values, k ascending.  The mantissa word is split by bit parity once
+// (Me = even bit positions, Mo = odd): group s shifted so its bits land on
+// bit 1 of every byte then has a ZERO bit 0 (that bit comes from a position of
+// the other parity), so one LOP3 (lo & 0x3C..) | (u & ~0x3C..) merges nibble
+// and mantissa (bits 6-7 are ignored by the converter).  Shifts run on the
+// FMA pipe (IMAD / IMAD.HI by register multipliers: sm.m26 = 2^26 etc.).
+__device__ __forceinline__ uint32_t lop3_3c(uint32_t lo, uint32_t u) {
+  uint32_t d;  // (lo & 0x3C3C3C3C) | (u & ~0x3C3C3C3C)
+  asm("lop3.b32 %0, %1, %2, %3, 0xE4;" : "=r"(d) : "r"(lo), "r"(u), "n"(0x3C3C3C3C));
+  return d;
 }
 __device__ __forceinline__ void fp5x32_cvt_f16x32(const uint32_t nib[4], uint32_t mw, uint32_t out[16],
                                                   const ShiftMuls& sm) {
-  uint32_t m[8];
-  m[0] = mant_bits<0>(mw, sm); m[1] = mant_bits<1>(mw, sm); m[2] = mant_bits<2>(mw, sm);
-  m[3] = mant_bits<3>(mw, sm); m[4] = mant_bits<4>(mw, sm); m[5] = mant_bits<5>(mw, sm);
-  m[6] = mant_bits<6>(mw, sm); m[7] = mant_bits<7>(mw, sm);
+  const uint32_t me = mw & 0x55555555u, mo = mw & 0xAAAAAAAAu;
+  const uint32_t two = sm.m26 >> 25, four = sm.m26 >> 24;  // registers: IMAD, not SHF
+  uint32_t u[8];  // group s = 2i + p: mantissa of byte t at bit 8t + 1
+  u[0] = me * two;                  // << 1
+  u[1] = mo;                        // bit 8t + 1 already
+  u[2] = me >> 1;
+  u[3] = __umulhi(mo, 1u << 30);    // >> 2
+  u[4] = __umulhi(me, 1u << 29);    // >> 3
+  u[5] = __umulhi(mo, sm.m28);      // >> 4
+  u[6] = __umulhi(me, 1u << 27);    // >> 5
+  u[7] = __umulhi(mo, sm.m26);      // >> 6
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
-    const uint32_t lo = nib[i] * 4u, hi = __umulhi(nib[i], sm.m30);  // << 2 (even nibbles), >> 2 (odd)
-    const uint32_t x0 = (lo & 0x3C3C3C3Cu) | (m[2 * i] & 0x02020202u);
-    const uint32_t x1 = (hi & 0x3C3C3C3Cu) | (m[2 * i + 1] & 0x02020202u);
+    const uint32_t lo = nib[i] * four, hi = __umulhi(nib[i], sm.m30);  // << 2 (even nibbles), >> 2 (odd)
+    const uint32_t x0 = lop3_3c(lo, u[2 * i]), x1 = lop3_3c(hi, u[2 * i + 1]);
     out[4 * i] = cvt_e3m2x2_lo(x0);
     out[4 * i + 1] = cvt_e3m2x2_hi(x0);
     out[4 * i + 2] = cvt_e3m2x2_lo(x1);

@@ -107,7 +107,12 @@ struct GemmArgs {
 // its row's parameter with one LDS; the rebuilt f16 weight carries the block
 // scale (the binary16 dequant of dequant.py:72-79) and the epilogue applies none.
 struct FgqArgs {
-  const uint8_t* stage;  // stage-ordered block parameters (null: CGQ FP6)
+  const uint8_t* stage;    // stage-ordered block parameters (null: CGQ FP6, sub-tile FGQ)
+  // sub-tile FGQ x FP6 (block B | 128, B % 16 == 0; decode widths): `sub` =
+  // 128 / B partials per 128-k tile, each scaled in fp32 by its block's raw
+  // f16 scale (row-major, `bpr` per row) read by the epilogue — gemm.py:96-110
+  const uint16_t* scales;
+  int sub, bpr;
 };
 // INT4 rebuild, 64 weights (8 words; nibble p of word w holds weight
 // 8w + 2(p & 3) + (p >> 2)): OR the nibble pair into the mantissa of
@@ -182,7 +187,9 @@ struct L2Prefetch {
 #ifndef LPQT_PD_WAIT
 #define LPQT_PD_WAIT 0     // the epilogue's partial-ready wait mode (see mbar_try_wait)
 #endif
-template <int BN, bool CSK, int WB = 6, bool FGQ = false>
+// FGQ: 0 = CGQ, 1 = block scales per 128-k tile (stage-ordered), 2 = blocks of
+// 16 / 32 / 64 (decode widths, FgqArgs::sub)
+template <int BN, bool CSK, int WB = 6, int FGQ = 0>
 struct Cfg {
   static constexpr int kTileB = WB == 6 ? kTileBytes : (WB == 5 ? kTileBytes5 : kTileN * kTileK / 2);
   // FGQ x FP6 at decode shapes (BN <= 32): "per-block partials" — every 128-k
@@ -204,7 +211,10 @@ struct Cfg {
   static constexpr int kXStageBytes = kKStep * kXTileBytes;
   // prefill (BN = 256): an X stage is 64 KB and covers ~1000 MMA cycles, so
   // three stages keep the L2 latency of X hidden (2 W stages of 12 KB suffice)
-  static constexpr int kXStages = BN <= 16 ? (CSK ? 4 : 6) : (BN <= 128 ? 4 : (BN == 192 ? LPQT_PREFILL_XSTAGES : 3));
+  // (native FP5 at BN 16: 4 X stages leave room for 8 W stages of 20 KB — bytes
+  // in flight per SM are what bound the decode stream)
+  static constexpr int kXStages =
+      BN <= 16 ? (CSK || WB == 5 ? 4 : 6) : (BN <= 128 ? 4 : (BN == 192 ? LPQT_PREFILL_XSTAGES : 3));
   // CSK: two partial staging buffers of 128 x BN fp32 (rounds alternate)
   static constexpr int kStageBufBytes = CSK ? kTileN * BN * 4 : 0;
   // decode: output tiles staged in smem (two 128 x BN buffers, fp32-sized) and
@@ -667,7 +677,7 @@ __device__ __forceinline__ void ystage_put(const GemmArgs& a, uint32_t buf, int 
 // RB: weight rebuild — 0 the hardware e3m2 converter (the product path);
 // 1 / 2 the paper's software bias-shift / naive rebuilds x the per-row scale
 // in binary16 (the ablation kernels, common.cuh fp6x32_soft_f16x32)
-template <int BN, bool CSK, bool RAGGED, bool FGQ = false, int WB = 6, bool PEERS = false, int RB = 0>
+template <int BN, bool CSK, bool RAGGED, int FGQ = 0, int WB = 6, bool PEERS = false, int RB = 0>
 __global__ void __launch_bounds__(kThreads, 1)
     w6a16_tcgen05_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constant__ CUtensorMap tmap_y,
                          const GemmArgs a, const L2Prefetch pf, const FgqArgs fg,
@@ -733,9 +743,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint8_t* src = a.tiles + ((int64_t)n_tile * a.k_tiles + kt) * C::kTileB;
     const uint32_t bytes = static_cast<uint32_t>(nt * C::kTileB);
     const uint32_t e = elect_one();
-    mbar_arrive_expect_tx_if(e, &full_w[s], bytes + static_cast<uint32_t>(nt * C::kSBytes));
+    const uint32_t pbytes = FGQ == 2 ? 0u : static_cast<uint32_t>(nt * C::kSBytes);
+    mbar_arrive_expect_tx_if(e, &full_w[s], bytes + pbytes);
     bulk_g2s_if(e, smem_w + s * C::kWStageBytes, src, bytes, &full_w[s], w_pol);
-    if constexpr (FGQ) {
+    if (FGQ && pbytes) {
       const uint8_t* sp = fg.stage + ((int64_t)n_tile * a.k_tiles + kt) * C::kSBytes;
       bulk_g2s_if(e, smem_w + s * C::kWStageBytes + KS * C::kTileB, sp, static_cast<uint32_t>(nt * C::kSBytes),
                   &full_w[s], w_pol);
@@ -1019,7 +1030,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
           tmem_st_x32(ta + h * 32, r);
         }
-        if constexpr (C::kPD) {
+        if constexpr (C::kPD && FGQ != 2) {
           // this row's block scale of tile ordinal q, for the epilogue (fp32)
           const uint32_t q = static_cast<uint32_t>(KS * i + (KS == 2 ? tl : 0));
           tmem_st_x1(t_row + C::kACols + C::kDBufs * C::kDCols + C::kPSlots * BN + (q & 31u),
@@ -1055,7 +1066,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     // that were written.
     setmaxnreg_dec<48>();
     const int mw = warp - kWarpMma0;
-    if (mw < C::kMmaWarps) {
+    // sub-tile FGQ: ONE issuer takes every stage — a tile's 128 / B partials
+    // would let two issuers on alternate stages run more than kPSlots
+    // ordinals ahead of the in-order epilogue (parity waits could alias)
+    constexpr int issuers = FGQ == 2 ? 1 : C::kMmaWarps;
+    if (mw < issuers) {
       constexpr uint32_t idesc = idesc_f16_m128(BN);
       Seg sg;
       int lu = 0;
@@ -1067,8 +1082,8 @@ __global__ void __launch_bounds__(kThreads, 1)
           tc_fence_after();
         }
         const uint32_t d_tmem = tmem_d0 + d * C::kDCols + mw * BN;
-        const int s_first = C::kMmaWarps == 2 ? ((mw - sg.i0) & 1) : 0;
-        for (int s = s_first; s < sg.len; s += C::kMmaWarps) {
+        const int s_first = issuers == 2 ? ((mw - sg.i0) & 1) : 0;
+        for (int s = s_first; s < sg.len; s += issuers) {
           const int it = sg.i0 + s;
           const int kt = sg.kt0 + s * KS;
           const int nt = min(KS, sg.kt1 - kt);
@@ -1092,13 +1107,34 @@ __global__ void __launch_bounds__(kThreads, 1)
             if constexpr (C::kTileRing) {
               // position 2 * (it >> 1) + t of this issuer's 3-slot ring
               const int pos = 2 * (it >> 1) + t, sl = pos % 3;
-              tb = mw * 3 + sl;
+              tb = (it & 1) * 3 + sl;  // (the ring of the stage's dequant group)
               mbar_wait<WM>(&afull[tb], (pos / 3) & 1);
               tc_fence_after();
               ta_t = tmem_base + tb * kAColsPerBuf;
             }
             if (t < nt) {
-              if constexpr (C::kPD) {
+              if constexpr (C::kPD && FGQ == 2) {
+                // partial ordinal q = (KS * stage + t) * P + p: a fresh partial in
+                // slot q % kPSlots for each of the tile's P = 128 / B blocks, each
+                // of 8 / P MMAs of K = 16 (one issuer: ordinals in order)
+                const int P = fg.sub, cpp = (kTileK / 16) / P;
+                int ps = 0;
+#pragma unroll
+                for (int j = 0; j < kTileK / 16; ++j) {
+                  const bool p0 = (j & (cpp - 1)) == 0;
+                  if (p0) {
+                    if (j) tc_commit_if(e, &pfull[ps]);
+                    const int q = (KS * it + t) * P + j / cpp;
+                    ps = q % C::kPSlots;
+                    mbar_wait<WM>(&pempty[ps], ((q / C::kPSlots) & 1) ^ 1);
+                    tc_fence_after();
+                  }
+                  const uint32_t p_tmem = tmem_d0 + C::kDBufs * C::kDCols + ps * BN;
+                  const uint32_t off = (t * C::kXTileBytes + (j >> 2) * (BN * 128) + (j & 3) * 32) >> 4;
+                  mma_f16_ts_if(e, p_tmem, ta_t + j * 8, bd_lo + off, bd_hi, idesc, p0 ? 0u : 1u);
+                }
+                tc_commit_if(e, &pfull[ps]);
+              } else if constexpr (C::kPD) {
                 // k-tile ordinal q = KS * stage + t: a fresh partial in slot q % kPSlots
                 // (with two issuers on alternate stages each slot keeps its issuer)
                 const int q = KS * it + t, ps = q % C::kPSlots;
@@ -1152,10 +1188,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       int nt, mt;
       tile_nm(a, g.tile, nt, mt);
       const int nn = nt * kTileN + rr;
-      if constexpr (FGQ && WB == 6)
+      if constexpr (FGQ && WB == 6) {
+        if constexpr (FGQ == 2) return nn < a.N ? 1.f : 0.f;  // (raw block scales, applied per partial)
         return nn < a.N ? __ldg(reinterpret_cast<const float*>(fg.stage + (int64_t)a.n_tiles * a.k_tiles * kTileN * 2) +
                                 nn)
                         : 0.f;
+      }
       if constexpr (FGQ || RB > 0) return nn < a.N ? 1.f : 0.f;  // (the scale is in A)
       return nn < a.N ? __half2float(__ushort_as_half(__ldg(a.scales + nn))) : 0.f;
     };
@@ -1359,24 +1397,53 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
           for (int t = 0; t < KS; ++t) {
             if (t < nt) {
-              const int q = KS * i + t, ps = q % C::kPSlots;
-              mbar_wait<LPQT_PD_WAIT>(&pfull[ps], (q / C::kPSlots) & 1);
-              tc_fence_after();
-              uint32_t sv;
-              tmem_ld_x1(t_sc + (q & 31), sv);
+              if constexpr (FGQ == 2) {
+                const int P = fg.sub;
+                int n_tile, m_tile;
+                tile_nm(a, sg.tile, n_tile, m_tile);
+                const int nn = n_tile * kTileN + rr;
+#pragma unroll 1
+                for (int p = 0; p < P; ++p) {
+                  const int q = (KS * i + t) * P + p, ps = q % C::kPSlots, blk = (kt + t) * P + p;
+                  // this row's raw block scale (the load overlaps the partial wait)
+                  const float scl = nn < a.N && blk < fg.bpr
+                                        ? __half2float(__ushort_as_half(__ldg(fg.scales + (int64_t)nn * fg.bpr + blk)))
+                                        : 0.f;
+                  mbar_wait<LPQT_PD_WAIT>(&pfull[ps], (q / C::kPSlots) & 1);
+                  tc_fence_after();
 #pragma unroll
-              for (int c0 = 0; c0 < BN; c0 += 16) {
-                uint32_t v[16];
-                tmem_ld_x16(t_p + ps * BN + c0, v);
-                tmem_wait_ld();
-                const float scl = __uint_as_float(sv);
+                  for (int c0 = 0; c0 < BN; c0 += 16) {
+                    uint32_t v[16];
+                    tmem_ld_x16(t_p + ps * BN + c0, v);
+                    tmem_wait_ld();
 #pragma unroll
-                for (int j = 0; j < 16; ++j)
-                  pacc[c0 + j] = __fadd_rn(pacc[c0 + j], __fmul_rn(scl, __uint_as_float(v[j])));
+                    for (int j = 0; j < 16; ++j)
+                      pacc[c0 + j] = __fadd_rn(pacc[c0 + j], __fmul_rn(scl, __uint_as_float(v[j])));
+                  }
+                  tc_fence_before();
+                  __syncwarp();
+                  if (lane == 0) mbar_arrive(&pempty[ps]);
+                }
+              } else {
+                const int q = KS * i + t, ps = q % C::kPSlots;
+                mbar_wait<LPQT_PD_WAIT>(&pfull[ps], (q / C::kPSlots) & 1);
+                tc_fence_after();
+                uint32_t sv;
+                tmem_ld_x1(t_sc + (q & 31), sv);
+#pragma unroll
+                for (int c0 = 0; c0 < BN; c0 += 16) {
+                  uint32_t v[16];
+                  tmem_ld_x16(t_p + ps * BN + c0, v);
+                  tmem_wait_ld();
+                  const float scl = __uint_as_float(sv);
+#pragma unroll
+                  for (int j = 0; j < 16; ++j)
+                    pacc[c0 + j] = __fadd_rn(pacc[c0 + j], __fmul_rn(scl, __uint_as_float(v[j])));
+                }
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&pempty[ps]);
               }
-              tc_fence_before();
-              __syncwarp();
-              if (lane == 0) mbar_arrive(&pempty[ps]);
             }
           }
         }
@@ -1965,7 +2032,7 @@ static int g_trace_n = 0;  // launches traced so far
 static int trace_next_slot() { return g_trace_n++ % kTraceSlots; }
 #endif
 
-template <int BN, bool CSK, bool RAGGED, bool FGQ = false, int WB = 6, bool PEERS = false, int RB = 0>
+template <int BN, bool CSK, bool RAGGED, int FGQ = 0, int WB = 6, bool PEERS = false, int RB = 0>
 static int launch_impl(const Plan& p, const GemmArgs& args, const L2Prefetch& pf, const FgqArgs& fg,
                        const uint16_t* Xt, int64_t ldx,
                        int64_t M, cudaStream_t stream, int flags, const lpqt_peer_out* peers = nullptr) {
@@ -2055,7 +2122,7 @@ static int launch_impl(const Plan& p, const GemmArgs& args, const L2Prefetch& pf
 using namespace lpqt;
 
 // Schedule / stage-shape dispatch shared by the FP6 (CGQ, FGQ) and INT4 entries.
-template <bool FGQ, int WB, bool PEERS = false>
+template <int FGQ, int WB, bool PEERS = false>
 static int dispatch(const Plan& p, const GemmArgs& args, const L2Prefetch& pfa, const FgqArgs& fga,
                     const uint16_t* Xt, int64_t ldx, int64_t M, cudaStream_t st, int flags,
                     const lpqt_peer_out* po = nullptr) {
@@ -2068,6 +2135,14 @@ static int dispatch(const Plan& p, const GemmArgs& args, const L2Prefetch& pfa, 
                     : launch_impl<16, true, false, FGQ, WB, PEERS>(p, args, pfa, fga, Xt, ldx, M, st, flags, po);
     return ragged ? launch_impl<32, true, true, FGQ, WB, PEERS>(p, args, pfa, fga, Xt, ldx, M, st, flags, po)
                   : launch_impl<32, true, false, FGQ, WB, PEERS>(p, args, pfa, fga, Xt, ldx, M, st, flags, po);
+  }
+  if constexpr (FGQ == 2) {  // (sub-tile FGQ blocks: decode widths only)
+    if (p.bn > 32) return LPQT_E_UNSUPPORTED;
+    if (p.bn <= 16)
+      return ragged ? launch_impl<16, false, true, FGQ, WB, PEERS>(p, args, pfa, fga, Xt, ldx, M, st, flags, po)
+                    : launch_impl<16, false, false, FGQ, WB, PEERS>(p, args, pfa, fga, Xt, ldx, M, st, flags, po);
+    return ragged ? launch_impl<32, false, true, FGQ, WB, PEERS>(p, args, pfa, fga, Xt, ldx, M, st, flags, po)
+                  : launch_impl<32, false, false, FGQ, WB, PEERS>(p, args, pfa, fga, Xt, ldx, M, st, flags, po);
   }
   switch (p.bn) {
     case 16:
@@ -2209,9 +2284,18 @@ static int w6a16_blocks_impl(const uint8_t* tiles, const uint16_t* scales, int64
   if (rebuild && (po || M > 16)) return LPQT_E_UNSUPPORTED;
   // FGQ: blocks of B columns (B = K, or block <= 0: one scale per row)
   const bool fgq = block > 0 && block < K;
-  if (fgq && block % kTileK != 0) return LPQT_E_UNSUPPORTED;   // block scales at 128-k tile granularity
+  // block scales at 128-k tile granularity (stage-ordered), or — decode widths
+  // (M <= 32) — blocks of 16 / 32 / 64 columns with raw row-major scales
+  const bool fgq_sub = fgq && block % kTileK != 0;
+  if (fgq_sub && (block % 16 != 0 || kTileK % block != 0 || M > 32)) return LPQT_E_UNSUPPORTED;
   FgqArgs fga{};
-  if (fgq) fga.stage = reinterpret_cast<const uint8_t*>(scales);  // stage-ordered (lpqt_fgq_stage_params)
+  if (fgq_sub) {
+    fga.scales = scales;
+    fga.sub = static_cast<int>(kTileK / block);
+    fga.bpr = static_cast<int>((K + block - 1) / block);
+  } else if (fgq) {
+    fga.stage = reinterpret_cast<const uint8_t*>(scales);  // stage-ordered (lpqt_fgq_stage_params)
+  }
   if ((flags & LPQT_SCHED_STREAMK) && (flags & LPQT_SCHED_CLUSTER)) return LPQT_E_INVALID_INPUT;
   if (M < 0 || N < 0 || K < 0) return LPQT_E_SHAPE;
   if (M == 0 || N == 0) return LPQT_OK;
@@ -2283,6 +2367,10 @@ static int w6a16_blocks_impl(const uint8_t* tiles, const uint16_t* scales, int64
   }
   if (rebuild == 1) return dispatch_rebuild<1>(p, args, pfa, fga, Xt, ldx, M, st, flags);
   if (rebuild == 2) return dispatch_rebuild<2>(p, args, pfa, fga, Xt, ldx, M, st, flags);
+  if (fgq_sub) {
+    if (po) return LPQT_E_UNSUPPORTED;
+    return dispatch<2, 6>(p, args, pfa, fga, Xt, ldx, M, st, flags);
+  }
   if (po)
     return fgq ? dispatch<true, 6, true>(p, args, pfa, fga, Xt, ldx, M, st, flags, po)
                : dispatch<false, 6, true>(p, args, pfa, fga, Xt, ldx, M, st, flags, po);

@@ -25,6 +25,12 @@ def _round_up(x: int, m: int) -> int:
     return (x + m - 1) // m * m
 
 
+def sub_tile_block(block: int) -> bool:
+    """FGQ blocks narrower than a 128-k tile that the decode GEMM scales per
+    block partial (16 / 32 / 64 columns; gemm.py:96-110 order)."""
+    return bool(block) and block % 16 == 0 and TILE % block == 0
+
+
 def stage_params(scales, zeros, n: int, k: int, block: int):
     """Row-major per-block f16 scales (and INT4 zero points) -> the GEMM's
     stage-ordered block parameters (`lpqt_fgq_stage_params`): built once per
@@ -129,9 +135,10 @@ class Fp6Weight:
         return w
 
     def gemm_scales(self):
-        """The scale operand of the GEMM: the per-row scales (CGQ) or the
-        stage-ordered block scales (FGQ)."""
-        return self._stage if self.block else self.scales
+        """The scale operand of the GEMM: the per-row scales (CGQ), the
+        stage-ordered block scales (FGQ, whole tiles) or the row-major block
+        scales (FGQ blocks of 16 / 32 / 64)."""
+        return self._stage if self._stage is not None else self.scales
 
     # -- inspection -----------------------------------------------------------
     @property
@@ -278,9 +285,11 @@ def _launch(weight: Fp6Weight, xt, ldx: int, m: int, y, y_dtype: int, y_layout: 
     flags = (_lib.LAUNCH_PDL if weight.static else 0) | _sched_flags(sched) | _REBUILD_FLAGS[rebuild]
     if getattr(weight, "wbits", 6) == 5:
         flags |= _lib.WEIGHTS_FP5
-    if weight.block and weight.block % TILE:
+    if weight.block and weight.block % TILE and (isinstance(weight, Int4Weight) or not sub_tile_block(weight.block)
+                                                 or m > 32):
         from .errors import InvalidScheme
-        raise InvalidScheme(f"FGQ block_size {weight.block} is not a multiple of 128: outside the B200 GEMM path")
+        raise InvalidScheme(f"FGQ block_size {weight.block}: the B200 GEMM takes multiples of 128, or 16 / 32 / 64 "
+                            f"at decode batches (M <= 32, FP6)")
     if isinstance(weight, Int4Weight):
         _lib.check(lib.lpqt_w4a16_linear_blocks(
             weight.tiles.data_ptr(), weight.params.data_ptr(), weight.block, xt.data_ptr(),
@@ -291,9 +300,6 @@ def _launch(weight: Fp6Weight, xt, ldx: int, m: int, y, y_dtype: int, y_layout: 
     if prefetch is not None and getattr(prefetch, "wbits", 6) == 6:
         # the next launch is assumed to use the same batch and the automatic schedule
         nxt = _lib.NextLinear(prefetch.tiles.data_ptr(), m, prefetch.n, prefetch.k, 0, 0, int(prefetch_bytes))
-    if weight.block and weight.block % TILE:
-        from .errors import InvalidScheme
-        raise InvalidScheme(f"FGQ block_size {weight.block} is not a multiple of 128: outside the B200 GEMM path")
     _lib.check(lib.lpqt_w6a16_linear_blocks(
         weight.tiles.data_ptr(), weight.gemm_scales().data_ptr(), weight.block, xt.data_ptr(), ldx, m, weight.n,
         weight.k,

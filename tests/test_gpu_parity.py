@@ -766,3 +766,33 @@ def test_random_shape_fuzz():
         assert torch.equal(y, L.w6a16_linear(x, w, out_dtype=torch.float32)), (n, k, m, block)
         ref = x.double() @ w.dequantize_f16().double().t()
         assert normwise_rel(y.cpu().numpy(), ref.cpu().numpy()) <= REL_TOL, (n, k, m, block)
+
+
+@pytest.mark.parametrize("m", [1, 8, 16, 32])
+@pytest.mark.parametrize("n,k,block", [(512, 1024, 64), (384, 1000, 32), (256, 2048, 16), (1024, 4096, 64)])
+def test_fgq_sub_tile_blocks_vs_oracle(n, k, block, m):
+    """FGQ blocks narrower than a 128-k tile (16 / 32 / 64 columns) at decode
+    widths: one tensor-core partial per block, scaled by the block's raw f16
+    scale in fp32 and summed in k order (the reference's FGQ loop,
+    gemm.py:96-110).  Block magnitudes 1e-6 .. 1 inside every row; checked
+    elementwise per row against the oracle's block-partial GEMM on the same
+    fp16 activations, and bit-identical across stream-K / cluster schedules
+    is not required (fp32 summation order) but within 1e-5 normwise."""
+    rng = np.random.default_rng(n + k + block + m)
+    nb = -(-k // block)
+    mag = 10.0 ** rng.uniform(-6, 0, size=(n, nb))
+    Wn = rng.standard_normal((n, k)) * np.repeat(mag, block, axis=1)[:, :k]
+    w = L.Fp6Weight.quantize(torch.from_numpy(Wn.astype(np.float32)).cuda(), block=block)
+    o = O.quantize_tensor_fgq(Wn.astype(np.float32), block, True)
+    assert np.array_equal(w.codes().cpu().numpy().ravel(), o["codes"])
+    x = torch.randn(m, k, device="cuda", generator=torch.Generator(device="cuda").manual_seed(m)).half()
+    X = x.t().float().cpu().numpy()
+    Yo = O.gemm_quantized_fgq(o["codes"], o["scales"], n, k, block, X).astype(np.float64)
+    # the reference's own f32 bound (gemm.py:118-122) per row: 4 eps32 K max_row|W_hat| max|X|
+    W_hat = O.value_table()[o["codes"].reshape(n, k)] * O.block_scale_per_element(o["scales"], n, k, block)
+    tol = 4 * np.finfo(np.float32).eps * k * np.abs(W_hat).max(axis=1, keepdims=True) * np.abs(X).max()
+    for sched in ("auto", "streamk", "cluster"):
+        y = L.w6a16_linear(x, w, out_dtype=torch.float32, sched=sched).t().cpu().numpy().astype(np.float64)
+        assert np.all(np.abs(y - Yo) <= tol), sched
+    with pytest.raises(L.InvalidScheme):   # prefill widths keep whole-tile blocks
+        L.w6a16_linear(torch.zeros(33, k, device="cuda").half(), w)
