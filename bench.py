@@ -223,7 +223,7 @@ def run_ours(args, world, rank, layers, m, e2e=True, burn_in=None):
         # programmatic dependent launch: the weights are static, so each GEMM
         # streams its weight tiles while the previous layer's kernel drains;
         # and its drain pulls the next linear's first weight bytes into L2
-        pf = None if nxt is None else _lib.NextLinear(nxt.tiles.data_ptr(), m, nxt.n, nxt.k, 0, 0, 0)
+        pf = None if nxt is None else _lib.NextLinear(nxt.tiles.data_ptr(), m, nxt.n, nxt.k, 0, 0, args.pf_bytes)
         _lib.check(lib.lpqt_w6a16_linear_pf(w.tiles.data_ptr(), w.scales.data_ptr(), xts[i].data_ptr(), w.k, m,
                                             w.n, w.k, ys[i].data_ptr(), _lib.F16, _lib.Y_NM, m, 0, _lib.ptr(ws),
                                             ws.numel() if ws is not None else 0, _lib.LAUNCH_PDL,
@@ -630,6 +630,7 @@ def main():
     ap.add_argument("--no-extras", action="store_true", help="skip the extra M=1 / 7B lines")
     ap.add_argument("--graph-steps", type=int, default=8, help="steps per replayed CUDA graph")
     ap.add_argument("--no-l2-next", action="store_true", help="no next-linear L2 prefetch hint")
+    ap.add_argument("--pf-bytes", type=int, default=0, help="next-linear L2 prefetch bytes per CTA (0: 64 KiB)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 

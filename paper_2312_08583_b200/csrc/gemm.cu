@@ -756,7 +756,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #ifndef LPQT_W_PROLOGUE
 #define LPQT_W_PROLOGUE 0  // measured slower (5-12 %, profiles/r02_abx_w_prologue.jsonl)
 #endif
-  const int w_pro = LPQT_W_PROLOGUE ? min(C::kWStages, n_st) : 0;
+  const int w_pro = min(LPQT_W_PROLOGUE < 0 ? C::kWStages : LPQT_W_PROLOGUE, n_st);
   if (warp == kWarpTmaW) {
     if (lane == 0) {
       for (int s = 0; s < C::kWStages; ++s) {
