@@ -127,5 +127,6 @@ def test_bench_preset_smoke(capsys):
     assert rc == 0
     lines = [ln for ln in so.splitlines() if ln.startswith("path=")]
     assert [ln.split()[0] for ln in lines] == ["path=fp16_dense", "path=fp6_naive", "path=fp6_bias_shift",
-                                               "path=int4_fgq", "path=fp6_w6a16"]
+                                               "path=int4_fgq", "path=fp6_w6a16", "path=fp6_w6a16_naive",
+                                               "path=fp6_w6a16_bias_shift"]
     assert "weight_bytes=8465152" in lines[1]   # 5504 x 2048 x 0.75 + 2 x 5504
