@@ -94,7 +94,6 @@ struct GemmArgs {
   int n_fastest;      // tile index order: 0 = batch tile fastest, 1 = weight-row tile fastest
   int y_tma;          // Y tiles leave through the TMA tensor store (tmap_y valid)
   int dp;             // prefill (BN >= 64): whole tiles round-robin, CTA c takes c, c + grid, ...
-  int ramp;           // SK: LPQT_SK_RAMP of this launch (0: equal ranges)
   ShiftMuls sm;       // 2^26, 2^28, 2^30: right shifts on the FMA pipe (common.cuh)
 };
 
@@ -165,7 +164,7 @@ __device__ __forceinline__ void scale_f16x2(uint32_t (&r)[32], uint32_t s2) {
 struct L2Prefetch {
   const uint8_t* base;
   int64_t total, bytes;
-  int count, ksteps, kstep, k_tiles, c, tiles, ramp;
+  int count, ksteps, kstep, k_tiles, c, tiles;
   uint32_t chunk;
 };
 
@@ -300,30 +299,12 @@ struct Seg {
 };
 
 // ---- stream-K ------------------------------------------------------------------
-// LPQT_SK_RAMP (percent, decode BN <= 32): CTA ranges shrink linearly with
-// blockIdx — CTAs are dispatched in blockIdx order, so in a PDL chain the low
-// ones land on the SMs the previous kernel frees first.  Range start of CTA c:
-// total * x (1 + r (1 - x)), x = c / grid (density 1 + r (1 - 2x)).
-#ifndef LPQT_SK_RAMP
-#define LPQT_SK_RAMP 0
-#endif
-__host__ __device__ __forceinline__ int64_t sk_begin_n(int64_t total, int c, int g, int ramp) {
-  if (ramp == 0) return (int64_t)c * total / g;
-  return total * c * (100 * (int64_t)g + ramp * (int64_t)(g - c)) / (100 * (int64_t)g * g);
-}
-__device__ __forceinline__ int sk_ramp(const GemmArgs& a) { return a.dp ? 0 : a.ramp; }
 __device__ __forceinline__ int64_t sk_begin(const GemmArgs& a, int c) {
-  return sk_begin_n(a.total, c, static_cast<int>(gridDim.x), sk_ramp(a));
+  return (int64_t)c * a.total / (int64_t)gridDim.x;
 }
 // CTA whose range holds global k-step position p
 __device__ __forceinline__ int sk_cta_of(const GemmArgs& a, int64_t p) {
-  if (sk_ramp(a) == 0) return static_cast<int>(((p + 1) * (int64_t)gridDim.x - 1) / a.total);
-  int lo = 0, hi = static_cast<int>(gridDim.x) - 1;  // largest c with begin(c) <= p
-  while (lo < hi) {
-    const int mid = (lo + hi + 1) >> 1;
-    if (sk_begin(a, mid) <= p) lo = mid; else hi = mid - 1;
-  }
-  return lo;
+  return static_cast<int>(((p + 1) * (int64_t)gridDim.x - 1) / a.total);
 }
 
 // A CTA's stream-K range [beg, end) in natural order; segments never
@@ -875,7 +856,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int c = blockIdx.x; c < pf.count; c += gridDim.x) {
           int64_t kt_lin;  // tile-linear k-tile index = byte offset / kTileBytes
           if (pf.total > 0) {
-            const int64_t q = sk_begin_n(pf.total, c, pf.count, pf.ramp);
+            const int64_t q = (int64_t)c * pf.total / pf.count;
             const int64_t t = q / pf.ksteps;
             kt_lin = t * pf.k_tiles + (q - t * pf.ksteps) * pf.kstep;
           } else {
@@ -1754,7 +1735,6 @@ struct Plan {
   bool dp;      // prefill: whole tiles round-robin (SkSched DP mode)
   int cluster;  // CSK cluster size
   int splits;   // max CTAs contributing to one tile
-  int ramp;     // SK range ramp (percent, LPQT_SK_RAMP; decode stream-K only)
   int64_t K;    // X's k extent: TMA zero-fills columns K .. ldx (W4A16 pads with Z, not 0)
 };
 
@@ -1936,8 +1916,7 @@ done_csk:
   if (g < 1) g = 1;
   p.grid = static_cast<int>(g);
   // partial tiles exist unless every CTA range is a whole number of tiles
-  p.ramp = (p.bn <= 32 && split_k == 0) ? LPQT_SK_RAMP : 0;
-  p.partials = p.ramp > 0 || !(p.total % g == 0 && (p.total / g) % p.ksteps == 0);
+  p.partials = !(p.total % g == 0 && (p.total / g) % p.ksteps == 0);
   if (p.partials) {
     p.counters_bytes = kMaxCounters * 4;  // fixed region, zeroed once, self-resetting
     p.ws_bytes = p.counters_bytes + (int64_t)p.grid * 2 * kTileN * p.bn * 4;
@@ -1948,7 +1927,6 @@ done_csk:
       p.tiles < ((int64_t)1 << 30) && split_k == 0 && !(flags & LPQT_SCHED_STREAMK)) {
     p.dp = true;
     p.grid = sms;
-    p.ramp = 0;
     p.partials = false;
     p.counters_bytes = 0;
     p.ws_bytes = 0;
@@ -1963,7 +1941,7 @@ done_csk:
 int launch_prefill_2sm(const uint8_t* tiles, const uint16_t* scales, const uint16_t* Xt, int64_t ldx, int64_t M,
                        int64_t N, int64_t K, void* Y, int y_dtype, int y_layout, int64_t ldy, int flags,
                        int force, void* workspace, int64_t workspace_bytes, cudaStream_t stream,
-                       int* grid_out);                         // prefill2sm.cu
+                       int* grid_out, bool fgq);               // prefill2sm.cu
 int prefill_2sm_pairs();                                       // prefill2sm.cu
 double prefill_2sm_choose(int64_t M, int64_t N, int64_t K, int* bn_out, int* sk_out, int force);  // prefill2sm.cu
 int64_t prefill_2sm_workspace();                                                              // prefill2sm.cu
@@ -2306,10 +2284,10 @@ static int w6a16_blocks_impl(const uint8_t* tiles, const uint16_t* scales, int64
   if (y_layout == LPQT_Y_NM ? ldy < M : ldy < N) return LPQT_E_SHAPE;
   if (split_k < 0) return LPQT_E_INVALID_INPUT;
   if (N > (int64_t)1 << 30 || M > (int64_t)1 << 30 || K > (int64_t)1 << 30) return LPQT_E_SHAPE;
-  if (!fgq && !po && !fp5 && pair_force(split_k, flags) >= 0 && use_pair_kernel(M, N, K, flags)) {
+  if (!fgq_sub && !po && !fp5 && pair_force(split_k, flags) >= 0 && use_pair_kernel(M, N, K, flags)) {
     const int st = launch_prefill_2sm(tiles, scales, Xt, ldx, M, N, K, Y, y_dtype, y_layout, ldy, flags,
                                       pair_force(split_k, flags), workspace, workspace_bytes, as_stream(stream),
-                                      nullptr);
+                                      nullptr, fgq);
     if (st != LPQT_E_UNSUPPORTED) return st;
   }
   Plan p = make_plan(M, N, K, split_k, flags, num_sms(), fgq);
@@ -2336,7 +2314,6 @@ static int w6a16_blocks_impl(const uint8_t* tiles, const uint16_t* scales, int64
   // X larger than ~1/3 of L2 (126 MB): keep each batch tile's X resident
   args.n_fastest = (p.m_tiles > 1 && M * K * 2 > (int64_t)40 << 20) ? 1 : 0;
   args.dp = p.dp ? 1 : 0;
-  args.ramp = p.ramp;
   args.y_dtype = y_dtype;
   args.y_layout = y_layout;
   args.sm = ShiftMuls{1u << 26, 1u << 28, 1u << 30};
@@ -2356,7 +2333,6 @@ static int w6a16_blocks_impl(const uint8_t* tiles, const uint16_t* scales, int64
       pfa.k_tiles = q.k_tiles;
       pfa.c = q.csk ? q.cluster : 1;
       pfa.tiles = static_cast<int>(q.tiles);
-      pfa.ramp = q.csk ? 0 : q.ramp;
       pfa.chunk = static_cast<uint32_t>(std::min<int64_t>(chunk, (int64_t)1 << 30) / 16 * 16);
     }
   }
@@ -2447,7 +2423,6 @@ int lpqt_w4a16_linear_blocks(const uint8_t* tiles, const uint32_t* params, int64
   args.tile_count = static_cast<int>(p.tiles);
   args.n_fastest = (p.m_tiles > 1 && M * K * 2 > (int64_t)40 << 20) ? 1 : 0;
   args.dp = p.dp ? 1 : 0;
-  args.ramp = p.ramp;
   args.y_dtype = y_dtype;
   args.y_layout = y_layout;
   args.sm = ShiftMuls{1u << 26, 1u << 28, 1u << 30};

@@ -72,7 +72,11 @@ constexpr int kDCol0 = kASlots * kAColsTile;  // D: 256 fp32 columns after the A
 constexpr int kTmemCols = 512;
 constexpr int kYChunk = 32;                   // epilogue: 32 batch columns per TMA store
 constexpr int kYBuf = kYChunk * kTileN * 2;   // 8 KB staging (16-bit Y), double-buffered
-constexpr int kSmemBytes = kXStages * kXStage + kWStages * kTileBytes + 2 * kYBuf +
+// a W stage: the weight tile + (FGQ) its 128 rows' f16 block scales, stage-ordered
+// (lpqt_fgq_stage_params, as in gemm.cu)
+constexpr int kSParams = kTileN * 2;
+constexpr int kWStageFgq = kTileBytes + kSParams;
+constexpr int kSmemBytes = kXStages * kXStage + kWStages * kWStageFgq + 2 * kYBuf +
                            8 * (2 * kXStages + 2 * kWStages + 2 * kASlots + 3) + 16;
 static_assert(kSmemBytes <= 227 * 1024, "shared memory");
 // stream-K: one partial slot per pair and CTA, 128 rows x kMaxBN fp32 (the
@@ -96,6 +100,12 @@ struct Args {
   int* counters;   // sk: [units][2] k-tiles published (self-resetting)
   float* partials; // sk: [pairs][2][kPartFloats], chunk-major float4 [bn / 4][128]
   ShiftMuls sm;
+};
+// FGQ block parameters: a separate kernel parameter (growing Args perturbs the
+// register allocation: 24 -> 64 bytes of spills in the CGQ kernel, measured)
+struct FgqP {
+  const uint8_t* stage;  // stage-ordered block scales (lpqt_fgq_stage_params)
+  const float* rowf;     // per-row power-of-two factors (after the stage-ordered scales)
 };
 
 // A pair's walk over its work, step i -> unit u, k tile kt: whole units
@@ -235,13 +245,17 @@ __device__ __forceinline__ void store_y(const Args& a, int n, int m, float v) {
   }
 }
 
+// FGQ: blocks of whole 128-k tiles (stage-ordered block scales applied to the
+// rebuilt binary16 weight); a separate instantiation so the CGQ code is unchanged
+template <bool FGQ>
 __global__ void __launch_bounds__(kThreads, 1)
     w6a16_prefill_2sm_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constant__ CUtensorMap tmap_y,
-                             const Args a) {
+                             const Args a, const FgqP fq) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem_x = smem_raw;
   uint8_t* smem_w = smem_x + kXStages * kXStage;
-  uint8_t* smem_y = smem_w + kWStages * kTileBytes;
+  constexpr int kWStage = FGQ ? kWStageFgq : kTileBytes;  // (CGQ keeps the 12 KB stage stride)
+  uint8_t* smem_y = smem_w + kWStages * kWStage;
   uint64_t* full_x = reinterpret_cast<uint64_t*>(smem_y + 2 * kYBuf);
   uint64_t* empty_x = full_x + kXStages;
   uint64_t* full_w = empty_x + kXStages;
@@ -312,8 +326,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int s = i % kWStages;
         mbar_wait<2>(&empty_w[s], ((i / kWStages) & 1) ^ 1);
         const uint32_t e = elect_one();
-        mbar_arrive_expect_tx_if(e, &full_w[s], kTileBytes);
-        bulk_g2s_if(e, smem_w + s * kTileBytes,
+        mbar_arrive_expect_tx_if(e, &full_w[s], kTileBytes + (FGQ ? kSParams : 0));
+        if constexpr (FGQ)
+          bulk_g2s_if(e, smem_w + s * kWStage + kTileBytes,
+                      fq.stage + ((int64_t)(2 * pair + rank) * a.k_tiles + w.kt) * kSParams, kSParams, &full_w[s], pol);
+        bulk_g2s_if(e, smem_w + s * kWStage,
                     a.tiles + ((int64_t)(2 * pair + rank) * a.k_tiles + w.kt) * kTileBytes, kTileBytes, &full_w[s],
                     pol);
       }
@@ -386,10 +403,12 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t af_leader = mapa(smem_u32(afull), 0);
     const ShiftMuls sm = a.sm;
     uint32_t q[12];
+    uint32_t fs2 = 0;  // FGQ: this row's block scale (binary16 x2) of the stage's tile
     auto load = [&](int i) {
       const int s = i % kWStages;
       mbar_wait<2>(&full_w[s], (i / kWStages) & 1);
-      const uint32_t src = w_src + s * kTileBytes;
+      if constexpr (FGQ) fs2 = __byte_perm(lds_u16(smem_u32(smem_w) + kTileBytes + row * 2 + s * kWStage), 0u, 0x1010);
+      const uint32_t src = w_src + s * kWStage;
       const uint4 v0 = lds128_u32(src), v1 = lds128_u32(src + kTileN * 16), v2 = lds128_u32(src + 2 * kTileN * 16);
       q[0] = v0.x; q[1] = v0.y; q[2] = v0.z; q[3] = v0.w; q[4] = v1.x; q[5] = v1.y;
       q[6] = v1.z; q[7] = v1.w; q[8] = v2.x; q[9] = v2.y; q[10] = v2.z; q[11] = v2.w;
@@ -399,6 +418,13 @@ __global__ void __launch_bounds__(kThreads, 1)
       uint32_t r[32];
       fp6x32_cvt_f16x32_fma(q, r, sm);
       fp6x32_cvt_f16x32_fma(q + 6, r + 16, sm);
+      if constexpr (FGQ) {  // FGQ: v * S'_b in binary16 (per-row power-of-two normalised scales, as gemm.cu BN >= 64)
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          const __half2 v = __hmul2(*reinterpret_cast<const __half2*>(&r[j]), *reinterpret_cast<const __half2*>(&fs2));
+          r[j] = *reinterpret_cast<const uint32_t*>(&v);
+        }
+      }
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty_w[i % kWStages]);  // words consumed
       const int sl = i % kASlots;
@@ -435,7 +461,13 @@ __global__ void __launch_bounds__(kThreads, 1)
       int pair, mt;
       unit_nm(a, u, pair, mt);
       const int n0 = (2 * pair + static_cast<int>(rank)) * kTileN, n = n0 + rr;
-      const float fs = n < a.N ? __half2float(__ushort_as_half(__ldg(a.scales + n))) : 0.f;
+      // CGQ: the row scale; FGQ: the row's power-of-two factor (the block scales are in A)
+      float fs;
+      if constexpr (FGQ) {
+        fs = n < a.N ? __ldg(fq.rowf + n) : 0.f;
+      } else {
+        fs = n < a.N ? __half2float(__ushort_as_half(__ldg(a.scales + n))) : 0.f;
+      }
       mbar_wait<2>(dfull, seg & 1);
       tc_fence_after();
       auto d_drained = [&]() {  // D may be overwritten by the next segment's MMAs
@@ -636,7 +668,7 @@ static int max_pairs() {
   static std::once_flag once;
   std::call_once(once, [] {
     int v = 0;
-    if (cudaFuncSetAttribute(p2::w6a16_prefill_2sm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    if (cudaFuncSetAttribute(p2::w6a16_prefill_2sm_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              p2::kSmemBytes) == cudaSuccess) {
       cudaLaunchConfig_t cfg = {};
       cfg.gridDim = dim3(2 * 64);
@@ -649,7 +681,7 @@ static int max_pairs() {
       attr[0].val.clusterDim.z = 1;
       cfg.attrs = attr;
       cfg.numAttrs = 1;
-      if (cudaOccupancyMaxActiveClusters(&v, p2::w6a16_prefill_2sm_kernel, &cfg) != cudaSuccess) v = 0;
+      if (cudaOccupancyMaxActiveClusters(&v, p2::w6a16_prefill_2sm_kernel<false>, &cfg) != cudaSuccess) v = 0;
     }
     cudaGetLastError();
     n = v > 0 ? v : 74;
@@ -718,9 +750,12 @@ int64_t prefill_2sm_workspace() { return p2::kCounters * 4 + (int64_t)max_pairs(
 // Host launch of the pair kernel (called from gemm.cu's dispatcher; CGQ FP6,
 // even number of 128-row weight tiles).  Returns LPQT_E_UNSUPPORTED when the
 // shape does not fit (the caller then uses the single-SM kernel).
+// scales: the f16 row scales (CGQ) or, with fgq, the stage-ordered block scales +
+// row factors of lpqt_fgq_stage_params (blocks of whole 128-k tiles)
 int launch_prefill_2sm(const uint8_t* tiles, const uint16_t* scales, const uint16_t* Xt, int64_t ldx, int64_t M,
                        int64_t N, int64_t K, void* Y, int y_dtype, int y_layout, int64_t ldy, int flags,
-                       int force, void* workspace, int64_t workspace_bytes, cudaStream_t stream, int* grid_out) {
+                       int force, void* workspace, int64_t workspace_bytes, cudaStream_t stream, int* grid_out,
+                       bool fgq) {
   const int n_tiles = static_cast<int>((N + kTileN - 1) / kTileN);
   if (n_tiles % 2 != 0) return LPQT_E_UNSUPPORTED;
   EncodeTiledFn2 enc = encode_fn_2sm();
@@ -760,6 +795,11 @@ int launch_prefill_2sm(const uint8_t* tiles, const uint16_t* scales, const uint1
   p2::Args a{};
   a.tiles = tiles;
   a.scales = scales;
+  p2::FgqP fq{};
+  if (fgq) {
+    fq.stage = reinterpret_cast<const uint8_t*>(scales);
+    fq.rowf = reinterpret_cast<const float*>(fq.stage + (int64_t)n_tiles * kTileN * ((K + kTileK - 1) / kTileK) * 2);
+  }
   a.y = Y;
   a.ldy = ldy;
   a.M = static_cast<int>(M);
@@ -803,8 +843,11 @@ int launch_prefill_2sm(const uint8_t* tiles, const uint16_t* scales, const uint1
   static std::once_flag once;
   static cudaError_t attr_err = cudaSuccess;
   std::call_once(once, [] {
-    attr_err = cudaFuncSetAttribute(p2::w6a16_prefill_2sm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    attr_err = cudaFuncSetAttribute(p2::w6a16_prefill_2sm_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     p2::kSmemBytes);
+    if (attr_err == cudaSuccess)
+      attr_err = cudaFuncSetAttribute(p2::w6a16_prefill_2sm_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      p2::kSmemBytes);
   });
   if (attr_err != cudaSuccess) return LPQT_E_CUDA;
   cudaLaunchConfig_t cfg = {};
@@ -827,7 +870,9 @@ int launch_prefill_2sm(const uint8_t* tiles, const uint16_t* scales, const uint1
   cfg.attrs = attr;
   cfg.numAttrs = na;
   if (grid_out) *grid_out = 2 * pairs;
-  if (cudaLaunchKernelEx(&cfg, p2::w6a16_prefill_2sm_kernel, map, ymap, a) != cudaSuccess) return LPQT_E_CUDA;
+  const cudaError_t le = fgq ? cudaLaunchKernelEx(&cfg, p2::w6a16_prefill_2sm_kernel<true>, map, ymap, a, fq)
+                             : cudaLaunchKernelEx(&cfg, p2::w6a16_prefill_2sm_kernel<false>, map, ymap, a, fq);
+  if (le != cudaSuccess) return LPQT_E_CUDA;
   note_launch();
   return check_launch();
 }
