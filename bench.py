@@ -337,6 +337,46 @@ def run_ours(args, world, rank, layers, m, e2e=True, burn_in=None):
     return res
 
 
+def time_quantize(layers, args):
+    """K1 on the GPU: RTN FP6 CGQ quantize of the step's four fp16 weights,
+    (a) the reference API `quantize_tensor(W, CGQ FP6, bias_shift=True)` ->
+    canonical 4+2 planes + scales + folded scales (quantizer.py:189-248) and
+    (b) `Fp6Weight.quantize` straight into the GEMM's tile layout.  Device
+    time (CUDA events), median of 5; algorithmic bytes = the fp16 weights
+    read twice (row peaks, encode) + 0.75 B per weight written."""
+    import torch
+    import paper_2312_08583_b200 as L
+    cgq = L.QuantScheme(L.Granularity.CGQ, L.TensorFormat.FP6_E3M2)
+    g = torch.Generator(device="cuda").manual_seed(11)
+    ws = [(torch.randn(n, k, generator=g, device="cuda") * 0.02).half() for _, n, k in layers]
+    nw = sum(w.numel() for w in ws)
+
+    def timed(fn):
+        fn()
+        torch.cuda.synchronize()
+        ts = []
+        for _ in range(5):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            fn()
+            e1.record()
+            torch.cuda.synchronize()
+            ts.append(e0.elapsed_time(e1) * 1e-3)
+        return sorted(ts)[2]
+    t_api = timed(lambda: [L.quantize_tensor(w, cgq, bias_shift=True) for w in ws])
+    t_tiles = timed(lambda: [L.Fp6Weight.quantize(w) for w in ws])
+    byts = nw * (2 * 2 + 0.75)
+    del ws
+    torch.cuda.empty_cache()
+    return {"workload": f"{args.model} quantize (RTN FP6 CGQ + 4+2 pack + fold) of the step's four weights, fp16 in",
+            "value": round(byts / t_api / 1e9, 1), "unit": "GB/s", "weights": nw,
+            "ms": round(t_api * 1e3, 3), "Mweights_per_s": round(nw / t_api / 1e6, 1),
+            "api": "paper_2312_08583_b200.quantize_tensor(W_cuda, CGQ FP6, bias_shift=True) -> canonical planes",
+            "tiles_path": {"ms": round(t_tiles * 1e3, 3), "GBps": round(byts / t_tiles / 1e9, 1),
+                           "api": "Fp6Weight.quantize (straight into the GEMM tile layout)"},
+            "note": "device time; compare cpu_baseline.quantize_weights_per_s (the reference's numpy quantize)"}
+
+
 def time_cublas(layers, world, rank, m, args):
     import torch
     from paper_2312_08583_b200.tp import shard_rows
@@ -710,6 +750,8 @@ def main():
                                    "frac": round(ent["tflops"] / peaks["bf16_tflops_sustained"], 4),
                                    "peak_source": peaks["source"] + " (sustained)"}
             extras.append(ent)
+        if world == 1:
+            extras.append(time_quantize(layers, args))
     if rank != 0:
         return
     line = {

@@ -362,6 +362,161 @@ __global__ void __launch_bounds__(256) encode_tiles_kernel(const void* __restric
   }
 }
 
+// ---- K1 fused (CGQ, 16-B aligned rows, K % 8 == 0): one CTA per group of
+// kQRows rows — phase 1: a warp per row computes the row's peak / scale /
+// folded scale (block_scales_kernel's arithmetic); phase 2: the CTA encodes the
+// same rows (their bytes are still in L2: the CTAs in flight hold
+// <= 148 x 2 x 8 rows) into the GEMM tiles (TILES) or the canonical planes.
+// DRAM traffic: the weights once + the codes, against twice + the codes for
+// the two-kernel path (which stays for FGQ and unaligned rows).
+constexpr int kQRows = 4;  // rows per CTA; 2 warps per row in phase 1
+template <int DT, bool TILES>
+__global__ void __launch_bounds__(256) quantize_fused_kernel(const void* __restrict__ W, int64_t N, int64_t K,
+                                                             int64_t ldw, double maxv, int bias_shift,
+                                                             uint16_t* __restrict__ scales,
+                                                             uint16_t* __restrict__ folded,
+                                                             uint32_t* __restrict__ flags, int64_t n_groups,
+                                                             int64_t k_tiles, uint8_t* __restrict__ out4,
+                                                             uint8_t* __restrict__ out2) {
+  using Acc = typename InTraits<DT>::Acc;
+  __shared__ double mids[32];
+  __shared__ float s_scale[kQRows];
+  __shared__ double s_peak[2 * kQRows];
+  if constexpr (!InTraits<DT>::kCvt) load_mids_f64(mids);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  uint32_t f = 0;
+  for (int64_t grp = blockIdx.x; grp < n_groups; grp += gridDim.x) {
+    const int64_t r0 = grp * kQRows;
+    // ---- phase 1: the row scales (quantizer.py:200-201, :224-227; _round_scales_f16 :142-153; fold dequant.py:61-69)
+    // 8 warps: warp 2q + h scans half h of row q; the two halves' peaks meet in
+    // shared memory as doubles (exact for every input type)
+    {
+      const int rq = warp >> 1, h = warp & 1;
+      const int64_t r = r0 + rq;
+      Acc peak = 0;
+      if (r < N) {
+        const char* row = static_cast<const char*>(W) + r * ldw * elem_bytes<DT>();
+        bool bad = false;
+        for (int64_t k = 8 * (lane + 32 * h); k < K; k += 512) {
+          Acc v[8];
+          load8<DT>(row + k * elem_bytes<DT>(), v);
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            bad |= !isfinite(v[q]);
+            peak = fmax(peak, fabs(v[q]));
+          }
+        }
+        if (__any_sync(0xffffffffu, bad)) f |= LPQT_F_NONFINITE;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) peak = fmax(peak, __shfl_xor_sync(0xffffffffu, peak, o));
+      }
+      if (lane == 0) s_peak[warp] = static_cast<double>(peak);
+      __syncthreads();
+      float sc = 0.f;
+      if (h == 0 && r < N) {
+        const double pk = fmax(s_peak[warp], s_peak[warp + 1]);
+        uint16_t sb = __half_as_ushort(__double2half(pk == 0.0 ? 1.0 : pk / maxv));
+        if ((sb & 0x7FFFu) == 0x7C00u) f |= LPQT_F_SCALE_INF;
+        if ((sb & 0x7FFFu) == 0) sb = 0x0001u;  // underflow clamps to 2^-24
+        sc = __half2float(__ushort_as_half(sb));
+        if (lane == 0) {
+          scales[r] = sb;
+          if (bias_shift) {
+            const double fv = static_cast<double>(sc) * 4096.0;
+            if (fv > 65504.0) f |= LPQT_F_FOLD_OVERFLOW;
+            folded[r] = (fv > 65504.0) ? (uint16_t)0x7C00u : __half_as_ushort(__double2half(fv));
+          }
+        }
+      }
+      if (h == 0 && lane == 0) s_scale[rq] = sc;
+    }
+    __syncthreads();
+    // ---- phase 2: encode the group's rows (the bytes phase 1 just read, from L2)
+    if constexpr (TILES) {
+      // thread unit = (row, 64-weight half of a 128-k tile), rows fastest (encode_tiles_kernel's body)
+      const int64_t units = (int64_t)kQRows * k_tiles * 2;
+      for (int64_t u = threadIdx.x; u < units; u += blockDim.x) {
+        const int rq = static_cast<int>(u % kQRows);
+        const int64_t sk = u / kQRows;
+        const int kh = static_cast<int>(sk & 1);
+        const int64_t kt = sk >> 1;
+        const int64_t n = r0 + rq, k0 = kt * kTileK + kh * 64;
+        uint32_t cw[16];
+        if (n < N) {
+          const char* row = static_cast<const char*>(W) + n * ldw * elem_bytes<DT>();
+          const float Sf = s_scale[rq];
+          if (k0 + 64 <= K) {
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+              Acc v[8];
+              load8<DT>(row + (k0 + 8 * q) * elem_bytes<DT>(), v);
+              const uint64_t c = encode8<DT>(v, Sf, static_cast<double>(Sf), mids);
+              cw[2 * q] = static_cast<uint32_t>(c);
+              cw[2 * q + 1] = static_cast<uint32_t>(c >> 32);
+            }
+          } else {
+#pragma unroll 1
+            for (int q = 0; q < 8; ++q) {
+              uint64_t c = 0;
+              if (k0 + 8 * q < K) {  // (K % 8 == 0: whole groups of 8)
+                Acc v[8];
+                load8<DT>(row + (k0 + 8 * q) * elem_bytes<DT>(), v);
+                c = encode8<DT>(v, Sf, static_cast<double>(Sf), mids);
+              }
+              cw[2 * q] = static_cast<uint32_t>(c);
+              cw[2 * q + 1] = static_cast<uint32_t>(c >> 32);
+            }
+          }
+        } else {
+#pragma unroll
+          for (int i = 0; i < 16; ++i) cw[i] = 0;  // padding rows: code 0, as prepack writes
+        }
+        uint32_t w[12];
+        pack_words_from_bytes(cw, w);
+        pack_words_from_bytes(cw + 8, w + 6);
+        const int64_t tile = (n / kTileN) * k_tiles + kt;
+        uint4* dst = reinterpret_cast<uint4*>(out4 + tile * kTileBytes) + (kh * 3) * kTileN + (n % kTileN);
+#pragma unroll
+        for (int q = 0; q < 3; ++q) dst[q * kTileN] = make_uint4(w[4 * q], w[4 * q + 1], w[4 * q + 2], w[4 * q + 3]);
+      }
+    } else {
+      // canonical planes: thread per 8 consecutive codes of a row (K % 8 == 0), one u32 of seg4 + one u16 of seg2
+      const int64_t per_row = K / 8, units = (int64_t)kQRows * per_row;
+      for (int64_t u = threadIdx.x; u < units; u += blockDim.x) {
+        const int rq = static_cast<int>(u / per_row);
+        const int64_t j = u - rq * per_row, n = r0 + rq;
+        if (n >= N) break;  // (rows are the slow index: every later unit is past N too)
+        Acc v[8];
+        load8<DT>(static_cast<const char*>(W) + (n * ldw + 8 * j) * elem_bytes<DT>(), v);
+        const float Sf = s_scale[rq];
+        const uint64_t c = encode8<DT>(v, Sf, static_cast<double>(Sf), mids);
+        uint32_t s4 = 0, s2 = 0;
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          const uint32_t ce = static_cast<uint32_t>(c >> (8 * e)) & 0x3Fu;
+          s4 |= (ce >> 2) << (4 * e);
+          s2 |= (ce & 3u) << (2 * e);
+        }
+        const int64_t g8 = (n * K) / 8 + j;
+        *reinterpret_cast<uint32_t*>(out4 + 4 * g8) = s4;
+        *reinterpret_cast<uint16_t*>(out2 + 2 * g8) = static_cast<uint16_t>(s2);
+      }
+    }
+    __syncthreads();  // s_scale is rewritten by the next group
+  }
+  if (f) atomicOr(flags, f);
+}
+
+// grid of the fused quantizer: the CTAs in flight (4 per SM, 4 rows each) keep
+// their rows in L2 up to K = 16384 (38 MB at K = 8192); longer rows take the
+// two-kernel path (measured: fused 12-13 % faster at K = 4096 / 8192, 16 %
+// slower at K = 28672; profiles/r02_quant_fused_vs_twopass.jsonl)
+static int fused_grid(int64_t groups, int64_t K) {
+  (void)K;
+  const int64_t cap = 148 * 4;
+  return static_cast<int>(groups < cap ? groups : cap);
+}
+
 // ---- canonical pack / unpack (packing.py:63-118) --------------------------
 // thread j owns seg2 byte j (codes 4j..4j+3) and seg4 bytes 2j, 2j+1; pad
 // bytes are written as zero (packing.py:73, :88).
@@ -808,6 +963,9 @@ int lpqt_fp6_dequant_naive(const uint8_t* codes, const uint16_t* scales, int64_t
   return check_launch();
 }
 
+#ifndef LPQT_FUSED_QUANT
+#define LPQT_FUSED_QUANT 1
+#endif
 static int quantize_scales(const void* W, int dtype, int64_t N, int64_t K, int64_t ldw, int64_t B, int64_t bpr,
                            int vec, int bias_shift, uint16_t* scales, uint16_t* folded, uint32_t* dev_flags,
                            cudaStream_t st, double maxv = 28.0) {
@@ -847,6 +1005,13 @@ int lpqt_fp6_quantize_pack_blocks(const void* W, int dtype, int64_t N, int64_t K
   int64_t B, bpr;
   block_geometry(K, block, B, bpr);
   const int vec = rows_vectorizable(W, ldw);
+  if (LPQT_FUSED_QUANT && bpr == 1 && vec && K % 8 == 0 && K <= 16384) {  // CGQ: one fused pass (scales + encode, W read once)
+    const int64_t ng = (N + kQRows - 1) / kQRows;
+    LPQT_DISPATCH_DT(dtype, (quantize_fused_kernel<DT, false><<<fused_grid(ng, K), 256, 0, st>>>(
+                                W, N, K, ldw, 28.0, bias_shift, scales, folded, dev_flags, ng, 0, seg4, seg2)));
+    note_launch();
+    return check_launch();
+  }
   rc = quantize_scales(W, dtype, N, K, ldw, B, bpr, vec, bias_shift, scales, folded, dev_flags, st);
   if (rc != LPQT_OK) return rc;
   const int64_t groups = (N * K + 7) / 8;
@@ -875,9 +1040,17 @@ int lpqt_fp6_quantize_tiles_blocks(const void* W, int dtype, int64_t N, int64_t 
   int64_t B, bpr;
   block_geometry(K, block, B, bpr);
   const int vec = rows_vectorizable(W, ldw);
+  const int64_t Np = (N + kTileN - 1) / kTileN * kTileN, k_tiles = (K + kTileK - 1) / kTileK;
+  if (LPQT_FUSED_QUANT && bpr == 1 && vec && K % 8 == 0 && K <= 16384) {  // CGQ: one fused pass (scales + encode, W read once)
+    const int64_t ng = Np / kQRows;  // (padding rows get code 0)
+    LPQT_DISPATCH_DT(dtype, (quantize_fused_kernel<DT, true><<<fused_grid(ng, K), 256, 0, st>>>(
+                                W, N, K, ldw, 28.0, bias_shift, scales, folded, dev_flags, ng, k_tiles, tiles,
+                                nullptr)));
+    note_launch();
+    return check_launch();
+  }
   rc = quantize_scales(W, dtype, N, K, ldw, B, bpr, vec, bias_shift, scales, folded, dev_flags, st);
   if (rc != LPQT_OK) return rc;
-  const int64_t Np = (N + kTileN - 1) / kTileN * kTileN, k_tiles = (K + kTileK - 1) / kTileK;
   const int64_t threads = Np * k_tiles * 2;
   const int tv = vec && (B % 8 == 0);
   LPQT_DISPATCH_DT(dtype, encode_tiles_kernel<DT><<<grid_for(threads, 256), 256, 0, st>>>(W, N, K, ldw, tv, B, bpr,
