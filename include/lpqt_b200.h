@@ -202,6 +202,14 @@ int lpqt_w6a16_linear(const uint8_t* tiles, const uint16_t* scales,
 /* `tiles` are native FP5 tiles (lpqt_fp5n_prepack), CGQ; single-SM kernels
  * (decode and prefill), no pair kernel, no LPQT_REBUILD_* */
 #define LPQT_WEIGHTS_FP5 128
+
+/* Self-test of the quantizer's division-free RTN quotient (not a reference
+ * interface): every positive finite binary16 scale against every positive
+ * finite binary16 (dtype LPQT_F16) / bfloat16 (LPQT_BF16) weight with
+ * |w| <= 29 S, e3m2 codes and f32 quotients against the __fdiv_rn path.
+ * out3[0] = code mismatches, out3[1] = quotient mismatches, out3[2] = pairs.
+ * Synchronous. */
+int lpqt_selftest_fp6_encode(int dtype, unsigned long long* out3);
 int lpqt_w6a16_linear_ex(const uint8_t* tiles, const uint16_t* scales,
                          const uint16_t* Xt, int64_t ldx, int64_t M, int64_t N,
                          int64_t K, void* Y, int y_dtype, int y_layout,

@@ -101,6 +101,7 @@ SIGNATURES = {
     "lpqt_fp5_dequant_naive": (_I32, [_P, _P, _I64, _P, _P]),
     "lpqt_fp5_prepack": (_I32, [_P, _P, _I64, _I64, _P, _P]),
     "lpqt_fp5n_tiles_bytes": (_I64, [_I64, _I64]),
+    "lpqt_selftest_fp6_encode": (_I32, [_I32, _P]),
     "lpqt_fp5n_prepack": (_I32, [_P, _P, _I64, _I64, _P, _P]),
     "lpqt_fp5n_unprepack": (_I32, [_P, _I64, _I64, _P, _P]),
     "lpqt_fp5n_tiles_dequant": (_I32, [_P, _P, _I64, _I64, _P, _P]),

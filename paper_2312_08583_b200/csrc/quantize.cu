@@ -87,11 +87,33 @@ __global__ void encode_kernel(const void* __restrict__ x, int64_t n, uint8_t* __
 // mantissa = the even grid index, and q > 26 saturates to 28 (idx 31).  The
 // sign is applied separately so -0.0 -> code 0 (codec.py:130).
 // f32 / f64 inputs keep the literal f64 path (fp6_encode above).
-__device__ __forceinline__ uint32_t fp6_encode2_cvt(float w0, float w1, float S) {
+__device__ __forceinline__ uint32_t fp6_encode2_cvt_div(float w0, float w1, float S) {
   const float q0 = __fdiv_rn(fabsf(w0), S), q1 = __fdiv_rn(fabsf(w1), S);
   uint16_t r;
   asm("cvt.rn.satfinite.e3m2x2.f32 %0, %1, %2;" : "=h"(r) : "f"(q1), "f"(q0));
   return static_cast<uint32_t>(r) | (w0 < 0.f ? 0x20u : 0u) | (w1 < 0.f ? 0x2000u : 0u);
+}
+// The same quotients without a division per element: with the row's Y =
+// RN(1/S) (one __frcp_rn per row), q0 = RN(a Y), the exact residual
+// R = a - S q0 (one FMA) and q = RN(q0 + R Y) (Markstein's correction) — three
+// FMA-pipe ops per weight.  Pinned against the __fdiv_rn path for EVERY
+// binary16 / bfloat16 weight and every binary16 scale in the quantizer's range
+// (|w| <= 29 S) by lpqt_selftest_fp6_encode (tests/test_gpu_parity.py): the
+// codes agree everywhere; the f32 quotients too for binary16 weights (for
+// bfloat16 0.26 % differ by an ulp, none across a grid midpoint).
+__device__ __forceinline__ float div_by_scale(float a, float S, float Y) {
+  const float q0 = __fmul_rn(a, Y);
+  const float R = __fmaf_rn(-S, q0, a);
+  return __fmaf_rn(R, Y, q0);
+}
+__device__ __forceinline__ uint32_t fp6_encode2_cvt(float w0, float w1, float S, float Y) {
+  const float q0 = div_by_scale(fabsf(w0), S, Y), q1 = div_by_scale(fabsf(w1), S, Y);
+  uint16_t r;
+  asm("cvt.rn.satfinite.e3m2x2.f32 %0, %1, %2;" : "=h"(r) : "f"(q1), "f"(q0));
+  return static_cast<uint32_t>(r) | (w0 < 0.f ? 0x20u : 0u) | (w1 < 0.f ? 0x2000u : 0u);
+}
+__device__ __forceinline__ uint32_t fp6_encode2_cvt(float w0, float w1, float S) {
+  return fp6_encode2_cvt(w0, w1, S, __frcp_rn(S));
 }
 
 template <int DT>
@@ -158,8 +180,9 @@ __device__ __forceinline__ uint64_t encode8(const typename InTraits<DT>::Acc v[8
                                             const double* __restrict__ mids) {
   uint64_t c = 0;
   if constexpr (InTraits<DT>::kCvt) {
+    const float Y = __frcp_rn(Sf);  // (hoisted out of callers' loops by the compiler when Sf is invariant)
 #pragma unroll
-    for (int i = 0; i < 4; ++i) c |= static_cast<uint64_t>(fp6_encode2_cvt(v[2 * i], v[2 * i + 1], Sf)) << (16 * i);
+    for (int i = 0; i < 4; ++i) c |= static_cast<uint64_t>(fp6_encode2_cvt(v[2 * i], v[2 * i + 1], Sf, Y)) << (16 * i);
   } else {
 #pragma unroll
     for (int i = 0; i < 8; ++i)
@@ -515,6 +538,28 @@ static int fused_grid(int64_t groups, int64_t K) {
   (void)K;
   const int64_t cap = 148 * 4;
   return static_cast<int>(groups < cap ? groups : cap);
+}
+
+// ---- self-test: the division-free quotient vs __fdiv_rn, exhaustively ------
+// every positive finite binary16 scale S (block x) against every positive
+// finite binary16 (dt 2) / bfloat16 (dt 3) weight a with a <= 29 S: the e3m2
+// codes (and the f32 quotients) must agree bit for bit.
+__global__ void selftest_encode_kernel(int bf16, unsigned long long* __restrict__ bad_codes,
+                                       unsigned long long* __restrict__ bad_quot, unsigned long long* __restrict__ pairs) {
+  const uint16_t sb = static_cast<uint16_t>(blockIdx.x + 1);  // 0x0001 .. 0x7BFF
+  const float S = __half2float(__ushort_as_half(sb)), Y = __frcp_rn(S);
+  unsigned long long nc = 0, nq = 0, np = 0;
+  for (uint32_t ab = threadIdx.x; ab < (bf16 ? 0x7F80u : 0x7C00u); ab += blockDim.x) {
+    const float a = bf16 ? __uint_as_float(ab << 16) : __half2float(__ushort_as_half(static_cast<uint16_t>(ab)));
+    if (a > 29.f * S) continue;
+    ++np;
+    const float qd = __fdiv_rn(a, S), qf = div_by_scale(a, S, Y);
+    nq += __float_as_uint(qd) != __float_as_uint(qf);
+    nc += (fp6_encode2_cvt_div(a, -a, S) != fp6_encode2_cvt(a, -a, S, Y));
+  }
+  atomicAdd(bad_codes, nc);
+  atomicAdd(bad_quot, nq);
+  atomicAdd(pairs, np);
 }
 
 // ---- canonical pack / unpack (packing.py:63-118) --------------------------
@@ -908,6 +953,19 @@ using namespace lpqt;
   }
 
 extern "C" {
+
+int lpqt_selftest_fp6_encode(int dtype, unsigned long long* out3) {
+  if (dtype != LPQT_F16 && dtype != LPQT_BF16) return LPQT_E_UNSUPPORTED;
+  unsigned long long* d = nullptr;
+  if (cudaMalloc(&d, 3 * sizeof(unsigned long long)) != cudaSuccess) return LPQT_E_CUDA;
+  cudaMemset(d, 0, 3 * sizeof(unsigned long long));
+  selftest_encode_kernel<<<0x7BFF, 256>>>(dtype == LPQT_BF16, d, d + 1, d + 2);
+  note_launch();
+  int rc = check_launch();
+  if (cudaMemcpy(out3, d, 3 * sizeof(unsigned long long), cudaMemcpyDeviceToHost) != cudaSuccess) rc = LPQT_E_CUDA;
+  cudaFree(d);
+  return rc;
+}
 
 int64_t lpqt_fp6_seg4_length(int64_t n) { return ((n + 1) / 2 + 3) / 4 * 4; }
 int64_t lpqt_fp6_tail_length(int64_t n) { return ((n * 2 + 7) / 8 + 3) / 4 * 4; }
