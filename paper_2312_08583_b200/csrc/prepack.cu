@@ -40,6 +40,35 @@ __global__ void prepack_kernel(const uint8_t* __restrict__ seg4, const uint8_t* 
   }
 }
 
+// K % 32 == 0 and 16-B aligned planes: a 32-weight group is 16 B of seg4 and
+// 8 B of seg2 (one vector load each); rows fastest across the warp so the
+// tile stores of a warp land in one [khalf][quad] plane (128 rows x 16 B)
+__global__ void prepack_vec_kernel(const uint8_t* __restrict__ seg4, const uint8_t* __restrict__ seg2, int64_t N,
+                                   int64_t K, int64_t Np, int64_t Kp, uint8_t* __restrict__ tiles) {
+  const int64_t groups = Kp / 32, total = Np * groups, k_tiles = Kp / kTileK;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t rr = t % kTileN, rest = t / kTileN;  // rows fastest inside a 128-row tile
+    const int64_t g = rest % groups, n = (rest / groups) * kTileN + rr;
+    uint8_t c[32];
+    if (n < N && 32 * g < K) {
+      const int64_t i0 = n * K + 32 * g;
+      const uint4 a = __ldg(reinterpret_cast<const uint4*>(seg4 + i0 / 2));
+      const uint2 b = __ldg(reinterpret_cast<const uint2*>(seg2 + i0 / 4));
+      const uint32_t s4[4] = {a.x, a.y, a.z, a.w}, s2[2] = {b.x, b.y};
+#pragma unroll
+      for (int j = 0; j < 32; ++j)
+        c[j] = static_cast<uint8_t>((((s4[j >> 3] >> (4 * (j & 7))) & 15u) << 2) | ((s2[j >> 4] >> (2 * (j & 15))) & 3u));
+    } else {
+#pragma unroll
+      for (int j = 0; j < 32; ++j) c[j] = 0;
+    }
+    uint32_t w[6];
+    fp6x32_pack_words(c, w);
+#pragma unroll
+    for (int i = 0; i < 6; ++i) *reinterpret_cast<uint32_t*>(tiles + tile_word_addr(n, g, i, k_tiles)) = w[i];
+  }
+}
+
 __device__ __forceinline__ void load_group(const uint8_t* __restrict__ tiles, int64_t n, int64_t g, int64_t k_tiles,
                                            uint32_t w[6]) {
 #pragma unroll
@@ -265,7 +294,10 @@ int lpqt_fp6_prepack(const uint8_t* seg4, const uint8_t* seg2, int64_t N, int64_
   if (N < 0 || K < 0) return LPQT_E_SHAPE;
   if (N == 0 || K == 0) return LPQT_OK;
   const int64_t Np = round_up(N, kTileN), Kp = round_up(K, kTileK);
-  prepack_kernel<<<grid_for(Np * (Kp / 32), 256), 256, 0, as_stream(stream)>>>(seg4, seg2, N, K, Np, Kp, tiles);
+  if (K % 32 == 0 && reinterpret_cast<uintptr_t>(seg4) % 16 == 0 && reinterpret_cast<uintptr_t>(seg2) % 8 == 0)
+    prepack_vec_kernel<<<grid_for(Np * (Kp / 32), 256), 256, 0, as_stream(stream)>>>(seg4, seg2, N, K, Np, Kp, tiles);
+  else
+    prepack_kernel<<<grid_for(Np * (Kp / 32), 256), 256, 0, as_stream(stream)>>>(seg4, seg2, N, K, Np, Kp, tiles);
   note_launch();
   return check_launch();
 }
