@@ -59,7 +59,7 @@ extern "C" {
 #define LPQT_Y_MN  1   /* Y[m, n] (torch.nn.Linear layout)                     */
 
 const char* lpqt_strerror(int status);
-int lpqt_abi_version(void);               /* bumps on any signature change (5: reference-order kernels, pair-kernel flags, FGQ row factors) */
+int lpqt_abi_version(void);               /* bumps on any signature change (6: ablation rebuild flags, native FP5 tiles, sub-tile FGQ, encode self-test) */
 
 /* codec.py:116-132 encode_rtn_array: x[n] (dtype) -> codes[n] (u8). */
 int lpqt_fp6_encode_rtn(const void* x, int dtype, int64_t n, uint8_t* codes,

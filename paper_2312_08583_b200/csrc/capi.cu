@@ -34,7 +34,7 @@ const char* lpqt_strerror(int status) {
   }
 }
 
-int lpqt_abi_version(void) { return 5; }
+int lpqt_abi_version(void) { return 6; }
 
 int64_t lpqt_launch_count(void) { return lpqt::g_launches.load(std::memory_order_relaxed); }
 

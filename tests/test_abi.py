@@ -43,7 +43,7 @@ def test_library_exports_every_declared_symbol(lib):
 
 
 def test_abi_version_and_status_strings(lib):
-    assert lib.lpqt_abi_version() == 5
+    assert lib.lpqt_abi_version() == 6
     from paper_2312_08583_b200 import _lib
     assert lib.lpqt_strerror(_lib.OK) == b"ok"
     assert b"ShapeError" in lib.lpqt_strerror(_lib.E_SHAPE)
