@@ -22,6 +22,9 @@ SHAPES = {
     "13b": [(15360, 5120), (5120, 5120), (27648, 5120), (5120, 13824)],
     "sc15b": [(6400, 6144), (6144, 6144), (24576, 6144), (6144, 24576)],
 }
+# BASELINE configs[3]: the 70B layers column-sharded over P GPUs (one rank's shard)
+for _p in (2, 4, 8):
+    SHAPES[f"70b_tp{_p}"] = [(n // _p, k) for n, k in SHAPES["70b"]]
 
 
 def time_fn(fn, iters=50, warm=5, flush=None):
