@@ -733,11 +733,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                   &full_w[s], w_pol);
     }
   };
-  // the first ring's worth of W stages goes out during setup (LPQT_W_PROLOGUE)
-#ifndef LPQT_W_PROLOGUE
-#define LPQT_W_PROLOGUE 0  // measured slower (5-12 %, profiles/r02_abx_w_prologue.jsonl)
-#endif
-  const int w_pro = min(LPQT_W_PROLOGUE < 0 ? C::kWStages : LPQT_W_PROLOGUE, n_st);
+  // (issuing the first W stages here, before the setup barrier, measured 5-12 %
+  // slower: profiles/r02_abx_w_prologue.jsonl, _1_2.jsonl)
   if (warp == kWarpTmaW) {
     if (lane == 0) {
       for (int s = 0; s < C::kWStages; ++s) {
@@ -773,15 +770,6 @@ __global__ void __launch_bounds__(kThreads, 1)
       CTA_STAMP(19);
     }
     __syncwarp();
-    // weights never depend on the preceding kernel: stream the first stages
-    // now, straight after the barrier init (the rest of the setup — TMEM
-    // allocation, register split, named barrier — overlaps their flight)
-    if (w_pro > 0) {
-      StageIter<Sched, KS> it;
-      it.start(a, sc, 0);
-      for (int i = 0; i < w_pro; ++i, it.next(a, sc)) issue_w(i, it);
-      if (lane == 0) CTA_STAMP(20);
-    }
     named_bar_arrive(2, kThreads);
   } else {
     if (warp == kWarpMma0) {
@@ -821,11 +809,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (!is_w && lane == 0) CTA_STAMP(13);
     // decode streams every weight byte once (evict-first); with several
     // batch tiles (prefill) the same weight tile is re-read per batch tile
-    // (w_pol).  The W producer resumes after its setup prologue.
+    // (w_pol).
     StageIter<Sched, KS> it;
-    const int i0 = is_w ? w_pro : 0;
-    it.start(a, sc, i0);
-    for (int i = i0; i < n_st; ++i, it.next(a, sc)) {
+    it.start(a, sc, 0);
+    for (int i = 0; i < n_st; ++i, it.next(a, sc)) {
       if (is_w) {
         const int s = i % C::kWStages;
         mbar_wait<WM>(&empty_w[s], ((i / C::kWStages) & 1) ^ 1);
