@@ -1928,7 +1928,7 @@ done_csk:
 int launch_prefill_2sm(const uint8_t* tiles, const uint16_t* scales, const uint16_t* Xt, int64_t ldx, int64_t M,
                        int64_t N, int64_t K, void* Y, int y_dtype, int y_layout, int64_t ldy, int flags,
                        int force, void* workspace, int64_t workspace_bytes, cudaStream_t stream,
-                       int* grid_out, bool fgq);               // prefill2sm.cu
+                       int* grid_out, bool fgq, bool fp5);     // prefill2sm.cu
 int prefill_2sm_pairs();                                       // prefill2sm.cu
 double prefill_2sm_choose(int64_t M, int64_t N, int64_t K, int* bn_out, int* sk_out, int force);  // prefill2sm.cu
 int64_t prefill_2sm_workspace();                                                              // prefill2sm.cu
@@ -2183,7 +2183,7 @@ int64_t lpqt_w6a16_workspace_bytes(int64_t M, int64_t N, int64_t K, int split_k)
 int lpqt_w6a16_plan_ex(int64_t M, int64_t N, int64_t K, int split_k, int flags, int* out, int n_out) {
   if (M <= 0 || N <= 0 || K <= 0) return LPQT_E_SHAPE;
   if ((flags & LPQT_SCHED_STREAMK) && (flags & LPQT_SCHED_CLUSTER)) return LPQT_E_INVALID_INPUT;
-  if (!(flags & LPQT_WEIGHTS_FP5) && pair_force(split_k, flags) >= 0 && use_pair_kernel(M, N, K, flags)) {
+  if (pair_force(split_k, flags) >= 0 && use_pair_kernel(M, N, K, flags)) {
     int bn = 256, sk = 0;
     prefill_2sm_choose(M, N, K, &bn, &sk, pair_force(split_k, flags));
     const int64_t units = ((N + kTileN - 1) / kTileN / 2) * ((M + bn - 1) / bn);
@@ -2271,10 +2271,10 @@ static int w6a16_blocks_impl(const uint8_t* tiles, const uint16_t* scales, int64
   if (y_layout == LPQT_Y_NM ? ldy < M : ldy < N) return LPQT_E_SHAPE;
   if (split_k < 0) return LPQT_E_INVALID_INPUT;
   if (N > (int64_t)1 << 30 || M > (int64_t)1 << 30 || K > (int64_t)1 << 30) return LPQT_E_SHAPE;
-  if (!fgq_sub && !po && !fp5 && pair_force(split_k, flags) >= 0 && use_pair_kernel(M, N, K, flags)) {
+  if (!fgq_sub && !po && pair_force(split_k, flags) >= 0 && use_pair_kernel(M, N, K, flags)) {
     const int st = launch_prefill_2sm(tiles, scales, Xt, ldx, M, N, K, Y, y_dtype, y_layout, ldy, flags,
                                       pair_force(split_k, flags), workspace, workspace_bytes, as_stream(stream),
-                                      nullptr, fgq);
+                                      nullptr, fgq, fp5);
     if (st != LPQT_E_UNSUPPORTED) return st;
   }
   Plan p = make_plan(M, N, K, split_k, flags, num_sms(), fgq);

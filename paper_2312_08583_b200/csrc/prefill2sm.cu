@@ -247,14 +247,17 @@ __device__ __forceinline__ void store_y(const Args& a, int n, int m, float v) {
 
 // FGQ: blocks of whole 128-k tiles (stage-ordered block scales applied to the
 // rebuilt binary16 weight); a separate instantiation so the CGQ code is unchanged
-template <bool FGQ>
+// WB: 6 = FP6 tiles (12 KB), 5 = native FP5 tiles (10 KB, common.cuh; CGQ)
+template <bool FGQ, int WB = 6>
 __global__ void __launch_bounds__(kThreads, 1)
     w6a16_prefill_2sm_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constant__ CUtensorMap tmap_y,
                              const Args a, const FgqP fq) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem_x = smem_raw;
   uint8_t* smem_w = smem_x + kXStages * kXStage;
-  constexpr int kWStage = FGQ ? kWStageFgq : kTileBytes;  // (CGQ keeps the 12 KB stage stride)
+  static_assert(WB == 6 || !FGQ, "FGQ FP5 streams the FP6-widened tiles");
+  constexpr int kTileB = WB == 6 ? kTileBytes : kTileBytes5;
+  constexpr int kWStage = FGQ ? kWStageFgq : kTileB;  // (CGQ keeps the tile stride)
   uint8_t* smem_y = smem_w + kWStages * kWStage;
   uint64_t* full_x = reinterpret_cast<uint64_t*>(smem_y + 2 * kYBuf);
   uint64_t* empty_x = full_x + kXStages;
@@ -326,13 +329,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int s = i % kWStages;
         mbar_wait<2>(&empty_w[s], ((i / kWStages) & 1) ^ 1);
         const uint32_t e = elect_one();
-        mbar_arrive_expect_tx_if(e, &full_w[s], kTileBytes + (FGQ ? kSParams : 0));
+        mbar_arrive_expect_tx_if(e, &full_w[s], kTileB + (FGQ ? kSParams : 0));
         if constexpr (FGQ)
           bulk_g2s_if(e, smem_w + s * kWStage + kTileBytes,
                       fq.stage + ((int64_t)(2 * pair + rank) * a.k_tiles + w.kt) * kSParams, kSParams, &full_w[s], pol);
         bulk_g2s_if(e, smem_w + s * kWStage,
-                    a.tiles + ((int64_t)(2 * pair + rank) * a.k_tiles + w.kt) * kTileBytes, kTileBytes, &full_w[s],
-                    pol);
+                    a.tiles + ((int64_t)(2 * pair + rank) * a.k_tiles + w.kt) * kTileB, kTileB, &full_w[s], pol);
       }
     } else if (warp == kWarpX) {
       // ------------------------------------------------ X producer (own half of the batch tile)
@@ -408,6 +410,15 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int s = i % kWStages;
       mbar_wait<2>(&full_w[s], (i / kWStages) & 1);
       if constexpr (FGQ) fs2 = __byte_perm(lds_u16(smem_u32(smem_w) + kTileBytes + row * 2 + s * kWStage), 0u, 0x1010);
+      if constexpr (WB == 5) {  // k-half tl: nibble quads [tl][grp 0, 1][row], mantissa words [tl][row][2]
+        const uint32_t base = smem_u32(smem_w) + s * kWStage;
+        const uint32_t nsrc = base + static_cast<uint32_t>((tl * 2 * kTileN + row) * 16);
+        const uint4 v0 = lds128_u32(nsrc), v1 = lds128_u32(nsrc + kTileN * 16);
+        const uint2 mv = lds64_u32(base + kTile5Nib + static_cast<uint32_t>((tl * kTileN + row) * 8));
+        q[0] = v0.x; q[1] = v0.y; q[2] = v0.z; q[3] = v0.w; q[4] = v1.x; q[5] = v1.y;
+        q[6] = v1.z; q[7] = v1.w; q[8] = mv.x; q[9] = mv.y;
+        return;
+      }
       const uint32_t src = w_src + s * kWStage;
       const uint4 v0 = lds128_u32(src), v1 = lds128_u32(src + kTileN * 16), v2 = lds128_u32(src + 2 * kTileN * 16);
       q[0] = v0.x; q[1] = v0.y; q[2] = v0.z; q[3] = v0.w; q[4] = v1.x; q[5] = v1.y;
@@ -416,8 +427,13 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (grp < n_st) load(grp);
     for (int i = grp; i < n_st; i += 2) {
       uint32_t r[32];
-      fp6x32_cvt_f16x32_fma(q, r, sm);
-      fp6x32_cvt_f16x32_fma(q + 6, r + 16, sm);
+      if constexpr (WB == 5) {
+        fp5x32_cvt_f16x32(q, q[8], r, sm);
+        fp5x32_cvt_f16x32(q + 4, q[9], r + 16, sm);
+      } else {
+        fp6x32_cvt_f16x32_fma(q, r, sm);
+        fp6x32_cvt_f16x32_fma(q + 6, r + 16, sm);
+      }
       if constexpr (FGQ) {  // FGQ: v * S'_b in binary16 (per-row power-of-two normalised scales, as gemm.cu BN >= 64)
 #pragma unroll
         for (int j = 0; j < 32; ++j) {
@@ -755,7 +771,7 @@ int64_t prefill_2sm_workspace() { return p2::kCounters * 4 + (int64_t)max_pairs(
 int launch_prefill_2sm(const uint8_t* tiles, const uint16_t* scales, const uint16_t* Xt, int64_t ldx, int64_t M,
                        int64_t N, int64_t K, void* Y, int y_dtype, int y_layout, int64_t ldy, int flags,
                        int force, void* workspace, int64_t workspace_bytes, cudaStream_t stream, int* grid_out,
-                       bool fgq) {
+                       bool fgq, bool fp5) {
   const int n_tiles = static_cast<int>((N + kTileN - 1) / kTileN);
   if (n_tiles % 2 != 0) return LPQT_E_UNSUPPORTED;
   EncodeTiledFn2 enc = encode_fn_2sm();
@@ -848,6 +864,9 @@ int launch_prefill_2sm(const uint8_t* tiles, const uint16_t* scales, const uint1
     if (attr_err == cudaSuccess)
       attr_err = cudaFuncSetAttribute(p2::w6a16_prefill_2sm_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       p2::kSmemBytes);
+    if (attr_err == cudaSuccess)
+      attr_err = cudaFuncSetAttribute(p2::w6a16_prefill_2sm_kernel<false, 5>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, p2::kSmemBytes);
   });
   if (attr_err != cudaSuccess) return LPQT_E_CUDA;
   cudaLaunchConfig_t cfg = {};
@@ -870,8 +889,10 @@ int launch_prefill_2sm(const uint8_t* tiles, const uint16_t* scales, const uint1
   cfg.attrs = attr;
   cfg.numAttrs = na;
   if (grid_out) *grid_out = 2 * pairs;
-  const cudaError_t le = fgq ? cudaLaunchKernelEx(&cfg, p2::w6a16_prefill_2sm_kernel<true>, map, ymap, a, fq)
-                             : cudaLaunchKernelEx(&cfg, p2::w6a16_prefill_2sm_kernel<false>, map, ymap, a, fq);
+  if (fgq && fp5) return LPQT_E_UNSUPPORTED;
+  const cudaError_t le = fgq   ? cudaLaunchKernelEx(&cfg, p2::w6a16_prefill_2sm_kernel<true>, map, ymap, a, fq)
+                         : fp5 ? cudaLaunchKernelEx(&cfg, p2::w6a16_prefill_2sm_kernel<false, 5>, map, ymap, a, fq)
+                               : cudaLaunchKernelEx(&cfg, p2::w6a16_prefill_2sm_kernel<false>, map, ymap, a, fq);
   if (le != cudaSuccess) return LPQT_E_CUDA;
   note_launch();
   return check_launch();

@@ -73,3 +73,16 @@ def test_native_fp5_reference_api_and_container():
     assert np.max(np.abs(Y - ref)) / np.max(np.abs(ref)) <= 1e-3
     wl = L.load_lpqt(L.write_lpqt(q))
     assert wl.wbits == 5 and torch.equal(wl.tiles, w5.tiles)
+
+
+@pytest.mark.parametrize("m", [65, 300, 700])
+def test_native_fp5_pair_kernel_equals_widened(m):
+    """Prefill on the CTA-pair kernel: native FP5 tiles rebuild the same MMA
+    operands as the FP6-widened tiles, so Y is bit-identical (same schedule)."""
+    n, k = 2048, 4096
+    W, q, o, w5, w6 = _weights(n, k, 100 + m)
+    assert L.plan(m, n, k)["schedule"] == "pair"
+    x = torch.from_numpy(np.random.default_rng(m).standard_normal((m, k)).astype(np.float16)).cuda()
+    y5 = L.w6a16_linear(x, w5, out_dtype=torch.float32)
+    y6 = L.w6a16_linear(x, w6, out_dtype=torch.float32)
+    assert torch.equal(y5, y6)
