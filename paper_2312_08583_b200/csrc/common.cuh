@@ -433,11 +433,21 @@ __device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity) {
 }
 // Spin with a watchdog: a pipeline deadlock traps (the launch fails with an
 // error) instead of hanging the device.
+// The watchdog counts ROUNDS of 4 polls, so a poll is just try_wait + branch:
+// the idle roles' polling shares the issue slots of the dequant warps, and a
+// per-poll counter (+ compare + branch) cost 2-4 % of the decode launches;
+// rounds of 4 polls are within 0.5 % of no watchdog at all, while 16 / 64
+// unrolled polls are slower again (code size) (profiles/r02_abx_watchdog*.jsonl).
+#ifndef LPQT_WATCHDOG_POLLS
+#define LPQT_WATCHDOG_POLLS 4
+#endif
 template <int MODE = LPQT_WAIT_MODE>
 __device__ __forceinline__ void mbar_wait_u32(uint32_t a, uint32_t parity) {
-  uint32_t spins = 0;
-  while (!mbar_try_wait<MODE>(a, parity)) {
-    if (++spins == (1u << 30)) __trap();
+  for (uint32_t rounds = 0;; ++rounds) {
+#pragma unroll
+    for (int j = 0; j < LPQT_WATCHDOG_POLLS; ++j)
+      if (mbar_try_wait<MODE>(a, parity)) return;
+    if (rounds == (1u << 30) / LPQT_WATCHDOG_POLLS) __trap();
   }
 }
 template <int MODE = LPQT_WAIT_MODE>

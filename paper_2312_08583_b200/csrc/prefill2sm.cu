@@ -169,18 +169,25 @@ __device__ __forceinline__ uint32_t mapa(uint32_t addr, uint32_t rank) {
 __device__ __forceinline__ void arrive_cluster(uint32_t cluster_addr) {
   asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
 }
+__device__ __forceinline__ bool try_wait_cluster(uint32_t addr, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2, %3;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(addr), "r"(parity), "r"(LPQT_WAIT_HINT_NS)
+      : "memory");
+  return ok != 0;
+}
 __device__ __forceinline__ void wait_cluster(uint32_t addr, uint32_t parity) {
-  uint32_t ok = 0, spins = 0;
-  do {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2, %3;\n\t"
-        "selp.u32 %0, 1, 0, p;\n\t}"
-        : "=r"(ok)
-        : "r"(addr), "r"(parity), "r"(LPQT_WAIT_HINT_NS)
-        : "memory");
-    if (++spins == (1u << 28)) __trap();  // a pipeline bug fails the launch instead of hanging
-  } while (!ok);
+  // (watchdog per round of polls, as mbar_wait_u32: a pipeline bug fails the launch instead of hanging)
+  for (uint32_t rounds = 0;; ++rounds) {
+#pragma unroll
+    for (int j = 0; j < LPQT_WATCHDOG_POLLS; ++j)
+      if (try_wait_cluster(addr, parity)) return;
+    if (rounds == (1u << 28) / LPQT_WATCHDOG_POLLS) __trap();
+  }
 }
 __device__ __forceinline__ void cluster_sync() {
   asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
