@@ -92,12 +92,17 @@ __device__ __forceinline__ uint32_t cvt_e3m2x2_hi(uint32_t w) {
   asm("{cvt.rn.f16x2.e3m2x2 %0, %1;}" : "=r"(r) : "h"(static_cast<uint16_t>(w >> 16)));
   return r;
 }
-__device__ __forceinline__ uint32_t lop3_sel(uint32_t a, uint32_t b, uint32_t mask_a) {
-  return (a & mask_a) | (b & ~mask_a);  // one LOP3 with an immediate mask
+// (a & M) | (b & ~M) as ONE LOP3 (ptxas splits the C form into two when it
+// knows some operand bits are zero: 3 LOP3 per spare gather instead of 2)
+template <uint32_t M>
+__device__ __forceinline__ uint32_t lop3_sel(uint32_t a, uint32_t b) {
+  uint32_t d;
+  asm("lop3.b32 %0, %1, %2, %3, 0xE4;" : "=r"(d) : "r"(a), "r"(b), "n"(M));
+  return d;
 }
 __device__ __forceinline__ uint32_t spare_gather(uint32_t wa, uint32_t wb, uint32_t wc) {
-  const uint32_t t = lop3_sel(wa >> 6, wb >> 4, 0x03030303u);
-  return lop3_sel(t, wc >> 2, 0x0F0F0F0Fu);  // bits 6-7 of each byte: don't care
+  const uint32_t t = lop3_sel<0x03030303u>(wa >> 6, wb >> 4);
+  return lop3_sel<0x0F0F0F0Fu>(t, wc >> 2);  // bits 6-7 of each byte: don't care
 }
 __device__ __forceinline__ void fp6x32_cvt_f16x32(const uint32_t w[6], uint32_t out[16]) {
 #pragma unroll
@@ -120,8 +125,8 @@ struct ShiftMuls {
   uint32_t m26, m28, m30;  // 2^26, 2^28, 2^30  ->  >> 6, >> 4, >> 2
 };
 __device__ __forceinline__ uint32_t spare_gather_fma(uint32_t wa, uint32_t wb, uint32_t wc, const ShiftMuls& sm) {
-  const uint32_t t = lop3_sel(__umulhi(wa, sm.m26), __umulhi(wb, sm.m28), 0x03030303u);
-  return lop3_sel(t, __umulhi(wc, sm.m30), 0x0F0F0F0Fu);
+  const uint32_t t = lop3_sel<0x03030303u>(__umulhi(wa, sm.m26), __umulhi(wb, sm.m28));
+  return lop3_sel<0x0F0F0F0Fu>(t, __umulhi(wc, sm.m30));
 }
 __device__ __forceinline__ void fp6x32_cvt_f16x32_fma(const uint32_t w[6], uint32_t out[16], const ShiftMuls& sm) {
 #pragma unroll
