@@ -1893,7 +1893,13 @@ done_csk:
   // (measured, profiles/r01_v8_abx_split_cap.jsonl: no split at K = 4096, two
   // at 8192, three at 11008, four at 28672)
   if (split_k == 0 && p.kstep == 1) {
-    const int64_t cap = LPQT_SK_SPLIT_WIDE > 0 ? LPQT_SK_SPLIT_WIDE : std::min(4, std::max(1, p.k_tiles / 24));
+    int64_t cap = LPQT_SK_SPLIT_WIDE > 0 ? LPQT_SK_SPLIT_WIDE : std::min(4, std::max(1, p.k_tiles / 24));
+    // few tiles (tensor-parallel shards): the capped grid would leave most SMs
+    // idle, so split further while every CTA keeps >= 16 k-tiles
+    // (profiles/r02_probe_tp8_split.jsonl: 1280 x 8192, M = 64: 4 splits 24.6 us
+    // against 2 splits 30.7 us)
+    if (LPQT_SK_SPLIT_WIDE == 0 && 2 * p.tiles * cap < sms)
+      cap = std::max<int64_t>(cap, std::min<int64_t>(p.k_tiles / 16, sms / p.tiles));
     if (g > p.tiles * cap) g = p.tiles * cap;
     // prefill (BN 192) tiles that fit one wave: one whole tile per CTA beats
     // spreading them over every SM (the 128 x 192 partial reduction costs
