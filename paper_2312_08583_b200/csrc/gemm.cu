@@ -1578,7 +1578,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               fence_proxy_async_global();  // generic-proxy partials (acquired above) -> bulk-copy reads
               mbar_arrive_expect_tx(fix_bar, static_cast<uint32_t>(c_last - c_first) * kPartBytes);
               for (int c = c_first + 1; c <= c_last; ++c)
-                bulk_g2s_plain(smem_w + (c - c_first) * kPartBytes, a.partials + ((int64_t)c * 2) * (kTileN * BN),
+                bulk_g2s_plain(smem_w + (c - c_first - 1) * kPartBytes, a.partials + ((int64_t)c * 2) * (kTileN * BN),
                                kPartBytes, fix_bar);
             }
             y_begin();
@@ -1600,7 +1600,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll 1
               for (int c = 1; c <= c_last - c_first; ++c) {
                 if constexpr (PartLayout<BN>::kChunkMajor) {
-                  const uint32_t src = base + c * kPartBytes + (c0 / 4) * kTileN * 16;
+                  const uint32_t src = base + (c - 1) * kPartBytes + (c0 / 4) * kTileN * 16;
 #pragma unroll
                   for (int j = 0; j < 4; ++j) {
                     const float4 v = lds128_f32(src + j * kTileN * 16);
@@ -1610,7 +1610,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     acc[4 * j + 3] += v.w;
                   }
                 } else {  // rows contiguous
-                  const uint32_t src = smem_u32(smem_w) + c * kPartBytes + (rr * BN + c0) * 4;
+                  const uint32_t src = smem_u32(smem_w) + (c - 1) * kPartBytes + (rr * BN + c0) * 4;
 #pragma unroll
                   for (int j = 0; j < 4; ++j) {
                     const float4 v = lds128_f32(src + j * 16);
