@@ -1,0 +1,50 @@
+"""Correctness sweep (dev tool): every BASELINE layer shape (7B, 13B,
+StarCoder-15B, 70B and its TP 2 / 4 / 8 shards) at batch sizes across every
+schedule boundary, automatic plan, against the f64 product of the same
+weights' binary16 dequant; prints one JSON line per shape and a summary.
+
+python tools/sweep_check.py [--ms 1,8,...]
+"""
+import argparse, json, os, sys
+import torch
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_2312_08583_b200 as L  # noqa: E402
+from tools.probe import SHAPES  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--ms", default="1,8,16,17,24,32,33,48,64,65,96,128,192,256,384,512,1024")
+ap.add_argument("--sets", default="7b,13b,sc15b,70b,70b_tp2,70b_tp4,70b_tp8")
+a = ap.parse_args()
+ms = [int(v) for v in a.ms.split(",")]
+shapes = []
+for s in a.sets.split(","):
+    for sh in SHAPES[s]:
+        if sh not in shapes:
+            shapes.append(sh)
+worst, bad = 0.0, []
+for n, k in shapes:
+    g = torch.Generator(device="cuda").manual_seed(n + 3 * k)
+    W = (torch.randn(n, k, generator=g, device="cuda") * 0.02).half()
+    w = L.Fp6Weight.quantize(W)
+    del W
+    wd = w.dequantize_f16().double()
+    errs = {}
+    for m in ms:
+        x = torch.randn(m, k, generator=g, device="cuda").half()
+        try:
+            y = L.w6a16_linear(x, w, out_dtype=torch.float32)
+            torch.cuda.synchronize()
+            ref = x.double() @ wd.t()
+            e = float((y.double() - ref).abs().max() / ref.abs().max())
+        except Exception as exc:  # noqa: BLE001
+            print(json.dumps({"n": n, "k": k, "m": m, "error": repr(exc)[:200]}), flush=True)
+            sys.exit(1)
+        errs[m] = e
+        worst = max(worst, e)
+        if e > 1e-3:
+            bad.append((n, k, m, e, L.plan(m, n, k)))
+    print(json.dumps({"n": n, "k": k, "max_err": max(errs.values()),
+                      "errs": {str(m): float(f"{e:.3g}") for m, e in errs.items()}}), flush=True)
+    del wd, w
+    torch.cuda.empty_cache()
+print(json.dumps({"shapes": len(shapes), "ms": ms, "worst": worst, "bad": bad}), flush=True)
