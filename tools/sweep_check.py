@@ -15,6 +15,8 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--ms", default="1,8,16,17,24,32,33,48,64,65,96,128,192,256,384,512,1024")
 ap.add_argument("--sets", default="7b,13b,sc15b,70b,70b_tp2,70b_tp4,70b_tp8")
 ap.add_argument("--kind", default="cgq", help="cgq / fgq128 / fgq64 / fgq32 / fgq16 / fp5")
+ap.add_argument("--sched", default="auto", help="auto / streamk / cluster / single / pair")
+ap.add_argument("--splits", default="0", help="comma list of forced split_k values")
 a = ap.parse_args()
 ms = [int(v) for v in a.ms.split(",")]
 shapes = []
@@ -37,24 +39,26 @@ for n, k in shapes:
     wd = w.dequantize_f16().double()
     errs = {}
     sub = w.block and w.block % 128
-    for m in ms:
+    for m, sp in ((m, int(sp)) for m in ms for sp in a.splits.split(",")):
         if sub and m > 32:
             continue  # (sub-tile blocks run at decode widths only: InvalidScheme above)
+        if a.sched == "cluster" and m > 32:
+            continue  # (cluster split-K is the decode schedule)
         x = torch.randn(m, k, generator=g, device="cuda").half()
         try:
-            y = L.w6a16_linear(x, w, out_dtype=torch.float32)
+            y = L.w6a16_linear(x, w, out_dtype=torch.float32, sched=a.sched, split_k=sp)
             torch.cuda.synchronize()
             ref = x.double() @ wd.t()
             e = float((y.double() - ref).abs().max() / ref.abs().max())
         except Exception as exc:  # noqa: BLE001
-            print(json.dumps({"n": n, "k": k, "m": m, "error": repr(exc)[:200]}), flush=True)
+            print(json.dumps({"n": n, "k": k, "m": m, "split_k": sp, "error": repr(exc)[:200]}), flush=True)
             sys.exit(1)
-        errs[m] = e
+        errs[f"{m}/{sp}"] = e
         worst = max(worst, e)
         if e > (2e-3 if (w.block and m > 32) else 1e-3):
-            bad.append((n, k, m, e, L.plan(m, n, k)))
+            bad.append((n, k, m, sp, e, L.plan(m, n, k, sp, sched=a.sched)))
     print(json.dumps({"n": n, "k": k, "max_err": max(errs.values()),
-                      "errs": {str(m): float(f"{e:.3g}") for m, e in errs.items()}}), flush=True)
+                      "errs": {m: float(f"{e:.3g}") for m, e in errs.items()}}), flush=True)
     del wd, w
     torch.cuda.empty_cache()
-print(json.dumps({"kind": a.kind, "shapes": len(shapes), "ms": ms, "worst": worst, "bad": bad}), flush=True)
+print(json.dumps({"kind": a.kind, "sched": a.sched, "splits": a.splits, "shapes": len(shapes), "ms": ms, "worst": worst, "bad": bad}), flush=True)
