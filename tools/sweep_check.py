@@ -6,6 +6,7 @@ weights' binary16 dequant; prints one JSON line per shape and a summary.
 python tools/sweep_check.py [--ms 1,8,...]
 """
 import argparse, json, os, sys
+import numpy as np
 import torch
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2312_08583_b200 as L  # noqa: E402
@@ -32,11 +33,20 @@ for n, k in shapes:
         w = L.Fp6Weight.quantize(W)
     elif a.kind.startswith("fgq"):
         w = L.Fp6Weight.quantize(W, block=int(a.kind[3:]))
+    elif a.kind.startswith("int4"):  # int4 = per row, int4_128 = blocks of 128 (the comparator)
+        b = int(a.kind[5:]) if "_" in a.kind else 0
+        q = L.quantize_tensor(W, L.QuantScheme(L.Granularity.FGQ if b else L.Granularity.CGQ,
+                                               L.TensorFormat.INT4_ASYM, b))
+        w = L.Int4Weight.from_quantized(q)
     else:
         q = L.quantize_tensor(W, L.QuantScheme(L.Granularity.CGQ, L.TensorFormat.FP5_E3M1), bias_shift=True)
         w = L.Fp6Weight.from_quantized(q)
     del W
-    wd = w.dequantize_f16().double()
+    if a.kind.startswith("int4"):  # the kernel's binary16 weight RN_f16(Z + S * level)
+        d = L.dequantize_tensor(q)
+        wd = (d if torch.is_tensor(d) else torch.from_numpy(np.asarray(d))).cuda().half().double()
+    else:
+        wd = w.dequantize_f16().double()
     errs = {}
     sub = w.block and w.block % 128
     for m, sp in ((m, int(sp)) for m in ms for sp in a.splits.split(",")):
