@@ -1129,6 +1129,19 @@ __global__ void __launch_bounds__(kThreads, 1)
                   mma_f16_ts_if(e, d_tmem, ta_t + j * 8, bd_lo + off, bd_hi, idesc, init ? 0u : 1u);
                 }
               }
+            } else if constexpr (C::kPD) {
+              // ragged stage (fewer than KS tiles): the missing tile's partial
+              // ordinals still pass through their slots (an empty commit) so
+              // every slot's phase count stays q / kPSlots — a skipped use
+              // would let a later parity wait alias an old phase
+              const int P = FGQ == 2 ? fg.sub : 1;
+#pragma unroll 1
+              for (int p = 0; p < P; ++p) {
+                const int q = (KS * it + t) * P + p, ps = q % C::kPSlots;
+                mbar_wait<WM>(&pempty[ps], ((q / C::kPSlots) & 1) ^ 1);
+                tc_fence_after();
+                tc_commit_if(e, &pfull[ps]);
+              }
             }
             if constexpr (C::kTileRing) tc_commit_if(e, &aempty[tb]);  // this tile's slot is free once read
           }
@@ -1414,6 +1427,18 @@ __global__ void __launch_bounds__(kThreads, 1)
                   for (int j = 0; j < 16; ++j)
                     pacc[c0 + j] = __fadd_rn(pacc[c0 + j], __fmul_rn(scl, __uint_as_float(v[j])));
                 }
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&pempty[ps]);
+              }
+            } else {
+              // ragged stage: pass the missing tile's (empty) partial ordinals on
+              const int P = FGQ == 2 ? fg.sub : 1;
+#pragma unroll 1
+              for (int p = 0; p < P; ++p) {
+                const int q = (KS * i + t) * P + p, ps = q % C::kPSlots;
+                mbar_wait<LPQT_PD_WAIT>(&pfull[ps], (q / C::kPSlots) & 1);
+                tc_fence_after();
                 tc_fence_before();
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&pempty[ps]);

@@ -50,3 +50,26 @@ def test_forced_splits_across_ring_capacity(m, split_k):
                                    (1280, 8192, 40), (2560, 8192, 32), (3072, 8192, 24)])
 def test_auto_plans_with_many_contributors(n, k, m):
     _check(n, k, m)
+
+
+@pytest.mark.parametrize("block", [128, 32])
+@pytest.mark.parametrize("n,k", [(1536, 13900), (1536, 28000), (3000, 28000), (1000, 11000)])
+@pytest.mark.parametrize("m", [1, 16, 32])
+def test_fgq_partials_over_ragged_stages(n, k, m, block):
+    """FGQ at decode widths (one fp32 partial per block in a TMEM slot ring):
+    an odd k-tile count leaves each tile's last two-tile stage ragged; the
+    missing tile's partial ordinals must still pass through their slots, or a
+    later parity wait aliases an old phase (1536 x 13900 once read stale
+    partials: 0.1 normwise).  Against the f64 product of the exact v * S_b."""
+    g = torch.Generator(device="cuda").manual_seed(n + k + block)
+    W = (torch.randn(n, k, generator=g, device="cuda") * 0.02).half()
+    w = L.Fp6Weight.quantize(W, block=block)
+    q = L.quantize_tensor(W, L.QuantScheme(L.Granularity.FGQ, L.TensorFormat.FP6_E3M2, block))
+    d = L.dequantize_tensor(q)
+    wd = (d if torch.is_tensor(d) else torch.from_numpy(d)).cuda().double()
+    x = torch.randn(m, k, generator=g, device="cuda").half()
+    y = L.w6a16_linear(x, w, out_dtype=torch.float32)
+    ref = x.double() @ wd.t()
+    err = float((y.double() - ref).abs().max() / ref.abs().max())
+    assert err <= 1e-5, (err, L.plan(m, n, k))
+    assert torch.equal(y, L.w6a16_linear(x, w, out_dtype=torch.float32))

@@ -12,6 +12,9 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2312_08583_b200 as L  # noqa: E402
 from tools.probe import SHAPES  # noqa: E402
 
+# ragged K (not a multiple of 128; odd k-tile counts) and N not a multiple of 128
+SHAPES = dict(SHAPES, ragged=[(1000, 11000), (1536, 13900), (4224, 5000), (3000, 28000), (640, 8200), (5000, 3000)])
+
 ap = argparse.ArgumentParser()
 ap.add_argument("--ms", default="1,8,16,17,24,32,33,48,64,65,96,128,192,256,384,512,1024")
 ap.add_argument("--sets", default="7b,13b,sc15b,70b,70b_tp2,70b_tp4,70b_tp8")
