@@ -15,7 +15,7 @@ import ctypes
 import numpy as np
 
 from . import _lib
-from .errors import ShapeError
+from .errors import InvalidInput, ShapeError
 from .packing import seg4_length
 
 TILE = 128
@@ -358,6 +358,9 @@ def w6a16_linear(x, weight: Fp6Weight, out=None, out_dtype=None, split_k: int = 
     t = _lib.torch()
     if x.shape[-1] != weight.k:
         raise ShapeError(f"inner dimensions differ: weights K={weight.k}, activations K={x.shape[-1]}")
+    if not (_lib.is_torch(x) and x.is_cuda and x.device == weight.tiles.device):
+        # (the kernel reads x by address: a host or other-device tensor must not reach it)
+        raise InvalidInput(f"activations must be a CUDA tensor on the weight's device {weight.tiles.device}")
     lead = tuple(x.shape[:-1])
     x2 = x.reshape(-1, weight.k)
     m = int(x2.shape[0])

@@ -373,6 +373,30 @@ def test_w6a16_linear_torch_layout():
         assert normwise_rel(y.float().cpu().numpy(), ref.cpu().numpy()) <= REL_TOL
 
 
+def test_w6a16_linear_input_forms_and_device_check():
+    """3-D / strided / bf16 activations give the same product as the plain
+    fp16 matrix; a host tensor is refused before any launch (the kernel reads
+    x by address)."""
+    g = torch.Generator(device="cuda").manual_seed(19)
+    W = (torch.randn(384, 640, generator=g, device="cuda") * 0.05).half()
+    w = L.Fp6Weight.quantize(W)
+    x = torch.randn(2, 3, 640, generator=g, device="cuda").half()
+    y = L.w6a16_linear(x, w, out_dtype=torch.float32)
+    assert y.shape == (2, 3, 384)
+    y2 = L.w6a16_linear(x.reshape(6, 640), w, out_dtype=torch.float32)
+    assert torch.equal(y.reshape(6, 384), y2)
+    xs = torch.randn(640, 6, generator=g, device="cuda").half().t()      # non-contiguous view
+    assert torch.equal(L.w6a16_linear(xs, w, out_dtype=torch.float32),
+                       L.w6a16_linear(xs.contiguous(), w, out_dtype=torch.float32))
+    xb = x.reshape(6, 640).to(torch.bfloat16)                            # cast once to fp16
+    assert torch.equal(L.w6a16_linear(xb, w, out_dtype=torch.float32),
+                       L.w6a16_linear(xb.half(), w, out_dtype=torch.float32))
+    with pytest.raises(L.InvalidInput):
+        L.w6a16_linear(x.cpu(), w)
+    with pytest.raises(L.ShapeError):
+        L.w6a16_linear(torch.zeros(4, 641, device="cuda").half(), w)
+
+
 def test_workspace_reuse_across_shapes():
     # a split-K call with many tiles after one with few must not read the
     # previous call's partials as tile counters (regression)
