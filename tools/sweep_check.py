@@ -22,6 +22,7 @@ ap.add_argument("--kind", default="cgq", help="cgq / fgq128 / fgq64 / fgq32 / fg
 ap.add_argument("--sched", default="auto", help="auto / streamk / cluster / single / pair")
 ap.add_argument("--splits", default="0", help="comma list of forced split_k values")
 ap.add_argument("--out", default="f32", help="f32 / f16 / bf16 output (bar + the output rounding)")
+ap.add_argument("--layout", default="mn", help="mn (torch layout, w6a16_linear) / nm (reference layout, gemm_nm)")
 a = ap.parse_args()
 ms = [int(v) for v in a.ms.split(",")]
 ODT = {"f32": torch.float32, "f16": torch.float16, "bf16": torch.bfloat16}[a.out]
@@ -62,7 +63,14 @@ for n, k in shapes:
             continue  # (cluster split-K is the decode schedule)
         x = torch.randn(m, k, generator=g, device="cuda").half()
         try:
-            y = L.w6a16_linear(x, w, out_dtype=ODT, sched=a.sched, split_k=sp)
+            if a.layout == "nm":
+                from paper_2312_08583_b200.linear import gemm_nm
+                kp = -(-k // 8) * 8  # (the staged B operand: row stride a multiple of 8, as gemm_quantized stages it)
+                xt = torch.zeros(m, kp, dtype=torch.float16, device="cuda")
+                xt[:, :k] = x
+                y = gemm_nm(w, xt, kp, m, split_k=sp, sched=a.sched).t()
+            else:
+                y = L.w6a16_linear(x, w, out_dtype=ODT, sched=a.sched, split_k=sp)
             torch.cuda.synchronize()
             ref = x.double() @ wd.t()
             e = float((y.double() - ref).abs().max() / ref.abs().max())
