@@ -22,6 +22,7 @@ ap.add_argument("--kind", default="cgq", help="cgq / fgq128 / fgq64 / fgq32 / fg
 ap.add_argument("--sched", default="auto", help="auto / streamk / cluster / single / pair")
 ap.add_argument("--splits", default="0", help="comma list of forced split_k values")
 ap.add_argument("--out", default="f32", help="f32 / f16 / bf16 output (bar + the output rounding)")
+ap.add_argument("--rebuild", default="cvt", help="cvt / bias_shift / naive (the ablation rebuilds, CGQ FP6, M <= 16)")
 ap.add_argument("--layout", default="mn", help="mn (torch layout, w6a16_linear) / nm (reference layout, gemm_nm)")
 a = ap.parse_args()
 ms = [int(v) for v in a.ms.split(",")]
@@ -70,7 +71,7 @@ for n, k in shapes:
                 xt[:, :k] = x
                 y = gemm_nm(w, xt, kp, m, split_k=sp, sched=a.sched).t()
             else:
-                y = L.w6a16_linear(x, w, out_dtype=ODT, sched=a.sched, split_k=sp)
+                y = L.w6a16_linear(x, w, out_dtype=ODT, sched=a.sched, split_k=sp, rebuild=a.rebuild)
             torch.cuda.synchronize()
             ref = x.double() @ wd.t()
             e = float((y.double() - ref).abs().max() / ref.abs().max())
