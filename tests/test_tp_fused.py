@@ -33,7 +33,8 @@ def test_block_offsets_tile_the_output():
 @pytest.mark.gpu
 @pytest.mark.parametrize("n,k,m,layout,dt", [(2048, 4096, 16, "nm", "f32"), (1920, 3000, 3, "mn", "f16"),
                                              (4096, 1024, 64, "mn", "bf16"), (1024, 8192, 1, "mn", "f16"),
-                                             (2048, 2048, 200, "nm", "f16")])
+                                             (2048, 2048, 200, "nm", "f16"), (1536, 13900, 16, "mn", "f16"),
+                                             (3000, 28000, 4, "nm", "f32")])
 def test_fused_gather_two_ranks_one_gpu(n, k, m, layout, dt):
     import torch
     tdt = {"f32": torch.float32, "f16": torch.float16, "bf16": torch.bfloat16}[dt]
@@ -116,3 +117,19 @@ def test_fused_layer_world1_symmetric_memory():
             assert torch.equal(y, L.w6a16_linear(x, layer.weight)), m
     finally:
         dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+def test_fused_gather_refuses_unaligned_rows():
+    """Decode tiles reach the peers only by TMA tensor stores: Y[N, M] f32 at
+    M = 1 (4-byte rows) cannot be described and is refused before the launch."""
+    import torch
+    w = L.Fp6Weight.quantize((torch.randn(256, 1024, device="cuda") * 0.02).half())
+    xt = torch.randn(1, 1024, device="cuda").half()
+    Y = torch.zeros(512, 1, dtype=torch.float32, device="cuda")
+    flags = torch.zeros(_lib.MAX_PEERS, dtype=torch.int32, device="cuda")
+    done = torch.zeros(1, dtype=torch.int32, device="cuda")
+    scratch = torch.zeros(8 << 20, dtype=torch.uint8, device="cuda")
+    with pytest.raises(L.ShapeError):
+        tp.gather_linear(w, xt, 1024, 1, [Y.data_ptr(), Y.data_ptr()], [flags.data_ptr(), flags.data_ptr()], 0, 1,
+                         done, _lib.F32, "nm", 1, 0, workspace=scratch)
