@@ -174,6 +174,13 @@ struct L2Prefetch {
 #ifndef LPQT_DECODE_KSTEP
 #define LPQT_DECODE_KSTEP 2  // decode (BN <= 32): 128-k tiles per stage
 #endif
+#ifndef LPQT_CSK32_XSTAGES
+// BN 32 cluster split-K (M 17-32): 2 X stages of 16 KB leave room for 4 weight
+// stages instead of 2 (next to the DSMEM staging buffers): 4096^2 / 5120^2 /
+// 6144^2 12-17 % faster; stream-K at BN 32 keeps 4 X stages (2 measured 2-5 %
+// slower there) (profiles/r02_abx_bn32_xstages.jsonl)
+#define LPQT_CSK32_XSTAGES 2
+#endif
 #ifndef LPQT_TILE_RING
 #define LPQT_TILE_RING 1
 #endif
@@ -213,7 +220,7 @@ struct Cfg {
   // (native FP5 at BN 16: 4 X stages leave room for 8 W stages of 20 KB — bytes
   // in flight per SM are what bound the decode stream)
   static constexpr int kXStages =
-      BN <= 16 ? (CSK || WB == 5 ? 4 : 6) : (BN <= 128 ? 4 : (BN == 192 ? LPQT_PREFILL_XSTAGES : 3));
+      BN <= 16 ? (CSK || WB == 5 ? 4 : 6) : BN == 32 && CSK && WB != 5 ? LPQT_CSK32_XSTAGES : (BN <= 128 ? 4 : (BN == 192 ? LPQT_PREFILL_XSTAGES : 3));
   // CSK: two partial staging buffers of 128 x BN fp32 (rounds alternate)
   static constexpr int kStageBufBytes = CSK ? kTileN * BN * 4 : 0;
   // decode: output tiles staged in smem (two 128 x BN buffers, fp32-sized) and
