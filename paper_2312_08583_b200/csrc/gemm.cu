@@ -181,6 +181,12 @@ struct L2Prefetch {
 // slower there) (profiles/r02_abx_bn32_xstages.jsonl)
 #define LPQT_CSK32_XSTAGES 2
 #endif
+#ifndef LPQT_BN32_ONE_YBUF
+// BN 32 stream-K (M 17-32): one Y staging buffer + a 224-KB budget -> 6 weight
+// stages instead of 4: 1-5.5 % faster on every 7B / 13B / 70B shape, none slower
+// (profiles/r02_abx_bn32_one_ybuf.jsonl)
+#define LPQT_BN32_ONE_YBUF 1
+#endif
 #ifndef LPQT_TILE_RING
 #define LPQT_TILE_RING 1
 #endif
@@ -226,9 +232,13 @@ struct Cfg {
   // decode: output tiles staged in smem (two 128 x BN buffers, fp32-sized) and
   // written by the TMA tensor store, off the epilogue's critical path
   static constexpr int kYBufBytes = BN <= 32 ? kTileN * BN * 4 : 0;
-  static constexpr int kBudget = BN >= 192 ? 221 * 1024 : kSmemBudget;
+  // BN 32 stream-K: ONE Y staging buffer and a 224-KB budget make room for
+  // 6 weight stages instead of 4 (LPQT_BN32_ONE_YBUF)
+  static constexpr bool kOneY = LPQT_BN32_ONE_YBUF && BN == 32 && !CSK && WB == 6;
+  static constexpr int kYBufs = kOneY ? 1 : 2;
+  static constexpr int kBudget = BN >= 192 ? 221 * 1024 : (kOneY ? 224 * 1024 : kSmemBudget);
   static constexpr int kWStagesRaw =
-      (kBudget - kXStages * kXStageBytes - 2 * kStageBufBytes - 2 * kYBufBytes) / kWStageBytes;
+      (kBudget - kXStages * kXStageBytes - 2 * kStageBufBytes - kYBufs * kYBufBytes) / kWStageBytes;
   static constexpr int kWStages = (kWStagesRaw > 12 ? 12 : kWStagesRaw) & ~1;  // even: see header
   static constexpr int kStages = kWStages;                  // reported by the plan
   // two accumulators in flight (the epilogue drains one while the next
@@ -261,7 +271,7 @@ struct Cfg {
   static constexpr int kABars = kTileRing ? 6 : kASlots;
   static constexpr int kBarCount = 2 * kWStages + 2 * kXStages + 2 * kABars + 2 * kDBufs + 5 + 2 * kPSlots;
   static constexpr int kSmemBytes = kXStages * kXStageBytes + kWStages * kWStageBytes + 2 * kStageBufBytes +
-                                    2 * kYBufBytes + 8 * kBarCount + 16;
+                                    kYBufs * kYBufBytes + 8 * kBarCount + 16;
   static_assert(kWStages >= 2 && kXStages >= 2, "pipeline too shallow");
   static_assert(kMmaWarps == 1 || kXStages % 2 == 0, "X ring slots must keep their issuer");
   static_assert(kSmemBytes <= 227 * 1024, "shared memory");
@@ -695,7 +705,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint8_t* smem_w = smem_x + C::kXStages * C::kXStageBytes;             // kWStages x kWStageBytes
   uint8_t* smem_stg = smem_w + C::kWStages * C::kWStageBytes;           // CSK: 2 x [BN/4][128] float4
   uint8_t* smem_y = smem_stg + 2 * C::kStageBufBytes;                  // 2 x Y tile (TMA store source)
-  uint64_t* full_w = reinterpret_cast<uint64_t*>(smem_y + 2 * C::kYBufBytes);
+  uint64_t* full_w = reinterpret_cast<uint64_t*>(smem_y + C::kYBufs * C::kYBufBytes);
   uint64_t* empty_w = full_w + C::kWStages;
   uint64_t* full_x = empty_w + C::kWStages;
   uint64_t* empty_x = full_x + C::kXStages;
@@ -1220,10 +1230,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int n = n_tile * kTileN + rr;
       const int m0 = m_tile * BN;
       const uint32_t t_d = t_lane + d * C::kDCols;
-      const uint32_t ybuf = smem_u32(smem_y) + (ys_n & 1) * C::kYBufBytes;
+      const uint32_t ybuf = smem_u32(smem_y) + (ys_n % C::kYBufs) * C::kYBufBytes;
       auto y_begin = [&]() {  // the staging buffer must have been read by its last TMA store
-        if (ytma && ys_n >= 2) {
-          if (warp == kWarpEpi0 && lane == 0) bulk_wait_read<1>();
+        if (ytma && ys_n >= C::kYBufs) {
+          if (warp == kWarpEpi0 && lane == 0) bulk_wait_read<C::kYBufs - 1>();
           named_bar_sync(1, kNumEpiWarps * 32);
         }
       };
