@@ -187,6 +187,9 @@ struct L2Prefetch {
 // (profiles/r02_abx_bn32_one_ybuf.jsonl)
 #define LPQT_BN32_ONE_YBUF 1
 #endif
+#ifndef LPQT_CSK32_ONE_YBUF
+#define LPQT_CSK32_ONE_YBUF 1  // (cluster plans too: 4 -> 6 weight stages, 0-3 % faster, profiles/r02_abx_bn32_one_ybuf.jsonl)
+#endif
 #ifndef LPQT_TILE_RING
 #define LPQT_TILE_RING 1
 #endif
@@ -234,7 +237,7 @@ struct Cfg {
   static constexpr int kYBufBytes = BN <= 32 ? kTileN * BN * 4 : 0;
   // BN 32 stream-K: ONE Y staging buffer and a 224-KB budget make room for
   // 6 weight stages instead of 4 (LPQT_BN32_ONE_YBUF)
-  static constexpr bool kOneY = LPQT_BN32_ONE_YBUF && BN == 32 && !CSK && WB == 6;
+  static constexpr bool kOneY = LPQT_BN32_ONE_YBUF && BN == 32 && (!CSK || LPQT_CSK32_ONE_YBUF) && WB == 6;
   static constexpr int kYBufs = kOneY ? 1 : 2;
   static constexpr int kBudget = BN >= 192 ? 221 * 1024 : (kOneY ? 224 * 1024 : kSmemBudget);
   static constexpr int kWStagesRaw =
