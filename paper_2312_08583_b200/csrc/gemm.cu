@@ -190,6 +190,14 @@ struct L2Prefetch {
 #ifndef LPQT_CSK32_ONE_YBUF
 #define LPQT_CSK32_ONE_YBUF 1  // (cluster plans too: 4 -> 6 weight stages, 0-3 % faster, profiles/r02_abx_bn32_one_ybuf.jsonl)
 #endif
+#ifndef LPQT_BN64_XSTAGES
+// BN 64 (M 33-64): 4 X stages of 16 KB; 2 X stages + 14 weight stages measured
+// 3-8 % slower (profiles/r02_abx_bn64_stages.jsonl)
+#define LPQT_BN64_XSTAGES 4
+#endif
+#ifndef LPQT_BN64_WCAP
+#define LPQT_BN64_WCAP 12
+#endif
 #ifndef LPQT_TILE_RING
 #define LPQT_TILE_RING 1
 #endif
@@ -229,7 +237,7 @@ struct Cfg {
   // (native FP5 at BN 16: 4 X stages leave room for 8 W stages of 20 KB — bytes
   // in flight per SM are what bound the decode stream)
   static constexpr int kXStages =
-      BN <= 16 ? (CSK || WB == 5 ? 4 : 6) : BN == 32 && CSK && WB != 5 ? LPQT_CSK32_XSTAGES : (BN <= 128 ? 4 : (BN == 192 ? LPQT_PREFILL_XSTAGES : 3));
+      BN <= 16 ? (CSK || WB == 5 ? 4 : 6) : BN == 32 && CSK && WB != 5 ? LPQT_CSK32_XSTAGES : BN == 64 ? LPQT_BN64_XSTAGES : (BN <= 128 ? 4 : (BN == 192 ? LPQT_PREFILL_XSTAGES : 3));
   // CSK: two partial staging buffers of 128 x BN fp32 (rounds alternate)
   static constexpr int kStageBufBytes = CSK ? kTileN * BN * 4 : 0;
   // decode: output tiles staged in smem (two 128 x BN buffers, fp32-sized) and
@@ -242,7 +250,8 @@ struct Cfg {
   static constexpr int kBudget = BN >= 192 ? 221 * 1024 : (kOneY ? 224 * 1024 : kSmemBudget);
   static constexpr int kWStagesRaw =
       (kBudget - kXStages * kXStageBytes - 2 * kStageBufBytes - kYBufs * kYBufBytes) / kWStageBytes;
-  static constexpr int kWStages = (kWStagesRaw > 12 ? 12 : kWStagesRaw) & ~1;  // even: see header
+  static constexpr int kWCap = BN == 64 ? LPQT_BN64_WCAP : 12;
+  static constexpr int kWStages = (kWStagesRaw > kWCap ? kWCap : kWStagesRaw) & ~1;  // even: see header
   static constexpr int kStages = kWStages;                  // reported by the plan
   // two accumulators in flight (the epilogue drains one while the next
   // tile's MMAs fill the other) up to BN 192: 2 x 192 + a 2-slot A ring = 512
