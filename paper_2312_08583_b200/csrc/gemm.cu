@@ -192,7 +192,7 @@ struct L2Prefetch {
 #endif
 #ifndef LPQT_BN64_XSTAGES
 // BN 64 (M 33-64): 4 X stages of 16 KB; 2 X stages + 14 weight stages measured
-// 3-8 % slower (profiles/r02_abx_bn64_stages.jsonl)
+// 3-8 % slower, 6 / 8 X stages neutral (profiles/r02_abx_bn64_stages.jsonl)
 #define LPQT_BN64_XSTAGES 4
 #endif
 #ifndef LPQT_BN64_WCAP
