@@ -391,7 +391,9 @@ int lpqt_fgq_stage_params(const uint16_t* scales, const uint16_t* zeros,
  * zero words (lpqt_fgq_stage_params with zeros); the binary16 weight
  * Z + S * level is rebuilt in registers and runs the same tcgen05 pipeline
  * as the FP6 GEMM (flags: LPQT_LAUNCH_PDL, LPQT_SCHED_STREAMK,
- * LPQT_SCHED_CLUSTER).  block: the parameters' block size (validated). */
+ * LPQT_SCHED_CLUSTER; LPQT_SCHED_SINGLE is a no-op — there is no CTA-pair
+ * W4A16 kernel, LPQT_SCHED_PAIR is refused with LPQT_E_INVALID_INPUT).
+ * block: the parameters' block size (validated). */
 int64_t lpqt_int4_tiles_bytes(int64_t N, int64_t K);
 int lpqt_int4_prepack(const uint8_t* nibbles, int64_t N, int64_t K,
                       uint8_t* tiles, void* stream);

@@ -2438,6 +2438,9 @@ int lpqt_w4a16_linear_blocks(const uint8_t* tiles, const uint32_t* params, int64
                              const uint16_t* Xt, int64_t ldx, int64_t M, int64_t N, int64_t K, void* Y, int y_dtype,
                              int y_layout, int64_t ldy, int split_k, void* workspace, int64_t workspace_bytes,
                              int flags, void* stream) {
+  // (W4A16 always runs the single-SM kernel: LPQT_SCHED_SINGLE is accepted as a
+  // no-op; there is no CTA-pair W4A16 kernel, so LPQT_SCHED_PAIR is refused)
+  flags &= ~LPQT_SCHED_SINGLE;
   if (flags & ~(LPQT_LAUNCH_PDL | LPQT_SCHED_STREAMK | LPQT_SCHED_CLUSTER)) return LPQT_E_INVALID_INPUT;
   if (M < 0 || N < 0 || K < 0) return LPQT_E_SHAPE;
   if (M == 0 || N == 0) return LPQT_OK;

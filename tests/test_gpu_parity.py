@@ -841,3 +841,18 @@ def test_division_free_encode_exhaustive(dtype):
     assert bad_codes == 0, (bad_codes, bad_quot, pairs)
     if dtype == "f16":   # (bf16 weights: 0.26 % of the quotients differ by an ulp, never across a code boundary)
         assert bad_quot == 0, (bad_codes, bad_quot, pairs)
+
+
+def test_w4a16_schedule_flags():
+    """The W4A16 comparator runs the single-SM kernel only: sched="single" is
+    the automatic path, sched="pair" is refused (no CTA-pair W4A16 kernel)."""
+    g = torch.Generator(device="cuda").manual_seed(41)
+    W = (torch.randn(512, 1024, generator=g, device="cuda") * 0.02).half()
+    q = L.quantize_tensor(W, L.QuantScheme(L.Granularity.FGQ, L.TensorFormat.INT4_ASYM, 128))
+    w = L.Int4Weight.from_quantized(q)
+    for m in (7, 200):
+        x = torch.randn(m, 1024, generator=g, device="cuda").half()
+        assert torch.equal(L.w6a16_linear(x, w, out_dtype=torch.float32, sched="single"),
+                           L.w6a16_linear(x, w, out_dtype=torch.float32))
+        with pytest.raises(L.InvalidInput):
+            L.w6a16_linear(x, w, sched="pair")
